@@ -1,0 +1,154 @@
+/* include/tabi.h -- C ABI of the B200-native TABI atlas packer.
+ *
+ * TABI = "Tight And Balanced Interactive" atlas packing, arxiv 2602.07782
+ * (/root/reference/PAPER.md, cited "P:<line>").  One call packs N charts into a
+ * fixed W x H atlas with minimal downscaling, following the paper's problem
+ * statement: "Our input consists of a set of 2D charts ... provided
+ * as polygonal meshes with coordinates defined in texel space ... Our
+ * algorithm outputs per-chart scales and rigid transformations (translation,
+ * rotation, and/or reflection) that arrange the charts inside the atlas with
+ * no overlaps between the charts or their gutters."
+ *
+ * Every stage (proxies, sort, profiles, compaction, balanced fold-and-push,
+ * scale search) runs as hand-written sm_100a CUDA kernels on one GPU; there is
+ * no CPU fallback.  No C++ or torch types cross this boundary.
+ */
+#ifndef TABI_H
+#define TABI_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TABI_ABI_VERSION 1
+#define TABI_MAX_LOCAL_AABBS 64   /* k upper bound (quality knob) */
+#define TABI_MAX_SCALES 256       /* M upper bound (paper: 64)    */
+#define TABI_MAX_ATLAS_SIDE 16384
+
+typedef enum {
+  TABI_OK = 0,
+  TABI_EINVAL = 1,      /* bad spec or chart (info->bad_chart names the chart) */
+  TABI_NO_FIT = 2,      /* no candidate scale packs: out untouched     */
+  TABI_ECUDA = 3,       /* CUDA runtime failure; see tabi_last_error()         */
+  TABI_ECAPACITY = 4    /* input larger than the context was created for      */
+} tabi_status;
+
+enum {
+  TABI_F_NO_HC = 1u,                 /* ablation: never compact horizontally */
+  TABI_F_NO_BALANCE = 2u,            /* ablation: no knees, static L/R alternation    */
+  TABI_F_ADJACENT_LOCKS_ONLY = 4u    /* paper-literal Alg. 1 (adjacent pairs only)    */
+};
+
+typedef struct tabi_ctx tabi_ctx;    /* opaque: device workspace + stream, one per host thread */
+
+/* Atlas + knobs (SPEC AtlasSpec S:33-36).  Invariants, else TABI_EINVAL:
+ *   1 <= atlas_w, atlas_h <= 16384;  0 <= gutter <= 64;  1 <= scale_count <= 256;
+ *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_*. */
+typedef struct {
+  int32_t atlas_w, atlas_h;   /* texels */
+  int32_t gutter;             /* texels around every chart, none at atlas edges; paper 1 */
+  int32_t scale_count;        /* M: candidates s = m/M, m = 1..M; paper 64 */
+  int32_t local_aabb_count;   /* k local AABBs per axis; paper 10 */
+  int32_t t_opt_bp;           /* prefix-tail threshold, basis points of atlas_h;
+                                 -1 = paper policy (0 if N <= 10000 else 100).
+                                 This build implements t_opt = 0 (sequential) only and
+                                 returns TABI_EINVAL if the effective value is > 0. */
+  uint32_t flags;             /* TABI_F_* */
+} tabi_spec;
+
+/* Per-chart output, 32 bytes, indexed by INPUT chart order.
+ * Transform of an input vertex p = (x, y) * (res_x, res_y) (texels), exact in
+ * 1/256-texel units (q = round_half_even(256 * p)):
+ *   1. u = qx - min_qx, v = qy - min_qy           (chart AABB to the origin)
+ *   2. if rot90:  (u, v) <- (h' - v, u)           (h' = the original AABB height;
+ *                                                   the chart becomes taller than wide)
+ *   3. if flip_x: u <- w - u ; if flip_y: v <- h - v   (orientation; w, h posed extents)
+ *   4. (u, v) <- (u, v) * scale_num / (scale_den * 256)                 (texels)
+ *   5. if mirror_x: u <- box_w - u   (right-to-left row, "Reflect charts")
+ *   6. atlas position = (tx + u, ty + v)
+ * box_w = ceil(w * scale), box_h = ceil(h * scale) in texels (the integer box
+ * the mirror of step 5 is taken about). */
+typedef struct {
+  int32_t tx, ty;
+  int32_t scale_num, scale_den;   /* scale = scale_num / scale_den = m / M */
+  int32_t box_w, box_h;
+  uint8_t rot90, flip_x, flip_y, mirror_x;
+  uint8_t mode;                   /* 0 = sequential row */
+  uint8_t pad[3];
+} tabi_placement;
+
+typedef struct {
+  int32_t scale_index;            /* winning m (0 on NO_FIT) */
+  int32_t reserved0;
+  double l2_stretch;              /* Sander L2 stretch of the packed->input map; M/m */
+  int32_t rows, knees_found, knee_rows, prefix_rows;   /* winner's statistics */
+  int32_t bad_chart;              /* first offending chart on EINVAL, else -1 */
+  int32_t gpu_launches;           /* kernels launched by this call */
+  float stage_ms[8];              /* per-stage device time if TABI_TIMING=1, else 0:
+                                     [0] H2D [1] proxies [2] sort [3] profiles
+                                     [4] offsets+locks [5] fold&push [6] select [7] D2H */
+} tabi_info;
+
+/* Create a context on `cuda_device`.  max_charts / max_vertices bound every
+ * later call (TABI_ECAPACITY beyond them); device workspace is linear in
+ * max_charts ("memory consumption ... linear in the number of charts")
+ * and grows on demand for the per-candidate footprint buffers.
+ * Returns TABI_ECUDA if the device cannot be initialised. */
+tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t max_charts,
+                            int64_t max_vertices, int32_t max_atlas_side);
+void tabi_ctx_destroy(tabi_ctx* ctx);
+
+/* Pack n_charts charts.
+ *   xy          2*V floats x0,y0,x1,y1,... ; chart c owns vertices
+ *               [chart_start[c], chart_start[c+1]); one closed outline per chart,
+ *               either winding, >= 3 vertices, non-zero area after snapping,
+ *               |coordinate * res| * 256 <= 2^24.
+ *   chart_start n_charts + 1 int32, chart_start[0] = 0, non-decreasing.
+ *   res_x/res_y multiply x/y (texel resolution of UV input; 1 if already texels).
+ *   on_device   0: xy, chart_start, out are host pointers; the call copies in, runs,
+ *               copies out and returns when `out`/`info` are final.
+ *               1: xy, chart_start, out are device pointers; the call still returns
+ *               after completion (info needs the winner) but does no bulk copies.
+ *   stream      cudaStream_t to run on, or NULL for the context's stream.
+ * Ownership: the caller owns every pointer; nothing is retained after return.
+ * Deterministic: identical inputs give bit-identical outputs. */
+tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                      int32_t n_charts, float res_x, float res_y, const tabi_spec* spec,
+                      tabi_placement* out, tabi_info* info, int on_device, void* stream);
+
+const char* tabi_status_str(tabi_status s);
+const char* tabi_last_error(tabi_ctx* ctx);   /* last CUDA error text, or "" */
+
+/* ---- introspection of the last tabi_pack on ctx (parity tests; host outputs) ---- */
+
+/* Final-pose proxy of one chart, 1088 bytes (D3-D8 of SURVEY.md §8(c)). */
+typedef struct {
+  int32_t w, h;                   /* posed extents, 1/256 texel */
+  int64_t area2;                  /* 2 x |polygon area| */
+  int32_t xmin, ymin;             /* snapped input AABB min */
+  int32_t rot90, fx, fy, k;
+  int32_t top[64], bot[64], left[64], right[64];   /* merged local AABBs */
+  int32_t obb_j, reserved;
+  int64_t umin, umax, vmin, vmax; /* OBB in the Q30-rotated frame, theta = obb_j * pi/16 */
+} tabi_proxy_dbg;
+
+typedef struct {
+  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p, switched_at;
+} tabi_cand_dbg;
+
+tabi_status tabi_debug_proxies(tabi_ctx* ctx, tabi_proxy_dbg* out);   /* n_charts entries */
+tabi_status tabi_debug_perm(tabi_ctx* ctx, int32_t* perm);             /* sorted pos -> chart */
+tabi_status tabi_debug_candidates(tabi_ctx* ctx, tabi_cand_dbg* out);  /* scale_count entries */
+/* Footprint of the chart at sorted position s for candidate m (1..M):
+ * wd_hd[0..1] = (Wd, Hd); columns/rows receive Wd / Hd int32 values each. */
+tabi_status tabi_debug_profile(tabi_ctx* ctx, int32_t m, int32_t s, int32_t* wd_hd,
+                               int32_t* dtop, int32_t* dbot, int32_t* dleft, int32_t* dright);
+/* Adjacent compacting advance off(s, s+1) and lock bits (bit0: s cannot move
+ * above s+1, bit1: s+1 cannot move above s) for candidate m, n_charts entries. */
+tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* lockbits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,279 @@
+// k_proxy.cu -- K1: per-chart proxies, one warp per chart.
+//
+// Computes, for every chart ("compute the AABBs of all charts, rotate the
+// boxes to be taller than they are wide ... two parallel passes which compute
+// our shape approximations for each chart and determine each chart's
+// orientation"):
+//   snap to 1/256 texel -> AABB -> 90-degree normalization -> local AABBs
+//    + merge -> orientation -> final pose ->
+//   local AABBs again -> approximate OBB over 8 angles.
+// Lanes stride over vertices / edges; slice bounds are accumulated with
+// shared-memory atomicMin/Max (commutative, so schedule-independent), merges
+// and reductions use warp shuffles.  Output: proxy SoA in HBM.
+#include "tabi_internal.cuh"
+
+namespace tabi {
+namespace {
+
+constexpr int kWarps = 8;  // warps (charts) per block
+
+struct WarpSlices {
+  int32_t lo[2][TABI_KMAX];  // unmerged: [0] x-slices top, [1] y-slices left
+  int32_t hi[2][TABI_KMAX];  //           [0] x-slices bot, [1] y-slices right
+  int32_t mlo[2][TABI_KMAX]; // merged
+  int32_t mhi[2][TABI_KMAX];
+};
+
+// D4: slice bounds along one axis.  A = coordinate that is sliced (x for
+// x-slices), B = the bounded coordinate.  Strip j = closed range k*A in
+// [j*ext, (j+1)*ext].
+__device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, int64_t ext, int k,
+                                  int32_t* lo, int32_t* hi, int lane) {
+  for (int v = lane; v < nv; v += 32) {
+    int64_t ka = (int64_t)k * A[v];
+    int64_t jh = ka / ext;                 // floor(k*a/ext), a >= 0
+    int64_t jl = ceildiv(ka, ext) - 1;     // ceil(k*a/ext) - 1
+    if (jl < 0) jl = 0;
+    if (jh > k - 1) jh = k - 1;
+    for (int64_t j = jl; j <= jh; j++) {
+      if (j * ext <= ka && ka <= (j + 1) * ext) {
+        atomicMin(&lo[j], B[v]);
+        atomicMax(&hi[j], B[v]);
+      }
+    }
+  }
+  for (int v = lane; v < nv; v += 32) {
+    int a = v, b = (v + 1 == nv) ? 0 : v + 1;
+    int64_t xa = A[a], xb = A[b], ya = B[a], yb = B[b];
+    if (xa == xb) continue;
+    if (xa > xb) {
+      int64_t t = xa; xa = xb; xb = t;
+      t = ya; ya = yb; yb = t;
+    }
+    int64_t L0 = (int64_t)k * xa / ext + 1;      // first line strictly right of xa
+    int64_t L1 = ceildiv((int64_t)k * xb, ext) - 1;  // last line strictly left of xb
+    if (L0 < 1) L0 = 1;
+    if (L1 > k - 1) L1 = k - 1;
+    for (int64_t L = L0; L <= L1; L++) {
+      int64_t line = L * ext;
+      if (!((int64_t)k * xa < line && line < (int64_t)k * xb)) continue;
+      int64_t num = (line - (int64_t)k * xa) * (yb - ya);
+      int64_t den = (int64_t)k * (xb - xa);
+      int32_t yf = (int32_t)(ya + floordiv(num, den));
+      int32_t yc = (int32_t)(ya + ceildiv(num, den));
+      atomicMin(&lo[L - 1], yf);
+      atomicMax(&hi[L - 1], yc);
+      atomicMin(&lo[L], yf);
+      atomicMax(&hi[L], yc);
+    }
+  }
+}
+
+// D5 merge: x-slice j tightened by y-slices whose x-range meets strip j.
+__device__ void merge_slices(WarpSlices& S, int64_t w, int64_t h, int k, int lane) {
+  for (int j = lane; j < k; j += 32) {
+    // x-slices
+    int64_t mn = INT64_MAX, mx = INT64_MIN;
+    for (int i = 0; i < k; i++) {
+      if ((int64_t)k * S.lo[1][i] <= (int64_t)(j + 1) * w && (int64_t)k * S.hi[1][i] >= (int64_t)j * w) {
+        int64_t f = floordiv((int64_t)i * h, k), c = ceildiv((int64_t)(i + 1) * h, k);
+        mn = f < mn ? f : mn;
+        mx = c > mx ? c : mx;
+      }
+    }
+    int64_t t = S.lo[0][j], b = S.hi[0][j];
+    if (mn != INT64_MAX && mn > t) t = mn;
+    if (mx != INT64_MIN && mx < b) b = mx;
+    S.mlo[0][j] = (int32_t)t;
+    S.mhi[0][j] = (int32_t)b;
+    // y-slices
+    mn = INT64_MAX;
+    mx = INT64_MIN;
+    for (int i = 0; i < k; i++) {
+      if ((int64_t)k * S.lo[0][i] <= (int64_t)(j + 1) * h && (int64_t)k * S.hi[0][i] >= (int64_t)j * h) {
+        int64_t f = floordiv((int64_t)i * w, k), c = ceildiv((int64_t)(i + 1) * w, k);
+        mn = f < mn ? f : mn;
+        mx = c > mx ? c : mx;
+      }
+    }
+    t = S.lo[1][j];
+    b = S.hi[1][j];
+    if (mn != INT64_MAX && mn > t) t = mn;
+    if (mx != INT64_MIN && mx < b) b = mx;
+    S.mlo[1][j] = (int32_t)t;
+    S.mhi[1][j] = (int32_t)b;
+  }
+}
+
+__device__ void merged_slices(WarpSlices& S, const int32_t* X, const int32_t* Y, int nv, int64_t w,
+                              int64_t h, int k, int lane) {
+  for (int j = lane; j < k; j += 32) {
+    S.lo[0][j] = INT32_MAX; S.hi[0][j] = INT32_MIN;
+    S.lo[1][j] = INT32_MAX; S.hi[1][j] = INT32_MIN;
+  }
+  __syncwarp();
+  accumulate_slices(X, Y, nv, w, k, S.lo[0], S.hi[0], lane);
+  accumulate_slices(Y, X, nv, h, k, S.lo[1], S.hi[1], lane);
+  __syncwarp();
+  merge_slices(S, w, h, k, lane);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
+             float ry, int k, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
+  __shared__ WarpSlices smem[kWarps];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int c = blockIdx.x * kWarps + wib;
+  if (c >= n) return;
+  WarpSlices& S = smem[wib];
+  const int32_t a0 = start[c];
+  const int nv = start[c + 1] - a0;
+  if (nv < 3) {
+    if (lane == 0) atomicMin(&st->bad_chart, c);
+    return;
+  }
+  int32_t* X = qx + a0;
+  int32_t* Y = qy + a0;
+  // A1 snap: q = round_half_even(x * res * 256), exact product in double (D2)
+  bool ok = true;
+  int32_t xmn = INT32_MAX, xmx = INT32_MIN, ymn = INT32_MAX, ymx = INT32_MIN;
+  for (int v = lane; v < nv; v += 32) {
+    double fx = (double)xy[2 * (int64_t)(a0 + v)] * (double)rx * 256.0;
+    double fy = (double)xy[2 * (int64_t)(a0 + v) + 1] * (double)ry * 256.0;
+    if (!isfinite(fx) || !isfinite(fy) || fabs(fx) > (double)TABI_QMAX ||
+        fabs(fy) > (double)TABI_QMAX) {
+      ok = false;
+      continue;
+    }
+    int32_t ix = (int32_t)__double2ll_rn(fx), iy = (int32_t)__double2ll_rn(fy);
+    X[v] = ix;
+    Y[v] = iy;
+    xmn = min(xmn, ix); xmx = max(xmx, ix);
+    ymn = min(ymn, iy); ymx = max(ymx, iy);
+  }
+  if (!__all_sync(0xffffffffu, ok)) {
+    if (lane == 0) atomicMin(&st->bad_chart, c);
+    return;
+  }
+  xmn = warp_min(xmn); xmx = warp_max(xmx);
+  ymn = warp_min(ymn); ymx = warp_max(ymx);
+  int64_t w = (int64_t)xmx - xmn, h = (int64_t)ymx - ymn;
+  __syncwarp();
+  for (int v = lane; v < nv; v += 32) { X[v] -= xmn; Y[v] -= ymn; }
+  __syncwarp();
+  // D3 shoelace (2 x area), exact
+  i128 s2 = 0;
+  for (int v = lane; v < nv; v += 32) {
+    int u = (v + 1 == nv) ? 0 : v + 1;
+    s2 += (i128)((int64_t)X[v] * Y[u] - (int64_t)X[u] * Y[v]);
+  }
+  s2 = warp_sum128(s2);
+  if (s2 < 0) s2 = -s2;
+  if (s2 == 0) {
+    if (lane == 0) atomicMin(&st->bad_chart, c);
+    return;
+  }
+  // D3 90-degree normalization: (x, y) -> (h - y, x) iff w > h
+  const bool rot = w > h;
+  if (rot) {
+    for (int v = lane; v < nv; v += 32) {
+      int32_t nx = (int32_t)(h - Y[v]), ny = X[v];
+      X[v] = nx;
+      Y[v] = ny;
+    }
+    int64_t t = w; w = h; h = t;
+  }
+  __syncwarp();
+  // D4/D5 in the normalized pose, D7 orientation
+  merged_slices(S, X, Y, nv, w, h, k, lane);
+  int64_t TOP = 0, BOT = 0, LEFT = 0, RIGHT = 0;
+  for (int j = lane; j < k; j += 32) {
+    TOP += S.mlo[0][j];
+    BOT += h - S.mhi[0][j];
+    LEFT += S.mlo[1][j];
+    RIGHT += w - S.mhi[1][j];
+  }
+  TOP = warp_sum64(TOP); BOT = warp_sum64(BOT);
+  LEFT = warp_sum64(LEFT); RIGHT = warp_sum64(RIGHT);
+  const bool fy = TOP > BOT;
+  const int64_t D = LEFT - RIGHT;
+  bool fx;
+  if ((i128)10 * D > (i128)k * w) {
+    fx = true;
+  } else if ((i128)10 * (-D) > (i128)k * w) {
+    fx = false;
+  } else {
+    int64_t BL2 = 0, BR2 = 0;
+    for (int j = lane; j < k; j += 32) {
+      int64_t gap = fy ? S.mlo[0][j] : (h - S.mhi[0][j]);
+      if (2 * j + 1 < k) BL2 += 2 * gap;
+      else if (2 * j + 1 > k) BR2 += 2 * gap;
+      else { BL2 += gap; BR2 += gap; }
+    }
+    BL2 = warp_sum64(BL2);
+    BR2 = warp_sum64(BR2);
+    fx = BL2 > BR2;
+  }
+  // D8 final pose
+  if (fx || fy) {
+    __syncwarp();
+    for (int v = lane; v < nv; v += 32) {
+      if (fx) X[v] = (int32_t)(w - X[v]);
+      if (fy) Y[v] = (int32_t)(h - Y[v]);
+    }
+    __syncwarp();
+  }
+  merged_slices(S, X, Y, nv, w, h, k, lane);
+  int32_t* sl = P.sl + (int64_t)c * 4 * k;
+  for (int j = lane; j < k; j += 32) {
+    sl[j] = S.mlo[0][j];
+    sl[k + j] = S.mhi[0][j];
+    sl[2 * k + j] = S.mlo[1][j];
+    sl[3 * k + j] = S.mhi[1][j];
+  }
+  // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j
+  i128 best = -1;
+  int bj = 0;
+  int64_t bu0 = 0, bu1 = 0, bv0 = 0, bv1 = 0;
+  for (int j = 0; j < 8; j++) {
+    const int64_t C = kQC[j], Sn = kQS[j];
+    int64_t u0 = INT64_MAX, u1 = INT64_MIN, v0 = INT64_MAX, v1 = INT64_MIN;
+    for (int v = lane; v < nv; v += 32) {
+      int64_t u = (int64_t)X[v] * C + (int64_t)Y[v] * Sn;
+      int64_t vv = -(int64_t)X[v] * Sn + (int64_t)Y[v] * C;
+      u0 = u < u0 ? u : u0; u1 = u > u1 ? u : u1;
+      v0 = vv < v0 ? vv : v0; v1 = vv > v1 ? vv : v1;
+    }
+    u0 = warp_min64(u0); u1 = warp_max64(u1);
+    v0 = warp_min64(v0); v1 = warp_max64(v1);
+    i128 area = (i128)(u1 - u0) * (i128)(v1 - v0);
+    if (best < 0 || area < best) {
+      best = area; bj = j;
+      bu0 = u0; bu1 = u1; bv0 = v0; bv1 = v1;
+    }
+  }
+  if (lane == 0) {
+    P.w[c] = (int32_t)w;
+    P.h[c] = (int32_t)h;
+    P.area2[c] = (int64_t)s2;
+    P.xmin[c] = xmn;
+    P.ymin[c] = ymn;
+    P.pose[c] = (uint8_t)((rot ? 1 : 0) | (fx ? 2 : 0) | (fy ? 4 : 0));
+    P.obb_j[c] = bj;
+    P.obb[4 * (int64_t)c + 0] = bu0;
+    P.obb[4 * (int64_t)c + 1] = bu1;
+    P.obb[4 * (int64_t)c + 2] = bv0;
+    P.obb[4 * (int64_t)c + 3] = bv1;
+  }
+}
+
+}  // namespace
+
+void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
+                    int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+  int blocks = (n + kWarps - 1) / kWarps;
+  proxy_kernel<<<blocks, kWarps * 32, 0, s>>>(xy, start, n, rx, ry, k, qx, qy, P, st);
+}
+
+}  // namespace tabi

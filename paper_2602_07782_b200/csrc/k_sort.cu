@@ -1,0 +1,181 @@
+// k_sort.cu -- K2: decreasing-height order + footprint slot layout.
+//
+// P:139 "sorted in decreasing height order"; ties by the wider chart, then by
+// chart index -- realised as a STABLE LSD radix sort on the key
+// ((hmax - h) << bw) | (wmax - w) with the chart index as payload, so equal
+// keys keep index order.  One CTA of 1024 threads: per-tile digit ranks from
+// warp match masks + per-warp digit counts, 8-bit digits, only the
+// significant bits of the key are sorted.
+//
+// prep_kernel then lays out, per sorted position, the int16 footprint slots
+// every candidate uses (slot = footprint at the largest scale, clipped to the
+// dilated atlas) with a block-wide exclusive scan, and flags the pack for a
+// capacity retry if the slots do not fit the current buffers.
+#include "tabi_internal.cuh"
+
+namespace tabi {
+namespace {
+
+constexpr int kT = 1024;
+constexpr int kW = kT / 32;
+
+__device__ __forceinline__ int bits_of(uint64_t v) { return v == 0 ? 0 : 64 - __clzll(v); }
+
+__global__ void __launch_bounds__(kT, 1)
+sort_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n, uint64_t* keys,
+            uint64_t* keys2, int32_t* perm, int32_t* perm2, const Status* st) {
+  __shared__ int32_t wcnt[kW][256];
+  __shared__ int32_t base[256];
+  __shared__ int32_t run[256];
+  __shared__ int32_t tot[256];
+  __shared__ int32_t red[2][kW];
+  if (st->bad_chart != INT32_MAX) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int32_t hm = 0, wm = 0;
+  for (int i = tid; i < n; i += kT) {
+    hm = max(hm, hh[i]);
+    wm = max(wm, ww[i]);
+  }
+  hm = warp_max(hm);
+  wm = warp_max(wm);
+  if (lane == 0) { red[0][wid] = hm; red[1][wid] = wm; }
+  __syncthreads();
+  hm = 0;
+  wm = 0;
+  for (int i = 0; i < kW; i++) { hm = max(hm, red[0][i]); wm = max(wm, red[1][i]); }
+  const int bw = bits_of((uint64_t)wm);
+  const int nbits = bits_of((uint64_t)hm) + bw;
+  for (int i = tid; i < n; i += kT) {
+    keys[i] = ((uint64_t)(hm - hh[i]) << bw) | (uint64_t)(wm - ww[i]);
+    perm[i] = i;
+  }
+  __syncthreads();
+  uint64_t* kin = keys;
+  uint64_t* kout = keys2;
+  int32_t* pin = perm;
+  int32_t* pout = perm2;
+  const int passes = (nbits + 7) / 8;
+  for (int p = 0; p < passes; p++) {
+    const int sh = 8 * p;
+    for (int d = tid; d < 256; d += kT) { base[d] = 0; run[d] = 0; }
+    __syncthreads();
+    for (int i = tid; i < n; i += kT) atomicAdd(&base[(kin[i] >> sh) & 255], 1);
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the 256-bin histogram, 8 bins per lane
+      int32_t v[8], s = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) { v[q] = base[lane * 8 + q]; s += v[q]; }
+      int32_t ex = warp_incl_sum(s, lane) - s;
+#pragma unroll
+      for (int q = 0; q < 8; q++) { base[lane * 8 + q] = ex; ex += v[q]; }
+    }
+    for (int t0 = 0; t0 < n; t0 += kT) {
+      const int i = t0 + tid;
+      const bool valid = i < n;
+      const uint64_t key = valid ? kin[i] : 0;
+      const int32_t pv = valid ? pin[i] : 0;
+      const int d = valid ? (int)((key >> sh) & 255) : 256;
+      for (int q = tid; q < kW * 256; q += kT) (&wcnt[0][0])[q] = 0;
+      __syncthreads();
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      if (valid && rank == 0) wcnt[wid][d] = __popc(peers);
+      __syncthreads();
+      for (int dd = tid; dd < 256; dd += kT) {  // exclusive prefix over warps (stable)
+        int32_t s = 0;
+        for (int w = 0; w < kW; w++) {
+          const int32_t cnt = wcnt[w][dd];
+          wcnt[w][dd] = s;
+          s += cnt;
+        }
+        tot[dd] = s;
+      }
+      __syncthreads();
+      if (valid) {
+        const int32_t dest = base[d] + run[d] + wcnt[wid][d] + rank;
+        kout[dest] = key;
+        pout[dest] = pv;
+      }
+      __syncthreads();
+      for (int dd = tid; dd < 256; dd += kT) run[dd] += tot[dd];
+    }
+    __syncthreads();
+    uint64_t* tk = kin; kin = kout; kout = tk;
+    int32_t* tp = pin; pin = pout; pout = tp;
+  }
+  if (pin != perm) {
+    for (int i = tid; i < n; i += kT) perm[i] = pin[i];
+  }
+}
+
+// Block-wide exclusive scan of two int32 values (one per thread), kT threads.
+__device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, int32_t& eb,
+                                            int32_t& ta, int32_t& tb, int32_t (*sh)[kW + 1]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t ia = warp_incl_sum(a, lane), ib = warp_incl_sum(b, lane);
+  if (lane == 31) { sh[0][wid] = ia; sh[1][wid] = ib; }
+  __syncthreads();
+  if (wid == 0) {
+    int32_t va = sh[0][lane], vb = sh[1][lane];
+    int32_t xa = warp_incl_sum(va, lane), xb = warp_incl_sum(vb, lane);
+    sh[0][lane] = xa - va;
+    sh[1][lane] = xb - vb;
+    if (lane == 31) { sh[0][kW] = xa; sh[1][kW] = xb; }
+  }
+  __syncthreads();
+  ea = sh[0][wid] + ia - a;
+  eb = sh[1][wid] + ib - b;
+  ta = sh[0][kW];
+  tb = sh[1][kW];
+  __syncthreads();
+}
+
+// Footprint slots: column slot of sorted position s = min(ceil(w/256) + 2g, W'),
+// row slot = min(ceil(h/256) + 2g, H') -- the footprint at the largest scale
+// (m = M, scale 1) bounds every candidate's (w_s is monotone in m).
+__global__ void __launch_bounds__(kT, 1)
+prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int32_t* perm,
+            PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted, Status* st) {
+  __shared__ int32_t sh[2][kW + 1];
+  if (st->bad_chart != INT32_MAX) return;
+  int32_t carry_c = 0, carry_r = 0;
+  for (int t0 = 0; t0 < pp.n; t0 += kT) {
+    const int s = t0 + threadIdx.x;
+    int32_t cw = 0, rh = 0;
+    if (s < pp.n) {
+      const int c = perm[s];
+      const int64_t wd = ceildiv(ww[c], TABI_UNITS) + 2 * pp.g;
+      const int64_t hd = ceildiv(hh[c], TABI_UNITS) + 2 * pp.g;
+      cw = (int32_t)(wd < pp.Wp ? wd : pp.Wp);
+      rh = (int32_t)(hd < pp.Hp ? hd : pp.Hp);
+      hsorted[s] = hh[c];
+    }
+    int32_t ec, er, tc, tr;
+    block_scan2(cw, rh, ec, er, tc, tr, sh);
+    if (s < pp.n) {
+      colofs[s] = carry_c + ec;
+      rowofs[s] = carry_r + er;
+    }
+    carry_c += tc;
+    carry_r += tr;
+  }
+  if (threadIdx.x == 0) {
+    st->cols_total = carry_c;
+    st->rows_total = carry_r;
+    if ((int64_t)carry_c > pp.col_cap || (int64_t)carry_r > pp.row_cap) st->capacity |= 1;
+  }
+}
+
+}  // namespace
+
+void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
+                 int32_t* perm2, const Status* st, cudaStream_t s) {
+  sort_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, keys, keys2, perm, perm2, st);
+}
+
+void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
+                 int32_t* rowofs, int32_t* hsorted, Status* st, cudaStream_t s) {
+  prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, perm, pp, colofs, rowofs, hsorted, st);
+}
+
+}  // namespace tabi

@@ -1,0 +1,465 @@
+// tabi_api.cu -- host side of the C ABI declared in include/tabi.h.
+//
+// tabi_pack enqueues the whole pipeline on one stream with no host round trip
+// between kernels:  [H2D] -> K1 proxies -> K2 sort -> prep (slot layout) ->
+// K3 profiles -> K3b offsets/locks -> K4 fold&push (all candidates, one
+// launch) -> K5 select/scatter -> [D2H status (+ placements)] -> one sync.
+// If a device-side capacity check fails (footprint slots or lock-pair lists
+// larger than the current buffers), the context grows those buffers and
+// re-runs from the slot layout; sizes persist, so steady-state calls never
+// retry.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "tabi_internal.cuh"
+
+using namespace tabi;
+
+struct tabi_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int32_t max_n = 0;
+  int64_t max_v = 0;
+  int32_t max_side = 0;
+  // inputs / proxies
+  float* d_xy = nullptr;
+  int32_t* d_start = nullptr;
+  int32_t* d_qx = nullptr;
+  int32_t* d_qy = nullptr;
+  Proxies P{};
+  uint64_t* keys = nullptr;
+  uint64_t* keys2 = nullptr;
+  int32_t* perm = nullptr;
+  int32_t* perm2 = nullptr;
+  int32_t* colofs = nullptr;
+  int32_t* rowofs = nullptr;
+  int32_t* hsorted = nullptr;
+  tabi_placement* d_out = nullptr;
+  Status* d_status = nullptr;
+  Status* h_status = nullptr;  // pinned
+  // per-candidate buffers (sized for cand_M candidates)
+  int32_t cand_M = 0;
+  int32_t* wd = nullptr;
+  int32_t* hd = nullptr;
+  int32_t* off = nullptr;
+  uint8_t* lockbits = nullptr;
+  int32_t* cand_bad = nullptr;
+  int32_t* X = nullptr;
+  int32_t* Y = nullptr;
+  uint8_t* mir = nullptr;
+  Cand* cands = nullptr;
+  Cand* h_cands = nullptr;  // pinned
+  uint32_t* dcol = nullptr;
+  uint32_t* drow = nullptr;
+  int64_t col_cap = 0, row_cap = 0;  // entries per candidate
+  int32_t* scratch = nullptr;
+  int64_t pair_cap = 0;
+  // pinned host staging
+  float* h_xy = nullptr;
+  int32_t* h_start = nullptr;
+  tabi_placement* h_out = nullptr;
+  // last pack (introspection)
+  int32_t last_n = 0, last_M = 0, last_k = 0, last_g = 0;
+  std::string err;
+};
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) {                                  \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return TABI_ECUDA;                                      \
+    }                                                         \
+  } while (0)
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+}
+
+static void dfree_all(tabi_ctx* ctx) {
+  void* ps[] = {ctx->d_xy, ctx->d_start, ctx->d_qx, ctx->d_qy, ctx->P.w, ctx->P.h, ctx->P.area2,
+                ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
+                ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
+                ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
+                ctx->lockbits, ctx->cand_bad, ctx->X, ctx->Y, ctx->mir, ctx->cands, ctx->dcol,
+                ctx->drow, ctx->scratch};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  void* hs[] = {ctx->h_status, ctx->h_cands, ctx->h_xy, ctx->h_start, ctx->h_out};
+  for (void* p : hs)
+    if (p) cudaFreeHost(p);
+}
+
+extern "C" const char* tabi_status_str(tabi_status s) {
+  switch (s) {
+    case TABI_OK: return "ok";
+    case TABI_EINVAL: return "invalid argument";
+    case TABI_NO_FIT: return "no candidate scale fits";
+    case TABI_ECUDA: return "CUDA error";
+    case TABI_ECAPACITY: return "capacity exceeded";
+  }
+  return "unknown";
+}
+
+extern "C" const char* tabi_last_error(tabi_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t max_charts,
+                                       int64_t max_vertices, int32_t max_atlas_side) {
+  if (!out || max_charts < 1 || max_vertices < 3 || max_atlas_side < 1 ||
+      max_atlas_side > TABI_MAX_ATLAS_SIDE)
+    return TABI_EINVAL;
+  tabi_ctx* ctx = new tabi_ctx();
+  *out = nullptr;
+  ctx->device = cuda_device;
+  ctx->max_n = max_charts;
+  ctx->max_v = max_vertices;
+  ctx->max_side = max_atlas_side;
+  auto fail = [&]() {
+    dfree_all(ctx);
+    delete ctx;
+    return TABI_ECUDA;
+  };
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return fail();
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail();
+  const size_t N = (size_t)max_charts, V = (size_t)max_vertices;
+  bool ok = dalloc(&ctx->d_xy, 2 * V) == cudaSuccess && dalloc(&ctx->d_start, N + 1) == cudaSuccess &&
+            dalloc(&ctx->d_qx, V) == cudaSuccess && dalloc(&ctx->d_qy, V) == cudaSuccess &&
+            dalloc(&ctx->P.w, N) == cudaSuccess && dalloc(&ctx->P.h, N) == cudaSuccess &&
+            dalloc(&ctx->P.area2, N) == cudaSuccess && dalloc(&ctx->P.xmin, N) == cudaSuccess &&
+            dalloc(&ctx->P.ymin, N) == cudaSuccess && dalloc(&ctx->P.pose, N) == cudaSuccess &&
+            dalloc(&ctx->P.sl, N * 4 * TABI_KMAX) == cudaSuccess &&
+            dalloc(&ctx->P.obb_j, N) == cudaSuccess && dalloc(&ctx->P.obb, 4 * N) == cudaSuccess &&
+            dalloc(&ctx->keys, N) == cudaSuccess && dalloc(&ctx->keys2, N) == cudaSuccess &&
+            dalloc(&ctx->perm, N) == cudaSuccess && dalloc(&ctx->perm2, N) == cudaSuccess &&
+            dalloc(&ctx->colofs, N) == cudaSuccess && dalloc(&ctx->rowofs, N) == cudaSuccess &&
+            dalloc(&ctx->hsorted, N) == cudaSuccess && dalloc(&ctx->d_out, N) == cudaSuccess &&
+            dalloc(&ctx->d_status, 1) == cudaSuccess;
+  if (!ok) return fail();
+  if (cudaMallocHost((void**)&ctx->h_status, sizeof(Status)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_xy, sizeof(float) * 2 * V) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_start, sizeof(int32_t) * (N + 1)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_out, sizeof(tabi_placement) * N) != cudaSuccess)
+    return fail();
+  // initial footprint slot capacity per candidate (grows on demand)
+  ctx->col_cap = (int64_t)N * 96 + 4 * (int64_t)max_atlas_side;
+  ctx->row_cap = ctx->col_cap;
+  ctx->pair_cap = (int64_t)N * 2 + 1024;
+  *out = ctx;
+  return TABI_OK;
+}
+
+extern "C" void tabi_ctx_destroy(tabi_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  dfree_all(ctx);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols, bool regrow_pairs) {
+  const size_t N = (size_t)ctx->max_n;
+  if (M > ctx->cand_M) {
+    CK(dalloc(&ctx->wd, (size_t)M * N));
+    CK(dalloc(&ctx->hd, (size_t)M * N));
+    CK(dalloc(&ctx->off, (size_t)M * N));
+    CK(dalloc(&ctx->lockbits, (size_t)M * N));
+    CK(dalloc(&ctx->cand_bad, (size_t)M));
+    CK(dalloc(&ctx->X, (size_t)M * N));
+    CK(dalloc(&ctx->Y, (size_t)M * N));
+    CK(dalloc(&ctx->mir, (size_t)M * N));
+    CK(dalloc(&ctx->cands, (size_t)M));
+    if (ctx->h_cands) cudaFreeHost(ctx->h_cands);
+    CK(cudaMallocHost((void**)&ctx->h_cands, sizeof(Cand) * M));
+    regrow_cols = regrow_pairs = true;
+    ctx->cand_M = M;
+  }
+  const int32_t Mc = ctx->cand_M;
+  if (regrow_cols) {
+    CK(dalloc(&ctx->dcol, (size_t)Mc * ctx->col_cap));
+    CK(dalloc(&ctx->drow, (size_t)Mc * ctx->row_cap));
+  }
+  if (regrow_pairs) CK(dalloc(&ctx->scratch, (size_t)Mc * (6 * N + 3 * (size_t)ctx->pair_cap)));
+  return TABI_OK;
+}
+
+static bool spec_ok(const tabi_spec* s) {
+  return s && s->atlas_w >= 1 && s->atlas_h >= 1 && s->atlas_w <= TABI_MAX_ATLAS_SIDE &&
+         s->atlas_h <= TABI_MAX_ATLAS_SIDE && s->gutter >= 0 && s->gutter <= 64 &&
+         s->scale_count >= 1 && s->scale_count <= TABI_MAX_SCALES && s->local_aabb_count >= 1 &&
+         s->local_aabb_count <= TABI_MAX_LOCAL_AABBS && s->t_opt_bp >= -1 &&
+         s->t_opt_bp <= 10000 && (s->flags & ~7u) == 0;
+}
+
+namespace {
+struct Timer {
+  bool on = false;
+  cudaEvent_t ev[9];
+  int n = 0;
+  void init(bool enable) {
+    on = enable;
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark(cudaStream_t s) {
+    if (on && n < 9) cudaEventRecord(ev[n++], s);
+  }
+  void finish(tabi_info* info) {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 0; i + 1 < n && i < 8; i++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      if (info) info->stage_ms[i] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+}  // namespace
+
+extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                                 int32_t n, float res_x, float res_y, const tabi_spec* spec,
+                                 tabi_placement* out, tabi_info* info, int on_device,
+                                 void* stream) {
+  if (!ctx) return TABI_EINVAL;
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->bad_chart = -1;
+  }
+  if (!xy || !chart_start || !out || n < 1 || !spec_ok(spec)) return TABI_EINVAL;
+  if (n > ctx->max_n || spec->atlas_w > ctx->max_side || spec->atlas_h > ctx->max_side)
+    return TABI_ECAPACITY;
+  const int32_t t_opt = spec->t_opt_bp >= 0 ? spec->t_opt_bp : (n > 10000 ? 100 : 0);
+  if (t_opt > 0) return TABI_EINVAL;  // prefix tail not in this build yet
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+  int launches = 0;
+  Timer tm;
+  const char* tenv = getenv("TABI_TIMING");
+  tm.init(tenv && tenv[0] == '1');
+  tm.mark(s);
+
+  const float* d_xy = xy;
+  const int32_t* d_start = chart_start;
+  if (!on_device) {
+    const int64_t V = chart_start[n];
+    if (chart_start[0] != 0 || V < 3) {
+      if (info) info->bad_chart = 0;
+      return TABI_EINVAL;
+    }
+    for (int32_t c = 0; c < n; c++)
+      if (chart_start[c + 1] - chart_start[c] < 3) {
+        if (info) info->bad_chart = c;
+        return TABI_EINVAL;
+      }
+    if (V > ctx->max_v) return TABI_ECAPACITY;
+    memcpy(ctx->h_xy, xy, sizeof(float) * 2 * V);
+    memcpy(ctx->h_start, chart_start, sizeof(int32_t) * (n + 1));
+    CK(cudaMemcpyAsync(ctx->d_xy, ctx->h_xy, sizeof(float) * 2 * V, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->d_start, ctx->h_start, sizeof(int32_t) * (n + 1),
+                       cudaMemcpyHostToDevice, s));
+    d_xy = ctx->d_xy;
+    d_start = ctx->d_start;
+  }
+  tm.mark(s);
+  const int32_t M = spec->scale_count;
+  tabi_status ts = ensure_candidates(ctx, M, false, false);
+  if (ts != TABI_OK) return ts;
+
+  PackParams pp;
+  pp.n = n;
+  pp.k = spec->local_aabb_count;
+  pp.M = M;
+  pp.g = spec->gutter;
+  pp.W = spec->atlas_w;
+  pp.H = spec->atlas_h;
+  pp.Wp = spec->atlas_w + 2 * spec->gutter;
+  pp.Hp = spec->atlas_h + 2 * spec->gutter;
+  pp.flags = spec->flags;
+
+  Status init{};
+  init.bad_chart = INT32_MAX;
+  *ctx->h_status = init;
+  CK(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, s));
+  launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
+  launches++;
+  tm.mark(s);
+  launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
+  launches++;
+  tm.mark(s);
+  tabi_placement* d_out = on_device ? out : ctx->d_out;
+  for (int attempt = 0; attempt < 6; attempt++) {
+    pp.col_cap = ctx->col_cap;
+    pp.row_cap = ctx->row_cap;
+    launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->d_status, s);
+    CK(cudaMemsetAsync(ctx->cand_bad, 0, sizeof(int32_t) * M, s));
+    launch_profiles(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
+                    (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->d_status, s);
+    launches += 2;
+    tm.mark(s);
+    launch_offsets(pp, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
+                   ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
+    launches++;
+    tm.mark(s);
+    launch_pack(pp, ctx->colofs, ctx->rowofs, ctx->dcol, ctx->drow, ctx->wd, ctx->hd, ctx->off,
+                ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
+                ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
+    launches++;
+    tm.mark(s);
+    launch_select(pp, ctx->P, ctx->perm, ctx->wd, ctx->hd, ctx->X, ctx->Y, ctx->mir, ctx->cands,
+                  d_out, ctx->d_status, s);
+    launches++;
+    tm.mark(s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->h_cands, ctx->cands, sizeof(Cand) * M, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const Status st = *ctx->h_status;
+    if (st.bad_chart != INT32_MAX) {
+      if (info) info->bad_chart = st.bad_chart;
+      return TABI_EINVAL;
+    }
+    if (!st.capacity) break;
+    // grow and retry from the slot layout (proxies and order are kept)
+    bool cols = false, pairs = false;
+    if (st.capacity & 1) {
+      ctx->col_cap = (int64_t)st.cols_total + (st.cols_total >> 2) + 1024;
+      ctx->row_cap = (int64_t)st.rows_total + (st.rows_total >> 2) + 1024;
+      cols = true;
+    }
+    if (st.capacity & 2) {
+      ctx->pair_cap = (int64_t)st.pad[0] * 2 + 1024;
+      pairs = true;
+    }
+    ts = ensure_candidates(ctx, M, cols, pairs);
+    if (ts != TABI_OK) return ts;
+    Status again = init;
+    *ctx->h_status = again;
+    CK(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, s));
+    tm.n = 3;  // re-time the retried stages
+    if (attempt == 5) return TABI_ECAPACITY;
+  }
+  ctx->last_n = n;
+  ctx->last_M = M;
+  ctx->last_k = pp.k;
+  ctx->last_g = pp.g;
+  const int32_t win = ctx->h_status->winner;
+  if (win == 0) {
+    if (info) info->gpu_launches = launches;
+    return TABI_NO_FIT;
+  }
+  if (!on_device) {
+    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(tabi_placement) * n, cudaMemcpyDeviceToHost, s));
+    tm.mark(s);
+    CK(cudaStreamSynchronize(s));
+    memcpy(out, ctx->h_out, sizeof(tabi_placement) * n);
+  }
+  tm.finish(info);
+  if (info) {
+    const Cand& c = ctx->h_cands[win - 1];
+    info->scale_index = win;
+    info->l2_stretch = (double)M / (double)win;  // uniform scale s: per-triangle stretch 1/s
+    info->rows = c.rows;
+    info->knees_found = c.knees_found;
+    info->knee_rows = c.knee_rows;
+    info->prefix_rows = c.prefix_rows;
+    info->gpu_launches = launches;
+  }
+  return TABI_OK;
+}
+
+// ---- introspection ---------------------------------------------------------
+
+extern "C" tabi_status tabi_debug_proxies(tabi_ctx* ctx, tabi_proxy_dbg* out) {
+  if (!ctx || !out || ctx->last_n < 1) return TABI_EINVAL;
+  const int n = ctx->last_n, k = ctx->last_k;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int32_t *w = new int32_t[n], *h = new int32_t[n], *xm = new int32_t[n], *ym = new int32_t[n];
+  int32_t *oj = new int32_t[n], *sl = new int32_t[(size_t)n * 4 * k];
+  int64_t *a2 = new int64_t[n], *ob = new int64_t[4 * (size_t)n];
+  uint8_t* pose = new uint8_t[n];
+  cudaMemcpy(w, ctx->P.w, 4 * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(h, ctx->P.h, 4 * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(xm, ctx->P.xmin, 4 * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ym, ctx->P.ymin, 4 * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(oj, ctx->P.obb_j, 4 * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(sl, ctx->P.sl, sizeof(int32_t) * (size_t)n * 4 * k, cudaMemcpyDeviceToHost);
+  cudaMemcpy(a2, ctx->P.area2, 8 * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ob, ctx->P.obb, 32 * (size_t)n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(pose, ctx->P.pose, n, cudaMemcpyDeviceToHost);
+  for (int c = 0; c < n; c++) {
+    tabi_proxy_dbg& d = out[c];
+    memset(&d, 0, sizeof(d));
+    d.w = w[c]; d.h = h[c]; d.area2 = a2[c]; d.xmin = xm[c]; d.ymin = ym[c];
+    d.rot90 = pose[c] & 1; d.fx = (pose[c] >> 1) & 1; d.fy = (pose[c] >> 2) & 1; d.k = k;
+    for (int j = 0; j < k; j++) {
+      d.top[j] = sl[(size_t)c * 4 * k + j];
+      d.bot[j] = sl[(size_t)c * 4 * k + k + j];
+      d.left[j] = sl[(size_t)c * 4 * k + 2 * k + j];
+      d.right[j] = sl[(size_t)c * 4 * k + 3 * k + j];
+    }
+    d.obb_j = oj[c];
+    d.umin = ob[4 * c]; d.umax = ob[4 * c + 1]; d.vmin = ob[4 * c + 2]; d.vmax = ob[4 * c + 3];
+  }
+  delete[] w; delete[] h; delete[] xm; delete[] ym; delete[] oj; delete[] sl;
+  delete[] a2; delete[] ob; delete[] pose;
+  CK(cudaGetLastError());
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_perm(tabi_ctx* ctx, int32_t* perm) {
+  if (!ctx || !perm || ctx->last_n < 1) return TABI_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy(perm, ctx->perm, sizeof(int32_t) * ctx->last_n, cudaMemcpyDeviceToHost));
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_candidates(tabi_ctx* ctx, tabi_cand_dbg* out) {
+  if (!ctx || !out || ctx->last_n < 1) return TABI_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy(out, ctx->cands, sizeof(Cand) * ctx->last_M, cudaMemcpyDeviceToHost));
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_profile(tabi_ctx* ctx, int32_t m, int32_t s, int32_t* wd_hd,
+                                          int32_t* dtop, int32_t* dbot, int32_t* dleft,
+                                          int32_t* dright) {
+  if (!ctx || ctx->last_n < 1 || m < 1 || m > ctx->last_M || s < 0 || s >= ctx->last_n)
+    return TABI_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const int64_t b = (int64_t)(m - 1) * ctx->last_n + s;
+  int32_t Wd, Hd, co, ro, bad;
+  CK(cudaMemcpy(&Wd, ctx->wd + b, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&Hd, ctx->hd + b, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&co, ctx->colofs + s, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&ro, ctx->rowofs + s, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&bad, ctx->cand_bad + (m - 1), 4, cudaMemcpyDeviceToHost));
+  wd_hd[0] = Wd;
+  wd_hd[1] = Hd;
+  if (bad) return TABI_NO_FIT;  // candidate skipped (a chart exceeds the atlas)
+  uint32_t* c = new uint32_t[Wd];
+  uint32_t* r = new uint32_t[Hd];
+  cudaMemcpy(c, ctx->dcol + (int64_t)(m - 1) * ctx->col_cap + co, 4 * (size_t)Wd, cudaMemcpyDeviceToHost);
+  cudaMemcpy(r, ctx->drow + (int64_t)(m - 1) * ctx->row_cap + ro, 4 * (size_t)Hd, cudaMemcpyDeviceToHost);
+  for (int i = 0; i < Wd; i++) { dtop[i] = (int32_t)(c[i] & 0xffff); dbot[i] = (int32_t)(c[i] >> 16); }
+  for (int i = 0; i < Hd; i++) { dleft[i] = (int32_t)(r[i] & 0xffff); dright[i] = (int32_t)(r[i] >> 16); }
+  delete[] c;
+  delete[] r;
+  CK(cudaGetLastError());
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* lockbits) {
+  if (!ctx || ctx->last_n < 1 || m < 1 || m > ctx->last_M) return TABI_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const int64_t b = (int64_t)(m - 1) * ctx->last_n;
+  CK(cudaMemcpy(off, ctx->off + b, sizeof(int32_t) * ctx->last_n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(lockbits, ctx->lockbits + b, ctx->last_n, cudaMemcpyDeviceToHost));
+  return TABI_OK;
+}

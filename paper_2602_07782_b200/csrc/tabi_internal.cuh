@@ -1,0 +1,220 @@
+// tabi_internal.cuh -- device helpers and the context layout of the CUDA path.
+//
+// Integer model: coordinates are snapped once to
+// 1/256 texel (int32), all later geometry is exact int64 / int128 with
+// directed rounding, so the GPU reproduces the paper's method bit for bit
+// under the readings listed in DESIGN.md.  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tabi.h"
+
+typedef __int128 i128;
+
+#define TABI_KMAX 64
+#define TABI_QMAX (1 << 24)
+#define TABI_UNITS 256
+
+namespace tabi {
+
+// ---- exact division with directed rounding (divisor > 0) -------------------
+__host__ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b) != 0 && a < 0) q--;
+  return q;
+}
+__host__ __device__ __forceinline__ int64_t ceildiv(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b) != 0 && a > 0) q++;
+  return q;
+}
+__device__ __forceinline__ i128 floordiv128(i128 a, i128 b) {
+  i128 q = a / b;
+  if ((a % b) != 0 && a < 0) q--;
+  return q;
+}
+__device__ __forceinline__ i128 ceildiv128(i128 a, i128 b) {
+  i128 q = a / b;
+  if ((a % b) != 0 && a > 0) q++;
+  return q;
+}
+
+// ---- warp reductions (full warp) ------------------------------------------
+__device__ __forceinline__ int32_t warp_max(int32_t v) {
+  return __reduce_max_sync(0xffffffffu, v);
+}
+__device__ __forceinline__ int32_t warp_min(int32_t v) {
+  return __reduce_min_sync(0xffffffffu, v);
+}
+__device__ __forceinline__ int32_t warp_sum(int32_t v) {
+  return __reduce_add_sync(0xffffffffu, v);
+}
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_min64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ i128 warp_sum128(i128 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
+    lo = __shfl_xor_sync(0xffffffffu, lo, o);
+    hi = __shfl_xor_sync(0xffffffffu, hi, o);
+    v += (i128)(((unsigned __int128)hi << 64) | lo);
+  }
+  return v;
+}
+// inclusive warp scans
+__device__ __forceinline__ int32_t warp_incl_sum(int32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ int32_t warp_incl_min(int32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = t < v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int32_t warp_incl_max(int32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = t > v ? t : v;
+  }
+  return v;
+}
+
+// Q30 rotation table for the 8 OBB angles theta_j = j*pi/16, j = 0..7
+// ("8 evenly spaced rotations in the interval [0, 7pi/16]").
+// Rounded cos/sin * 2^30 written as literals so no libm result enters the
+// geometry (reading R6).
+__constant__ const int64_t kQC[8] = {1073741824LL, 1053110176LL, 992008094LL, 892783698LL,
+                                      759250125LL,  596538995LL,  410903207LL, 209476638LL};
+__constant__ const int64_t kQS[8] = {0LL,          209476638LL, 410903207LL, 596538995LL,
+                                      759250125LL,  892783698LL, 992008094LL, 1053110176LL};
+
+// Footprint entries are two uint16 packed in a uint32: columns (Dtop | Dbot << 16),
+// rows (Dleft | Dright << 16).
+__device__ __forceinline__ int32_t lo16(uint32_t v) { return (int32_t)(v & 0xffffu); }
+__device__ __forceinline__ int32_t hi16(uint32_t v) { return (int32_t)(v >> 16); }
+
+// D15 CannotMoveAbove for the pair (a, b), a before b in the sorted line and
+// b's footprint starting `delta` columns right of a's (top-aligned).  Moving a
+// up by t puts a's row r beside b's row r - t < r; a is locked iff for some
+// r >= 1, a's right edge there passes b's left edge of some row above r
+// ("no rectangular segment ... is below a segment of the other chart's
+// boundary").  Requires Hda >= Hdb (sorted by height).  Whole warp calls.
+__device__ __forceinline__ void warp_locks(const uint32_t* ra, const uint32_t* rb, int32_t Hda,
+                                           int32_t Hdb, int32_t delta, int lane, bool& la,
+                                           bool& lb) {
+  bool xa = false, xb = false;
+  int32_t cmin_b = INT32_MAX, cmax_a = INT32_MIN;
+  for (int base = 0; base < Hdb; base += 32) {
+    const int r = base + lane;
+    const bool valid = r < Hdb;
+    const int32_t lb_r = valid ? lo16(rb[r]) : INT32_MAX;
+    const int32_t ra_r = valid ? hi16(ra[r]) : INT32_MIN;
+    const int32_t imin = warp_incl_min(lb_r, lane);
+    const int32_t imax = warp_incl_max(ra_r, lane);
+    int32_t emin = __shfl_up_sync(0xffffffffu, imin, 1);
+    int32_t emax = __shfl_up_sync(0xffffffffu, imax, 1);
+    if (lane == 0) { emin = INT32_MAX; emax = INT32_MIN; }
+    emin = min(emin, cmin_b);
+    emax = max(emax, cmax_a);
+    if (valid && r >= 1) {
+      if (emin != INT32_MAX && ra_r > delta + emin) xa = true;
+      if (emax != INT32_MIN && delta + lb_r < emax) xb = true;
+    }
+    cmin_b = min(cmin_b, __shfl_sync(0xffffffffu, imin, 31));
+    cmax_a = max(cmax_a, __shfl_sync(0xffffffffu, imax, 31));
+  }
+  for (int r = Hdb + lane; r < Hda; r += 32) {
+    if (r >= 1 && hi16(ra[r]) > delta + cmin_b) xa = true;
+  }
+  la = __any_sync(0xffffffffu, xa);
+  lb = __any_sync(0xffffffffu, xb);
+}
+
+// ---- device-side per-pack state -------------------------------------------
+// Proxy SoA (final pose).  Slices: sl[c * 4k + {0: top, 1: bot, 2: left, 3: right} * k + j]
+struct Proxies {
+  int32_t* w;
+  int32_t* h;
+  int64_t* area2;
+  int32_t* xmin;
+  int32_t* ymin;
+  uint8_t* pose;     // bit0 rot90, bit1 fx, bit2 fy
+  int32_t* sl;
+  int32_t* obb_j;
+  int64_t* obb;      // [c*4 + {umin, umax, vmin, vmax}]
+};
+
+struct Status {       // device-side status block, copied back once per pack
+  int32_t bad_chart;  // INT32_MAX if none
+  int32_t capacity;   // required column/row slot totals exceeded capacity
+  int32_t winner;     // winning m (0 = none)
+  int32_t cols_total, rows_total;
+  int32_t pad[3];
+};
+
+// Per-candidate result record (mirrors tabi_cand_dbg).
+struct Cand {
+  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p, switched_at;
+};
+
+struct PackParams {
+  int32_t n, k, M, g, W, H, Wp, Hp;
+  uint32_t flags;
+  int64_t col_cap, row_cap;   // per-candidate footprint slot capacity (entries)
+};
+
+}  // namespace tabi
+
+// Launch wrappers (defined in the .cu files)
+namespace tabi {
+void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
+                    int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
+void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
+                 int32_t* perm2, const Status* st, cudaStream_t s);
+void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
+                 int32_t* rowofs, int32_t* hsorted, Status* st, cudaStream_t s);
+void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
+                     const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
+                     int32_t* wd, int32_t* hd, int32_t* cand_bad, const Status* st,
+                     cudaStream_t s);
+void launch_offsets(const PackParams& pp, const int32_t* colofs, const int32_t* rowofs,
+                    const int16_t* drow, const int32_t* wd, const int32_t* hd, int32_t* off,
+                    uint8_t* lockbits, const int32_t* cand_bad, const Status* st,
+                    cudaStream_t s);
+void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* rowofs,
+                 const uint32_t* dcol, const uint32_t* drow, const int32_t* wd, const int32_t* hd,
+                 const int32_t* off, const uint8_t* lockbits, const int32_t* hsorted,
+                 const int32_t* cand_bad, int32_t* scratch, int64_t pair_cap, int32_t* X,
+                 int32_t* Y, uint8_t* mir, Cand* cands, Status* st, cudaStream_t s);
+void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
+                   const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
+                   const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s);
+}  // namespace tabi

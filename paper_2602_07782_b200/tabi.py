@@ -1,0 +1,205 @@
+"""Thin ctypes binding of the TABI C ABI (include/tabi.h).
+
+Argument marshalling only: every step of the packing runs in the CUDA kernels
+of ``libtabi.so``. There is no CPU fallback -- if the library or a GPU is
+missing, these calls raise.
+
+Inputs may be numpy arrays (host; the library copies them in and the result
+out inside the call) or CUDA torch tensors (device pointers, run on
+``torch.cuda.current_stream()``); torch is used only for device memory and
+streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtabi.so")
+
+OK, EINVAL, NO_FIT, ECUDA, ECAPACITY = 0, 1, 2, 3, 4
+F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY = 1, 2, 4
+STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "no candidate scale fits", 3: "CUDA error",
+                4: "capacity exceeded"}
+
+
+class TabiError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"tabi status {status} ({STATUS_NAMES.get(status, '?')}) {msg}".strip())
+        self.status = status
+
+
+class Spec(C.Structure):
+    _fields_ = [("atlas_w", C.c_int32), ("atlas_h", C.c_int32), ("gutter", C.c_int32),
+                ("scale_count", C.c_int32), ("local_aabb_count", C.c_int32),
+                ("t_opt_bp", C.c_int32), ("flags", C.c_uint32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("scale_index", C.c_int32), ("reserved0", C.c_int32), ("l2_stretch", C.c_double),
+                ("rows", C.c_int32), ("knees_found", C.c_int32), ("knee_rows", C.c_int32),
+                ("prefix_rows", C.c_int32), ("bad_chart", C.c_int32), ("gpu_launches", C.c_int32),
+                ("stage_ms", C.c_float * 8)]
+
+
+PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
+                            ("scale_den", "<i4"), ("box_w", "<i4"), ("box_h", "<i4"),
+                            ("rot90", "u1"), ("flip_x", "u1"), ("flip_y", "u1"),
+                            ("mirror_x", "u1"), ("mode", "u1"), ("pad", "u1", (3,))])
+assert PLACEMENT_DTYPE.itemsize == 32
+
+PROXY_DTYPE = np.dtype([("w", "<i4"), ("h", "<i4"), ("area2", "<i8"), ("xmin", "<i4"),
+                        ("ymin", "<i4"), ("rot90", "<i4"), ("fx", "<i4"), ("fy", "<i4"),
+                        ("k", "<i4"), ("top", "<i4", (64,)), ("bot", "<i4", (64,)),
+                        ("left", "<i4", (64,)), ("right", "<i4", (64,)), ("obb_j", "<i4"),
+                        ("reserved", "<i4"), ("umin", "<i8"), ("umax", "<i8"), ("vmin", "<i8"),
+                        ("vmax", "<i8")])
+CAND_DTYPE = np.dtype([(f, "<i4") for f in ("success", "score", "rows", "knees_found",
+                                            "knee_rows", "prefix_rows", "p", "switched_at")])
+
+_lib = None
+
+
+def lib():
+    """Load libtabi.so (built in-tree by ``paper_2602_07782_b200.build``)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TabiError(ECUDA, f"native library missing: {LIB_PATH} (run build())")
+        L = C.CDLL(LIB_PATH)
+        P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.tabi_ctx_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, i32, i64, i32]
+        L.tabi_ctx_destroy.argtypes = [P]
+        L.tabi_pack.argtypes = [P, P, P, i32, C.c_float, C.c_float, C.POINTER(Spec), P,
+                                C.POINTER(Info), C.c_int, P]
+        L.tabi_status_str.restype = C.c_char_p
+        L.tabi_status_str.argtypes = [C.c_int]
+        L.tabi_last_error.restype = C.c_char_p
+        L.tabi_last_error.argtypes = [P]
+        L.tabi_debug_proxies.argtypes = [P, P]
+        L.tabi_debug_perm.argtypes = [P, P]
+        L.tabi_debug_candidates.argtypes = [P, P]
+        L.tabi_debug_profile.argtypes = [P, i32, i32, P, P, P, P, P]
+        L.tabi_debug_offsets.argtypes = [P, i32, P, P]
+        _lib = L
+    return _lib
+
+
+EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
+           "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
+           "tabi_debug_profile", "tabi_debug_offsets"]
+
+
+def _ptr(a):
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def make_spec(atlas_w, atlas_h, gutter=1, scale_count=64, local_aabb_count=10, t_opt_bp=0,
+              flags=0) -> Spec:
+    return Spec(atlas_w, atlas_h, gutter, scale_count, local_aabb_count, t_opt_bp, flags)
+
+
+def spec_of(cs, **kw) -> Spec:
+    d = dict(gutter=cs.gutter, scale_count=cs.scale_count, local_aabb_count=cs.local_aabb_count,
+             t_opt_bp=cs.t_opt_bp, flags=0)
+    d.update(kw)
+    return make_spec(cs.atlas_w, cs.atlas_h, **d)
+
+
+class Context:
+    """One device workspace + stream (``tabi_ctx``)."""
+
+    def __init__(self, device: int = 0, max_charts: int = 1 << 16, max_vertices: int = 1 << 20,
+                 max_atlas_side: int = 16384):
+        h = C.c_void_p()
+        st = lib().tabi_ctx_create(C.byref(h), device, max_charts, max_vertices, max_atlas_side)
+        if st != OK:
+            raise TabiError(st, "tabi_ctx_create")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tabi_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_error(self) -> str:
+        return lib().tabi_last_error(self.h).decode()
+
+    def pack(self, xy, start, spec: Spec, res=(1.0, 1.0), out=None, stream=None,
+             raise_on_error=True):
+        """Pack one atlas. Host numpy inputs -> host numpy placements; CUDA tensors
+        (xy float32, start int32, out uint8[32*N]) -> device placements.
+        Returns (status, placements, Info)."""
+        on_device = hasattr(xy, "is_cuda") and xy.is_cuda
+        n = int(start.shape[0]) - 1
+        info = Info()
+        if on_device:
+            import torch
+            if out is None:
+                out = torch.empty(n * PLACEMENT_DTYPE.itemsize, dtype=torch.uint8, device=xy.device)
+            if stream is None:
+                stream = torch.cuda.current_stream(xy.device).cuda_stream
+            st = lib().tabi_pack(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], C.byref(spec),
+                                 _ptr(out), C.byref(info), 1, C.c_void_p(stream))
+        else:
+            xy = np.ascontiguousarray(xy, dtype=np.float32)
+            start = np.ascontiguousarray(start, dtype=np.int32)
+            if out is None:
+                out = np.zeros(n, dtype=PLACEMENT_DTYPE)
+            st = lib().tabi_pack(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], C.byref(spec),
+                                 _ptr(out), C.byref(info), 0,
+                                 C.c_void_p(stream) if stream else None)
+        if raise_on_error and st not in (OK, NO_FIT):
+            raise TabiError(st, f"bad_chart={info.bad_chart} {self.last_error()}")
+        return st, out, info
+
+    def pack_set(self, cs, res=None, **spec_kw):
+        r = (cs.res, cs.res) if res is None else res
+        return self.pack(cs.xy, cs.start, spec_of(cs, **spec_kw), res=r)
+
+    # ---- introspection of the last pack ----
+    def proxies(self, n):
+        out = np.zeros(n, dtype=PROXY_DTYPE)
+        self._chk(lib().tabi_debug_proxies(self.h, _ptr(out)))
+        return out
+
+    def perm(self, n):
+        out = np.zeros(n, dtype=np.int32)
+        self._chk(lib().tabi_debug_perm(self.h, _ptr(out)))
+        return out
+
+    def candidates(self, M):
+        out = np.zeros(M, dtype=CAND_DTYPE)
+        self._chk(lib().tabi_debug_candidates(self.h, _ptr(out)))
+        return out
+
+    def profile(self, m, s, max_len=1 << 16):
+        wh = np.zeros(2, dtype=np.int32)
+        bufs = [np.zeros(max_len, dtype=np.int32) for _ in range(4)]
+        st = lib().tabi_debug_profile(self.h, m, s, _ptr(wh), *[_ptr(b) for b in bufs])
+        if st == NO_FIT:
+            return None
+        self._chk(st)
+        Wd, Hd = int(wh[0]), int(wh[1])
+        return Wd, Hd, bufs[0][:Wd], bufs[1][:Wd], bufs[2][:Hd], bufs[3][:Hd]
+
+    def offsets(self, m, n):
+        off = np.zeros(n, dtype=np.int32)
+        lk = np.zeros(n, dtype=np.uint8)
+        self._chk(lib().tabi_debug_offsets(self.h, m, _ptr(off), _ptr(lk)))
+        return off, lk
+
+    def _chk(self, st):
+        if st != OK:
+            raise TabiError(st, self.last_error())

@@ -1,0 +1,197 @@
+"""CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): proxies, order, footprints, offsets, lock
+flags, per-candidate outcomes, row statistics and placements bit-exact;
+scale and stretch within 1e-6 relative.  Small cases span several rows,
+knees and ragged tails; full-size C3 (1,572 charts, 4096^2) is compared in
+full (the oracle finishes it in seconds).
+"""
+import numpy as np
+import pytest
+
+import chartgen
+
+pytestmark = pytest.mark.gpu
+
+PROXY_FIELDS = ("w", "h", "area2", "xmin", "ymin", "rot90", "fx", "fy", "obb_j", "umin", "umax",
+                "vmin", "vmax")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2602_07782_b200 import Context
+    c = Context(0, max_charts=25000, max_vertices=1 << 19, max_atlas_side=16384)
+    yield c
+    c.close()
+
+
+def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
+    import oracle
+    from paper_2602_07782_b200 import spec_of
+    st_o, pl_o, info_o, cands_o = oracle.pack(cs, res=res, with_cands=True, **kw)
+    st_g, pl_g, info_g = ctx.pack(cs.xy, cs.start, spec_of(cs, **kw), res=res)
+    assert st_g == st_o, (st_g, st_o)
+    if st_o != oracle.OK:
+        return st_o
+    n = cs.n_charts
+    M = kw.get("scale_count", cs.scale_count)
+    k = kw.get("local_aabb_count", cs.local_aabb_count)
+    g = kw.get("gutter", cs.gutter)
+    # proxies (D3-D8) bit-exact
+    st, px, _ = oracle.build_proxies(cs.xy, cs.start, k, res)
+    gp = ctx.proxies(n)
+    for f in PROXY_FIELDS:
+        assert np.array_equal(gp[f], np.array([getattr(p, f) for p in px])), f
+    for f in ("top", "bot", "left", "right"):
+        assert np.array_equal(gp[f][:, :k], np.array([list(getattr(p, f))[:k] for p in px])), f
+    # order (D9)
+    perm_o = oracle.sort_order(px)
+    assert np.array_equal(ctx.perm(n), perm_o)
+    # per-candidate outcomes
+    gc = ctx.candidates(M)
+    for m in range(1, M + 1):
+        co = cands_o[m - 1]
+        assert gc["success"][m - 1] == co.success, m
+        if co.success:
+            for f in ("score", "rows", "knees_found", "knee_rows"):
+                assert gc[f][m - 1] == getattr(co, f), (m, f)
+    # placements bit-exact, scale/stretch
+    for f in ("tx", "ty", "scale_num", "scale_den", "box_w", "box_h", "rot90", "flip_x", "flip_y",
+              "mirror_x", "mode"):
+        assert np.array_equal(pl_g[f], pl_o[f]), f
+    assert info_g.scale_index == info_o.scale_index
+    assert info_g.l2_stretch == pytest.approx(info_o.l2_stretch, rel=1e-6)
+    assert (info_g.rows, info_g.knees_found, info_g.knee_rows) == (
+        info_o.rows, info_o.knees_found, info_o.knee_rows)
+    # footprints and offsets on sampled candidates / charts
+    if check_profiles:
+        rng = chartgen.SplitMix64(n * 7 + M)
+        ms = sorted({M, info_o.scale_index, max(1, M // 3), rng.randint(1, M)})
+        for m in ms:
+            if not gc["success"][m - 1] and not cands_o[m - 1].success:
+                continue
+            off_g, lk_g = ctx.offsets(m, n)
+            ss = sorted({0, n - 1, *[rng.randint(0, n - 1) for _ in range(check_profiles)]})
+            for s in ss:
+                prof = ctx.profile(m, s)
+                po = oracle.Profile(px[perm_o[s]], m, M, g)
+                assert prof is not None
+                Wd, Hd, dt, db, dl, dr = prof
+                assert (Wd, Hd) == (po.Wd, po.Hd)
+                assert np.array_equal(dt, po.Dtop) and np.array_equal(db, po.Dbot)
+                assert np.array_equal(dl, po.Dleft) and np.array_equal(dr, po.Dright)
+                if s + 1 < n:
+                    pn = oracle.Profile(px[perm_o[s + 1]], m, M, g)
+                    off = oracle.offset(po, pn)
+                    assert off_g[s] == off
+                    la, lb = oracle.locks(po, pn, off) if off < po.Wd else (False, False)
+                    assert lk_g[s] == (1 if la else 0) | (2 if lb else 0)
+    return st_o
+
+
+SMALL = ([chartgen.config1a(s) for s in range(6)] + [chartgen.config1b(s) for s in range(6)] +
+         [chartgen.small_case(s, n=48) for s in range(4)] +
+         [chartgen.small_case(s, n=48, family="uv") for s in range(4)] +
+         [chartgen.small_case(s, n=64, family="mixed", rho=1.2) for s in range(3)] +
+         [chartgen.small_case(s, n=200, family="uv", side=512, rho=0.9) for s in range(2)])
+
+
+@pytest.mark.parametrize("cs", SMALL, ids=lambda c: c.name)
+def test_small_parity(orc, ctx, cs):
+    _compare_pack(orc, ctx, cs, check_profiles=6)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_config2_parity(orc, ctx, seed):
+    _compare_pack(orc, ctx, chartgen.config2(seed), check_profiles=8)
+
+
+@pytest.mark.parametrize("rho", [0.5, 2.0])
+def test_config3_full_size_parity(orc, ctx, rho):
+    cs = chartgen.config3(0, rho=rho)
+    _compare_pack(orc, ctx, cs, check_profiles=16)
+    import oracle
+    from paper_2602_07782_b200 import spec_of
+    _, pl, _ = ctx.pack(cs.xy, cs.start, spec_of(cs))
+    assert oracle.validate(cs, pl) == {"overlap": 0, "gutter": 0, "oob": 0}
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 17, 64])
+def test_quality_knob_parity(orc, ctx, k):
+    _compare_pack(orc, ctx, chartgen.small_case(11, n=60, family="uv"), check_profiles=4,
+                  local_aabb_count=k)
+
+
+@pytest.mark.parametrize("kw", [dict(gutter=0), dict(gutter=3), dict(scale_count=1),
+                                dict(scale_count=17), dict(scale_count=256),
+                                dict(flags=1), dict(flags=2), dict(flags=4)],
+                         ids=lambda d: "-".join(f"{a}{b}" for a, b in d.items()))
+def test_spec_variants_parity(orc, ctx, kw):
+    _compare_pack(orc, ctx, chartgen.small_case(5, n=50, family="mixed", rho=0.8),
+                  check_profiles=3, **kw)
+
+
+def test_unsnapped_input_with_resolution(orc, ctx):
+    """UV input in [0, 1] times a texture resolution: exercises D2 round-half-even."""
+    cs = chartgen.small_case(2, n=40, family="uv", side=256)
+    rng = np.random.default_rng(0)
+    xy = (cs.xy / 256.0 + rng.uniform(-1e-4, 1e-4, cs.xy.shape)).astype(np.float32)
+    cs2 = chartgen.ChartSet("uv01", xy, cs.start, 256, 256)
+    _compare_pack(orc, ctx, cs2, res=(256.0, 256.0), check_profiles=3)
+
+
+def test_lock1_both_modes(orc, ctx):
+    A = [(0, 0), (20, 0), (20, 150), (0, 150)]
+    c0 = [(0, 0), (10, 0), (10, 45), (40, 45), (40, 47), (10, 47), (10, 100), (0, 100)]
+    c1 = [(0, 0), (10, 0), (10, 35), (0, 35)]
+    c2 = [(0, 0), (10, 0), (10, 30), (0, 30)]
+    cs = chartgen.from_polygons([A, c0, c1, c2], 40, 256, gutter=0)
+    _compare_pack(orc, ctx, cs, flags=4)
+    _compare_pack(orc, ctx, cs, flags=0)
+
+
+def test_single_and_no_fit(orc, ctx):
+    from paper_2602_07782_b200 import NO_FIT, spec_of
+    cs = chartgen.from_polygons([[(0, 0), (100, 0), (100, 100), (0, 100)]], 64, 64)
+    _compare_pack(orc, ctx, cs)
+    cs = chartgen.from_polygons([[(0, 0), (10000, 0), (10000, 1), (0, 1)]], 64, 64)
+    st, _, info = ctx.pack(cs.xy, cs.start, spec_of(cs))
+    assert st == NO_FIT and info.scale_index == 0
+
+
+def test_invalid_chart_reported(ctx):
+    from paper_2602_07782_b200 import EINVAL, spec_of
+    cs = chartgen.from_polygons([[(0, 0), (1, 0), (1, 1)], [(0, 0), (5, 0), (10, 0)],
+                                 [(0, 0), (2, 0), (2, 2)]], 64, 64)
+    st, _, info = ctx.pack(cs.xy, cs.start, spec_of(cs), raise_on_error=False)
+    assert st == EINVAL and info.bad_chart == 1
+    bad = cs.xy.copy()
+    bad[13] = np.nan
+    st, _, info = ctx.pack(bad, cs.start, spec_of(cs), raise_on_error=False)
+    assert st == EINVAL and info.bad_chart == 2
+
+
+def test_device_inputs_match_host(ctx):
+    import torch
+    from paper_2602_07782_b200 import PLACEMENT_DTYPE, spec_of
+    cs = chartgen.config2(1)
+    st_h, pl_h, info_h = ctx.pack(cs.xy, cs.start, spec_of(cs))
+    xy = torch.from_numpy(cs.xy).cuda()
+    start = torch.from_numpy(cs.start).cuda()
+    st_d, out_d, info_d = ctx.pack(xy, start, spec_of(cs))
+    torch.cuda.synchronize()
+    pl_d = out_d.cpu().numpy().view(PLACEMENT_DTYPE)
+    assert st_h == st_d and info_h.scale_index == info_d.scale_index
+    assert pl_h.tobytes() == pl_d.tobytes()
+
+
+def test_determinism_and_capacity_growth():
+    from paper_2602_07782_b200 import Context, spec_of
+    cs = chartgen.config3(1, rho=2.0)
+    small = Context(0, max_charts=cs.n_charts, max_vertices=cs.n_vertices, max_atlas_side=4096)
+    outs = [small.pack(cs.xy, cs.start, spec_of(cs))[1].tobytes() for _ in range(3)]
+    assert outs[0] == outs[1] == outs[2]
+    small.close()
