@@ -88,6 +88,9 @@ typedef struct {
   float stage_ms[8];              /* per-stage device time if TABI_TIMING=1, else 0:
                                      [0] H2D [1] proxies [2] sort [3] profiles
                                      [4] offsets+locks [5] fold&push [6] select [7] D2H */
+  int64_t work_pack;              /* fold&push: frontline column visits, all candidates
+                                     (push + score per evaluated configuration, + commit) */
+  int64_t work_profile;           /* footprint entries evaluated, sum over m, s of Wd + Hd */
 } tabi_info;
 
 /* Create a context on `cuda_device`.  max_charts / max_vertices bound every

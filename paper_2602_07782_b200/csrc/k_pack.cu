@@ -40,6 +40,7 @@ struct Smem {
   int32_t changed, npairs, pair_overflow;
   int32_t sel_cfg;
   unsigned long long knee_key;
+  unsigned long long work;
 };
 
 __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, int32_t& eb,
@@ -101,10 +102,17 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, -1};
     return;
   }
+  {  // work accounting: footprint entries K3 produced for this candidate
+    unsigned long long pe = 0;
+    for (int s = tid; s < n; s += kNT) pe += (unsigned long long)(wd[s] + hd[s]);
+    for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
+    if (lane == 0) atomicAdd(&st->work_prof, pe);
+  }
   for (int x = tid; x < Wp; x += kNT) F[x] = 0;  // frontline starts at the top
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
+    S.work = 0ull;
   }
   __syncthreads();
 
@@ -274,7 +282,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         v = max(v, F[X + i] - lo16(cp[ii]));
       }
       v = warp_max(v);
-      if (lane == 0) __stcg(&Yc[(int64_t)cfg * n + s], v);
+      if (lane == 0) {
+        __stcg(&Yc[(int64_t)cfg * n + s], v);
+        atomicAdd(&S.work, (unsigned long long)W_s);
+      }
     }
     __syncthreads();
     // ---- Alg. 1 CorrectYOffsets over adjacent + non-adjacent pairs ---------
@@ -327,7 +338,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         v = max(v, y + hi16(cp[ii]));
       }
       v = warp_max(v);
-      if (lane == 0) atomicMax(&S.newmax[cfg], v);
+      if (lane == 0) {
+        atomicMax(&S.newmax[cfg], v);
+        atomicAdd(&S.work, (unsigned long long)W_s);
+      }
     }
     __syncthreads();
     // ---- hierarchical selection -----------------------------------
@@ -367,6 +381,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         Xo[s] = X;
         Yo[s] = y;
         mir[s] = (uint8_t)dir;
+        atomicAdd(&S.work, (unsigned long long)W_s);
       }
     }
     // ---- FindKnee after an atlas-fold row -----------
@@ -403,6 +418,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   }
   if (tid == 0) {
     cands[m - 1] = Cand{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, -1};
+    atomicAdd(&st->work_pack, S.work);
   }
 }
 

@@ -369,6 +369,8 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     info->knee_rows = c.knee_rows;
     info->prefix_rows = c.prefix_rows;
     info->gpu_launches = launches;
+    info->work_pack = (int64_t)ctx->h_status->work_pack;
+    info->work_profile = (int64_t)ctx->h_status->work_prof;
   }
   return TABI_OK;
 }

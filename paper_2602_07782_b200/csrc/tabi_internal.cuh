@@ -178,6 +178,8 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t winner;     // winning m (0 = none)
   int32_t cols_total, rows_total;
   int32_t pad[3];
+  unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
+  unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
 };
 
 // Per-candidate result record (mirrors tabi_cand_dbg).

@@ -41,7 +41,8 @@ class Info(C.Structure):
     _fields_ = [("scale_index", C.c_int32), ("reserved0", C.c_int32), ("l2_stretch", C.c_double),
                 ("rows", C.c_int32), ("knees_found", C.c_int32), ("knee_rows", C.c_int32),
                 ("prefix_rows", C.c_int32), ("bad_chart", C.c_int32), ("gpu_launches", C.c_int32),
-                ("stage_ms", C.c_float * 8)]
+                ("stage_ms", C.c_float * 8), ("work_pack", C.c_int64),
+                ("work_profile", C.c_int64)]
 
 
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),

@@ -168,8 +168,10 @@ def test_invalid_chart_reported(ctx):
                                  [(0, 0), (2, 0), (2, 2)]], 64, 64)
     st, _, info = ctx.pack(cs.xy, cs.start, spec_of(cs), raise_on_error=False)
     assert st == EINVAL and info.bad_chart == 1
+    cs = chartgen.from_polygons([[(0, 0), (1, 0), (1, 1)], [(0, 0), (5, 0), (10, 3)],
+                                 [(0, 0), (2, 0), (2, 2)]], 64, 64)
     bad = cs.xy.copy()
-    bad[13] = np.nan
+    bad[13] = np.nan  # y of chart 2's first vertex
     st, _, info = ctx.pack(bad, cs.start, spec_of(cs), raise_on_error=False)
     assert st == EINVAL and info.bad_chart == 2
 
