@@ -4,16 +4,25 @@
 //
 // Per candidate the CTA runs Alg. 4 row by row with the frontline
 // F (one int32 per dilated atlas column) resident in shared memory:
-//   Alg. 2 knee refinement (block arg-max/min over F)            P:540-562
+//   Alg. 2 knee refinement (block arg-max/min over F)              P:540-562
 //   Alg. 3 fold of both HC settings as two block-wide exclusive
-//   scans + first-overflow min-reductions                          P:565-592
-//   non-adjacent lock pairs of the row (D15)                        P:462-477
-//   push: warp per (config, chart), max over covered columns of
-//   F - TopEdge (reads the packed footprints, coalesced)
-//   Alg. 1 fixpoint over the lock pairs                             P:496-521
-//   score: max over covered columns of Y + BottomEdge, per config
+//   scans + first-overflow min-reductions                           P:565-592
+//   non-adjacent lock pairs of the row (D15)                         P:462-477
+//   push: max over covered columns of F - TopEdge
+//   Alg. 1 fixpoint over the lock pairs                              P:496-521
+//   score: max over covered columns of Y + BottomEdge
 //   hierarchical selection, commit (shared atomicMax into F),
-//   FindKnee (block max of the height drop)                         P:282-304
+//   FindKnee (block max of the height drop)                          P:282-304
+//
+// Data movement: a row is processed in windows of up to kRW charts.  Per
+// window the charts' scalars (fold positions, widths, footprint offsets) go to
+// shared memory and their column footprints -- contiguous in HBM because the
+// slots follow the sorted order -- are staged with ONE TMA bulk copy
+// (cp.async.bulk + mbarrier) into shared memory.  Push, score and commit are
+// then flattened over the window's (chart, column) pairs: each thread walks a
+// contiguous run of columns, so all 512 threads work regardless of chart
+// sizes and no warp waits on per-chart global-load chains.
+//
 // Selection is decided before pushing where the paper allows it: the
 // horizontal-compaction choice depends only on the fold's row end (P:304
 // "enable horizontal compacting if it allows more charts to fit"), so each
@@ -26,6 +35,8 @@ namespace {
 
 constexpr int kNT = 512;
 constexpr int kNW = kNT / 32;
+constexpr int kRW = 2048;          // charts per row window
+constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for static Smem
 
 struct Smem {
   int32_t scan[2][kNW + 1];
@@ -39,9 +50,41 @@ struct Smem {
   int32_t newmax[4];
   int32_t changed, npairs, pair_overflow;
   int32_t sel_cfg;
+  int32_t win_s0, win_e, pglobal;
   unsigned long long knee_key;
   unsigned long long work;
+  alignas(8) uint64_t mbar;
 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+// 1-D TMA: global -> shared, completion counted in bytes on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
 
 __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, int32_t& eb,
                                             int32_t& ta, int32_t& tb, Smem& S) {
@@ -63,6 +106,45 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
   __syncthreads();
 }
 
+struct Win {                 // shared-memory window of one row
+  int32_t* rx0;              // fold position without HC (= prefix of widths)
+  int32_t* rx1;              // fold position with HC
+  int32_t* rwd;              // dilated width
+  int32_t* rco;              // footprint offset in the staged buffer (or in HBM)
+  int32_t* rY;               // [4][kRW] vertical offsets per configuration
+  uint32_t* prof;            // staged column footprints
+  int32_t prof_cap;
+};
+
+// Walk the flattened (chart, column) pairs [t, tend) of the window; body(i, j)
+// gets the window chart index i and column j; seg(i, first) is called when a
+// run enters chart i (first = the run starts at column 0), fin(i) when it leaves.
+template <class Enter, class Body, class Leave>
+__device__ __forceinline__ void walk(const Win& w, int nwin, Enter enter, Body body, Leave leave) {
+  const int32_t base0 = w.rx0[0];
+  const int32_t T = w.rx0[nwin - 1] - base0 + w.rwd[nwin - 1];
+  const int32_t C = (T + kNT - 1) / kNT;
+  int32_t t = threadIdx.x * C;
+  const int32_t tend = min(T, t + C);
+  if (t >= tend) return;
+  int lo = 0, hi = nwin - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (w.rx0[mid] - base0 <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  int i = lo;
+  while (t < tend) {
+    const int32_t j0 = t - (w.rx0[i] - base0);
+    const int32_t j1 = min(w.rwd[i], j0 + (tend - t));
+    enter(i, j0);
+    for (int32_t j = j0; j < j1; j++) body(i, j);
+    leave(i);
+    t += j1 - j0;
+    i++;
+  }
+}
+
 __global__ void __launch_bounds__(kNT, 1)
 pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
             const uint32_t* __restrict__ dcol, const uint32_t* __restrict__ drow,
@@ -70,8 +152,8 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
             const int32_t* __restrict__ off_all, const uint8_t* __restrict__ lock_all,
             const int32_t* __restrict__ hsorted, const int32_t* __restrict__ cand_bad,
             int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
-            Cand* cands, Status* st) {
-  extern __shared__ int32_t F[];
+            Cand* cands, Status* st, int32_t prof_cap) {
+  extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Smem S;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int m = blockIdx.x + 1;
@@ -97,6 +179,19 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   const bool adj_only = (pp.flags & TABI_F_ADJACENT_LOCKS_ONLY) != 0;
   const bool no_hc = (pp.flags & TABI_F_NO_HC) != 0;
   const bool no_bal = (pp.flags & TABI_F_NO_BALANCE) != 0;
+  const int32_t cols_total = st->cols_total;
+
+  // dynamic shared memory: F | window scalars | staged footprints
+  int32_t* F = (int32_t*)dsm;
+  const int32_t f_words = (Wp + 3) & ~3;
+  Win W;
+  W.rx0 = F + f_words;
+  W.rx1 = W.rx0 + kRW;
+  W.rwd = W.rx1 + kRW;
+  W.rco = W.rwd + kRW;
+  W.rY = W.rco + kRW;
+  W.prof = (uint32_t*)(W.rY + 4 * kRW);
+  W.prof_cap = prof_cap;
 
   if (cand_bad[m - 1]) {  // some chart exceeds the dilated atlas at this scale
     if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, -1};
@@ -113,8 +208,36 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
+    mbar_init(&S.mbar);
   }
   __syncthreads();
+  uint32_t phase = 0;
+  unsigned long long wk = 0;  // frontline column visits by this thread
+
+  // Stage window [ws0, we) of the current row (no-op if already staged).
+  auto stage = [&](int ws0, int we) {
+    if (S.win_s0 == ws0 && S.win_e == we) return;
+    const int nwin = we - ws0;
+    const int32_t c0 = colofs[ws0];
+    const int32_t c1 = we < n ? colofs[we] : cols_total;
+    const int32_t a0 = c0 & ~3, a1 = (c1 + 3) & ~3;
+    const bool pg = (a1 - a0) > W.prof_cap;
+    __syncthreads();  // previous readers of the window buffers are done
+    for (int k = tid; k < nwin; k += kNT) {
+      const int s = ws0 + k;
+      W.rx0[k] = xs0[s];
+      W.rx1[k] = xs1[s];
+      W.rwd[k] = wd[s];
+      W.rco[k] = colofs[s] - (pg ? 0 : a0);
+    }
+    if (!pg && tid == 0) bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
+    if (tid == 0) { S.win_s0 = ws0; S.win_e = we; S.pglobal = pg; }
+    if (!pg) {
+      mbar_wait(&S.mbar, phase);
+      phase ^= 1u;
+    }
+    __syncthreads();
+  };
 
   while (true) {
     const int32_t rs = S.row_start;
@@ -150,7 +273,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       __syncthreads();
     }
     const int32_t kv = S.knee_valid;
-    const int32_t ka = kv ? (S.knee_ltr ? S.knee_right : 0) : 0;   // knee fold region [ka, kb)
+    const int32_t ka = kv ? (S.knee_ltr ? S.knee_right : 0) : 0;  // knee fold region [ka, kb)
     const int32_t kb = kv ? (S.knee_ltr ? Wp : S.knee_left) : 0;
     if (kv) {
       int32_t mx = INT32_MIN;
@@ -159,8 +282,8 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       if (lane == 0) atomicMax(&S.conc_max, mx);
     }
     // ---- Alg. 3 FoldRow for both HC settings and both folds --------------
-    if (tid < 4) { S.endv[tid] = INT32_MIN; }
-    if (tid == 0) S.done = 0;
+    if (tid < 4) S.endv[tid] = INT32_MIN;
+    if (tid == 0) { S.done = 0; S.win_s0 = -1; S.win_e = -1; }
     __syncthreads();
     {
       int32_t carry0 = 0, carry1 = 0;
@@ -216,7 +339,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     const int32_t knee_ok = S.knee_ok;
     const int32_t hc0 = S.hcsel[0], hc1 = S.hcsel[1];
     const int32_t endA = S.end_cfg[0], endK = S.end_cfg[2];
-    const int32_t nA = endA - rs + 1, nK = knee_ok ? endK - rs + 1 : 0;
+    const int ncfg = knee_ok ? 4 : 2;
     // ---- D15: non-adjacent lock pairs of the row (HC folds only) ----------
     const int32_t R = max(hc0 ? endA : -1, (knee_ok && hc1) ? endK : -1);
     if (!adj_only && R > rs) {
@@ -232,14 +355,12 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         block_scan2(cnt, 0, ex, dummy, tot, tot2, S);
         if (a <= R && cnt > 0) {
           int32_t p = carry + ex;
-          const int32_t xa = xs1[a];
           for (int b = a + 2; b < a + 2 + cnt; b++, p++) {
             if (p < pair_cap) {
               pa[p] = a;
               pb[p] = b;
             }
           }
-          (void)xa;
         }
         carry += tot;
       }
@@ -252,7 +373,11 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         }
       }
       __syncthreads();
-      if (S.pair_overflow) { if (tid == 0) S.fail = 1; __syncthreads(); break; }
+      if (S.pair_overflow) {
+        if (tid == 0) S.fail = 1;
+        __syncthreads();
+        break;
+      }
       const int32_t np = S.npairs;
       for (int p = wid; p < np; p += kNW) {
         const int a = pa[p], b = pb[p];
@@ -263,34 +388,57 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       __syncthreads();
     }
     const int32_t np = S.npairs;
-    // ---- push (P:615-618): Y = max over covered columns of F - TopEdge ----
-    const int32_t total = 2 * nA + 2 * nK;
-    for (int it = wid; it < total; it += kNW) {
-      int cfg, s;
-      if (it < 2 * nA) { cfg = it / nA; s = rs + it % nA; }
-      else { const int t = it - 2 * nA; cfg = 2 + t / nK; s = rs + t % nK; }
+
+    // per-configuration geometry of chart (window index i, sorted s): X
+    auto cfgX = [&](int cfg, int i) -> int32_t {
       const int f = cfg >> 1, dir = cfg & 1;
       const int hc = f ? hc1 : hc0;
-      const int32_t a_f = f ? ka : 0, b_f = f ? kb : Wp;
-      const int32_t W_s = wd[s];
-      const int32_t xl = hc ? xs1[s] : xs0[s];
-      const int32_t X = dir ? b_f - xl - W_s : a_f + xl;
-      const uint32_t* cp = col + colofs[s];
-      int32_t v = INT32_MIN;
-      for (int i = lane; i < W_s; i += 32) {
-        const int ii = dir ? W_s - 1 - i : i;
-        v = max(v, F[X + i] - lo16(cp[ii]));
+      const int32_t xl = hc ? W.rx1[i] : W.rx0[i];
+      const int32_t Wd = W.rwd[i];
+      return dir ? (f ? kb : Wp) - xl - Wd : (f ? ka : 0) + xl;
+    };
+
+    // ---- push (P:615-618): Y = max over covered columns of F - TopEdge ----
+    for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
+      const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
+      stage(ws0, we);
+      for (int k = tid; k < 4 * nwin; k += kNT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
+      __syncthreads();
+      const uint32_t* pr = S.pglobal ? col : W.prof;
+      int32_t X[4], mx[4];
+      int nact = 0;
+      walk(
+          W, nwin,
+          [&](int i, int32_t) {
+            nact = (knee_ok && ws0 + i <= endK) ? 4 : 2;
+            for (int q = 0; q < 4; q++) { mx[q] = INT32_MIN; X[q] = q < nact ? cfgX(q, i) : 0; }
+          },
+          [&](int i, int32_t j) {
+            const int32_t top = lo16(pr[W.rco[i] + j]);
+            const int32_t Wd = W.rwd[i];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              if (q < nact) {
+                const int32_t pos = (q & 1) ? X[q] + Wd - 1 - j : X[q] + j;
+                mx[q] = max(mx[q], F[pos] - top);
+              }
+            }
+            wk += nact;
+          },
+          [&](int i) {
+            for (int q = 0; q < nact; q++) atomicMax(&W.rY[q * kRW + i], mx[q]);
+          });
+      __syncthreads();
+      for (int k = tid; k < nwin; k += kNT) {
+        const int s = ws0 + k;
+        const int na = (knee_ok && s <= endK) ? 4 : 2;
+        for (int q = 0; q < na; q++) __stcg(&Yc[(int64_t)q * n + s], W.rY[q * kRW + k]);
       }
-      v = warp_max(v);
-      if (lane == 0) {
-        __stcg(&Yc[(int64_t)cfg * n + s], v);
-        atomicAdd(&S.work, (unsigned long long)W_s);
-      }
+      __syncthreads();
     }
-    __syncthreads();
     // ---- Alg. 1 CorrectYOffsets over adjacent + non-adjacent pairs ---------
     {
-      const int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // hc1 configs [c0, c1)
+      const int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // HC configs [c0, c1)
       if (c1 > c0) {
         const int32_t per = (endA - rs) + (adj_only ? 0 : np);  // adjacent pairs + list
         while (true) {
@@ -302,12 +450,14 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
             const int32_t endc = S.end_cfg[cfg];
             int a, b, bits;
             if (q < endA - rs) {
-              a = rs + q; b = a + 1;
+              a = rs + q;
+              b = a + 1;
               if (b > endc) continue;
               bits = lk[a];
             } else {
               const int p = q - (endA - rs);
-              a = pa[p]; b = pb[p];
+              a = pa[p];
+              b = pb[p];
               if (b > endc) continue;
               bits = plk[p];
             }
@@ -324,31 +474,47 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       }
     }
     // ---- score: max over covered columns of Y + BottomEdge ----
-    for (int it = wid; it < total; it += kNW) {
-      int cfg, s;
-      if (it < 2 * nA) { cfg = it / nA; s = rs + it % nA; }
-      else { const int t = it - 2 * nA; cfg = 2 + t / nK; s = rs + t % nK; }
-      const int dir = cfg & 1;
-      const int32_t W_s = wd[s];
-      const uint32_t* cp = col + colofs[s];
-      const int32_t y = __ldcg(&Yc[(int64_t)cfg * n + s]);
-      int32_t v = INT32_MIN;
-      for (int i = lane; i < W_s; i += 32) {
-        const int ii = dir ? W_s - 1 - i : i;
-        v = max(v, y + hi16(cp[ii]));
+    {
+      int32_t nm[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
+      for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
+        const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
+        stage(ws0, we);
+        for (int k = tid; k < nwin; k += kNT) {
+          const int s = ws0 + k;
+          const int na = (knee_ok && s <= endK) ? 4 : 2;
+          for (int q = 0; q < na; q++) W.rY[q * kRW + k] = __ldcg(&Yc[(int64_t)q * n + s]);
+        }
+        __syncthreads();
+        const uint32_t* pr = S.pglobal ? col : W.prof;
+        int32_t Yv[4];
+        int nact = 0;
+        walk(
+            W, nwin,
+            [&](int i, int32_t) {
+              nact = (knee_ok && ws0 + i <= endK) ? 4 : 2;
+              for (int q = 0; q < 4; q++) Yv[q] = q < nact ? W.rY[q * kRW + i] : 0;
+            },
+            [&](int i, int32_t j) {
+              const int32_t bot = hi16(pr[W.rco[i] + j]);
+#pragma unroll
+              for (int q = 0; q < 4; q++)
+                if (q < nact) nm[q] = max(nm[q], Yv[q] + bot);
+              wk += nact;
+            },
+            [&](int) {});
+        __syncthreads();
       }
-      v = warp_max(v);
-      if (lane == 0) {
-        atomicMax(&S.newmax[cfg], v);
-        atomicAdd(&S.work, (unsigned long long)W_s);
+      for (int q = 0; q < ncfg; q++) {
+        const int32_t v = warp_max(nm[q]);
+        if (lane == 0) atomicMax(&S.newmax[q], v);
       }
     }
     __syncthreads();
     // ---- hierarchical selection -----------------------------------
     if (tid == 0) {
       const int32_t sw0 = max(S.fmax, S.newmax[0]), sw1 = max(S.fmax, S.newmax[1]);
-      int d0 = sw1 < sw0 ? 1 : 0;                 // ties -> left to right
-      if (no_bal) d0 = S.rows & 1;                // static alternation (ablation)
+      int d0 = sw1 < sw0 ? 1 : 0;   // ties -> left to right
+      if (no_bal) d0 = S.rows & 1;  // static alternation (ablation)
       int cfg = d0;
       if (knee_ok) {
         const int32_t sk0 = max(S.conc_max, S.newmax[2]), sk1 = max(S.conc_max, S.newmax[3]);
@@ -364,25 +530,35 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     // ---- commit: F <- max(F, Y + BottomEdge); record placements ------------
     const int cfg = S.sel_cfg;
     const int f = cfg >> 1, dir = cfg & 1;
-    const int hc = f ? hc1 : hc0;
-    const int32_t a_f = f ? ka : 0, b_f = f ? kb : Wp;
     const int32_t endS = S.end_cfg[cfg];
-    for (int s = rs + wid; s <= endS; s += kNW) {
-      const int32_t W_s = wd[s];
-      const int32_t xl = hc ? xs1[s] : xs0[s];
-      const int32_t X = dir ? b_f - xl - W_s : a_f + xl;
-      const uint32_t* cp = col + colofs[s];
-      const int32_t y = __ldcg(&Yc[(int64_t)cfg * n + s]);
-      for (int i = lane; i < W_s; i += 32) {
-        const int ii = dir ? W_s - 1 - i : i;
-        atomicMax(&F[X + i], y + hi16(cp[ii]));
-      }
-      if (lane == 0) {
-        Xo[s] = X;
-        Yo[s] = y;
-        mir[s] = (uint8_t)dir;
-        atomicAdd(&S.work, (unsigned long long)W_s);
-      }
+    for (int ws0 = rs; ws0 <= endS; ws0 += kRW) {
+      const int we = min(endA + 1, ws0 + kRW), nwin = min(we, endS + 1) - ws0;
+      stage(ws0, we);
+      for (int k = tid; k < nwin; k += kNT) W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
+      __syncthreads();
+      const uint32_t* pr = S.pglobal ? col : W.prof;
+      int32_t Xc = 0, Yv = 0, Wd = 0;
+      walk(
+          W, nwin,
+          [&](int i, int32_t j0) {
+            Xc = cfgX(cfg, i);
+            Yv = W.rY[i];
+            Wd = W.rwd[i];
+            if (j0 == 0) {
+              const int s = ws0 + i;
+              Xo[s] = Xc;
+              Yo[s] = Yv;
+              mir[s] = (uint8_t)dir;
+            }
+          },
+          [&](int i, int32_t j) {
+            const int32_t bot = hi16(pr[W.rco[i] + j]);
+            const int32_t pos = dir ? Xc + Wd - 1 - j : Xc + j;
+            atomicMax(&F[pos], Yv + bot);
+            wk += 1;
+          },
+          [&](int) {});
+      __syncthreads();
     }
     // ---- FindKnee after an atlas-fold row -----------
     if (f == 0 && !no_bal) {
@@ -416,9 +592,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     }
     __syncthreads();
   }
+  for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
+  if (lane == 0) atomicAdd(&st->work_pack, wk);
   if (tid == 0) {
     cands[m - 1] = Cand{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, -1};
-    atomicAdd(&st->work_pack, S.work);
   }
 }
 
@@ -469,15 +646,17 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
                  const int32_t* off, const uint8_t* lockbits, const int32_t* hsorted,
                  const int32_t* cand_bad, int32_t* scratch, int64_t pair_cap, int32_t* X,
                  int32_t* Y, uint8_t* mir, Cand* cands, Status* st, cudaStream_t s) {
-  const size_t smem = sizeof(int32_t) * (size_t)pp.Wp;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(int32_t) * (TABI_MAX_ATLAS_SIDE + 2 * 64 + 8)));
+    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     attr = true;
   }
-  pack_kernel<<<pp.M, kNT, smem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
-                                      hsorted, cand_bad, scratch, pair_cap, X, Y, mir, cands, st);
+  const int f_words = (pp.Wp + 3) & ~3;
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 8 * (size_t)kRW);
+  const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
+  pack_kernel<<<pp.M, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
+                                             hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
+                                             cands, st, prof_cap);
 }
 
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,

@@ -10,6 +10,14 @@
 // store packed uint16 pairs coalesced; the dilation is an in-place window
 // min/max over the warp's slot.
 //
+// OBB bound per column: the top boundary y_top(x) = max of a decreasing and an
+// increasing line, minimised over the column's strip.  Its crossing point and
+// crossing value are per-(chart, candidate) constants, so per column exactly
+// one line matters (the increasing one right of the crossing, the decreasing
+// one left of it): one exact division per bound per column, done by a
+// double-precision estimate plus integer correction (fdiv_fast*) instead of an
+// emulated int128 divide.
+//
 // K3b computes, per candidate and adjacent sorted pair, the horizontal
 // compaction advance (a max-reduction of profile gaps over shared
 // rows, D14) and the CannotMoveAbove flags (D15) with warp scans.
@@ -19,53 +27,6 @@ namespace tabi {
 namespace {
 
 constexpr int kWarps = 8;
-
-// ---- D11 OBB bounds on the unscaled strip [P0/num, P1/num] -----------------
-// top: y_top(x) = max((Umin - xC)/S, (Vmin + xS)/C), convex, min at
-// x* = (C Umin - S Vmin)/(C^2+S^2) with value (S Umin + C Vmin)/(C^2+S^2).
-__device__ int64_t obb_top(i128 C, i128 S, i128 umin, i128 vmin, i128 num, i128 SC, i128 P0,
-                           i128 P1) {
-  const i128 N2 = C * C + S * S;
-  const i128 xs = num * (C * umin - S * vmin);
-  if (P0 * N2 <= xs && xs <= P1 * N2) return (int64_t)floordiv128(num * (S * umin + C * vmin), N2 * SC);
-  const i128 P = xs < P0 * N2 ? P0 : P1;
-  const i128 y1 = floordiv128(umin * num - P * C, S * SC);
-  const i128 y2 = floordiv128(vmin * num + P * S, C * SC);
-  return (int64_t)(y1 > y2 ? y1 : y2);
-}
-// bottom: y_bot(x) = min((Umax - xC)/S, (Vmax + xS)/C), concave.
-__device__ int64_t obb_bot(i128 C, i128 S, i128 umax, i128 vmax, i128 num, i128 SC, i128 P0,
-                           i128 P1) {
-  const i128 N2 = C * C + S * S;
-  const i128 xs = num * (C * umax - S * vmax);
-  if (P0 * N2 <= xs && xs <= P1 * N2) return (int64_t)ceildiv128(num * (S * umax + C * vmax), N2 * SC);
-  const i128 P = xs < P0 * N2 ? P0 : P1;
-  const i128 y1 = ceildiv128(umax * num - P * C, S * SC);
-  const i128 y2 = ceildiv128(vmax * num + P * S, C * SC);
-  return (int64_t)(y1 < y2 ? y1 : y2);
-}
-// left: x_left(y) = max((Umin - yS)/C, (yC - Vmax)/S), convex.
-__device__ int64_t obb_left(i128 C, i128 S, i128 umin, i128 vmax, i128 num, i128 SC, i128 Q0,
-                            i128 Q1) {
-  const i128 N2 = C * C + S * S;
-  const i128 ys = num * (S * umin + C * vmax);
-  if (Q0 * N2 <= ys && ys <= Q1 * N2) return (int64_t)floordiv128(num * (C * umin - S * vmax), N2 * SC);
-  const i128 Q = ys < Q0 * N2 ? Q0 : Q1;
-  const i128 x1 = floordiv128(umin * num - Q * S, C * SC);
-  const i128 x2 = floordiv128(Q * C - vmax * num, S * SC);
-  return (int64_t)(x1 > x2 ? x1 : x2);
-}
-// right: x_right(y) = min((Umax - yS)/C, (yC - Vmin)/S), concave.
-__device__ int64_t obb_right(i128 C, i128 S, i128 umax, i128 vmin, i128 num, i128 SC, i128 Q0,
-                             i128 Q1) {
-  const i128 N2 = C * C + S * S;
-  const i128 ys = num * (S * umax + C * vmin);
-  if (Q0 * N2 <= ys && ys <= Q1 * N2) return (int64_t)ceildiv128(num * (C * umax - S * vmin), N2 * SC);
-  const i128 Q = ys < Q0 * N2 ? Q0 : Q1;
-  const i128 x1 = ceildiv128(umax * num - Q * S, C * SC);
-  const i128 x2 = ceildiv128(Q * C - vmin * num, S * SC);
-  return (int64_t)(x1 < x2 ? x1 : x2);
-}
 
 // In-place Chebyshev dilation of a slot holding raw (lo, hi) pairs at
 // positions [2g, 2g + n0): out[i] = (min lo, max hi + 2g) over raw [i-2g, i].
@@ -102,7 +63,8 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   const int c = perm[s];
   const int64_t w = P.w[c], h = P.h[c], k = pp.k;
   const int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
-  const int64_t ws = ceildiv(w * num, SC), hs = ceildiv(h * num, SC);
+  const int64_t nw = num * w, nh = num * h;
+  const int64_t ws = cdiv_fast(nw, SC), hs = cdiv_fast(nh, SC);
   const int32_t Wd = (int32_t)(ws + 2 * pp.g), Hd = (int32_t)(hs + 2 * pp.g);
   if (lane == 0) {
     wd_all[(int64_t)(m - 1) * pp.n + s] = Wd;
@@ -114,15 +76,29 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   }
   const int32_t* sl = P.sl + (int64_t)c * 4 * k;
   const int j8 = P.obb_j[c];
-  const i128 C = kQC[j8], S = kQS[j8];
-  const i128 umin = P.obb[4 * (int64_t)c], umax = P.obb[4 * (int64_t)c + 1];
-  const i128 vmin = P.obb[4 * (int64_t)c + 2], vmax = P.obb[4 * (int64_t)c + 3];
   uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
   uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-  const int64_t nw = num * w, nh = num * h;
+  // per-(chart, candidate) OBB constants (D11)
+  const i128 C = kQC[j8], S = kQS[j8], N2 = C * C + S * S;
+  const i128 umin = P.obb[4 * (int64_t)c], umax = P.obb[4 * (int64_t)c + 1];
+  const i128 vmin = P.obb[4 * (int64_t)c + 2], vmax = P.obb[4 * (int64_t)c + 3];
+  const i128 N2SC = N2 * SC;
+  i128 xsT = 0, xsB = 0, ysL = 0, ysR = 0;
+  int64_t starT = 0, starB = 0, starL = 0, starR = 0;
+  if (j8 != 0) {
+    xsT = num * (C * umin - S * vmin);
+    starT = fdiv_fast128(num * (S * umin + C * vmin), N2SC);
+    xsB = num * (C * umax - S * vmax);
+    starB = cdiv_fast128(num * (S * umax + C * vmax), N2SC);
+    ysL = num * (S * umin + C * vmax);
+    starL = fdiv_fast128(num * (C * umin - S * vmax), N2SC);
+    ysR = num * (S * umax + C * vmin);
+    starR = cdiv_fast128(num * (C * umax - S * vmin), N2SC);
+  }
+  const i128 SSC = S * SC, CSC = C * SC;
   for (int64_t i = lane; i < ws; i += 32) {
     // local-AABB bound: slices whose scaled range openly overlaps [i, i+1]
-    int64_t jl = (i * SC * k) / nw, jh = ceildiv((i + 1) * SC * k, nw) - 1;
+    int64_t jl = fdiv_fast(i * SC * k, nw), jh = cdiv_fast((i + 1) * SC * k, nw) - 1;
     if (jl < 0) jl = 0;
     if (jh > k - 1) jh = k - 1;
     int64_t mt = INT64_MAX, mb = INT64_MIN;
@@ -132,17 +108,25 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
         mb = max(mb, (int64_t)sl[k + j]);
       }
     }
-    int64_t t = max((int64_t)0, floordiv(num * mt, SC));
-    int64_t b = min(hs, ceildiv(num * mb, SC));
+    int64_t t = max((int64_t)0, fdiv_fast(num * mt, SC));
+    int64_t b = min(hs, cdiv_fast(num * mb, SC));
     if (j8 != 0) {
       const i128 P0 = (i128)i * SC, P1 = (i128)min((i + 1) * SC, nw);
-      t = max(t, obb_top(C, S, umin, vmin, num, SC, P0, P1));
-      b = min(b, obb_bot(C, S, umax, vmax, num, SC, P0, P1));
+      const i128 P0N = P0 * N2, P1N = P1 * N2;
+      int64_t ot, ob;
+      if (P0N <= xsT && xsT <= P1N) ot = starT;
+      else if (xsT < P0N) ot = fdiv_fast128(vmin * num + P0 * S, CSC);  // increasing part, at P0
+      else ot = fdiv_fast128(umin * num - P1 * C, SSC);                 // decreasing part, at P1
+      if (P0N <= xsB && xsB <= P1N) ob = starB;
+      else if (xsB < P0N) ob = cdiv_fast128(umax * num - P0 * C, SSC);  // decreasing, at P0
+      else ob = cdiv_fast128(vmax * num + P1 * S, CSC);                 // increasing, at P1
+      t = max(t, ot);
+      b = min(b, ob);
     }
     col[i + 2 * pp.g] = (uint32_t)t | ((uint32_t)b << 16);
   }
   for (int64_t r = lane; r < hs; r += 32) {
-    int64_t jl = (r * SC * k) / nh, jh = ceildiv((r + 1) * SC * k, nh) - 1;
+    int64_t jl = fdiv_fast(r * SC * k, nh), jh = cdiv_fast((r + 1) * SC * k, nh) - 1;
     if (jl < 0) jl = 0;
     if (jh > k - 1) jh = k - 1;
     int64_t ml = INT64_MAX, mr = INT64_MIN;
@@ -152,12 +136,20 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
         mr = max(mr, (int64_t)sl[3 * k + j]);
       }
     }
-    int64_t l = max((int64_t)0, floordiv(num * ml, SC));
-    int64_t rr = min(ws, ceildiv(num * mr, SC));
+    int64_t l = max((int64_t)0, fdiv_fast(num * ml, SC));
+    int64_t rr = min(ws, cdiv_fast(num * mr, SC));
     if (j8 != 0) {
       const i128 Q0 = (i128)r * SC, Q1 = (i128)min((r + 1) * SC, nh);
-      l = max(l, obb_left(C, S, umin, vmax, num, SC, Q0, Q1));
-      rr = min(rr, obb_right(C, S, umax, vmin, num, SC, Q0, Q1));
+      const i128 Q0N = Q0 * N2, Q1N = Q1 * N2;
+      int64_t ol, orr;
+      if (Q0N <= ysL && ysL <= Q1N) ol = starL;
+      else if (ysL < Q0N) ol = fdiv_fast128(Q0 * C - vmax * num, SSC);   // increasing, at Q0
+      else ol = fdiv_fast128(umin * num - Q1 * S, CSC);                  // decreasing, at Q1
+      if (Q0N <= ysR && ysR <= Q1N) orr = starR;
+      else if (ysR < Q0N) orr = cdiv_fast128(umax * num - Q0 * S, CSC);  // decreasing, at Q0
+      else orr = cdiv_fast128(Q1 * C - vmin * num, SSC);                 // increasing, at Q1
+      l = max(l, ol);
+      rr = min(rr, orr);
     }
     row[r + 2 * pp.g] = (uint32_t)l | ((uint32_t)rr << 16);
   }

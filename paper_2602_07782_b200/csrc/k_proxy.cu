@@ -22,6 +22,8 @@ struct WarpSlices {
   int32_t hi[2][TABI_KMAX];  //           [0] x-slices bot, [1] y-slices right
   int32_t mlo[2][TABI_KMAX]; // merged
   int32_t mhi[2][TABI_KMAX];
+  int64_t fl[2][TABI_KMAX];  // floor(i * ext / k) for the other axis' slice edges
+  int64_t cl[2][TABI_KMAX];  // ceil((i + 1) * ext / k)
 };
 
 // D4: slice bounds along one axis.  A = coordinate that is sliced (x for
@@ -31,8 +33,8 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
                                   int32_t* lo, int32_t* hi, int lane) {
   for (int v = lane; v < nv; v += 32) {
     int64_t ka = (int64_t)k * A[v];
-    int64_t jh = ka / ext;                 // floor(k*a/ext), a >= 0
-    int64_t jl = ceildiv(ka, ext) - 1;     // ceil(k*a/ext) - 1
+    int64_t jh = fdiv_fast(ka, ext);                // floor(k*a/ext), a >= 0
+    int64_t jl = cdiv_fast(ka, ext) - 1;     // ceil(k*a/ext) - 1
     if (jl < 0) jl = 0;
     if (jh > k - 1) jh = k - 1;
     for (int64_t j = jl; j <= jh; j++) {
@@ -50,8 +52,8 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
       int64_t t = xa; xa = xb; xb = t;
       t = ya; ya = yb; yb = t;
     }
-    int64_t L0 = (int64_t)k * xa / ext + 1;      // first line strictly right of xa
-    int64_t L1 = ceildiv((int64_t)k * xb, ext) - 1;  // last line strictly left of xb
+    int64_t L0 = fdiv_fast((int64_t)k * xa, ext) + 1;      // first line strictly right of xa
+    int64_t L1 = cdiv_fast((int64_t)k * xb, ext) - 1;  // last line strictly left of xb
     if (L0 < 1) L0 = 1;
     if (L1 > k - 1) L1 = k - 1;
     for (int64_t L = L0; L <= L1; L++) {
@@ -59,8 +61,8 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
       if (!((int64_t)k * xa < line && line < (int64_t)k * xb)) continue;
       int64_t num = (line - (int64_t)k * xa) * (yb - ya);
       int64_t den = (int64_t)k * (xb - xa);
-      int32_t yf = (int32_t)(ya + floordiv(num, den));
-      int32_t yc = (int32_t)(ya + ceildiv(num, den));
+      int32_t yf = (int32_t)(ya + fdiv_fast(num, den));
+      int32_t yc = (int32_t)(ya + cdiv_fast(num, den));
       atomicMin(&lo[L - 1], yf);
       atomicMax(&hi[L - 1], yc);
       atomicMin(&lo[L], yf);
@@ -71,12 +73,19 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
 
 // D5 merge: x-slice j tightened by y-slices whose x-range meets strip j.
 __device__ void merge_slices(WarpSlices& S, int64_t w, int64_t h, int k, int lane) {
+  for (int i = lane; i < k; i += 32) {
+    S.fl[0][i] = fdiv_fast((int64_t)i * h, k);
+    S.cl[0][i] = cdiv_fast((int64_t)(i + 1) * h, k);
+    S.fl[1][i] = fdiv_fast((int64_t)i * w, k);
+    S.cl[1][i] = cdiv_fast((int64_t)(i + 1) * w, k);
+  }
+  __syncwarp();
   for (int j = lane; j < k; j += 32) {
     // x-slices
     int64_t mn = INT64_MAX, mx = INT64_MIN;
     for (int i = 0; i < k; i++) {
       if ((int64_t)k * S.lo[1][i] <= (int64_t)(j + 1) * w && (int64_t)k * S.hi[1][i] >= (int64_t)j * w) {
-        int64_t f = floordiv((int64_t)i * h, k), c = ceildiv((int64_t)(i + 1) * h, k);
+        const int64_t f = S.fl[0][i], c = S.cl[0][i];
         mn = f < mn ? f : mn;
         mx = c > mx ? c : mx;
       }
@@ -91,7 +100,7 @@ __device__ void merge_slices(WarpSlices& S, int64_t w, int64_t h, int k, int lan
     mx = INT64_MIN;
     for (int i = 0; i < k; i++) {
       if ((int64_t)k * S.lo[0][i] <= (int64_t)(j + 1) * h && (int64_t)k * S.hi[0][i] >= (int64_t)j * h) {
-        int64_t f = floordiv((int64_t)i * w, k), c = ceildiv((int64_t)(i + 1) * w, k);
+        const int64_t f = S.fl[1][i], c = S.cl[1][i];
         mn = f < mn ? f : mn;
         mx = c > mx ? c : mx;
       }

@@ -162,7 +162,8 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
   if (threadIdx.x == 0) {
     st->cols_total = carry_c;
     st->rows_total = carry_r;
-    if ((int64_t)carry_c > pp.col_cap || (int64_t)carry_r > pp.row_cap) st->capacity |= 1;
+    // +4: the TMA bulk copy of a row window rounds its end up to 16 bytes
+    if ((int64_t)carry_c + 4 > pp.col_cap || (int64_t)carry_r + 4 > pp.row_cap) st->capacity |= 1;
   }
 }
 

@@ -146,7 +146,7 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
       cudaMallocHost((void**)&ctx->h_out, sizeof(tabi_placement) * N) != cudaSuccess)
     return fail();
   // initial footprint slot capacity per candidate (grows on demand)
-  ctx->col_cap = (int64_t)N * 96 + 4 * (int64_t)max_atlas_side;
+  ctx->col_cap = ((int64_t)N * 96 + 4 * (int64_t)max_atlas_side) & ~(int64_t)3;  // 16-B aligned per candidate
   ctx->row_cap = ctx->col_cap;
   ctx->pair_cap = (int64_t)N * 2 + 1024;
   *out = ctx;
@@ -328,8 +328,8 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     // grow and retry from the slot layout (proxies and order are kept)
     bool cols = false, pairs = false;
     if (st.capacity & 1) {
-      ctx->col_cap = (int64_t)st.cols_total + (st.cols_total >> 2) + 1024;
-      ctx->row_cap = (int64_t)st.rows_total + (st.rows_total >> 2) + 1024;
+      ctx->col_cap = ((int64_t)st.cols_total + (st.cols_total >> 2) + 1024) & ~(int64_t)3;
+      ctx->row_cap = ((int64_t)st.rows_total + (st.rows_total >> 2) + 1024) & ~(int64_t)3;
       cols = true;
     }
     if (st.capacity & 2) {

@@ -40,6 +40,30 @@ __device__ __forceinline__ i128 ceildiv128(i128 a, i128 b) {
   return q;
 }
 
+// Exact floor/ceil division from a double-precision estimate plus integer
+// correction (no emulated 64/128-bit divide).  Exact for any operands: the
+// correction loops run until the remainder is in [0, b); with |a/b| < 2^50
+// the estimate is already within one unit so they run at most once or twice.
+__device__ __forceinline__ int64_t fdiv_fast(int64_t a, int64_t b) {
+  int64_t q = (int64_t)floor((double)a / (double)b);
+  int64_t r = a - q * b;
+  while (r < 0) { q--; r += b; }
+  while (r >= b) { q++; r -= b; }
+  return q;
+}
+__device__ __forceinline__ int64_t cdiv_fast(int64_t a, int64_t b) { return -fdiv_fast(-a, b); }
+__device__ __forceinline__ double i128_to_double(i128 a) {
+  return (double)(int64_t)(a >> 64) * 18446744073709551616.0 + (double)(uint64_t)a;
+}
+__device__ __forceinline__ int64_t fdiv_fast128(i128 a, i128 b) {
+  int64_t q = (int64_t)floor(i128_to_double(a) / i128_to_double(b));
+  i128 r = a - (i128)q * b;
+  while (r < 0) { q--; r += b; }
+  while (r >= b) { q++; r -= b; }
+  return q;
+}
+__device__ __forceinline__ int64_t cdiv_fast128(i128 a, i128 b) { return -fdiv_fast128(-a, b); }
+
 // ---- warp reductions (full warp) ------------------------------------------
 __device__ __forceinline__ int32_t warp_max(int32_t v) {
   return __reduce_max_sync(0xffffffffu, v);
