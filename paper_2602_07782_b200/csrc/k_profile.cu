@@ -10,13 +10,17 @@
 // store packed uint16 pairs coalesced; the dilation is an in-place window
 // min/max over the warp's slot.
 //
-// OBB bound per column: the top boundary y_top(x) = max of a decreasing and an
-// increasing line, minimised over the column's strip.  Its crossing point and
-// crossing value are per-(chart, candidate) constants, so per column exactly
-// one line matters (the increasing one right of the crossing, the decreasing
-// one left of it): one exact division per bound per column, done by a
-// double-precision estimate plus integer correction (fdiv_fast*) instead of an
-// emulated int128 divide.
+// Cost structure (what makes this kernel fast):
+//  * local-AABB bound: each slice's scaled floor/ceil and the column range it
+//    openly overlaps are computed once per (chart, candidate) by lanes j < k;
+//    a column then takes min/max over its 1-2 slices found by a per-lane
+//    pointer (columns of a lane increase monotonically) -- no division;
+//  * OBB bound: y_top(x) = max(decreasing, increasing line) is minimised over
+//    the column strip; the crossing point and value are per-(chart,
+//    candidate) constants, so per column exactly one line is evaluated (left
+//    of the crossing the decreasing one at the strip's right end, right of it
+//    the increasing one at the left end): one exact division, done as a
+//    multiply by a precomputed reciprocal plus an integer correction.
 //
 // K3b computes, per candidate and adjacent sorted pair, the horizontal
 // compaction advance (a max-reduction of profile gaps over shared
@@ -27,6 +31,13 @@ namespace tabi {
 namespace {
 
 constexpr int kWarps = 8;
+
+struct SliceTab {  // per-warp tables, one axis
+  int32_t lo[TABI_KMAX];    // first texel column/row the slice openly overlaps
+  int32_t hi[TABI_KMAX];    // last one
+  int32_t flo[TABI_KMAX];   // floor(num * low bound / SC)
+  int32_t chi[TABI_KMAX];   // ceil(num * high bound / SC)
+};
 
 // In-place Chebyshev dilation of a slot holding raw (lo, hi) pairs at
 // positions [2g, 2g + n0): out[i] = (min lo, max hi + 2g) over raw [i-2g, i].
@@ -49,19 +60,42 @@ __device__ void dilate_slot(uint32_t* slot, int32_t n0, int32_t g, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32)
+// Slice table of one axis: slice j spans [j*ext/k, (j+1)*ext/k] (units), i.e.
+// the scaled range [num*j*ext/(SC*k), num*(j+1)*ext/(SC*k)]; it openly
+// overlaps texel t iff num*j*ext < (t+1)*SC*k and num*(j+1)*ext > t*SC*k, i.e.
+// t in [floor(num*j*ext/(SC*k)), ceil(num*(j+1)*ext/(SC*k)) - 1].
+__device__ void build_tab(SliceTab& T, const int32_t* blo, const int32_t* bhi, int64_t ext,
+                          int64_t num, int64_t SC, int k, int lane) {
+  const int64_t SCk = SC * k, nx = num * ext;
+  for (int j = lane; j < k; j += 32) {
+    T.lo[j] = (int32_t)fdiv_fast(nx * j, SCk);
+    T.hi[j] = (int32_t)(cdiv_fast(nx * (j + 1), SCk) - 1);
+    T.flo[j] = (int32_t)fdiv_fast(num * blo[j], SC);
+    T.chi[j] = (int32_t)cdiv_fast(num * bhi[j], SC);
+  }
+  __syncwarp();
+}
+
+struct ObbLine {   // constants of one axis' OBB bounds at one scale
+  i128 cross_lo, cross_hi;   // num * crossing numerator (compare with P * N2)
+  int64_t star_lo, star_hi;  // bound values at the crossings (floor / ceil, scaled)
+};
+
+__global__ void __launch_bounds__(kWarps * 32, 2)
 profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
                const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
                uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all, int32_t* cand_bad,
                const Status* st) {
+  __shared__ SliceTab tabs[kWarps][2];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t item = (int64_t)blockIdx.x * kWarps + wib;
   if (item >= (int64_t)pp.n * pp.M) return;
   const int m = (int)(item / pp.n) + 1;
   const int s = (int)(item % pp.n);
   const int c = perm[s];
-  const int64_t w = P.w[c], h = P.h[c], k = pp.k;
+  const int64_t w = P.w[c], h = P.h[c];
+  const int k = pp.k;
   const int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
   const int64_t nw = num * w, nh = num * h;
   const int64_t ws = cdiv_fast(nw, SC), hs = cdiv_fast(nh, SC);
@@ -75,83 +109,86 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
     return;
   }
   const int32_t* sl = P.sl + (int64_t)c * 4 * k;
+  SliceTab& TX = tabs[wib][0];
+  SliceTab& TY = tabs[wib][1];
+  build_tab(TX, sl, sl + k, w, num, SC, k, lane);
+  build_tab(TY, sl + 2 * k, sl + 3 * k, h, num, SC, k, lane);
   const int j8 = P.obb_j[c];
   uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
   uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-  // per-(chart, candidate) OBB constants (D11)
-  const i128 C = kQC[j8], S = kQS[j8], N2 = C * C + S * S;
-  const i128 umin = P.obb[4 * (int64_t)c], umax = P.obb[4 * (int64_t)c + 1];
-  const i128 vmin = P.obb[4 * (int64_t)c + 2], vmax = P.obb[4 * (int64_t)c + 3];
-  const i128 N2SC = N2 * SC;
-  i128 xsT = 0, xsB = 0, ysL = 0, ysR = 0;
-  int64_t starT = 0, starB = 0, starL = 0, starR = 0;
+  // ---- OBB constants (D11): lines of the box in the (x, y) chart frame ----
+  const int64_t C = kQC[j8], S = kQS[j8], N2 = C * C + S * S;
+  const int64_t umin = P.obb[4 * (int64_t)c], umax = P.obb[4 * (int64_t)c + 1];
+  const int64_t vmin = P.obb[4 * (int64_t)c + 2], vmax = P.obb[4 * (int64_t)c + 3];
+  const i128 UMN = mul_wide(umin, num), UXN = mul_wide(umax, num);
+  const i128 VMN = mul_wide(vmin, num), VXN = mul_wide(vmax, num);
+  const int64_t DS = S * SC, DC = C * SC;          // divisors of the two lines
+  const double rDS = 1.0 / (double)DS, rDC = 1.0 / (double)DC;
+  ObbLine OX{}, OY{};
   if (j8 != 0) {
-    xsT = num * (C * umin - S * vmin);
-    starT = fdiv_fast128(num * (S * umin + C * vmin), N2SC);
-    xsB = num * (C * umax - S * vmax);
-    starB = cdiv_fast128(num * (S * umax + C * vmax), N2SC);
-    ysL = num * (S * umin + C * vmax);
-    starL = fdiv_fast128(num * (C * umin - S * vmax), N2SC);
-    ysR = num * (S * umax + C * vmin);
-    starR = cdiv_fast128(num * (C * umax - S * vmin), N2SC);
+    const i128 N2SC = (i128)N2 * SC;
+    OX.cross_lo = (i128)C * UMN - (i128)S * VMN;     // x* of the top boundary  (x num N2)
+    OX.star_lo = fdiv_fast128((i128)S * UMN + (i128)C * VMN, N2SC);
+    OX.cross_hi = (i128)C * UXN - (i128)S * VXN;     // x** of the bottom boundary
+    OX.star_hi = cdiv_fast128((i128)S * UXN + (i128)C * VXN, N2SC);
+    OY.cross_lo = (i128)S * UMN + (i128)C * VXN;     // y* of the left boundary
+    OY.star_lo = fdiv_fast128((i128)C * UMN - (i128)S * VXN, N2SC);
+    OY.cross_hi = (i128)S * UXN + (i128)C * VMN;     // y** of the right boundary
+    OY.star_hi = cdiv_fast128((i128)C * UXN - (i128)S * VMN, N2SC);
   }
-  const i128 SSC = S * SC, CSC = C * SC;
-  for (int64_t i = lane; i < ws; i += 32) {
-    // local-AABB bound: slices whose scaled range openly overlaps [i, i+1]
-    int64_t jl = fdiv_fast(i * SC * k, nw), jh = cdiv_fast((i + 1) * SC * k, nw) - 1;
-    if (jl < 0) jl = 0;
-    if (jh > k - 1) jh = k - 1;
-    int64_t mt = INT64_MAX, mb = INT64_MIN;
-    for (int64_t j = jl; j <= jh; j++) {
-      if (num * j * w < (i + 1) * SC * k && num * (j + 1) * w > i * SC * k) {
-        mt = min(mt, (int64_t)sl[j]);
-        mb = max(mb, (int64_t)sl[k + j]);
+  // ---- columns: Top / Bottom -------------------------------------------------
+  {
+    int jp = 0;
+    for (int64_t i = lane; i < ws; i += 32) {
+      while (TX.hi[jp] < i) jp++;
+      int32_t t = INT32_MAX, b = INT32_MIN;
+      for (int j = jp; j < k && TX.lo[j] <= i; j++) {
+        t = min(t, TX.flo[j]);
+        b = max(b, TX.chi[j]);
       }
+      int64_t T = max(0, t), B = min((int64_t)b, hs);
+      if (j8 != 0) {
+        const int64_t P0 = i * SC, P1 = min((i + 1) * SC, nw);
+        const i128 P0N = mul_wide(P0, N2), P1N = mul_wide(P1, N2);
+        int64_t ot, ob;
+        if (P0N <= OX.cross_lo && OX.cross_lo <= P1N) ot = OX.star_lo;
+        else if (OX.cross_lo < P0N) ot = fdiv_rcp(VMN + mul_wide(P0, S), DC, rDC);  // increasing line at P0
+        else ot = fdiv_rcp(UMN - mul_wide(P1, C), DS, rDS);                         // decreasing line at P1
+        if (P0N <= OX.cross_hi && OX.cross_hi <= P1N) ob = OX.star_hi;
+        else if (OX.cross_hi < P0N) ob = cdiv_rcp(UXN - mul_wide(P0, C), DS, rDS);  // decreasing line at P0
+        else ob = cdiv_rcp(VXN + mul_wide(P1, S), DC, rDC);                         // increasing line at P1
+        T = max(T, ot);
+        B = min(B, ob);
+      }
+      col[i + 2 * pp.g] = (uint32_t)T | ((uint32_t)B << 16);
     }
-    int64_t t = max((int64_t)0, fdiv_fast(num * mt, SC));
-    int64_t b = min(hs, cdiv_fast(num * mb, SC));
-    if (j8 != 0) {
-      const i128 P0 = (i128)i * SC, P1 = (i128)min((i + 1) * SC, nw);
-      const i128 P0N = P0 * N2, P1N = P1 * N2;
-      int64_t ot, ob;
-      if (P0N <= xsT && xsT <= P1N) ot = starT;
-      else if (xsT < P0N) ot = fdiv_fast128(vmin * num + P0 * S, CSC);  // increasing part, at P0
-      else ot = fdiv_fast128(umin * num - P1 * C, SSC);                 // decreasing part, at P1
-      if (P0N <= xsB && xsB <= P1N) ob = starB;
-      else if (xsB < P0N) ob = cdiv_fast128(umax * num - P0 * C, SSC);  // decreasing, at P0
-      else ob = cdiv_fast128(vmax * num + P1 * S, CSC);                 // increasing, at P1
-      t = max(t, ot);
-      b = min(b, ob);
-    }
-    col[i + 2 * pp.g] = (uint32_t)t | ((uint32_t)b << 16);
   }
-  for (int64_t r = lane; r < hs; r += 32) {
-    int64_t jl = fdiv_fast(r * SC * k, nh), jh = cdiv_fast((r + 1) * SC * k, nh) - 1;
-    if (jl < 0) jl = 0;
-    if (jh > k - 1) jh = k - 1;
-    int64_t ml = INT64_MAX, mr = INT64_MIN;
-    for (int64_t j = jl; j <= jh; j++) {
-      if (num * j * h < (r + 1) * SC * k && num * (j + 1) * h > r * SC * k) {
-        ml = min(ml, (int64_t)sl[2 * k + j]);
-        mr = max(mr, (int64_t)sl[3 * k + j]);
+  // ---- rows: Left / Right -----------------------------------------------------
+  {
+    int jp = 0;
+    for (int64_t r = lane; r < hs; r += 32) {
+      while (TY.hi[jp] < r) jp++;
+      int32_t l = INT32_MAX, rr = INT32_MIN;
+      for (int j = jp; j < k && TY.lo[j] <= r; j++) {
+        l = min(l, TY.flo[j]);
+        rr = max(rr, TY.chi[j]);
       }
+      int64_t L = max(0, l), R = min((int64_t)rr, ws);
+      if (j8 != 0) {
+        const int64_t Q0 = r * SC, Q1 = min((r + 1) * SC, nh);
+        const i128 Q0N = mul_wide(Q0, N2), Q1N = mul_wide(Q1, N2);
+        int64_t ol, orr;
+        if (Q0N <= OY.cross_lo && OY.cross_lo <= Q1N) ol = OY.star_lo;
+        else if (OY.cross_lo < Q0N) ol = fdiv_rcp(mul_wide(Q0, C) - VXN, DS, rDS);  // increasing at Q0
+        else ol = fdiv_rcp(UMN - mul_wide(Q1, S), DC, rDC);                         // decreasing at Q1
+        if (Q0N <= OY.cross_hi && OY.cross_hi <= Q1N) orr = OY.star_hi;
+        else if (OY.cross_hi < Q0N) orr = cdiv_rcp(UXN - mul_wide(Q0, S), DC, rDC);  // decreasing at Q0
+        else orr = cdiv_rcp(mul_wide(Q1, C) - VMN, DS, rDS);                         // increasing at Q1
+        L = max(L, ol);
+        R = min(R, orr);
+      }
+      row[r + 2 * pp.g] = (uint32_t)L | ((uint32_t)R << 16);
     }
-    int64_t l = max((int64_t)0, fdiv_fast(num * ml, SC));
-    int64_t rr = min(ws, cdiv_fast(num * mr, SC));
-    if (j8 != 0) {
-      const i128 Q0 = (i128)r * SC, Q1 = (i128)min((r + 1) * SC, nh);
-      const i128 Q0N = Q0 * N2, Q1N = Q1 * N2;
-      int64_t ol, orr;
-      if (Q0N <= ysL && ysL <= Q1N) ol = starL;
-      else if (ysL < Q0N) ol = fdiv_fast128(Q0 * C - vmax * num, SSC);   // increasing, at Q0
-      else ol = fdiv_fast128(umin * num - Q1 * S, CSC);                  // decreasing, at Q1
-      if (Q0N <= ysR && ysR <= Q1N) orr = starR;
-      else if (ysR < Q0N) orr = cdiv_fast128(umax * num - Q0 * S, CSC);  // decreasing, at Q0
-      else orr = cdiv_fast128(Q1 * C - vmin * num, SSC);                 // increasing, at Q1
-      l = max(l, ol);
-      rr = min(rr, orr);
-    }
-    row[r + 2 * pp.g] = (uint32_t)l | ((uint32_t)rr << 16);
   }
   __syncwarp();
   dilate_slot(col, (int32_t)ws, pp.g, lane);

@@ -63,6 +63,24 @@ __device__ __forceinline__ int64_t fdiv_fast128(i128 a, i128 b) {
   return q;
 }
 __device__ __forceinline__ int64_t cdiv_fast128(i128 a, i128 b) { return -fdiv_fast128(-a, b); }
+// 64 x 64 -> 128-bit signed product with two native multiplies.
+__device__ __forceinline__ i128 mul_wide(int64_t a, int64_t b) {
+  const uint64_t lo = (uint64_t)a * (uint64_t)b;
+  const int64_t hi = __mul64hi(a, b);
+  return (i128)(((unsigned __int128)(uint64_t)hi << 64) | lo);
+}
+// floor(a / b), b > 0 fits int64, from a precomputed reciprocal 1/b and an
+// exact integer correction.
+__device__ __forceinline__ int64_t fdiv_rcp(i128 a, int64_t b, double rcp) {
+  int64_t q = (int64_t)floor(i128_to_double(a) * rcp);
+  i128 r = a - mul_wide(q, b);
+  while (r < 0) { q--; r += b; }
+  while (r >= (i128)b) { q++; r -= b; }
+  return q;
+}
+__device__ __forceinline__ int64_t cdiv_rcp(i128 a, int64_t b, double rcp) {
+  return -fdiv_rcp(-a, b, rcp);
+}
 
 // ---- warp reductions (full warp) ------------------------------------------
 __device__ __forceinline__ int32_t warp_max(int32_t v) {
