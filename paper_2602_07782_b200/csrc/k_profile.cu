@@ -6,21 +6,21 @@
 // scale m/M ("We evaluate TopEdge and BottomEdge using both
 // proxies and use the result per-texel that provides the tightest bound"),
 // rounded outward (D11), then applies the gutter as a Chebyshev dilation by g
-// (D13).  One warp per (chart, candidate); lanes walk the columns/rows and
-// store packed uint16 pairs coalesced; the dilation is an in-place window
-// min/max over the warp's slot.
+// (D13).  One warp per (chart, candidate); lanes walk the columns and rows
+// (one merged index space, so narrow charts still fill the warp) and store
+// packed uint16 pairs coalesced; the dilation is an in-place window min/max.
 //
-// Cost structure (what makes this kernel fast):
-//  * local-AABB bound: each slice's scaled floor/ceil and the column range it
+// Cost structure:
+//  * local-AABB bound: each slice's scaled floor/ceil and the cell range it
 //    openly overlaps are computed once per (chart, candidate) by lanes j < k;
-//    a column then takes min/max over its 1-2 slices found by a per-lane
-//    pointer (columns of a lane increase monotonically) -- no division;
-//  * OBB bound: y_top(x) = max(decreasing, increasing line) is minimised over
-//    the column strip; the crossing point and value are per-(chart,
-//    candidate) constants, so per column exactly one line is evaluated (left
-//    of the crossing the decreasing one at the strip's right end, right of it
-//    the increasing one at the left end): one exact division, done as a
-//    multiply by a precomputed reciprocal plus an integer correction.
+//    a cell takes min/max over its 1-2 slices, found by a per-lane pointer
+//    (a lane's cells increase monotonically) -- no division per cell;
+//  * OBB bound: y_top(x) = max(decreasing, increasing line) minimised over the
+//    cell's strip.  Which case applies (crossing inside / left / right) is an
+//    integer compare of the cell index with per-(chart, candidate) crossing
+//    indices; each line evaluated at a cell edge is floor((A + i*B)/D), an
+//    int64 progression (LinDiv) whose 128-bit parts are split off once per
+//    warp, lane-parallel.  So a cell costs two int64 multiply-corrects.
 //
 // K3b computes, per candidate and adjacent sorted pair, the horizontal
 // compaction advance (a max-reduction of profile gaps over shared
@@ -33,10 +33,23 @@ namespace {
 constexpr int kWarps = 8;
 
 struct SliceTab {  // per-warp tables, one axis
-  int32_t lo[TABI_KMAX];    // first texel column/row the slice openly overlaps
+  int32_t lo[TABI_KMAX];    // first texel cell the slice openly overlaps
   int32_t hi[TABI_KMAX];    // last one
   int32_t flo[TABI_KMAX];   // floor(num * low bound / SC)
   int32_t chi[TABI_KMAX];   // ceil(num * high bound / SC)
+};
+
+// Per-warp OBB constants.  Index q = axis * 2 + (0: low bound, 1: high bound);
+// lines lin[axis * 4 + kind]: kind 0 low-bound line right of the crossing
+// (evaluated at the cell's left edge), 1 low-bound line left of it (right
+// edge, non-last cells), 2 / 3 the same for the high bound (negated floors).
+struct ObbW {
+  LinDiv lin[8];
+  int64_t last[4];   // value at the clipped right edge of the last cell
+  int64_t star[4];   // value at the crossing
+  int64_t iA[4];     // crossing at or right of cell i's left edge  <=>  i <= iA
+  int64_t iB[4];     // crossing at or left of cell i's right edge  <=>  i >= iB (non-last)
+  int32_t lastB[4];  // same test for the last cell (edge = chart extent)
 };
 
 // In-place Chebyshev dilation of a slot holding raw (lo, hi) pairs at
@@ -73,13 +86,67 @@ __device__ void build_tab(SliceTab& T, const int32_t* blo, const int32_t* bhi, i
     T.flo[j] = (int32_t)fdiv_fast(num * blo[j], SC);
     T.chi[j] = (int32_t)cdiv_fast(num * bhi[j], SC);
   }
-  __syncwarp();
 }
 
-struct ObbLine {   // constants of one axis' OBB bounds at one scale
-  i128 cross_lo, cross_hi;   // num * crossing numerator (compare with P * N2)
-  int64_t star_lo, star_hi;  // bound values at the crossings (floor / ceil, scaled)
-};
+// Lane-parallel setup of the OBB constants (D11).  The box is
+// {Umin <= xC + yS <= Umax, Vmin <= -xS + yC <= Vmax}; with num/SC scaling:
+//  top    y_top(x)   = max((Umin - xC)/S, (Vmin + xS)/C)
+//  bottom y_bot(x)   = min((Umax - xC)/S, (Vmax + xS)/C)
+//  left   x_left(y)  = max((Umin - yS)/C, (yC - Vmax)/S)
+//  right  x_right(y) = min((Umax - yS)/C, (yC - Vmin)/S)
+__device__ void build_obb(ObbW& O, int64_t C, int64_t S, i128 UMN, i128 UXN, i128 VMN, i128 VXN,
+                          int64_t SC, int64_t nw, int64_t nh, int lane) {
+  const int64_t N2 = C * C + S * S, DS = S * SC, DC = C * SC;
+  const i128 N2SC = (i128)N2 * SC;
+  const int64_t SCS = SC * S, SCC = SC * C;
+  if (lane < 8) {
+    i128 A;
+    int64_t B, D;
+    switch (lane) {
+      case 0: A = VMN; B = SCS; D = DC; break;               // top, increasing line at P0
+      case 1: A = UMN - SCC; B = -SCC; D = DS; break;        // top, decreasing line at P1
+      case 2: A = -UXN; B = SCC; D = DS; break;              // bottom, decreasing at P0 (neg)
+      case 3: A = -VXN - SCS; B = -SCS; D = DC; break;       // bottom, increasing at P1 (neg)
+      case 4: A = -VXN; B = SCC; D = DS; break;              // left, increasing at Q0
+      case 5: A = UMN - SCS; B = -SCS; D = DC; break;        // left, decreasing at Q1
+      case 6: A = -UXN; B = SCS; D = DC; break;              // right, decreasing at Q0 (neg)
+      default: A = VMN - SCC; B = -SCC; D = DS; break;       // right, increasing at Q1 (neg)
+    }
+    O.lin[lane] = make_lindiv(A, B, D);
+  } else if (lane < 12) {
+    const int q = lane - 8;
+    int64_t v;
+    switch (q) {
+      case 0: v = fdiv_fast128(UMN - mul_wide(nw, C), (i128)DS); break;
+      case 1: v = cdiv_fast128(VXN + mul_wide(nw, S), (i128)DC); break;
+      case 2: v = fdiv_fast128(UMN - mul_wide(nh, S), (i128)DC); break;
+      default: v = cdiv_fast128(mul_wide(nh, C) - VMN, (i128)DS); break;
+    }
+    O.last[q] = v;
+  } else if (lane < 16) {
+    const int q = lane - 12;
+    int64_t v;
+    switch (q) {
+      case 0: v = fdiv_fast128((i128)S * UMN + (i128)C * VMN, N2SC); break;
+      case 1: v = cdiv_fast128((i128)S * UXN + (i128)C * VXN, N2SC); break;
+      case 2: v = fdiv_fast128((i128)C * UMN - (i128)S * VXN, N2SC); break;
+      default: v = cdiv_fast128((i128)C * UXN - (i128)S * VMN, N2SC); break;
+    }
+    O.star[q] = v;
+  } else if (lane < 20) {
+    const int q = lane - 16;
+    i128 cross;
+    switch (q) {
+      case 0: cross = (i128)C * UMN - (i128)S * VMN; break;   // x* of the top boundary
+      case 1: cross = (i128)C * UXN - (i128)S * VXN; break;   // x** of the bottom
+      case 2: cross = (i128)S * UMN + (i128)C * VXN; break;   // y* of the left
+      default: cross = (i128)S * UXN + (i128)C * VMN; break;  // y** of the right
+    }
+    O.iA[q] = fdiv_clamp128(cross, N2SC);
+    O.iB[q] = -fdiv_clamp128(-cross, N2SC) - 1;
+    O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
+  }
+}
 
 __global__ void __launch_bounds__(kWarps * 32, 2)
 profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
@@ -87,6 +154,7 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
                uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all, int32_t* cand_bad,
                const Status* st) {
   __shared__ SliceTab tabs[kWarps][2];
+  __shared__ ObbW obbs[kWarps];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t item = (int64_t)blockIdx.x * kWarps + wib;
@@ -109,86 +177,48 @@ profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
     return;
   }
   const int32_t* sl = P.sl + (int64_t)c * 4 * k;
-  SliceTab& TX = tabs[wib][0];
-  SliceTab& TY = tabs[wib][1];
-  build_tab(TX, sl, sl + k, w, num, SC, k, lane);
-  build_tab(TY, sl + 2 * k, sl + 3 * k, h, num, SC, k, lane);
+  const SliceTab* TT = tabs[wib];
+  build_tab(tabs[wib][0], sl, sl + k, w, num, SC, k, lane);
+  build_tab(tabs[wib][1], sl + 2 * k, sl + 3 * k, h, num, SC, k, lane);
   const int j8 = P.obb_j[c];
+  ObbW& O = obbs[wib];
+  if (j8 != 0) {
+    const int64_t C = kQC[j8], S = kQS[j8];
+    const int64_t* ob = P.obb + 4 * (int64_t)c;
+    build_obb(O, C, S, mul_wide(ob[0], num), mul_wide(ob[1], num), mul_wide(ob[2], num),
+              mul_wide(ob[3], num), SC, nw, nh, lane);
+  }
+  __syncwarp();
   uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
   uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-  // ---- OBB constants (D11): lines of the box in the (x, y) chart frame ----
-  const int64_t C = kQC[j8], S = kQS[j8], N2 = C * C + S * S;
-  const int64_t umin = P.obb[4 * (int64_t)c], umax = P.obb[4 * (int64_t)c + 1];
-  const int64_t vmin = P.obb[4 * (int64_t)c + 2], vmax = P.obb[4 * (int64_t)c + 3];
-  const i128 UMN = mul_wide(umin, num), UXN = mul_wide(umax, num);
-  const i128 VMN = mul_wide(vmin, num), VXN = mul_wide(vmax, num);
-  const int64_t DS = S * SC, DC = C * SC;          // divisors of the two lines
-  const double rDS = 1.0 / (double)DS, rDC = 1.0 / (double)DC;
-  ObbLine OX{}, OY{};
-  if (j8 != 0) {
-    const i128 N2SC = (i128)N2 * SC;
-    OX.cross_lo = (i128)C * UMN - (i128)S * VMN;     // x* of the top boundary  (x num N2)
-    OX.star_lo = fdiv_fast128((i128)S * UMN + (i128)C * VMN, N2SC);
-    OX.cross_hi = (i128)C * UXN - (i128)S * VXN;     // x** of the bottom boundary
-    OX.star_hi = cdiv_fast128((i128)S * UXN + (i128)C * VXN, N2SC);
-    OY.cross_lo = (i128)S * UMN + (i128)C * VXN;     // y* of the left boundary
-    OY.star_lo = fdiv_fast128((i128)C * UMN - (i128)S * VXN, N2SC);
-    OY.cross_hi = (i128)S * UXN + (i128)C * VMN;     // y** of the right boundary
-    OY.star_hi = cdiv_fast128((i128)C * UXN - (i128)S * VMN, N2SC);
-  }
-  // ---- columns: Top / Bottom -------------------------------------------------
-  {
-    int jp = 0;
-    for (int64_t i = lane; i < ws; i += 32) {
-      while (TX.hi[jp] < i) jp++;
-      int32_t t = INT32_MAX, b = INT32_MIN;
-      for (int j = jp; j < k && TX.lo[j] <= i; j++) {
-        t = min(t, TX.flo[j]);
-        b = max(b, TX.chi[j]);
-      }
-      int64_t T = max(0, t), B = min((int64_t)b, hs);
-      if (j8 != 0) {
-        const int64_t P0 = i * SC, P1 = min((i + 1) * SC, nw);
-        const i128 P0N = mul_wide(P0, N2), P1N = mul_wide(P1, N2);
-        int64_t ot, ob;
-        if (P0N <= OX.cross_lo && OX.cross_lo <= P1N) ot = OX.star_lo;
-        else if (OX.cross_lo < P0N) ot = fdiv_rcp(VMN + mul_wide(P0, S), DC, rDC);  // increasing line at P0
-        else ot = fdiv_rcp(UMN - mul_wide(P1, C), DS, rDS);                         // decreasing line at P1
-        if (P0N <= OX.cross_hi && OX.cross_hi <= P1N) ob = OX.star_hi;
-        else if (OX.cross_hi < P0N) ob = cdiv_rcp(UXN - mul_wide(P0, C), DS, rDS);  // decreasing line at P0
-        else ob = cdiv_rcp(VXN + mul_wide(P1, S), DC, rDC);                         // increasing line at P1
-        T = max(T, ot);
-        B = min(B, ob);
-      }
-      col[i + 2 * pp.g] = (uint32_t)T | ((uint32_t)B << 16);
+  int jp = 0, ax_prev = 0;
+  for (int64_t e = lane; e < ws + hs; e += 32) {
+    const int ax = e >= ws ? 1 : 0;      // 0: column i (top/bottom), 1: row i (left/right)
+    const int64_t i = ax ? e - ws : e;
+    const int64_t cnt = ax ? hs : ws;
+    const SliceTab& T = TT[ax];
+    if (ax != ax_prev) { jp = 0; ax_prev = ax; }
+    while (T.hi[jp] < i) jp++;
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (int j = jp; j < k && T.lo[j] <= i; j++) {
+      lo = min(lo, T.flo[j]);
+      hi = max(hi, T.chi[j]);
     }
-  }
-  // ---- rows: Left / Right -----------------------------------------------------
-  {
-    int jp = 0;
-    for (int64_t r = lane; r < hs; r += 32) {
-      while (TY.hi[jp] < r) jp++;
-      int32_t l = INT32_MAX, rr = INT32_MIN;
-      for (int j = jp; j < k && TY.lo[j] <= r; j++) {
-        l = min(l, TY.flo[j]);
-        rr = max(rr, TY.chi[j]);
-      }
-      int64_t L = max(0, l), R = min((int64_t)rr, ws);
-      if (j8 != 0) {
-        const int64_t Q0 = r * SC, Q1 = min((r + 1) * SC, nh);
-        const i128 Q0N = mul_wide(Q0, N2), Q1N = mul_wide(Q1, N2);
-        int64_t ol, orr;
-        if (Q0N <= OY.cross_lo && OY.cross_lo <= Q1N) ol = OY.star_lo;
-        else if (OY.cross_lo < Q0N) ol = fdiv_rcp(mul_wide(Q0, C) - VXN, DS, rDS);  // increasing at Q0
-        else ol = fdiv_rcp(UMN - mul_wide(Q1, S), DC, rDC);                         // decreasing at Q1
-        if (Q0N <= OY.cross_hi && OY.cross_hi <= Q1N) orr = OY.star_hi;
-        else if (OY.cross_hi < Q0N) orr = cdiv_rcp(UXN - mul_wide(Q0, S), DC, rDC);  // decreasing at Q0
-        else orr = cdiv_rcp(mul_wide(Q1, C) - VMN, DS, rDS);                         // increasing at Q1
-        L = max(L, ol);
-        R = min(R, orr);
-      }
-      row[r + 2 * pp.g] = (uint32_t)L | ((uint32_t)R << 16);
+    int64_t L = max(0, lo), H = min((int64_t)hi, ax ? ws : hs);
+    if (j8 != 0) {
+      const bool last = i == cnt - 1;
+      const int q0 = 2 * ax, q1 = 2 * ax + 1;
+      int64_t v;
+      if (i <= O.iA[q0] && (last ? O.lastB[q0] != 0 : i >= O.iB[q0])) v = O.star[q0];
+      else if (i > O.iA[q0]) v = lindiv_eval(O.lin[4 * ax + 0], i);
+      else v = last ? O.last[q0] : lindiv_eval(O.lin[4 * ax + 1], i);
+      L = max(L, v);
+      if (i <= O.iA[q1] && (last ? O.lastB[q1] != 0 : i >= O.iB[q1])) v = O.star[q1];
+      else if (i > O.iA[q1]) v = -lindiv_eval(O.lin[4 * ax + 2], i);
+      else v = last ? O.last[q1] : -lindiv_eval(O.lin[4 * ax + 3], i);
+      H = min(H, v);
     }
+    (ax ? row : col)[i + 2 * pp.g] = (uint32_t)L | ((uint32_t)H << 16);
   }
   __syncwarp();
   dilate_slot(col, (int32_t)ws, pp.g, lane);

@@ -81,6 +81,39 @@ __device__ __forceinline__ int64_t fdiv_rcp(i128 a, int64_t b, double rcp) {
 __device__ __forceinline__ int64_t cdiv_rcp(i128 a, int64_t b, double rcp) {
   return -fdiv_rcp(-a, b, rcp);
 }
+// floor(a / b) clamped to [-2^40, 2^40] (callers compare it with small indices).
+__device__ __forceinline__ int64_t fdiv_clamp128(i128 a, i128 b) {
+  const double est = i128_to_double(a) / i128_to_double(b);
+  if (est > 1099511627776.0) return 1099511627776LL;
+  if (est < -1099511627776.0) return -1099511627776LL;
+  return fdiv_fast128(a, b);
+}
+
+// f(i) = floor((A + i*B) / D) for i >= 0 as an int64 progression:
+// A = qA*D + rA, B = qB*D + rB (0 <= rA, rB < D), so
+// f(i) = qA + i*qB + floor((rA + i*rB) / D) with a small int64 numerator.
+struct LinDiv {
+  int64_t qA, rA, qB, rB, D;
+  double rcp;
+};
+__device__ __forceinline__ LinDiv make_lindiv(i128 A, int64_t B, int64_t D) {
+  LinDiv L;
+  L.D = D;
+  L.rcp = 1.0 / (double)D;
+  L.qA = fdiv_fast128(A, (i128)D);
+  L.rA = (int64_t)(A - mul_wide(L.qA, D));
+  L.qB = fdiv_fast(B, D);
+  L.rB = B - L.qB * D;
+  return L;
+}
+__device__ __forceinline__ int64_t lindiv_eval(const LinDiv& L, int64_t i) {
+  const int64_t N = L.rA + i * L.rB;
+  int64_t t = (int64_t)((double)N * L.rcp);
+  int64_t r = N - t * L.D;
+  while (r < 0) { t--; r += L.D; }
+  while (r >= L.D) { t++; r -= L.D; }
+  return L.qA + i * L.qB + t;
+}
 
 // ---- warp reductions (full warp) ------------------------------------------
 __device__ __forceinline__ int32_t warp_max(int32_t v) {
