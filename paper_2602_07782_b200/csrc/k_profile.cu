@@ -6,21 +6,22 @@
 // scale m/M ("We evaluate TopEdge and BottomEdge using both
 // proxies and use the result per-texel that provides the tightest bound"),
 // rounded outward (D11), then applies the gutter as a Chebyshev dilation by g
-// (D13).  One warp per (chart, candidate); lanes walk the columns and rows
-// (one merged index space, so narrow charts still fill the warp) and store
-// packed uint16 pairs coalesced; the dilation is an in-place window min/max.
+// (D13).
 //
-// Cost structure:
-//  * local-AABB bound: each slice's scaled floor/ceil and the cell range it
-//    openly overlaps are computed once per (chart, candidate) by lanes j < k;
-//    a cell takes min/max over its 1-2 slices, found by a per-lane pointer
-//    (a lane's cells increase monotonically) -- no division per cell;
-//  * OBB bound: y_top(x) = max(decreasing, increasing line) minimised over the
-//    cell's strip.  Which case applies (crossing inside / left / right) is an
-//    integer compare of the cell index with per-(chart, candidate) crossing
-//    indices; each line evaluated at a cell edge is floor((A + i*B)/D), an
-//    int64 progression (LinDiv) whose 128-bit parts are split off once per
-//    warp, lane-parallel.  So a cell costs two int64 multiply-corrects.
+// Work decomposition (tile kernel): one CTA takes kTC consecutive sorted
+// charts of one candidate.  Setup -- the per-(chart, candidate) constants --
+// is split into 8 uniform jobs per chart (no divergent lane groups, every
+// division a multiply by a precomputed reciprocal plus an exact integer
+// correction).  Then all threads walk the tile's flattened cells into a
+// shared-memory raw buffer and dilate from it into the HBM slots (coalesced).
+// Charts whose raw cells exceed the buffer go to a compacted list processed
+// by a warp-per-chart kernel (same arithmetic).
+//
+// Per cell: the local-AABB bound takes min/max over the 1-2 slices that
+// openly overlap it (slice range by reciprocal multiply, per-slice scaled
+// floor/ceil from the setup tables); the OBB bound is an integer compare of
+// the cell index with the crossing indices plus one int64 progression
+// (LinDiv) per bound.
 //
 // K3b computes, per candidate and adjacent sorted pair, the horizontal
 // compaction advance (a max-reduction of profile gaps over shared
@@ -30,30 +31,278 @@
 namespace tabi {
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kTC = 16;      // charts per tile
+constexpr int kTT = 128;     // threads per tile CTA (8 per chart during setup)
+constexpr int kRaw = 8192;   // raw cells per chunk (32 KB)
+constexpr int kWarps = 8;    // big-chart kernel: warps per CTA
 
-struct SliceTab {  // per-warp tables, one axis
-  int32_t lo[TABI_KMAX];    // first texel cell the slice openly overlaps
-  int32_t hi[TABI_KMAX];    // last one
-  int32_t flo[TABI_KMAX];   // floor(num * low bound / SC)
-  int32_t chi[TABI_KMAX];   // ceil(num * high bound / SC)
-};
-
-// Per-warp OBB constants.  Index q = axis * 2 + (0: low bound, 1: high bound);
+// Per-(chart, candidate) constants.  OBB index q = axis * 2 + (0 low, 1 high);
 // lines lin[axis * 4 + kind]: kind 0 low-bound line right of the crossing
-// (evaluated at the cell's left edge), 1 low-bound line left of it (right
-// edge, non-last cells), 2 / 3 the same for the high bound (negated floors).
-struct ObbW {
+// (at the cell's low edge), 1 low-bound line left of it (high edge, non-last
+// cells), 2 / 3 the same for the high bound (negated floors).
+struct ObbC {
   LinDiv lin[8];
-  int64_t last[4];   // value at the clipped right edge of the last cell
+  int64_t last[4];   // value at the clipped high edge of the last cell
   int64_t star[4];   // value at the crossing
-  int64_t iA[4];     // crossing at or right of cell i's left edge  <=>  i <= iA
-  int64_t iB[4];     // crossing at or left of cell i's right edge  <=>  i >= iB (non-last)
+  int64_t iA[4];     // crossing at or beyond cell i's low edge  <=>  i <= iA
+  int64_t iB[4];     // crossing at or before cell i's high edge <=>  i >= iB (non-last)
   int32_t lastB[4];  // same test for the last cell (edge = chart extent)
 };
 
-// In-place Chebyshev dilation of a slot holding raw (lo, hi) pairs at
-// positions [2g, 2g + n0): out[i] = (min lo, max hi + 2g) over raw [i-2g, i].
+struct ChartK3 {
+  int32_t s, c, ws, hs, j8, small;  // small: handled by the tile kernel
+  int32_t col_o, row_o;             // slot offsets in dcol / drow (candidate base added)
+  int64_t nw, nh;
+  double rnw, rnh;                  // 1 / (num * w), 1 / (num * h)
+  ObbC O;
+};
+
+// ---- setup jobs ---------------------------------------------------------
+// Slice entry: scaled floor of the low bound / ceil of the high bound.
+__device__ __forceinline__ void slice_job(int32_t* tab, const int32_t* blo, const int32_t* bhi, int j,
+                                          int64_t num, int64_t SC, double rSC) {
+  tab[2 * j] = (int32_t)fdiv_r64(num * blo[j], SC, rSC);
+  tab[2 * j + 1] = (int32_t)(-fdiv_r64(-num * bhi[j], SC, rSC));
+}
+
+// OBB job r (0..7) of a chart: LinDiv r, one of last/star, one of iA/iB.  The
+// box is {Umin <= xC + yS <= Umax, Vmin <= -xS + yC <= Vmax}; with num/SC:
+//  top    y_top(x)   = max((Umin - xC)/S, (Vmin + xS)/C)
+//  bottom y_bot(x)   = min((Umax - xC)/S, (Vmax + xS)/C)
+//  left   x_left(y)  = max((Umin - yS)/C, (yC - Vmax)/S)
+//  right  x_right(y) = min((Umax - yS)/C, (yC - Vmin)/S)
+__device__ void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i128 UXN, i128 VMN, i128 VXN,
+                        int64_t SC, int64_t nw, int64_t nh) {
+  const int64_t N2 = C * C + S * S, DS = S * SC, DC = C * SC;
+  const i128 N2SC = (i128)N2 * SC;
+  const double rDS = 1.0 / (double)DS, rDC = 1.0 / (double)DC, rN2SC = 1.0 / i128_to_double(N2SC);
+  const int64_t SCS = SC * S, SCC = SC * C;
+  {  // LinDiv r
+    i128 A;
+    int64_t B, D;
+    double rD;
+    switch (r) {
+      case 0: A = VMN; B = SCS; D = DC; rD = rDC; break;          // top, increasing line at P0
+      case 1: A = UMN - SCC; B = -SCC; D = DS; rD = rDS; break;   // top, decreasing line at P1
+      case 2: A = -UXN; B = SCC; D = DS; rD = rDS; break;         // bottom, decreasing at P0 (neg)
+      case 3: A = -VXN - SCS; B = -SCS; D = DC; rD = rDC; break;  // bottom, increasing at P1 (neg)
+      case 4: A = -VXN; B = SCC; D = DS; rD = rDS; break;         // left, increasing at Q0
+      case 5: A = UMN - SCS; B = -SCS; D = DC; rD = rDC; break;   // left, decreasing at Q1
+      case 6: A = -UXN; B = SCS; D = DC; rD = rDC; break;         // right, decreasing at Q0 (neg)
+      default: A = VMN - SCC; B = -SCC; D = DS; rD = rDS; break;  // right, increasing at Q1 (neg)
+    }
+    LinDiv L;
+    L.D = D;
+    L.rcp = rD;
+    L.qA = fdiv_r128(A, (i128)D, rD, false);
+    L.rA = (int64_t)(A - mul_wide(L.qA, D));
+    L.qB = fdiv_r64(B, D, rD);
+    L.rB = B - L.qB * D;
+    O.lin[r] = L;
+  }
+  const int q = r & 3;
+  if (r < 4) {  // value at the last cell's clipped edge
+    int64_t v;
+    switch (q) {
+      case 0: v = fdiv_r128(UMN - mul_wide(nw, C), (i128)DS, rDS, false); break;
+      case 1: v = -fdiv_r128(-(VXN + mul_wide(nw, S)), (i128)DC, rDC, false); break;
+      case 2: v = fdiv_r128(UMN - mul_wide(nh, S), (i128)DC, rDC, false); break;
+      default: v = -fdiv_r128(-(mul_wide(nh, C) - VMN), (i128)DS, rDS, false); break;
+    }
+    O.last[q] = v;
+  } else {  // value at the crossing
+    int64_t v;
+    switch (q) {
+      case 0: v = fdiv_r128((i128)S * UMN + (i128)C * VMN, N2SC, rN2SC, false); break;
+      case 1: v = -fdiv_r128(-((i128)S * UXN + (i128)C * VXN), N2SC, rN2SC, false); break;
+      case 2: v = fdiv_r128((i128)C * UMN - (i128)S * VXN, N2SC, rN2SC, false); break;
+      default: v = -fdiv_r128(-((i128)C * UXN - (i128)S * VMN), N2SC, rN2SC, false); break;
+    }
+    O.star[q] = v;
+  }
+  i128 cross;
+  switch (q) {
+    case 0: cross = (i128)C * UMN - (i128)S * VMN; break;   // x* of the top boundary
+    case 1: cross = (i128)C * UXN - (i128)S * VXN; break;   // x** of the bottom
+    case 2: cross = (i128)S * UMN + (i128)C * VXN; break;   // y* of the left
+    default: cross = (i128)S * UXN + (i128)C * VMN; break;  // y** of the right
+  }
+  if (r < 4) {
+    O.iA[q] = fdiv_r128(cross, N2SC, rN2SC, true);
+    O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
+  } else {
+    O.iB[q] = -fdiv_r128(-cross, N2SC, rN2SC, true) - 1;
+  }
+}
+
+// Raw (undilated) bounds of cell i on axis ax (0: column -> (Top, Bottom),
+// 1: row -> (Left, Right)), packed lo | hi << 16.
+__device__ __forceinline__ uint32_t raw_cell(const ChartK3& H, const int32_t* tab, int k, int ax,
+                                             int64_t i, int64_t num, int64_t SC) {
+  const int64_t nx = ax ? H.nh : H.nw;
+  const double rnx = ax ? H.rnh : H.rnw;
+  const int64_t SCk = SC * k;
+  int64_t jl = fdiv_r64(i * SCk, nx, rnx);
+  int64_t jh = -fdiv_r64(-(i + 1) * SCk, nx, rnx) - 1;
+  if (jl < 0) jl = 0;
+  if (jh > k - 1) jh = k - 1;
+  const int32_t* t = tab + ax * 2 * k;
+  int32_t lo = INT32_MAX, hi = INT32_MIN;
+  for (int64_t j = jl; j <= jh; j++) {
+    lo = min(lo, t[2 * j]);
+    hi = max(hi, t[2 * j + 1]);
+  }
+  const int64_t cnt = ax ? H.hs : H.ws;
+  int64_t L = max(0, lo), Hh = min((int64_t)hi, ax ? (int64_t)H.ws : (int64_t)H.hs);
+  if (H.j8 != 0) {
+    const ObbC& O = H.O;
+    const bool last = i == cnt - 1;
+    const int q0 = 2 * ax, q1 = 2 * ax + 1;
+    int64_t v;
+    if (i <= O.iA[q0] && (last ? O.lastB[q0] != 0 : i >= O.iB[q0])) v = O.star[q0];
+    else if (i > O.iA[q0]) v = lindiv_eval(O.lin[4 * ax + 0], i);
+    else v = last ? O.last[q0] : lindiv_eval(O.lin[4 * ax + 1], i);
+    L = max(L, v);
+    if (i <= O.iA[q1] && (last ? O.lastB[q1] != 0 : i >= O.iB[q1])) v = O.star[q1];
+    else if (i > O.iA[q1]) v = -lindiv_eval(O.lin[4 * ax + 2], i);
+    else v = last ? O.last[q1] : -lindiv_eval(O.lin[4 * ax + 3], i);
+    Hh = min(Hh, v);
+  }
+  return (uint32_t)L | ((uint32_t)Hh << 16);
+}
+
+// Setup of one chart by 8 cooperating threads r = 0..7 (rank r).
+__device__ void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, int64_t num,
+                            int64_t SC, int r) {
+  const int c = H.c;
+  const int32_t* sl = P.sl + (int64_t)c * 4 * k;
+  const double rSC = 1.0 / (double)SC;
+  for (int idx = r; idx < 2 * k; idx += 8) {
+    const int ax = idx >= k, j = ax ? idx - k : idx;
+    slice_job(tab + ax * 2 * k, sl + 2 * ax * k, sl + 2 * ax * k + k, j, num, SC, rSC);
+  }
+  if (H.j8 != 0) {
+    const int64_t* ob = P.obb + 4 * (int64_t)c;
+    obb_job(H.O, r, kQC[H.j8], kQS[H.j8], mul_wide(ob[0], num), mul_wide(ob[1], num),
+            mul_wide(ob[2], num), mul_wide(ob[3], num), SC, H.nw, H.nh);
+  }
+}
+
+__global__ void __launch_bounds__(kTT, 4)
+profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
+                    const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
+                    uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all,
+                    int32_t* cand_bad, int32_t* big_list, Status* st) {
+  __shared__ ChartK3 CH[kTC];
+  __shared__ int32_t cells[kTC], cpre[kTC + 1], opre[kTC + 1];
+  __shared__ int32_t chunk_end;
+  extern __shared__ __align__(16) int32_t dyn[];
+  if (st->bad_chart != INT32_MAX || st->capacity) return;
+  const int k = pp.k;
+  int32_t* tabs = dyn;                          // [kTC][2 axes][k][2]
+  uint32_t* raw = (uint32_t*)(dyn + kTC * 4 * k);
+  const int tid = threadIdx.x;
+  const int m = blockIdx.y + 1;
+  const int s0 = blockIdx.x * kTC;
+  const int nt = min(kTC, pp.n - s0);
+  const int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
+  const double rSC = 1.0 / (double)SC;
+  const int ci = tid >> 3, r = tid & 7;
+  if (ci < nt && r == 0) {
+    ChartK3& H = CH[ci];
+    const int s = s0 + ci;
+    const int c = perm[s];
+    const int64_t w = P.w[c], h = P.h[c];
+    H.s = s;
+    H.c = c;
+    H.nw = num * w;
+    H.nh = num * h;
+    H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
+    H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
+    H.rnw = 1.0 / (double)H.nw;
+    H.rnh = 1.0 / (double)H.nh;
+    H.j8 = P.obb_j[c];
+    const int64_t b = (int64_t)(m - 1) * pp.n + s;
+    wd_all[b] = H.ws + 2 * pp.g;
+    hd_all[b] = H.hs + 2 * pp.g;
+    const bool fits = H.ws + 2 * pp.g <= pp.Wp && H.hs + 2 * pp.g <= pp.Hp;
+    if (!fits) cand_bad[m - 1] = 1;
+    H.small = fits && (H.ws + H.hs <= kRaw);
+    if (fits && !H.small) big_list[atomicAdd(&st->pad[1], 1)] = (m - 1) * pp.n + s;
+    H.col_o = colofs[s];
+    H.row_o = rowofs[s];
+    cells[ci] = H.small ? H.ws + H.hs : 0;
+  }
+  __syncthreads();
+  if (ci < nt && CH[ci].small) chart_setup(CH[ci], tabs + ci * 4 * k, P, k, num, SC, r);
+  __syncthreads();
+  uint32_t* colb = dcol + (int64_t)(m - 1) * pp.col_cap;
+  uint32_t* rowb = drow + (int64_t)(m - 1) * pp.row_cap;
+  const int g = pp.g;
+  for (int cb = 0; cb < nt;) {
+    if (tid == 0) {  // chunk [cb, ce): raw cells fit the buffer
+      int e = cb, tot = 0, otot = 0;
+      cpre[0] = 0;
+      opre[0] = 0;
+      while (e < nt && tot + cells[e] <= kRaw) {
+        tot += cells[e];
+        otot += cells[e] ? cells[e] + 4 * g : 0;
+        e++;
+        cpre[e - cb] = tot;
+        opre[e - cb] = otot;
+      }
+      chunk_end = e;
+    }
+    __syncthreads();
+    const int ce = chunk_end, nc = ce - cb;
+    const int32_t ncell = cpre[nc], nout = opre[nc];
+    // raw pass over the chunk's flattened cells
+    for (int e = tid; e < ncell; e += kTT) {
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cpre[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const ChartK3& H = CH[cb + lo];
+      const int32_t x = e - cpre[lo];
+      const int ax = x >= H.ws;
+      raw[e] = raw_cell(H, tabs + (cb + lo) * 4 * k, k, ax, ax ? x - H.ws : x, num, SC);
+    }
+    __syncthreads();
+    // dilation pass over the chunk's flattened outputs (Wd columns, Hd rows)
+    for (int o = tid; o < nout; o += kTT) {
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (opre[mid] <= o) lo = mid;
+        else hi = mid - 1;
+      }
+      const ChartK3& H = CH[cb + lo];
+      const int32_t y = o - opre[lo];
+      const int Wd = H.ws + 2 * g;
+      const int ax = y >= Wd;
+      const int32_t i = ax ? y - Wd : y;
+      const int32_t n0 = ax ? H.hs : H.ws;
+      const uint32_t* rr = raw + cpre[lo] + (ax ? H.ws : 0);
+      const int q0 = max(0, i - 2 * g), q1 = min(i, n0 - 1);
+      int32_t vl = INT32_MAX, vh = INT32_MIN;
+      for (int q = q0; q <= q1; q++) {
+        const uint32_t v = rr[q];
+        vl = min(vl, lo16(v));
+        vh = max(vh, hi16(v));
+      }
+      (ax ? rowb + H.row_o : colb + H.col_o)[i] = (uint32_t)vl | ((uint32_t)(vh + 2 * g) << 16);
+    }
+    __syncthreads();
+    cb = ce;
+    while (cb < nt && cells[cb] == 0) cb++;  // skip charts handled elsewhere
+    __syncthreads();
+  }
+}
+
+// Warp per large chart (raw cells > kRaw) from the compacted list; raw values
+// go straight into the HBM slot, then an in-place dilation.
 __device__ void dilate_slot(uint32_t* slot, int32_t n0, int32_t g, int lane) {
   const int32_t nd = n0 + 2 * g;
   for (int base = 0; base < nd; base += 32) {
@@ -73,156 +322,52 @@ __device__ void dilate_slot(uint32_t* slot, int32_t n0, int32_t g, int lane) {
   }
 }
 
-// Slice table of one axis: slice j spans [j*ext/k, (j+1)*ext/k] (units), i.e.
-// the scaled range [num*j*ext/(SC*k), num*(j+1)*ext/(SC*k)]; it openly
-// overlaps texel t iff num*j*ext < (t+1)*SC*k and num*(j+1)*ext > t*SC*k, i.e.
-// t in [floor(num*j*ext/(SC*k)), ceil(num*(j+1)*ext/(SC*k)) - 1].
-__device__ void build_tab(SliceTab& T, const int32_t* blo, const int32_t* bhi, int64_t ext,
-                          int64_t num, int64_t SC, int k, int lane) {
-  const int64_t SCk = SC * k, nx = num * ext;
-  for (int j = lane; j < k; j += 32) {
-    T.lo[j] = (int32_t)fdiv_fast(nx * j, SCk);
-    T.hi[j] = (int32_t)(cdiv_fast(nx * (j + 1), SCk) - 1);
-    T.flo[j] = (int32_t)fdiv_fast(num * blo[j], SC);
-    T.chi[j] = (int32_t)cdiv_fast(num * bhi[j], SC);
-  }
-}
-
-// Lane-parallel setup of the OBB constants (D11).  The box is
-// {Umin <= xC + yS <= Umax, Vmin <= -xS + yC <= Vmax}; with num/SC scaling:
-//  top    y_top(x)   = max((Umin - xC)/S, (Vmin + xS)/C)
-//  bottom y_bot(x)   = min((Umax - xC)/S, (Vmax + xS)/C)
-//  left   x_left(y)  = max((Umin - yS)/C, (yC - Vmax)/S)
-//  right  x_right(y) = min((Umax - yS)/C, (yC - Vmin)/S)
-__device__ void build_obb(ObbW& O, int64_t C, int64_t S, i128 UMN, i128 UXN, i128 VMN, i128 VXN,
-                          int64_t SC, int64_t nw, int64_t nh, int lane) {
-  const int64_t N2 = C * C + S * S, DS = S * SC, DC = C * SC;
-  const i128 N2SC = (i128)N2 * SC;
-  const int64_t SCS = SC * S, SCC = SC * C;
-  if (lane < 8) {
-    i128 A;
-    int64_t B, D;
-    switch (lane) {
-      case 0: A = VMN; B = SCS; D = DC; break;               // top, increasing line at P0
-      case 1: A = UMN - SCC; B = -SCC; D = DS; break;        // top, decreasing line at P1
-      case 2: A = -UXN; B = SCC; D = DS; break;              // bottom, decreasing at P0 (neg)
-      case 3: A = -VXN - SCS; B = -SCS; D = DC; break;       // bottom, increasing at P1 (neg)
-      case 4: A = -VXN; B = SCC; D = DS; break;              // left, increasing at Q0
-      case 5: A = UMN - SCS; B = -SCS; D = DC; break;        // left, decreasing at Q1
-      case 6: A = -UXN; B = SCS; D = DC; break;              // right, decreasing at Q0 (neg)
-      default: A = VMN - SCC; B = -SCC; D = DS; break;       // right, increasing at Q1 (neg)
-    }
-    O.lin[lane] = make_lindiv(A, B, D);
-  } else if (lane < 12) {
-    const int q = lane - 8;
-    int64_t v;
-    switch (q) {
-      case 0: v = fdiv_fast128(UMN - mul_wide(nw, C), (i128)DS); break;
-      case 1: v = cdiv_fast128(VXN + mul_wide(nw, S), (i128)DC); break;
-      case 2: v = fdiv_fast128(UMN - mul_wide(nh, S), (i128)DC); break;
-      default: v = cdiv_fast128(mul_wide(nh, C) - VMN, (i128)DS); break;
-    }
-    O.last[q] = v;
-  } else if (lane < 16) {
-    const int q = lane - 12;
-    int64_t v;
-    switch (q) {
-      case 0: v = fdiv_fast128((i128)S * UMN + (i128)C * VMN, N2SC); break;
-      case 1: v = cdiv_fast128((i128)S * UXN + (i128)C * VXN, N2SC); break;
-      case 2: v = fdiv_fast128((i128)C * UMN - (i128)S * VXN, N2SC); break;
-      default: v = cdiv_fast128((i128)C * UXN - (i128)S * VMN, N2SC); break;
-    }
-    O.star[q] = v;
-  } else if (lane < 20) {
-    const int q = lane - 16;
-    i128 cross;
-    switch (q) {
-      case 0: cross = (i128)C * UMN - (i128)S * VMN; break;   // x* of the top boundary
-      case 1: cross = (i128)C * UXN - (i128)S * VXN; break;   // x** of the bottom
-      case 2: cross = (i128)S * UMN + (i128)C * VXN; break;   // y* of the left
-      default: cross = (i128)S * UXN + (i128)C * VMN; break;  // y** of the right
-    }
-    O.iA[q] = fdiv_clamp128(cross, N2SC);
-    O.iB[q] = -fdiv_clamp128(-cross, N2SC) - 1;
-    O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
-  }
-}
-
-__global__ void __launch_bounds__(kWarps * 32, 2)
-profile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
-               const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
-               uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all, int32_t* cand_bad,
-               const Status* st) {
-  __shared__ SliceTab tabs[kWarps][2];
-  __shared__ ObbW obbs[kWarps];
+__global__ void __launch_bounds__(kWarps * 32)
+profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
+                   const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
+                   uint32_t* dcol, uint32_t* drow, const int32_t* __restrict__ big_list,
+                   const Status* st) {
+  __shared__ ChartK3 CH[kWarps];
+  extern __shared__ __align__(16) int32_t dyn[];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kWarps + wib;
-  if (item >= (int64_t)pp.n * pp.M) return;
-  const int m = (int)(item / pp.n) + 1;
-  const int s = (int)(item % pp.n);
-  const int c = perm[s];
-  const int64_t w = P.w[c], h = P.h[c];
   const int k = pp.k;
-  const int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
-  const int64_t nw = num * w, nh = num * h;
-  const int64_t ws = cdiv_fast(nw, SC), hs = cdiv_fast(nh, SC);
-  const int32_t Wd = (int32_t)(ws + 2 * pp.g), Hd = (int32_t)(hs + 2 * pp.g);
-  if (lane == 0) {
-    wd_all[(int64_t)(m - 1) * pp.n + s] = Wd;
-    hd_all[(int64_t)(m - 1) * pp.n + s] = Hd;
-  }
-  if (ws + 2 * pp.g > pp.Wp || hs + 2 * pp.g > pp.Hp) {  // cannot fit at this scale
-    if (lane == 0) cand_bad[m - 1] = 1;
-    return;
-  }
-  const int32_t* sl = P.sl + (int64_t)c * 4 * k;
-  const SliceTab* TT = tabs[wib];
-  build_tab(tabs[wib][0], sl, sl + k, w, num, SC, k, lane);
-  build_tab(tabs[wib][1], sl + 2 * k, sl + 3 * k, h, num, SC, k, lane);
-  const int j8 = P.obb_j[c];
-  ObbW& O = obbs[wib];
-  if (j8 != 0) {
-    const int64_t C = kQC[j8], S = kQS[j8];
-    const int64_t* ob = P.obb + 4 * (int64_t)c;
-    build_obb(O, C, S, mul_wide(ob[0], num), mul_wide(ob[1], num), mul_wide(ob[2], num),
-              mul_wide(ob[3], num), SC, nw, nh, lane);
-  }
-  __syncwarp();
-  uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
-  uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-  int jp = 0, ax_prev = 0;
-  for (int64_t e = lane; e < ws + hs; e += 32) {
-    const int ax = e >= ws ? 1 : 0;      // 0: column i (top/bottom), 1: row i (left/right)
-    const int64_t i = ax ? e - ws : e;
-    const int64_t cnt = ax ? hs : ws;
-    const SliceTab& T = TT[ax];
-    if (ax != ax_prev) { jp = 0; ax_prev = ax; }
-    while (T.hi[jp] < i) jp++;
-    int32_t lo = INT32_MAX, hi = INT32_MIN;
-    for (int j = jp; j < k && T.lo[j] <= i; j++) {
-      lo = min(lo, T.flo[j]);
-      hi = max(hi, T.chi[j]);
+  int32_t* tab = dyn + wib * 4 * k;
+  const int nbig = st->pad[1];
+  const int64_t SC = (int64_t)pp.M * TABI_UNITS;
+  const double rSC = 1.0 / (double)SC;
+  for (int it = blockIdx.x * kWarps + wib; it < nbig; it += gridDim.x * kWarps) {
+    const int item = big_list[it];
+    const int m = item / pp.n + 1, s = item % pp.n;
+    const int64_t num = m;
+    ChartK3& H = CH[wib];
+    if (lane == 0) {
+      const int c = perm[s];
+      H.s = s;
+      H.c = c;
+      H.nw = num * P.w[c];
+      H.nh = num * P.h[c];
+      H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
+      H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
+      H.rnw = 1.0 / (double)H.nw;
+      H.rnh = 1.0 / (double)H.nh;
+      H.j8 = P.obb_j[c];
     }
-    int64_t L = max(0, lo), H = min((int64_t)hi, ax ? ws : hs);
-    if (j8 != 0) {
-      const bool last = i == cnt - 1;
-      const int q0 = 2 * ax, q1 = 2 * ax + 1;
-      int64_t v;
-      if (i <= O.iA[q0] && (last ? O.lastB[q0] != 0 : i >= O.iB[q0])) v = O.star[q0];
-      else if (i > O.iA[q0]) v = lindiv_eval(O.lin[4 * ax + 0], i);
-      else v = last ? O.last[q0] : lindiv_eval(O.lin[4 * ax + 1], i);
-      L = max(L, v);
-      if (i <= O.iA[q1] && (last ? O.lastB[q1] != 0 : i >= O.iB[q1])) v = O.star[q1];
-      else if (i > O.iA[q1]) v = -lindiv_eval(O.lin[4 * ax + 2], i);
-      else v = last ? O.last[q1] : -lindiv_eval(O.lin[4 * ax + 3], i);
-      H = min(H, v);
+    __syncwarp();
+    if (lane < 8) chart_setup(H, tab, P, k, num, SC, lane);
+    __syncwarp();
+    uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
+    uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
+    for (int64_t e = lane; e < (int64_t)H.ws + H.hs; e += 32) {
+      const int ax = e >= H.ws;
+      const int64_t i = ax ? e - H.ws : e;
+      (ax ? row : col)[i + 2 * pp.g] = raw_cell(H, tab, k, ax, i, num, SC);
     }
-    (ax ? row : col)[i + 2 * pp.g] = (uint32_t)L | ((uint32_t)H << 16);
+    __syncwarp();
+    dilate_slot(col, H.ws, pp.g, lane);
+    dilate_slot(row, H.hs, pp.g, lane);
+    __syncwarp();
   }
-  __syncwarp();
-  dilate_slot(col, (int32_t)ws, pp.g, lane);
-  dilate_slot(row, (int32_t)hs, pp.g, lane);
 }
 
 __global__ void __launch_bounds__(kWarps * 32)
@@ -261,12 +406,20 @@ offsets_kernel(PackParams pp, const int32_t* __restrict__ rowofs, const uint32_t
 
 void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
-                     int32_t* wd, int32_t* hd, int32_t* cand_bad, const Status* st,
+                     int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
                      cudaStream_t s) {
-  const int64_t items = (int64_t)pp.n * pp.M;
-  const int blocks = (int)((items + kWarps - 1) / kWarps);
-  profile_kernel<<<blocks, kWarps * 32, 0, s>>>(P, perm, pp, colofs, rowofs, (uint32_t*)dcol,
-                                                 (uint32_t*)drow, wd, hd, cand_bad, st);
+  const size_t dyn = sizeof(int32_t) * (size_t)(kTC * 4 * pp.k) + sizeof(uint32_t) * kRaw;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(profile_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(int32_t) * (kTC * 4 * TABI_KMAX) + sizeof(uint32_t) * kRaw));
+    attr = true;
+  }
+  dim3 grid((pp.n + kTC - 1) / kTC, pp.M);
+  profile_tile_kernel<<<grid, kTT, dyn, s>>>(P, perm, pp, colofs, rowofs, (uint32_t*)dcol,
+                                             (uint32_t*)drow, wd, hd, cand_bad, big_list, st);
+  profile_big_kernel<<<296, kWarps * 32, sizeof(int32_t) * kWarps * 4 * pp.k, s>>>(
+      P, perm, pp, colofs, rowofs, (uint32_t*)dcol, (uint32_t*)drow, big_list, st);
 }
 
 void launch_offsets(const PackParams& pp, const int32_t* colofs, const int32_t* rowofs,

@@ -46,6 +46,7 @@ struct tabi_ctx {
   int32_t* off = nullptr;
   uint8_t* lockbits = nullptr;
   int32_t* cand_bad = nullptr;
+  int32_t* big_list = nullptr;  // (candidate, chart) items too large for K3's tile buffer
   int32_t* X = nullptr;
   int32_t* Y = nullptr;
   uint8_t* mir = nullptr;
@@ -86,7 +87,8 @@ static void dfree_all(tabi_ctx* ctx) {
                 ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
                 ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
-                ctx->lockbits, ctx->cand_bad, ctx->X, ctx->Y, ctx->mir, ctx->cands, ctx->dcol,
+                ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->X, ctx->Y, ctx->mir,
+                ctx->cands, ctx->dcol,
                 ctx->drow, ctx->scratch};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -170,6 +172,7 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
     CK(dalloc(&ctx->off, (size_t)M * N));
     CK(dalloc(&ctx->lockbits, (size_t)M * N));
     CK(dalloc(&ctx->cand_bad, (size_t)M));
+    CK(dalloc(&ctx->big_list, (size_t)M * N));
     CK(dalloc(&ctx->X, (size_t)M * N));
     CK(dalloc(&ctx->Y, (size_t)M * N));
     CK(dalloc(&ctx->mir, (size_t)M * N));
@@ -299,8 +302,9 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->d_status, s);
     CK(cudaMemsetAsync(ctx->cand_bad, 0, sizeof(int32_t) * M, s));
     launch_profiles(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
-                    (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->d_status, s);
-    launches += 2;
+                    (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
+                    ctx->d_status, s);
+    launches += 3;  // prep, K3 tiles, K3 large charts
     tm.mark(s);
     launch_offsets(pp, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
                    ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);

@@ -106,6 +106,28 @@ __device__ __forceinline__ LinDiv make_lindiv(i128 A, int64_t B, int64_t D) {
   L.rB = B - L.qB * D;
   return L;
 }
+// floor(a / b) for int64 a, b > 0 from a precomputed reciprocal (exact).
+__device__ __forceinline__ int64_t fdiv_r64(int64_t a, int64_t b, double rcp) {
+  int64_t q = (int64_t)floor((double)a * rcp);
+  int64_t r = a - q * b;
+  while (r < 0) { q--; r += b; }
+  while (r >= b) { q++; r -= b; }
+  return q;
+}
+// floor(a / b) for i128 a and i128 b > 0 from a reciprocal; result clamped to
+// [-2^40, 2^40] when clamp is set (for index comparisons).
+__device__ __forceinline__ int64_t fdiv_r128(i128 a, i128 b, double rcp, bool clamp) {
+  const double est = floor(i128_to_double(a) * rcp);
+  if (clamp) {
+    if (est > 1099511627776.0) return 1099511627776LL;
+    if (est < -1099511627776.0) return -1099511627776LL;
+  }
+  int64_t q = (int64_t)est;
+  i128 r = a - (i128)q * b;
+  while (r < 0) { q--; r += b; }
+  while (r >= b) { q++; r -= b; }
+  return q;
+}
 __device__ __forceinline__ int64_t lindiv_eval(const LinDiv& L, int64_t i) {
   const int64_t N = L.rA + i * L.rB;
   int64_t t = (int64_t)((double)N * L.rcp);
@@ -280,7 +302,7 @@ void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, in
                  int32_t* rowofs, int32_t* hsorted, Status* st, cudaStream_t s);
 void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
-                     int32_t* wd, int32_t* hd, int32_t* cand_bad, const Status* st,
+                     int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
                      cudaStream_t s);
 void launch_offsets(const PackParams& pp, const int32_t* colofs, const int32_t* rowofs,
                     const int16_t* drow, const int32_t* wd, const int32_t* hd, int32_t* off,

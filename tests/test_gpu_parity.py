@@ -143,6 +143,16 @@ def test_unsnapped_input_with_resolution(orc, ctx):
     _compare_pack(orc, ctx, cs2, res=(256.0, 256.0), check_profiles=3)
 
 
+def test_large_chart_path(orc, ctx):
+    """Charts whose footprint exceeds the K3 tile buffer (> 8192 cells) take the
+    warp-per-chart path; both must agree with the oracle."""
+    big = [[(0, 0), (300, 40), (260, 9000), (10, 8800)],
+           [(0, 0), (7000, 0), (7000, 2500), (3000, 2600), (0, 2500)]]
+    small = [chartgen.config1a(3).polygon(c).tolist() for c in range(10)]
+    cs = chartgen.from_polygons(big + small, 16384, 16384)
+    _compare_pack(orc, ctx, cs, check_profiles=4, scale_count=8)
+
+
 def test_lock1_both_modes(orc, ctx):
     A = [(0, 0), (20, 0), (20, 150), (0, 150)]
     c0 = [(0, 0), (10, 0), (10, 45), (40, 45), (40, 47), (10, 47), (10, 100), (0, 100)]

@@ -1,7 +1,7 @@
 """Minimal driver for ncu: W warm-up packs then one pack of the bench workload.
 
     python tools/profile_once.py [--workload C3] [--rho 0.5] [--warmup 3]
-Each pack launches 7 kernels (proxy, sort, prep, profile, offsets, pack, select).
+Each pack launches 8 kernels (proxy, sort, prep, profile tiles, profile large, offsets, pack, select).
 """
 import argparse
 import os
