@@ -137,7 +137,8 @@ typedef struct {
 } tabi_proxy_dbg;
 
 typedef struct {
-  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p, switched_at;
+  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p;
+  int32_t evaluated;              /* 0: skipped (above the area bound or below the winning wave) */
 } tabi_cand_dbg;
 
 tabi_status tabi_debug_proxies(tabi_ctx* ctx, tabi_proxy_dbg* out);   /* n_charts entries */

@@ -156,7 +156,8 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Smem S;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int m = blockIdx.x + 1;
+  const int m = wave_m(pp, st->pad[2], blockIdx.x);
+  if (m == 0) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   const int64_t cb = (int64_t)(m - 1) * n;
@@ -194,7 +195,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   W.prof_cap = prof_cap;
 
   if (cand_bad[m - 1]) {  // some chart exceeds the dilated atlas at this scale
-    if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, -1};
+    if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1};
     return;
   }
   {  // work accounting: footprint entries K3 produced for this candidate
@@ -595,7 +596,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
   if (lane == 0) atomicAdd(&st->work_pack, wk);
   if (tid == 0) {
-    cands[m - 1] = Cand{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, -1};
+    cands[m - 1] = Cand{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1};
   }
 }
 
@@ -654,7 +655,7 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
   const int f_words = (pp.Wp + 3) & ~3;
   const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 8 * (size_t)kRW);
   const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
-  pack_kernel<<<pp.M, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
+  pack_kernel<<<pp.B, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
                                              hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
                                              cands, st, prof_cap);
 }

@@ -10,17 +10,18 @@
 //
 // Work decomposition (tile kernel): one CTA takes kTC consecutive sorted
 // charts of one candidate.  Setup -- the per-(chart, candidate) constants --
-// is split into 8 uniform jobs per chart (every division a multiply by a
-// precomputed reciprocal plus an exact integer correction).  Then each thread
-// walks a contiguous run of the tile's flattened OUTPUT cells: one search per
-// run, raw cells computed in increasing order (monotone slice pointer, no
-// division), the Chebyshev window kept in a small per-thread ring in shared
-// memory, each dilated cell written once.  Charts with more than kBig raw
-// cells go to a compacted list handled warp-per-chart (same arithmetic).
+// is split into 8 uniform jobs per chart (no divergent lane groups, every
+// division a multiply by a precomputed reciprocal plus an exact integer
+// correction).  Then all threads walk the tile's flattened cells into a
+// shared-memory raw buffer and dilate from it into the HBM slots (coalesced).
+// Charts whose raw cells exceed the buffer go to a compacted list processed
+// by a warp-per-chart kernel (same arithmetic).
 //
-// Per raw cell: the local-AABB bound is the min/max over the 1-2 slices that
-// openly overlap it; the OBB bound is an integer compare of the cell index
-// with the crossing indices plus one int64 progression (LinDiv) per bound.
+// Per cell: the local-AABB bound takes min/max over the 1-2 slices that
+// openly overlap it (slice range by reciprocal multiply, per-slice scaled
+// floor/ceil from the setup tables); the OBB bound is an integer compare of
+// the cell index with the crossing indices plus one int64 progression
+// (LinDiv) per bound.
 //
 // K3b computes, per candidate and adjacent sorted pair, the horizontal
 // compaction advance (a max-reduction of profile gaps over shared
@@ -32,7 +33,7 @@ namespace {
 
 constexpr int kTC = 16;      // charts per tile
 constexpr int kTT = 128;     // threads per tile CTA (8 per chart during setup)
-constexpr int kBig = 8192;   // raw cells above which a chart takes the warp path
+constexpr int kRaw = 8192;   // raw cells per chunk (32 KB)
 constexpr int kWarps = 8;    // big-chart kernel: warps per CTA
 
 // Per-(chart, candidate) constants.  OBB index q = axis * 2 + (0 low, 1 high);
@@ -52,24 +53,16 @@ struct ChartK3 {
   int32_t s, c, ws, hs, j8, small;  // small: handled by the tile kernel
   int32_t col_o, row_o;             // slot offsets in dcol / drow (candidate base added)
   int64_t nw, nh;
+  double rnw, rnh;                  // 1 / (num * w), 1 / (num * h)
   ObbC O;
 };
 
 // ---- setup jobs ---------------------------------------------------------
-// Slice table entry (4 ints): first/last texel cell the slice openly
-// overlaps, scaled floor of its low bound, scaled ceil of its high bound.
-// Slice j spans [j*ext/k, (j+1)*ext/k] (units) = scaled [num*j*ext/(SC*k),
-// num*(j+1)*ext/(SC*k)]; it openly overlaps cell t iff num*j*ext < (t+1)*SC*k
-// and num*(j+1)*ext > t*SC*k, i.e. t in [floor(num*j*ext/(SC*k)),
-// ceil(num*(j+1)*ext/(SC*k)) - 1].
-__device__ __forceinline__ void slice_job(int32_t* tab, const int32_t* blo, const int32_t* bhi,
-                                          int j, int64_t nx, int k, int64_t num, int64_t SC,
-                                          double rSC, double rSCk) {
-  const int64_t SCk = SC * k;
-  tab[4 * j] = (int32_t)fdiv_r64(nx * j, SCk, rSCk);
-  tab[4 * j + 1] = (int32_t)(-fdiv_r64(-nx * (j + 1), SCk, rSCk) - 1);
-  tab[4 * j + 2] = (int32_t)fdiv_r64(num * blo[j], SC, rSC);
-  tab[4 * j + 3] = (int32_t)(-fdiv_r64(-num * bhi[j], SC, rSC));
+// Slice entry: scaled floor of the low bound / ceil of the high bound.
+__device__ __forceinline__ void slice_job(int32_t* tab, const int32_t* blo, const int32_t* bhi, int j,
+                                          int64_t num, int64_t SC, double rSC) {
+  tab[2 * j] = (int32_t)fdiv_r64(num * blo[j], SC, rSC);
+  tab[2 * j + 1] = (int32_t)(-fdiv_r64(-num * bhi[j], SC, rSC));
 }
 
 // OBB job r (0..7) of a chart: LinDiv r, one of last/star, one of iA/iB.  The
@@ -142,35 +135,22 @@ __device__ void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i128 UXN
   }
 }
 
-// Setup of one chart by 8 cooperating threads r = 0..7.
-__device__ void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, int64_t num,
-                            int64_t SC, int r) {
-  const int c = H.c;
-  const int32_t* sl = P.sl + (int64_t)c * 4 * k;
-  const double rSC = 1.0 / (double)SC, rSCk = 1.0 / (double)(SC * k);
-  for (int idx = r; idx < 2 * k; idx += 8) {
-    const int ax = idx >= k, j = ax ? idx - k : idx;
-    slice_job(tab + ax * 4 * k, sl + 2 * ax * k, sl + 2 * ax * k + k, j, ax ? H.nh : H.nw, k,
-              num, SC, rSC, rSCk);
-  }
-  if (H.j8 != 0) {
-    const int64_t* ob = P.obb + 4 * (int64_t)c;
-    obb_job(H.O, r, kQC[H.j8], kQS[H.j8], mul_wide(ob[0], num), mul_wide(ob[1], num),
-            mul_wide(ob[2], num), mul_wide(ob[3], num), SC, H.nw, H.nh);
-  }
-}
-
 // Raw (undilated) bounds of cell i on axis ax (0: column -> (Top, Bottom),
-// 1: row -> (Left, Right)), packed lo | hi << 16.  jp: slice pointer, valid
-// for non-decreasing i within one (chart, axis).
+// 1: row -> (Left, Right)), packed lo | hi << 16.
 __device__ __forceinline__ uint32_t raw_cell(const ChartK3& H, const int32_t* tab, int k, int ax,
-                                             int64_t i, int& jp) {
-  const int32_t* t = tab + ax * 4 * k;
-  while (t[4 * jp + 1] < i) jp++;
+                                             int64_t i, int64_t num, int64_t SC) {
+  const int64_t nx = ax ? H.nh : H.nw;
+  const double rnx = ax ? H.rnh : H.rnw;
+  const int64_t SCk = SC * k;
+  int64_t jl = fdiv_r64(i * SCk, nx, rnx);
+  int64_t jh = -fdiv_r64(-(i + 1) * SCk, nx, rnx) - 1;
+  if (jl < 0) jl = 0;
+  if (jh > k - 1) jh = k - 1;
+  const int32_t* t = tab + ax * 2 * k;
   int32_t lo = INT32_MAX, hi = INT32_MIN;
-  for (int j = jp; j < k && t[4 * j] <= i; j++) {
-    lo = min(lo, t[4 * j + 2]);
-    hi = max(hi, t[4 * j + 3]);
+  for (int64_t j = jl; j <= jh; j++) {
+    lo = min(lo, t[2 * j]);
+    hi = max(hi, t[2 * j + 1]);
   }
   const int64_t cnt = ax ? H.hs : H.ws;
   int64_t L = max(0, lo), Hh = min((int64_t)hi, ax ? (int64_t)H.ws : (int64_t)H.hs);
@@ -191,16 +171,21 @@ __device__ __forceinline__ uint32_t raw_cell(const ChartK3& H, const int32_t* ta
   return (uint32_t)L | ((uint32_t)Hh << 16);
 }
 
-// first slice whose cell range ends at or after cell i (binary search)
-__device__ __forceinline__ int slice_ptr(const int32_t* tab, int k, int ax, int64_t i) {
-  const int32_t* t = tab + ax * 4 * k;
-  int lo = 0, hi = k - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (t[4 * mid + 1] < i) lo = mid + 1;
-    else hi = mid;
+// Setup of one chart by 8 cooperating threads r = 0..7 (rank r).
+__device__ void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, int64_t num,
+                            int64_t SC, int r) {
+  const int c = H.c;
+  const int32_t* sl = P.sl + (int64_t)c * 4 * k;
+  const double rSC = 1.0 / (double)SC;
+  for (int idx = r; idx < 2 * k; idx += 8) {
+    const int ax = idx >= k, j = ax ? idx - k : idx;
+    slice_job(tab + ax * 2 * k, sl + 2 * ax * k, sl + 2 * ax * k + k, j, num, SC, rSC);
   }
-  return lo;
+  if (H.j8 != 0) {
+    const int64_t* ob = P.obb + 4 * (int64_t)c;
+    obb_job(H.O, r, kQC[H.j8], kQS[H.j8], mul_wide(ob[0], num), mul_wide(ob[1], num),
+            mul_wide(ob[2], num), mul_wide(ob[3], num), SC, H.nw, H.nh);
+  }
 }
 
 __global__ void __launch_bounds__(kTT, 4)
@@ -209,22 +194,24 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
                     uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all,
                     int32_t* cand_bad, int32_t* big_list, Status* st) {
   __shared__ ChartK3 CH[kTC];
-  __shared__ int32_t opre[kTC + 1];
+  __shared__ int32_t cells[kTC], cpre[kTC + 1], opre[kTC + 1];
+  __shared__ int32_t chunk_end;
   extern __shared__ __align__(16) int32_t dyn[];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int k = pp.k, g = pp.g, R = 2 * g + 1;
-  int32_t* tabs = dyn;                                      // [kTC][2 axes][k][4]
-  uint32_t* ring = (uint32_t*)(dyn + kTC * 8 * k) + threadIdx.x * R;  // per-thread window
+  const int k = pp.k;
+  int32_t* tabs = dyn;                          // [kTC][2 axes][k][2]
+  uint32_t* raw = (uint32_t*)(dyn + kTC * 4 * k);
   const int tid = threadIdx.x;
-  const int m = blockIdx.y + 1;
+  const int m = wave_m(pp, st->pad[2], blockIdx.y);
+  if (m == 0) return;
   const int s0 = blockIdx.x * kTC;
   const int nt = min(kTC, pp.n - s0);
   const int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
   const double rSC = 1.0 / (double)SC;
-  const int ci0 = tid >> 3, r = tid & 7;
-  if (ci0 < nt && r == 0) {
-    ChartK3& H = CH[ci0];
-    const int s = s0 + ci0;
+  const int ci = tid >> 3, r = tid & 7;
+  if (ci < nt && r == 0) {
+    ChartK3& H = CH[ci];
+    const int s = s0 + ci;
     const int c = perm[s];
     const int64_t w = P.w[c], h = P.h[c];
     H.s = s;
@@ -233,91 +220,89 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
     H.nh = num * h;
     H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
     H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
+    H.rnw = 1.0 / (double)H.nw;
+    H.rnh = 1.0 / (double)H.nh;
     H.j8 = P.obb_j[c];
     const int64_t b = (int64_t)(m - 1) * pp.n + s;
-    wd_all[b] = H.ws + 2 * g;
-    hd_all[b] = H.hs + 2 * g;
-    const bool fits = H.ws + 2 * g <= pp.Wp && H.hs + 2 * g <= pp.Hp;
+    wd_all[b] = H.ws + 2 * pp.g;
+    hd_all[b] = H.hs + 2 * pp.g;
+    const bool fits = H.ws + 2 * pp.g <= pp.Wp && H.hs + 2 * pp.g <= pp.Hp;
     if (!fits) cand_bad[m - 1] = 1;
-    H.small = fits && (H.ws + H.hs <= kBig);
+    H.small = fits && (H.ws + H.hs <= kRaw);
     if (fits && !H.small) big_list[atomicAdd(&st->pad[1], 1)] = (m - 1) * pp.n + s;
     H.col_o = colofs[s];
     H.row_o = rowofs[s];
+    cells[ci] = H.small ? H.ws + H.hs : 0;
   }
   __syncthreads();
-  if (ci0 < nt && CH[ci0].small) chart_setup(CH[ci0], tabs + ci0 * 8 * k, P, k, num, SC, r);
-  if (tid == 0) {
-    int32_t acc = 0;
-    opre[0] = 0;
-    for (int ci = 0; ci < nt; ci++) {
-      acc += CH[ci].small ? CH[ci].ws + CH[ci].hs + 4 * g : 0;
-      opre[ci + 1] = acc;
-    }
-  }
+  if (ci < nt && CH[ci].small) chart_setup(CH[ci], tabs + ci * 4 * k, P, k, num, SC, r);
   __syncthreads();
   uint32_t* colb = dcol + (int64_t)(m - 1) * pp.col_cap;
   uint32_t* rowb = drow + (int64_t)(m - 1) * pp.row_cap;
-  // this thread's run of flattened output cells [o, o1)
-  const int32_t T = opre[nt];
-  const int32_t Cn = (T + kTT - 1) / kTT;
-  int32_t o = tid * Cn;
-  const int32_t o1 = min(T, o + Cn);
-  if (o >= o1) return;
-  int ci = 0;
-  {
-    int lo = 0, hi = nt - 1;
-    while (lo < hi) {  // last chart whose outputs start at or before o
-      const int mid = (lo + hi + 1) >> 1;
-      if (opre[mid] <= o) lo = mid;
-      else hi = mid - 1;
-    }
-    ci = lo;
-  }
-  while (o < o1) {
-    const ChartK3& H = CH[ci];
-    const int32_t* tab = tabs + ci * 8 * k;
-    const int32_t Wd = H.ws + 2 * g;
-    const int32_t lo_local = o - opre[ci];
-    const int ax = lo_local >= Wd;
-    const int32_t i0 = ax ? lo_local - Wd : lo_local;
-    const int32_t cnt = ax ? H.hs : H.ws;
-    const int32_t iend = min(cnt + 2 * g, i0 + (o1 - o));
-    uint32_t* out = ax ? rowb + H.row_o : colb + H.col_o;
-    // raw cells are pushed in increasing order into the ring; cell q sits at q % R
-    const int32_t qs = max(0, i0 - 2 * g);
-    int jp = slice_ptr(tab, k, ax, qs);
-    int32_t q = qs;           // next raw cell to compute
-    int rpos = qs % R;        // ring slot of cell q
-    for (int32_t i = i0; i < iend; i++) {
-      const int32_t qlast = min(i, cnt - 1);
-      while (q <= qlast) {
-        ring[rpos] = raw_cell(H, tab, k, ax, q, jp);
-        q++;
-        if (++rpos == R) rpos = 0;
+  const int g = pp.g;
+  for (int cb = 0; cb < nt;) {
+    if (tid == 0) {  // chunk [cb, ce): raw cells fit the buffer
+      int e = cb, tot = 0, otot = 0;
+      cpre[0] = 0;
+      opre[0] = 0;
+      while (e < nt && tot + cells[e] <= kRaw) {
+        tot += cells[e];
+        otot += cells[e] ? cells[e] + 4 * g : 0;
+        e++;
+        cpre[e - cb] = tot;
+        opre[e - cb] = otot;
       }
-      // window: cells [max(0, i - 2g), qlast] are the most recent ones
-      const int nv = qlast - max(0, i - 2 * g) + 1;
-      int p = rpos;
+      chunk_end = e;
+    }
+    __syncthreads();
+    const int ce = chunk_end, nc = ce - cb;
+    const int32_t ncell = cpre[nc], nout = opre[nc];
+    // raw pass over the chunk's flattened cells
+    for (int e = tid; e < ncell; e += kTT) {
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cpre[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const ChartK3& H = CH[cb + lo];
+      const int32_t x = e - cpre[lo];
+      const int ax = x >= H.ws;
+      raw[e] = raw_cell(H, tabs + (cb + lo) * 4 * k, k, ax, ax ? x - H.ws : x, num, SC);
+    }
+    __syncthreads();
+    // dilation pass over the chunk's flattened outputs (Wd columns, Hd rows)
+    for (int o = tid; o < nout; o += kTT) {
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (opre[mid] <= o) lo = mid;
+        else hi = mid - 1;
+      }
+      const ChartK3& H = CH[cb + lo];
+      const int32_t y = o - opre[lo];
+      const int Wd = H.ws + 2 * g;
+      const int ax = y >= Wd;
+      const int32_t i = ax ? y - Wd : y;
+      const int32_t n0 = ax ? H.hs : H.ws;
+      const uint32_t* rr = raw + cpre[lo] + (ax ? H.ws : 0);
+      const int q0 = max(0, i - 2 * g), q1 = min(i, n0 - 1);
       int32_t vl = INT32_MAX, vh = INT32_MIN;
-      for (int t = 0; t < nv; t++) {
-        if (--p < 0) p = R - 1;
-        const uint32_t v = ring[p];
+      for (int q = q0; q <= q1; q++) {
+        const uint32_t v = rr[q];
         vl = min(vl, lo16(v));
         vh = max(vh, hi16(v));
       }
-      out[i] = (uint32_t)vl | ((uint32_t)(vh + 2 * g) << 16);
+      (ax ? rowb + H.row_o : colb + H.col_o)[i] = (uint32_t)vl | ((uint32_t)(vh + 2 * g) << 16);
     }
-    o += iend - i0;
-    if (o < o1) {
-      if (ax == 1 || iend < cnt + 2 * g) {
-        ci++;
-        while (ci < nt && opre[ci + 1] == opre[ci]) ci++;  // charts handled elsewhere
-      }
-    }
+    __syncthreads();
+    cb = ce;
+    while (cb < nt && cells[cb] == 0) cb++;  // skip charts handled elsewhere
+    __syncthreads();
   }
 }
 
-// Warp per large chart (raw cells > kBig) from the compacted list; raw values
+// Warp per large chart (raw cells > kRaw) from the compacted list; raw values
 // go straight into the HBM slot, then an in-place dilation.
 __device__ void dilate_slot(uint32_t* slot, int32_t n0, int32_t g, int lane) {
   const int32_t nd = n0 + 2 * g;
@@ -348,7 +333,7 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int k = pp.k;
-  int32_t* tab = dyn + wib * 8 * k;
+  int32_t* tab = dyn + wib * 4 * k;
   const int nbig = st->pad[1];
   const int64_t SC = (int64_t)pp.M * TABI_UNITS;
   const double rSC = 1.0 / (double)SC;
@@ -365,6 +350,8 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
       H.nh = num * P.h[c];
       H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
       H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
+      H.rnw = 1.0 / (double)H.nw;
+      H.rnh = 1.0 / (double)H.nh;
       H.j8 = P.obb_j[c];
     }
     __syncwarp();
@@ -372,9 +359,11 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
     __syncwarp();
     uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
     uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-    int jp0 = 0, jp1 = 0;
-    for (int64_t i = lane; i < H.ws; i += 32) col[i + 2 * pp.g] = raw_cell(H, tab, k, 0, i, jp0);
-    for (int64_t i = lane; i < H.hs; i += 32) row[i + 2 * pp.g] = raw_cell(H, tab, k, 1, i, jp1);
+    for (int64_t e = lane; e < (int64_t)H.ws + H.hs; e += 32) {
+      const int ax = e >= H.ws;
+      const int64_t i = ax ? e - H.ws : e;
+      (ax ? row : col)[i + 2 * pp.g] = raw_cell(H, tab, k, ax, i, num, SC);
+    }
     __syncwarp();
     dilate_slot(col, H.ws, pp.g, lane);
     dilate_slot(row, H.hs, pp.g, lane);
@@ -390,8 +379,9 @@ offsets_kernel(PackParams pp, const int32_t* __restrict__ rowofs, const uint32_t
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (item >= (int64_t)pp.n * pp.M) return;
-  const int m = (int)(item / pp.n) + 1;
+  if (item >= (int64_t)pp.n * pp.B) return;
+  const int m = wave_m(pp, st->pad[2], (int)(item / pp.n));
+  if (m == 0) return;
   const int s = (int)(item % pp.n);
   if (cand_bad[m - 1]) return;
   const int64_t base = (int64_t)(m - 1) * pp.n;
@@ -420,17 +410,17 @@ void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
                      int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
                      cudaStream_t s) {
-  const size_t dyn = sizeof(int32_t) * ((size_t)kTC * 8 * pp.k + (size_t)kTT * (2 * pp.g + 1));
+  const size_t dyn = sizeof(int32_t) * (size_t)(kTC * 4 * pp.k) + sizeof(uint32_t) * kRaw;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(profile_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(int32_t) * (kTC * 8 * TABI_KMAX + kTT * (2 * 64 + 1))));
+                         (int)(sizeof(int32_t) * (kTC * 4 * TABI_KMAX) + sizeof(uint32_t) * kRaw));
     attr = true;
   }
-  dim3 grid((pp.n + kTC - 1) / kTC, pp.M);
+  dim3 grid((pp.n + kTC - 1) / kTC, pp.B);
   profile_tile_kernel<<<grid, kTT, dyn, s>>>(P, perm, pp, colofs, rowofs, (uint32_t*)dcol,
                                              (uint32_t*)drow, wd, hd, cand_bad, big_list, st);
-  profile_big_kernel<<<296, kWarps * 32, sizeof(int32_t) * kWarps * 8 * pp.k, s>>>(
+  profile_big_kernel<<<296, kWarps * 32, sizeof(int32_t) * kWarps * 4 * pp.k, s>>>(
       P, perm, pp, colofs, rowofs, (uint32_t*)dcol, (uint32_t*)drow, big_list, st);
 }
 
@@ -439,7 +429,7 @@ void launch_offsets(const PackParams& pp, const int32_t* colofs, const int32_t* 
                     uint8_t* lockbits, const int32_t* cand_bad, const Status* st,
                     cudaStream_t s) {
   (void)colofs;
-  const int64_t items = (int64_t)pp.n * pp.M;
+  const int64_t items = (int64_t)pp.n * pp.B;
   const int blocks = (int)((items + kWarps - 1) / kWarps);
   offsets_kernel<<<blocks, kWarps * 32, 0, s>>>(pp, rowofs, (const uint32_t*)drow, wd, hd, off,
                                                  lockbits, cand_bad, st);

@@ -134,10 +134,36 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
 // row slot = min(ceil(h/256) + 2g, H') -- the footprint at the largest scale
 // (m = M, scale 1) bounds every candidate's (w_s is monotone in m).
 __global__ void __launch_bounds__(kT, 1)
-prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int32_t* perm,
-            PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted, Status* st) {
+prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int64_t* area2,
+            const int32_t* perm, PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
+            Status* st) {
   __shared__ int32_t sh[2][kW + 1];
+  __shared__ unsigned long long asum[2][kW];
   if (st->bad_chart != INT32_MAX) return;
+  // Area bound on the candidate scales: the packed charts are disjoint and
+  // inside the atlas, so (m/M)^2 * sum(area) <= W*H for any candidate that can
+  // succeed; in units (2*area, 1/256 texel): m^2 * A2 <= 2 * 65536 * W * H * M^2.
+  {
+    i128 a = 0;
+    for (int i = threadIdx.x; i < pp.n; i += kT) a += area2[i];
+    a = warp_sum128(a);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+      asum[0][wid] = (unsigned long long)(uint64_t)a;
+      asum[1][wid] = (unsigned long long)(uint64_t)(a >> 64);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      i128 tot = 0;
+      for (int w = 0; w < kW; w++)
+        tot += (i128)(((unsigned __int128)asum[1][w] << 64) | asum[0][w]);
+      const i128 rhs = (i128)2 * 65536 * pp.W * pp.H * (i128)pp.M * pp.M;
+      int m_hi = 0;
+      for (int m = pp.M; m >= 1; m--)
+        if ((i128)m * m * tot <= rhs) { m_hi = m; break; }
+      st->pad[2] = m_hi;
+    }
+  }
   int32_t carry_c = 0, carry_r = 0;
   for (int t0 = 0; t0 < pp.n; t0 += kT) {
     const int s = t0 + threadIdx.x;
@@ -176,7 +202,7 @@ void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, i
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, Status* st, cudaStream_t s) {
-  prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, perm, pp, colofs, rowofs, hsorted, st);
+  prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, st);
 }
 
 }  // namespace tabi

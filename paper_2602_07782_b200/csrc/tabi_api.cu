@@ -296,15 +296,31 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   launches++;
   tm.mark(s);
   tabi_placement* d_out = on_device ? out : ctx->d_out;
-  for (int attempt = 0; attempt < 6; attempt++) {
+  // Candidate waves: prep_kernel computes the area
+  // bound m_hi (every m above it must fail); wave w evaluates m_hi - w*B - j,
+  // j < B, all in parallel.  The first wave containing a success holds the
+  // largest successful m, so later waves are skipped -- the result equals the
+  // exhaustive search.  A further wave costs one host round trip.
+  const char* wenv = getenv("TABI_WAVE");
+  int B = wenv ? atoi(wenv) : 16;
+  if (B < 1 || B > M) B = M;
+  pp.B = B;
+  int wave = 0;
+  for (int attempt = 0; attempt < 64; attempt++) {
     pp.col_cap = ctx->col_cap;
     pp.row_cap = ctx->row_cap;
-    launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->d_status, s);
+    pp.wave = wave;
+    if (wave == 0) {
+      launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->d_status, s);
+      launches++;
+      CK(cudaMemsetAsync(ctx->cands, 0, sizeof(Cand) * M, s));
+    }
     CK(cudaMemsetAsync(ctx->cand_bad, 0, sizeof(int32_t) * M, s));
+    CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));  // large-chart list
     launch_profiles(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
                     (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
                     ctx->d_status, s);
-    launches += 3;  // prep, K3 tiles, K3 large charts
+    launches += 2;  // K3 tiles, K3 large charts
     tm.mark(s);
     launch_offsets(pp, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
                    ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
@@ -328,7 +344,12 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
       if (info) info->bad_chart = st.bad_chart;
       return TABI_EINVAL;
     }
-    if (!st.capacity) break;
+    if (!st.capacity) {
+      if (st.winner > 0 || st.pad[2] - (wave + 1) * B < 1) break;  // found, or no candidates left
+      wave++;
+      continue;
+    }
+    wave = 0;
     // grow and retry from the slot layout (proxies and order are kept)
     bool cols = false, pairs = false;
     if (st.capacity & 1) {
@@ -346,7 +367,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     *ctx->h_status = again;
     CK(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, s));
     tm.n = 3;  // re-time the retried stages
-    if (attempt == 5) return TABI_ECAPACITY;
+    if (attempt >= 8) return TABI_ECAPACITY;
   }
   ctx->last_n = n;
   ctx->last_M = M;
@@ -446,9 +467,13 @@ extern "C" tabi_status tabi_debug_profile(tabi_ctx* ctx, int32_t m, int32_t s, i
   CK(cudaMemcpy(&co, ctx->colofs + s, 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&ro, ctx->rowofs + s, 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&bad, ctx->cand_bad + (m - 1), 4, cudaMemcpyDeviceToHost));
+  Cand cd;
+  CK(cudaMemcpy(&cd, ctx->cands + (m - 1), sizeof(Cand), cudaMemcpyDeviceToHost));
   wd_hd[0] = Wd;
   wd_hd[1] = Hd;
-  if (bad) return TABI_NO_FIT;  // candidate skipped (a chart exceeds the atlas)
+  // candidate not evaluated (outside the searched waves) or skipped because a
+  // chart exceeds the atlas at this scale: no footprints
+  if (bad || !cd.evaluated) return TABI_NO_FIT;
   uint32_t* c = new uint32_t[Wd];
   uint32_t* r = new uint32_t[Hd];
   cudaMemcpy(c, ctx->dcol + (int64_t)(m - 1) * ctx->col_cap + co, 4 * (size_t)Wd, cudaMemcpyDeviceToHost);

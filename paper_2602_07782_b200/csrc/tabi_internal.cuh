@@ -281,14 +281,22 @@ struct Status {       // device-side status block, copied back once per pack
 
 // Per-candidate result record (mirrors tabi_cand_dbg).
 struct Cand {
-  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p, switched_at;
+  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p, evaluated;
 };
 
 struct PackParams {
   int32_t n, k, M, g, W, H, Wp, Hp;
   uint32_t flags;
+  int32_t wave, B;            // candidate wave: m = m_hi - wave * B - j, j < B
   int64_t col_cap, row_cap;   // per-candidate footprint slot capacity (entries)
 };
+
+// Candidate j of the current wave (0 if below 1).  m_hi = st->pad[2] is the
+// area bound computed by prep_kernel.
+__host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_hi, int j) {
+  const int m = m_hi - pp.wave * pp.B - j;
+  return m >= 1 ? m : 0;
+}
 
 }  // namespace tabi
 

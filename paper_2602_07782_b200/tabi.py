@@ -58,7 +58,7 @@ PROXY_DTYPE = np.dtype([("w", "<i4"), ("h", "<i4"), ("area2", "<i8"), ("xmin", "
                         ("reserved", "<i4"), ("umin", "<i8"), ("umax", "<i8"), ("vmin", "<i8"),
                         ("vmax", "<i8")])
 CAND_DTYPE = np.dtype([(f, "<i4") for f in ("success", "score", "rows", "knees_found",
-                                            "knee_rows", "prefix_rows", "p", "switched_at")])
+                                            "knee_rows", "prefix_rows", "p", "evaluated")])
 
 _lib = None
 

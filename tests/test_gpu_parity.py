@@ -52,8 +52,16 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
     assert np.array_equal(ctx.perm(n), perm_o)
     # per-candidate outcomes
     gc = ctx.candidates(M)
+    # the GPU evaluates candidate waves below the area bound; every
+    # evaluated candidate must agree with the exhaustive oracle, and the winner is
+    # the oracle's largest successful m
+    assert gc["evaluated"].sum() >= 1
+    assert info_g.scale_index == max(m for m in range(1, M + 1) if cands_o[m - 1].success)
     for m in range(1, M + 1):
         co = cands_o[m - 1]
+        if not gc["evaluated"][m - 1]:
+            assert m < info_g.scale_index or not co.success, m
+            continue
         assert gc["success"][m - 1] == co.success, m
         if co.success:
             for f in ("score", "rows", "knees_found", "knee_rows"):
@@ -71,7 +79,8 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
         rng = chartgen.SplitMix64(n * 7 + M)
         ms = sorted({M, info_o.scale_index, max(1, M // 3), rng.randint(1, M)})
         for m in ms:
-            if not gc["success"][m - 1] and not cands_o[m - 1].success:
+            if not gc["evaluated"][m - 1] or (not gc["success"][m - 1]
+                                                 and not cands_o[m - 1].success):
                 continue
             off_g, lk_g = ctx.offsets(m, n)
             ss = sorted({0, n - 1, *[rng.randint(0, n - 1) for _ in range(check_profiles)]})
@@ -141,6 +150,15 @@ def test_unsnapped_input_with_resolution(orc, ctx):
     xy = (cs.xy / 256.0 + rng.uniform(-1e-4, 1e-4, cs.xy.shape)).astype(np.float32)
     cs2 = chartgen.ChartSet("uv01", xy, cs.start, 256, 256)
     _compare_pack(orc, ctx, cs2, res=(256.0, 256.0), check_profiles=3)
+
+
+@pytest.mark.parametrize("wave", ["1", "3", "256"])
+def test_wave_sizes(orc, ctx, wave, monkeypatch):
+    """Candidate waves of any size give the exhaustive result: 1 = one candidate
+    per wave (many host round trips), 256 = all candidates at once."""
+    monkeypatch.setenv("TABI_WAVE", wave)
+    for cs in (chartgen.config1b(2), chartgen.small_case(4, n=60, family="mixed", rho=1.3)):
+        _compare_pack(orc, ctx, cs, check_profiles=3)
 
 
 def test_large_chart_path(orc, ctx):

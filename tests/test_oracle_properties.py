@@ -47,6 +47,24 @@ def test_validity_and_search_consistency(orc, cs):
     assert set(pl["scale_num"].tolist()) == {info.scale_index}
 
 
+@pytest.mark.parametrize("cs", corpus()[::3], ids=lambda c: c.name)
+def test_area_bound_prunes_only_failures(orc, cs):
+    """The CUDA path skips candidates whose scaled total chart area exceeds the
+    atlas (DESIGN.md scale search).  That is exact: every such candidate fails in
+    the exhaustive oracle, because successful packings are overlap-free and in
+    bounds (validator)."""
+    st, pl, info, cands = orc.pack(cs, with_cands=True)
+    a2 = 0
+    for c in range(cs.n_charts):
+        q = _snapped(cs.polygon(c))
+        a2 += abs(sum(q[i][0] * q[(i + 1) % len(q)][1] - q[(i + 1) % len(q)][0] * q[i][1]
+                      for i in range(len(q))))
+    M = cs.scale_count
+    for m in range(1, M + 1):
+        if m * m * a2 > 2 * 65536 * cs.atlas_w * cs.atlas_h * M * M:
+            assert not cands[m - 1].success, m
+
+
 def test_determinism(orc):
     cs = chartgen.small_case(3, n=60, family="uv")
     a = orc.pack(cs)
