@@ -583,6 +583,107 @@ static void eval_config(or_config* cf, const or_prof* pr, const int32_t* wd, con
     if (cf->F[x] > cf->score_knee) cf->score_knee = cf->F[x];
 }
 
+/* ---- D24 prefix-sum tail ("Performance Optimization") --------
+ * Remaining sorted charts [r0, n) at candidate m: FastAtlas-style fold of the
+ * prefix sum of the horizontal OFFSETS (HC always on), rows cut at
+ * multiples of W'; one global intermediate downscale s' = p / 2^20 (P:141
+ * "all charts must undergo an intermediate scaling-down") re-rasterized and
+ * re-laid per row until every row fits (at most 8 adjustments); rows placed
+ * with the fixed FastAtlas alternation, one left-to-right row then two
+ * right-to-left rows, pushed with locks, no knees.
+ * Returns 1 on success (F, X, Y, mir, pr_tail filled for [r0, n)). */
+static int prefix_tail(const or_proxy* px, const int32_t* perm, int32_t n, int32_t r0, int32_t m,
+                       const or_spec* spec, const or_prof* pr, const int32_t* off, int32_t* F,
+                       int32_t* X, int32_t* Y, uint8_t* mir, or_prof* pt, or_cand* cand) {
+  const int32_t g = spec->gutter, M = spec->scale_count;
+  const int64_t Wp = spec->atlas_w + 2 * g, Hp = spec->atlas_h + 2 * g;
+  const int64_t P20 = (int64_t)1 << 20;
+  /* step 1: prefix sum of offsets at scale m, rows = floor(start / W') */
+  int32_t* q = malloc(sizeof(int32_t) * n);
+  int64_t start = 0, Emax = 0, row_first_start = 0;
+  for (int32_t c = r0; c < n; c++) {
+    q[c] = (int32_t)(start / Wp);
+    if (c == r0 || q[c] != q[c - 1]) row_first_start = start;
+    int64_t e = start - row_first_start + pr[c].Wd;
+    if (e > Emax) Emax = e;
+    if (c + 1 < n) start += off[c];
+  }
+  /* step 2: global intermediate scale p / 2^20 = (m / M) * sigma with
+   * sigma = min(1, W' / Emax) -- an intermediate DOWNscaling (
+   * DESIGN.md reading R3 caps sigma at 1) */
+  int64_t p = ((i128)m * P20 * Wp) / ((i128)M * Emax);
+  const int64_t pm = ((i128)m * P20) / M;
+  if (p > pm) p = pm;
+  int32_t* xl = malloc(sizeof(int32_t) * n);
+  int ok = 0;
+  for (int iter = 0; iter <= 8; iter++) {
+    if (p < 1) break;
+    for (int32_t c = r0; c < n; c++) {
+      or_prof_free(&pt[c]);
+      or_profile(&px[perm[c]], p, P20, g, &pt[c]);
+    }
+    int64_t E2 = 0;
+    for (int32_t c = r0; c < n; c++) {
+      xl[c] = (c == r0 || q[c] != q[c - 1]) ? 0 : xl[c - 1] + or_offset(&pt[c - 1], &pt[c]);
+      if (xl[c] + pt[c].Wd > E2) E2 = xl[c] + pt[c].Wd;
+    }
+    if (E2 <= Wp) { ok = 1; break; }
+    if (iter == 8) break;
+    p = (p * Wp) / E2;
+  }
+  cand->p = (int32_t)p;
+  cand->switched_at = r0;
+  if (!ok) { free(q); free(xl); return 0; }
+  /* steps 3-4: rows in order, L->R iff row index % 3 == 0, push with locks */
+  int32_t row_idx = 0;
+  int32_t cap = 1, np;
+  int32_t *qa = malloc(sizeof(int32_t)), *qb = malloc(sizeof(int32_t));
+  int32_t *la = malloc(sizeof(int32_t)), *lb = malloc(sizeof(int32_t));
+  for (int32_t a = r0; a < n;) {
+    int32_t b = a;
+    while (b + 1 < n && q[b + 1] == q[a]) b++;
+    const int dir = (row_idx % 3 == 0) ? 0 : 1;
+    for (int32_t c = a; c <= b; c++) {
+      X[c] = dir == 0 ? xl[c] : (int32_t)Wp - xl[c] - pt[c].Wd;
+      Y[c] = or_push_y(F, X[c], pt[c].Wd, pt[c].Dtop, dir);
+      mir[c] = (uint8_t)dir;
+    }
+    np = 0;
+    for (int32_t s1 = a; s1 <= b; s1++)
+      for (int32_t s2 = s1 + 1; s2 <= b; s2++) {
+        int32_t delta = xl[s2] - xl[s1];
+        if (delta >= pt[s1].Wd) continue;
+        if ((spec->flags & OR_F_ADJACENT_LOCKS_ONLY) && s2 != s1 + 1) continue;
+        if (np + 1 > cap) {
+          cap = 2 * cap + 8;
+          qa = realloc(qa, sizeof(int32_t) * cap); qb = realloc(qb, sizeof(int32_t) * cap);
+          la = realloc(la, sizeof(int32_t) * cap); lb = realloc(lb, sizeof(int32_t) * cap);
+        }
+        qa[np] = s1; qb[np] = s2;
+        or_locks(&pt[s1], &pt[s2], delta, &la[np], &lb[np]);
+        np++;
+      }
+    or_correct_y(np, qa, qb, la, lb, Y);
+    int32_t score = 0;
+    for (int32_t c = a; c <= b; c++)
+      for (int32_t i = 0; i < pt[c].Wd; i++) {
+        int32_t db = dir == 0 ? pt[c].Dbot[i] : pt[c].Dbot[pt[c].Wd - 1 - i];
+        if (Y[c] + db > F[X[c] + i]) F[X[c] + i] = Y[c] + db;
+      }
+    for (int64_t x = 0; x < Wp; x++)
+      if (F[x] > score) score = F[x];
+    cand->prefix_rows++;
+    cand->score = score;
+    if (score > Hp) { ok = 0; break; }
+    row_idx++;
+    a = b + 1;
+  }
+  free(qa); free(qb); free(la); free(lb);
+  free(q);
+  free(xl);
+  return ok;
+}
+
 int or_pack_candidate(const or_proxy* px, const int32_t* perm, int32_t n, const or_spec* spec,
                       int32_t m, or_placement* out, or_cand* cand) {
   const int32_t g = spec->gutter, M = spec->scale_count;
@@ -624,7 +725,23 @@ int or_pack_candidate(const or_proxy* px, const int32_t* perm, int32_t n, const 
   int32_t score = 0;
   int32_t row_start = 0;
   int fail = 0;
+  /* D23: t_opt policy ("t_opt = 0% for inputs with up to 10,000 charts and
+   * t_opt = 1% otherwise"), in basis points of the atlas height */
+  const int32_t t_opt = spec->t_opt_bp >= 0 ? spec->t_opt_bp : (n > 10000 ? 100 : 0);
+  or_prof* pt = calloc(n, sizeof(or_prof));  /* tail footprints at s' */
+  int32_t r0 = n;
   while (row_start < n && !fail) {
+    /* D23 switch to prefix folding "when no more knees are detected and the
+     * height of the tallest chart in the row decreases below t_opt";
+     * checked before each row, latched. */
+    if (t_opt > 0 && !knee_valid &&
+        cdiv64(hu[row_start] * m, (int64_t)M * 256) * 10000 < (int64_t)t_opt * spec->atlas_h) {
+      r0 = row_start;
+      cand->score = score;
+      if (!prefix_tail(px, perm, n, r0, m, spec, pr, off, F, X, Y, mir, pt, cand)) fail = 1;
+      score = cand->score;
+      break;
+    }
     if (knee_valid) knee_valid = or_update_knee(F, Wp, knee_ltr, &knee_left, &knee_right);
     int nf = knee_valid ? 2 : 1;
     for (int f = 0; f < nf; f++) {
@@ -699,19 +816,22 @@ int or_pack_candidate(const or_proxy* px, const int32_t* perm, int32_t n, const 
       int32_t c = perm[s];
       or_placement* o = &out[c];
       memset(o, 0, sizeof(*o));
+      const int tail = s >= r0;  /* prefix-folded chart: final scale p / 2^20 */
       o->tx = X[s];
       o->ty = Y[s];
-      o->scale_num = m;
-      o->scale_den = M;
-      o->box_w = pr[s].ws;
-      o->box_h = pr[s].hs;
+      o->scale_num = tail ? cand->p : m;
+      o->scale_den = tail ? (1 << 20) : M;
+      o->box_w = tail ? pt[s].ws : pr[s].ws;
+      o->box_h = tail ? pt[s].hs : pr[s].hs;
       o->rot90 = (uint8_t)px[c].rot90;
       o->flip_x = (uint8_t)px[c].fx;
       o->flip_y = (uint8_t)px[c].fy;
       o->mirror_x = mir[s];
-      o->mode = 0;
+      o->mode = (uint8_t)tail;
     }
   }
+  for (int32_t s = 0; s < n; s++) or_prof_free(&pt[s]);
+  free(pt);
   for (int f = 0; f < 2; f++)
     for (int hc = 0; hc < 2; hc++) {
       free(xloc[f][hc]);
@@ -747,20 +867,46 @@ int or_pack(const float* xy, const int32_t* start, int32_t n, float res_x, float
   if (st != OR_OK) { free(px); free(perm); return st; }
   or_sort(px, n, perm);
   const int32_t M = spec->scale_count;
+  const i128 P20 = (i128)1 << 20;
+  /* area-prefix by sorted position for the D25 weights */
+  i128* apre = malloc(sizeof(i128) * (n + 1));
+  apre[0] = 0;
+  for (int32_t s = 0; s < n; s++) apre[s + 1] = apre[s] + px[perm[s]].area2;
   int32_t best = 0;
+  i128 bestV = -1;
   or_cand bc;
   memset(&bc, 0, sizeof(bc));
   for (int32_t m = 1; m <= M; m++) {
     or_cand cd;
     or_pack_candidate(px, perm, n, spec, m, NULL, &cd);
     if (cands) cands[m - 1] = cd;
-    if (cd.success) { best = m; bc = cd; } /* sequential: the largest success */
+    if (!cd.success) continue;
+    /* D25: the largest area-weighted mean final scale ("the candidate
+     * scale factor S that maximizes the average final scale weighted by chart
+     * area"); sequential candidates reduce to the largest m.  Exact:
+     * V = A_seq * m * 2^20 + A_pre * p * M; ties go to the larger m. */
+    const int32_t r0 = cd.switched_at >= 0 ? cd.switched_at : n;
+    const i128 V = apre[r0] * m * P20 + (apre[n] - apre[r0]) * (i128)cd.p * M;
+    if (V >= bestV) { bestV = V; best = m; bc = cd; }
   }
-  if (best == 0) { free(px); free(perm); return OR_NO_FIT; }
+  if (best == 0) { free(px); free(perm); free(apre); return OR_NO_FIT; }
   or_cand cd;
   or_pack_candidate(px, perm, n, spec, best, out, &cd);
   info->scale_index = best;
-  info->l2_stretch = (double)M / (double)best; /* D26: uniform scale => 1/s */
+  {
+    /* D26: every map is a similarity, so the per-triangle L2 stretch is 1/s;
+     * area-weighted RMS over the charts. */
+    const int32_t r0 = bc.switched_at >= 0 ? bc.switched_at : n;
+    if (r0 == n) {
+      info->l2_stretch = (double)M / (double)best;
+    } else {
+      const double fs = (double)apre[r0] / (double)apre[n];
+      const double fp = (double)(apre[n] - apre[r0]) / (double)apre[n];
+      const double a = (double)M / (double)best, b = (double)(1 << 20) / (double)bc.p;
+      info->l2_stretch = sqrt(fs * a * a + fp * b * b);
+    }
+  }
+  free(apre);
   info->rows = bc.rows;
   info->knees_found = bc.knees_found;
   info->knee_rows = bc.knee_rows;
