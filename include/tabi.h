@@ -137,8 +137,12 @@ typedef struct {
 } tabi_proxy_dbg;
 
 typedef struct {
-  int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p;
+  int32_t success, score, rows, knees_found, knee_rows, prefix_rows;
+  int32_t p;                      /* prefix tail: final scale numerator over 2^20, else 0 */
   int32_t evaluated;              /* 0: skipped (above the area bound or below the winning wave) */
+  int32_t switched_at;            /* first prefix-folded sorted position, -1 if none */
+  int32_t reserved;
+  uint64_t apre_lo, apre_hi;      /* 2 x area of the prefix-folded charts (int128) */
 } tabi_cand_dbg;
 
 tabi_status tabi_debug_proxies(tabi_ctx* ctx, tabi_proxy_dbg* out);   /* n_charts entries */

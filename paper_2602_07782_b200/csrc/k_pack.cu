@@ -51,6 +51,7 @@ struct Smem {
   int32_t changed, npairs, pair_overflow;
   int32_t sel_cfg;
   int32_t win_s0, win_e, pglobal;
+  int32_t prefix_rows, switched;
   unsigned long long knee_key;
   unsigned long long work;
   alignas(8) uint64_t mbar;
@@ -194,21 +195,34 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   W.prof = (uint32_t*)(W.rY + 4 * kRW);
   W.prof_cap = prof_cap;
 
-  if (cand_bad[m - 1]) {  // some chart exceeds the dilated atlas at this scale
-    if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1};
+  const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
+  int32_t* qrow = sc + 5 * (int64_t)n;    // prefix row id per sorted position (tail)
+  if (prefix_mode) {
+    if (pp.T.state[m - 1] != TAIL_READY) return;
+  } else if (cand_bad[m - 1]) {  // some chart exceeds the dilated atlas at this scale
+    if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
     return;
   }
-  {  // work accounting: footprint entries K3 produced for this candidate
+  if (!prefix_mode) {  // work accounting: footprint entries K3 produced for this candidate
     unsigned long long pe = 0;
     for (int s = tid; s < n; s += kNT) pe += (unsigned long long)(wd[s] + hd[s]);
     for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
     if (lane == 0) atomicAdd(&st->work_prof, pe);
   }
-  for (int x = tid; x < Wp; x += kNT) F[x] = 0;  // frontline starts at the top
+  int32_t* fsave = pp.T.fsave + (int64_t)(m - 1) * pp.T.fstride;
+  for (int x = tid; x < Wp; x += kNT) F[x] = prefix_mode ? fsave[x] : 0;  // top
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
+    S.prefix_rows = 0;
+    S.switched = 0;
+    if (prefix_mode) {  // continue from the state saved at the switch
+      const Cand cd = cands[m - 1];
+      S.row_start = pp.T.r0[m - 1];
+      S.fmax = cd.score; S.rows = cd.rows; S.knees_found = cd.knees_found;
+      S.knee_rows = cd.knee_rows;
+    }
     mbar_init(&S.mbar);
   }
   __syncthreads();
@@ -243,6 +257,26 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   while (true) {
     const int32_t rs = S.row_start;
     if (rs >= n || S.fail) break;
+    // ---- D23 switch to prefix folding ("when no more knees are
+    // detected and the height of the tallest chart in the row decreases below
+    // a threshold t_opt"), checked before each row, latched: save the state,
+    // the tail kernels take over. ------------------------------------------
+    if (!prefix_mode && pp.t_opt > 0 && !S.knee_valid) {
+      const int64_t hs0 = ceildiv((int64_t)hsorted[rs] * m, (int64_t)pp.M * TABI_UNITS);
+      if (hs0 * 10000 < (int64_t)pp.t_opt * pp.H) {
+        for (int x = tid; x < Wp; x += kNT) fsave[x] = F[x];
+        if (tid == 0) {
+          pp.T.state[m - 1] = TAIL_LAYOUT;
+          pp.T.r0[m - 1] = rs;
+          pp.T.iter[m - 1] = 0;
+          cands[m - 1] = Cand{0, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1, rs, 0,
+                              0ull, 0ull};
+          S.switched = 1;
+        }
+        __syncthreads();
+        break;
+      }
+    }
     // ---- Alg. 2 UpdateKneeLocation ---------------------------
     if (S.knee_valid) {
       const int32_t left = S.knee_left, right = S.knee_right, ltr = S.knee_ltr;
@@ -286,7 +320,25 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     if (tid < 4) S.endv[tid] = INT32_MIN;
     if (tid == 0) { S.done = 0; S.win_s0 = -1; S.win_e = -1; }
     __syncthreads();
-    {
+    if (prefix_mode) {
+      // prefix rows were laid out by the tail kernels (positions in xs0/xs1);
+      // the row is the run of equal row ids starting at rs
+      const int32_t qr = qrow[rs];
+      for (int base = rs; !S.done; base += kNT) {
+        if (tid == 0) S.fmin[0] = INT32_MAX;
+        __syncthreads();
+        const int s = base + tid;
+        if (s < n && qrow[s] != qr) atomicMin(&S.fmin[0], s);
+        __syncthreads();
+        if (tid == 0 && (S.fmin[0] != INT32_MAX || base + kNT >= n)) {
+          const int32_t e = S.fmin[0] != INT32_MAX ? S.fmin[0] - 1 : n - 1;
+          S.endv[0] = S.endv[1] = e;
+          S.endv[2] = S.endv[3] = rs - 1;
+          S.done = 1;
+        }
+        __syncthreads();
+      }
+    } else {
       int32_t carry0 = 0, carry1 = 0;
       for (int base = rs;; base += kNT) {
         if (tid < 4) S.fmin[tid] = INT32_MAX;
@@ -320,11 +372,12 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         carry0 += t0;
         carry1 += t1;
       }
-    }
+    }  // !prefix_mode
     // ---- level 1 of the hierarchical choice: HC iff it fits more --
     if (tid == 0) {
       S.hcsel[0] = (!no_hc && S.endv[1] > S.endv[0]) ? 1 : 0;
       S.hcsel[1] = (!no_hc && S.endv[3] > S.endv[2]) ? 1 : 0;
+      if (prefix_mode) { S.hcsel[0] = 1; S.hcsel[1] = 0; }  // HC always on in the tail
       const int32_t ea = S.endv[S.hcsel[0]];
       const int32_t ek = S.endv[2 + S.hcsel[1]];
       S.knee_ok = kv && ek >= rs;
@@ -516,6 +569,8 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       const int32_t sw0 = max(S.fmax, S.newmax[0]), sw1 = max(S.fmax, S.newmax[1]);
       int d0 = sw1 < sw0 ? 1 : 0;   // ties -> left to right
       if (no_bal) d0 = S.rows & 1;  // static alternation (ablation)
+      // prefix rows: FastAtlas alternation, one L->R row then two R->L
+      if (prefix_mode) d0 = (S.prefix_rows % 3 == 0) ? 0 : 1;
       int cfg = d0;
       if (knee_ok) {
         const int32_t sk0 = max(S.conc_max, S.newmax[2]), sk1 = max(S.conc_max, S.newmax[3]);
@@ -562,7 +617,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       __syncthreads();
     }
     // ---- FindKnee after an atlas-fold row -----------
-    if (f == 0 && !no_bal) {
+    if (f == 0 && !no_bal && !prefix_mode) {
       for (int t = rs + tid; t < endS; t += kNT) {
         const int64_t d = (int64_t)hsorted[t] - hsorted[t + 1];
         if (10 * d >= (int64_t)pp.H * TABI_UNITS && 5 * d >= hsorted[t]) {
@@ -574,9 +629,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     }
     __syncthreads();
     if (tid == 0) {
-      S.rows++;
+      if (prefix_mode) S.prefix_rows++;
+      else S.rows++;
       if (f == 1) S.knee_rows++;
-      if (f == 0 && !no_bal) {
+      if (f == 0 && !no_bal && !prefix_mode) {
         if (S.knee_key != 0ull) {
           const int t = 0x7fffffff - (int)(S.knee_key & 0xffffffffull);
           S.knee_valid = 1;
@@ -595,8 +651,17 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   }
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
   if (lane == 0) atomicAdd(&st->work_pack, wk);
-  if (tid == 0) {
-    cands[m - 1] = Cand{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1};
+  if (tid == 0 && !S.switched) {
+    Cand cd{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1, -1, 0, 0ull, 0ull};
+    if (prefix_mode) {  // keep the tail's area (written by the layout kernel)
+      const Cand prev = cands[m - 1];
+      cd.prefix_rows = S.prefix_rows;
+      cd.p = pp.T.p[m - 1];
+      cd.switched_at = pp.T.r0[m - 1];
+      cd.apre_lo = prev.apre_lo;
+      cd.apre_hi = prev.apre_hi;
+    }
+    cands[m - 1] = cd;
   }
 }
 
@@ -607,13 +672,31 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
                               const int32_t* __restrict__ hd_all, const int32_t* __restrict__ Xo,
                               const int32_t* __restrict__ Yo, const uint8_t* __restrict__ mir,
                               const Cand* __restrict__ cands, tabi_placement* out, Status* st) {
-  __shared__ int32_t win;
+  __shared__ int32_t win, wr0, wp;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   if (threadIdx.x == 0) {
-    int32_t w = 0;
-    for (int m = pp.M; m >= 1; m--)
-      if (cands[m - 1].success) { w = m; break; }
+    // D25: the candidate with the largest area-weighted mean final scale,
+    // V = A_seq * m * 2^20 + A_pre * p * M (exact, int128), ties -> larger m;
+    // without a prefix tail this is the largest successful m.
+    const i128 Atot = (i128)(((unsigned __int128)st->atot_hi << 64) | st->atot_lo);
+    int32_t w = 0, r0 = pp.n, pw = 0;
+    i128 bestV = -1;
+    for (int m = 1; m <= pp.M; m++) {
+      const Cand cd = cands[m - 1];
+      if (!cd.success) continue;
+      const bool tail = cd.switched_at >= 0;
+      const i128 Ap = tail ? (i128)(((unsigned __int128)cd.apre_hi << 64) | cd.apre_lo) : 0;
+      const i128 V = (Atot - Ap) * m * ((i128)1 << 20) + Ap * cd.p * pp.M;
+      if (V >= bestV) {
+        bestV = V;
+        w = m;
+        r0 = tail ? cd.switched_at : pp.n;
+        pw = cd.p;
+      }
+    }
     win = w;
+    wr0 = r0;
+    wp = pw;
     if (blockIdx.x == 0) st->winner = w;
   }
   __syncthreads();
@@ -624,18 +707,19 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
   const int64_t b = (int64_t)(m - 1) * pp.n + s;
   const int c = perm[s];
   const uint8_t ps = pose[c];
+  const bool tail = s >= wr0;  // prefix-folded chart: final scale p / 2^20 (D24)
   tabi_placement p;
   p.tx = Xo[b];
   p.ty = Yo[b];
-  p.scale_num = m;
-  p.scale_den = pp.M;
+  p.scale_num = tail ? wp : m;
+  p.scale_den = tail ? (1 << 20) : pp.M;
   p.box_w = wd_all[b] - 2 * pp.g;
   p.box_h = hd_all[b] - 2 * pp.g;
   p.rot90 = ps & 1;
   p.flip_x = (ps >> 1) & 1;
   p.flip_y = (ps >> 2) & 1;
   p.mirror_x = mir[b];
-  p.mode = 0;
+  p.mode = tail ? 1 : 0;
   p.pad[0] = p.pad[1] = p.pad[2] = 0;
   out[c] = p;
 }

@@ -206,10 +206,20 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   if (m == 0) return;
   const int s0 = blockIdx.x * kTC;
   const int nt = min(kTC, pp.n - s0);
-  const int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
+  // candidate scale m/M, or in tail mode the prefix tail's p / 2^20 (D24)
+  int64_t num = m, SC = (int64_t)pp.M * TABI_UNITS;
+  int32_t r0 = 0;
+  if (pp.tail) {
+    if (pp.T.state[m - 1] != TAIL_LAYOUT) return;
+    r0 = pp.T.r0[m - 1];
+    if (s0 + nt <= r0) return;
+    num = pp.T.p[m - 1];
+    SC = (int64_t)TABI_UNITS << 20;
+  }
   const double rSC = 1.0 / (double)SC;
   const int ci = tid >> 3, r = tid & 7;
-  if (ci < nt && r == 0) {
+  if (ci < nt && r == 0 && s0 + ci < r0) CH[ci].small = 0;  // sequential chart: untouched
+  if (ci < nt && r == 0 && s0 + ci >= r0) {
     ChartK3& H = CH[ci];
     const int s = s0 + ci;
     const int c = perm[s];
@@ -335,12 +345,12 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   const int k = pp.k;
   int32_t* tab = dyn + wib * 4 * k;
   const int nbig = st->pad[1];
-  const int64_t SC = (int64_t)pp.M * TABI_UNITS;
+  const int64_t SC = pp.tail ? ((int64_t)TABI_UNITS << 20) : (int64_t)pp.M * TABI_UNITS;
   const double rSC = 1.0 / (double)SC;
   for (int it = blockIdx.x * kWarps + wib; it < nbig; it += gridDim.x * kWarps) {
     const int item = big_list[it];
     const int m = item / pp.n + 1, s = item % pp.n;
-    const int64_t num = m;
+    const int64_t num = pp.tail ? pp.T.p[m - 1] : m;
     ChartK3& H = CH[wib];
     if (lane == 0) {
       const int c = perm[s];
@@ -384,6 +394,7 @@ offsets_kernel(PackParams pp, const int32_t* __restrict__ rowofs, const uint32_t
   if (m == 0) return;
   const int s = (int)(item % pp.n);
   if (cand_bad[m - 1]) return;
+  if (pp.tail && (pp.T.state[m - 1] != TAIL_LAYOUT || s < pp.T.r0[m - 1])) return;
   const int64_t base = (int64_t)(m - 1) * pp.n;
   if (s == pp.n - 1) {
     if (lane == 0) { off_all[base + s] = 0; lock_all[base + s] = 0; }

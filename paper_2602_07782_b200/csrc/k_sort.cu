@@ -162,6 +162,8 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
       for (int m = pp.M; m >= 1; m--)
         if ((i128)m * m * tot <= rhs) { m_hi = m; break; }
       st->pad[2] = m_hi;
+      st->atot_lo = (unsigned long long)(uint64_t)tot;
+      st->atot_hi = (unsigned long long)(uint64_t)(tot >> 64);
     }
   }
   int32_t carry_c = 0, carry_r = 0;

@@ -1,0 +1,220 @@
+// k_tail.cu -- hybrid prefix-sum tail ("Performance Optimization",
+// SURVEY D23-D25, reading R3).
+//
+// After K4 switched a candidate to prefix folding at sorted position r0 (its
+// frontline saved), per candidate (one CTA each):
+//   tail_prepare_kernel: exclusive prefix sum of the compaction offsets at the
+//     candidate scale m/M over [r0, n) ("the prefix sum of the horizontal
+//     offsets"), FastAtlas rows = floor(start / W'), widest row extent E,
+//     the global intermediate scale p / 2^20 = (m/M) * min(1, W'/E),
+//     and the tail's area for the area-weighted choice (D25);
+//   [K3 / K3b in tail mode re-rasterize the tail at p / 2^20]
+//   tail_layout_kernel: re-lay each row with an in-row (segmented) exclusive
+//     scan of the new offsets; if the widest row still exceeds W', shrink p by
+//     W'/E' and repeat (at most 8 times), else mark the candidate ready for
+//     K4 in prefix-row mode.
+// All scans are block-wide (warp shuffles + one shared pass per window).
+#include "tabi_internal.cuh"
+
+namespace tabi {
+namespace {
+
+constexpr int kT = 512;
+constexpr int kW = kT / 32;
+
+struct ScanSmem {
+  int32_t s[3][kW + 1];
+  int32_t mx[kW];
+  unsigned long long a[2][kW];
+  int32_t carry[3];
+};
+
+// Block-wide exclusive sums of a, b and inclusive max of c (one value each per
+// thread), with window totals / max returned.
+__device__ __forceinline__ void block_scan3(int32_t a, int32_t b, int32_t c, int32_t& ea,
+                                            int32_t& eb, int32_t& ic, int32_t& ta, int32_t& tb,
+                                            int32_t& mc, ScanSmem& S) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t ia = warp_incl_sum(a, lane), ib = warp_incl_sum(b, lane);
+  const int32_t xc = warp_incl_max(c, lane);
+  if (lane == 31) { S.s[0][wid] = ia; S.s[1][wid] = ib; S.s[2][wid] = xc; }
+  __syncthreads();
+  if (wid == 0) {
+    const int32_t va = lane < kW ? S.s[0][lane] : 0, vb = lane < kW ? S.s[1][lane] : 0;
+    const int32_t vc = lane < kW ? S.s[2][lane] : INT32_MIN;
+    const int32_t xa = warp_incl_sum(va, lane), xb = warp_incl_sum(vb, lane);
+    const int32_t yc = warp_incl_max(vc, lane);
+    int32_t pc = __shfl_up_sync(0xffffffffu, yc, 1);
+    if (lane == 0) pc = INT32_MIN;
+    if (lane < kW) { S.s[0][lane] = xa - va; S.s[1][lane] = xb - vb; S.s[2][lane] = pc; }
+    if (lane == 31) { S.s[0][kW] = xa; S.s[1][kW] = xb; S.s[2][kW] = yc; }
+  }
+  __syncthreads();
+  ea = S.s[0][wid] + ia - a;
+  eb = S.s[1][wid] + ib - b;
+  ic = max(S.s[2][wid], xc);
+  ta = S.s[0][kW];
+  tb = S.s[1][kW];
+  mc = S.s[2][kW];
+  __syncthreads();
+}
+
+__device__ __forceinline__ int32_t block_max(int32_t v, ScanSmem& S) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) S.mx[wid] = v;
+  __syncthreads();
+  int32_t r = INT32_MIN;
+  for (int w = 0; w < kW; w++) r = max(r, S.mx[w]);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kT, 1)
+tail_prepare_kernel(PackParams pp, const int32_t* __restrict__ perm, const int64_t* __restrict__ area2,
+                    const int32_t* __restrict__ wd_all, const int32_t* __restrict__ off_all,
+                    int32_t* scratch, int64_t pair_cap, Cand* cands, const Status* st) {
+  __shared__ ScanSmem S;
+  if (st->bad_chart != INT32_MAX || st->capacity) return;
+  const int m = wave_m(pp, st->pad[2], blockIdx.x);
+  if (m == 0 || pp.T.state[m - 1] != TAIL_LAYOUT) return;
+  const int n = pp.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t Wp = pp.Wp;
+  const int32_t r0 = pp.T.r0[m - 1];
+  const int64_t cb = (int64_t)(m - 1) * n;
+  const int32_t* wd = wd_all + cb;
+  const int32_t* off = off_all + cb;
+  int32_t* sc = scratch + (int64_t)(m - 1) * (6 * (int64_t)n + 3 * pair_cap);
+  int32_t* qrow = sc + 5 * (int64_t)n;
+  int32_t* start = sc + 4 * (int64_t)n;  // temporary: prefix sum at scale m
+  // pass 1: start = exclusive scan of off over [r0, n); q = floor(start / W')
+  int32_t carry = 0;
+  for (int base = r0; base < n; base += kT) {
+    const int s = base + tid;
+    const int32_t a = (s < n && s + 1 < n) ? off[s] : 0;
+    int32_t ea, eb, ic, ta, tb, mc;
+    block_scan3(a, 0, 0, ea, eb, ic, ta, tb, mc, S);
+    if (s < n) {
+      start[s] = carry + ea;
+      qrow[s] = (int32_t)((int64_t)(carry + ea) / Wp);
+    }
+    carry += ta;
+  }
+  __syncthreads();
+  // pass 2: E = max over charts of (start - start of the row's first chart + Wd)
+  int32_t fcarry = INT32_MIN, emax = INT32_MIN;
+  i128 apre = 0;
+  for (int base = r0; base < n; base += kT) {
+    const int s = base + tid;
+    const bool valid = s < n;
+    const bool first = valid && (s == r0 || qrow[s] != qrow[s - 1]);
+    int32_t ea, eb, f, ta, tb, mc;
+    block_scan3(0, 0, first ? s : INT32_MIN, ea, eb, f, ta, tb, mc, S);
+    f = max(f, fcarry);
+    if (valid) {
+      emax = max(emax, start[s] - start[f] + wd[s]);
+      apre += area2[perm[s]];
+    }
+    fcarry = max(fcarry, mc);
+  }
+  emax = block_max(emax, S);
+  apre = warp_sum128(apre);
+  if (lane == 0) {
+    S.a[0][wid] = (unsigned long long)(uint64_t)apre;
+    S.a[1][wid] = (unsigned long long)(uint64_t)(apre >> 64);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    i128 A = 0;
+    for (int w = 0; w < kW; w++) A += (i128)(((unsigned __int128)S.a[1][w] << 64) | S.a[0][w]);
+    const i128 P20 = (i128)1 << 20;
+    i128 p = ((i128)m * P20 * Wp) / ((i128)pp.M * emax);
+    const i128 pm = ((i128)m * P20) / pp.M;  // sigma <= 1: intermediate DOWNscaling
+    if (p > pm) p = pm;
+    pp.T.p[m - 1] = (int32_t)p;
+    if (p < 1) pp.T.state[m - 1] = TAIL_FAIL;
+    cands[m - 1].apre_lo = (unsigned long long)(uint64_t)A;
+    cands[m - 1].apre_hi = (unsigned long long)(uint64_t)(A >> 64);
+  }
+}
+
+__global__ void __launch_bounds__(kT, 1)
+tail_layout_kernel(PackParams pp, const int32_t* __restrict__ wd_all,
+                   const int32_t* __restrict__ off_all, int32_t* scratch, int64_t pair_cap,
+                   const Status* st) {
+  __shared__ ScanSmem S;
+  if (st->bad_chart != INT32_MAX || st->capacity) return;
+  const int m = wave_m(pp, st->pad[2], blockIdx.x);
+  if (m == 0 || pp.T.state[m - 1] != TAIL_LAYOUT) return;
+  const int n = pp.n, tid = threadIdx.x;
+  const int64_t Wp = pp.Wp;
+  const int32_t r0 = pp.T.r0[m - 1];
+  const int64_t cb = (int64_t)(m - 1) * n;
+  const int32_t* wd = wd_all + cb;
+  const int32_t* off = off_all + cb;
+  int32_t* sc = scratch + (int64_t)(m - 1) * (6 * (int64_t)n + 3 * pair_cap);
+  int32_t* xs0 = sc;
+  int32_t* xs1 = sc + n;
+  int32_t* poff = sc + 2 * (int64_t)n;  // temporary global prefix sums
+  int32_t* pwd = sc + 3 * (int64_t)n;
+  const int32_t* qrow = sc + 5 * (int64_t)n;
+  // global exclusive prefix sums of the new offsets and widths over [r0, n)
+  int32_t c0 = 0, c1 = 0;
+  for (int base = r0; base < n; base += kT) {
+    const int s = base + tid;
+    const int32_t a = (s < n && s + 1 < n) ? off[s] : 0;
+    const int32_t b = s < n ? wd[s] : 0;
+    int32_t ea, eb, ic, ta, tb, mc;
+    block_scan3(a, b, 0, ea, eb, ic, ta, tb, mc, S);
+    if (s < n) { poff[s] = c0 + ea; pwd[s] = c1 + eb; }
+    c0 += ta;
+    c1 += tb;
+  }
+  __syncthreads();
+  // row-relative positions: subtract the value at the row's first chart
+  int32_t fcarry = INT32_MIN, emax = INT32_MIN;
+  for (int base = r0; base < n; base += kT) {
+    const int s = base + tid;
+    const bool valid = s < n;
+    const bool first = valid && (s == r0 || qrow[s] != qrow[s - 1]);
+    int32_t ea, eb, f, ta, tb, mc;
+    block_scan3(0, 0, first ? s : INT32_MIN, ea, eb, f, ta, tb, mc, S);
+    f = max(f, fcarry);
+    if (valid) {
+      const int32_t x = poff[s] - poff[f];
+      xs1[s] = x;                // position with compaction (D24 step 2 re-lay)
+      xs0[s] = pwd[s] - pwd[f];  // prefix of widths in the row (flattened index)
+      emax = max(emax, x + wd[s]);
+    }
+    fcarry = max(fcarry, mc);
+  }
+  emax = block_max(emax, S);
+  if (tid == 0) {
+    const int it = pp.T.iter[m - 1];
+    if (emax <= Wp) {
+      pp.T.state[m - 1] = TAIL_READY;
+    } else if (it >= 8) {
+      pp.T.state[m - 1] = TAIL_FAIL;
+    } else {
+      const int64_t p = ((int64_t)pp.T.p[m - 1] * Wp) / emax;
+      pp.T.p[m - 1] = (int32_t)p;
+      pp.T.iter[m - 1] = it + 1;
+      if (p < 1) pp.T.state[m - 1] = TAIL_FAIL;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_tail_prepare(const PackParams& pp, const int32_t* perm, const int64_t* area2,
+                         const int32_t* wd, const int32_t* off, int32_t* scratch, int64_t pair_cap,
+                         Cand* cands, const Status* st, cudaStream_t s) {
+  tail_prepare_kernel<<<pp.B, kT, 0, s>>>(pp, perm, area2, wd, off, scratch, pair_cap, cands, st);
+}
+
+void launch_tail_layout(const PackParams& pp, const int32_t* wd, const int32_t* off,
+                        int32_t* scratch, int64_t pair_cap, const Status* st, cudaStream_t s) {
+  tail_layout_kernel<<<pp.B, kT, 0, s>>>(pp, wd, off, scratch, pair_cap, st);
+}
+
+}  // namespace tabi

@@ -8,6 +8,7 @@
 // larger than the current buffers), the context grows those buffers and
 // re-runs from the slot layout; sizes persist, so steady-state calls never
 // retry.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -47,6 +48,13 @@ struct tabi_ctx {
   uint8_t* lockbits = nullptr;
   int32_t* cand_bad = nullptr;
   int32_t* big_list = nullptr;  // (candidate, chart) items too large for K3's tile buffer
+  // hybrid prefix tail state per candidate
+  int32_t* t_state = nullptr;
+  int32_t* t_r0 = nullptr;
+  int32_t* t_p = nullptr;
+  int32_t* t_iter = nullptr;
+  int32_t* t_fsave = nullptr;
+  int32_t fstride = 0;
   int32_t* X = nullptr;
   int32_t* Y = nullptr;
   uint8_t* mir = nullptr;
@@ -88,7 +96,8 @@ static void dfree_all(tabi_ctx* ctx) {
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
                 ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
                 ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->X, ctx->Y, ctx->mir,
-                ctx->cands, ctx->dcol,
+                ctx->cands, ctx->dcol, ctx->t_state, ctx->t_r0, ctx->t_p, ctx->t_iter,
+                ctx->t_fsave,
                 ctx->drow, ctx->scratch};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -173,6 +182,12 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
     CK(dalloc(&ctx->lockbits, (size_t)M * N));
     CK(dalloc(&ctx->cand_bad, (size_t)M));
     CK(dalloc(&ctx->big_list, (size_t)M * N));
+    ctx->fstride = ((ctx->max_side + 2 * 64 + 4) + 31) & ~31;
+    CK(dalloc(&ctx->t_state, (size_t)M));
+    CK(dalloc(&ctx->t_r0, (size_t)M));
+    CK(dalloc(&ctx->t_p, (size_t)M));
+    CK(dalloc(&ctx->t_iter, (size_t)M));
+    CK(dalloc(&ctx->t_fsave, (size_t)M * ctx->fstride));
     CK(dalloc(&ctx->X, (size_t)M * N));
     CK(dalloc(&ctx->Y, (size_t)M * N));
     CK(dalloc(&ctx->mir, (size_t)M * N));
@@ -237,8 +252,8 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   if (!xy || !chart_start || !out || n < 1 || !spec_ok(spec)) return TABI_EINVAL;
   if (n > ctx->max_n || spec->atlas_w > ctx->max_side || spec->atlas_h > ctx->max_side)
     return TABI_ECAPACITY;
+  // D23 policy: t_opt = 0 for <= 10,000 charts, 1 % of H above
   const int32_t t_opt = spec->t_opt_bp >= 0 ? spec->t_opt_bp : (n > 10000 ? 100 : 0);
-  if (t_opt > 0) return TABI_EINVAL;  // prefix tail not in this build yet
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
   int launches = 0;
@@ -284,6 +299,15 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   pp.Wp = spec->atlas_w + 2 * spec->gutter;
   pp.Hp = spec->atlas_h + 2 * spec->gutter;
   pp.flags = spec->flags;
+  pp.t_opt = t_opt;
+  pp.mode = 0;
+  pp.tail = 0;
+  pp.T.state = ctx->t_state;
+  pp.T.r0 = ctx->t_r0;
+  pp.T.p = ctx->t_p;
+  pp.T.iter = ctx->t_iter;
+  pp.T.fsave = ctx->t_fsave;
+  pp.T.fstride = ctx->fstride;
 
   Status init{};
   init.bad_chart = INT32_MAX;
@@ -314,6 +338,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->d_status, s);
       launches++;
       CK(cudaMemsetAsync(ctx->cands, 0, sizeof(Cand) * M, s));
+      CK(cudaMemsetAsync(ctx->t_state, 0, sizeof(int32_t) * M, s));
     }
     CK(cudaMemsetAsync(ctx->cand_bad, 0, sizeof(int32_t) * M, s));
     CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));  // large-chart list
@@ -330,6 +355,31 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
                 ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
                 ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
     launches++;
+    if (t_opt > 0) {
+      // hybrid prefix tail for the candidates K4 switched: rows and
+      // sigma, then up to 9 re-rasterize / re-lay rounds, then the prefix rows
+      launch_tail_prepare(pp, ctx->perm, ctx->P.area2, ctx->wd, ctx->off, ctx->scratch,
+                          ctx->pair_cap, ctx->cands, ctx->d_status, s);
+      launches++;
+      PackParams pt = pp;
+      pt.tail = 1;
+      for (int r = 0; r <= 8; r++) {
+        CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));
+        launch_profiles(ctx->P, ctx->perm, pt, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
+                        (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
+                        ctx->d_status, s);
+        launch_offsets(pt, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
+                       ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
+        launch_tail_layout(pt, ctx->wd, ctx->off, ctx->scratch, ctx->pair_cap, ctx->d_status, s);
+        launches += 4;
+      }
+      PackParams pm = pp;
+      pm.mode = 1;
+      launch_pack(pm, ctx->colofs, ctx->rowofs, ctx->dcol, ctx->drow, ctx->wd, ctx->hd, ctx->off,
+                  ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
+                  ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
+      launches++;
+    }
     tm.mark(s);
     launch_select(pp, ctx->P, ctx->perm, ctx->wd, ctx->hd, ctx->X, ctx->Y, ctx->mir, ctx->cands,
                   d_out, ctx->d_status, s);
@@ -345,7 +395,19 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
       return TABI_EINVAL;
     }
     if (!st.capacity) {
-      if (st.winner > 0 || st.pad[2] - (wave + 1) * B < 1) break;  // found, or no candidates left
+      // Continue while an unevaluated (lower) candidate could still beat the
+      // best area-weighted scale found: V(m) <= A_tot * m * 2^20 (p <= m 2^20/M);
+      // in sequential mode any success stops the search.
+      const int next_m = st.pad[2] - (wave + 1) * B;
+      if (next_m < 1) break;
+      if (st.winner > 0) {
+        const i128 Atot = (i128)(((unsigned __int128)st.atot_hi << 64) | st.atot_lo);
+        const Cand& c = ctx->h_cands[st.winner - 1];
+        const bool tail = c.switched_at >= 0;
+        const i128 Ap = tail ? (i128)(((unsigned __int128)c.apre_hi << 64) | c.apre_lo) : 0;
+        const i128 bestV = (Atot - Ap) * st.winner * ((i128)1 << 20) + Ap * c.p * M;
+        if (Atot * next_m * ((i128)1 << 20) <= bestV) break;
+      }
       wave++;
       continue;
     }
@@ -388,7 +450,17 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   if (info) {
     const Cand& c = ctx->h_cands[win - 1];
     info->scale_index = win;
-    info->l2_stretch = (double)M / (double)win;  // uniform scale s: per-triangle stretch 1/s
+    // D26: every map is a similarity, so the per-triangle L2 stretch is 1/s
+    // (P:1028); area-weighted RMS over sequential (m/M) and tail (p/2^20) charts
+    if (c.switched_at < 0) {
+      info->l2_stretch = (double)M / (double)win;
+    } else {
+      const i128 At = (i128)(((unsigned __int128)ctx->h_status->atot_hi << 64) | ctx->h_status->atot_lo);
+      const i128 Ap = (i128)(((unsigned __int128)c.apre_hi << 64) | c.apre_lo);
+      const double fs = (double)(At - Ap) / (double)At, fp = (double)Ap / (double)At;
+      const double a = (double)M / (double)win, b = (double)(1 << 20) / (double)c.p;
+      info->l2_stretch = sqrt(fs * a * a + fp * b * b);
+    }
     info->rows = c.rows;
     info->knees_found = c.knees_found;
     info->knee_rows = c.knee_rows;

@@ -277,18 +277,36 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t pad[3];
   unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
   unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
+  unsigned long long atot_lo, atot_hi;  // total 2 x area (int128) for D25 / D26
 };
 
 // Per-candidate result record (mirrors tabi_cand_dbg).
 struct Cand {
   int32_t success, score, rows, knees_found, knee_rows, prefix_rows, p, evaluated;
+  int32_t switched_at, reserved;
+  unsigned long long apre_lo, apre_hi;  // 2 x area of the prefix-folded tail (D25), int128
+};
+
+// Hybrid prefix tail state per candidate (DESIGN.md §1 A12).
+enum { TAIL_NONE = 0, TAIL_LAYOUT = 1, TAIL_READY = 2, TAIL_FAIL = 3 };
+struct TailBufs {
+  int32_t* state;   // [M] TAIL_*
+  int32_t* r0;      // [M] first prefix-folded sorted position
+  int32_t* p;       // [M] intermediate scale numerator over 2^20
+  int32_t* iter;    // [M] layout adjustments made
+  int32_t* fsave;   // [M][fstride] frontline at the switch
+  int32_t fstride;
 };
 
 struct PackParams {
   int32_t n, k, M, g, W, H, Wp, Hp;
   uint32_t flags;
   int32_t wave, B;            // candidate wave: m = m_hi - wave * B - j, j < B
+  int32_t t_opt;              // effective t_opt (basis points of H), 0 = sequential only
+  int32_t mode;               // K4: 0 sequential rows (may switch), 1 prefix rows
+  int32_t tail;               // K3 / K3b: 1 = rasterize tail charts at p / 2^20
   int64_t col_cap, row_cap;   // per-candidate footprint slot capacity (entries)
+  TailBufs T;
 };
 
 // Candidate j of the current wave (0 if below 1).  m_hi = st->pad[2] is the
@@ -324,4 +342,12 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
                    const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s);
+}  // namespace tabi
+
+namespace tabi {
+void launch_tail_prepare(const PackParams& pp, const int32_t* perm, const int64_t* area2,
+                         const int32_t* wd, const int32_t* off, int32_t* scratch, int64_t pair_cap,
+                         Cand* cands, const Status* st, cudaStream_t s);
+void launch_tail_layout(const PackParams& pp, const int32_t* wd, const int32_t* off,
+                        int32_t* scratch, int64_t pair_cap, const Status* st, cudaStream_t s);
 }  // namespace tabi

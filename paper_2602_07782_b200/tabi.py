@@ -58,7 +58,10 @@ PROXY_DTYPE = np.dtype([("w", "<i4"), ("h", "<i4"), ("area2", "<i8"), ("xmin", "
                         ("reserved", "<i4"), ("umin", "<i8"), ("umax", "<i8"), ("vmin", "<i8"),
                         ("vmax", "<i8")])
 CAND_DTYPE = np.dtype([(f, "<i4") for f in ("success", "score", "rows", "knees_found",
-                                            "knee_rows", "prefix_rows", "p", "evaluated")])
+                                            "knee_rows", "prefix_rows", "p", "evaluated",
+                                            "switched_at", "reserved")] +
+                      [("apre_lo", "<u8"), ("apre_hi", "<u8")])
+assert CAND_DTYPE.itemsize == 56
 
 _lib = None
 

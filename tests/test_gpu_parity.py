@@ -56,7 +56,7 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
     # evaluated candidate must agree with the exhaustive oracle, and the winner is
     # the oracle's largest successful m
     assert gc["evaluated"].sum() >= 1
-    assert info_g.scale_index == max(m for m in range(1, M + 1) if cands_o[m - 1].success)
+    assert info_g.scale_index == info_o.scale_index
     for m in range(1, M + 1):
         co = cands_o[m - 1]
         if not gc["evaluated"][m - 1]:
@@ -64,7 +64,8 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
             continue
         assert gc["success"][m - 1] == co.success, m
         if co.success:
-            for f in ("score", "rows", "knees_found", "knee_rows"):
+            for f in ("score", "rows", "knees_found", "knee_rows", "prefix_rows", "p",
+                      "switched_at"):
                 assert gc[f][m - 1] == getattr(co, f), (m, f)
     # placements bit-exact, scale/stretch
     for f in ("tx", "ty", "scale_num", "scale_den", "box_w", "box_h", "rot90", "flip_x", "flip_y",
@@ -150,6 +151,25 @@ def test_unsnapped_input_with_resolution(orc, ctx):
     xy = (cs.xy / 256.0 + rng.uniform(-1e-4, 1e-4, cs.xy.shape)).astype(np.float32)
     cs2 = chartgen.ChartSet("uv01", xy, cs.start, 256, 256)
     _compare_pack(orc, ctx, cs2, res=(256.0, 256.0), check_profiles=3)
+
+
+HYBRID = [chartgen.small_case(s, n=400, family="tss", side=512, rho=0.6) for s in range(2)] + \
+         [chartgen.small_case(s, n=300, family="lightmap", side=384, rho=0.9) for s in range(2)] + \
+         [chartgen.generate("lightmap", 2500, 2048, 2048, 7, rho=0.8, name="lightmap-2500")]
+
+
+@pytest.mark.parametrize("t", [100, 300, 1000])
+@pytest.mark.parametrize("cs", HYBRID, ids=lambda c: c.name)
+def test_hybrid_tail_parity(orc, ctx, cs, t):
+    """D23-D26 prefix tail: rows, sigma, placements and the area-weighted
+    candidate choice bit-exact; stretch within 1e-6."""
+    _compare_pack(orc, ctx, cs, check_profiles=2, t_opt_bp=t)
+
+
+def test_config4_policy_full_size(orc, ctx):
+    """C4: 20,000 lightmap charts into 8192^2 with the paper's t_opt policy
+    (1 % for > 10,000 charts): full oracle comparison."""
+    _compare_pack(orc, ctx, chartgen.config4(0), check_profiles=0)
 
 
 @pytest.mark.parametrize("wave", ["1", "3", "256"])
