@@ -46,6 +46,10 @@ def workload(name: str, seed: int, rho: float):
     elif name == "C4":
         cs = chartgen.config4(seed, t_opt_bp=0)
         desc = f"C4 configs[3]: 20000 lightmap charts (seed={seed}, rho=0.8) into 8192x8192, t_opt=0"
+    elif name == "C4P":
+        cs = chartgen.config4(seed, t_opt_bp=-1)
+        desc = (f"C4 configs[3]: 20000 lightmap charts (seed={seed}, rho=0.8) into 8192x8192, "
+                f"paper t_opt policy (1% for > 10,000 charts, hybrid prefix tail)")
     else:
         raise SystemExit(f"unknown workload {name}")
     return cs, desc

@@ -218,7 +218,10 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   }
   const double rSC = 1.0 / (double)SC;
   const int ci = tid >> 3, r = tid & 7;
-  if (ci < nt && r == 0 && s0 + ci < r0) CH[ci].small = 0;  // sequential chart: untouched
+  if (ci < nt && r == 0 && s0 + ci < r0) {  // sequential chart: untouched in tail mode
+    CH[ci].small = 0;
+    cells[ci] = 0;
+  }
   if (ci < nt && r == 0 && s0 + ci >= r0) {
     ChartK3& H = CH[ci];
     const int s = s0 + ci;

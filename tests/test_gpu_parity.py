@@ -85,16 +85,24 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
                 continue
             off_g, lk_g = ctx.offsets(m, n)
             ss = sorted({0, n - 1, *[rng.randint(0, n - 1) for _ in range(check_profiles)]})
+            r0 = int(gc["switched_at"][m - 1])
+            r0 = n if r0 < 0 else r0
+
+            def scale(pos):  # tail charts were re-rasterized at p / 2^20 (D24)
+                return (int(gc["p"][m - 1]), 1 << 20) if pos >= r0 else (m, M)
+
             for s in ss:
                 prof = ctx.profile(m, s)
-                po = oracle.Profile(px[perm_o[s]], m, M, g)
+                po = oracle.Profile(px[perm_o[s]], *scale(s), g)
                 assert prof is not None
                 Wd, Hd, dt, db, dl, dr = prof
                 assert (Wd, Hd) == (po.Wd, po.Hd)
                 assert np.array_equal(dt, po.Dtop) and np.array_equal(db, po.Dbot)
                 assert np.array_equal(dl, po.Dleft) and np.array_equal(dr, po.Dright)
                 if s + 1 < n:
-                    pn = oracle.Profile(px[perm_o[s + 1]], m, M, g)
+                    pn = oracle.Profile(px[perm_o[s + 1]], *scale(s), g)
+                    if s < r0:
+                        po = oracle.Profile(px[perm_o[s]], m, M, g)
                     off = oracle.offset(po, pn)
                     assert off_g[s] == off
                     la, lb = oracle.locks(po, pn, off) if off < po.Wd else (False, False)
