@@ -194,6 +194,21 @@ def run_reference(args, ws, rank):
     print(json.dumps(line))
 
 
+def rank_atlases(name, rank, ws, rho):
+    """The chart sets this rank packs each step, and the per-step total over ranks."""
+    if name == "C5":
+        import chartgen
+        from paper_2602_07782_b200 import shard_plan
+        sizes = chartgen.config5_sizes(512)
+        a = shard_plan(sizes, ws)
+        mine = [chartgen.config5(i) for i in range(512) if a[i] == rank]
+        desc = ("C5 configs[4]: batch of 512 tss atlases (200-2000 charts each, rho~U[0.3,1.5]) "
+                "into 2048x2048, LPT-sharded over the ranks")
+        return mine, desc, 512, "strong"
+    cs, desc = workload(name, rank, rho)
+    return [cs], desc, ws, "weak"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -219,21 +234,24 @@ def main():
         nbuild.build()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cs, desc = workload(args.workload, rank, args.rho)
-    spec = spec_of(cs)
-    ctx = Context(local, max_charts=max(cs.n_charts, 1024), max_vertices=cs.n_vertices + 16,
-                  max_atlas_side=max(cs.atlas_w, cs.atlas_h))
+    sets, desc, units_per_step, scaling = rank_atlases(args.workload, rank, ws, args.rho)
+    specs = [spec_of(cs) for cs in sets]
+    ctx = Context(local, max_charts=max(max(cs.n_charts for cs in sets), 1024),
+                  max_vertices=max(cs.n_vertices for cs in sets) + 16,
+                  max_atlas_side=max(max(cs.atlas_w, cs.atlas_h) for cs in sets))
     stream = torch.cuda.current_stream(dev)
-    xy_d = torch.from_numpy(cs.xy).to(dev)
-    start_d = torch.from_numpy(cs.start).to(dev)
-    out_d = torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)
+    dev_in = [(torch.from_numpy(cs.xy).to(dev), torch.from_numpy(cs.start).to(dev),
+               torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)) for cs in sets]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def pack_dev():
-        return ctx.pack(xy_d, start_d, spec, out=out_d, stream=stream.cuda_stream)
+    def step_dev():
+        infos = []
+        for (xy_d, start_d, out_d), spec in zip(dev_in, specs):
+            infos.append(ctx.pack(xy_d, start_d, spec, out=out_d, stream=stream.cuda_stream)[2])
+        return infos
 
     for _ in range(args.warmup):
-        pack_dev()
+        step_dev()
     torch.cuda.synchronize()
     os.environ["TABI_TIMING"] = "1"
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -241,32 +259,33 @@ def main():
     stage = np.zeros(8)
     launches = 0
     work_pack = work_prof = 0
-    info = None
+    infos = None
     barrier(ws)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            st, _, info = pack_dev()
+            infos = step_dev()
             ev[i][1].record(stream)
-            stage += np.array(info.stage_ms[:8])
-            launches += info.gpu_launches
-            work_pack += info.work_pack
-            work_prof += info.work_profile
+            for info in infos:
+                stage += np.array(info.stage_ms[:8])
+                launches += info.gpu_launches
+                work_pack += info.work_pack
+                work_prof += info.work_profile
     torch.cuda.synchronize()
     barrier(ws)
     os.environ["TABI_TIMING"] = "0"
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = allmax(sum(step_ms), ws)
     ms_per_step = total_ms / args.steps
-    value = ws * args.steps / (total_ms / 1000.0)
+    value = units_per_step * args.steps / (total_ms / 1000.0)
     p50 = statistics.median(step_ms)
     p99 = float(np.percentile(step_ms, 99))
 
     # ---- e2e through the public host-pointer call -------------------------
-    e2e_steps = max(10, args.steps // 4)
-    for _ in range(2):
+    e2e_steps = max(10, args.steps // 4) if len(sets) == 1 else 3
+    for cs, spec in zip(sets, specs):
         ctx.pack(cs.xy, cs.start, spec, stream=stream.cuda_stream)
     e2e_ev = []
     torch.cuda.synchronize()
@@ -275,23 +294,25 @@ def main():
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        ctx.pack(cs.xy, cs.start, spec, stream=stream.cuda_stream)
+        for cs, spec in zip(sets, specs):
+            ctx.pack(cs.xy, cs.start, spec, stream=stream.cuda_stream)
         b.record(stream)
         e2e_ev.append((a, b))
     torch.cuda.synchronize()
     e2e_ms = allmax(sum(a.elapsed_time(b) for a, b in e2e_ev), ws) / e2e_steps
-    h2d = int(cs.xy.nbytes + cs.start.nbytes)
-    d2h = int(cs.n_charts * 32 + 64 + 32 * cs.scale_count)
+    h2d = int(sum(cs.xy.nbytes + cs.start.nbytes for cs in sets))
+    d2h = int(sum(cs.n_charts * 32 + 64 + 56 * cs.scale_count for cs in sets))
 
     # ---- roofline of the dominant kernel -------------------------------
-    stage_avg = stage / args.steps
+    npk = args.steps * len(sets)
+    stage_avg = stage / npk
     names = ["h2d", "proxies", "sort", "profiles", "offsets_locks", "fold_push", "select", "d2h"]
     k_dom = int(np.argmax(stage_avg[1:7])) + 1
     pk, pk_kind = peaks()
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    # int32 lane-op issue peak: 148 SMs x 4 SMSPs x 32 lanes x clock (DESIGN.md "Roofline")
+    # int32 lane-op issue peak: 148 SMs x 4 SMSPs x 32 lanes x clock (DESIGN.md §6)
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # G lane-ops/s
-    work = {5: work_pack / args.steps, 3: work_prof / args.steps}.get(k_dom)
+    work = {5: work_pack / npk, 3: work_prof / npk}.get(k_dom)
     roof = {"kernel": names[k_dom], "bound": "alu", "unit": "Gop/s",
             "peak": alu_peak, "peak_kind": f"derived from {pk_kind} sm_max_mhz (148x128 int32 lanes)",
             "stage_ms": {names[i]: round(float(stage_avg[i]), 5) for i in range(8)},
@@ -306,33 +327,38 @@ def main():
         roof.update({"achieved": None, "frac": None})
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
-        t = json.load(open(tr)).get(names[k_dom])
-        roof["traffic"] = t
+        roof["traffic"] = json.load(open(tr)).get(names[k_dom])
     # HBM context: compulsory bytes per pack
-    hbm_bytes = cs.xy.nbytes + cs.start.nbytes + 32 * cs.n_charts
+    hbm_bytes = sum(cs.xy.nbytes + cs.start.nbytes + 32 * cs.n_charts for cs in sets) / len(sets)
+    info = infos[0]
     line = {"metric": METRIC, "value": value, "unit": "atlases/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (chartgen SplitMix64, seed = rank)",
             "config": {"workload": desc, "l2": "flushed between steps (256 MB write, untimed)",
-                       "parallelism": f"{ws} independent packs per step (one per GPU)"},
-            "p50_ms": p50, "p99_ms": p99, "l2_stretch": info.l2_stretch,
+                       "parallelism": (f"{ws} independent packs per step (one per GPU)"
+                                       if scaling == "weak" else
+                                       f"512 atlases per step sharded over {ws} GPU(s)")},
+            "p50_ms": p50, "p99_ms": p99,
+            "l2_stretch": (info.l2_stretch if len(sets) == 1 else
+                           float(np.mean([i.l2_stretch for i in infos]))),
             "scale_index": info.scale_index, "rows": info.rows,
             "interactive_budget_ms": 15.0,
             "hbm_compulsory": {"bytes_per_pack": int(hbm_bytes),
-                               "gbs": hbm_bytes / (p50 * 1e-3) / 1e9,
-                               "frac_of_measured": hbm_bytes / (p50 * 1e-3) / 1e9 / pk.get("hbm_gbs", 6650.0)},
+                               "gbs": hbm_bytes * len(sets) / (p50 * 1e-3) / 1e9,
+                               "frac_of_measured": hbm_bytes * len(sets) / (p50 * 1e-3) / 1e9 /
+                               pk.get("hbm_gbs", 6650.0)},
             "roofline": roof,
-            "e2e": {"value": ws * 1000.0 / e2e_ms, "unit": "atlases/s", "ms_per_pack": e2e_ms,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": units_per_step * 1000.0 / e2e_ms, "unit": "atlases/s",
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "paper_context": PAPER_CONTEXT}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, n, dt, m = cpu_oracle_rate(cs)
+        rate, n, dt, m = cpu_oracle_rate(sets[0])
         line["cpu_baseline"] = {"value": rate, "unit": "atlases/s", "cores": 1, "kind": "oracle",
-                                "sample": f"{n} full oracle packs of the same chart set "
-                                          f"(all 64 candidates) in {dt:.1f} s, 1 thread",
+                                "sample": f"{n} full oracle packs of the first chart set "
+                                          f"(all candidates) in {dt:.1f} s, 1 thread",
                                 "host_cores": os.cpu_count()}
     if rank == 0:
         print(json.dumps(line))

@@ -123,6 +123,24 @@ tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start
 const char* tabi_status_str(tabi_status s);
 const char* tabi_last_error(tabi_ctx* ctx);   /* last CUDA error text, or "" */
 
+/* ---- batches of independent atlases over several GPUs ----
+ * A single pack never shards; a batch shards by atlas.  tabi_shard_plan
+ * assigns atlas i to GPU assignment[i] by LPT (longest processing time first):
+ * atlases sorted by estimated cost n*(1 + log2 n) descending (ties by index),
+ * each to the currently least-loaded GPU (ties to the lowest GPU index).
+ * Deterministic; pure host code.  Returns TABI_EINVAL on bad arguments. */
+tabi_status tabi_shard_plan(int32_t n_atlases, const int32_t* n_charts, int32_t n_gpus,
+                            int32_t* assignment);
+/* Pack n_atlases atlases (host pointers) on n_gpus contexts, one host thread
+ * per context, atlases assigned by tabi_shard_plan.  out[i] / infos[i] receive
+ * atlas i's placements / info.  Returns TABI_OK if every atlas packed or hit
+ * NO_FIT (see infos[i].scale_index == 0), else the first other error.  There is
+ * no inter-GPU communication: results land in the caller's host buffers. */
+tabi_status tabi_pack_batch(tabi_ctx* const* ctxs, int32_t n_gpus, int32_t n_atlases,
+                            const float* const* xy, const int32_t* const* chart_start,
+                            const int32_t* n_charts, const float* res_xy, const tabi_spec* specs,
+                            tabi_placement* const* out, tabi_info* infos);
+
 /* ---- introspection of the last tabi_pack on ctx (parity tests; host outputs) ---- */
 
 /* Final-pose proxy of one chart, 1088 bytes (D3-D8 of SURVEY.md §8(c)). */

@@ -5,4 +5,4 @@ the C ABI in ``include/tabi.h``); this package is its thin Python binding.
 """
 from .tabi import (CAND_DTYPE, EINVAL, ECAPACITY, ECUDA, EXPORTS, F_ADJACENT_LOCKS_ONLY,  # noqa
                    F_NO_BALANCE, F_NO_HC, NO_FIT, OK, PLACEMENT_DTYPE, PROXY_DTYPE, Context,
-                   Info, Spec, TabiError, lib, make_spec, spec_of)
+                   Info, Spec, TabiError, lib, make_spec, pack_batch, shard_plan, spec_of)

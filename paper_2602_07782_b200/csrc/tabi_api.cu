@@ -8,8 +8,11 @@
 // larger than the current buffers), the context grows those buffers and
 // re-runs from the slot layout; sizes persist, so steady-state calls never
 // retry.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <thread>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -469,6 +472,59 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     info->work_pack = (int64_t)ctx->h_status->work_pack;
     info->work_profile = (int64_t)ctx->h_status->work_prof;
   }
+  return TABI_OK;
+}
+
+// ---- batches over several GPUs --------------------------------
+
+extern "C" tabi_status tabi_shard_plan(int32_t n_atlases, const int32_t* n_charts, int32_t n_gpus,
+                                       int32_t* assignment) {
+  if (n_atlases < 0 || n_gpus < 1 || (n_atlases > 0 && (!n_charts || !assignment)))
+    return TABI_EINVAL;
+  std::vector<int32_t> order(n_atlases);
+  std::vector<double> cost(n_atlases);
+  for (int32_t i = 0; i < n_atlases; i++) {
+    order[i] = i;
+    const double n = n_charts[i] > 0 ? (double)n_charts[i] : 0.0;
+    cost[i] = n * (1.0 + std::log2(n + 1.0));  // sort + per-row work estimate
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+  std::vector<double> load(n_gpus, 0.0);
+  for (int32_t i : order) {
+    int32_t g = 0;
+    for (int32_t q = 1; q < n_gpus; q++)
+      if (load[q] < load[g]) g = q;
+    assignment[i] = g;
+    load[g] += cost[i];
+  }
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_pack_batch(tabi_ctx* const* ctxs, int32_t n_gpus, int32_t n_atlases,
+                                       const float* const* xy, const int32_t* const* chart_start,
+                                       const int32_t* n_charts, const float* res_xy,
+                                       const tabi_spec* specs, tabi_placement* const* out,
+                                       tabi_info* infos) {
+  if (!ctxs || n_gpus < 1 || n_atlases < 0) return TABI_EINVAL;
+  std::vector<int32_t> asg(n_atlases);
+  tabi_status st = tabi_shard_plan(n_atlases, n_charts, n_gpus, asg.data());
+  if (st != TABI_OK) return st;
+  std::vector<tabi_status> res(n_atlases, TABI_OK);
+  std::vector<std::thread> th;
+  for (int32_t g = 0; g < n_gpus; g++) {
+    th.emplace_back([&, g]() {
+      for (int32_t i = 0; i < n_atlases; i++) {
+        if (asg[i] != g) continue;
+        const float rx = res_xy ? res_xy[2 * i] : 1.0f, ry = res_xy ? res_xy[2 * i + 1] : 1.0f;
+        res[i] = tabi_pack(ctxs[g], xy[i], chart_start[i], n_charts[i], rx, ry, &specs[i], out[i],
+                           infos ? &infos[i] : nullptr, 0, nullptr);
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int32_t i = 0; i < n_atlases; i++)
+    if (res[i] != TABI_OK && res[i] != TABI_NO_FIT) return res[i];
   return TABI_OK;
 }
 

@@ -87,13 +87,45 @@ def lib():
         L.tabi_debug_candidates.argtypes = [P, P]
         L.tabi_debug_profile.argtypes = [P, i32, i32, P, P, P, P, P]
         L.tabi_debug_offsets.argtypes = [P, i32, P, P]
+        L.tabi_shard_plan.argtypes = [i32, P, i32, P]
+        L.tabi_pack_batch.argtypes = [P, i32, i32, P, P, P, P, P, P, P]
         _lib = L
     return _lib
 
 
 EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
-           "tabi_debug_profile", "tabi_debug_offsets"]
+           "tabi_debug_profile", "tabi_debug_offsets", "tabi_shard_plan", "tabi_pack_batch"]
+
+
+def shard_plan(n_charts, n_gpus: int) -> np.ndarray:
+    """LPT assignment of atlases to GPUs (tabi_shard_plan; host code, no GPU)."""
+    nc = np.ascontiguousarray(n_charts, dtype=np.int32)
+    out = np.zeros(nc.shape[0], dtype=np.int32)
+    st = lib().tabi_shard_plan(nc.shape[0], _ptr(nc), n_gpus, _ptr(out))
+    if st != OK:
+        raise TabiError(st, "tabi_shard_plan")
+    return out
+
+
+def pack_batch(contexts, chart_sets, specs):
+    """Pack independent atlases on several contexts (one host thread each).
+    Returns (status, [placements], [Info])."""
+    n = len(chart_sets)
+    xys = [np.ascontiguousarray(cs.xy, dtype=np.float32) for cs in chart_sets]
+    starts = [np.ascontiguousarray(cs.start, dtype=np.int32) for cs in chart_sets]
+    outs = [np.zeros(cs.n_charts, dtype=PLACEMENT_DTYPE) for cs in chart_sets]
+    infos = (Info * n)()
+    ctx_arr = (C.c_void_p * len(contexts))(*[c.h.value for c in contexts])
+    xy_arr = (C.c_void_p * n)(*[a.ctypes.data for a in xys])
+    st_arr = (C.c_void_p * n)(*[a.ctypes.data for a in starts])
+    out_arr = (C.c_void_p * n)(*[a.ctypes.data for a in outs])
+    nch = np.array([cs.n_charts for cs in chart_sets], dtype=np.int32)
+    res = np.array([[cs.res, cs.res] for cs in chart_sets], dtype=np.float32).reshape(-1)
+    spec_arr = (Spec * n)(*specs)
+    st = lib().tabi_pack_batch(ctx_arr, len(contexts), n, xy_arr, st_arr, _ptr(nch), _ptr(res),
+                               spec_arr, out_arr, infos)
+    return st, outs, list(infos)
 
 
 def _ptr(a):

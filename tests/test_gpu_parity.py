@@ -246,6 +246,23 @@ def test_device_inputs_match_host(ctx):
     assert pl_h.tobytes() == pl_d.tobytes()
 
 
+def test_pack_batch_equals_single_packs(ctx):
+    """tabi_pack_batch (two contexts / host threads on one GPU here) gives the
+    same bytes as packing each atlas alone (S:457 determinism across jobs)."""
+    from paper_2602_07782_b200 import Context, OK, pack_batch, spec_of
+    sets = [chartgen.config5(i) for i in range(6)]
+    c2 = Context(0, max_charts=2100, max_vertices=1 << 17, max_atlas_side=2048)
+    c3 = Context(0, max_charts=2100, max_vertices=1 << 17, max_atlas_side=2048)
+    st, outs, infos = pack_batch([c2, c3], sets, [spec_of(cs) for cs in sets])
+    assert st == OK
+    for cs, pl, inf in zip(sets, outs, infos):
+        st1, pl1, inf1 = ctx.pack(cs.xy, cs.start, spec_of(cs))
+        assert st1 == OK and inf.scale_index == inf1.scale_index
+        assert pl.tobytes() == pl1.tobytes()
+    c2.close()
+    c3.close()
+
+
 def test_determinism_and_capacity_growth():
     from paper_2602_07782_b200 import Context, spec_of
     cs = chartgen.config3(1, rho=2.0)
