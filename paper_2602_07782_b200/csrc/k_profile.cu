@@ -75,7 +75,8 @@ __device__ void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i128 UXN
                         int64_t SC, int64_t nw, int64_t nh) {
   const int64_t N2 = C * C + S * S, DS = S * SC, DC = C * SC;
   const i128 N2SC = (i128)N2 * SC;
-  const double rDS = 1.0 / (double)DS, rDC = 1.0 / (double)DC, rN2SC = 1.0 / i128_to_double(N2SC);
+  const double rDS = rcp_approx((double)DS), rDC = rcp_approx((double)DC);
+  const double rN2SC = rcp_approx(i128_to_double(N2SC));
   const int64_t SCS = SC * S, SCC = SC * C;
   {  // LinDiv r
     i128 A;
@@ -176,7 +177,7 @@ __device__ void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, i
                             int64_t SC, int r) {
   const int c = H.c;
   const int32_t* sl = P.sl + (int64_t)c * 4 * k;
-  const double rSC = 1.0 / (double)SC;
+  const double rSC = rcp_approx((double)SC);
   for (int idx = r; idx < 2 * k; idx += 8) {
     const int ax = idx >= k, j = ax ? idx - k : idx;
     slice_job(tab + ax * 2 * k, sl + 2 * ax * k, sl + 2 * ax * k + k, j, num, SC, rSC);
@@ -216,7 +217,7 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
     num = pp.T.p[m - 1];
     SC = (int64_t)TABI_UNITS << 20;
   }
-  const double rSC = 1.0 / (double)SC;
+  const double rSC = rcp_approx((double)SC);
   const int ci = tid >> 3, r = tid & 7;
   if (ci < nt && r == 0 && s0 + ci < r0) {  // sequential chart: untouched in tail mode
     CH[ci].small = 0;
@@ -233,8 +234,8 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
     H.nh = num * h;
     H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
     H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
-    H.rnw = 1.0 / (double)H.nw;
-    H.rnh = 1.0 / (double)H.nh;
+    H.rnw = rcp_approx((double)H.nw);
+    H.rnh = rcp_approx((double)H.nh);
     H.j8 = P.obb_j[c];
     const int64_t b = (int64_t)(m - 1) * pp.n + s;
     wd_all[b] = H.ws + 2 * pp.g;
@@ -349,7 +350,7 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   int32_t* tab = dyn + wib * 4 * k;
   const int nbig = st->pad[1];
   const int64_t SC = pp.tail ? ((int64_t)TABI_UNITS << 20) : (int64_t)pp.M * TABI_UNITS;
-  const double rSC = 1.0 / (double)SC;
+  const double rSC = rcp_approx((double)SC);
   for (int it = blockIdx.x * kWarps + wib; it < nbig; it += gridDim.x * kWarps) {
     const int item = big_list[it];
     const int m = item / pp.n + 1, s = item % pp.n;
@@ -363,8 +364,8 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
       H.nh = num * P.h[c];
       H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
       H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
-      H.rnw = 1.0 / (double)H.nw;
-      H.rnh = 1.0 / (double)H.nh;
+      H.rnw = rcp_approx((double)H.nw);
+      H.rnh = rcp_approx((double)H.nh);
       H.j8 = P.obb_j[c];
     }
     __syncwarp();

@@ -44,8 +44,17 @@ __device__ __forceinline__ i128 ceildiv128(i128 a, i128 b) {
 // correction (no emulated 64/128-bit divide).  Exact for any operands: the
 // correction loops run until the remainder is in [0, b); with |a/b| < 2^50
 // the estimate is already within one unit so they run at most once or twice.
+// 1/b to ~1 ulp without the fp64 divide routine: MUFU.RCP in fp32, then two
+// Newton steps in fp64.  Only ever used as an estimate that an exact integer
+// correction follows, so its last bits do not matter.
+__device__ __forceinline__ double rcp_approx(double b) {
+  double r = (double)__frcp_rn((float)b);
+  r = r * (2.0 - b * r);
+  r = r * (2.0 - b * r);
+  return r;
+}
 __device__ __forceinline__ int64_t fdiv_fast(int64_t a, int64_t b) {
-  int64_t q = (int64_t)floor((double)a / (double)b);
+  int64_t q = (int64_t)floor((double)a * rcp_approx((double)b));
   int64_t r = a - q * b;
   while (r < 0) { q--; r += b; }
   while (r >= b) { q++; r -= b; }
@@ -56,7 +65,7 @@ __device__ __forceinline__ double i128_to_double(i128 a) {
   return (double)(int64_t)(a >> 64) * 18446744073709551616.0 + (double)(uint64_t)a;
 }
 __device__ __forceinline__ int64_t fdiv_fast128(i128 a, i128 b) {
-  int64_t q = (int64_t)floor(i128_to_double(a) / i128_to_double(b));
+  int64_t q = (int64_t)floor(i128_to_double(a) * rcp_approx(i128_to_double(b)));
   i128 r = a - (i128)q * b;
   while (r < 0) { q--; r += b; }
   while (r >= b) { q++; r -= b; }
@@ -83,7 +92,7 @@ __device__ __forceinline__ int64_t cdiv_rcp(i128 a, int64_t b, double rcp) {
 }
 // floor(a / b) clamped to [-2^40, 2^40] (callers compare it with small indices).
 __device__ __forceinline__ int64_t fdiv_clamp128(i128 a, i128 b) {
-  const double est = i128_to_double(a) / i128_to_double(b);
+  const double est = i128_to_double(a) * rcp_approx(i128_to_double(b));
   if (est > 1099511627776.0) return 1099511627776LL;
   if (est < -1099511627776.0) return -1099511627776LL;
   return fdiv_fast128(a, b);
@@ -99,7 +108,7 @@ struct LinDiv {
 __device__ __forceinline__ LinDiv make_lindiv(i128 A, int64_t B, int64_t D) {
   LinDiv L;
   L.D = D;
-  L.rcp = 1.0 / (double)D;
+  L.rcp = rcp_approx((double)D);
   L.qA = fdiv_fast128(A, (i128)D);
   L.rA = (int64_t)(A - mul_wide(L.qA, D));
   L.qB = fdiv_fast(B, D);
