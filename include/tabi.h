@@ -52,8 +52,10 @@ typedef struct {
   int32_t local_aabb_count;   /* k local AABBs per axis; paper 10 */
   int32_t t_opt_bp;           /* prefix-tail threshold, basis points of atlas_h;
                                  -1 = paper policy (0 if N <= 10000 else 100).
-                                 This build implements t_opt = 0 (sequential) only and
-                                 returns TABI_EINVAL if the effective value is > 0. */
+                                 > 0: hybrid mode -- a candidate switches to
+                                 prefix (FastAtlas) rows once no knee is pending and the
+                                 tallest chart of the next row is below t_opt * H; the
+                                 tail's scale is re-solved for sigma <= 1 (R3). */
   uint32_t flags;             /* TABI_F_* */
 } tabi_spec;
 
@@ -74,14 +76,16 @@ typedef struct {
   int32_t scale_num, scale_den;   /* scale = scale_num / scale_den = m / M */
   int32_t box_w, box_h;
   uint8_t rot90, flip_x, flip_y, mirror_x;
-  uint8_t mode;                   /* 0 = sequential row */
+  uint8_t mode;                   /* 0 = sequential row, 1 = prefix-tail row (scale
+                                     scale_num / scale_den = p / 2^20) */
   uint8_t pad[3];
 } tabi_placement;
 
 typedef struct {
   int32_t scale_index;            /* winning m (0 on NO_FIT) */
-  int32_t reserved0;
-  double l2_stretch;              /* Sander L2 stretch of the packed->input map; M/m */
+  int32_t fused;                  /* 1: waves ran as one fused persistent kernel (stages
+                                     [3] and [4] are then inside [5]); 0: split kernels */
+  double l2_stretch;             /* Sander L2 stretch of the packed->input map; M/m */
   int32_t rows, knees_found, knee_rows, prefix_rows;   /* winner's statistics */
   int32_t bad_chart;              /* first offending chart on EINVAL, else -1 */
   int32_t gpu_launches;           /* kernels launched by this call */
@@ -173,6 +177,14 @@ tabi_status tabi_debug_profile(tabi_ctx* ctx, int32_t m, int32_t s, int32_t* wd_
 /* Adjacent compacting advance off(s, s+1) and lock bits (bit0: s cannot move
  * above s+1, bit1: s+1 cannot move above s) for candidate m, n_charts entries. */
 tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* lockbits);
+/* Device timeline of the last wave (%globaltimer ns), 16 entries:
+ * [0] last raster group end and [1] last packer end, both from the fused
+ * kernel's first CTA start (0 if split); [2] packer ns waiting for tiles (sum
+ * over packers); [3] raster ns waiting for a left neighbour tile (sum);
+ * [4] tiles rasterized; [5] fused (0/1); [6..13] K4 row-phase ns summed over
+ * packers (knee update, fold, HC choice + lock pairs, push, Alg. 1, score,
+ * select + commit, FindKnee); [14..15] 0. */
+tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16);
 
 #ifdef __cplusplus
 }

@@ -16,11 +16,13 @@ SOURCES = ["tabi_api.cu", "k_proxy.cu", "k_sort.cu", "k_profile.cu", "k_pack.cu"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("TABI_NVCC_EXTRA", "").split()  # experiments, e.g. -DTABI_FUSED_RG=2
 
 
 def _deps():
     files = [os.path.join(CSRC, s) for s in SOURCES]
-    files += [os.path.join(CSRC, "tabi_internal.cuh"), os.path.join(ROOT, "include", "tabi.h")]
+    files += [os.path.join(CSRC, "tabi_internal.cuh"), os.path.join(CSRC, "k3_dev.cuh"),
+              os.path.join(ROOT, "include", "tabi.h")]
     return files
 
 

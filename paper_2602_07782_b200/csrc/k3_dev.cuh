@@ -1,0 +1,369 @@
+// k3_dev.cuh -- device-side footprint rasterization shared by the K3 kernels
+// (k_profile.cu) and the fused persistent pack kernel (k_pack.cu).
+// See k_profile.cu for the method (D11, D13).
+#pragma once
+#include "tabi_internal.cuh"
+
+namespace tabi {
+namespace k3 {
+
+constexpr int kRaw = 8192;   // raw cells per chunk (32 KB)
+// Per-(chart, candidate) constants.  OBB index q = axis * 2 + (0 low, 1 high);
+// lines lin[axis * 4 + kind]: kind 0 low-bound line right of the crossing
+// (at the cell's low edge), 1 low-bound line left of it (high edge, non-last
+// cells), 2 / 3 the same for the high bound (negated floors).
+struct ObbC {
+  LinDiv lin[8];
+  int64_t last[4];   // value at the clipped high edge of the last cell
+  int64_t star[4];   // value at the crossing
+  int64_t iA[4];     // crossing at or beyond cell i's low edge  <=>  i <= iA
+  int64_t iB[4];     // crossing at or before cell i's high edge <=>  i >= iB (non-last)
+  int32_t lastB[4];  // same test for the last cell (edge = chart extent)
+};
+
+struct ChartK3 {
+  int32_t s, c, ws, hs, j8, small;  // small: handled by the tile kernel
+  int32_t col_o, row_o;             // slot offsets in dcol / drow (candidate base added)
+  int64_t nw, nh;
+  double rnw, rnh;                  // 1 / (num * w), 1 / (num * h)
+  ObbC O;
+};
+
+// ---- setup jobs ---------------------------------------------------------
+// Slice entry: scaled floor of the low bound / ceil of the high bound.
+__device__ __forceinline__ void slice_job(int32_t* tab, const int32_t* blo, const int32_t* bhi, int j,
+                                          int64_t num, int64_t SC, double rSC) {
+  tab[2 * j] = (int32_t)fdiv_r64(num * blo[j], SC, rSC);
+  tab[2 * j + 1] = (int32_t)(-fdiv_r64(-num * bhi[j], SC, rSC));
+}
+
+// OBB job r (0..7) of a chart: LinDiv r, one of last/star, one of iA/iB.  The
+// box is {Umin <= xC + yS <= Umax, Vmin <= -xS + yC <= Vmax}; with num/SC:
+//  top    y_top(x)   = max((Umin - xC)/S, (Vmin + xS)/C)
+//  bottom y_bot(x)   = min((Umax - xC)/S, (Vmax + xS)/C)
+//  left   x_left(y)  = max((Umin - yS)/C, (yC - Vmax)/S)
+//  right  x_right(y) = min((Umax - yS)/C, (yC - Vmin)/S)
+__device__ inline void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i128 UXN, i128 VMN, i128 VXN,
+                        int64_t SC, int64_t nw, int64_t nh) {
+  const int64_t N2 = C * C + S * S, DS = S * SC, DC = C * SC;
+  const i128 N2SC = (i128)N2 * SC;
+  const double rDS = rcp_approx((double)DS), rDC = rcp_approx((double)DC);
+  const double rN2SC = rcp_approx(i128_to_double(N2SC));
+  const int64_t SCS = SC * S, SCC = SC * C;
+  {  // LinDiv r
+    i128 A;
+    int64_t B, D;
+    double rD;
+    switch (r) {
+      case 0: A = VMN; B = SCS; D = DC; rD = rDC; break;          // top, increasing line at P0
+      case 1: A = UMN - SCC; B = -SCC; D = DS; rD = rDS; break;   // top, decreasing line at P1
+      case 2: A = -UXN; B = SCC; D = DS; rD = rDS; break;         // bottom, decreasing at P0 (neg)
+      case 3: A = -VXN - SCS; B = -SCS; D = DC; rD = rDC; break;  // bottom, increasing at P1 (neg)
+      case 4: A = -VXN; B = SCC; D = DS; rD = rDS; break;         // left, increasing at Q0
+      case 5: A = UMN - SCS; B = -SCS; D = DC; rD = rDC; break;   // left, decreasing at Q1
+      case 6: A = -UXN; B = SCS; D = DC; rD = rDC; break;         // right, decreasing at Q0 (neg)
+      default: A = VMN - SCC; B = -SCC; D = DS; rD = rDS; break;  // right, increasing at Q1 (neg)
+    }
+    LinDiv L;
+    L.D = D;
+    L.rcp = rD;
+    L.qA = fdiv_r128(A, (i128)D, rD, false);
+    L.rA = (int64_t)(A - mul_wide(L.qA, D));
+    L.qB = fdiv_r64(B, D, rD);
+    L.rB = B - L.qB * D;
+    O.lin[r] = L;
+  }
+  const int q = r & 3;
+  if (r < 4) {  // value at the last cell's clipped edge
+    int64_t v;
+    switch (q) {
+      case 0: v = fdiv_r128(UMN - mul_wide(nw, C), (i128)DS, rDS, false); break;
+      case 1: v = -fdiv_r128(-(VXN + mul_wide(nw, S)), (i128)DC, rDC, false); break;
+      case 2: v = fdiv_r128(UMN - mul_wide(nh, S), (i128)DC, rDC, false); break;
+      default: v = -fdiv_r128(-(mul_wide(nh, C) - VMN), (i128)DS, rDS, false); break;
+    }
+    O.last[q] = v;
+  } else {  // value at the crossing
+    int64_t v;
+    switch (q) {
+      case 0: v = fdiv_r128((i128)S * UMN + (i128)C * VMN, N2SC, rN2SC, false); break;
+      case 1: v = -fdiv_r128(-((i128)S * UXN + (i128)C * VXN), N2SC, rN2SC, false); break;
+      case 2: v = fdiv_r128((i128)C * UMN - (i128)S * VXN, N2SC, rN2SC, false); break;
+      default: v = -fdiv_r128(-((i128)C * UXN - (i128)S * VMN), N2SC, rN2SC, false); break;
+    }
+    O.star[q] = v;
+  }
+  i128 cross;
+  switch (q) {
+    case 0: cross = (i128)C * UMN - (i128)S * VMN; break;   // x* of the top boundary
+    case 1: cross = (i128)C * UXN - (i128)S * VXN; break;   // x** of the bottom
+    case 2: cross = (i128)S * UMN + (i128)C * VXN; break;   // y* of the left
+    default: cross = (i128)S * UXN + (i128)C * VMN; break;  // y** of the right
+  }
+  if (r < 4) {
+    O.iA[q] = fdiv_r128(cross, N2SC, rN2SC, true);
+    O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
+  } else {
+    O.iB[q] = -fdiv_r128(-cross, N2SC, rN2SC, true) - 1;
+  }
+}
+
+// Raw (undilated) bounds of cell i on axis ax (0: column -> (Top, Bottom),
+// 1: row -> (Left, Right)), packed lo | hi << 16.
+__device__ __forceinline__ uint32_t raw_cell(const ChartK3& H, const int32_t* tab, int k, int ax,
+                                             int64_t i, int64_t num, int64_t SC) {
+  const int64_t nx = ax ? H.nh : H.nw;
+  const double rnx = ax ? H.rnh : H.rnw;
+  const int64_t SCk = SC * k;
+  int64_t jl = fdiv_r64(i * SCk, nx, rnx);
+  int64_t jh = -fdiv_r64(-(i + 1) * SCk, nx, rnx) - 1;
+  if (jl < 0) jl = 0;
+  if (jh > k - 1) jh = k - 1;
+  const int32_t* t = tab + ax * 2 * k;
+  int32_t lo = INT32_MAX, hi = INT32_MIN;
+  for (int64_t j = jl; j <= jh; j++) {
+    lo = min(lo, t[2 * j]);
+    hi = max(hi, t[2 * j + 1]);
+  }
+  const int64_t cnt = ax ? H.hs : H.ws;
+  int64_t L = max(0, lo), Hh = min((int64_t)hi, ax ? (int64_t)H.ws : (int64_t)H.hs);
+  if (H.j8 != 0) {
+    const ObbC& O = H.O;
+    const bool last = i == cnt - 1;
+    const int q0 = 2 * ax, q1 = 2 * ax + 1;
+    int64_t v;
+    if (i <= O.iA[q0] && (last ? O.lastB[q0] != 0 : i >= O.iB[q0])) v = O.star[q0];
+    else if (i > O.iA[q0]) v = lindiv_eval(O.lin[4 * ax + 0], i);
+    else v = last ? O.last[q0] : lindiv_eval(O.lin[4 * ax + 1], i);
+    L = max(L, v);
+    if (i <= O.iA[q1] && (last ? O.lastB[q1] != 0 : i >= O.iB[q1])) v = O.star[q1];
+    else if (i > O.iA[q1]) v = -lindiv_eval(O.lin[4 * ax + 2], i);
+    else v = last ? O.last[q1] : -lindiv_eval(O.lin[4 * ax + 3], i);
+    Hh = min(Hh, v);
+  }
+  return (uint32_t)L | ((uint32_t)Hh << 16);
+}
+
+// Setup of one chart by 8 cooperating threads r = 0..7 (rank r).
+__device__ inline void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, int64_t num,
+                            int64_t SC, int r) {
+  const int c = H.c;
+  const int32_t* sl = P.sl + (int64_t)c * 4 * k;
+  const double rSC = rcp_approx((double)SC);
+  for (int idx = r; idx < 2 * k; idx += 8) {
+    const int ax = idx >= k, j = ax ? idx - k : idx;
+    slice_job(tab + ax * 2 * k, sl + 2 * ax * k, sl + 2 * ax * k + k, j, num, SC, rSC);
+  }
+  if (H.j8 != 0) {
+    const int64_t* ob = P.obb + 4 * (int64_t)c;
+    obb_job(H.O, r, kQC[H.j8], kQS[H.j8], mul_wide(ob[0], num), mul_wide(ob[1], num),
+            mul_wide(ob[2], num), mul_wide(ob[3], num), SC, H.nw, H.nh);
+  }
+}
+
+// Warp per large chart (raw cells > kRaw) from the compacted list; raw values
+// go straight into the HBM slot, then an in-place dilation.
+__device__ inline void dilate_slot(uint32_t* slot, int32_t n0, int32_t g, int lane) {
+  const int32_t nd = n0 + 2 * g;
+  for (int base = 0; base < nd; base += 32) {
+    const int i = base + lane;
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    if (i < nd) {
+      const int q0 = max(0, i - 2 * g), q1 = min(i, n0 - 1);
+      for (int q = q0; q <= q1; q++) {
+        const uint32_t v = slot[q + 2 * g];
+        lo = min(lo, lo16(v));
+        hi = max(hi, hi16(v));
+      }
+    }
+    __syncwarp();
+    if (i < nd) slot[i] = (uint32_t)lo | ((uint32_t)(hi + 2 * g) << 16);
+    __syncwarp();
+  }
+}
+
+// Scale of candidate m: m/M, or in tail mode the prefix tail's p / 2^20 (D24).
+struct Scale {
+  int64_t num, SC;
+  int32_t r0;  // first sorted position rasterized (tail mode), else 0
+};
+
+// Rasterize the footprints of the TC charts [s0, s0 + TC) of candidate m with
+// TT threads (8 per chart during setup).  Charts that fit the dilated atlas but
+// have more than kRaw raw cells are left for a warp-per-chart pass: their tile
+// index is flagged in big[ci].  Writes wd/hd, the footprint slots, cand_bad.
+template <int TC, int TT, int RAW, class Sync>
+__device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, const PackParams& pp,
+                            const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
+                            uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all,
+                            int32_t* cand_bad, int m, int s0, Scale sc, ChartK3* CH,
+                            int32_t* cells, int32_t* cpre, int32_t* opre, int32_t* chunk_end,
+                            int32_t* big, int32_t* tabs, uint32_t* raw, int tid, Sync sync) {
+  const int k = pp.k, g = pp.g;
+  const int nt = min(TC, pp.n - s0);
+  const int64_t num = sc.num, SC = sc.SC;
+  const double rSC = rcp_approx((double)SC);
+  const int ci = tid >> 3, r = tid & 7;
+  if (ci < TC && r == 0) {
+    cells[ci] = 0;
+    big[ci] = 0;
+    CH[ci].small = 0;
+  }
+  if (ci < nt && r == 0 && s0 + ci >= sc.r0) {
+    ChartK3& H = CH[ci];
+    const int s = s0 + ci;
+    const int c = perm[s];
+    const int64_t w = P.w[c], h = P.h[c];
+    H.s = s;
+    H.c = c;
+    H.nw = num * w;
+    H.nh = num * h;
+    H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
+    H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
+    H.rnw = rcp_approx((double)H.nw);
+    H.rnh = rcp_approx((double)H.nh);
+    H.j8 = P.obb_j[c];
+    const int64_t b = (int64_t)(m - 1) * pp.n + s;
+    wd_all[b] = H.ws + 2 * g;
+    hd_all[b] = H.hs + 2 * g;
+    const bool fits = H.ws + 2 * g <= pp.Wp && H.hs + 2 * g <= pp.Hp;
+    if (!fits) cand_bad[m - 1] = 1;
+    H.small = fits && (H.ws + H.hs <= RAW);
+    big[ci] = fits && !H.small;
+    H.col_o = colofs[s];
+    H.row_o = rowofs[s];
+    cells[ci] = H.small ? H.ws + H.hs : 0;
+  }
+  sync();
+  if (ci < nt && CH[ci].small) chart_setup(CH[ci], tabs + ci * 4 * k, P, k, num, SC, r);
+  sync();
+  uint32_t* colb = dcol + (int64_t)(m - 1) * pp.col_cap;
+  uint32_t* rowb = drow + (int64_t)(m - 1) * pp.row_cap;
+  int cb = 0;
+  while (cb < nt && cells[cb] == 0) cb++;
+  while (cb < nt) {
+    if (tid == 0) {  // chunk [cb, ce): raw cells fit the buffer
+      int e = cb, tot = 0, otot = 0;
+      cpre[0] = 0;
+      opre[0] = 0;
+      while (e < nt && tot + cells[e] <= RAW) {
+        tot += cells[e];
+        otot += cells[e] ? cells[e] + 4 * g : 0;
+        e++;
+        cpre[e - cb] = tot;
+        opre[e - cb] = otot;
+      }
+      *chunk_end = e;
+    }
+    sync();
+    const int ce = *chunk_end, nc = ce - cb;
+    const int32_t ncell = cpre[nc], nout = opre[nc];
+    for (int e = tid; e < ncell; e += TT) {  // raw pass over the chunk's flattened cells
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cpre[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const ChartK3& H = CH[cb + lo];
+      const int32_t x = e - cpre[lo];
+      const int ax = x >= H.ws;
+      raw[e] = raw_cell(H, tabs + (cb + lo) * 4 * k, k, ax, ax ? x - H.ws : x, num, SC);
+    }
+    sync();
+    for (int o = tid; o < nout; o += TT) {  // dilation over the flattened outputs
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (opre[mid] <= o) lo = mid;
+        else hi = mid - 1;
+      }
+      const ChartK3& H = CH[cb + lo];
+      const int32_t y = o - opre[lo];
+      const int Wd = H.ws + 2 * g;
+      const int ax = y >= Wd;
+      const int32_t i = ax ? y - Wd : y;
+      const int32_t n0 = ax ? H.hs : H.ws;
+      const uint32_t* rr = raw + cpre[lo] + (ax ? H.ws : 0);
+      const int q0 = max(0, i - 2 * g), q1 = min(i, n0 - 1);
+      int32_t vl = INT32_MAX, vh = INT32_MIN;
+      for (int q = q0; q <= q1; q++) {
+        const uint32_t v = rr[q];
+        vl = min(vl, lo16(v));
+        vh = max(vh, hi16(v));
+      }
+      (ax ? rowb + H.row_o : colb + H.col_o)[i] = (uint32_t)vl | ((uint32_t)(vh + 2 * g) << 16);
+    }
+    sync();
+    cb = ce;
+    while (cb < nt && cells[cb] == 0) cb++;  // skip charts handled elsewhere
+    sync();
+  }
+}
+
+// One large chart (sorted position s, candidate m) by one warp: raw values
+// straight into the HBM slot, then an in-place dilation.
+__device__ inline void big_chart(const Proxies& P, const int32_t* __restrict__ perm, const PackParams& pp,
+                          const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
+                          uint32_t* dcol, uint32_t* drow, int m, int s, Scale sc, ChartK3& H,
+                          int32_t* tab, int lane) {
+  const int k = pp.k;
+  const int64_t num = sc.num, SC = sc.SC;
+  const double rSC = rcp_approx((double)SC);
+  if (lane == 0) {
+    const int c = perm[s];
+    H.s = s;
+    H.c = c;
+    H.nw = num * P.w[c];
+    H.nh = num * P.h[c];
+    H.ws = (int32_t)(-fdiv_r64(-H.nw, SC, rSC));
+    H.hs = (int32_t)(-fdiv_r64(-H.nh, SC, rSC));
+    H.rnw = rcp_approx((double)H.nw);
+    H.rnh = rcp_approx((double)H.nh);
+    H.j8 = P.obb_j[c];
+  }
+  __syncwarp();
+  if (lane < 8) chart_setup(H, tab, P, k, num, SC, lane);
+  __syncwarp();
+  uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
+  uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
+  for (int64_t e = lane; e < (int64_t)H.ws + H.hs; e += 32) {
+    const int ax = e >= H.ws;
+    const int64_t i = ax ? e - H.ws : e;
+    (ax ? row : col)[i + 2 * pp.g] = raw_cell(H, tab, k, ax, i, num, SC);
+  }
+  __syncwarp();
+  dilate_slot(col, H.ws, pp.g, lane);
+  dilate_slot(row, H.hs, pp.g, lane);
+  __syncwarp();
+}
+
+// Compaction advance off(s, s+1) and CannotMoveAbove bits of the adjacent
+// pair, by one warp (D14, D15).  The footprint arrays
+// are plain (coherent) loads: in the fused kernel another CTA wrote chart s.
+__device__ __forceinline__ void pair_offset(const PackParams& pp, const int32_t* __restrict__ rowofs,
+                                            const uint32_t* drow, const int32_t* wd_all,
+                                            const int32_t* hd_all, int32_t* off_all,
+                                            uint8_t* lock_all, int m, int s, int lane) {
+  const int64_t base = (int64_t)(m - 1) * pp.n;
+  if (s == pp.n - 1) {
+    if (lane == 0) { off_all[base + s] = 0; lock_all[base + s] = 0; }
+    return;
+  }
+  const int32_t Hda = hd_all[base + s], Hdb = hd_all[base + s + 1], Wda = wd_all[base + s];
+  const uint32_t* ra = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
+  const uint32_t* rb = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s + 1];
+  const int rows = min(Hda, Hdb);
+  int32_t off = 0;
+  for (int j = lane; j < rows; j += 32) off = max(off, hi16(ra[j]) - lo16(rb[j]));
+  off = warp_max(off);
+  bool la = false, lb = false;
+  if (off < Wda) warp_locks(ra, rb, Hda, Hdb, off, lane, la, lb);
+  if (lane == 0) {
+    off_all[base + s] = off;
+    lock_all[base + s] = (uint8_t)((la ? 1 : 0) | (lb ? 2 : 0));
+  }
+}
+
+}  // namespace k3
+}  // namespace tabi

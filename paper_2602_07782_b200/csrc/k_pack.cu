@@ -28,7 +28,7 @@
 // "enable horizontal compacting if it allows more charts to fit"), so each
 // fold pushes 2 directions instead of 4 configurations, with identical
 // results.
-#include "tabi_internal.cuh"
+#include "k3_dev.cuh"
 
 namespace tabi {
 namespace {
@@ -124,7 +124,9 @@ template <class Enter, class Body, class Leave>
 __device__ __forceinline__ void walk(const Win& w, int nwin, Enter enter, Body body, Leave leave) {
   const int32_t base0 = w.rx0[0];
   const int32_t T = w.rx0[nwin - 1] - base0 + w.rwd[nwin - 1];
-  const int32_t C = (T + kNT - 1) / kNT;
+  // run length per thread, forced odd: lanes then hit F / the staged footprints
+  // at addresses C apart, i.e. 32 distinct shared-memory banks per warp access
+  const int32_t C = ((T + kNT - 1) / kNT) | 1;
   int32_t t = threadIdx.x * C;
   const int32_t tend = min(T, t + C);
   if (t >= tend) return;
@@ -146,21 +148,56 @@ __device__ __forceinline__ void walk(const Win& w, int nwin, Enter enter, Body b
   }
 }
 
-__global__ void __launch_bounds__(kNT, 1)
-pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
-            const uint32_t* __restrict__ dcol, const uint32_t* __restrict__ drow,
-            const int32_t* __restrict__ wd_all, const int32_t* __restrict__ hd_all,
-            const int32_t* __restrict__ off_all, const uint8_t* __restrict__ lock_all,
-            const int32_t* __restrict__ hsorted, const int32_t* __restrict__ cand_bad,
+// Fused-mode readiness: tile t (charts [t*tcf, (t+1)*tcf)) of wave slot j is
+// published by a rasterizer CTA: rdy = 1 footprints written, 2 also the
+// adjacent-pair offsets/locks of the pairs ending in the tile.
+struct Ready {
+  int32_t* flags;  // [B][T] or nullptr (non-fused: everything precomputed)
+  int32_t T, tcf;
+};
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The footprint/offset arrays are not __restrict__ here: in fused mode other
+// CTAs write them during the launch, so they must not go through the
+// non-coherent load path.
+__device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict__ colofs,
+            const int32_t* __restrict__ rowofs,
+            const uint32_t* dcol, const uint32_t* drow,
+            const int32_t* wd_all, const int32_t* hd_all,
+            const int32_t* off_all, const uint8_t* lock_all,
+            const int32_t* __restrict__ hsorted, const int32_t* cand_bad,
             int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
-            Cand* cands, Status* st, int32_t prof_cap) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+            Cand* cands, Status* st, int32_t prof_cap, int jslot, Ready rd, unsigned char* dsm) {
   __shared__ Smem S;
+  __shared__ int32_t ready_upto;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int m = wave_m(pp, st->pad[2], blockIdx.x);
+  const int m = wave_m(pp, st->pad[2], jslot);
   if (m == 0) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
+  // wait until every sorted position <= s_hi has its footprints, width/height
+  // and the offset of the pair (s, s+1) published (fused mode only)
+  if (tid == 0) ready_upto = -1;
+  auto wait_upto = [&](int s_hi) {
+    if (!rd.flags) return;
+    const int t_req = min(rd.T - 1, min(s_hi + 1, n - 1) / rd.tcf);
+    if (tid == 0 && ready_upto < t_req) {
+      int32_t* fl = rd.flags + (int64_t)jslot * rd.T;
+      const unsigned long long t0 = gtime();
+      while (ready_upto < t_req) {
+        while (ld_acquire(fl + ready_upto + 1) < 2) __nanosleep(64);
+        ready_upto++;
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
+      atomicAdd(&st->tr[3], gtime() - t0);
+    }
+    __syncthreads();
+  };
   const int64_t cb = (int64_t)(m - 1) * n;
   const int32_t* wd = wd_all + cb;
   const int32_t* hd = hd_all + cb;
@@ -199,11 +236,11 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   int32_t* qrow = sc + 5 * (int64_t)n;    // prefix row id per sorted position (tail)
   if (prefix_mode) {
     if (pp.T.state[m - 1] != TAIL_READY) return;
-  } else if (cand_bad[m - 1]) {  // some chart exceeds the dilated atlas at this scale
+  } else if (!rd.flags && cand_bad[m - 1]) {  // a chart exceeds the dilated atlas at this scale
     if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
     return;
   }
-  if (!prefix_mode) {  // work accounting: footprint entries K3 produced for this candidate
+  if (!prefix_mode && !rd.flags) {  // work accounting: footprint entries K3 produced
     unsigned long long pe = 0;
     for (int s = tid; s < n; s += kNT) pe += (unsigned long long)(wd[s] + hd[s]);
     for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
@@ -228,6 +265,15 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   __syncthreads();
   uint32_t phase = 0;
   unsigned long long wk = 0;  // frontline column visits by this thread
+  // row-phase timing (thread 0, %globaltimer; a few reads per row)
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t_last = gtime();
+  auto phase_mark = [&](int i) {
+    if (tid == 0) {
+      const unsigned long long t = gtime();
+      ph[i] += t - t_last;
+      t_last = t;
+    }
+  };
 
   // Stage window [ws0, we) of the current row (no-op if already staged).
   auto stage = [&](int ws0, int we) {
@@ -264,6 +310,14 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     if (!prefix_mode && pp.t_opt > 0 && !S.knee_valid) {
       const int64_t hs0 = ceildiv((int64_t)hsorted[rs] * m, (int64_t)pp.M * TABI_UNITS);
       if (hs0 * 10000 < (int64_t)pp.t_opt * pp.H) {
+        if (rd.flags) {  // fused: the split path never switches a candidate with a bad chart
+          wait_upto(n - 1);
+          if (__ldcg(cand_bad + m - 1)) {
+            if (tid == 0) S.fail = 1;
+            __syncthreads();
+            break;
+          }
+        }
         for (int x = tid; x < Wp; x += kNT) fsave[x] = F[x];
         if (tid == 0) {
           pp.T.state[m - 1] = TAIL_LAYOUT;
@@ -307,6 +361,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       }
       __syncthreads();
     }
+    phase_mark(0);
     const int32_t kv = S.knee_valid;
     const int32_t ka = kv ? (S.knee_ltr ? S.knee_right : 0) : 0;  // knee fold region [ka, kb)
     const int32_t kb = kv ? (S.knee_ltr ? Wp : S.knee_left) : 0;
@@ -341,11 +396,15 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     } else {
       int32_t carry0 = 0, carry1 = 0;
       for (int base = rs;; base += kNT) {
+        wait_upto(base + kNT - 1);
         if (tid < 4) S.fmin[tid] = INT32_MAX;
         const int s = base + tid;
         const bool valid = s < n;
         const int32_t w_s = valid ? wd[s] : 0;
         const int32_t a1 = valid ? off[s] : 0;
+        // fused mode: a chart that cannot fit the dilated atlas at this scale
+        // makes the candidate fail (it must be placed in some row)
+        if (rd.flags && valid && (w_s > Wp || hd[s] > Hp)) S.fail = 1;
         int32_t e0, e1, t0, t1;
         block_scan2(w_s, a1, e0, e1, t0, t1, S);
         const int32_t x0 = carry0 + e0, x1 = carry1 + e1;
@@ -373,6 +432,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         carry1 += t1;
       }
     }  // !prefix_mode
+    phase_mark(1);
     // ---- level 1 of the hierarchical choice: HC iff it fits more --
     if (tid == 0) {
       S.hcsel[0] = (!no_hc && S.endv[1] > S.endv[0]) ? 1 : 0;
@@ -442,6 +502,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       __syncthreads();
     }
     const int32_t np = S.npairs;
+    phase_mark(2);
 
     // per-configuration geometry of chart (window index i, sorted s): X
     auto cfgX = [&](int cfg, int i) -> int32_t {
@@ -453,6 +514,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     };
 
     // ---- push: Y = max over covered columns of F - TopEdge ----
+    // A row of at most kRW charts (the normal case) is one window: its Y
+    // values then live in shared memory from push to commit; longer rows
+    // round-trip them through Yc in HBM per window.
+    const bool one = endA - rs + 1 <= kRW;
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
       stage(ws0, we);
@@ -483,6 +548,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
             for (int q = 0; q < nact; q++) atomicMax(&W.rY[q * kRW + i], mx[q]);
           });
       __syncthreads();
+      if (one) continue;  // Y stays in shared memory for Alg. 1, score and commit
       for (int k = tid; k < nwin; k += kNT) {
         const int s = ws0 + k;
         const int na = (knee_ok && s <= endK) ? 4 : 2;
@@ -490,6 +556,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       }
       __syncthreads();
     }
+    phase_mark(3);
     // ---- Alg. 1 CorrectYOffsets over adjacent + non-adjacent pairs ---------
     {
       const int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // HC configs [c0, c1)
@@ -515,9 +582,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
               if (b > endc) continue;
               bits = plk[p];
             }
-            int32_t* Ya = &Yc[(int64_t)cfg * n + a];
-            int32_t* Yb = &Yc[(int64_t)cfg * n + b];
-            const int32_t ya = __ldcg(Ya), yb = __ldcg(Yb);
+            int32_t* Ya = one ? &W.rY[cfg * kRW + (a - rs)] : &Yc[(int64_t)cfg * n + a];
+            int32_t* Yb = one ? &W.rY[cfg * kRW + (b - rs)] : &Yc[(int64_t)cfg * n + b];
+            const int32_t ya = one ? *(volatile int32_t*)Ya : __ldcg(Ya);
+            const int32_t yb = one ? *(volatile int32_t*)Yb : __ldcg(Yb);
             if ((bits & 1) && ya < yb) { atomicMax(Ya, yb); S.changed = 1; }
             if ((bits & 2) && yb < ya) { atomicMax(Yb, ya); S.changed = 1; }
           }
@@ -527,13 +595,14 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
         }
       }
     }
+    phase_mark(4);
     // ---- score: max over covered columns of Y + BottomEdge ----
     {
       int32_t nm[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
       for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
         const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
         stage(ws0, we);
-        for (int k = tid; k < nwin; k += kNT) {
+        for (int k = tid; k < nwin && !one; k += kNT) {
           const int s = ws0 + k;
           const int na = (knee_ok && s <= endK) ? 4 : 2;
           for (int q = 0; q < na; q++) W.rY[q * kRW + k] = __ldcg(&Yc[(int64_t)q * n + s]);
@@ -564,6 +633,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       }
     }
     __syncthreads();
+    phase_mark(5);
     // ---- hierarchical selection -----------------------------------
     if (tid == 0) {
       const int32_t sw0 = max(S.fmax, S.newmax[0]), sw1 = max(S.fmax, S.newmax[1]);
@@ -590,15 +660,17 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
     for (int ws0 = rs; ws0 <= endS; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = min(we, endS + 1) - ws0;
       stage(ws0, we);
-      for (int k = tid; k < nwin; k += kNT) W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
+      for (int k = tid; k < nwin && !one; k += kNT)
+        W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
       __syncthreads();
       const uint32_t* pr = S.pglobal ? col : W.prof;
+      const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
       int32_t Xc = 0, Yv = 0, Wd = 0;
       walk(
           W, nwin,
           [&](int i, int32_t j0) {
             Xc = cfgX(cfg, i);
-            Yv = W.rY[i];
+            Yv = rYc[i];
             Wd = W.rwd[i];
             if (j0 == 0) {
               const int s = ws0 + i;
@@ -616,6 +688,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
           [&](int) {});
       __syncthreads();
     }
+    phase_mark(6);
     // ---- FindKnee after an atlas-fold row -----------
     if (f == 0 && !no_bal && !prefix_mode) {
       for (int t = rs + tid; t < endS; t += kNT) {
@@ -648,9 +721,22 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       S.row_start = endS + 1;
     }
     __syncthreads();
+    phase_mark(7);
   }
+  if (tid == 0)
+    for (int i = 0; i < 8; i++) atomicAdd(&st->ph[i], ph[i]);
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
   if (lane == 0) atomicAdd(&st->work_pack, wk);
+  if (rd.flags && tid == 0) atomicMax(&st->tr[2], gtime());
+  if (rd.flags && S.fail) {
+    // fused mode: report a chart that exceeds the dilated atlas the way the
+    // split path does (the whole candidate's footprints must be in first)
+    wait_upto(n - 1);
+    if (tid == 0 && __ldcg(cand_bad + m - 1)) {
+      cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
+      return;
+    }
+  }
   if (tid == 0 && !S.switched) {
     Cand cd{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1, -1, 0, 0ull, 0ull};
     if (prefix_mode) {  // keep the tail's area (written by the layout kernel)
@@ -662,6 +748,163 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
       cd.apre_hi = prev.apre_hi;
     }
     cands[m - 1] = cd;
+  }
+}
+
+__global__ void __launch_bounds__(kNT, 1)
+pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
+            const uint32_t* __restrict__ dcol, const uint32_t* __restrict__ drow,
+            const int32_t* __restrict__ wd_all, const int32_t* __restrict__ hd_all,
+            const int32_t* __restrict__ off_all, const uint8_t* __restrict__ lock_all,
+            const int32_t* __restrict__ hsorted, const int32_t* __restrict__ cand_bad,
+            int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
+            Cand* cands, Status* st, int32_t prof_cap) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  packer(pp, colofs, rowofs, dcol, drow, wd_all, hd_all, off_all, lock_all, hsorted, cand_bad,
+         scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, blockIdx.x,
+         Ready{nullptr, 0, 0}, dsm);
+}
+
+// ---- fused persistent kernel: one cooperative launch per candidate wave ----
+// CTAs [0, B) are packers (one candidate each); every other CTA runs kRG
+// independent raster groups of kRGT threads (named barriers 1..kRG), each
+// taking tiles of kTCF sorted charts of one candidate from a work queue in
+// sorted (tile-major) order: footprints, then the adjacent-pair offsets and
+// locks.  Each tile is published with a release flag that the packers acquire
+// before reading it.  K3/K3b thus run on the SMs the packers leave idle and
+// overlap with the row loop; no host round trip inside the wave.  Several
+// groups per SM hide the latency of one group's setup / barrier phases the
+// way several resident CTAs do in the split kernels.
+#ifndef TABI_FUSED_RG
+#define TABI_FUSED_RG 1
+#endif
+constexpr int kRG = TABI_FUSED_RG;  // raster groups per CTA
+constexpr int kRGT = kNT / kRG;     // threads per group (8 per chart in setup)
+constexpr int kTCF = kRGT / 8;      // charts per raster tile
+constexpr int kRGW = kRGT / 32;    // warps per group
+constexpr int kRawF = 16384 / kRG;  // raw cells per group chunk (64 KB per CTA)
+static_assert(kTCF * 8 == kRGT, "setup maps 8 threads to a chart");
+
+struct GroupSync {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRGT) : "memory");
+  }
+};
+
+struct RasterArgs {
+  Proxies P;
+  const int32_t* perm;
+  int32_t* wd;
+  int32_t* hd;
+  int32_t* off;
+  uint8_t* lock;
+  int32_t* cand_bad;
+  uint32_t* dcol;
+  uint32_t* drow;
+  int32_t* rdy;
+};
+
+__host__ __device__ __forceinline__ size_t r16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+// per-group carve of the dynamic shared memory
+__host__ __device__ __forceinline__ size_t group_bytes(int k) {
+  return r16(sizeof(k3::ChartK3) * kTCF) + r16(4 * kTCF) + 2 * r16(4 * (kTCF + 1)) +
+         r16(4 * kTCF) + r16(16) + r16((size_t)4 * kTCF * 4 * k) + r16(4 * (size_t)kRawF);
+}
+
+__device__ __forceinline__ unsigned char* carve(unsigned char*& p, size_t bytes) {
+  unsigned char* r = p;
+  p += r16(bytes);
+  return r;
+}
+
+__global__ void __launch_bounds__(kNT, 1)
+fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
+             const int32_t* __restrict__ hsorted, int32_t* scratch, int64_t pair_cap,
+             int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all, Cand* cands, Status* st,
+             int32_t prof_cap, RasterArgs ra) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int T = (pp.n + kTCF - 1) / kTCF;
+  if (threadIdx.x == 0) atomicMin(&st->tr[0], gtime());
+  if ((int)blockIdx.x < pp.B) {
+    packer(pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, hsorted,
+           ra.cand_bad, scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap,
+           blockIdx.x, Ready{ra.rdy, T, kTCF}, dsm);
+    return;
+  }
+  // ---- rasterizer role ----
+  if (st->bad_chart != INT32_MAX || st->capacity) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int grp = tid / kRGT, gt = tid % kRGT, gw = gt >> 5;
+  const GroupSync gsync{1 + grp};
+  const int k = pp.k;
+  unsigned char* p = dsm + group_bytes(k) * grp;
+  k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kTCF);
+  int32_t* cells = (int32_t*)carve(p, 4 * kTCF);
+  int32_t* cpre = (int32_t*)carve(p, 4 * (kTCF + 1));
+  int32_t* opre = (int32_t*)carve(p, 4 * (kTCF + 1));
+  int32_t* big = (int32_t*)carve(p, 4 * kTCF);
+  int32_t* misc = (int32_t*)carve(p, 16);
+  int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kTCF * 4 * k);
+  uint32_t* raw = (uint32_t*)carve(p, 4 * (size_t)kRawF);
+  p = dsm + group_bytes(k) * kRG;  // per-warp large-chart state
+  k3::ChartK3* CW = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kNW);
+  int32_t* wtab = (int32_t*)carve(p, (size_t)4 * kNW * 4 * k);
+  const int32_t m_hi = st->pad[2];
+  const int NB = T * pp.B;
+  const int64_t SCm = (int64_t)pp.M * TABI_UNITS;
+  while (true) {
+    if (gt == 0) misc[0] = atomicAdd(&st->work_next, 1);
+    gsync();
+    const int it = misc[0];
+    gsync();
+    if (it >= NB) {
+      if (gt == 0) atomicMax(&st->tr[1], gtime());
+      break;
+    }
+    const int t = it / pp.B, j = it % pp.B;
+    const int m = wave_m(pp, m_hi, j);
+    if (m == 0) continue;
+    const int s0 = t * kTCF, nt = min(kTCF, pp.n - s0);
+    const k3::Scale sc{m, SCm, 0};
+    k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
+                                       ra.hd, ra.cand_bad, m, s0, sc, CH, cells, cpre, opre,
+                                       &misc[1], big, tabs, raw, gt, gsync);
+    for (int ci = gw; ci < nt; ci += kRGW)
+      if (big[ci])
+        k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m, s0 + ci, sc, CW[wid],
+                      wtab + wid * 4 * k, lane);
+    if (gt < 32) {  // work accounting: footprint entries of the tile
+      unsigned long long pe = 0;
+      if (gt < nt)
+        pe = (unsigned long long)(ra.wd[(int64_t)(m - 1) * pp.n + s0 + gt] +
+                                  ra.hd[(int64_t)(m - 1) * pp.n + s0 + gt]);
+      for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
+      if (gt == 0) atomicAdd(&st->work_prof, pe);
+    }
+    gsync();
+    int32_t* fl = ra.rdy + (int64_t)j * T;
+    if (gt == 0) {
+      __threadfence();
+      atomicExch(fl + t, 1);  // footprints of tile t published
+      atomicAdd(&st->tr[5], 1ull);
+      if (t > 0 && ld_acquire(fl + t - 1) < 1) {  // left neighbour's footprints
+        const unsigned long long t0 = gtime();
+        while (ld_acquire(fl + t - 1) < 1) __nanosleep(32);
+        atomicAdd(&st->tr[4], gtime() - t0);
+      }
+    }
+    gsync();
+    // pairs (s, s+1) for s in [s0 - 1, s0 + nt - 2] (+ the last chart's zero entry)
+    const int lo = max(0, s0 - 1), hi = (s0 + nt == pp.n) ? pp.n - 1 : s0 + nt - 2;
+    for (int s = lo + gw; s <= hi; s += kRGW)
+      k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
+    gsync();
+    if (gt == 0) {
+      __threadfence();
+      atomicExch(fl + t, 2);  // offsets of the pairs ending in tile t published
+    }
   }
 }
 
@@ -742,6 +985,48 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
   pack_kernel<<<pp.B, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
                                              hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
                                              cands, st, prof_cap);
+}
+
+int fused_grid(int device) {
+  static int cached[64];
+  static bool have[64];
+  if (device < 0 || device >= 64) return 0;
+  if (!have[device]) {
+    cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    int sms = 0, per = 0, coop = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fused_kernel, kNT, kMaxDynSmem);
+    cached[device] = coop ? sms * per : 0;
+    have[device] = true;
+  }
+  return cached[device];
+}
+
+int fused_tile_charts() { return kTCF; }
+
+bool fused_fits(int k) {  // the rasterizer role's carve of the dynamic smem
+  const size_t need = group_bytes(k) * kRG + r16(sizeof(k3::ChartK3) * kNW) +
+                      r16((size_t)4 * kNW * 4 * k);
+  return need <= (size_t)kMaxDynSmem;
+}
+
+cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const PackParams& pp,
+                         const int32_t* colofs, const int32_t* rowofs, uint32_t* dcol,
+                         uint32_t* drow, int32_t* wd, int32_t* hd, int32_t* off, uint8_t* lockbits,
+                         const int32_t* hsorted, int32_t* cand_bad, int32_t* rdy, int32_t* scratch,
+                         int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
+                         Status* st, cudaStream_t s) {
+  const int f_words = (pp.Wp + 3) & ~3;
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 8 * (size_t)kRW);
+  int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
+  RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy};
+  PackParams p = pp;
+  void* args[] = {&p,       (void*)&colofs, (void*)&rowofs, (void*)&hsorted, &scratch, &pair_cap,
+                  &X,       &Y,             &mir,           &cands,          &st,      &prof_cap,
+                  &ra};
+  return cudaLaunchCooperativeKernel((const void*)fused_kernel, dim3(grid), dim3(kNT), args,
+                                     kMaxDynSmem, s);
 }
 
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,

@@ -51,6 +51,7 @@ struct tabi_ctx {
   uint8_t* lockbits = nullptr;
   int32_t* cand_bad = nullptr;
   int32_t* big_list = nullptr;  // (candidate, chart) items too large for K3's tile buffer
+  int32_t* rdy = nullptr;       // fused kernel: per (wave slot, tile) ready flags
   // hybrid prefix tail state per candidate
   int32_t* t_state = nullptr;
   int32_t* t_r0 = nullptr;
@@ -73,7 +74,7 @@ struct tabi_ctx {
   int32_t* h_start = nullptr;
   tabi_placement* h_out = nullptr;
   // last pack (introspection)
-  int32_t last_n = 0, last_M = 0, last_k = 0, last_g = 0;
+  int32_t last_n = 0, last_M = 0, last_k = 0, last_g = 0, last_fused = 0;
   std::string err;
 };
 
@@ -98,7 +99,7 @@ static void dfree_all(tabi_ctx* ctx) {
                 ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
                 ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
-                ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->X, ctx->Y, ctx->mir,
+                ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->rdy, ctx->X, ctx->Y, ctx->mir,
                 ctx->cands, ctx->dcol, ctx->t_state, ctx->t_r0, ctx->t_p, ctx->t_iter,
                 ctx->t_fsave,
                 ctx->drow, ctx->scratch};
@@ -185,6 +186,7 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
     CK(dalloc(&ctx->lockbits, (size_t)M * N));
     CK(dalloc(&ctx->cand_bad, (size_t)M));
     CK(dalloc(&ctx->big_list, (size_t)M * N));
+    CK(dalloc(&ctx->rdy, (size_t)M * ((N + fused_tile_charts() - 1) / fused_tile_charts())));
     ctx->fstride = ((ctx->max_side + 2 * 64 + 4) + 31) & ~31;
     CK(dalloc(&ctx->t_state, (size_t)M));
     CK(dalloc(&ctx->t_r0, (size_t)M));
@@ -314,6 +316,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
 
   Status init{};
   init.bad_chart = INT32_MAX;
+  init.tr[0] = ~0ull;
   *ctx->h_status = init;
   CK(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, s));
   launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
@@ -332,6 +335,12 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   int B = wenv ? atoi(wenv) : 16;
   if (B < 1 || B > M) B = M;
   pp.B = B;
+  // fused wave kernel: needs B packer CTAs plus rasterizer CTAs co-resident
+  const char* fenv = getenv("TABI_FUSED");
+  const int fgrid = fused_grid(ctx->device);
+  const bool fused = !(fenv && fenv[0] == '0') && fgrid >= B + 8 && fused_fits(pp.k);
+  if (info) info->fused = fused ? 1 : 0;
+  ctx->last_fused = fused ? 1 : 0;
   int wave = 0;
   for (int attempt = 0; attempt < 64; attempt++) {
     pp.col_cap = ctx->col_cap;
@@ -345,19 +354,33 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     }
     CK(cudaMemsetAsync(ctx->cand_bad, 0, sizeof(int32_t) * M, s));
     CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));  // large-chart list
-    launch_profiles(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
-                    (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
-                    ctx->d_status, s);
-    launches += 2;  // K3 tiles, K3 large charts
-    tm.mark(s);
-    launch_offsets(pp, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
-                   ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
-    launches++;
-    tm.mark(s);
-    launch_pack(pp, ctx->colofs, ctx->rowofs, ctx->dcol, ctx->drow, ctx->wd, ctx->hd, ctx->off,
-                ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
-                ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
-    launches++;
+    if (fused) {
+      // K3 + K3b + K4 as one cooperative persistent launch
+      const int T = (n + fused_tile_charts() - 1) / fused_tile_charts();
+      CK(cudaMemsetAsync(ctx->rdy, 0, sizeof(int32_t) * (size_t)B * T, s));
+      CK(cudaMemsetAsync(&ctx->d_status->work_next, 0, sizeof(int32_t), s));
+      tm.mark(s);
+      tm.mark(s);
+      CK(launch_fused(fgrid, ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->dcol,
+                      ctx->drow, ctx->wd, ctx->hd, ctx->off, ctx->lockbits, ctx->hsorted,
+                      ctx->cand_bad, ctx->rdy, ctx->scratch, ctx->pair_cap, ctx->X, ctx->Y,
+                      ctx->mir, ctx->cands, ctx->d_status, s));
+      launches++;
+    } else {
+      launch_profiles(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
+                      (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
+                      ctx->d_status, s);
+      launches += 2;  // K3 tiles, K3 large charts
+      tm.mark(s);
+      launch_offsets(pp, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
+                     ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
+      launches++;
+      tm.mark(s);
+      launch_pack(pp, ctx->colofs, ctx->rowofs, ctx->dcol, ctx->drow, ctx->wd, ctx->hd, ctx->off,
+                  ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
+                  ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
+      launches++;
+    }
     if (t_opt > 0) {
       // hybrid prefix tail for the candidates K4 switched: rows and
       // sigma, then up to 9 re-rasterize / re-lay rounds, then the prefix rows
@@ -611,6 +634,22 @@ extern "C" tabi_status tabi_debug_profile(tabi_ctx* ctx, int32_t m, int32_t s, i
   delete[] c;
   delete[] r;
   CK(cudaGetLastError());
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16) {
+  if (!ctx || !out16 || ctx->last_n < 1) return TABI_EINVAL;
+  const Status& st = *ctx->h_status;
+  const unsigned long long t0 = st.tr[0];
+  const bool f = ctx->last_fused != 0;
+  out16[0] = f && st.tr[1] > t0 ? (int64_t)(st.tr[1] - t0) : 0;
+  out16[1] = f && st.tr[2] > t0 ? (int64_t)(st.tr[2] - t0) : 0;
+  out16[2] = (int64_t)st.tr[3];
+  out16[3] = (int64_t)st.tr[4];
+  out16[4] = (int64_t)st.tr[5];
+  out16[5] = ctx->last_fused;
+  for (int i = 0; i < 8; i++) out16[6 + i] = (int64_t)st.ph[i];
+  out16[14] = out16[15] = 0;
   return TABI_OK;
 }
 

@@ -284,10 +284,25 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t winner;     // winning m (0 = none)
   int32_t cols_total, rows_total;
   int32_t pad[3];
+  int32_t work_next;  // fused kernel: raster work-queue head
+  int32_t pad2;
   unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
   unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
   unsigned long long atot_lo, atot_hi;  // total 2 x area (int128) for D25 / D26
+  // fused-kernel trace (%globaltimer ns): [0] first CTA start, [1] last raster
+  // group end, [2] last packer end, [3] packer ns spent waiting for tiles,
+  // [4] raster ns spent waiting for the left tile, [5] tiles rasterized
+  unsigned long long tr[6];
+  // K4 row-phase time (ns, thread 0 of every packer, summed): knee update,
+  // fold, HC choice + lock pairs, push, Alg. 1, score, select + commit, FindKnee
+  unsigned long long ph[8];
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Per-candidate result record (mirrors tabi_cand_dbg).
 struct Cand {
@@ -348,6 +363,18 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
                  const int32_t* off, const uint8_t* lockbits, const int32_t* hsorted,
                  const int32_t* cand_bad, int32_t* scratch, int64_t pair_cap, int32_t* X,
                  int32_t* Y, uint8_t* mir, Cand* cands, Status* st, cudaStream_t s);
+// Fused persistent wave kernel (k_pack.cu): K3 + K3b + K4 in one cooperative
+// launch.  fused_grid = co-resident CTAs (0 if cooperative launch is
+// unsupported); the ready flags are [B][ceil(n / fused_tile_charts())].
+int fused_grid(int device);
+int fused_tile_charts();
+bool fused_fits(int k);
+cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const PackParams& pp,
+                         const int32_t* colofs, const int32_t* rowofs, uint32_t* dcol,
+                         uint32_t* drow, int32_t* wd, int32_t* hd, int32_t* off, uint8_t* lockbits,
+                         const int32_t* hsorted, int32_t* cand_bad, int32_t* rdy, int32_t* scratch,
+                         int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
+                         Status* st, cudaStream_t s);
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
                    const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s);

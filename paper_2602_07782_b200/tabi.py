@@ -38,7 +38,7 @@ class Spec(C.Structure):
 
 
 class Info(C.Structure):
-    _fields_ = [("scale_index", C.c_int32), ("reserved0", C.c_int32), ("l2_stretch", C.c_double),
+    _fields_ = [("scale_index", C.c_int32), ("fused", C.c_int32), ("l2_stretch", C.c_double),
                 ("rows", C.c_int32), ("knees_found", C.c_int32), ("knee_rows", C.c_int32),
                 ("prefix_rows", C.c_int32), ("bad_chart", C.c_int32), ("gpu_launches", C.c_int32),
                 ("stage_ms", C.c_float * 8), ("work_pack", C.c_int64),
@@ -87,6 +87,7 @@ def lib():
         L.tabi_debug_candidates.argtypes = [P, P]
         L.tabi_debug_profile.argtypes = [P, i32, i32, P, P, P, P, P]
         L.tabi_debug_offsets.argtypes = [P, i32, P, P]
+        L.tabi_debug_trace.argtypes = [P, P]
         L.tabi_shard_plan.argtypes = [i32, P, i32, P]
         L.tabi_pack_batch.argtypes = [P, i32, i32, P, P, P, P, P, P, P]
         _lib = L
@@ -95,7 +96,8 @@ def lib():
 
 EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
-           "tabi_debug_profile", "tabi_debug_offsets", "tabi_shard_plan", "tabi_pack_batch"]
+           "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace", "tabi_shard_plan",
+           "tabi_pack_batch"]
 
 
 def shard_plan(n_charts, n_gpus: int) -> np.ndarray:
@@ -235,6 +237,16 @@ class Context:
         lk = np.zeros(n, dtype=np.uint8)
         self._chk(lib().tabi_debug_offsets(self.h, m, _ptr(off), _ptr(lk)))
         return off, lk
+
+    def trace(self):
+        """Fused-kernel timeline of the last wave (tabi_debug_trace): dict of ns."""
+        out = np.zeros(16, dtype=np.int64)
+        self._chk(lib().tabi_debug_trace(self.h, _ptr(out)))
+        keys = ("raster_end", "pack_end", "pack_wait", "raster_wait", "tiles", "fused")
+        d = dict(zip(keys, (int(v) for v in out[:6])))
+        d["phases"] = dict(zip(("knee", "fold", "hc_locks", "push", "alg1", "score", "commit",
+                                "findknee"), (int(v) for v in out[6:14])))
+        return d
 
     def _chk(self, st):
         if st != OK:

@@ -189,6 +189,20 @@ def test_wave_sizes(orc, ctx, wave, monkeypatch):
         _compare_pack(orc, ctx, cs, check_profiles=3)
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_fused_and_split_paths(orc, ctx, fused, monkeypatch):
+    """The fused persistent wave kernel (default) and the split K3 / K3b / K4
+    launches (TABI_FUSED=0) both agree with the oracle, hybrid tail included."""
+    monkeypatch.setenv("TABI_FUSED", fused)
+    cases = (chartgen.config2(1), chartgen.small_case(7, n=200, family="uv", side=512, rho=0.9))
+    for cs in cases:
+        _compare_pack(orc, ctx, cs, check_profiles=6)
+    _compare_pack(orc, ctx, HYBRID[2], check_profiles=2, t_opt_bp=300)
+    from paper_2602_07782_b200 import spec_of
+    _, _, info = ctx.pack(cases[0].xy, cases[0].start, spec_of(cases[0]))
+    assert info.fused == int(fused)
+
+
 def test_large_chart_path(orc, ctx):
     """Charts whose footprint exceeds the K3 tile buffer (> 8192 cells) take the
     warp-per-chart path; both must agree with the oracle."""

@@ -23,7 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def main():
     rep, kname, cu = sys.argv[1], sys.argv[2], sys.argv[3]
     topn = int(sys.argv[4]) if len(sys.argv) > 4 else 30
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "--kernel-name", f"regex:{kname}"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hi = next(i for i, r in enumerate(rows) if "Instructions Executed" in r)
