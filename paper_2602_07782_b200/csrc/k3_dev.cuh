@@ -144,6 +144,79 @@ __device__ __forceinline__ uint32_t raw_cell(const ChartK3& H, const int32_t* ta
   return (uint32_t)L | ((uint32_t)Hh << 16);
 }
 
+// raw_cell for the consecutive cells i0 .. i0 + len - 1 of one axis, written
+// to out[0 .. len).  Same values; the per-cell divisions become running
+// quotients: the slice index bounds jl(i) = floor(i SCk / nx) and
+// jh(i) = floor(((i + 1) SCk - 1) / nx) and the four OBB line progressions each
+// advance by one add and one conditional carry per cell.
+__device__ __forceinline__ void raw_run(const ChartK3& H, const int32_t* tab, int k, int ax,
+                                        int64_t i0, int len, int64_t SC, uint32_t* out) {
+  const int64_t nx = ax ? H.nh : H.nw;
+  const double rnx = ax ? H.rnh : H.rnw;
+  const int64_t SCk = SC * k;
+  const int64_t dq = fdiv_r64(SCk, nx, rnx), dr = SCk - dq * nx;
+  int64_t a = i0 * SCk;
+  int64_t ql = fdiv_r64(a, nx, rnx), rl = a - ql * nx;
+  a += SCk - 1;
+  int64_t qh = fdiv_r64(a, nx, rnx), rh = a - qh * nx;
+  const int32_t* t = tab + ax * 2 * k;
+  const int64_t cnt = ax ? H.hs : H.ws;
+  const int64_t ext = ax ? H.ws : H.hs;
+  const bool obb = H.j8 != 0;
+  const ObbC& O = H.O;
+  const int q0 = 2 * ax, q1 = 2 * ax + 1;
+  int64_t v[4] = {0, 0, 0, 0}, r[4] = {0, 0, 0, 0}, sq[4] = {0, 0, 0, 0}, sr[4] = {0, 0, 0, 0},
+          D[4] = {1, 1, 1, 1};
+  int64_t iA0 = 0, iA1 = 0, iB0 = 0, iB1 = 0, st0 = 0, st1 = 0, la0 = 0, la1 = 0;
+  int32_t lb0 = 0, lb1 = 0;
+  if (obb) {
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      const LinDiv& L = O.lin[4 * ax + p];
+      lindiv_start(L, i0, v[p], r[p]);
+      sq[p] = L.qB;
+      sr[p] = L.rB;
+      D[p] = L.D;
+    }
+    iA0 = O.iA[q0]; iA1 = O.iA[q1]; iB0 = O.iB[q0]; iB1 = O.iB[q1];
+    st0 = O.star[q0]; st1 = O.star[q1]; la0 = O.last[q0]; la1 = O.last[q1];
+    lb0 = O.lastB[q0]; lb1 = O.lastB[q1];
+  }
+  for (int c = 0; c < len; c++) {
+    const int64_t i = i0 + c;
+    const int64_t jl = ql < 0 ? 0 : ql, jh = qh > k - 1 ? k - 1 : qh;
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (int64_t j = jl; j <= jh; j++) {
+      lo = min(lo, t[2 * j]);
+      hi = max(hi, t[2 * j + 1]);
+    }
+    int64_t L = max(0, lo), Hh = min((int64_t)hi, ext);
+    if (obb) {
+      const bool last = i == cnt - 1;
+      int64_t w;
+      if (i <= iA0 && (last ? lb0 != 0 : i >= iB0)) w = st0;
+      else if (i > iA0) w = v[0];
+      else w = last ? la0 : v[1];
+      L = max(L, w);
+      if (i <= iA1 && (last ? lb1 != 0 : i >= iB1)) w = st1;
+      else if (i > iA1) w = -v[2];
+      else w = last ? la1 : -v[3];
+      Hh = min(Hh, w);
+#pragma unroll
+      for (int p = 0; p < 4; p++) {
+        v[p] += sq[p];
+        r[p] += sr[p];
+        if (r[p] >= D[p]) { r[p] -= D[p]; v[p]++; }
+      }
+    }
+    out[c] = (uint32_t)L | ((uint32_t)Hh << 16);
+    ql += dq; rl += dr;
+    if (rl >= nx) { rl -= nx; ql++; }
+    qh += dq; rh += dr;
+    if (rh >= nx) { rh -= nx; qh++; }
+  }
+}
+
 // Setup of one chart by 8 cooperating threads r = 0..7 (rank r).
 __device__ inline void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, int64_t num,
                             int64_t SC, int r) {
@@ -198,9 +271,9 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
                             uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all,
                             int32_t* cand_bad, int m, int s0, Scale sc, ChartK3* CH,
                             int32_t* cells, int32_t* cpre, int32_t* opre, int32_t* chunk_end,
-                            int32_t* big, int32_t* tabs, uint32_t* raw, int tid, Sync sync) {
-  const int k = pp.k, g = pp.g;
-  const int nt = min(TC, pp.n - s0);
+                            int32_t* big, int32_t* tabs, uint32_t* raw, int nt, int tid,
+                            Sync sync) {
+  const int k = pp.k, g = pp.g;  // tile = sorted positions [s0, s0 + nt), nt <= TC
   const int64_t num = sc.num, SC = sc.SC;
   const double rSC = rcp_approx((double)SC);
   const int ci = tid >> 3, r = tid & 7;
@@ -258,17 +331,28 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
     sync();
     const int ce = *chunk_end, nc = ce - cb;
     const int32_t ncell = cpre[nc], nout = opre[nc];
-    for (int e = tid; e < ncell; e += TT) {  // raw pass over the chunk's flattened cells
-      int lo = 0, hi = nc - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (cpre[mid] <= e) lo = mid;
-        else hi = mid - 1;
+    {  // raw pass: each thread a contiguous run of the flattened cells (odd
+       // length: the runs' smem stores hit distinct banks), evaluated incrementally
+      const int32_t R = ((ncell + TT - 1) / TT) | 1;
+      int32_t e = tid * R;
+      const int32_t e1 = min(ncell, e + R);
+      if (e < e1) {
+        int lo = 0, hi = nc - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (cpre[mid] <= e) lo = mid;
+          else hi = mid - 1;
+        }
+        while (e < e1) {
+          const ChartK3& H = CH[cb + lo];
+          const int32_t x = e - cpre[lo];
+          const int ax = x >= H.ws;
+          const int32_t len = min(e1 - e, (ax ? H.ws + H.hs : H.ws) - x);
+          raw_run(H, tabs + (cb + lo) * 4 * k, k, ax, ax ? x - H.ws : x, len, SC, raw + e);
+          e += len;
+          while (lo < nc - 1 && cpre[lo + 1] <= e) lo++;  // next chart with cells
+        }
       }
-      const ChartK3& H = CH[cb + lo];
-      const int32_t x = e - cpre[lo];
-      const int ax = x >= H.ws;
-      raw[e] = raw_cell(H, tabs + (cb + lo) * 4 * k, k, ax, ax ? x - H.ws : x, num, SC);
     }
     sync();
     for (int o = tid; o < nout; o += TT) {  // dilation over the flattened outputs

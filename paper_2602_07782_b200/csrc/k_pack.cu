@@ -152,10 +152,20 @@ __device__ __forceinline__ void walk(const Win& w, int nwin, Enter enter, Body b
 // published by a rasterizer CTA: rdy = 1 footprints written, 2 also the
 // adjacent-pair offsets/locks of the pairs ending in the tile.
 struct Ready {
-  int32_t* flags;  // [B][T] or nullptr (non-fused: everything precomputed)
-  int32_t T, tcf;
+  int32_t* flags;        // [B][T] or nullptr (non-fused: everything precomputed)
+  int32_t T;             // tiles
+  const int32_t* tstart; // [T + 1] first sorted position of each tile
+  const int32_t* tix;    // [n] tile of each sorted position
 };
 
+__device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -185,7 +195,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   if (tid == 0) ready_upto = -1;
   auto wait_upto = [&](int s_hi) {
     if (!rd.flags) return;
-    const int t_req = min(rd.T - 1, min(s_hi + 1, n - 1) / rd.tcf);
+    const int t_req = rd.tix[min(s_hi + 1, n - 1)];
     if (tid == 0 && ready_upto < t_req) {
       int32_t* fl = rd.flags + (int64_t)jslot * rd.T;
       const unsigned long long t0 = gtime();
@@ -197,6 +207,52 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       atomicAdd(&st->tr[3], gtime() - t0);
     }
     __syncthreads();
+  };
+  // Fold-side readiness: block until position s (and its pair offset) is
+  // published, then take whatever further tiles are already published (no
+  // waiting).  Returns the last sorted position the fold may scan, so the
+  // packer runs right behind the rasterizers instead of a whole scan chunk
+  // behind them.
+  // Warp 0 probes 32 flags per step with relaxed loads; each lane then
+  // fences (acquire pattern: relaxed load + fence.acq_rel, which also drops
+  // the SM's L1 so later plain loads see the published data).
+  __shared__ int32_t ready_lim;
+  auto wait_ready = [&](int s) -> int {
+    if (!rd.flags) return n - 1;
+    const int t_need = rd.tix[min(s + 1, n - 1)];
+    const int t_cap = max(t_need, rd.tix[min(s + kNT, n - 1)]);
+    // enough is known ready: no probe (a probe's fence also empties the L1
+    // that keeps the row's scalars warm between rows)
+    if (ready_upto >= rd.tix[min(s + 64, n - 1)]) return ready_lim;
+    if (wid == 0) {
+      const int32_t* fl = rd.flags + (int64_t)jslot * rd.T;
+      int up = ready_upto;
+      const unsigned long long t0 = up < t_need && lane == 0 ? gtime() : 0ull;
+      const bool blocked = up < t_need;
+      while (true) {
+        const int tt = up + 1 + lane;
+        int32_t f = 2;
+        if (tt <= t_cap && tt < rd.T)
+          asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(fl + tt) : "memory");
+        else
+          f = 0;
+        const unsigned ok = __ballot_sync(0xffffffffu, f >= 2);
+        const int adv = ok == 0xffffffffu ? 32 : __ffs(~ok) - 1;  // consecutive ready tiles
+        up += adv;
+        if (up >= t_need && adv < 32) break;
+        if (up >= t_cap || up + 1 >= rd.T) break;
+        if (adv == 0) __nanosleep(64);
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (lane == 0) {
+        if (blocked) atomicAdd(&st->tr[3], gtime() - t0);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
+        ready_upto = up;
+        ready_lim = up == rd.T - 1 ? n - 1 : rd.tstart[up + 1] - 2;
+      }
+    }
+    __syncthreads();
+    return ready_lim;
   };
   const int64_t cb = (int64_t)(m - 1) * n;
   const int32_t* wd = wd_all + cb;
@@ -395,11 +451,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       }
     } else {
       int32_t carry0 = 0, carry1 = 0;
-      for (int base = rs;; base += kNT) {
-        wait_upto(base + kNT - 1);
+      for (int base = rs;;) {
+        const int cnt = min(kNT, wait_ready(base) - base + 1);  // positions [base, base + cnt)
         if (tid < 4) S.fmin[tid] = INT32_MAX;
         const int s = base + tid;
-        const bool valid = s < n;
+        const bool valid = tid < cnt;
         const int32_t w_s = valid ? wd[s] : 0;
         const int32_t a1 = valid ? off[s] : 0;
         // fused mode: a chart that cannot fit the dilated atlas at this scale
@@ -420,7 +476,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         if (tid == 0) {
           for (int q = 0; q < 4; q++)
             if (S.endv[q] == INT32_MIN && S.fmin[q] != INT32_MAX) S.endv[q] = S.fmin[q] - 1;
-          if (S.endv[1] != INT32_MIN || base + kNT >= n) {
+          if (S.endv[1] != INT32_MIN || base + cnt >= n) {
             for (int q = 0; q < 4; q++)
               if (S.endv[q] == INT32_MIN) S.endv[q] = n - 1;
             S.done = 1;
@@ -430,6 +486,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         if (S.done) break;
         carry0 += t0;
         carry1 += t1;
+        base += cnt;
       }
     }  // !prefix_mode
     phase_mark(1);
@@ -762,7 +819,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
   extern __shared__ __align__(16) unsigned char dsm[];
   packer(pp, colofs, rowofs, dcol, drow, wd_all, hd_all, off_all, lock_all, hsorted, cand_bad,
          scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, blockIdx.x,
-         Ready{nullptr, 0, 0}, dsm);
+         Ready{nullptr, 0, nullptr, nullptr}, dsm);
 }
 
 // ---- fused persistent kernel: one cooperative launch per candidate wave ----
@@ -775,15 +832,13 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
 // overlap with the row loop; no host round trip inside the wave.  Several
 // groups per SM hide the latency of one group's setup / barrier phases the
 // way several resident CTAs do in the split kernels.
-#ifndef TABI_FUSED_RG
-#define TABI_FUSED_RG 1
-#endif
-constexpr int kRG = TABI_FUSED_RG;  // raster groups per CTA
+constexpr int kRG = kFusedGroups;   // raster groups per CTA
 constexpr int kRGT = kNT / kRG;     // threads per group (8 per chart in setup)
 constexpr int kTCF = kRGT / 8;      // charts per raster tile
 constexpr int kRGW = kRGT / 32;    // warps per group
 constexpr int kRawF = 16384 / kRG;  // raw cells per group chunk (64 KB per CTA)
 static_assert(kTCF * 8 == kRGT, "setup maps 8 threads to a chart");
+static_assert(kTCF >= kFusedTileCharts, "prep_kernel's tiles must fit a raster group");
 
 struct GroupSync {
   int id;
@@ -803,6 +858,8 @@ struct RasterArgs {
   uint32_t* dcol;
   uint32_t* drow;
   int32_t* rdy;
+  const int32_t* tstart;  // [T + 1] tile boundaries (prep_kernel)
+  const int32_t* tix;     // [n] tile of each sorted position
 };
 
 __host__ __device__ __forceinline__ size_t r16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -825,12 +882,12 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
              int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all, Cand* cands, Status* st,
              int32_t prof_cap, RasterArgs ra) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  const int T = (pp.n + kTCF - 1) / kTCF;
+  const int T = st->ntiles;
   if (threadIdx.x == 0) atomicMin(&st->tr[0], gtime());
   if ((int)blockIdx.x < pp.B) {
     packer(pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, hsorted,
            ra.cand_bad, scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap,
-           blockIdx.x, Ready{ra.rdy, T, kTCF}, dsm);
+           blockIdx.x, Ready{ra.rdy, T, ra.tstart, ra.tix}, dsm);
     return;
   }
   // ---- rasterizer role ----
@@ -866,11 +923,11 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     const int t = it / pp.B, j = it % pp.B;
     const int m = wave_m(pp, m_hi, j);
     if (m == 0) continue;
-    const int s0 = t * kTCF, nt = min(kTCF, pp.n - s0);
+    const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
     const k3::Scale sc{m, SCm, 0};
     k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
                                        ra.hd, ra.cand_bad, m, s0, sc, CH, cells, cpre, opre,
-                                       &misc[1], big, tabs, raw, gt, gsync);
+                                       &misc[1], big, tabs, raw, nt, gt, gsync);
     for (int ci = gw; ci < nt; ci += kRGW)
       if (big[ci])
         k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m, s0 + ci, sc, CW[wid],
@@ -884,26 +941,29 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       if (gt == 0) atomicAdd(&st->work_prof, pe);
     }
     gsync();
+    // Adjacent pairs: the tile's internal pairs here; a boundary pair with a
+    // neighbour tile is done by whichever of the two tiles publishes its
+    // footprints second (arrival counter per boundary, acq_rel), so no tile
+    // waits for another.  rdy[t] reaches 2 once the pairs (s, s + 1) of all
+    // s in tile t are done: its internal pairs (+1) and its right boundary (+1;
+    // the last tile adds its own zero entry instead).
     int32_t* fl = ra.rdy + (int64_t)j * T;
+    int32_t* arr = ra.rdy + (int64_t)pp.B * pp.n + (int64_t)j * T;  // boundary t | t+1
     if (gt == 0) {
-      __threadfence();
-      atomicExch(fl + t, 1);  // footprints of tile t published
       atomicAdd(&st->tr[5], 1ull);
-      if (t > 0 && ld_acquire(fl + t - 1) < 1) {  // left neighbour's footprints
-        const unsigned long long t0 = gtime();
-        while (ld_acquire(fl + t - 1) < 1) __nanosleep(32);
-        atomicAdd(&st->tr[4], gtime() - t0);
-      }
+      misc[2] = t > 0 && atom_add_acq_rel(arr + t - 1, 1) == 1;      // left boundary is ours
+      misc[3] = t < T - 1 && atom_add_acq_rel(arr + t, 1) == 1;      // right boundary is ours
     }
     gsync();
-    // pairs (s, s+1) for s in [s0 - 1, s0 + nt - 2] (+ the last chart's zero entry)
-    const int lo = max(0, s0 - 1), hi = (s0 + nt == pp.n) ? pp.n - 1 : s0 + nt - 2;
+    const bool needL = misc[2] != 0, needR = misc[3] != 0;
+    const int lo = needL ? s0 - 1 : s0;
+    const int hi = (t == T - 1) ? pp.n - 1 : (needR ? s0 + nt - 1 : s0 + nt - 2);
     for (int s = lo + gw; s <= hi; s += kRGW)
       k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
     gsync();
     if (gt == 0) {
-      __threadfence();
-      atomicExch(fl + t, 2);  // offsets of the pairs ending in tile t published
+      red_add_release(fl + t, (t == T - 1 || needR) ? 2 : 1);
+      if (needL) red_add_release(fl + t - 1, 1);
     }
   }
 }
@@ -1003,7 +1063,6 @@ int fused_grid(int device) {
   return cached[device];
 }
 
-int fused_tile_charts() { return kTCF; }
 
 bool fused_fits(int k) {  // the rasterizer role's carve of the dynamic smem
   const size_t need = group_bytes(k) * kRG + r16(sizeof(k3::ChartK3) * kNW) +
@@ -1014,13 +1073,14 @@ bool fused_fits(int k) {  // the rasterizer role's carve of the dynamic smem
 cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const PackParams& pp,
                          const int32_t* colofs, const int32_t* rowofs, uint32_t* dcol,
                          uint32_t* drow, int32_t* wd, int32_t* hd, int32_t* off, uint8_t* lockbits,
-                         const int32_t* hsorted, int32_t* cand_bad, int32_t* rdy, int32_t* scratch,
+                         const int32_t* hsorted, int32_t* cand_bad, int32_t* rdy,
+                         const int32_t* tstart, const int32_t* tix, int32_t* scratch,
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s) {
   const int f_words = (pp.Wp + 3) & ~3;
   const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 8 * (size_t)kRW);
   int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
-  RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy};
+  RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy, tstart, tix};
   PackParams p = pp;
   void* args[] = {&p,       (void*)&colofs, (void*)&rowofs, (void*)&hsorted, &scratch, &pair_cap,
                   &X,       &Y,             &mir,           &cands,          &st,      &prof_cap,

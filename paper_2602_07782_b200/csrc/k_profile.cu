@@ -68,7 +68,7 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   uint32_t* raw = (uint32_t*)(dyn + kTC * 4 * pp.k);
   tile_raster<kTC, kTT, kRaw>(P, perm, pp, colofs, rowofs, dcol, drow, wd_all, hd_all, cand_bad, m,
                               s0, sc, CH, cells, cpre, opre, &chunk_end, big, tabs, raw,
-                              (int)threadIdx.x, [] { __syncthreads(); });
+                              min(kTC, pp.n - s0), (int)threadIdx.x, [] { __syncthreads(); });
   if (threadIdx.x == 0) {
     for (int ci = 0; ci < kTC; ci++)
       if (big[ci]) big_list[atomicAdd(&st->pad[1], 1)] = (m - 1) * pp.n + s0 + ci;

@@ -136,8 +136,9 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
 __global__ void __launch_bounds__(kT, 1)
 prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int64_t* area2,
             const int32_t* perm, PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
-            Status* st) {
+            int32_t* tstart, int32_t* tix, Status* st) {
   __shared__ int32_t sh[2][kW + 1];
+  __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
   if (st->bad_chart != INT32_MAX) return;
   // Area bound on the candidate scales: the packed charts are disjoint and
@@ -166,7 +167,7 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
       st->atot_hi = (unsigned long long)(uint64_t)(tot >> 64);
     }
   }
-  int32_t carry_c = 0, carry_r = 0;
+  int32_t carry_c = 0, carry_r = 0, carry_t = 0, prev_id = -1;
   for (int t0 = 0; t0 < pp.n; t0 += kT) {
     const int s = t0 + threadIdx.x;
     int32_t cw = 0, rh = 0;
@@ -180,16 +181,39 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
     }
     int32_t ec, er, tc, tr;
     block_scan2(cw, rh, ec, er, tc, tr, sh);
+    // Fused-kernel raster tiles: consecutive sorted charts with tile key
+    // floor(slot prefix / kFusedTileCells) + floor(s / kFusedTileCharts) --
+    // non-decreasing in s, so equal keys are runs of <= kFusedTileCharts
+    // charts holding about kFusedTileCells footprint cells (the tallest
+    // charts come first and get small tiles, so their tiles are not the long
+    // pole every packer waits on).
+    const int32_t id = s < pp.n ? (int32_t)(((int64_t)carry_c + ec + carry_r + er) / kFusedTileCells +
+                                            s / kFusedTileCharts)
+                                : INT32_MAX;
+    idl[threadIdx.x] = id;
+    __syncthreads();
+    const int32_t idp = threadIdx.x == 0 ? prev_id : idl[threadIdx.x - 1];
+    const int32_t first = (s < pp.n && id != idp) ? 1 : 0;
+    int32_t ef, e2, tf, t2;
+    block_scan2(first, 0, ef, e2, tf, t2, sh);
     if (s < pp.n) {
       colofs[s] = carry_c + ec;
       rowofs[s] = carry_r + er;
+      const int32_t t = carry_t + ef + first - 1;
+      tix[s] = t;
+      if (first) tstart[t] = s;
     }
+    prev_id = idl[kT - 1];
     carry_c += tc;
     carry_r += tr;
+    carry_t += tf;
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
     st->cols_total = carry_c;
     st->rows_total = carry_r;
+    st->ntiles = carry_t;
+    tstart[carry_t] = pp.n;
     // +4: the TMA bulk copy of a row window rounds its end up to 16 bytes
     if ((int64_t)carry_c + 4 > pp.col_cap || (int64_t)carry_r + 4 > pp.row_cap) st->capacity |= 1;
   }
@@ -203,8 +227,10 @@ void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, i
 }
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
-                 int32_t* rowofs, int32_t* hsorted, Status* st, cudaStream_t s) {
-  prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, st);
+                 int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
+                 cudaStream_t s) {
+  prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart, tix,
+                               st);
 }
 
 }  // namespace tabi

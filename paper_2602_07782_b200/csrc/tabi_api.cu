@@ -52,6 +52,8 @@ struct tabi_ctx {
   int32_t* cand_bad = nullptr;
   int32_t* big_list = nullptr;  // (candidate, chart) items too large for K3's tile buffer
   int32_t* rdy = nullptr;       // fused kernel: per (wave slot, tile) ready flags
+  int32_t* tstart = nullptr;    // fused kernel: raster tile boundaries [N + 1]
+  int32_t* tix = nullptr;       // fused kernel: tile of each sorted position [N]
   // hybrid prefix tail state per candidate
   int32_t* t_state = nullptr;
   int32_t* t_r0 = nullptr;
@@ -99,7 +101,7 @@ static void dfree_all(tabi_ctx* ctx) {
                 ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
                 ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
-                ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->rdy, ctx->X, ctx->Y, ctx->mir,
+                ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->rdy, ctx->tstart, ctx->tix, ctx->X, ctx->Y, ctx->mir,
                 ctx->cands, ctx->dcol, ctx->t_state, ctx->t_r0, ctx->t_p, ctx->t_iter,
                 ctx->t_fsave,
                 ctx->drow, ctx->scratch};
@@ -153,6 +155,7 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
             dalloc(&ctx->perm, N) == cudaSuccess && dalloc(&ctx->perm2, N) == cudaSuccess &&
             dalloc(&ctx->colofs, N) == cudaSuccess && dalloc(&ctx->rowofs, N) == cudaSuccess &&
             dalloc(&ctx->hsorted, N) == cudaSuccess && dalloc(&ctx->d_out, N) == cudaSuccess &&
+            dalloc(&ctx->tstart, N + 1) == cudaSuccess && dalloc(&ctx->tix, N) == cudaSuccess &&
             dalloc(&ctx->d_status, 1) == cudaSuccess;
   if (!ok) return fail();
   if (cudaMallocHost((void**)&ctx->h_status, sizeof(Status)) != cudaSuccess ||
@@ -186,7 +189,7 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
     CK(dalloc(&ctx->lockbits, (size_t)M * N));
     CK(dalloc(&ctx->cand_bad, (size_t)M));
     CK(dalloc(&ctx->big_list, (size_t)M * N));
-    CK(dalloc(&ctx->rdy, (size_t)M * ((N + fused_tile_charts() - 1) / fused_tile_charts())));
+    CK(dalloc(&ctx->rdy, 2 * (size_t)M * N));  // ready flags + boundary arrival counters
     ctx->fstride = ((ctx->max_side + 2 * 64 + 4) + 31) & ~31;
     CK(dalloc(&ctx->t_state, (size_t)M));
     CK(dalloc(&ctx->t_r0, (size_t)M));
@@ -347,7 +350,8 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     pp.row_cap = ctx->row_cap;
     pp.wave = wave;
     if (wave == 0) {
-      launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->d_status, s);
+      launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
+                  ctx->tix, ctx->d_status, s);
       launches++;
       CK(cudaMemsetAsync(ctx->cands, 0, sizeof(Cand) * M, s));
       CK(cudaMemsetAsync(ctx->t_state, 0, sizeof(int32_t) * M, s));
@@ -356,14 +360,14 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));  // large-chart list
     if (fused) {
       // K3 + K3b + K4 as one cooperative persistent launch
-      const int T = (n + fused_tile_charts() - 1) / fused_tile_charts();
-      CK(cudaMemsetAsync(ctx->rdy, 0, sizeof(int32_t) * (size_t)B * T, s));
+      CK(cudaMemsetAsync(ctx->rdy, 0, sizeof(int32_t) * (size_t)B * n, s));
+      CK(cudaMemsetAsync(ctx->rdy + (size_t)B * n, 0, sizeof(int32_t) * (size_t)B * n, s));
       CK(cudaMemsetAsync(&ctx->d_status->work_next, 0, sizeof(int32_t), s));
       tm.mark(s);
       tm.mark(s);
       CK(launch_fused(fgrid, ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->dcol,
                       ctx->drow, ctx->wd, ctx->hd, ctx->off, ctx->lockbits, ctx->hsorted,
-                      ctx->cand_bad, ctx->rdy, ctx->scratch, ctx->pair_cap, ctx->X, ctx->Y,
+                      ctx->cand_bad, ctx->rdy, ctx->tstart, ctx->tix, ctx->scratch, ctx->pair_cap, ctx->X, ctx->Y,
                       ctx->mir, ctx->cands, ctx->d_status, s));
       launches++;
     } else {

@@ -137,6 +137,17 @@ __device__ __forceinline__ int64_t fdiv_r128(i128 a, i128 b, double rcp, bool cl
   while (r >= b) { q++; r -= b; }
   return q;
 }
+// Start a running evaluation at i: v = f(i), r = (rA + i*rB) mod D; then
+// lindiv_step moves to i + 1 with one add and one conditional carry (rB < D).
+__device__ __forceinline__ void lindiv_start(const LinDiv& L, int64_t i, int64_t& v, int64_t& r) {
+  const int64_t N = L.rA + i * L.rB;
+  int64_t t = (int64_t)((double)N * L.rcp);
+  int64_t rr = N - t * L.D;
+  while (rr < 0) { t--; rr += L.D; }
+  while (rr >= L.D) { t++; rr -= L.D; }
+  v = L.qA + i * L.qB + t;
+  r = rr;
+}
 __device__ __forceinline__ int64_t lindiv_eval(const LinDiv& L, int64_t i) {
   const int64_t N = L.rA + i * L.rB;
   int64_t t = (int64_t)((double)N * L.rcp);
@@ -278,6 +289,15 @@ struct Proxies {
   int64_t* obb;      // [c*4 + {umin, umax, vmin, vmax}]
 };
 
+// Fused-kernel raster tiles (prep_kernel / k_pack.cu): at most
+// kFusedTileCharts sorted charts and about kFusedTileCells footprint cells.
+#ifndef TABI_FUSED_RG
+#define TABI_FUSED_RG 1
+#endif
+constexpr int kFusedGroups = TABI_FUSED_RG;  // independent raster groups per CTA
+constexpr int kFusedTileCharts = 64 / kFusedGroups;
+constexpr int kFusedTileCells = 8192 / kFusedGroups;
+
 struct Status {       // device-side status block, copied back once per pack
   int32_t bad_chart;  // INT32_MAX if none
   int32_t capacity;   // required column/row slot totals exceeded capacity
@@ -285,7 +305,7 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t cols_total, rows_total;
   int32_t pad[3];
   int32_t work_next;  // fused kernel: raster work-queue head
-  int32_t pad2;
+  int32_t ntiles;     // fused kernel: raster tiles (prep_kernel)
   unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
   unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
   unsigned long long atot_lo, atot_hi;  // total 2 x area (int128) for D25 / D26
@@ -349,7 +369,8 @@ void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, 
 void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
                  int32_t* perm2, const Status* st, cudaStream_t s);
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
-                 int32_t* rowofs, int32_t* hsorted, Status* st, cudaStream_t s);
+                 int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
+                 cudaStream_t s);
 void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
                      int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
@@ -365,14 +386,14 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
                  int32_t* Y, uint8_t* mir, Cand* cands, Status* st, cudaStream_t s);
 // Fused persistent wave kernel (k_pack.cu): K3 + K3b + K4 in one cooperative
 // launch.  fused_grid = co-resident CTAs (0 if cooperative launch is
-// unsupported); the ready flags are [B][ceil(n / fused_tile_charts())].
+// unsupported); the ready flags are [B][n] (at most n tiles).
 int fused_grid(int device);
-int fused_tile_charts();
 bool fused_fits(int k);
 cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const PackParams& pp,
                          const int32_t* colofs, const int32_t* rowofs, uint32_t* dcol,
                          uint32_t* drow, int32_t* wd, int32_t* hd, int32_t* off, uint8_t* lockbits,
-                         const int32_t* hsorted, int32_t* cand_bad, int32_t* rdy, int32_t* scratch,
+                         const int32_t* hsorted, int32_t* cand_bad, int32_t* rdy,
+                         const int32_t* tstart, const int32_t* tix, int32_t* scratch,
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s);
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,

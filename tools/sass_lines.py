@@ -69,7 +69,10 @@ def main():
         tot[1] += s
     print(f"total warp instructions {tot[0]:.0f}, stall samples {tot[1]:.0f}, mapped lines {len(agg)}")
     for (f, l), (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:topn]:
-        text = src[l - 1].strip()[:80] if f == os.path.basename(cu) and 0 < l <= len(src) else ""
+        fp = os.path.join(ROOT, "paper_2602_07782_b200", "csrc", f)
+        lines = src if f == os.path.basename(cu) else (
+            open(fp).read().splitlines() if os.path.exists(fp) else [])
+        text = lines[l - 1].strip()[:80] if 0 < l <= len(lines) else ""
         print(f"{n / tot[0] * 100:5.1f}% inst {s / max(tot[1], 1) * 100:5.1f}% stall  {f}:{l}  {text}")
 
 
