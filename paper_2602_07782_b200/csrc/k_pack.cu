@@ -50,7 +50,7 @@ struct Smem {
   int32_t newmax[4];
   int32_t changed, npairs, pair_overflow;
   int32_t sel_cfg;
-  int32_t win_s0, win_e, pglobal;
+  int32_t win_s0, win_e, pglobal, a0;
   int32_t prefix_rows, switched;
   unsigned long long knee_key;
   unsigned long long work;
@@ -111,8 +111,9 @@ struct Win {                 // shared-memory window of one row
   int32_t* rx0;              // fold position without HC (= prefix of widths)
   int32_t* rx1;              // fold position with HC
   int32_t* rwd;              // dilated width
-  int32_t* rco;              // footprint offset in the staged buffer (or in HBM)
+  int32_t* rco;              // footprint offset (colofs, absolute; see pr_base)
   int32_t* rY;               // [4][kRW] vertical offsets per configuration
+  int32_t* rbot;             // max over the chart's columns of BottomEdge (push walk)
   uint32_t* prof;            // staged column footprints
   int32_t prof_cap;
 };
@@ -285,7 +286,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   W.rwd = W.rx1 + kRW;
   W.rco = W.rwd + kRW;
   W.rY = W.rco + kRW;
-  W.prof = (uint32_t*)(W.rY + 4 * kRW);
+  W.rbot = W.rY + 4 * kRW;
+  W.prof = (uint32_t*)(W.rbot + kRW);
   W.prof_cap = prof_cap;
 
   const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
@@ -339,16 +341,18 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t c1 = we < n ? colofs[we] : cols_total;
     const int32_t a0 = c0 & ~3, a1 = (c1 + 3) & ~3;
     const bool pg = (a1 - a0) > W.prof_cap;
+    // the fold already wrote the scalars of the row's first kRW charts
+    const bool have = !prefix_mode && ws0 == S.row_start && nwin <= kRW;
     __syncthreads();  // previous readers of the window buffers are done
-    for (int k = tid; k < nwin; k += kNT) {
+    for (int k = tid; k < nwin && !have; k += kNT) {
       const int s = ws0 + k;
       W.rx0[k] = xs0[s];
       W.rx1[k] = xs1[s];
       W.rwd[k] = wd[s];
-      W.rco[k] = colofs[s] - (pg ? 0 : a0);
+      W.rco[k] = colofs[s];
     }
     if (!pg && tid == 0) bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
-    if (tid == 0) { S.win_s0 = ws0; S.win_e = we; S.pglobal = pg; }
+    if (tid == 0) { S.win_s0 = ws0; S.win_e = we; S.pglobal = pg; S.a0 = a0; }
     if (!pg) {
       mbar_wait(&S.mbar, phase);
       phase ^= 1u;
@@ -467,6 +471,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         if (valid) {
           xs0[s] = x0;
           xs1[s] = x1;
+          if (s - rs < kRW) {  // the row's window scalars, straight into smem
+            W.rx0[s - rs] = x0;
+            W.rx1[s - rs] = x1;
+            W.rwd[s - rs] = w_s;
+            W.rco[s - rs] = colofs[s];
+          }
           if (x0 + w_s > Wp) atomicMin(&S.fmin[0], s);
           if (x1 + w_s > Wp) atomicMin(&S.fmin[1], s);
           if (x0 + w_s > kb - ka) atomicMin(&S.fmin[2], s);
@@ -578,19 +588,22 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
       stage(ws0, we);
-      for (int k = tid; k < 4 * nwin; k += kNT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
-      __syncthreads();
-      const uint32_t* pr = S.pglobal ? col : W.prof;
-      int32_t X[4], mx[4];
+      for (int k = tid; k < 5 * nwin; k += kNT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
+      __syncthreads();  // (index 4 of rY is rbot)
+      const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
+      int32_t X[4], mx[4], bm = INT32_MIN;
       int nact = 0;
       walk(
           W, nwin,
           [&](int i, int32_t) {
             nact = (knee_ok && ws0 + i <= endK) ? 4 : 2;
             for (int q = 0; q < 4; q++) { mx[q] = INT32_MIN; X[q] = q < nact ? cfgX(q, i) : 0; }
+            bm = INT32_MIN;
           },
           [&](int i, int32_t j) {
-            const int32_t top = lo16(pr[W.rco[i] + j]);
+            const uint32_t v = pr[W.rco[i] + j];
+            const int32_t top = lo16(v);
+            bm = max(bm, hi16(v));  // the score needs only max_j BottomEdge per chart
             const int32_t Wd = W.rwd[i];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
@@ -603,6 +616,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           },
           [&](int i) {
             for (int q = 0; q < nact; q++) atomicMax(&W.rY[q * kRW + i], mx[q]);
+            atomicMax(&W.rbot[i], bm);
           });
       __syncthreads();
       if (one) continue;  // Y stays in shared memory for Alg. 1, score and commit
@@ -654,9 +668,19 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     }
     phase_mark(4);
     // ---- score: max over covered columns of Y + BottomEdge ----
+    // Y is constant per chart, so the max over its columns is Y + the chart's
+    // largest BottomEdge, which the push walk recorded (rbot): one pass over
+    // the row's charts instead of a column walk.  Multi-window rows walk.
     {
       int32_t nm[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
-      for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
+      if (one) {
+        const int nwin = endA - rs + 1;
+        for (int k = tid; k < nwin; k += kNT) {
+          const int na = (knee_ok && rs + k <= endK) ? 4 : 2;
+          for (int q = 0; q < na; q++) nm[q] = max(nm[q], W.rY[q * kRW + k] + W.rbot[k]);
+        }
+      }
+      for (int ws0 = rs; ws0 <= endA && !one; ws0 += kRW) {
         const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
         stage(ws0, we);
         for (int k = tid; k < nwin && !one; k += kNT) {
@@ -665,7 +689,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           for (int q = 0; q < na; q++) W.rY[q * kRW + k] = __ldcg(&Yc[(int64_t)q * n + s]);
         }
         __syncthreads();
-        const uint32_t* pr = S.pglobal ? col : W.prof;
+        const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
         int32_t Yv[4];
         int nact = 0;
         walk(
@@ -720,7 +744,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       for (int k = tid; k < nwin && !one; k += kNT)
         W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
       __syncthreads();
-      const uint32_t* pr = S.pglobal ? col : W.prof;
+      const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
       int32_t Xc = 0, Yv = 0, Wd = 0;
       walk(
@@ -1040,7 +1064,7 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
     attr = true;
   }
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 8 * (size_t)kRW);
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 9 * (size_t)kRW);
   const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   pack_kernel<<<pp.B, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
                                              hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
@@ -1078,7 +1102,7 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s) {
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 8 * (size_t)kRW);
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 9 * (size_t)kRW);
   int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy, tstart, tix};
   PackParams p = pp;
