@@ -183,7 +183,8 @@ tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* 
  * over packers); [3] raster ns waiting for a left neighbour tile (sum);
  * [4] tiles rasterized; [5] fused (0/1); [6..13] K4 row-phase ns summed over
  * packers (knee update, fold, HC choice + lock pairs, push, Alg. 1, score,
- * select + commit, FindKnee); [14..15] 0. */
+ * select + commit, FindKnee); [14] of which push staging, [15] of which
+ * commit staging. */
 tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16);
 
 #ifdef __cplusplus

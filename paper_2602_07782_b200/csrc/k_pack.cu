@@ -324,7 +324,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   uint32_t phase = 0;
   unsigned long long wk = 0;  // frontline column visits by this thread
   // row-phase timing (thread 0, %globaltimer; a few reads per row)
-  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t_last = gtime();
+  unsigned long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t_last = gtime();
   auto phase_mark = [&](int i) {
     if (tid == 0) {
       const unsigned long long t = gtime();
@@ -590,6 +590,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       stage(ws0, we);
       for (int k = tid; k < 5 * nwin; k += kNT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
       __syncthreads();  // (index 4 of rY is rbot)
+      phase_mark(8);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       int32_t X[4], mx[4], bm = INT32_MIN;
       int nact = 0;
@@ -744,6 +745,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       for (int k = tid; k < nwin && !one; k += kNT)
         W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
       __syncthreads();
+      phase_mark(9);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
       int32_t Xc = 0, Yv = 0, Wd = 0;
@@ -805,7 +807,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     phase_mark(7);
   }
   if (tid == 0)
-    for (int i = 0; i < 8; i++) atomicAdd(&st->ph[i], ph[i]);
+    for (int i = 0; i < 10; i++) atomicAdd(&st->ph[i], ph[i]);
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
   if (lane == 0) atomicAdd(&st->work_pack, wk);
   if (rd.flags && tid == 0) atomicMax(&st->tr[2], gtime());

@@ -24,6 +24,7 @@ struct WarpSlices {
   int32_t mhi[2][TABI_KMAX];
   int64_t fl[2][TABI_KMAX];  // floor(i * ext / k) for the other axis' slice edges
   int64_t cl[2][TABI_KMAX];  // ceil((i + 1) * ext / k)
+  int64_t ob[8][4];          // OBB extents per angle: Umin, Umax, Vmin, Vmax
 };
 
 // D4: slice bounds along one axis.  A = coordinate that is sliced (x for
@@ -196,15 +197,18 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   __syncwarp();
   // D4/D5 in the normalized pose, D7 orientation
   merged_slices(S, X, Y, nv, w, h, k, lane);
-  int64_t TOP = 0, BOT = 0, LEFT = 0, RIGHT = 0;
+  // empty-area sums: every term is in [0, 2^25] and k <= 64, so the sums fit
+  // 32 unsigned bits and reduce in hardware (REDUX)
+  uint32_t top = 0, bot = 0, left = 0, right = 0;
   for (int j = lane; j < k; j += 32) {
-    TOP += S.mlo[0][j];
-    BOT += h - S.mhi[0][j];
-    LEFT += S.mlo[1][j];
-    RIGHT += w - S.mhi[1][j];
+    top += (uint32_t)S.mlo[0][j];
+    bot += (uint32_t)(h - S.mhi[0][j]);
+    left += (uint32_t)S.mlo[1][j];
+    right += (uint32_t)(w - S.mhi[1][j]);
   }
-  TOP = warp_sum64(TOP); BOT = warp_sum64(BOT);
-  LEFT = warp_sum64(LEFT); RIGHT = warp_sum64(RIGHT);
+  const int64_t TOP = __reduce_add_sync(0xffffffffu, top), BOT = __reduce_add_sync(0xffffffffu, bot);
+  const int64_t LEFT = __reduce_add_sync(0xffffffffu, left);
+  const int64_t RIGHT = __reduce_add_sync(0xffffffffu, right);
   const bool fy = TOP > BOT;
   const int64_t D = LEFT - RIGHT;
   bool fx;
@@ -241,28 +245,39 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     sl[2 * k + j] = S.mlo[1][j];
     sl[3 * k + j] = S.mhi[1][j];
   }
-  // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j
-  i128 best = -1;
-  int bj = 0;
-  int64_t bu0 = 0, bu1 = 0, bv0 = 0, bv1 = 0;
-  for (int j = 0; j < 8; j++) {
+  // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j.
+  // All 8 angles at once: lane = 4 * angle + vertex group, so the extents are
+  // reduced over 4 lanes (2 shuffle steps) instead of 32 lanes per angle.
+  {
+    const int j = lane >> 2, g = lane & 3;
     const int64_t C = kQC[j], Sn = kQS[j];
     int64_t u0 = INT64_MAX, u1 = INT64_MIN, v0 = INT64_MAX, v1 = INT64_MIN;
-    for (int v = lane; v < nv; v += 32) {
-      int64_t u = (int64_t)X[v] * C + (int64_t)Y[v] * Sn;
-      int64_t vv = -(int64_t)X[v] * Sn + (int64_t)Y[v] * C;
+    for (int v = g; v < nv; v += 4) {
+      const int64_t x = X[v], y = Y[v];
+      const int64_t u = x * C + y * Sn, vv = -x * Sn + y * C;
       u0 = u < u0 ? u : u0; u1 = u > u1 ? u : u1;
       v0 = vv < v0 ? vv : v0; v1 = vv > v1 ? vv : v1;
     }
-    u0 = warp_min64(u0); u1 = warp_max64(u1);
-    v0 = warp_min64(v0); v1 = warp_max64(v1);
-    i128 area = (i128)(u1 - u0) * (i128)(v1 - v0);
-    if (best < 0 || area < best) {
-      best = area; bj = j;
-      bu0 = u0; bu1 = u1; bv0 = v0; bv1 = v1;
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      int64_t t = __shfl_xor_sync(0xffffffffu, u0, o); u0 = t < u0 ? t : u0;
+      t = __shfl_xor_sync(0xffffffffu, u1, o); u1 = t > u1 ? t : u1;
+      t = __shfl_xor_sync(0xffffffffu, v0, o); v0 = t < v0 ? t : v0;
+      t = __shfl_xor_sync(0xffffffffu, v1, o); v1 = t > v1 ? t : v1;
     }
+    if (g == 0) {
+      S.ob[j][0] = u0; S.ob[j][1] = u1; S.ob[j][2] = v0; S.ob[j][3] = v1;
+    }
+    __syncwarp();
   }
   if (lane == 0) {
+    i128 best = -1;
+    int bj = 0;
+    for (int j = 0; j < 8; j++) {
+      const i128 area = (i128)(S.ob[j][1] - S.ob[j][0]) * (i128)(S.ob[j][3] - S.ob[j][2]);
+      if (best < 0 || area < best) { best = area; bj = j; }
+    }
+    const int64_t bu0 = S.ob[bj][0], bu1 = S.ob[bj][1], bv0 = S.ob[bj][2], bv1 = S.ob[bj][3];
     P.w[c] = (int32_t)w;
     P.h[c] = (int32_t)h;
     P.area2[c] = (int64_t)s2;

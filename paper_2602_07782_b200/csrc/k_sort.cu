@@ -1,16 +1,22 @@
 // k_sort.cu -- K2: decreasing-height order + footprint slot layout.
 //
 // P:139 "sorted in decreasing height order"; ties by the wider chart, then by
-// chart index -- realised as a STABLE LSD radix sort on the key
-// ((hmax - h) << bw) | (wmax - w) with the chart index as payload, so equal
-// keys keep index order.  One CTA of 1024 threads: per-tile digit ranks from
-// warp match masks + per-warp digit counts, 8-bit digits, only the
-// significant bits of the key are sorted.
+// chart index.  Three exact paths by N:
+//   N <= 4096    bitonic sort in one CTA's shared memory of the packed unique
+//                keys (h, w, index) -- a few microseconds;
+//   N <= 2^17    rank sort: rank(i) = #{j : (key_j, j) < (key_i, i)} over a
+//                2-D grid of (key block, key tile), then a scatter;
+//   larger       STABLE LSD radix sort on ((hmax - h) << bw) | (wmax - w) with
+//                the chart index as payload, one CTA of 1024 threads: per-tile
+//                digit ranks from warp match masks + per-warp digit counts.
 //
 // prep_kernel then lays out, per sorted position, the int16 footprint slots
 // every candidate uses (slot = footprint at the largest scale, clipped to the
 // dilated atlas) with a block-wide exclusive scan, and flags the pack for a
 // capacity retry if the slots do not fit the current buffers.
+#include <cstdlib>
+#include <cstring>
+
 #include "tabi_internal.cuh"
 
 namespace tabi {
@@ -130,6 +136,73 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
   __syncthreads();
 }
 
+// ---- small and medium N: comparison sorts on unique keys -------------------
+// D9 order (h desc, w desc, index asc) as one unsigned key per chart; w, h <
+// 2^26 units (|coordinate| <= 2^24), so (2^26-1-h, 2^26-1-w, index) packs in
+// 64 bits for N <= 4096 and the packed keys are unique: any correct sort gives
+// the stable order.
+constexpr int kBitonicMax = 4096;
+constexpr int kRankMax = 1 << 17;
+constexpr int kRankT = 256;   // rank sort: keys i per block
+constexpr int kRankJ = 1024;  // rank sort: keys j per block (shared-memory tile)
+
+__device__ __forceinline__ uint64_t order_key(int32_t h, int32_t w) {
+  return ((uint64_t)(0x3ffffffu - (uint32_t)h) << 26) | (uint64_t)(0x3ffffffu - (uint32_t)w);
+}
+
+// N <= 4096: bitonic sort of the packed keys in shared memory, one CTA.
+__global__ void __launch_bounds__(kT, 1)
+bitonic_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n,
+               int32_t* perm, const Status* st) {
+  __shared__ uint64_t key[kBitonicMax];
+  if (st->bad_chart != INT32_MAX) return;
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += kT)
+    key[i] = i < n ? (order_key(hh[i], ww[i]) << 12) | (uint64_t)i : ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += kT) {
+        const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const uint64_t a = key[lo], b = key[hi];
+        if ((a > b) == ((lo & size) == 0)) { key[lo] = b; key[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += kT) perm[i] = (int32_t)(key[i] & 0xfffu);
+}
+
+// N <= 2^17: rank of key i = #{j : (key_j, j) < (key_i, i)}, counted over a 2-D
+// grid of (i block, j tile) with one atomicAdd per thread and tile, then a
+// scatter perm[rank[i]] = i.
+__global__ void __launch_bounds__(kRankT)
+rank_count_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n,
+                  int32_t* rank, const Status* st) {
+  __shared__ uint64_t tile[kRankJ];
+  if (st->bad_chart != INT32_MAX) return;
+  const int i = blockIdx.x * kRankT + threadIdx.x;
+  const int j0 = blockIdx.y * kRankJ, m = min(kRankJ, n - j0);
+  for (int q = threadIdx.x; q < m; q += kRankT) tile[q] = order_key(hh[j0 + q], ww[j0 + q]);
+  __syncthreads();
+  if (i >= n) return;
+  const uint64_t ki = order_key(hh[i], ww[i]);
+  const int lim = min(m, i - j0);  // tile entries with index j < i (ties count)
+  int cnt = 0;
+  int q = 0;
+  for (; q < lim; q++) cnt += tile[q] <= ki;
+  for (; q < m; q++) cnt += tile[q] < ki;
+  if (cnt) atomicAdd(&rank[i], cnt);
+}
+
+__global__ void rank_scatter_kernel(const int32_t* __restrict__ rank, int32_t n, int32_t* perm,
+                                    const Status* st) {
+  if (st->bad_chart != INT32_MAX) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) perm[rank[i]] = i;
+}
+
 // Footprint slots: column slot of sorted position s = min(ceil(w/256) + 2g, W'),
 // row slot = min(ceil(h/256) + 2g, H') -- the footprint at the largest scale
 // (m = M, scale 1) bounds every candidate's (w_s is monotone in m).
@@ -221,9 +294,26 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
 
 }  // namespace
 
-void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
-                 int32_t* perm2, const Status* st, cudaStream_t s) {
+int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
+                int32_t* perm2, const Status* st, cudaStream_t s) {
+  // TABI_SORT=bitonic|rank|radix forces a path (tests cover all three)
+  const char* force = getenv("TABI_SORT");
+  const bool want_rank = force && strcmp(force, "rank") == 0;
+  const bool want_radix = force && strcmp(force, "radix") == 0;
+  if (n <= kBitonicMax && !want_rank && !want_radix) {
+    bitonic_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, perm, st);
+    return 1;
+  }
+  if (n <= kRankMax && !want_radix) {
+    int32_t* rank = (int32_t*)keys2;
+    cudaMemsetAsync(rank, 0, sizeof(int32_t) * (size_t)n, s);
+    rank_count_kernel<<<dim3((n + kRankT - 1) / kRankT, (n + kRankJ - 1) / kRankJ), kRankT, 0, s>>>(
+        P.h, P.w, n, rank, st);
+    rank_scatter_kernel<<<(n + 255) / 256, 256, 0, s>>>(rank, n, perm, st);
+    return 2;
+  }
   sort_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, keys, keys2, perm, perm2, st);
+  return 1;
 }
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,

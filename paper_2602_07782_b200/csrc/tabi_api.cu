@@ -325,8 +325,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
   launches++;
   tm.mark(s);
-  launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
-  launches++;
+  launches += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
   tm.mark(s);
   tabi_placement* d_out = on_device ? out : ctx->d_out;
   // Candidate waves: prep_kernel computes the area
@@ -652,8 +651,7 @@ extern "C" tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16) {
   out16[3] = (int64_t)st.tr[4];
   out16[4] = (int64_t)st.tr[5];
   out16[5] = ctx->last_fused;
-  for (int i = 0; i < 8; i++) out16[6 + i] = (int64_t)st.ph[i];
-  out16[14] = out16[15] = 0;
+  for (int i = 0; i < 10; i++) out16[6 + i] = (int64_t)st.ph[i];
   return TABI_OK;
 }
 

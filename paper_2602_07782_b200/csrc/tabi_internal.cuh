@@ -315,7 +315,7 @@ struct Status {       // device-side status block, copied back once per pack
   unsigned long long tr[6];
   // K4 row-phase time (ns, thread 0 of every packer, summed): knee update,
   // fold, HC choice + lock pairs, push, Alg. 1, score, select + commit, FindKnee
-  unsigned long long ph[8];
+  unsigned long long ph[10];  // + [8] push staging, [9] commit staging
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -366,8 +366,10 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
 namespace tabi {
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
-void launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
-                 int32_t* perm2, const Status* st, cudaStream_t s);
+// D9 sort: bitonic in smem (N <= 4096), rank sort (N <= 2^17), else radix.
+// Returns the number of kernels launched.
+int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
+                int32_t* perm2, const Status* st, cudaStream_t s);
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
                  cudaStream_t s);

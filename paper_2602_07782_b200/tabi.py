@@ -245,7 +245,8 @@ class Context:
         keys = ("raster_end", "pack_end", "pack_wait", "raster_wait", "tiles", "fused")
         d = dict(zip(keys, (int(v) for v in out[:6])))
         d["phases"] = dict(zip(("knee", "fold", "hc_locks", "push", "alg1", "score", "commit",
-                                "findknee"), (int(v) for v in out[6:14])))
+                                "findknee", "push_stage", "commit_stage"),
+                               (int(v) for v in out[6:16])))
         return d
 
     def _chk(self, st):

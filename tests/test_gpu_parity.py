@@ -277,6 +277,28 @@ def test_pack_batch_equals_single_packs(ctx):
     c3.close()
 
 
+@pytest.mark.parametrize("path", ["bitonic", "rank", "radix"])
+def test_sort_paths_with_ties(orc, ctx, path, monkeypatch):
+    """D9 order (h desc, w desc, index asc) through each of the three sort paths
+    (TABI_SORT forces one), on inputs full of exact (h, w) ties: index order
+    must decide them."""
+    import oracle
+    from paper_2602_07782_b200 import spec_of
+    monkeypatch.setenv("TABI_SORT", path)
+    rng = np.random.default_rng(5)
+    polys = []
+    for i in range(900):
+        w, h = [(8, 8), (8, 12), (12, 8), (5, 20)][rng.integers(0, 4)]
+        if rng.random() < 0.2:
+            w, h = int(rng.integers(3, 30)), int(rng.integers(3, 30))
+        polys.append([(0, 0), (w, 0), (w, h), (0, h)])
+    cs = chartgen.from_polygons(polys, 512, 512)
+    ctx.pack(cs.xy, cs.start, spec_of(cs, scale_count=4))
+    _, px, _ = oracle.build_proxies(cs.xy, cs.start, cs.local_aabb_count, (1.0, 1.0))
+    assert np.array_equal(ctx.perm(cs.n_charts), oracle.sort_order(px))
+    _compare_pack(orc, ctx, chartgen.config2(2), check_profiles=0)
+
+
 def test_determinism_and_capacity_growth():
     from paper_2602_07782_b200 import Context, spec_of
     cs = chartgen.config3(1, rho=2.0)
