@@ -218,6 +218,9 @@ def main():
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--rho", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flush", default="write", choices=["write", "write+read"],
+                    help="L2 flush between timed steps: a 256 MB write (default), or that "
+                         "write followed by a 256 MB read so L2 holds no dirty lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_setup()
@@ -243,6 +246,13 @@ def main():
     dev_in = [(torch.from_numpy(cs.xy).to(dev), torch.from_numpy(cs.start).to(dev),
                torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)) for cs in sets]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.zeros(64 << 20, dtype=torch.int32, device=dev) if args.flush == "write+read" \
+        else None
+
+    def do_flush():
+        flush.zero_()
+        if flush_rd is not None:
+            flush_rd.sum()
 
     def step_dev():
         infos = []
@@ -264,7 +274,7 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            flush.zero_()
+            do_flush()
             ev[i][0].record(stream)
             infos = step_dev()
             ev[i][1].record(stream)
@@ -291,7 +301,7 @@ def main():
     torch.cuda.synchronize()
     barrier(ws)
     for i in range(e2e_steps):
-        flush.zero_()
+        do_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for cs, spec in zip(sets, specs):
@@ -312,7 +322,14 @@ def main():
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     # int32 lane-op issue peak: 148 SMs x 4 SMSPs x 32 lanes x clock
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # G lane-ops/s
-    work = {5: work_pack / npk, 3: work_prof / npk}.get(k_dom)
+    fused = bool(infos[0].fused)
+    if fused and k_dom == 5:
+        # the fused wave kernel rasterizes footprints (K3), computes pair offsets
+        # (K3b) and runs the row loop (K4) in one launch: its work is both
+        work = (work_pack + work_prof) / npk
+        names[5] = "fused_wave (K3+K3b+K4)"
+    else:
+        work = {5: work_pack / npk, 3: work_prof / npk}.get(k_dom)
     roof = {"kernel": names[k_dom], "bound": "alu", "unit": "Gop/s",
             "peak": alu_peak, "peak_kind": f"derived from {pk_kind} sm_max_mhz (148x128 int32 lanes)",
             "stage_ms": {names[i]: round(float(stage_avg[i]), 5) for i in range(8)},
@@ -321,13 +338,15 @@ def main():
         ach = work / (stage_avg[k_dom] * 1e-3) / 1e9
         roof.update({"achieved": ach, "frac": ach / alu_peak,
                      "work_per_launch": work,
-                     "work_unit": ("frontline column visits" if k_dom == 5 else
+                     "work_unit": ("frontline column visits + footprint entries"
+                                   if fused and k_dom == 5 else
+                                   "frontline column visits" if k_dom == 5 else
                                    "footprint entries")})
     else:
         roof.update({"achieved": None, "frac": None})
     tr = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr):
-        roof["traffic"] = json.load(open(tr)).get(names[k_dom])
+        roof["traffic"] = json.load(open(tr)).get(args.workload, {}).get(names[k_dom])
     # HBM context: compulsory bytes per pack
     hbm_bytes = sum(cs.xy.nbytes + cs.start.nbytes + 32 * cs.n_charts for cs in sets) / len(sets)
     info = infos[0]
@@ -335,7 +354,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (chartgen SplitMix64, seed = rank)",
-            "config": {"workload": desc, "l2": "flushed between steps (256 MB write, untimed)",
+            "config": {"workload": desc, "l2": ("flushed between steps (256 MB write, untimed)" if args.flush == "write"
+                             else "flushed between steps (256 MB write + 256 MB read, untimed)"),
                        "parallelism": (f"{ws} independent packs per step (one per GPU)"
                                        if scaling == "weak" else
                                        f"512 atlases per step sharded over {ws} GPU(s)")},

@@ -3,7 +3,8 @@
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--json out.json]
 
 Prints, per captured kernel: duration, SM/memory throughput, occupancy,
-registers, IPC, active threads per warp, DRAM bytes (read+write -> the
+registers, IPC, active threads per warp (durations in ns, bytes in bytes,
+converted from the report's units), DRAM bytes (read+write -> the
 `traffic` of bench.py's roofline) and the top warp-stall reasons.
 """
 import csv
@@ -37,6 +38,10 @@ def main():
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
+    unit_of = dict(zip(hdr, units))
+    scale = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+             "second": 1e9, "s": 1e9,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     out = []
     for r in data:
         d = dict(zip(hdr, r))
@@ -45,7 +50,7 @@ def main():
         for k, v in KEYS.items():
             if k in d:
                 try:
-                    rec[v] = float(d[k].replace(",", ""))
+                    rec[v] = float(d[k].replace(",", "")) * scale.get(unit_of.get(k, ""), 1.0)
                 except ValueError:
                     rec[v] = d[k]
         stalls = {}
