@@ -218,9 +218,10 @@ def main():
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--rho", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--flush", default="write", choices=["write", "write+read"],
+    ap.add_argument("--flush", default="write", choices=["write", "write+read", "none"],
                     help="L2 flush between timed steps: a 256 MB write (default), or that "
-                         "write followed by a 256 MB read so L2 holds no dirty lines")
+                         "write followed by a 256 MB read so L2 holds no dirty lines; "
+                         "'none' is a warm-cache diagnostic, not a bench value")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_setup()
@@ -250,6 +251,8 @@ def main():
         else None
 
     def do_flush():
+        if args.flush == "none":
+            return
         flush.zero_()
         if flush_rd is not None:
             flush_rd.sum()
@@ -260,13 +263,12 @@ def main():
             infos.append(ctx.pack(xy_d, start_d, spec, out=out_d, stream=stream.cuda_stream)[2])
         return infos
 
+    os.environ["TABI_TIMING"] = "0"
     for _ in range(args.warmup):
         step_dev()
     torch.cuda.synchronize()
-    os.environ["TABI_TIMING"] = "1"
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    stage = np.zeros(8)
     launches = 0
     work_pack = work_prof = 0
     infos = None
@@ -279,12 +281,21 @@ def main():
             infos = step_dev()
             ev[i][1].record(stream)
             for info in infos:
-                stage += np.array(info.stage_ms[:8])
                 launches += info.gpu_launches
                 work_pack += info.work_pack
                 work_prof += info.work_profile
     torch.cuda.synchronize()
     barrier(ws)
+    # per-stage device times (TABI_TIMING events inside tabi_pack) from separate,
+    # untimed steps: the events and their host syncs stay out of the timed loop
+    os.environ["TABI_TIMING"] = "1"
+    stage = np.zeros(8)
+    stage_steps = min(args.steps, 20)
+    for i in range(stage_steps):
+        do_flush()
+        for info in step_dev():
+            stage += np.array(info.stage_ms[:8])
+    torch.cuda.synchronize()
     os.environ["TABI_TIMING"] = "0"
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = allmax(sum(step_ms), ws)
@@ -315,7 +326,7 @@ def main():
 
     # ---- roofline of the dominant kernel -------------------------------
     npk = args.steps * len(sets)
-    stage_avg = stage / npk
+    stage_avg = stage / (stage_steps * len(sets))
     names = ["h2d", "proxies", "sort", "profiles", "offsets_locks", "fold_push", "select", "d2h"]
     k_dom = int(np.argmax(stage_avg[1:7])) + 1
     pk, pk_kind = peaks()
@@ -354,8 +365,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (chartgen SplitMix64, seed = rank)",
-            "config": {"workload": desc, "l2": ("flushed between steps (256 MB write, untimed)" if args.flush == "write"
-                             else "flushed between steps (256 MB write + 256 MB read, untimed)"),
+            "config": {"workload": desc,
+                       "l2": {"write": "flushed between steps (256 MB write, untimed)",
+                              "write+read": "flushed between steps (256 MB write + 256 MB read, "
+                                            "untimed)",
+                              "none": "NOT flushed (warm-cache diagnostic, not a bench value)"
+                              }[args.flush],
                        "parallelism": (f"{ws} independent packs per step (one per GPU)"
                                        if scaling == "weak" else
                                        f"512 atlases per step sharded over {ws} GPU(s)")},

@@ -181,10 +181,11 @@ tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* 
  * [0] last raster group end and [1] last packer end, both from the fused
  * kernel's first CTA start (0 if split); [2] packer ns waiting for tiles (sum
  * over packers); [3] raster ns waiting for a left neighbour tile (sum);
- * [4] tiles rasterized; [5] fused (0/1); [6..13] K4 row-phase ns summed over
- * packers (knee update, fold, HC choice + lock pairs, push, Alg. 1, score,
- * select + commit, FindKnee); [14] of which push staging, [15] of which
- * commit staging. */
+ * [4] tiles rasterized; [5] fused (0/1); [6..13] K4 row-phase SM cycles
+ * summed over packers (knee update, fold, HC choice + lock pairs, push,
+ * Alg. 1, score, select + commit, FindKnee); [14] of which push staging, [15]
+ * of which commit staging.  [6..15] are 0 unless the library was built with
+ * -DTABI_PHASE_TRACE. */
 tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16);
 
 #ifdef __cplusplus

@@ -51,6 +51,9 @@ struct Smem {
   int32_t changed, npairs, pair_overflow;
   int32_t sel_cfg;
   int32_t win_s0, win_e, pglobal, a0;
+  int32_t pf_out, pf_a0, pf_a1;  // row-top footprint prefetch (words [pf_a0, pf_a1))
+  int32_t fold_hi, next_a0;      // fold's scanned end; colofs of the next row start (or -1)
+  int32_t changed3[3];           // Alg. 1 rotating change flags
   int32_t prefix_rows, switched;
   unsigned long long knee_key;
   unsigned long long work;
@@ -218,6 +221,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   // fences (acquire pattern: relaxed load + fence.acq_rel, which also drops
   // the SM's L1 so later plain loads see the published data).
   __shared__ int32_t ready_lim;
+  if (tid == 0) ready_lim = -1;
   auto wait_ready = [&](int s) -> int {
     if (!rd.flags) return n - 1;
     const int t_need = rd.tix[min(s + 1, n - 1)];
@@ -308,6 +312,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   for (int x = tid; x < Wp; x += kNT) F[x] = prefix_mode ? fsave[x] : 0;  // top
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
+    S.next_a0 = 0; S.fold_hi = 0; S.pf_out = 0;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
     S.prefix_rows = 0;
@@ -323,26 +328,41 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   __syncthreads();
   uint32_t phase = 0;
   unsigned long long wk = 0;  // frontline column visits by this thread
-  // row-phase timing (thread 0, %globaltimer; a few reads per row)
-  unsigned long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t_last = gtime();
+  // row-phase timing (thread 0, SM clock cycles), compiled in only for the
+  // trace build (-DTABI_PHASE_TRACE, tools/fused_trace.py)
+  unsigned long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#ifdef TABI_PHASE_TRACE
+  long long t_last = clock64();
   auto phase_mark = [&](int i) {
     if (tid == 0) {
-      const unsigned long long t = gtime();
-      ph[i] += t - t_last;
+      const long long t = clock64();
+      ph[i] += (unsigned long long)(t - t_last);
       t_last = t;
     }
   };
+#else
+  auto phase_mark = [](int) {};
+#endif
 
   // Stage window [ws0, we) of the current row (no-op if already staged).
+  // A row's footprints are prefetched by one TMA copy issued at the top of the
+  // row (before the knee update and the fold), covering the published slots
+  // from the row start up to a cap; the first stage() of the row consumes it
+  // if its window lies inside (else drains it and copies the exact window).
+  bool pf_pending = false;  // uniform: a prefetch copy is in flight
   auto stage = [&](int ws0, int we) {
     if (S.win_s0 == ws0 && S.win_e == we) return;
     const int nwin = we - ws0;
-    const int32_t c0 = colofs[ws0];
-    const int32_t c1 = we < n ? colofs[we] : cols_total;
+    // the fold already wrote the scalars of the row's first kRW charts
+    // (positions below S.fold_hi), footprint offsets included
+    const bool fw = !prefix_mode && ws0 == S.row_start;
+    const bool have = fw && nwin <= kRW;
+    const int32_t c0 = have ? W.rco[0] : colofs[ws0];
+    const int32_t c1 = we >= n ? cols_total
+                               : (fw && we < S.fold_hi && nwin < kRW) ? W.rco[nwin] : colofs[we];
     const int32_t a0 = c0 & ~3, a1 = (c1 + 3) & ~3;
     const bool pg = (a1 - a0) > W.prof_cap;
-    // the fold already wrote the scalars of the row's first kRW charts
-    const bool have = !prefix_mode && ws0 == S.row_start && nwin <= kRW;
+    const bool hit = pf_pending && c0 >= S.pf_a0 && c1 <= S.pf_a1;
     __syncthreads();  // previous readers of the window buffers are done
     for (int k = tid; k < nwin && !have; k += kNT) {
       const int s = ws0 + k;
@@ -351,9 +371,18 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       W.rwd[k] = wd[s];
       W.rco[k] = colofs[s];
     }
-    if (!pg && tid == 0) bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
-    if (tid == 0) { S.win_s0 = ws0; S.win_e = we; S.pglobal = pg; S.a0 = a0; }
-    if (!pg) {
+    if (pf_pending) {  // consume (hit) or drain (miss) the row-top prefetch
+      mbar_wait(&S.mbar, phase);
+      phase ^= 1u;
+      pf_pending = false;
+    }
+    if (!hit && !pg && tid == 0) bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
+    if (tid == 0) {
+      S.win_s0 = ws0; S.win_e = we;
+      S.pglobal = hit ? 0 : pg;
+      S.a0 = hit ? S.pf_a0 : a0;
+    }
+    if (!hit && !pg) {
       mbar_wait(&S.mbar, phase);
       phase ^= 1u;
     }
@@ -389,6 +418,22 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         }
         __syncthreads();
         break;
+      }
+    }
+    // ---- footprint prefetch for this row (consumed by the push's stage) ----
+    // (no global loads on thread 0's path: the row start's slot offset was
+    // kept from the previous row's fold; in fused mode only once every tile
+    // is published)
+    if (!prefix_mode && tid == 0) {
+      S.pf_out = 0;
+      const bool all = !rd.flags || ready_lim == n - 1;
+      if (all && S.next_a0 >= 0) {
+        const int32_t a0 = S.next_a0 & ~3;
+        const int32_t a1 = min((cols_total + 3) & ~3, a0 + min(W.prof_cap, 4 * f_words));
+        if (a1 > a0) {
+          bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
+          S.pf_out = 1; S.pf_a0 = a0; S.pf_a1 = a1;
+        }
       }
     }
     // ---- Alg. 2 UpdateKneeLocation ---------------------------
@@ -435,6 +480,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     if (tid < 4) S.endv[tid] = INT32_MIN;
     if (tid == 0) { S.done = 0; S.win_s0 = -1; S.win_e = -1; }
     __syncthreads();
+    pf_pending = S.pf_out != 0 && !prefix_mode;
     if (prefix_mode) {
       // prefix rows were laid out by the tail kernels (positions in xs0/xs1);
       // the row is the run of equal row ids starting at rs
@@ -490,6 +536,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             for (int q = 0; q < 4; q++)
               if (S.endv[q] == INT32_MIN) S.endv[q] = n - 1;
             S.done = 1;
+            S.fold_hi = base + cnt;  // W.* hold positions [rs, min(fold_hi, rs + kRW))
           }
         }
         __syncthreads();
@@ -521,6 +568,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t hc0 = S.hcsel[0], hc1 = S.hcsel[1];
     const int32_t endA = S.end_cfg[0], endK = S.end_cfg[2];
     const int ncfg = knee_ok ? 4 : 2;
+    // A row of at most kRW charts (the normal case) is one window: its Y
+    // values then live in shared memory from push to commit, and the fold's
+    // window scalars (W.rx1, W.rwd) serve the lock-pair scan; longer rows
+    // round-trip through HBM per window.
+    const bool one = endA - rs + 1 <= kRW;
+    const bool useW = one && !prefix_mode;
     // ---- D15: non-adjacent lock pairs of the row (HC folds only) ----------
     const int32_t R = max(hc0 ? endA : -1, (knee_ok && hc1) ? endK : -1);
     if (!adj_only && R > rs) {
@@ -528,7 +581,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       for (int base = rs; base <= R; base += kNT) {
         const int a = base + tid;
         int32_t cnt = 0;
-        if (a <= R) {
+        if (a <= R && useW) {
+          const int32_t xa = W.rx1[a - rs], wa = W.rwd[a - rs];
+          for (int b = a + 2; b <= R && W.rx1[b - rs] - xa < wa; b++) cnt++;
+        } else if (a <= R) {
           const int32_t xa = xs1[a], wa = wd[a];
           for (int b = a + 2; b <= R && xs1[b] - xa < wa; b++) cnt++;
         }
@@ -563,7 +619,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       for (int p = wid; p < np; p += kNW) {
         const int a = pa[p], b = pb[p];
         bool la, lb;
-        warp_locks(row + rowofs[a], row + rowofs[b], hd[a], hd[b], xs1[b] - xs1[a], lane, la, lb);
+        const int32_t dx = useW ? W.rx1[b - rs] - W.rx1[a - rs] : xs1[b] - xs1[a];
+        warp_locks(row + rowofs[a], row + rowofs[b], hd[a], hd[b], dx, lane, la, lb);
         if (lane == 0) plk[p] = (la ? 1 : 0) | (lb ? 2 : 0);
       }
       __syncthreads();
@@ -581,10 +638,6 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     };
 
     // ---- push: Y = max over covered columns of F - TopEdge ----
-    // A row of at most kRW charts (the normal case) is one window: its Y
-    // values then live in shared memory from push to commit; longer rows
-    // round-trip them through Yc in HBM per window.
-    const bool one = endA - rs + 1 <= kRW;
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
       stage(ws0, we);
@@ -634,36 +687,63 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       const int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // HC configs [c0, c1)
       if (c1 > c0) {
         const int32_t per = (endA - rs) + (adj_only ? 0 : np);  // adjacent pairs + list
-        while (true) {
-          if (tid == 0) S.changed = 0;
-          __syncthreads();
-          for (int it = tid; it < (c1 - c0) * per; it += kNT) {
-            const int cfg = c0 + it / per;
-            const int q = it % per;
-            const int32_t endc = S.end_cfg[cfg];
-            int a, b, bits;
-            if (q < endA - rs) {
-              a = rs + q;
-              b = a + 1;
-              if (b > endc) continue;
-              bits = lk[a];
-            } else {
-              const int p = q - (endA - rs);
-              a = pa[p];
-              b = pb[p];
-              if (b > endc) continue;
-              bits = plk[p];
+        const int nitems = (c1 - c0) * per;
+        // item -> (Ya, Yb, lock bits); with <= 2 items per thread they are
+        // resolved once and kept in registers across the fixpoint iterations
+        auto item = [&](int it, int32_t*& Ya, int32_t*& Yb, int& bits) -> bool {
+          const int cfg = c0 + it / per;
+          const int q = it % per;
+          const int32_t endc = S.end_cfg[cfg];
+          int a, b;
+          if (q < endA - rs) {
+            a = rs + q;
+            b = a + 1;
+            if (b > endc) return false;
+            bits = lk[a];
+          } else {
+            const int p = q - (endA - rs);
+            a = pa[p];
+            b = pb[p];
+            if (b > endc) return false;
+            bits = plk[p];
+          }
+          Ya = one ? &W.rY[cfg * kRW + (a - rs)] : &Yc[(int64_t)cfg * n + a];
+          Yb = one ? &W.rY[cfg * kRW + (b - rs)] : &Yc[(int64_t)cfg * n + b];
+          return bits != 0;
+        };
+        auto relax = [&](int32_t* Ya, int32_t* Yb, int bits, int flag) {
+          const int32_t ya = one ? *(volatile int32_t*)Ya : __ldcg(Ya);
+          const int32_t yb = one ? *(volatile int32_t*)Yb : __ldcg(Yb);
+          if ((bits & 1) && ya < yb) { atomicMax(Ya, yb); S.changed3[flag] = 1; }
+          if ((bits & 2) && yb < ya) { atomicMax(Yb, ya); S.changed3[flag] = 1; }
+        };
+        const bool cached = nitems <= 2 * kNT;
+        int32_t *ya0 = nullptr, *yb0 = nullptr, *ya1 = nullptr, *yb1 = nullptr;
+        int bits0 = 0, bits1 = 0;
+        bool v0 = false, v1 = false;
+        if (cached) {
+          if (tid < nitems) v0 = item(tid, ya0, yb0, bits0);
+          if (tid + kNT < nitems) v1 = item(tid + kNT, ya1, yb1, bits1);
+        }
+        // one barrier per iteration: iteration i raises flag i % 3 and clears
+        // flag (i + 1) % 3, last read two barriers ago
+        if (tid == 0) { S.changed3[0] = 0; S.changed3[1] = 0; }
+        __syncthreads();
+        for (int iter = 0;; iter++) {
+          const int fl = iter % 3;
+          if (tid == 0) S.changed3[(iter + 1) % 3] = 0;
+          if (cached) {
+            if (v0) relax(ya0, yb0, bits0, fl);
+            if (v1) relax(ya1, yb1, bits1, fl);
+          } else {
+            for (int it = tid; it < nitems; it += kNT) {
+              int32_t *Ya, *Yb;
+              int bits;
+              if (item(it, Ya, Yb, bits)) relax(Ya, Yb, bits, fl);
             }
-            int32_t* Ya = one ? &W.rY[cfg * kRW + (a - rs)] : &Yc[(int64_t)cfg * n + a];
-            int32_t* Yb = one ? &W.rY[cfg * kRW + (b - rs)] : &Yc[(int64_t)cfg * n + b];
-            const int32_t ya = one ? *(volatile int32_t*)Ya : __ldcg(Ya);
-            const int32_t yb = one ? *(volatile int32_t*)Yb : __ldcg(Yb);
-            if ((bits & 1) && ya < yb) { atomicMax(Ya, yb); S.changed = 1; }
-            if ((bits & 2) && yb < ya) { atomicMax(Yb, ya); S.changed = 1; }
           }
           __syncthreads();
-          if (!S.changed) break;
-          __syncthreads();
+          if (!S.changed3[fl]) break;
         }
       }
     }
@@ -739,6 +819,19 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int cfg = S.sel_cfg;
     const int f = cfg >> 1, dir = cfg & 1;
     const int32_t endS = S.end_cfg[cfg];
+    // ---- FindKnee after an atlas-fold row: the height
+    // drops of the row's charts, issued here so their loads overlap the commit
+    // walk (the commit's last barrier publishes S.knee_key) ------------------
+    if (f == 0 && !no_bal && !prefix_mode) {
+      for (int t = rs + tid; t < endS; t += kNT) {
+        const int64_t d = (int64_t)hsorted[t] - hsorted[t + 1];
+        if (10 * d >= (int64_t)pp.H * TABI_UNITS && 5 * d >= hsorted[t]) {
+          const unsigned long long key =
+              ((unsigned long long)d << 32) | (unsigned long long)(0x7fffffff - t);
+          atomicMax(&S.knee_key, key);
+        }
+      }
+    }
     for (int ws0 = rs; ws0 <= endS; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = min(we, endS + 1) - ws0;
       stage(ws0, we);
@@ -772,18 +865,6 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       __syncthreads();
     }
     phase_mark(6);
-    // ---- FindKnee after an atlas-fold row -----------
-    if (f == 0 && !no_bal && !prefix_mode) {
-      for (int t = rs + tid; t < endS; t += kNT) {
-        const int64_t d = (int64_t)hsorted[t] - hsorted[t + 1];
-        if (10 * d >= (int64_t)pp.H * TABI_UNITS && 5 * d >= hsorted[t]) {
-          const unsigned long long key =
-              ((unsigned long long)d << 32) | (unsigned long long)(0x7fffffff - t);
-          atomicMax(&S.knee_key, key);
-        }
-      }
-    }
-    __syncthreads();
     if (tid == 0) {
       if (prefix_mode) S.prefix_rows++;
       else S.rows++;
@@ -802,9 +883,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       }
       if (S.fmax > Hp) S.fail = 1;  // overflow below the atlas bottom
       S.row_start = endS + 1;
+      const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
+      S.next_a0 = (!prefix_mode && nx < n && nx < S.fold_hi && nx - rs < kRW) ? W.rco[nx - rs] : -1;
     }
     __syncthreads();
     phase_mark(7);
+  }
+  if (pf_pending) {  // a failed row left its prefetch in flight: let it land first
+    mbar_wait(&S.mbar, phase);
+    phase ^= 1u;
   }
   if (tid == 0)
     for (int i = 0; i < 10; i++) atomicAdd(&st->ph[i], ph[i]);
@@ -1002,7 +1089,10 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
                               const int32_t* __restrict__ Yo, const uint8_t* __restrict__ mir,
                               const Cand* __restrict__ cands, tabi_placement* out, Status* st) {
   __shared__ int32_t win, wr0, wp;
+  __shared__ Cand sc[TABI_MAX_SCALES];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
+  for (int i = threadIdx.x; i < pp.M; i += blockDim.x) sc[i] = cands[i];  // one parallel load
+  __syncthreads();
   if (threadIdx.x == 0) {
     // D25: the candidate with the largest area-weighted mean final scale,
     // V = A_seq * m * 2^20 + A_pre * p * M (exact, int128), ties -> larger m;
@@ -1011,7 +1101,7 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
     int32_t w = 0, r0 = pp.n, pw = 0;
     i128 bestV = -1;
     for (int m = 1; m <= pp.M; m++) {
-      const Cand cd = cands[m - 1];
+      const Cand& cd = sc[m - 1];
       if (!cd.success) continue;
       const bool tail = cd.switched_at >= 0;
       const i128 Ap = tail ? (i128)(((unsigned __int128)cd.apre_hi << 64) | cd.apre_lo) : 0;

@@ -292,7 +292,44 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
   }
 }
 
+// One launch instead of a status upload plus a string of memsets.
+// mode 2: initialise the status block (bad_chart = none, trace start = max);
+// mode >= 1: zero the candidate records and hybrid-tail states;
+// always: zero per-wave state (cand_bad, large-chart list, raster queue head,
+// fused ready flags / arrival counters).
+__global__ void reset_kernel(Status* st, int mode, Cand* cands, int32_t* t_state,
+                             int32_t* cand_bad, int M, int32_t* rdy, int64_t nrdy) {
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (t0 == 0) {
+    if (mode == 2) {
+      uint32_t* w = (uint32_t*)st;
+      for (size_t i = 0; i < sizeof(Status) / 4; i++) w[i] = 0;
+      st->bad_chart = INT32_MAX;
+      st->tr[0] = ~0ull;
+    } else {
+      st->pad[1] = 0;
+      st->work_next = 0;
+    }
+  }
+  if (mode >= 1) {
+    int32_t* cw = (int32_t*)cands;
+    for (int64_t i = t0; i < (int64_t)M * (int64_t)(sizeof(Cand) / 4); i += stride) cw[i] = 0;
+    for (int64_t i = t0; i < M; i += stride) t_state[i] = 0;
+  }
+  for (int64_t i = t0; i < M; i += stride) cand_bad[i] = 0;
+  for (int64_t i = t0; i < nrdy; i += stride) rdy[i] = 0;
+}
+
 }  // namespace
+
+void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
+                  int32_t* rdy, int64_t nrdy, cudaStream_t s) {
+  const int64_t work = nrdy > (int64_t)M * 16 ? nrdy : (int64_t)M * 16;
+  int blocks = (int)((work + 255) / 256);
+  if (blocks > 296) blocks = 296;
+  reset_kernel<<<blocks, 256, 0, s>>>(st, mode, cands, t_state, cand_bad, M, rdy, nrdy);
+}
 
 int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
                 int32_t* perm2, const Status* st, cudaStream_t s) {

@@ -21,6 +21,27 @@
 
 using namespace tabi;
 
+// Everything a captured first-wave graph bakes in: if any of it changes, the
+// graph is re-captured.
+struct GraphKey {
+  const void* xy;
+  const void* start;
+  const void* out;
+  int32_t n;
+  int64_t V;
+  int on_device;
+  float rx, ry;
+  tabi_spec spec;
+  int B, fused;
+  int64_t gen;
+  char sort_env;  // TABI_SORT (test knob) is read at capture time
+  bool operator==(const GraphKey& o) const {
+    return xy == o.xy && start == o.start && out == o.out && n == o.n && V == o.V &&
+           on_device == o.on_device && rx == o.rx && ry == o.ry && B == o.B && fused == o.fused &&
+           gen == o.gen && sort_env == o.sort_env && memcmp(&spec, &o.spec, sizeof(tabi_spec)) == 0;
+  }
+};
+
 struct tabi_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -78,6 +99,11 @@ struct tabi_ctx {
   // last pack (introspection)
   int32_t last_n = 0, last_M = 0, last_k = 0, last_g = 0, last_fused = 0;
   std::string err;
+  // first-wave CUDA graph (tabi_pack) and the buffer generation it was captured on
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{};
+  int g_launches = 0;
+  int64_t alloc_gen = 0;
 };
 
 #define CK(call)                                              \
@@ -88,6 +114,8 @@ struct tabi_ctx {
       return TABI_ECUDA;                                      \
     }                                                         \
   } while (0)
+
+constexpr size_t kStatusPad = (sizeof(Status) + 63) & ~(size_t)63;
 
 template <class T>
 static cudaError_t dalloc(T** p, size_t count) {
@@ -102,12 +130,12 @@ static void dfree_all(tabi_ctx* ctx) {
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
                 ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
                 ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->rdy, ctx->tstart, ctx->tix, ctx->X, ctx->Y, ctx->mir,
-                ctx->cands, ctx->dcol, ctx->t_state, ctx->t_r0, ctx->t_p, ctx->t_iter,
+                ctx->dcol, ctx->t_state, ctx->t_r0, ctx->t_p, ctx->t_iter,
                 ctx->t_fsave,
-                ctx->drow, ctx->scratch};
+                ctx->drow, ctx->scratch};  // cands / h_cands live inside the status blocks
   for (void* p : ps)
     if (p) cudaFree(p);
-  void* hs[] = {ctx->h_status, ctx->h_cands, ctx->h_xy, ctx->h_start, ctx->h_out};
+  void* hs[] = {ctx->h_status, ctx->h_xy, ctx->h_start, ctx->h_out};
   for (void* p : hs)
     if (p) cudaFreeHost(p);
 }
@@ -144,7 +172,9 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
   if (cudaSetDevice(cuda_device) != cudaSuccess) return fail();
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail();
   const size_t N = (size_t)max_charts, V = (size_t)max_vertices;
-  bool ok = dalloc(&ctx->d_xy, 2 * V) == cudaSuccess && dalloc(&ctx->d_start, N + 1) == cudaSuccess &&
+  // d_xy / h_xy: outline (2V floats) followed by the chart offsets (N + 1 ints)
+  bool ok = dalloc(&ctx->d_xy, 2 * V + N + 1) == cudaSuccess &&
+            dalloc(&ctx->d_start, 1) == cudaSuccess &&
             dalloc(&ctx->d_qx, V) == cudaSuccess && dalloc(&ctx->d_qy, V) == cudaSuccess &&
             dalloc(&ctx->P.w, N) == cudaSuccess && dalloc(&ctx->P.h, N) == cudaSuccess &&
             dalloc(&ctx->P.area2, N) == cudaSuccess && dalloc(&ctx->P.xmin, N) == cudaSuccess &&
@@ -159,8 +189,8 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
             dalloc(&ctx->d_status, 1) == cudaSuccess;
   if (!ok) return fail();
   if (cudaMallocHost((void**)&ctx->h_status, sizeof(Status)) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->h_xy, sizeof(float) * 2 * V) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->h_start, sizeof(int32_t) * (N + 1)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_xy, sizeof(float) * (2 * V + N + 1)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_start, sizeof(int32_t)) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->h_out, sizeof(tabi_placement) * N) != cudaSuccess)
     return fail();
   // initial footprint slot capacity per candidate (grows on demand)
@@ -175,6 +205,7 @@ extern "C" void tabi_ctx_destroy(tabi_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   dfree_all(ctx);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -199,12 +230,23 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
     CK(dalloc(&ctx->X, (size_t)M * N));
     CK(dalloc(&ctx->Y, (size_t)M * N));
     CK(dalloc(&ctx->mir, (size_t)M * N));
-    CK(dalloc(&ctx->cands, (size_t)M));
-    if (ctx->h_cands) cudaFreeHost(ctx->h_cands);
-    CK(cudaMallocHost((void**)&ctx->h_cands, sizeof(Cand) * M));
+    // status block and candidate records in ONE allocation (device and pinned
+    // host) so a wave's results come back with a single D2H copy
+    {
+      const size_t bytes = kStatusPad + sizeof(Cand) * (size_t)M;
+      cudaFree(ctx->d_status);
+      ctx->d_status = nullptr;
+      CK(cudaMalloc((void**)&ctx->d_status, bytes));
+      ctx->cands = (Cand*)((char*)ctx->d_status + kStatusPad);
+      cudaFreeHost(ctx->h_status);
+      ctx->h_status = nullptr;
+      CK(cudaMallocHost((void**)&ctx->h_status, bytes));
+      ctx->h_cands = (Cand*)((char*)ctx->h_status + kStatusPad);
+    }
     regrow_cols = regrow_pairs = true;
     ctx->cand_M = M;
   }
+  if (regrow_cols || regrow_pairs) ctx->alloc_gen++;  // captured graphs hold stale pointers
   const int32_t Mc = ctx->cand_M;
   if (regrow_cols) {
     CK(dalloc(&ctx->dcol, (size_t)Mc * ctx->col_cap));
@@ -284,13 +326,12 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
         return TABI_EINVAL;
       }
     if (V > ctx->max_v) return TABI_ECAPACITY;
+    // outline and chart offsets staged back to back: one H2D copy (enqueued
+    // with the first wave)
     memcpy(ctx->h_xy, xy, sizeof(float) * 2 * V);
-    memcpy(ctx->h_start, chart_start, sizeof(int32_t) * (n + 1));
-    CK(cudaMemcpyAsync(ctx->d_xy, ctx->h_xy, sizeof(float) * 2 * V, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ctx->d_start, ctx->h_start, sizeof(int32_t) * (n + 1),
-                       cudaMemcpyHostToDevice, s));
+    memcpy(ctx->h_xy + 2 * V, chart_start, sizeof(int32_t) * (n + 1));
     d_xy = ctx->d_xy;
-    d_start = ctx->d_start;
+    d_start = (const int32_t*)(ctx->d_xy + 2 * V);
   }
   tm.mark(s);
   const int32_t M = spec->scale_count;
@@ -317,17 +358,6 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   pp.T.fsave = ctx->t_fsave;
   pp.T.fstride = ctx->fstride;
 
-  Status init{};
-  init.bad_chart = INT32_MAX;
-  init.tr[0] = ~0ull;
-  *ctx->h_status = init;
-  CK(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, s));
-  launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
-  launches++;
-  tm.mark(s);
-  launches += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
-  tm.mark(s);
-  tabi_placement* d_out = on_device ? out : ctx->d_out;
   // Candidate waves: prep_kernel computes the area
   // bound m_hi (every m above it must fail); wave w evaluates m_hi - w*B - j,
   // j < B, all in parallel.  The first wave containing a success holds the
@@ -343,53 +373,64 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   const bool fused = !(fenv && fenv[0] == '0') && fgrid >= B + 8 && fused_fits(pp.k);
   if (info) info->fused = fused ? 1 : 0;
   ctx->last_fused = fused ? 1 : 0;
+  const int64_t nrdy = fused ? 2 * (int64_t)B * n : 0;  // ready flags + arrival counters
+
+  tabi_placement* d_out = on_device ? out : ctx->d_out;
+  const int64_t V_in = on_device ? 0 : (int64_t)chart_start[n];
   int wave = 0;
-  for (int attempt = 0; attempt < 64; attempt++) {
-    pp.col_cap = ctx->col_cap;
-    pp.row_cap = ctx->row_cap;
-    pp.wave = wave;
+  int reset_mode = 2;  // 2: fresh status; 0: next wave
+  // One wave's work, enqueued on s: [H2D + reset + proxies + sort] for the
+  // first wave, the candidate wave, select, [placements D2H], status D2H.
+  auto enqueue_wave = [&](bool prologue, int& nl) -> tabi_status {
+    if (prologue && !on_device)
+      CK(cudaMemcpyAsync(ctx->d_xy, ctx->h_xy, sizeof(float) * 2 * V_in + sizeof(int32_t) * (n + 1),
+                         cudaMemcpyHostToDevice, s));
+    launch_reset(ctx->d_status, reset_mode, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy,
+                 nrdy, s);
+    nl++;
+    if (prologue) {
+      launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, ctx->d_qx, ctx->d_qy, ctx->P,
+                     ctx->d_status, s);
+      nl++;
+      tm.mark(s);
+      nl += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
+      tm.mark(s);
+    }
     if (wave == 0) {
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
                   ctx->tix, ctx->d_status, s);
-      launches++;
-      CK(cudaMemsetAsync(ctx->cands, 0, sizeof(Cand) * M, s));
-      CK(cudaMemsetAsync(ctx->t_state, 0, sizeof(int32_t) * M, s));
+      nl++;
     }
-    CK(cudaMemsetAsync(ctx->cand_bad, 0, sizeof(int32_t) * M, s));
-    CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));  // large-chart list
     if (fused) {
-      // K3 + K3b + K4 as one cooperative persistent launch (DESIGN.md §5.6)
-      CK(cudaMemsetAsync(ctx->rdy, 0, sizeof(int32_t) * (size_t)B * n, s));
-      CK(cudaMemsetAsync(ctx->rdy + (size_t)B * n, 0, sizeof(int32_t) * (size_t)B * n, s));
-      CK(cudaMemsetAsync(&ctx->d_status->work_next, 0, sizeof(int32_t), s));
+      // K3 + K3b + K4 as one cooperative persistent launch (DESIGN.md §6)
       tm.mark(s);
       tm.mark(s);
       CK(launch_fused(fgrid, ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->dcol,
                       ctx->drow, ctx->wd, ctx->hd, ctx->off, ctx->lockbits, ctx->hsorted,
                       ctx->cand_bad, ctx->rdy, ctx->tstart, ctx->tix, ctx->scratch, ctx->pair_cap, ctx->X, ctx->Y,
                       ctx->mir, ctx->cands, ctx->d_status, s));
-      launches++;
+      nl++;
     } else {
       launch_profiles(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
                       (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
                       ctx->d_status, s);
-      launches += 2;  // K3 tiles, K3 large charts
+      nl += 2;  // K3 tiles, K3 large charts
       tm.mark(s);
       launch_offsets(pp, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
                      ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
-      launches++;
+      nl++;
       tm.mark(s);
       launch_pack(pp, ctx->colofs, ctx->rowofs, ctx->dcol, ctx->drow, ctx->wd, ctx->hd, ctx->off,
                   ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
                   ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
-      launches++;
+      nl++;
     }
     if (t_opt > 0) {
       // hybrid prefix tail for the candidates K4 switched: rows and
       // sigma, then up to 9 re-rasterize / re-lay rounds, then the prefix rows
       launch_tail_prepare(pp, ctx->perm, ctx->P.area2, ctx->wd, ctx->off, ctx->scratch,
                           ctx->pair_cap, ctx->cands, ctx->d_status, s);
-      launches++;
+      nl++;
       PackParams pt = pp;
       pt.tail = 1;
       for (int r = 0; r <= 8; r++) {
@@ -400,23 +441,72 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
         launch_offsets(pt, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
                        ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
         launch_tail_layout(pt, ctx->wd, ctx->off, ctx->scratch, ctx->pair_cap, ctx->d_status, s);
-        launches += 4;
+        nl += 4;
       }
       PackParams pm = pp;
       pm.mode = 1;
       launch_pack(pm, ctx->colofs, ctx->rowofs, ctx->dcol, ctx->drow, ctx->wd, ctx->hd, ctx->off,
                   ctx->lockbits, ctx->hsorted, ctx->cand_bad, ctx->scratch, ctx->pair_cap, ctx->X,
                   ctx->Y, ctx->mir, ctx->cands, ctx->d_status, s);
-      launches++;
+      nl++;
     }
     tm.mark(s);
     launch_select(pp, ctx->P, ctx->perm, ctx->wd, ctx->hd, ctx->X, ctx->Y, ctx->mir, ctx->cands,
                   d_out, ctx->d_status, s);
-    launches++;
+    nl++;
     tm.mark(s);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->h_cands, ctx->cands, sizeof(Cand) * M, cudaMemcpyDeviceToHost, s));
+    if (!on_device)  // placements (used only if this wave holds the winner)
+      CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(tabi_placement) * n, cudaMemcpyDeviceToHost,
+                         s));
+    // status + candidate records: one contiguous block, one copy
+    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, kStatusPad + sizeof(Cand) * M,
+                       cudaMemcpyDeviceToHost, s));
+    return TABI_OK;
+  };
+
+  // The first wave (the only one in the common case) runs as a CUDA graph,
+  // captured once per (pointers, sizes, spec, buffer generation) and relaunched
+  // with one call: no per-kernel launch overhead on the critical path.
+  const char* genv = getenv("TABI_GRAPH");
+  const bool use_graph = !tm.on && !(genv && genv[0] == '0');
+  for (int attempt = 0; attempt < 64; attempt++) {
+    pp.col_cap = ctx->col_cap;
+    pp.row_cap = ctx->row_cap;
+    pp.wave = wave;
+    const bool prologue = attempt == 0;
+    if (prologue && use_graph) {
+      char sort_env = 0;
+      for (const char* p = getenv("TABI_SORT"); p && *p; p++) sort_env = (char)(sort_env * 31 + *p);
+      GraphKey key{xy, chart_start, out, n, V_in, on_device, res_x, res_y, *spec, B,
+                   fused ? 1 : 0, ctx->alloc_gen, sort_env};
+      if (!ctx->gexec || !(key == ctx->gkey)) {
+        if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+        cudaGraph_t g = nullptr;
+        int nl = 0;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const tabi_status es = enqueue_wave(true, nl);
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (es != TABI_OK) {
+          if (g) cudaGraphDestroy(g);
+          return es;
+        }
+        CK(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+        ctx->gkey = key;
+        ctx->g_launches = nl;
+      }
+      CK(cudaGraphLaunch(ctx->gexec, s));
+      launches += ctx->g_launches;
+    } else {
+      int nl = 0;
+      const tabi_status es = enqueue_wave(prologue, nl);
+      if (es != TABI_OK) return es;
+      launches += nl;
+    }
     CK(cudaStreamSynchronize(s));
     const Status st = *ctx->h_status;
     if (st.bad_chart != INT32_MAX) {
@@ -438,6 +528,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
         if (Atot * next_m * ((i128)1 << 20) <= bestV) break;
       }
       wave++;
+      reset_mode = 0;
       continue;
     }
     wave = 0;
@@ -454,9 +545,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     }
     ts = ensure_candidates(ctx, M, cols, pairs);
     if (ts != TABI_OK) return ts;
-    Status again = init;
-    *ctx->h_status = again;
-    CK(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(Status), cudaMemcpyHostToDevice, s));
+    reset_mode = 2;  // fresh status (prep recomputes its fields), records, wave state
     tm.n = 3;  // re-time the retried stages
     if (attempt >= 8) return TABI_ECAPACITY;
   }
@@ -469,12 +558,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     if (info) info->gpu_launches = launches;
     return TABI_NO_FIT;
   }
-  if (!on_device) {
-    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(tabi_placement) * n, cudaMemcpyDeviceToHost, s));
-    tm.mark(s);
-    CK(cudaStreamSynchronize(s));
-    memcpy(out, ctx->h_out, sizeof(tabi_placement) * n);
-  }
+  if (!on_device) memcpy(out, ctx->h_out, sizeof(tabi_placement) * n);  // copied with the status
   tm.finish(info);
   if (info) {
     const Cand& c = ctx->h_cands[win - 1];

@@ -313,7 +313,8 @@ struct Status {       // device-side status block, copied back once per pack
   // group end, [2] last packer end, [3] packer ns spent waiting for tiles,
   // [4] raster ns spent waiting for the left tile, [5] tiles rasterized
   unsigned long long tr[6];
-  // K4 row-phase time (ns, thread 0 of every packer, summed): knee update,
+  // K4 row-phase time (SM cycles, thread 0 of every packer, summed; only in a
+  // -DTABI_PHASE_TRACE build): knee update,
   // fold, HC choice + lock pairs, push, Alg. 1, score, select + commit, FindKnee
   unsigned long long ph[10];  // + [8] push staging, [9] commit staging
 };
@@ -366,6 +367,9 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
 namespace tabi {
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
+// Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
+void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
+                  int32_t* rdy, int64_t nrdy, cudaStream_t s);
 // D9 sort: bitonic in smem (N <= 4096), rank sort (N <= 2^17), else radix.
 // Returns the number of kernels launched.
 int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
