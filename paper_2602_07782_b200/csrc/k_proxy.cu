@@ -32,10 +32,11 @@ struct WarpSlices {
 // [j*ext, (j+1)*ext].
 __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, int64_t ext, int k,
                                   int32_t* lo, int32_t* hi, int lane) {
+  const double rext = rcp_approx((double)ext);
   for (int v = lane; v < nv; v += 32) {
     int64_t ka = (int64_t)k * A[v];
-    int64_t jh = fdiv_fast(ka, ext);                // floor(k*a/ext), a >= 0
-    int64_t jl = cdiv_fast(ka, ext) - 1;     // ceil(k*a/ext) - 1
+    int64_t jh = fdiv_r64(ka, ext, rext);            // floor(k*a/ext), a >= 0
+    int64_t jl = -fdiv_r64(-ka, ext, rext) - 1;      // ceil(k*a/ext) - 1
     if (jl < 0) jl = 0;
     if (jh > k - 1) jh = k - 1;
     for (int64_t j = jl; j <= jh; j++) {
@@ -53,8 +54,8 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
       int64_t t = xa; xa = xb; xb = t;
       t = ya; ya = yb; yb = t;
     }
-    int64_t L0 = fdiv_fast((int64_t)k * xa, ext) + 1;      // first line strictly right of xa
-    int64_t L1 = cdiv_fast((int64_t)k * xb, ext) - 1;  // last line strictly left of xb
+    int64_t L0 = fdiv_r64((int64_t)k * xa, ext, rext) + 1;       // first line strictly right of xa
+    int64_t L1 = -fdiv_r64(-(int64_t)k * xb, ext, rext) - 1;     // last line strictly left of xb
     if (L0 < 1) L0 = 1;
     if (L1 > k - 1) L1 = k - 1;
     for (int64_t L = L0; L <= L1; L++) {
@@ -228,16 +229,40 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     BR2 = warp_sum64(BR2);
     fx = BL2 > BR2;
   }
-  // D8 final pose
+  // D8 final pose.  The slices of the reflected chart are the reflected
+  // slices: x -> w - x maps x-strip j to strip k-1-j (closed strips, the same
+  // crossings) and a floored left bound to w - (ceiled right bound); the merge
+  // commutes with both maps.  So the final-pose merged slices are an index
+  // mirror plus a value reflection of the ones just computed -- no second
+  // slicing pass (tests compare every slice with the oracle, which re-slices).
   if (fx || fy) {
     __syncwarp();
     for (int v = lane; v < nv; v += 32) {
       if (fx) X[v] = (int32_t)(w - X[v]);
       if (fy) Y[v] = (int32_t)(h - Y[v]);
     }
+    int32_t t0[2], b0[2], l1[2], r1[2];  // k <= 64: two slices per lane
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int j = lane + 32 * u;
+      if (j >= k) continue;
+      const int sx = fx ? k - 1 - j : j;  // x-slices are indexed along x
+      const int sy = fy ? k - 1 - j : j;  // y-slices along y
+      t0[u] = fy ? (int32_t)(h - S.mhi[0][sx]) : S.mlo[0][sx];
+      b0[u] = fy ? (int32_t)(h - S.mlo[0][sx]) : S.mhi[0][sx];
+      l1[u] = fx ? (int32_t)(w - S.mhi[1][sy]) : S.mlo[1][sy];
+      r1[u] = fx ? (int32_t)(w - S.mlo[1][sy]) : S.mhi[1][sy];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int j = lane + 32 * u;
+      if (j >= k) continue;
+      S.mlo[0][j] = t0[u]; S.mhi[0][j] = b0[u];
+      S.mlo[1][j] = l1[u]; S.mhi[1][j] = r1[u];
+    }
     __syncwarp();
   }
-  merged_slices(S, X, Y, nv, w, h, k, lane);
   int32_t* sl = P.sl + (int64_t)c * 4 * k;
   for (int j = lane; j < k; j += 32) {
     sl[j] = S.mlo[0][j];
