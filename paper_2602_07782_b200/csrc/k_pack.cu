@@ -144,7 +144,7 @@ __device__ __forceinline__ void walk(const Win& w, int nwin, Enter enter, Body b
   while (t < tend) {
     const int32_t j0 = t - (w.rx0[i] - base0);
     const int32_t j1 = min(w.rwd[i], j0 + (tend - t));
-    enter(i, j0);
+    enter(i, j0, j1);
     for (int32_t j = j0; j < j1; j++) body(i, j);
     leave(i);
     t += j1 - j0;
@@ -645,33 +645,68 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       __syncthreads();  // (index 4 of rY is rbot)
       phase_mark(8);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
-      int32_t X[4], mx[4], bm = INT32_MIN;
-      int nact = 0;
-      walk(
-          W, nwin,
-          [&](int i, int32_t) {
-            nact = (knee_ok && ws0 + i <= endK) ? 4 : 2;
-            for (int q = 0; q < 4; q++) { mx[q] = INT32_MIN; X[q] = q < nact ? cfgX(q, i) : 0; }
-            bm = INT32_MIN;
-          },
-          [&](int i, int32_t j) {
-            const uint32_t v = pr[W.rco[i] + j];
-            const int32_t top = lo16(v);
-            bm = max(bm, hi16(v));  // the score needs only max_j BottomEdge per chart
-            const int32_t Wd = W.rwd[i];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-              if (q < nact) {
-                const int32_t pos = (q & 1) ? X[q] + Wd - 1 - j : X[q] + j;
-                mx[q] = max(mx[q], F[pos] - top);
-              }
+      // flattened (chart, column) runs (see walk()); per chart segment the
+      // configurations' frontline pointers are set once and the column loop is
+      // specialised on 2 / 4 configurations (L->R reads F[X + j], R->L reads
+      // F[X + Wd - 1 - j])
+      {
+        const int32_t base0 = W.rx0[0];
+        const int32_t T = W.rx0[nwin - 1] - base0 + W.rwd[nwin - 1];
+        const int32_t C = ((T + kNT - 1) / kNT) | 1;
+        int32_t t = tid * C;
+        const int32_t tend = min(T, t + C);
+        int i = 0;
+        if (t < tend) {
+          int lo = 0, hi = nwin - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (W.rx0[mid] - base0 <= t) lo = mid;
+            else hi = mid - 1;
+          }
+          i = lo;
+        }
+        while (t < tend) {
+          const int32_t Wd = W.rwd[i];
+          const int32_t j0 = t - (W.rx0[i] - base0);
+          const int32_t j1 = min(Wd, j0 + (tend - t));
+          const uint32_t* pc = pr + W.rco[i];
+          const int32_t* f0 = F + cfgX(0, i);
+          const int32_t* f1 = F + cfgX(1, i) + Wd - 1;
+          int32_t m0 = INT32_MIN, m1 = INT32_MIN, m2 = INT32_MIN, m3 = INT32_MIN, bm = INT32_MIN;
+          const bool four = knee_ok && ws0 + i <= endK;
+          if (four) {
+            const int32_t* f2 = F + cfgX(2, i);
+            const int32_t* f3 = F + cfgX(3, i) + Wd - 1;
+            for (int32_t j = j0; j < j1; j++) {
+              const uint32_t v = pc[j];
+              const int32_t top = lo16(v);
+              bm = max(bm, hi16(v));  // the score needs only max_j BottomEdge per chart
+              m0 = max(m0, f0[j] - top);
+              m1 = max(m1, f1[-j] - top);
+              m2 = max(m2, f2[j] - top);
+              m3 = max(m3, f3[-j] - top);
             }
-            wk += nact;
-          },
-          [&](int i) {
-            for (int q = 0; q < nact; q++) atomicMax(&W.rY[q * kRW + i], mx[q]);
-            atomicMax(&W.rbot[i], bm);
-          });
+          } else {
+            for (int32_t j = j0; j < j1; j++) {
+              const uint32_t v = pc[j];
+              const int32_t top = lo16(v);
+              bm = max(bm, hi16(v));
+              m0 = max(m0, f0[j] - top);
+              m1 = max(m1, f1[-j] - top);
+            }
+          }
+          wk += (unsigned long long)((four ? 4 : 2) * (j1 - j0));
+          atomicMax(&W.rY[i], m0);
+          atomicMax(&W.rY[kRW + i], m1);
+          if (four) {
+            atomicMax(&W.rY[2 * kRW + i], m2);
+            atomicMax(&W.rY[3 * kRW + i], m3);
+          }
+          atomicMax(&W.rbot[i], bm);
+          t += j1 - j0;
+          i++;
+        }
+      }
       __syncthreads();
       if (one) continue;  // Y stays in shared memory for Alg. 1, score and commit
       for (int k = tid; k < nwin; k += kNT) {
@@ -775,7 +810,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         int nact = 0;
         walk(
             W, nwin,
-            [&](int i, int32_t) {
+            [&](int i, int32_t, int32_t) {
               nact = (knee_ok && ws0 + i <= endK) ? 4 : 2;
               for (int q = 0; q < 4; q++) Yv[q] = q < nact ? W.rY[q * kRW + i] : 0;
             },
@@ -841,27 +876,29 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       phase_mark(9);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
-      int32_t Xc = 0, Yv = 0, Wd = 0;
+      int32_t* const Fs = F;
       walk(
           W, nwin,
-          [&](int i, int32_t j0) {
-            Xc = cfgX(cfg, i);
-            Yv = rYc[i];
-            Wd = W.rwd[i];
+          [&](int i, int32_t j0, int32_t j1) {
+            const int32_t Xc = cfgX(cfg, i), Yv = rYc[i], Wd = W.rwd[i];
             if (j0 == 0) {
               const int s = ws0 + i;
               Xo[s] = Xc;
               Yo[s] = Yv;
               mir[s] = (uint8_t)dir;
             }
+            // the whole run of this chart at once: F <- max(F, Y + BottomEdge)
+            const uint32_t* pc = pr + W.rco[i];
+            if (dir) {
+              int32_t* fp = Fs + Xc + Wd - 1;
+              for (int32_t j = j0; j < j1; j++) atomicMax(fp - j, Yv + hi16(pc[j]));
+            } else {
+              int32_t* fp = Fs + Xc;
+              for (int32_t j = j0; j < j1; j++) atomicMax(fp + j, Yv + hi16(pc[j]));
+            }
+            wk += (unsigned long long)(j1 - j0);
           },
-          [&](int i, int32_t j) {
-            const int32_t bot = hi16(pr[W.rco[i] + j]);
-            const int32_t pos = dir ? Xc + Wd - 1 - j : Xc + j;
-            atomicMax(&F[pos], Yv + bot);
-            wk += 1;
-          },
-          [&](int) {});
+          [&](int, int32_t) {}, [&](int) {});
       __syncthreads();
     }
     phase_mark(6);
