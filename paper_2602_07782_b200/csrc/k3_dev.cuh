@@ -315,18 +315,36 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   int cb = 0;
   while (cb < nt && cells[cb] == 0) cb++;
   while (cb < nt) {
-    if (tid == 0) {  // chunk [cb, ce): raw cells fit the buffer
+    if (tid < 32) {  // warp 0 plans chunk [cb, ce): raw cells fit the buffer
+      // 32 charts per step: inclusive scans of raw cells and dilated outputs;
+      // "fits" is a prefix property (cells >= 0), so a ballot gives the count
+      const int lane = tid;
       int e = cb, tot = 0, otot = 0;
-      cpre[0] = 0;
-      opre[0] = 0;
-      while (e < nt && tot + cells[e] <= RAW) {
-        tot += cells[e];
-        otot += cells[e] ? cells[e] + 4 * g : 0;
-        e++;
-        cpre[e - cb] = tot;
-        opre[e - cb] = otot;
+      if (lane == 0) { cpre[0] = 0; opre[0] = 0; }
+      while (e < nt) {
+        const int idx = e + lane;
+        const int c = idx < nt ? cells[idx] : RAW + 1;  // past the tile: never fits
+        int ic = c, io = (idx < nt && c) ? c + 4 * g : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int a = __shfl_up_sync(0xffffffffu, ic, o);
+          const int b = __shfl_up_sync(0xffffffffu, io, o);
+          if (lane >= o) { ic += a; io += b; }
+        }
+        const unsigned fit = __ballot_sync(0xffffffffu, tot + ic <= RAW);
+        const int nf = fit == 0xffffffffu ? 32 : __ffs(~fit) - 1;
+        if (lane < nf) {
+          cpre[e - cb + lane + 1] = tot + ic;
+          opre[e - cb + lane + 1] = otot + io;
+        }
+        if (nf > 0) {
+          tot += __shfl_sync(0xffffffffu, ic, nf - 1);
+          otot += __shfl_sync(0xffffffffu, io, nf - 1);
+        }
+        e += nf;
+        if (nf < 32) break;
       }
-      *chunk_end = e;
+      if (lane == 0) *chunk_end = e;
     }
     sync();
     const int ce = *chunk_end, nc = ce - cb;

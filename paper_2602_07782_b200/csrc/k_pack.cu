@@ -1062,6 +1062,8 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   const int NB = T * pp.B;
   const int64_t SCm = (int64_t)pp.M * TABI_UNITS;
   while (true) {
+    // (fetching the next item ahead would hide this round trip, but lets a
+    // busy CTA sit on an early tile the packers are waiting for)
     if (gt == 0) misc[0] = atomicAdd(&st->work_next, 1);
     gsync();
     const int it = misc[0];
@@ -1082,11 +1084,10 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       if (big[ci])
         k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m, s0 + ci, sc, CW[wid],
                       wtab + wid * 4 * k, lane);
-    if (gt < 32) {  // work accounting: footprint entries of the tile
+    if (gt < 32) {  // work accounting: footprint entries of the tile (from smem)
       unsigned long long pe = 0;
-      if (gt < nt)
-        pe = (unsigned long long)(ra.wd[(int64_t)(m - 1) * pp.n + s0 + gt] +
-                                  ra.hd[(int64_t)(m - 1) * pp.n + s0 + gt]);
+      for (int ci = gt; ci < nt; ci += 32)
+        pe += (unsigned long long)(CH[ci].ws + CH[ci].hs + 4 * pp.g);
       for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
       if (gt == 0) atomicAdd(&st->work_prof, pe);
     }
@@ -1099,10 +1100,13 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     // the last tile adds its own zero entry instead).
     int32_t* fl = ra.rdy + (int64_t)j * T;
     int32_t* arr = ra.rdy + (int64_t)pp.B * pp.n + (int64_t)j * T;  // boundary t | t+1
-    if (gt == 0) {
-      atomicAdd(&st->tr[5], 1ull);
-      misc[2] = t > 0 && atom_add_acq_rel(arr + t - 1, 1) == 1;      // left boundary is ours
-      misc[3] = t < T - 1 && atom_add_acq_rel(arr + t, 1) == 1;      // right boundary is ours
+    if (gt < 2) {  // both arrivals in one instruction: lane 0 left, lane 1 right boundary
+      const bool has = gt == 0 ? t > 0 : t < T - 1;
+      int32_t* a = arr + t - 1 + gt;
+      int ours = 0;
+      if (has) ours = atom_add_acq_rel(a, 1) == 1;  // second to arrive computes the pair
+      misc[2 + gt] = ours;
+      if (gt == 0) atomicAdd(&st->tr[5], 1ull);
     }
     gsync();
     const bool needL = misc[2] != 0, needR = misc[3] != 0;
