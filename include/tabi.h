@@ -187,6 +187,11 @@ tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* 
  * of which commit staging.  [6..15] are 0 unless the library was built with
  * -DTABI_PHASE_TRACE. */
 tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16);
+/* Fused rasterizer per-item phase SM cycles of the last wave, summed over
+ * raster groups (0 unless built with -DTABI_PHASE_TRACE): queue fetch,
+ * footprints, large charts + accounting, boundary arrivals, pair offsets,
+ * publish, 0, 0. */
+tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out8);
 
 #ifdef __cplusplus
 }

@@ -265,14 +265,18 @@ struct Scale {
 // TT threads (8 per chart during setup).  Charts that fit the dilated atlas but
 // have more than kRaw raw cells are left for a warp-per-chart pass: their tile
 // index is flagged in big[ci].  Writes wd/hd, the footprint slots, cand_bad.
-template <int TC, int TT, int RAW, class Sync>
+struct NoMark {
+  __device__ void operator()() const {}
+};
+
+template <int TC, int TT, int RAW, class Sync, class Mark = NoMark>
 __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, const PackParams& pp,
                             const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
                             uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all,
                             int32_t* cand_bad, int m, int s0, Scale sc, ChartK3* CH,
                             int32_t* cells, int32_t* cpre, int32_t* opre, int32_t* chunk_end,
                             int32_t* big, int32_t* tabs, uint32_t* raw, int nt, int tid,
-                            Sync sync) {
+                            Sync sync, Mark setup_done = Mark()) {
   const int k = pp.k, g = pp.g;  // tile = sorted positions [s0, s0 + nt), nt <= TC
   const int64_t num = sc.num, SC = sc.SC;
   const double rSC = rcp_approx((double)SC);
@@ -310,6 +314,7 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   sync();
   if (ci < nt && CH[ci].small) chart_setup(CH[ci], tabs + ci * 4 * k, P, k, num, SC, r);
   sync();
+  setup_done();
   uint32_t* colb = dcol + (int64_t)(m - 1) * pp.col_cap;
   uint32_t* rowb = drow + (int64_t)(m - 1) * pp.row_cap;
   int cb = 0;

@@ -54,6 +54,7 @@ struct Smem {
   int32_t pf_out, pf_a0, pf_a1;  // row-top footprint prefetch (words [pf_a0, pf_a1))
   int32_t fold_hi, next_a0;      // fold's scanned end; colofs of the next row start (or -1)
   int32_t changed3[3];           // Alg. 1 rotating change flags
+  int32_t abort;                 // sequential fused mode: a higher candidate won
   int32_t prefix_rows, switched;
   unsigned long long knee_key;
   unsigned long long work;
@@ -197,15 +198,23 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   // wait until every sorted position <= s_hi has its footprints, width/height
   // and the offset of the pair (s, s+1) published (fused mode only)
   if (tid == 0) ready_upto = -1;
+  // sequential mode: a higher candidate already succeeded, so this one cannot
+  // win -- its remaining tiles may never be rasterized; stop
+  auto beaten = [&]() -> bool {
+    return pp.early && *(volatile int32_t*)&st->win_j < jslot;
+  };
   auto wait_upto = [&](int s_hi) {
     if (!rd.flags) return;
     const int t_req = rd.tix[min(s_hi + 1, n - 1)];
     if (tid == 0 && ready_upto < t_req) {
       int32_t* fl = rd.flags + (int64_t)jslot * rd.T;
       const unsigned long long t0 = gtime();
-      while (ready_upto < t_req) {
-        while (ld_acquire(fl + ready_upto + 1) < 2) __nanosleep(64);
-        ready_upto++;
+      while (ready_upto < t_req && !S.abort) {
+        while (ld_acquire(fl + ready_upto + 1) < 2) {
+          if (beaten()) { S.abort = 1; break; }
+          __nanosleep(64);
+        }
+        if (!S.abort) ready_upto++;
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
       atomicAdd(&st->tr[3], gtime() - t0);
@@ -223,9 +232,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   __shared__ int32_t ready_lim;
   if (tid == 0) ready_lim = -1;
   auto wait_ready = [&](int s) -> int {
-    if (!rd.flags) return n - 1;
+    if (!rd.flags || ready_upto == rd.T - 1) return n - 1;  // (no tile-index loads)
     const int t_need = rd.tix[min(s + 1, n - 1)];
-    const int t_cap = max(t_need, rd.tix[min(s + kNT, n - 1)]);
+    // probe as far as the published prefix reaches (32 flags per step): once
+    // every tile is in, later calls take the fast path above
+    const int t_cap = rd.T - 1;
     // enough is known ready: no probe (a probe's fence also empties the L1
     // that keeps the row's scalars warm between rows)
     if (ready_upto >= rd.tix[min(s + 64, n - 1)]) return ready_lim;
@@ -246,7 +257,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         up += adv;
         if (up >= t_need && adv < 32) break;
         if (up >= t_cap || up + 1 >= rd.T) break;
-        if (adv == 0) __nanosleep(64);
+        if (adv == 0) {
+          if (__shfl_sync(0xffffffffu, beaten() ? 1 : 0, 0)) break;  // uniform: lane 0 decides
+          __nanosleep(64);
+        }
       }
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       if (lane == 0) {
@@ -254,6 +268,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
         ready_upto = up;
         ready_lim = up == rd.T - 1 ? n - 1 : rd.tstart[up + 1] - 2;
+        if (up < t_need) { S.abort = 1; ready_lim = -2; }  // beaten while waiting
       }
     }
     __syncthreads();
@@ -312,7 +327,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   for (int x = tid; x < Wp; x += kNT) F[x] = prefix_mode ? fsave[x] : 0;  // top
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
-    S.next_a0 = 0; S.fold_hi = 0; S.pf_out = 0;
+    S.next_a0 = 0; S.fold_hi = 0; S.pf_out = 0; S.abort = 0;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
     S.prefix_rows = 0;
@@ -350,6 +365,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   // from the row start up to a cap; the first stage() of the row consumes it
   // if its window lies inside (else drains it and copies the exact window).
   bool pf_pending = false;  // uniform: a prefetch copy is in flight
+  int32_t wj = INT32_MAX;   // thread 0: last seen st->win_j
   auto stage = [&](int ws0, int we) {
     if (S.win_s0 == ws0 && S.win_e == we) return;
     const int nwin = we - ws0;
@@ -391,7 +407,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
 
   while (true) {
     const int32_t rs = S.row_start;
-    if (rs >= n || S.fail) break;
+    if (rs >= n || S.fail || S.abort) break;
     // ---- D23 switch to prefix folding ("when no more knees are
     // detected and the height of the tallest chart in the row decreases below
     // a threshold t_opt"), checked before each row, latched: save the state,
@@ -420,6 +436,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         break;
       }
     }
+    // sequential fused mode: has a higher candidate won?  Loaded here, used at
+    // the row end, so the load's latency hides behind the row
+    if (tid == 0 && rd.flags && pp.early) wj = *(volatile int32_t*)&st->win_j;
     // ---- footprint prefetch for this row (consumed by the push's stage) ----
     // (no global loads on thread 0's path: the row start's slot offset was
     // kept from the previous row's fold; in fused mode only once every tile
@@ -502,7 +521,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     } else {
       int32_t carry0 = 0, carry1 = 0;
       for (int base = rs;;) {
-        const int cnt = min(kNT, wait_ready(base) - base + 1);  // positions [base, base + cnt)
+        const int lim = wait_ready(base);
+        if (lim == -2) break;  // beaten (S.abort): leave the row loop below
+        const int cnt = min(kNT, lim - base + 1);  // positions [base, base + cnt)
         if (tid < 4) S.fmin[tid] = INT32_MAX;
         const int s = base + tid;
         const bool valid = tid < cnt;
@@ -546,6 +567,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         base += cnt;
       }
     }  // !prefix_mode
+    if (S.abort) break;  // beaten while waiting for tiles (set before a barrier)
     phase_mark(1);
     // ---- level 1 of the hierarchical choice: HC iff it fits more --
     if (tid == 0) {
@@ -920,6 +942,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       }
       if (S.fmax > Hp) S.fail = 1;  // overflow below the atlas bottom
       S.row_start = endS + 1;
+      if (rd.flags && pp.early && wj < jslot) S.abort = 1;  // checked at the next row start
       const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
       S.next_a0 = (!prefix_mode && nx < n && nx < S.fold_hi && nx - rs < kRW) ? W.rco[nx - rs] : -1;
     }
@@ -935,17 +958,20 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
   if (lane == 0) atomicAdd(&st->work_pack, wk);
   if (rd.flags && tid == 0) atomicMax(&st->tr[2], gtime());
-  if (rd.flags && S.fail) {
+  if (rd.flags && S.fail && !S.abort) {
     // fused mode: report a chart that exceeds the dilated atlas the way the
     // split path does (the whole candidate's footprints must be in first)
     wait_upto(n - 1);
-    if (tid == 0 && __ldcg(cand_bad + m - 1)) {
+    if (tid == 0 && !S.abort && __ldcg(cand_bad + m - 1)) {
       cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
       return;
     }
   }
-  if (tid == 0 && !S.switched) {
+  // a beaten candidate stays "not evaluated" (its record keeps the reset zeros)
+  if (tid == 0 && !S.switched && !S.abort) {
     Cand cd{S.fail ? 0 : 1, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1, -1, 0, 0ull, 0ull};
+    // sequential fused mode: announce the success so lower candidates stop
+    if (!S.fail && rd.flags && pp.early) atomicMin(&st->win_j, jslot);
     if (prefix_mode) {  // keep the tail's area (written by the layout kernel)
       const Cand prev = cands[m - 1];
       cd.prefix_rows = S.prefix_rows;
@@ -1017,7 +1043,7 @@ __host__ __device__ __forceinline__ size_t r16(size_t b) { return (b + 15) & ~(s
 // per-group carve of the dynamic shared memory
 __host__ __device__ __forceinline__ size_t group_bytes(int k) {
   return r16(sizeof(k3::ChartK3) * kTCF) + r16(4 * kTCF) + 2 * r16(4 * (kTCF + 1)) +
-         r16(4 * kTCF) + r16(16) + r16((size_t)4 * kTCF * 4 * k) + r16(4 * (size_t)kRawF);
+         r16(4 * kTCF) + r16(32) + r16((size_t)4 * kTCF * 4 * k) + r16(4 * (size_t)kRawF);
 }
 
 __device__ __forceinline__ unsigned char* carve(unsigned char*& p, size_t bytes) {
@@ -1052,7 +1078,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   int32_t* cpre = (int32_t*)carve(p, 4 * (kTCF + 1));
   int32_t* opre = (int32_t*)carve(p, 4 * (kTCF + 1));
   int32_t* big = (int32_t*)carve(p, 4 * kTCF);
-  int32_t* misc = (int32_t*)carve(p, 16);
+  int32_t* misc = (int32_t*)carve(p, 32);
   int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kTCF * 4 * k);
   uint32_t* raw = (uint32_t*)carve(p, 4 * (size_t)kRawF);
   p = dsm + group_bytes(k) * kRG;  // per-warp large-chart state
@@ -1061,25 +1087,69 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   const int32_t m_hi = st->pad[2];
   const int NB = T * pp.B;
   const int64_t SCm = (int64_t)pp.M * TABI_UNITS;
+#ifdef TABI_PHASE_TRACE
+  unsigned long long rph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long rt = clock64();
+  auto rmark = [&](int i) {
+    if (gt == 0) {
+      const long long t1 = clock64();
+      rph[i] += (unsigned long long)(t1 - rt);
+      rt = t1;
+    }
+  };
+#else
+  auto rmark = [](int) {};
+#endif
   while (true) {
     // (fetching the next item ahead would hide this round trip, but lets a
     // busy CTA sit on an early tile the packers are waiting for)
-    if (gt == 0) misc[0] = atomicAdd(&st->work_next, 1);
+    if (gt == 0) {
+      const int it0 = atomicAdd(&st->work_next, 1);
+      misc[0] = it0;
+      // sequential mode: drop items of candidates below a successful one
+      // (decided once, by the leader, so the group branches uniformly)
+      const int j0 = !pp.early || pp.B == 1 ? it0 % pp.B
+                     : it0 < T ? 0 : 1 + (it0 - T) % (pp.B - 1);  // item -> slot, as below
+      misc[4] = pp.early && *(volatile int32_t*)&st->win_j < j0;
+    }
     gsync();
     const int it = misc[0];
+    const bool dropped = misc[4] != 0;
     gsync();
+    rmark(0);
     if (it >= NB) {
       if (gt == 0) atomicMax(&st->tr[1], gtime());
+#ifdef TABI_PHASE_TRACE
+      if (gt == 0)
+        for (int i = 0; i < 8; i++) atomicAdd(&st->rph[i], rph[i]);
+#endif
       break;
     }
-    const int t = it / pp.B, j = it % pp.B;
+    // sequential mode: the highest candidate's tiles first (it wins whenever
+    // it succeeds), then the other candidates tile-major; items of a candidate
+    // below a successful one are dropped (its packer exits too).  Hybrid mode:
+    // tile-major for all.
+    int t, j;
+    if (!pp.early || pp.B == 1) {
+      t = it / pp.B;
+      j = it % pp.B;
+    } else if (it < T) {
+      t = it;
+      j = 0;
+    } else {
+      t = (it - T) / (pp.B - 1);
+      j = 1 + (it - T) % (pp.B - 1);
+    }
+    if (dropped) continue;
     const int m = wave_m(pp, m_hi, j);
     if (m == 0) continue;
     const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
     const k3::Scale sc{m, SCm, 0};
     k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
                                        ra.hd, ra.cand_bad, m, s0, sc, CH, cells, cpre, opre,
-                                       &misc[1], big, tabs, raw, nt, gt, gsync);
+                                       &misc[1], big, tabs, raw, nt, gt, gsync,
+                                       [&]() { rmark(6); });
+    rmark(1);
     for (int ci = gw; ci < nt; ci += kRGW)
       if (big[ci])
         k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m, s0 + ci, sc, CW[wid],
@@ -1092,6 +1162,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       if (gt == 0) atomicAdd(&st->work_prof, pe);
     }
     gsync();
+    rmark(2);
     // Adjacent pairs: the tile's internal pairs here; a boundary pair with a
     // neighbour tile is done by whichever of the two tiles publishes its
     // footprints second (arrival counter per boundary, acq_rel), so no tile
@@ -1109,16 +1180,19 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       if (gt == 0) atomicAdd(&st->tr[5], 1ull);
     }
     gsync();
+    rmark(3);
     const bool needL = misc[2] != 0, needR = misc[3] != 0;
     const int lo = needL ? s0 - 1 : s0;
     const int hi = (t == T - 1) ? pp.n - 1 : (needR ? s0 + nt - 1 : s0 + nt - 2);
     for (int s = lo + gw; s <= hi; s += kRGW)
       k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
     gsync();
+    rmark(4);
     if (gt == 0) {
       red_add_release(fl + t, (t == T - 1 || needR) ? 2 : 1);
       if (needL) red_add_release(fl + t - 1, 1);
     }
+    rmark(5);
   }
 }
 

@@ -307,9 +307,11 @@ __global__ void reset_kernel(Status* st, int mode, Cand* cands, int32_t* t_state
       for (size_t i = 0; i < sizeof(Status) / 4; i++) w[i] = 0;
       st->bad_chart = INT32_MAX;
       st->tr[0] = ~0ull;
+      st->win_j = INT32_MAX;
     } else {
       st->pad[1] = 0;
       st->work_next = 0;
+      st->win_j = INT32_MAX;
     }
   }
   if (mode >= 1) {

@@ -351,6 +351,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   pp.t_opt = t_opt;
   pp.mode = 0;
   pp.tail = 0;
+  pp.early = t_opt == 0 ? 1 : 0;  // sequential: the smallest successful slot wins outright
   pp.T.state = ctx->t_state;
   pp.T.r0 = ctx->t_r0;
   pp.T.p = ctx->t_p;
@@ -736,6 +737,12 @@ extern "C" tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16) {
   out16[4] = (int64_t)st.tr[5];
   out16[5] = ctx->last_fused;
   for (int i = 0; i < 10; i++) out16[6 + i] = (int64_t)st.ph[i];
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out8) {
+  if (!ctx || !out8 || ctx->last_n < 1) return TABI_EINVAL;
+  for (int i = 0; i < 8; i++) out8[i] = (int64_t)ctx->h_status->rph[i];
   return TABI_OK;
 }
 

@@ -296,7 +296,10 @@ struct Proxies {
 #endif
 constexpr int kFusedGroups = TABI_FUSED_RG;  // independent raster groups per CTA
 constexpr int kFusedTileCharts = 64 / kFusedGroups;
-constexpr int kFusedTileCells = 8192 / kFusedGroups;
+#ifndef TABI_TILE_CELLS
+#define TABI_TILE_CELLS 4096
+#endif
+constexpr int kFusedTileCells = TABI_TILE_CELLS / kFusedGroups;
 
 struct Status {       // device-side status block, copied back once per pack
   int32_t bad_chart;  // INT32_MAX if none
@@ -306,6 +309,8 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t pad[3];
   int32_t work_next;  // fused kernel: raster work-queue head
   int32_t ntiles;     // fused kernel: raster tiles (prep_kernel)
+  int32_t win_j;      // fused, sequential mode: smallest wave slot that succeeded
+  int32_t pad3;
   unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
   unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
   unsigned long long atot_lo, atot_hi;  // total 2 x area (int128) for D25 / D26
@@ -317,6 +322,10 @@ struct Status {       // device-side status block, copied back once per pack
   // -DTABI_PHASE_TRACE build): knee update,
   // fold, HC choice + lock pairs, push, Alg. 1, score, select + commit, FindKnee
   unsigned long long ph[10];  // + [8] push staging, [9] commit staging
+  // fused rasterizer per-item phases (SM cycles, summed; trace build only):
+  // queue fetch, footprints (tile_raster), large charts, accounting,
+  // boundary arrivals, pair offsets, publish
+  unsigned long long rph[8];
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -350,6 +359,8 @@ struct PackParams {
   int32_t t_opt;              // effective t_opt (basis points of H), 0 = sequential only
   int32_t mode;               // K4: 0 sequential rows (may switch), 1 prefix rows
   int32_t tail;               // K3 / K3b: 1 = rasterize tail charts at p / 2^20
+  int32_t early;              // fused, sequential mode: candidate-major raster order and
+                              // early exit once a higher candidate has succeeded
   int64_t col_cap, row_cap;   // per-candidate footprint slot capacity (entries)
   TailBufs T;
 };

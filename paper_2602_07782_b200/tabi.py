@@ -88,6 +88,7 @@ def lib():
         L.tabi_debug_profile.argtypes = [P, i32, i32, P, P, P, P, P]
         L.tabi_debug_offsets.argtypes = [P, i32, P, P]
         L.tabi_debug_trace.argtypes = [P, P]
+        L.tabi_debug_trace_raster.argtypes = [P, P]
         L.tabi_shard_plan.argtypes = [i32, P, i32, P]
         L.tabi_pack_batch.argtypes = [P, i32, i32, P, P, P, P, P, P, P]
         _lib = L
@@ -96,8 +97,8 @@ def lib():
 
 EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
-           "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace", "tabi_shard_plan",
-           "tabi_pack_batch"]
+           "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace",
+           "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch"]
 
 
 def shard_plan(n_charts, n_gpus: int) -> np.ndarray:
@@ -244,6 +245,10 @@ class Context:
         self._chk(lib().tabi_debug_trace(self.h, _ptr(out)))
         keys = ("raster_end", "pack_end", "pack_wait", "raster_wait", "tiles", "fused")
         d = dict(zip(keys, (int(v) for v in out[:6])))
+        r8 = np.zeros(8, dtype=np.int64)
+        self._chk(lib().tabi_debug_trace_raster(self.h, _ptr(r8)))
+        d["raster_phases"] = dict(zip(("fetch", "cells", "big_acct", "arrivals", "pairs",
+                                       "publish", "setup"), (int(v) for v in r8[:7])))
         d["phases"] = dict(zip(("knee", "fold", "hc_locks", "push", "alg1", "score", "commit",
                                 "findknee", "push_stage", "commit_stage"),
                                (int(v) for v in out[6:16])))

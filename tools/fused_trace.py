@@ -29,9 +29,12 @@ for name, cs in (("C3", chartgen.config3(0, rho=0.5)), ("C2", chartgen.config2(0
         ev = cands["evaluated"] != 0
         rows = int(cands["rows"][ev].sum())
         ph = tr.pop("phases")
+        rp = tr.pop("raster_phases")
+        tiles = max(tr.get("tiles", 0), 1)
         print(name, "fused" if f == "1" else "split", "m", info.scale_index,
               "stages_us", [round(x * 1000) for x in info.stage_ms[:7]],
               {k: (us(v) if k in ("raster_end", "pack_end", "pack_wait", "raster_wait") else v)
                for k, v in tr.items()},
               "rows", rows, "ns/row", {k: round(v / MHZ * 1000 / max(rows, 1)) for k, v in ph.items()},
+              "raster ns/tile", {k: round(v / MHZ * 1000 / tiles) for k, v in rp.items()},
               flush=True)
