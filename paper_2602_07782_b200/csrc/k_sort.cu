@@ -174,6 +174,62 @@ bitonic_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, i
   for (int i = threadIdx.x; i < n; i += kT) perm[i] = (int32_t)(key[i] & 0xfffu);
 }
 
+// N <= 2048: the same bitonic network with each thread holding elements 2t
+// and 2t + 1 in registers: the compare-exchange stages of element distance
+// <= 32 are warp shuffles (partner thread t ^ (stride / 2), same slot) with no
+// barrier; only distances >= 64 go through shared memory.
+__global__ void __launch_bounds__(kT, 1)
+bitonic_reg_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n,
+                   int32_t* perm, const Status* st) {
+  __shared__ uint64_t key[2 * kT];
+  if (st->bad_chart != INT32_MAX) return;
+  const int t = threadIdx.x;
+  uint64_t v[2];
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const int i = 2 * t + s;
+    v[s] = i < n ? (order_key(hh[i], ww[i]) << 12) | (uint64_t)i : ~0ull;
+  }
+  int P = 2;
+  while (P < n) P <<= 1;  // sorting [0, P) suffices: the rest are sentinels
+  for (int size = 2; size <= P; size <<= 1) {
+    int stride = size >> 1;
+    if (stride >= 64) {
+      key[2 * t] = v[0];
+      key[2 * t + 1] = v[1];
+      __syncthreads();
+      for (; stride >= 64; stride >>= 1) {
+        const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const uint64_t a = key[lo], b = key[hi];
+        if ((a > b) == ((lo & size) == 0)) { key[lo] = b; key[hi] = a; }
+        __syncthreads();
+      }
+      v[0] = key[2 * t];
+      v[1] = key[2 * t + 1];
+    }
+    const bool asc = ((2 * t) & size) == 0;
+    for (; stride >= 2; stride >>= 1) {
+      const int d = stride >> 1;
+      const bool keep_min = (((2 * t) & stride) == 0) == asc;
+#pragma unroll
+      for (int s = 0; s < 2; s++) {
+        const uint64_t p = __shfl_xor_sync(0xffffffffu, v[s], d);
+        v[s] = keep_min ? (p < v[s] ? p : v[s]) : (p > v[s] ? p : v[s]);
+      }
+    }
+    if ((v[0] > v[1]) == asc) {  // stride 1: the thread's own pair
+      const uint64_t x = v[0];
+      v[0] = v[1];
+      v[1] = x;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const int i = 2 * t + s;
+    if (i < n) perm[i] = (int32_t)(v[s] & 0xfffu);
+  }
+}
+
 // N <= 2^17: rank of key i = #{j : (key_j, j) < (key_i, i)}, counted over a 2-D
 // grid of (i block, j tile) with one atomicAdd per thread and tile, then a
 // scatter perm[rank[i]] = i.
@@ -339,6 +395,10 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
   const char* force = getenv("TABI_SORT");
   const bool want_rank = force && strcmp(force, "rank") == 0;
   const bool want_radix = force && strcmp(force, "radix") == 0;
+  if (n <= 2 * kT && !want_rank && !want_radix && !(force && strcmp(force, "bitonic") == 0)) {
+    bitonic_reg_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, perm, st);
+    return 1;
+  }
   if (n <= kBitonicMax && !want_rank && !want_radix) {
     bitonic_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, perm, st);
     return 1;

@@ -277,14 +277,18 @@ def test_pack_batch_equals_single_packs(ctx):
     c3.close()
 
 
-@pytest.mark.parametrize("path", ["bitonic", "rank", "radix"])
+@pytest.mark.parametrize("path", ["default", "bitonic", "rank", "radix"])
 def test_sort_paths_with_ties(orc, ctx, path, monkeypatch):
-    """D9 order (h desc, w desc, index asc) through each of the three sort paths
-    (TABI_SORT forces one), on inputs full of exact (h, w) ties: index order
-    must decide them."""
+    """D9 order (h desc, w desc, index asc) through each sort path (default:
+    the register bitonic network for N <= 2048; TABI_SORT forces the smem
+    bitonic, rank or radix path), on inputs full of exact (h, w) ties: index
+    order must decide them."""
     import oracle
     from paper_2602_07782_b200 import spec_of
-    monkeypatch.setenv("TABI_SORT", path)
+    if path == "default":
+        monkeypatch.delenv("TABI_SORT", raising=False)
+    else:
+        monkeypatch.setenv("TABI_SORT", path)
     rng = np.random.default_rng(5)
     polys = []
     for i in range(900):
