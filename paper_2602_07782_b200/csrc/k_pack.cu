@@ -238,8 +238,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // every tile is in, later calls take the fast path above
     const int t_cap = rd.T - 1;
     // enough is known ready: no probe (a probe's fence also empties the L1
-    // that keeps the row's scalars warm between rows)
-    if (ready_upto >= rd.tix[min(s + 64, n - 1)]) return ready_lim;
+    // that keeps the row's scalars warm between rows) -- except every 4th row,
+    // so the known-ready prefix catches up with the raster and reaches the
+    // all-ready fast path (which also enables the row-top prefetch)
+    if (ready_upto >= rd.tix[min(s + 64, n - 1)] && (S.rows & 3) != 0) return ready_lim;
     if (wid == 0) {
       const int32_t* fl = rd.flags + (int64_t)jslot * rd.T;
       int up = ready_upto;
@@ -445,7 +447,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // is published)
     if (!prefix_mode && tid == 0) {
       S.pf_out = 0;
+#ifdef TABI_NO_PREFETCH
+      const bool all = false;  // experiment: measure the row without the prefetch
+#else
       const bool all = !rd.flags || ready_lim == n - 1;
+#endif
       if (all && S.next_a0 >= 0) {
         const int32_t a0 = S.next_a0 & ~3;
         const int32_t a1 = min((cols_total + 3) & ~3, a0 + min(W.prof_cap, 4 * f_words));

@@ -316,9 +316,14 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
     // charts holding about kFusedTileCells footprint cells (the tallest
     // charts come first and get small tiles, so their tiles are not the long
     // pole every packer waits on).
-    const int32_t id = s < pp.n ? (int32_t)(((int64_t)carry_c + ec + carry_r + er) / kFusedTileCells +
-                                            s / kFusedTileCharts)
-                                : INT32_MAX;
+    // the first kFusedHeadCells cells (the tallest charts, which every packer
+    // needs first) are cut into quarter-size tiles so the first rows start early
+    const int64_t cum = (int64_t)carry_c + ec + carry_r + er;
+    const int64_t q4 = kFusedTileCells / 4;
+    const int64_t cell_key = cum < kFusedHeadCells
+                                 ? cum / q4
+                                 : kFusedHeadCells / q4 + (cum - kFusedHeadCells) / kFusedTileCells;
+    const int32_t id = s < pp.n ? (int32_t)(cell_key + s / kFusedTileCharts) : INT32_MAX;
     idl[threadIdx.x] = id;
     __syncthreads();
     const int32_t idp = threadIdx.x == 0 ? prev_id : idl[threadIdx.x - 1];

@@ -300,6 +300,10 @@ constexpr int kFusedTileCharts = 64 / kFusedGroups;
 #define TABI_TILE_CELLS 4096
 #endif
 constexpr int kFusedTileCells = TABI_TILE_CELLS / kFusedGroups;
+#ifndef TABI_HEAD_CELLS
+#define TABI_HEAD_CELLS 0  // measured: quarter-size head tiles do not shorten the first wait
+#endif
+constexpr int kFusedHeadCells = TABI_HEAD_CELLS;  // quarter-size tiles below this prefix
 
 struct Status {       // device-side status block, copied back once per pack
   int32_t bad_chart;  // INT32_MAX if none
