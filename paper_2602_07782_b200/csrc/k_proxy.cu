@@ -1,39 +1,90 @@
-// k_proxy.cu -- K1: per-chart proxies, one warp per chart.
+// k_proxy.cu -- K1: per-chart proxies, one lane group (8, 16 or 32 lanes) per
+// chart.
 //
 // Computes, for every chart ("compute the AABBs of all charts, rotate the
 // boxes to be taller than they are wide ... two parallel passes which compute
 // our shape approximations for each chart and determine each chart's
 // orientation"):
 //   snap to 1/256 texel -> AABB -> 90-degree normalization -> local AABBs
-//    + merge -> orientation -> final pose ->
-//   local AABBs again -> approximate OBB over 8 angles.
+//    + merge -> orientation -> final pose (the
+//   slices reflected, D8) -> approximate OBB over 8 angles.
 // Lanes stride over vertices / edges; slice bounds are accumulated with
 // shared-memory atomicMin/Max (commutative, so schedule-independent), merges
-// and reductions use warp shuffles.  Output: proxy SoA in HBM.
+// and reductions use shuffles within the group.  The group size trades
+// per-chart latency (wide groups, few charts) against charts in flight (narrow
+// groups, many small charts): 32 lanes below 4096 charts (a pack of a few
+// thousand charts is latency-bound per chart), 16 below 8192, else 8.
+// Output: proxy SoA in HBM.
+#include <cstdlib>
+
 #include "tabi_internal.cuh"
 
 namespace tabi {
 namespace {
 
-constexpr int kWarps = 8;  // warps (charts) per block
+constexpr int kBlock = 256;  // threads per block
 
-struct WarpSlices {
-  int32_t lo[2][TABI_KMAX];  // unmerged: [0] x-slices top, [1] y-slices left
-  int32_t hi[2][TABI_KMAX];  //           [0] x-slices bot, [1] y-slices right
-  int32_t mlo[2][TABI_KMAX]; // merged
-  int32_t mhi[2][TABI_KMAX];
-  int64_t fl[2][TABI_KMAX];  // floor(i * ext / k) for the other axis' slice edges
-  int64_t cl[2][TABI_KMAX];  // ceil((i + 1) * ext / k)
-  int64_t ob[8][4];          // OBB extents per angle: Umin, Umax, Vmin, Vmax
+// Per-group shared scratch, k slices per axis (sized by k at launch).
+struct Slices {
+  int32_t *lo0, *lo1, *hi0, *hi1;      // unmerged: x-slices top/bot, y-slices left/right
+  int32_t *mlo0, *mlo1, *mhi0, *mhi1;  // merged
+  int64_t *fl0, *fl1, *cl0, *cl1;      // floor(i ext / k), ceil((i + 1) ext / k)
+  int64_t* ob;                         // [8][4] OBB extents per angle
+  __device__ int32_t* lo(int a) const { return a ? lo1 : lo0; }
+  __device__ int32_t* hi(int a) const { return a ? hi1 : hi0; }
+  __device__ int32_t* mlo(int a) const { return a ? mlo1 : mlo0; }
+  __device__ int32_t* mhi(int a) const { return a ? mhi1 : mhi0; }
+};
+
+__host__ __device__ constexpr size_t slice_bytes(int k) {
+  return ((size_t)8 * 4 * k + (size_t)4 * 8 * k + 256 + 15) & ~(size_t)15;
+}
+
+template <int G>
+struct Group {
+  int gl;         // lane within the group
+  unsigned mask;  // the group's lanes
+  __device__ void sync() const { __syncwarp(mask); }
+  template <class T>
+  __device__ T xorv(T v, int o) const { return __shfl_xor_sync(mask, v, o, G); }
+  __device__ int32_t min32(int32_t v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = min(v, xorv(v, o));
+    return v;
+  }
+  __device__ int32_t max32(int32_t v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = max(v, xorv(v, o));
+    return v;
+  }
+  __device__ uint32_t sumu(uint32_t v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += xorv(v, o);
+    return v;
+  }
+  __device__ int64_t sum64(int64_t v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += xorv(v, o);
+    return v;
+  }
+  __device__ i128 sum128(i128 v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const uint64_t lo = xorv((uint64_t)v, o), hi = xorv((uint64_t)(v >> 64), o);
+      v += (i128)(((unsigned __int128)hi << 64) | lo);
+    }
+    return v;
+  }
 };
 
 // D4: slice bounds along one axis.  A = coordinate that is sliced (x for
 // x-slices), B = the bounded coordinate.  Strip j = closed range k*A in
 // [j*ext, (j+1)*ext].
-__device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, int64_t ext, int k,
-                                  int32_t* lo, int32_t* hi, int lane) {
+template <int G>
+__device__ void accumulate_slices(const Group<G>& g, const int32_t* A, const int32_t* B, int nv,
+                                  int64_t ext, int k, int32_t* lo, int32_t* hi) {
   const double rext = rcp_approx((double)ext);
-  for (int v = lane; v < nv; v += 32) {
+  for (int v = g.gl; v < nv; v += G) {
     int64_t ka = (int64_t)k * A[v];
     int64_t jh = fdiv_r64(ka, ext, rext);            // floor(k*a/ext), a >= 0
     int64_t jl = -fdiv_r64(-ka, ext, rext) - 1;      // ceil(k*a/ext) - 1
@@ -46,7 +97,7 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
       }
     }
   }
-  for (int v = lane; v < nv; v += 32) {
+  for (int v = g.gl; v < nv; v += G) {
     int a = v, b = (v + 1 == nv) ? 0 : v + 1;
     int64_t xa = A[a], xb = A[b], ya = B[a], yb = B[b];
     if (xa == xb) continue;
@@ -74,74 +125,90 @@ __device__ void accumulate_slices(const int32_t* A, const int32_t* B, int nv, in
 }
 
 // D5 merge: x-slice j tightened by y-slices whose x-range meets strip j.
-__device__ void merge_slices(WarpSlices& S, int64_t w, int64_t h, int k, int lane) {
-  for (int i = lane; i < k; i += 32) {
-    S.fl[0][i] = fdiv_fast((int64_t)i * h, k);
-    S.cl[0][i] = cdiv_fast((int64_t)(i + 1) * h, k);
-    S.fl[1][i] = fdiv_fast((int64_t)i * w, k);
-    S.cl[1][i] = cdiv_fast((int64_t)(i + 1) * w, k);
+template <int G>
+__device__ void merge_slices(const Group<G>& g, const Slices& S, int64_t w, int64_t h, int k) {
+  for (int i = g.gl; i < k; i += G) {
+    S.fl0[i] = fdiv_fast((int64_t)i * h, k);
+    S.cl0[i] = cdiv_fast((int64_t)(i + 1) * h, k);
+    S.fl1[i] = fdiv_fast((int64_t)i * w, k);
+    S.cl1[i] = cdiv_fast((int64_t)(i + 1) * w, k);
   }
-  __syncwarp();
-  for (int j = lane; j < k; j += 32) {
+  g.sync();
+  for (int j = g.gl; j < k; j += G) {
     // x-slices
     int64_t mn = INT64_MAX, mx = INT64_MIN;
     for (int i = 0; i < k; i++) {
-      if ((int64_t)k * S.lo[1][i] <= (int64_t)(j + 1) * w && (int64_t)k * S.hi[1][i] >= (int64_t)j * w) {
-        const int64_t f = S.fl[0][i], c = S.cl[0][i];
+      if ((int64_t)k * S.lo1[i] <= (int64_t)(j + 1) * w && (int64_t)k * S.hi1[i] >= (int64_t)j * w) {
+        const int64_t f = S.fl0[i], c = S.cl0[i];
         mn = f < mn ? f : mn;
         mx = c > mx ? c : mx;
       }
     }
-    int64_t t = S.lo[0][j], b = S.hi[0][j];
+    int64_t t = S.lo0[j], b = S.hi0[j];
     if (mn != INT64_MAX && mn > t) t = mn;
     if (mx != INT64_MIN && mx < b) b = mx;
-    S.mlo[0][j] = (int32_t)t;
-    S.mhi[0][j] = (int32_t)b;
+    S.mlo0[j] = (int32_t)t;
+    S.mhi0[j] = (int32_t)b;
     // y-slices
     mn = INT64_MAX;
     mx = INT64_MIN;
     for (int i = 0; i < k; i++) {
-      if ((int64_t)k * S.lo[0][i] <= (int64_t)(j + 1) * h && (int64_t)k * S.hi[0][i] >= (int64_t)j * h) {
-        const int64_t f = S.fl[1][i], c = S.cl[1][i];
+      if ((int64_t)k * S.lo0[i] <= (int64_t)(j + 1) * h && (int64_t)k * S.hi0[i] >= (int64_t)j * h) {
+        const int64_t f = S.fl1[i], c = S.cl1[i];
         mn = f < mn ? f : mn;
         mx = c > mx ? c : mx;
       }
     }
-    t = S.lo[1][j];
-    b = S.hi[1][j];
+    t = S.lo1[j];
+    b = S.hi1[j];
     if (mn != INT64_MAX && mn > t) t = mn;
     if (mx != INT64_MIN && mx < b) b = mx;
-    S.mlo[1][j] = (int32_t)t;
-    S.mhi[1][j] = (int32_t)b;
+    S.mlo1[j] = (int32_t)t;
+    S.mhi1[j] = (int32_t)b;
   }
 }
 
-__device__ void merged_slices(WarpSlices& S, const int32_t* X, const int32_t* Y, int nv, int64_t w,
-                              int64_t h, int k, int lane) {
-  for (int j = lane; j < k; j += 32) {
-    S.lo[0][j] = INT32_MAX; S.hi[0][j] = INT32_MIN;
-    S.lo[1][j] = INT32_MAX; S.hi[1][j] = INT32_MIN;
+template <int G>
+__device__ void merged_slices(const Group<G>& g, const Slices& S, const int32_t* X, const int32_t* Y,
+                              int nv, int64_t w, int64_t h, int k) {
+  for (int j = g.gl; j < k; j += G) {
+    S.lo0[j] = INT32_MAX; S.hi0[j] = INT32_MIN;
+    S.lo1[j] = INT32_MAX; S.hi1[j] = INT32_MIN;
   }
-  __syncwarp();
-  accumulate_slices(X, Y, nv, w, k, S.lo[0], S.hi[0], lane);
-  accumulate_slices(Y, X, nv, h, k, S.lo[1], S.hi[1], lane);
-  __syncwarp();
-  merge_slices(S, w, h, k, lane);
-  __syncwarp();
+  g.sync();
+  accumulate_slices(g, X, Y, nv, w, k, S.lo0, S.hi0);
+  accumulate_slices(g, Y, X, nv, h, k, S.lo1, S.hi1);
+  g.sync();
+  merge_slices(g, S, w, h, k);
+  g.sync();
 }
 
-__global__ void __launch_bounds__(kWarps * 32)
+template <int G>
+__global__ void __launch_bounds__(kBlock)
 proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
              float ry, int k, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
-  __shared__ WarpSlices smem[kWarps];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int c = blockIdx.x * kWarps + wib;
-  if (c >= n) return;
-  WarpSlices& S = smem[wib];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int lane = threadIdx.x & 31, gib = threadIdx.x / G;
+  Group<G> g;
+  g.gl = lane % G;
+  g.mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane / G * G));
+  const int c = blockIdx.x * (kBlock / G) + gib;
+  if (c >= n) return;  // the whole group leaves together
+  Slices S;
+  {
+    unsigned char* p = dsm + slice_bytes(k) * gib;
+    int32_t* i32 = (int32_t*)p;
+    S.lo0 = i32; S.lo1 = i32 + k; S.hi0 = i32 + 2 * k; S.hi1 = i32 + 3 * k;
+    S.mlo0 = i32 + 4 * k; S.mlo1 = i32 + 5 * k; S.mhi0 = i32 + 6 * k; S.mhi1 = i32 + 7 * k;
+    int64_t* i64 = (int64_t*)(p + 32 * (size_t)k);
+    S.fl0 = i64; S.fl1 = i64 + k; S.cl0 = i64 + 2 * k; S.cl1 = i64 + 3 * k;
+    S.ob = i64 + 4 * k;
+  }
+  const int gl = g.gl;
   const int32_t a0 = start[c];
   const int nv = start[c + 1] - a0;
   if (nv < 3) {
-    if (lane == 0) atomicMin(&st->bad_chart, c);
+    if (gl == 0) atomicMin(&st->bad_chart, c);
     return;
   }
   int32_t* X = qx + a0;
@@ -149,7 +216,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   // A1 snap: q = round_half_even(x * res * 256), exact product in double (D2)
   bool ok = true;
   int32_t xmn = INT32_MAX, xmx = INT32_MIN, ymn = INT32_MAX, ymx = INT32_MIN;
-  for (int v = lane; v < nv; v += 32) {
+  for (int v = gl; v < nv; v += G) {
     double fx = (double)xy[2 * (int64_t)(a0 + v)] * (double)rx * 256.0;
     double fy = (double)xy[2 * (int64_t)(a0 + v) + 1] * (double)ry * 256.0;
     if (!isfinite(fx) || !isfinite(fy) || fabs(fx) > (double)TABI_QMAX ||
@@ -163,53 +230,52 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     xmn = min(xmn, ix); xmx = max(xmx, ix);
     ymn = min(ymn, iy); ymx = max(ymx, iy);
   }
-  if (!__all_sync(0xffffffffu, ok)) {
-    if (lane == 0) atomicMin(&st->bad_chart, c);
+  if (__ballot_sync(g.mask, !ok) != 0u) {
+    if (gl == 0) atomicMin(&st->bad_chart, c);
     return;
   }
-  xmn = warp_min(xmn); xmx = warp_max(xmx);
-  ymn = warp_min(ymn); ymx = warp_max(ymx);
+  xmn = g.min32(xmn); xmx = g.max32(xmx);
+  ymn = g.min32(ymn); ymx = g.max32(ymx);
   int64_t w = (int64_t)xmx - xmn, h = (int64_t)ymx - ymn;
-  __syncwarp();
-  for (int v = lane; v < nv; v += 32) { X[v] -= xmn; Y[v] -= ymn; }
-  __syncwarp();
+  g.sync();
+  for (int v = gl; v < nv; v += G) { X[v] -= xmn; Y[v] -= ymn; }
+  g.sync();
   // D3 shoelace (2 x area), exact
   i128 s2 = 0;
-  for (int v = lane; v < nv; v += 32) {
+  for (int v = gl; v < nv; v += G) {
     int u = (v + 1 == nv) ? 0 : v + 1;
     s2 += (i128)((int64_t)X[v] * Y[u] - (int64_t)X[u] * Y[v]);
   }
-  s2 = warp_sum128(s2);
+  s2 = g.sum128(s2);
   if (s2 < 0) s2 = -s2;
   if (s2 == 0) {
-    if (lane == 0) atomicMin(&st->bad_chart, c);
+    if (gl == 0) atomicMin(&st->bad_chart, c);
     return;
   }
   // D3 90-degree normalization: (x, y) -> (h - y, x) iff w > h
   const bool rot = w > h;
   if (rot) {
-    for (int v = lane; v < nv; v += 32) {
+    for (int v = gl; v < nv; v += G) {
       int32_t nx = (int32_t)(h - Y[v]), ny = X[v];
       X[v] = nx;
       Y[v] = ny;
     }
     int64_t t = w; w = h; h = t;
   }
-  __syncwarp();
+  g.sync();
   // D4/D5 in the normalized pose, D7 orientation
-  merged_slices(S, X, Y, nv, w, h, k, lane);
+  merged_slices(g, S, X, Y, nv, w, h, k);
   // empty-area sums: every term is in [0, 2^25] and k <= 64, so the sums fit
-  // 32 unsigned bits and reduce in hardware (REDUX)
+  // 32 unsigned bits
   uint32_t top = 0, bot = 0, left = 0, right = 0;
-  for (int j = lane; j < k; j += 32) {
-    top += (uint32_t)S.mlo[0][j];
-    bot += (uint32_t)(h - S.mhi[0][j]);
-    left += (uint32_t)S.mlo[1][j];
-    right += (uint32_t)(w - S.mhi[1][j]);
+  for (int j = gl; j < k; j += G) {
+    top += (uint32_t)S.mlo0[j];
+    bot += (uint32_t)(h - S.mhi0[j]);
+    left += (uint32_t)S.mlo1[j];
+    right += (uint32_t)(w - S.mhi1[j]);
   }
-  const int64_t TOP = __reduce_add_sync(0xffffffffu, top), BOT = __reduce_add_sync(0xffffffffu, bot);
-  const int64_t LEFT = __reduce_add_sync(0xffffffffu, left);
-  const int64_t RIGHT = __reduce_add_sync(0xffffffffu, right);
+  const int64_t TOP = g.sumu(top), BOT = g.sumu(bot);
+  const int64_t LEFT = g.sumu(left), RIGHT = g.sumu(right);
   const bool fy = TOP > BOT;
   const int64_t D = LEFT - RIGHT;
   bool fx;
@@ -219,14 +285,14 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     fx = false;
   } else {
     int64_t BL2 = 0, BR2 = 0;
-    for (int j = lane; j < k; j += 32) {
-      int64_t gap = fy ? S.mlo[0][j] : (h - S.mhi[0][j]);
+    for (int j = gl; j < k; j += G) {
+      int64_t gap = fy ? S.mlo0[j] : (h - S.mhi0[j]);
       if (2 * j + 1 < k) BL2 += 2 * gap;
       else if (2 * j + 1 > k) BR2 += 2 * gap;
       else { BL2 += gap; BR2 += gap; }
     }
-    BL2 = warp_sum64(BL2);
-    BR2 = warp_sum64(BR2);
+    BL2 = g.sum64(BL2);
+    BR2 = g.sum64(BR2);
     fx = BL2 > BR2;
   }
   // D8 final pose.  The slices of the reflected chart are the reflected
@@ -236,73 +302,74 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   // mirror plus a value reflection of the ones just computed -- no second
   // slicing pass (tests compare every slice with the oracle, which re-slices).
   if (fx || fy) {
-    __syncwarp();
-    for (int v = lane; v < nv; v += 32) {
+    g.sync();
+    for (int v = gl; v < nv; v += G) {
       if (fx) X[v] = (int32_t)(w - X[v]);
       if (fy) Y[v] = (int32_t)(h - Y[v]);
     }
-    int32_t t0[2], b0[2], l1[2], r1[2];  // k <= 64: two slices per lane
+    constexpr int U = TABI_KMAX / G;  // slices per lane (k <= 64)
+    int32_t t0[U], b0[U], l1[U], r1[U];
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
-      const int j = lane + 32 * u;
+    for (int u = 0; u < U; u++) {
+      const int j = gl + G * u;
       if (j >= k) continue;
       const int sx = fx ? k - 1 - j : j;  // x-slices are indexed along x
       const int sy = fy ? k - 1 - j : j;  // y-slices along y
-      t0[u] = fy ? (int32_t)(h - S.mhi[0][sx]) : S.mlo[0][sx];
-      b0[u] = fy ? (int32_t)(h - S.mlo[0][sx]) : S.mhi[0][sx];
-      l1[u] = fx ? (int32_t)(w - S.mhi[1][sy]) : S.mlo[1][sy];
-      r1[u] = fx ? (int32_t)(w - S.mlo[1][sy]) : S.mhi[1][sy];
+      t0[u] = fy ? (int32_t)(h - S.mhi0[sx]) : S.mlo0[sx];
+      b0[u] = fy ? (int32_t)(h - S.mlo0[sx]) : S.mhi0[sx];
+      l1[u] = fx ? (int32_t)(w - S.mhi1[sy]) : S.mlo1[sy];
+      r1[u] = fx ? (int32_t)(w - S.mlo1[sy]) : S.mhi1[sy];
     }
-    __syncwarp();
+    g.sync();
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
-      const int j = lane + 32 * u;
+    for (int u = 0; u < U; u++) {
+      const int j = gl + G * u;
       if (j >= k) continue;
-      S.mlo[0][j] = t0[u]; S.mhi[0][j] = b0[u];
-      S.mlo[1][j] = l1[u]; S.mhi[1][j] = r1[u];
+      S.mlo0[j] = t0[u]; S.mhi0[j] = b0[u];
+      S.mlo1[j] = l1[u]; S.mhi1[j] = r1[u];
     }
-    __syncwarp();
+    g.sync();
   }
   int32_t* sl = P.sl + (int64_t)c * 4 * k;
-  for (int j = lane; j < k; j += 32) {
-    sl[j] = S.mlo[0][j];
-    sl[k + j] = S.mhi[0][j];
-    sl[2 * k + j] = S.mlo[1][j];
-    sl[3 * k + j] = S.mhi[1][j];
+  for (int j = gl; j < k; j += G) {
+    sl[j] = S.mlo0[j];
+    sl[k + j] = S.mhi0[j];
+    sl[2 * k + j] = S.mlo1[j];
+    sl[3 * k + j] = S.mhi1[j];
   }
   // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j.
-  // All 8 angles at once: lane = 4 * angle + vertex group, so the extents are
-  // reduced over 4 lanes (2 shuffle steps) instead of 32 lanes per angle.
+  // All 8 angles at once: lane = (G / 8) * angle + vertex subgroup, so each
+  // angle's extents reduce over G / 8 lanes only.
   {
-    const int j = lane >> 2, g = lane & 3;
+    constexpr int VG = G / 8;  // lanes per angle
+    const int j = gl / VG, vg = gl % VG;
     const int64_t C = kQC[j], Sn = kQS[j];
     int64_t u0 = INT64_MAX, u1 = INT64_MIN, v0 = INT64_MAX, v1 = INT64_MIN;
-    for (int v = g; v < nv; v += 4) {
+    for (int v = vg; v < nv; v += VG) {
       const int64_t x = X[v], y = Y[v];
       const int64_t u = x * C + y * Sn, vv = -x * Sn + y * C;
       u0 = u < u0 ? u : u0; u1 = u > u1 ? u : u1;
       v0 = vv < v0 ? vv : v0; v1 = vv > v1 ? vv : v1;
     }
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-      int64_t t = __shfl_xor_sync(0xffffffffu, u0, o); u0 = t < u0 ? t : u0;
-      t = __shfl_xor_sync(0xffffffffu, u1, o); u1 = t > u1 ? t : u1;
-      t = __shfl_xor_sync(0xffffffffu, v0, o); v0 = t < v0 ? t : v0;
-      t = __shfl_xor_sync(0xffffffffu, v1, o); v1 = t > v1 ? t : v1;
+    for (int o = 1; o < VG; o <<= 1) {
+      int64_t t = g.xorv(u0, o); u0 = t < u0 ? t : u0;
+      t = g.xorv(u1, o); u1 = t > u1 ? t : u1;
+      t = g.xorv(v0, o); v0 = t < v0 ? t : v0;
+      t = g.xorv(v1, o); v1 = t > v1 ? t : v1;
     }
-    if (g == 0) {
-      S.ob[j][0] = u0; S.ob[j][1] = u1; S.ob[j][2] = v0; S.ob[j][3] = v1;
+    if (vg == 0) {
+      S.ob[4 * j + 0] = u0; S.ob[4 * j + 1] = u1; S.ob[4 * j + 2] = v0; S.ob[4 * j + 3] = v1;
     }
-    __syncwarp();
+    g.sync();
   }
-  if (lane == 0) {
+  if (gl == 0) {
     i128 best = -1;
     int bj = 0;
     for (int j = 0; j < 8; j++) {
-      const i128 area = (i128)(S.ob[j][1] - S.ob[j][0]) * (i128)(S.ob[j][3] - S.ob[j][2]);
+      const i128 area = (i128)(S.ob[4 * j + 1] - S.ob[4 * j]) * (i128)(S.ob[4 * j + 3] - S.ob[4 * j + 2]);
       if (best < 0 || area < best) { best = area; bj = j; }
     }
-    const int64_t bu0 = S.ob[bj][0], bu1 = S.ob[bj][1], bv0 = S.ob[bj][2], bv1 = S.ob[bj][3];
     P.w[c] = (int32_t)w;
     P.h[c] = (int32_t)h;
     P.area2[c] = (int64_t)s2;
@@ -310,19 +377,39 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     P.ymin[c] = ymn;
     P.pose[c] = (uint8_t)((rot ? 1 : 0) | (fx ? 2 : 0) | (fy ? 4 : 0));
     P.obb_j[c] = bj;
-    P.obb[4 * (int64_t)c + 0] = bu0;
-    P.obb[4 * (int64_t)c + 1] = bu1;
-    P.obb[4 * (int64_t)c + 2] = bv0;
-    P.obb[4 * (int64_t)c + 3] = bv1;
+    P.obb[4 * (int64_t)c + 0] = S.ob[4 * bj + 0];
+    P.obb[4 * (int64_t)c + 1] = S.ob[4 * bj + 1];
+    P.obb[4 * (int64_t)c + 2] = S.ob[4 * bj + 2];
+    P.obb[4 * (int64_t)c + 3] = S.ob[4 * bj + 3];
   }
+}
+
+template <int G>
+void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
+              int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+  constexpr int per_block = kBlock / G;
+  const int blocks = (n + per_block - 1) / per_block;
+  const size_t smem = slice_bytes(k) * per_block;
+  static bool attr = false;
+  if (!attr) {  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
+    cudaFuncSetAttribute(proxy_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(slice_bytes(TABI_KMAX) * per_block));
+    attr = true;
+  }
+  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, qx, qy, P, st);
 }
 
 }  // namespace
 
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
-  int blocks = (n + kWarps - 1) / kWarps;
-  proxy_kernel<<<blocks, kWarps * 32, 0, s>>>(xy, start, n, rx, ry, k, qx, qy, P, st);
+  const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
+  const int forced = genv ? atoi(genv) : 0;
+  const int G = forced == 8 || forced == 16 || forced == 32 ? forced
+                : n < 4096 ? 32 : n < 8192 ? 16 : 8;  // measured: C3 (1572) 32, C4 (20000) 8
+  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, qx, qy, P, st, s);
+  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, qx, qy, P, st, s);
+  else launch_g<8>(xy, start, n, rx, ry, k, qx, qy, P, st, s);
 }
 
 }  // namespace tabi

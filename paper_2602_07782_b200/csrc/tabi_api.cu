@@ -477,8 +477,10 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     pp.wave = wave;
     const bool prologue = attempt == 0;
     if (prologue && use_graph) {
-      char sort_env = 0;
+      char sort_env = 0;  // test knobs read while enqueuing: part of the key
       for (const char* p = getenv("TABI_SORT"); p && *p; p++) sort_env = (char)(sort_env * 31 + *p);
+      for (const char* p = getenv("TABI_PROXY_LANES"); p && *p; p++)
+        sort_env = (char)(sort_env * 37 + *p);
       GraphKey key{xy, chart_start, out, n, V_in, on_device, res_x, res_y, *spec, B,
                    fused ? 1 : 0, ctx->alloc_gen, sort_env};
       if (!ctx->gexec || !(key == ctx->gkey)) {

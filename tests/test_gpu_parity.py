@@ -303,6 +303,18 @@ def test_sort_paths_with_ties(orc, ctx, path, monkeypatch):
     _compare_pack(orc, ctx, chartgen.config2(2), check_profiles=0)
 
 
+@pytest.mark.parametrize("lanes", ["8", "16", "32"])
+def test_proxy_lane_groups(orc, ctx, lanes, monkeypatch):
+    """K1 with 8, 16 and 32 lanes per chart (TABI_PROXY_LANES forces the
+    group size the launcher otherwise picks by chart count): proxies, order
+    and the whole pack bit-exact, on charts from 3 to ~100 vertices."""
+    monkeypatch.setenv("TABI_PROXY_LANES", lanes)
+    _compare_pack(orc, ctx, chartgen.small_case(9, n=120, family="mixed", rho=0.9),
+                  check_profiles=2)
+    _compare_pack(orc, ctx, chartgen.small_case(4, n=60, family="uv"), check_profiles=2,
+                  local_aabb_count=64)
+
+
 def test_determinism_and_capacity_growth():
     from paper_2602_07782_b200 import Context, spec_of
     cs = chartgen.config3(1, rho=2.0)
