@@ -472,5 +472,76 @@ __device__ __forceinline__ void pair_offset(const PackParams& pp, const int32_t*
   }
 }
 
+// pair_offset for a pair with many shared rows, by a whole group of TT
+// threads: the gap maximum is a block reduction, and the lock tests' running
+// prefix min / max over rows become one exclusive block scan of per-thread
+// segment extrema followed by a walk of each segment -- the same predicates as
+// warp_locks, evaluated by TT threads instead of one warp.  red: >= 2 * (TT /
+// 32) + 1 ints of shared scratch.  s < n - 1.  Ends with a sync.
+template <int TT, class Sync>
+__device__ void pair_offset_group(const PackParams& pp, const int32_t* __restrict__ rowofs,
+                                  const uint32_t* drow, const int32_t* wd_all,
+                                  const int32_t* hd_all, int32_t* off_all, uint8_t* lock_all,
+                                  int m, int s, int tid, Sync sync, int32_t* red) {
+  constexpr int NW = TT / 32;
+  const int lane = tid & 31, w = tid >> 5;
+  const int64_t base = (int64_t)(m - 1) * pp.n;
+  const int32_t Hda = hd_all[base + s], Hdb = hd_all[base + s + 1], Wda = wd_all[base + s];
+  const uint32_t* ra = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
+  const uint32_t* rb = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s + 1];
+  const int rows = min(Hda, Hdb);
+  int32_t off = 0;
+  for (int j = tid; j < rows; j += TT) off = max(off, hi16(ra[j]) - lo16(rb[j]));
+  off = warp_max(off);
+  if (lane == 0) red[w] = off;
+  if (tid == 0) red[2 * NW] = 0;
+  sync();
+  off = 0;
+  for (int i = 0; i < NW; i++) off = max(off, red[i]);
+  sync();
+  bool xa = false, xb = false;
+  if (off < Wda) {
+    const int L = (Hdb + TT - 1) / TT;  // rows [r0, r1) of this thread
+    const int r0 = min(Hdb, tid * L), r1 = min(Hdb, r0 + L);
+    int32_t smin = INT32_MAX, smax = INT32_MIN;
+    for (int r = r0; r < r1; r++) {
+      smin = min(smin, lo16(rb[r]));
+      smax = max(smax, hi16(ra[r]));
+    }
+    const int32_t imin = warp_incl_min(smin, lane), imax = warp_incl_max(smax, lane);
+    if (lane == 31) { red[w] = imin; red[NW + w] = imax; }
+    sync();
+    int32_t cmin = INT32_MAX, cmax = INT32_MIN, tmin = INT32_MAX;
+    for (int i = 0; i < NW; i++) {
+      if (i < w) { cmin = min(cmin, red[i]); cmax = max(cmax, red[NW + i]); }
+      tmin = min(tmin, red[i]);
+    }
+    int32_t emin = __shfl_up_sync(0xffffffffu, imin, 1);
+    int32_t emax = __shfl_up_sync(0xffffffffu, imax, 1);
+    if (lane == 0) { emin = INT32_MAX; emax = INT32_MIN; }
+    emin = min(emin, cmin);  // prefix over rows < r0
+    emax = max(emax, cmax);
+    for (int r = r0; r < r1; r++) {
+      const int32_t lb_r = lo16(rb[r]), ra_r = hi16(ra[r]);
+      if (r >= 1) {
+        if (emin != INT32_MAX && ra_r > off + emin) xa = true;
+        if (emax != INT32_MIN && off + lb_r < emax) xb = true;
+      }
+      emin = min(emin, lb_r);
+      emax = max(emax, ra_r);
+    }
+    for (int r = Hdb + tid; r < Hda; r += TT)
+      if (r >= 1 && hi16(ra[r]) > off + tmin) xa = true;
+  }
+  const bool any_a = __any_sync(0xffffffffu, xa), any_b = __any_sync(0xffffffffu, xb);
+  if (lane == 0 && (any_a || any_b)) atomicOr(&red[2 * NW], (any_a ? 1 : 0) | (any_b ? 2 : 0));
+  sync();
+  if (tid == 0) {
+    off_all[base + s] = off;
+    lock_all[base + s] = (uint8_t)red[2 * NW];
+  }
+  sync();
+}
+
 }  // namespace k3
 }  // namespace tabi

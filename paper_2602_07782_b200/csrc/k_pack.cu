@@ -1049,7 +1049,7 @@ __host__ __device__ __forceinline__ size_t r16(size_t b) { return (b + 15) & ~(s
 // per-group carve of the dynamic shared memory
 __host__ __device__ __forceinline__ size_t group_bytes(int k) {
   return r16(sizeof(k3::ChartK3) * kTCF) + r16(4 * kTCF) + 2 * r16(4 * (kTCF + 1)) +
-         r16(4 * kTCF) + r16(32) + r16((size_t)4 * kTCF * 4 * k) + r16(4 * (size_t)kRawF);
+         r16(4 * kTCF) + r16(32) + r16(4 * (2 * kRGW + 4)) + r16((size_t)4 * kTCF * 4 * k) + r16(4 * (size_t)kRawF);
 }
 
 __device__ __forceinline__ unsigned char* carve(unsigned char*& p, size_t bytes) {
@@ -1085,6 +1085,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   int32_t* opre = (int32_t*)carve(p, 4 * (kTCF + 1));
   int32_t* big = (int32_t*)carve(p, 4 * kTCF);
   int32_t* misc = (int32_t*)carve(p, 32);
+  int32_t* red = (int32_t*)carve(p, 4 * (2 * kRGW + 4));  // group reductions (big pairs)
   int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kTCF * 4 * k);
   uint32_t* raw = (uint32_t*)carve(p, 4 * (size_t)kRawF);
   p = dsm + group_bytes(k) * kRG;  // per-warp large-chart state
@@ -1190,8 +1191,22 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     const bool needL = misc[2] != 0, needR = misc[3] != 0;
     const int lo = needL ? s0 - 1 : s0;
     const int hi = (t == T - 1) ? pp.n - 1 : (needR ? s0 + nt - 1 : s0 + nt - 2);
+    // internal pairs with many shared rows (the tallest charts, first in the
+    // order and first needed by the packers) go to the whole group; the rest
+    // one warp each
+    // (only in tiles with fewer charts than half the group's warps: otherwise
+    // warp-per-pair already keeps every warp busy)
+    auto big_pair = [&](int s) {
+      return 2 * nt <= kRGW && s >= s0 && s + 1 < s0 + nt &&
+             min(CH[s - s0].hs, CH[s + 1 - s0].hs) >= 512;
+    };
     for (int s = lo + gw; s <= hi; s += kRGW)
-      k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
+      if (!big_pair(s))
+        k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
+    for (int s = max(lo, s0); s <= hi; s++)
+      if (big_pair(s))
+        k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, gt,
+                                    gsync, red);
     gsync();
     rmark(4);
     if (gt == 0) {
