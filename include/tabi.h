@@ -188,10 +188,12 @@ tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* 
  * -DTABI_PHASE_TRACE. */
 tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16);
 /* Fused rasterizer per-item phase SM cycles of the last wave, summed over
- * raster groups (0 unless built with -DTABI_PHASE_TRACE): queue fetch,
- * footprints, large charts + accounting, boundary arrivals, pair offsets,
- * publish, 0, 0. */
-tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out8);
+ * raster groups, 16 entries (0 unless built with -DTABI_PHASE_TRACE): [0..6]
+ * queue fetch, cells, large charts + accounting, boundary arrivals, pair
+ * offsets, publish, setup; [7] 0; [8..11] wave slot 0's first-row timeline in
+ * ns from the kernel start: tile 0 footprints done, tile 0 published, packer
+ * 0's first fold unblocked, packer 0's first row done; [12..15] 0. */
+tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out16);
 
 #ifdef __cplusplus
 }

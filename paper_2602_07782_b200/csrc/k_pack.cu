@@ -529,6 +529,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       for (int base = rs;;) {
         const int lim = wait_ready(base);
         if (lim == -2) break;  // beaten (S.abort): leave the row loop below
+#ifdef TABI_PHASE_TRACE
+        if (rd.flags && jslot == 0 && rs == 0 && base == 0 && tid == 0) st->tfirst[2] = gtime();
+#endif
         const int cnt = min(kNT, lim - base + 1);  // positions [base, base + cnt)
         if (tid < 4) S.fmin[tid] = INT32_MAX;
         const int s = base + tid;
@@ -933,6 +936,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     if (tid == 0) {
       if (prefix_mode) S.prefix_rows++;
       else S.rows++;
+#ifdef TABI_PHASE_TRACE
+      if (rd.flags && jslot == 0 && S.rows == 1 && !prefix_mode) st->tfirst[3] = gtime();
+#endif
       if (f == 1) S.knee_rows++;
       if (f == 0 && !no_bal && !prefix_mode) {
         if (S.knee_key != 0ull) {
@@ -1155,8 +1161,16 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
                                        ra.hd, ra.cand_bad, m, s0, sc, CH, cells, cpre, opre,
                                        &misc[1], big, tabs, raw, nt, gt, gsync,
-                                       [&]() { rmark(6); });
+                                       [&]() {
+                                         rmark(6);
+#ifdef TABI_PHASE_TRACE
+                                         if (gt == 0 && t == 0 && j == 0) st->tfirst[5] = gtime();
+#endif
+                                       });
     rmark(1);
+#ifdef TABI_PHASE_TRACE
+    if (gt == 0 && t == 0 && j == 0) atomicMax(&st->tfirst[0], gtime());
+#endif
     for (int ci = gw; ci < nt; ci += kRGW)
       if (big[ci])
         k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m, s0 + ci, sc, CW[wid],
@@ -1188,30 +1202,41 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     }
     gsync();
     rmark(3);
+#ifdef TABI_PHASE_TRACE
+    if (gt == 0 && t == 0 && j == 0) st->tfirst[6] = gtime();
+#endif
     const bool needL = misc[2] != 0, needR = misc[3] != 0;
     const int lo = needL ? s0 - 1 : s0;
     const int hi = (t == T - 1) ? pp.n - 1 : (needR ? s0 + nt - 1 : s0 + nt - 2);
-    // internal pairs with many shared rows (the tallest charts, first in the
-    // order and first needed by the packers) go to the whole group; the rest
-    // one warp each
-    // (only in tiles with fewer charts than half the group's warps: otherwise
-    // warp-per-pair already keeps every warp busy)
+    // pairs with many shared rows (the tallest charts, first in the order and
+    // first needed by the packers) go to the whole group, one after another;
+    // the rest one warp each.  Only in tiles with fewer charts than half the
+    // group's warps: otherwise warp-per-pair already keeps every warp busy.
     auto big_pair = [&](int s) {
-      return 2 * nt <= kRGW && s >= s0 && s + 1 < s0 + nt &&
-             min(CH[s - s0].hs, CH[s + 1 - s0].hs) >= 512;
+      if (2 * nt > kRGW || s + 1 >= pp.n) return false;
+      const int64_t b = (int64_t)(m - 1) * pp.n;  // boundary pairs: heights from HBM
+      const int32_t ha = s >= s0 ? CH[s - s0].hs : ra.hd[b + s] - 2 * pp.g;
+      const int32_t hb = s + 1 < s0 + nt ? CH[s + 1 - s0].hs : ra.hd[b + s + 1] - 2 * pp.g;
+      return min(ha, hb) >= 512;
     };
     for (int s = lo + gw; s <= hi; s += kRGW)
       if (!big_pair(s))
         k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
-    for (int s = max(lo, s0); s <= hi; s++)
+    for (int s = lo; s <= hi; s++)
       if (big_pair(s))
         k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, gt,
                                     gsync, red);
     gsync();
     rmark(4);
+#ifdef TABI_PHASE_TRACE
+    if (gt == 0 && t == 0 && j == 0) st->tfirst[7] = gtime();
+#endif
     if (gt == 0) {
       red_add_release(fl + t, (t == T - 1 || needR) ? 2 : 1);
       if (needL) red_add_release(fl + t - 1, 1);
+#ifdef TABI_PHASE_TRACE
+      if (j == 0 && (t == 0 || (t == 1 && needL))) atomicMax(&st->tfirst[1], gtime());
+#endif
     }
     rmark(5);
   }

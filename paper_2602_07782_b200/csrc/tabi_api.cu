@@ -742,9 +742,12 @@ extern "C" tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16) {
   return TABI_OK;
 }
 
-extern "C" tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out8) {
-  if (!ctx || !out8 || ctx->last_n < 1) return TABI_EINVAL;
-  for (int i = 0; i < 8; i++) out8[i] = (int64_t)ctx->h_status->rph[i];
+extern "C" tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out16) {
+  if (!ctx || !out16 || ctx->last_n < 1) return TABI_EINVAL;
+  const Status& st = *ctx->h_status;
+  for (int i = 0; i < 8; i++) out16[i] = (int64_t)st.rph[i];
+  for (int i = 0; i < 8; i++)
+    out16[8 + i] = st.tfirst[i] > st.tr[0] && st.tfirst[i] != 0 ? (int64_t)(st.tfirst[i] - st.tr[0]) : 0;
   return TABI_OK;
 }
 

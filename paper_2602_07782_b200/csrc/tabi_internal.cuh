@@ -330,6 +330,10 @@ struct Status {       // device-side status block, copied back once per pack
   // queue fetch, footprints (tile_raster), large charts, accounting,
   // boundary arrivals, pair offsets, publish
   unsigned long long rph[8];
+  // first-row timeline of wave slot 0 (%globaltimer, trace build): [0] its
+  // tile 0 footprints done, [1] tile 0 published, [2] packer 0's first fold
+  // unblocked, [3] packer 0's first row done
+  unsigned long long tfirst[8];  // + [4..7] its tile 0: fetched, setup, pairs start, pairs end
 };
 
 __device__ __forceinline__ unsigned long long gtime() {

@@ -245,10 +245,13 @@ class Context:
         self._chk(lib().tabi_debug_trace(self.h, _ptr(out)))
         keys = ("raster_end", "pack_end", "pack_wait", "raster_wait", "tiles", "fused")
         d = dict(zip(keys, (int(v) for v in out[:6])))
-        r8 = np.zeros(8, dtype=np.int64)
-        self._chk(lib().tabi_debug_trace_raster(self.h, _ptr(r8)))
+        r16 = np.zeros(16, dtype=np.int64)
+        self._chk(lib().tabi_debug_trace_raster(self.h, _ptr(r16)))
         d["raster_phases"] = dict(zip(("fetch", "cells", "big_acct", "arrivals", "pairs",
-                                       "publish", "setup"), (int(v) for v in r8[:7])))
+                                       "publish", "setup"), (int(v) for v in r16[:7])))
+        d["first_row_ns"] = dict(zip(("tile0_cells", "tile0_published", "fold_unblocked",
+                                      "row0_done", "-", "tile0_setup", "tile0_pairs_start",
+                                      "tile0_pairs_end"), (int(v) for v in r16[8:16])))
         d["phases"] = dict(zip(("knee", "fold", "hc_locks", "push", "alg1", "score", "commit",
                                 "findknee", "push_stage", "commit_stage"),
                                (int(v) for v in out[6:16])))
