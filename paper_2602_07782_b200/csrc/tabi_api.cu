@@ -1,9 +1,13 @@
 // tabi_api.cu -- host side of the C ABI declared in include/tabi.h.
 //
 // tabi_pack enqueues the whole pipeline on one stream with no host round trip
-// between kernels:  [H2D] -> K1 proxies -> K2 sort -> prep (slot layout) ->
-// K3 profiles -> K3b offsets/locks -> K4 fold&push (all candidates, one
-// launch) -> K5 select/scatter -> [D2H status (+ placements)] -> one sync.
+// between kernels:  [H2D] -> reset -> K1 proxies -> K2 sort -> prep (slot
+// layout, area bound, raster tiles) -> fused wave kernel (K3 footprints + K3b
+// pair offsets + K4 fold & push of a wave of candidates, one cooperative
+// launch; split K3/K3b/K4 kernels with TABI_FUSED=0) -> [hybrid tail] -> K5
+// select/scatter -> [D2H placements] + D2H status/records -> one sync.  The
+// first wave is captured once as a CUDA graph and replayed.  Further waves
+// (only when every candidate of a wave fails) cost one host round trip each.
 // If a device-side capacity check fails (footprint slots or lock-pair lists
 // larger than the current buffers), the context grows those buffers and
 // re-runs from the slot layout; sizes persist, so steady-state calls never
@@ -104,6 +108,8 @@ struct tabi_ctx {
   GraphKey gkey{};
   int g_launches = 0;
   int64_t alloc_gen = 0;
+  cudaError_t last_cuda = cudaSuccess;
+  bool fused_off = false;  // the cooperative launch was refused once: split kernels from now on
 };
 
 #define CK(call)                                              \
@@ -111,6 +117,7 @@ struct tabi_ctx {
     cudaError_t e_ = (call);                                  \
     if (e_ != cudaSuccess) {                                  \
       ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      ctx->last_cuda = e_;                                    \
       return TABI_ECUDA;                                      \
     }                                                         \
   } while (0)
@@ -290,10 +297,33 @@ struct Timer {
 };
 }  // namespace
 
+static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                             int32_t n, float res_x, float res_y, const tabi_spec* spec,
+                             tabi_placement* out, tabi_info* info, int on_device, void* stream);
+
 extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
                                  int32_t n, float res_x, float res_y, const tabi_spec* spec,
                                  tabi_placement* out, tabi_info* info, int on_device,
                                  void* stream) {
+  if (!ctx) return TABI_EINVAL;
+  ctx->last_cuda = cudaSuccess;
+  tabi_status st = pack_impl(ctx, xy, chart_start, n, res_x, res_y, spec, out, info, on_device,
+                             stream);
+  if (st == TABI_ECUDA && ctx->last_cuda == cudaErrorCooperativeLaunchTooLarge && !ctx->fused_off) {
+    // the GPU cannot hold the fused wave kernel's grid right now (shared
+    // device, MPS limits): same result from the split kernels
+    cudaGetLastError();
+    ctx->fused_off = true;
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+    st = pack_impl(ctx, xy, chart_start, n, res_x, res_y, spec, out, info, on_device, stream);
+  }
+  return st;
+}
+
+static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                             int32_t n, float res_x, float res_y, const tabi_spec* spec,
+                             tabi_placement* out, tabi_info* info, int on_device, void* stream) {
   if (!ctx) return TABI_EINVAL;
   if (info) {
     memset(info, 0, sizeof(*info));
@@ -371,7 +401,8 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
   // fused wave kernel: needs B packer CTAs plus rasterizer CTAs co-resident
   const char* fenv = getenv("TABI_FUSED");
   const int fgrid = fused_grid(ctx->device);
-  const bool fused = !(fenv && fenv[0] == '0') && fgrid >= B + 8 && fused_fits(pp.k);
+  const bool fused = !(fenv && fenv[0] == '0') && !ctx->fused_off && fgrid >= B + 8 &&
+                     fused_fits(pp.k);
   if (info) info->fused = fused ? 1 : 0;
   ctx->last_fused = fused ? 1 : 0;
   const int64_t nrdy = fused ? 2 * (int64_t)B * n : 0;  // ready flags + arrival counters
