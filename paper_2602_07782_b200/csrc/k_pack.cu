@@ -708,6 +708,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           if (four) {
             const int32_t* f2 = F + cfgX(2, i);
             const int32_t* f3 = F + cfgX(3, i) + Wd - 1;
+            #pragma unroll 4
             for (int32_t j = j0; j < j1; j++) {
               const uint32_t v = pc[j];
               const int32_t top = lo16(v);
@@ -718,6 +719,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               m3 = max(m3, f3[-j] - top);
             }
           } else {
+            #pragma unroll 4
             for (int32_t j = j0; j < j1; j++) {
               const uint32_t v = pc[j];
               const int32_t top = lo16(v);
@@ -922,9 +924,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             const uint32_t* pc = pr + W.rco[i];
             if (dir) {
               int32_t* fp = Fs + Xc + Wd - 1;
+              #pragma unroll 4
               for (int32_t j = j0; j < j1; j++) atomicMax(fp - j, Yv + hi16(pc[j]));
             } else {
               int32_t* fp = Fs + Xc;
+              #pragma unroll 4
               for (int32_t j = j0; j < j1; j++) atomicMax(fp + j, Yv + hi16(pc[j]));
             }
             wk += (unsigned long long)(j1 - j0);
