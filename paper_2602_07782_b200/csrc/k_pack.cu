@@ -811,6 +811,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             }
           }
           __syncthreads();
+#ifdef TABI_PHASE_TRACE
+          if (tid == 0 && jslot == 0) atomicAdd(&st->rph[7], 1ull);  // Alg. 1 passes
+#endif
           if (!S.changed3[fl]) break;
         }
       }

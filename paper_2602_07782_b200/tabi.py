@@ -249,6 +249,7 @@ class Context:
         self._chk(lib().tabi_debug_trace_raster(self.h, _ptr(r16)))
         d["raster_phases"] = dict(zip(("fetch", "cells", "big_acct", "arrivals", "pairs",
                                        "publish", "setup"), (int(v) for v in r16[:7])))
+        d["alg1_passes"] = int(r16[7])  # trace build: Alg. 1 passes of wave slot 0
         d["first_row_ns"] = dict(zip(("tile0_cells", "tile0_published", "fold_unblocked",
                                       "row0_done", "-", "tile0_setup", "tile0_pairs_start",
                                       "tile0_pairs_end"), (int(v) for v in r16[8:16])))

@@ -32,6 +32,7 @@ for name, cs in (("C3", chartgen.config3(0, rho=0.5)), ("C2", chartgen.config2(0
         rp = tr.pop("raster_phases")
         fr = tr.pop("first_row_ns")
         tiles = max(tr.get("tiles", 0), 1)
+        alg1_passes = tr.pop("alg1_passes", 0)
         print(name, "fused" if f == "1" else "split", "m", info.scale_index,
               "stages_us", [round(x * 1000) for x in info.stage_ms[:7]],
               {k: (us(v) if k in ("raster_end", "pack_end", "pack_wait", "raster_wait") else v)
@@ -39,4 +40,5 @@ for name, cs in (("C3", chartgen.config3(0, rho=0.5)), ("C2", chartgen.config2(0
               "rows", rows, "ns/row", {k: round(v / MHZ * 1000 / max(rows, 1)) for k, v in ph.items()},
               "raster ns/tile", {k: round(v / MHZ * 1000 / tiles) for k, v in rp.items()},
               "first row us", {k: round(v / 1000, 1) for k, v in fr.items()},
+              "alg1 passes (slot 0)", alg1_passes,
               flush=True)
