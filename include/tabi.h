@@ -37,14 +37,17 @@ typedef enum {
 enum {
   TABI_F_NO_HC = 1u,                 /* ablation: never compact horizontally */
   TABI_F_NO_BALANCE = 2u,            /* ablation: no knees, static L/R alternation    */
-  TABI_F_ADJACENT_LOCKS_ONLY = 4u    /* paper-literal Alg. 1 (adjacent pairs only)    */
+  TABI_F_ADJACENT_LOCKS_ONLY = 4u,   /* paper-literal Alg. 1 (adjacent pairs only)    */
+  TABI_F_PREROTATE = 8u              /* UV pre-rotation to the OBB angle (for UV
+                                        charts, not TSS -- rotation by non-90-degree angles
+                                        resamples the texture); see tabi_placement step 0 */
 };
 
 typedef struct tabi_ctx tabi_ctx;    /* opaque: device workspace + stream, one per host thread */
 
 /* Atlas + knobs (SPEC AtlasSpec S:33-36).  Invariants, else TABI_EINVAL:
  *   1 <= atlas_w, atlas_h <= 16384;  0 <= gutter <= 64;  1 <= scale_count <= 256;
- *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_*. */
+ *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_* (0..15). */
 typedef struct {
   int32_t atlas_w, atlas_h;   /* texels */
   int32_t gutter;             /* texels around every chart, none at atlas edges; paper 1 */
@@ -62,6 +65,9 @@ typedef struct {
 /* Per-chart output, 32 bytes, indexed by INPUT chart order.
  * Transform of an input vertex p = (x, y) * (res_x, res_y) (texels), exact in
  * 1/256-texel units (q = round_half_even(256 * p)):
+ *   0. if prerot = j > 0 (TABI_F_PREROTATE): q <- (round_half_even((qx C + qy S) / 2^30),
+ *      round_half_even((-qx S + qy C) / 2^30)) with (C, S) the Q30 cos / sin of j pi / 16
+ *      (the chart's minimum-area OBB angle, D6) -- its OBB becomes axis-aligned
  *   1. u = qx - min_qx, v = qy - min_qy           (chart AABB to the origin)
  *   2. if rot90:  (u, v) <- (h' - v, u)           (h' = the original AABB height;
  *                                                   the chart becomes taller than wide)
@@ -78,7 +84,8 @@ typedef struct {
   uint8_t rot90, flip_x, flip_y, mirror_x;
   uint8_t mode;                   /* 0 = sequential row, 1 = prefix-tail row (scale
                                      scale_num / scale_den = p / 2^20) */
-  uint8_t pad[3];
+  uint8_t prerot;                 /* pre-rotation angle index j (step 0), 0 = none */
+  uint8_t pad[2];
 } tabi_placement;
 
 typedef struct {
@@ -154,7 +161,7 @@ typedef struct {
   int32_t xmin, ymin;             /* snapped input AABB min */
   int32_t rot90, fx, fy, k;
   int32_t top[64], bot[64], left[64], right[64];   /* merged local AABBs */
-  int32_t obb_j, reserved;
+  int32_t obb_j, prerot;          /* prerot: pre-rotation angle index (TABI_F_PREROTATE) */
   int64_t umin, umax, vmin, vmax; /* OBB in the Q30-rotated frame, theta = obb_j * pi/16 */
 } tabi_proxy_dbg;
 

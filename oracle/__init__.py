@@ -21,7 +21,7 @@ SRCS = [os.path.join(HERE, f) for f in ("tabi_oracle.c", "validate.c")]
 KMAX = 64
 
 OK, EINVAL, NO_FIT = 0, 1, 2
-F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY = 1, 2, 4
+F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE = 1, 2, 4, 8
 
 
 def build(force: bool = False) -> str:
@@ -40,7 +40,7 @@ class Proxy(C.Structure):
                 ("rot90", C.c_int32), ("fx", C.c_int32), ("fy", C.c_int32), ("k", C.c_int32),
                 ("top", C.c_int32 * KMAX), ("bot", C.c_int32 * KMAX),
                 ("left", C.c_int32 * KMAX), ("right", C.c_int32 * KMAX),
-                ("obb_j", C.c_int32),
+                ("obb_j", C.c_int32), ("prerot", C.c_int32),
                 ("umin", C.c_int64), ("umax", C.c_int64), ("vmin", C.c_int64), ("vmax", C.c_int64)]
 
 
@@ -53,7 +53,8 @@ class Prof(C.Structure):
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
                             ("scale_den", "<i4"), ("box_w", "<i4"), ("box_h", "<i4"),
                             ("rot90", "u1"), ("flip_x", "u1"), ("flip_y", "u1"),
-                            ("mirror_x", "u1"), ("mode", "u1"), ("pad", "u1", (3,))])
+                            ("mirror_x", "u1"), ("mode", "u1"), ("prerot", "u1"),
+                            ("pad", "u1", (2,))])
 assert PLACEMENT_DTYPE.itemsize == 32
 
 
@@ -84,7 +85,7 @@ def lib():
         _lib = C.CDLL(build())
         P = C.c_void_p
         i32, i64 = C.c_int32, C.c_int64
-        _lib.or_build_proxies.argtypes = [P, P, i32, C.c_float, C.c_float, i32, P, P]
+        _lib.or_build_proxies.argtypes = [P, P, i32, C.c_float, C.c_float, i32, C.c_uint32, P, P]
         _lib.or_sort.argtypes = [P, i32, P]
         _lib.or_profile.argtypes = [P, i64, i64, i32, C.POINTER(Prof)]
         _lib.or_prof_free.argtypes = [C.POINTER(Prof)]
@@ -124,13 +125,13 @@ def make_spec(cs=None, **kw) -> Spec:
     return Spec(**d)
 
 
-def build_proxies(xy, start, k=10, res=(1.0, 1.0)):
+def build_proxies(xy, start, k=10, res=(1.0, 1.0), flags=0):
     xy = np.ascontiguousarray(xy, dtype=np.float32)
     start = _i32(start)
     n = start.shape[0] - 1
     out = (Proxy * n)()
     bad = np.full(1, -1, dtype=np.int32)
-    st = lib().or_build_proxies(_ptr(xy), _ptr(start), n, res[0], res[1], k, out, _ptr(bad))
+    st = lib().or_build_proxies(_ptr(xy), _ptr(start), n, res[0], res[1], k, flags, out, _ptr(bad))
     return st, list(out), int(bad[0])
 
 

@@ -18,7 +18,8 @@
 #define OR_QMAX (1 << 24)          /* |snapped coordinate| bound, units */
 
 enum { OR_OK = 0, OR_EINVAL = 1, OR_NO_FIT = 2 };
-enum { OR_F_NO_HC = 1u, OR_F_NO_BALANCE = 2u, OR_F_ADJACENT_LOCKS_ONLY = 4u };
+enum { OR_F_NO_HC = 1u, OR_F_NO_BALANCE = 2u, OR_F_ADJACENT_LOCKS_ONLY = 4u,
+       OR_F_PREROTATE = 8u /* UV pre-rotation to the OBB angle (DESIGN R4) */ };
 
 /* Per-chart proxy in its final pre-packing pose ("two parallel passes
  * which compute our shape approximations ... and determine each chart's
@@ -32,6 +33,7 @@ typedef struct {
   int32_t top[OR_KMAX], bot[OR_KMAX];     /* merged x-slices (D4, D5) */
   int32_t left[OR_KMAX], right[OR_KMAX];  /* merged y-slices */
   int32_t obb_j;                          /* OBB angle index, theta = j*pi/16 */
+  int32_t prerot;                         /* pre-rotation angle index (R4), 0 if none */
   int64_t umin, umax, vmin, vmax;         /* OBB box in Q30-rotated frame */
 } or_proxy;
 
@@ -47,7 +49,7 @@ typedef struct {                 /* mirrors tabi_placement (include/tabi.h) */
   int32_t scale_num, scale_den;
   int32_t box_w, box_h;
   uint8_t rot90, flip_x, flip_y, mirror_x;
-  uint8_t mode, pad0, pad1, pad2;
+  uint8_t mode, prerot, pad1, pad2;
 } or_placement;
 
 typedef struct {
@@ -71,7 +73,7 @@ typedef struct {
 } or_info;
 
 int or_build_proxies(const float* xy, const int32_t* start, int32_t n, float res_x,
-                     float res_y, int32_t k, or_proxy* out, int32_t* bad_chart);
+                     float res_y, int32_t k, uint32_t flags, or_proxy* out, int32_t* bad_chart);
 void or_sort(const or_proxy* p, int32_t n, int32_t* perm);
 int or_profile(const or_proxy* p, int64_t num, int64_t den, int32_t g, or_prof* out);
 void or_prof_free(or_prof* pr);

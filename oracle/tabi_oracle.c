@@ -192,8 +192,48 @@ static void obb(const int64_t* X, const int64_t* Y, int nv, or_proxy* p) {
   }
 }
 
+/* ---- R4: pre-rotation ("We pre-rotate the UV charts to align their
+ * tight bounding boxes with the major axes prior to packing"
+ * "rotated by the negative of its approximate-OBB angle").  The angle is the
+ * D6 minimum-area angle of the snapped polygon; the rotated coordinates are
+ * the Q30 frame (u, v) = (x C + y S, -x S + y C) divided by 2^30, rounded
+ * half to even, so the pipeline continues on an integer polygon. ---------- */
+static int64_t q30_round(int64_t a) { /* round_half_even(a / 2^30) */
+  int64_t q = a >> 30;                 /* floor */
+  int64_t r = a - (q << 30);           /* in [0, 2^30) */
+  if (r > ((int64_t)1 << 29) || (r == ((int64_t)1 << 29) && (q & 1))) q++;
+  return q;
+}
+
+static int prerotate_angle(const int64_t* X, const int64_t* Y, int nv) {
+  i128 best = -1;
+  int bj = 0;
+  for (int j = 0; j < 8; j++) {
+    int64_t umin = INT64_MAX, umax = INT64_MIN, vmin = INT64_MAX, vmax = INT64_MIN;
+    for (int v = 0; v < nv; v++) {
+      int64_t u = X[v] * OR_QC[j] + Y[v] * OR_QS[j];
+      int64_t vv = -X[v] * OR_QS[j] + Y[v] * OR_QC[j];
+      umin = min64(umin, u); umax = max64(umax, u);
+      vmin = min64(vmin, vv); vmax = max64(vmax, vv);
+    }
+    i128 area = (i128)(umax - umin) * (i128)(vmax - vmin);
+    if (best < 0 || area < best) { best = area; bj = j; }  /* ties: smaller angle */
+  }
+  return bj;
+}
+
+static void prerotate(int64_t* X, int64_t* Y, int nv, int j) {
+  for (int v = 0; v < nv; v++) {
+    int64_t u = X[v] * OR_QC[j] + Y[v] * OR_QS[j];
+    int64_t vv = -X[v] * OR_QS[j] + Y[v] * OR_QC[j];
+    X[v] = q30_round(u);
+    Y[v] = q30_round(vv);
+  }
+}
+
 /* ---- A1-A5: one chart's proxy ------------------------------------------ */
-static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, or_proxy* p) {
+static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, int prerot_on,
+                       or_proxy* p) {
   memset(p, 0, sizeof(*p));
   if (nv < 3) return 0;
   int64_t* X = malloc(sizeof(int64_t) * nv);
@@ -201,6 +241,10 @@ static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, or_pr
   int ok = 1;
   for (int v = 0; v < nv && ok; v++) ok = snap(xy[2 * v], rx, &X[v]) && snap(xy[2 * v + 1], ry, &Y[v]);
   if (!ok) { free(X); free(Y); return 0; }
+  if (prerot_on) {
+    p->prerot = prerotate_angle(X, Y, nv);
+    if (p->prerot) prerotate(X, Y, nv, p->prerot);
+  }
   /* D3: AABB, translate to the origin ("compute the AABBs"). */
   int64_t xmin = X[0], xmax = X[0], ymin = Y[0], ymax = Y[0];
   for (int v = 1; v < nv; v++) {
@@ -250,12 +294,13 @@ static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, or_pr
 }
 
 int or_build_proxies(const float* xy, const int32_t* start, int32_t n, float res_x,
-                     float res_y, int32_t k, or_proxy* out, int32_t* bad_chart) {
+                     float res_y, int32_t k, uint32_t flags, or_proxy* out, int32_t* bad_chart) {
   *bad_chart = -1;
   if (n < 1 || k < 1 || k > OR_KMAX) return OR_EINVAL;
   for (int32_t c = 0; c < n; c++) {
     int nv = start[c + 1] - start[c];
-    if (!chart_proxy(xy + 2 * (int64_t)start[c], nv, res_x, res_y, k, &out[c])) {
+    if (!chart_proxy(xy + 2 * (int64_t)start[c], nv, res_x, res_y, k,
+                     (flags & OR_F_PREROTATE) != 0, &out[c])) {
       *bad_chart = c;
       return OR_EINVAL;
     }
@@ -824,6 +869,7 @@ int or_pack_candidate(const or_proxy* px, const int32_t* perm, int32_t n, const 
       o->box_w = tail ? pt[s].ws : pr[s].ws;
       o->box_h = tail ? pt[s].hs : pr[s].hs;
       o->rot90 = (uint8_t)px[c].rot90;
+      o->prerot = (uint8_t)px[c].prerot;
       o->flip_x = (uint8_t)px[c].fx;
       o->flip_y = (uint8_t)px[c].fy;
       o->mirror_x = mir[s];
@@ -849,7 +895,7 @@ static int spec_ok(const or_spec* s) {
   return s->atlas_w >= 1 && s->atlas_h >= 1 && s->atlas_w <= 16384 && s->atlas_h <= 16384 &&
          s->gutter >= 0 && s->gutter <= 64 && s->scale_count >= 1 && s->scale_count <= 256 &&
          s->local_aabb_count >= 1 && s->local_aabb_count <= OR_KMAX && s->t_opt_bp >= -1 &&
-         s->t_opt_bp <= 10000 && (s->flags & ~7u) == 0;
+         s->t_opt_bp <= 10000 && (s->flags & ~15u) == 0;
 }
 
 /* ---- scale search + output ("return the largest scale and
@@ -863,7 +909,8 @@ int or_pack(const float* xy, const int32_t* start, int32_t n, float res_x, float
     if (start[c + 1] - start[c] < 3) { info->bad_chart = c; return OR_EINVAL; }
   or_proxy* px = malloc(sizeof(or_proxy) * n);
   int32_t* perm = malloc(sizeof(int32_t) * n);
-  int st = or_build_proxies(xy, start, n, res_x, res_y, spec->local_aabb_count, px, &info->bad_chart);
+  int st = or_build_proxies(xy, start, n, res_x, res_y, spec->local_aabb_count, spec->flags, px,
+                            &info->bad_chart);
   if (st != OR_OK) { free(px); free(perm); return st; }
   or_sort(px, n, perm);
   const int32_t M = spec->scale_count;

@@ -28,6 +28,19 @@ static int vsnap(float v, float res, int64_t* q) {
   return 1;
 }
 
+/* Q30 cos / sin of j pi / 16 for the pre-rotation step. */
+static const int64_t V_QC[8] = {1073741824, 1053110176, 992008094, 892783698,
+                                759250125,  596538995,  410903207, 209476638};
+static const int64_t V_QS[8] = {0,         209476638, 410903207, 596538995,
+                                759250125, 892783698, 992008094, 1053110176};
+
+static int64_t v_q30_round(int64_t a) { /* round_half_even(a / 2^30) */
+  int64_t q = a >> 30;
+  int64_t r = a - (q << 30);
+  if (r > ((int64_t)1 << 29) || (r == ((int64_t)1 << 29) && (q & 1))) q++;
+  return q;
+}
+
 /* Placement transform documented in include/tabi.h (tabi_placement). */
 static int atlas_coords(const float* xy, int32_t nv, float rx, float ry, const or_placement* P,
                         int64_t* AX, int64_t* AY, int64_t* D) {
@@ -35,6 +48,12 @@ static int atlas_coords(const float* xy, int32_t nv, float rx, float ry, const o
   for (int32_t v = 0; v < nv; v++) {
     int64_t x, y;
     if (!vsnap(xy[2 * v], rx, &x) || !vsnap(xy[2 * v + 1], ry, &y)) return 0;
+    if (P->prerot) {  /* step 0: pre-rotation into the OBB frame, rounded (R4) */
+      const int64_t u = x * V_QC[P->prerot] + y * V_QS[P->prerot];
+      const int64_t t = -x * V_QS[P->prerot] + y * V_QC[P->prerot];
+      x = v_q30_round(u);
+      y = v_q30_round(t);
+    }
     AX[v] = x;
     AY[v] = y;
     if (v == 0 || x < xmin) xmin = x;

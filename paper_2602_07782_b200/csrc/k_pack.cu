@@ -1252,7 +1252,8 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 // K5: the largest successful m ("return the largest scale and packing
 // that succeed"), then every chart's placement in input order.
 __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
-                              const uint8_t* __restrict__ pose, const int32_t* __restrict__ wd_all,
+                              const uint8_t* __restrict__ pose, const uint8_t* __restrict__ prerot,
+                              const int32_t* __restrict__ wd_all,
                               const int32_t* __restrict__ hd_all, const int32_t* __restrict__ Xo,
                               const int32_t* __restrict__ Yo, const uint8_t* __restrict__ mir,
                               const Cand* __restrict__ cands, tabi_placement* out, Status* st) {
@@ -1307,7 +1308,8 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
   p.flip_y = (ps >> 2) & 1;
   p.mirror_x = mir[b];
   p.mode = tail ? 1 : 0;
-  p.pad[0] = p.pad[1] = p.pad[2] = 0;
+  p.prerot = prerot[c];
+  p.pad[0] = p.pad[1] = 0;
   out[c] = p;
 }
 
@@ -1377,7 +1379,7 @@ void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, 
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
                    const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s) {
   const int blocks = (pp.n + 255) / 256;
-  select_kernel<<<blocks, 256, 0, s>>>(pp, perm, P.pose, wd, hd, X, Y, mir, cands, out, st);
+  select_kernel<<<blocks, 256, 0, s>>>(pp, perm, P.pose, P.prerot, wd, hd, X, Y, mir, cands, out, st);
 }
 
 }  // namespace tabi

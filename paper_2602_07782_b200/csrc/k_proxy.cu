@@ -183,10 +183,58 @@ __device__ void merged_slices(const Group<G>& g, const Slices& S, const int32_t*
   g.sync();
 }
 
+// round_half_even(a / 2^30)
+__device__ __forceinline__ int64_t q30_round(int64_t a) {
+  int64_t q = a >> 30;  // floor
+  const int64_t r = a - (q << 30);
+  if (r > ((int64_t)1 << 29) || (r == ((int64_t)1 << 29) && (q & 1))) q++;
+  return q;
+}
+
+// D6's minimum-area angle (ties to the smaller j) of the group's polygon:
+// lane = (G / 8) * angle + vertex subgroup; the per-angle extents go through
+// S.ob and lane 0 picks.  Returns the same j in every lane.
+template <int G>
+__device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, int nv,
+                         const Slices& S) {
+  constexpr int VG = G / 8;
+  const int j = g.gl / VG, vg = g.gl % VG;
+  const int64_t C = kQC[j], Sn = kQS[j];
+  int64_t u0 = INT64_MAX, u1 = INT64_MIN, v0 = INT64_MAX, v1 = INT64_MIN;
+  for (int v = vg; v < nv; v += VG) {
+    const int64_t x = X[v], y = Y[v];
+    const int64_t u = x * C + y * Sn, vv = -x * Sn + y * C;
+    u0 = u < u0 ? u : u0; u1 = u > u1 ? u : u1;
+    v0 = vv < v0 ? vv : v0; v1 = vv > v1 ? vv : v1;
+  }
+#pragma unroll
+  for (int o = 1; o < VG; o <<= 1) {
+    int64_t t = g.xorv(u0, o); u0 = t < u0 ? t : u0;
+    t = g.xorv(u1, o); u1 = t > u1 ? t : u1;
+    t = g.xorv(v0, o); v0 = t < v0 ? t : v0;
+    t = g.xorv(v1, o); v1 = t > v1 ? t : v1;
+  }
+  if (vg == 0) {
+    S.ob[4 * j + 0] = u0; S.ob[4 * j + 1] = u1; S.ob[4 * j + 2] = v0; S.ob[4 * j + 3] = v1;
+  }
+  g.sync();
+  int bj = 0;
+  if (g.gl == 0) {
+    i128 best = -1;
+    for (int a = 0; a < 8; a++) {
+      const i128 area = (i128)(S.ob[4 * a + 1] - S.ob[4 * a]) * (i128)(S.ob[4 * a + 3] - S.ob[4 * a + 2]);
+      if (best < 0 || area < best) { best = area; bj = a; }
+    }
+  }
+  bj = __shfl_sync(g.mask, bj, 0, G);
+  g.sync();  // S.ob is reused
+  return bj;
+}
+
 template <int G>
 __global__ void __launch_bounds__(kBlock)
 proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
-             float ry, int k, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
+             float ry, int k, bool prerot_on, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, gib = threadIdx.x / G;
   Group<G> g;
@@ -233,6 +281,27 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   if (__ballot_sync(g.mask, !ok) != 0u) {
     if (gl == 0) atomicMin(&st->bad_chart, c);
     return;
+  }
+  int prerot = 0;
+  if (prerot_on) {
+    // R4 pre-rotation (TABI_F_PREROTATE): the D6 minimum-area angle
+    // of the snapped polygon, then every vertex moves to that OBB frame,
+    // rounded half to even to 1/256 texel (tabi_placement step 0).
+    g.sync();
+    prerot = obb_angle(g, X, Y, nv, S);
+    if (prerot) {
+      const int64_t C = kQC[prerot], Sn = kQS[prerot];
+      xmn = INT32_MAX; xmx = INT32_MIN; ymn = INT32_MAX; ymx = INT32_MIN;
+      for (int v = gl; v < nv; v += G) {
+        const int64_t x = X[v], y = Y[v];
+        const int32_t u = (int32_t)q30_round(x * C + y * Sn);
+        const int32_t t = (int32_t)q30_round(-x * Sn + y * C);
+        X[v] = u;
+        Y[v] = t;
+        xmn = min(xmn, u); xmx = max(xmx, u);
+        ymn = min(ymn, t); ymx = max(ymx, t);
+      }
+    }
   }
   xmn = g.min32(xmn); xmx = g.max32(xmx);
   ymn = g.min32(ymn); ymx = g.max32(ymx);
@@ -338,44 +407,16 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     sl[3 * k + j] = S.mhi1[j];
   }
   // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j.
-  // All 8 angles at once: lane = (G / 8) * angle + vertex subgroup, so each
-  // angle's extents reduce over G / 8 lanes only.
-  {
-    constexpr int VG = G / 8;  // lanes per angle
-    const int j = gl / VG, vg = gl % VG;
-    const int64_t C = kQC[j], Sn = kQS[j];
-    int64_t u0 = INT64_MAX, u1 = INT64_MIN, v0 = INT64_MAX, v1 = INT64_MIN;
-    for (int v = vg; v < nv; v += VG) {
-      const int64_t x = X[v], y = Y[v];
-      const int64_t u = x * C + y * Sn, vv = -x * Sn + y * C;
-      u0 = u < u0 ? u : u0; u1 = u > u1 ? u : u1;
-      v0 = vv < v0 ? vv : v0; v1 = vv > v1 ? vv : v1;
-    }
-#pragma unroll
-    for (int o = 1; o < VG; o <<= 1) {
-      int64_t t = g.xorv(u0, o); u0 = t < u0 ? t : u0;
-      t = g.xorv(u1, o); u1 = t > u1 ? t : u1;
-      t = g.xorv(v0, o); v0 = t < v0 ? t : v0;
-      t = g.xorv(v1, o); v1 = t > v1 ? t : v1;
-    }
-    if (vg == 0) {
-      S.ob[4 * j + 0] = u0; S.ob[4 * j + 1] = u1; S.ob[4 * j + 2] = v0; S.ob[4 * j + 3] = v1;
-    }
-    g.sync();
-  }
+  g.sync();
+  const int bj = obb_angle(g, X, Y, nv, S);
   if (gl == 0) {
-    i128 best = -1;
-    int bj = 0;
-    for (int j = 0; j < 8; j++) {
-      const i128 area = (i128)(S.ob[4 * j + 1] - S.ob[4 * j]) * (i128)(S.ob[4 * j + 3] - S.ob[4 * j + 2]);
-      if (best < 0 || area < best) { best = area; bj = j; }
-    }
     P.w[c] = (int32_t)w;
     P.h[c] = (int32_t)h;
     P.area2[c] = (int64_t)s2;
     P.xmin[c] = xmn;
     P.ymin[c] = ymn;
     P.pose[c] = (uint8_t)((rot ? 1 : 0) | (fx ? 2 : 0) | (fy ? 4 : 0));
+    P.prerot[c] = (uint8_t)prerot;
     P.obb_j[c] = bj;
     P.obb[4 * (int64_t)c + 0] = S.ob[4 * bj + 0];
     P.obb[4 * (int64_t)c + 1] = S.ob[4 * bj + 1];
@@ -386,7 +427,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
 
 template <int G>
 void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-              int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+              bool prerot, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
   constexpr int per_block = kBlock / G;
   const int blocks = (n + per_block - 1) / per_block;
   const size_t smem = slice_bytes(k) * per_block;
@@ -396,20 +437,20 @@ void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float 
                          (int)(slice_bytes(TABI_KMAX) * per_block));
     attr = true;
   }
-  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, qx, qy, P, st);
+  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st);
 }
 
 }  // namespace
 
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-                    int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+                    bool prerot, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
   const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
   const int forced = genv ? atoi(genv) : 0;
   const int G = forced == 8 || forced == 16 || forced == 32 ? forced
                 : n < 4096 ? 32 : n < 8192 ? 16 : 8;  // measured: C3 (1572) 32, C4 (20000) 8
-  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, qx, qy, P, st, s);
-  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, qx, qy, P, st, s);
-  else launch_g<8>(xy, start, n, rx, ry, k, qx, qy, P, st, s);
+  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st, s);
+  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st, s);
+  else launch_g<8>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st, s);
 }
 
 }  // namespace tabi

@@ -133,7 +133,7 @@ static cudaError_t dalloc(T** p, size_t count) {
 
 static void dfree_all(tabi_ctx* ctx) {
   void* ps[] = {ctx->d_xy, ctx->d_start, ctx->d_qx, ctx->d_qy, ctx->P.w, ctx->P.h, ctx->P.area2,
-                ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
+                ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.prerot, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
                 ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
                 ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->rdy, ctx->tstart, ctx->tix, ctx->X, ctx->Y, ctx->mir,
@@ -186,6 +186,7 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
             dalloc(&ctx->P.w, N) == cudaSuccess && dalloc(&ctx->P.h, N) == cudaSuccess &&
             dalloc(&ctx->P.area2, N) == cudaSuccess && dalloc(&ctx->P.xmin, N) == cudaSuccess &&
             dalloc(&ctx->P.ymin, N) == cudaSuccess && dalloc(&ctx->P.pose, N) == cudaSuccess &&
+            dalloc(&ctx->P.prerot, N) == cudaSuccess &&
             dalloc(&ctx->P.sl, N * 4 * TABI_KMAX) == cudaSuccess &&
             dalloc(&ctx->P.obb_j, N) == cudaSuccess && dalloc(&ctx->P.obb, 4 * N) == cudaSuccess &&
             dalloc(&ctx->keys, N) == cudaSuccess && dalloc(&ctx->keys2, N) == cudaSuccess &&
@@ -268,7 +269,7 @@ static bool spec_ok(const tabi_spec* s) {
          s->atlas_h <= TABI_MAX_ATLAS_SIDE && s->gutter >= 0 && s->gutter <= 64 &&
          s->scale_count >= 1 && s->scale_count <= TABI_MAX_SCALES && s->local_aabb_count >= 1 &&
          s->local_aabb_count <= TABI_MAX_LOCAL_AABBS && s->t_opt_bp >= -1 &&
-         s->t_opt_bp <= 10000 && (s->flags & ~7u) == 0;
+         s->t_opt_bp <= 10000 && (s->flags & ~15u) == 0;
 }
 
 namespace {
@@ -421,8 +422,8 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
                  nrdy, s);
     nl++;
     if (prologue) {
-      launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, ctx->d_qx, ctx->d_qy, ctx->P,
-                     ctx->d_status, s);
+      launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, (pp.flags & TABI_F_PREROTATE) != 0,
+                     ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
       nl++;
       tm.mark(s);
       nl += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
@@ -683,6 +684,8 @@ extern "C" tabi_status tabi_debug_proxies(tabi_ctx* ctx, tabi_proxy_dbg* out) {
   int32_t *oj = new int32_t[n], *sl = new int32_t[(size_t)n * 4 * k];
   int64_t *a2 = new int64_t[n], *ob = new int64_t[4 * (size_t)n];
   uint8_t* pose = new uint8_t[n];
+  uint8_t* pre = new uint8_t[n];
+  cudaMemcpy(pre, ctx->P.prerot, n, cudaMemcpyDeviceToHost);
   cudaMemcpy(w, ctx->P.w, 4 * n, cudaMemcpyDeviceToHost);
   cudaMemcpy(h, ctx->P.h, 4 * n, cudaMemcpyDeviceToHost);
   cudaMemcpy(xm, ctx->P.xmin, 4 * n, cudaMemcpyDeviceToHost);
@@ -704,10 +707,11 @@ extern "C" tabi_status tabi_debug_proxies(tabi_ctx* ctx, tabi_proxy_dbg* out) {
       d.right[j] = sl[(size_t)c * 4 * k + 3 * k + j];
     }
     d.obb_j = oj[c];
+    d.prerot = pre[c];
     d.umin = ob[4 * c]; d.umax = ob[4 * c + 1]; d.vmin = ob[4 * c + 2]; d.vmax = ob[4 * c + 3];
   }
   delete[] w; delete[] h; delete[] xm; delete[] ym; delete[] oj; delete[] sl;
-  delete[] a2; delete[] ob; delete[] pose;
+  delete[] a2; delete[] ob; delete[] pose; delete[] pre;
   CK(cudaGetLastError());
   return TABI_OK;
 }

@@ -284,6 +284,7 @@ struct Proxies {
   int32_t* xmin;
   int32_t* ymin;
   uint8_t* pose;     // bit0 rot90, bit1 fx, bit2 fy
+  uint8_t* prerot;   // pre-rotation angle index (TABI_F_PREROTATE), 0 = none
   int32_t* sl;
   int32_t* obb_j;
   int64_t* obb;      // [c*4 + {umin, umax, vmin, vmax}]
@@ -385,7 +386,7 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
 // Launch wrappers (defined in the .cu files)
 namespace tabi {
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-                    int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
+                    bool prerot, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
 // Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
 void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
                   int32_t* rdy, int64_t nrdy, cudaStream_t s);

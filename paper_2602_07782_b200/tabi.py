@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtabi.so")
 
 OK, EINVAL, NO_FIT, ECUDA, ECAPACITY = 0, 1, 2, 3, 4
-F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY = 1, 2, 4
+F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE = 1, 2, 4, 8
 STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "no candidate scale fits", 3: "CUDA error",
                 4: "capacity exceeded"}
 
@@ -48,14 +48,15 @@ class Info(C.Structure):
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
                             ("scale_den", "<i4"), ("box_w", "<i4"), ("box_h", "<i4"),
                             ("rot90", "u1"), ("flip_x", "u1"), ("flip_y", "u1"),
-                            ("mirror_x", "u1"), ("mode", "u1"), ("pad", "u1", (3,))])
+                            ("mirror_x", "u1"), ("mode", "u1"), ("prerot", "u1"),
+                            ("pad", "u1", (2,))])
 assert PLACEMENT_DTYPE.itemsize == 32
 
 PROXY_DTYPE = np.dtype([("w", "<i4"), ("h", "<i4"), ("area2", "<i8"), ("xmin", "<i4"),
                         ("ymin", "<i4"), ("rot90", "<i4"), ("fx", "<i4"), ("fy", "<i4"),
                         ("k", "<i4"), ("top", "<i4", (64,)), ("bot", "<i4", (64,)),
                         ("left", "<i4", (64,)), ("right", "<i4", (64,)), ("obb_j", "<i4"),
-                        ("reserved", "<i4"), ("umin", "<i8"), ("umax", "<i8"), ("vmin", "<i8"),
+                        ("prerot", "<i4"), ("umin", "<i8"), ("umax", "<i8"), ("vmin", "<i8"),
                         ("vmax", "<i8")])
 CAND_DTYPE = np.dtype([(f, "<i4") for f in ("success", "score", "rows", "knees_found",
                                             "knee_rows", "prefix_rows", "p", "evaluated",

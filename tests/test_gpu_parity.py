@@ -13,8 +13,8 @@ import chartgen
 
 pytestmark = pytest.mark.gpu
 
-PROXY_FIELDS = ("w", "h", "area2", "xmin", "ymin", "rot90", "fx", "fy", "obb_j", "umin", "umax",
-                "vmin", "vmax")
+PROXY_FIELDS = ("w", "h", "area2", "xmin", "ymin", "rot90", "fx", "fy", "obb_j", "prerot", "umin",
+                "umax", "vmin", "vmax")
 
 
 @pytest.fixture(scope="module")
@@ -41,7 +41,7 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
     k = kw.get("local_aabb_count", cs.local_aabb_count)
     g = kw.get("gutter", cs.gutter)
     # proxies (D3-D8) bit-exact
-    st, px, _ = oracle.build_proxies(cs.xy, cs.start, k, res)
+    st, px, _ = oracle.build_proxies(cs.xy, cs.start, k, res, flags=kw.get("flags", 0))
     gp = ctx.proxies(n)
     for f in PROXY_FIELDS:
         assert np.array_equal(gp[f], np.array([getattr(p, f) for p in px])), f
@@ -69,7 +69,7 @@ def _compare_pack(orc, ctx, cs, res=(1.0, 1.0), check_profiles=0, **kw):
                 assert gc[f][m - 1] == getattr(co, f), (m, f)
     # placements bit-exact, scale/stretch
     for f in ("tx", "ty", "scale_num", "scale_den", "box_w", "box_h", "rot90", "flip_x", "flip_y",
-              "mirror_x", "mode"):
+              "mirror_x", "mode", "prerot"):
         assert np.array_equal(pl_g[f], pl_o[f]), f
     assert info_g.scale_index == info_o.scale_index
     assert info_g.l2_stretch == pytest.approx(info_o.l2_stretch, rel=1e-6)
@@ -150,6 +150,24 @@ def test_quality_knob_parity(orc, ctx, k):
 def test_spec_variants_parity(orc, ctx, kw):
     _compare_pack(orc, ctx, chartgen.small_case(5, n=50, family="mixed", rho=0.8),
                   check_profiles=3, **kw)
+
+
+PREROT = ([chartgen.small_case(s, n=48, family="uv") for s in range(3)] +
+          [chartgen.small_case(s, n=300, family="tss", side=512, rho=0.6) for s in range(2)] +
+          [chartgen.config2(0), chartgen.config3(0)])
+
+
+@pytest.mark.parametrize("cs", PREROT, ids=lambda c: c.name)
+def test_prerotate_parity(orc, ctx, cs):
+    """R4 pre-rotation (TABI_F_PREROTATE): angle, rotated proxies, order,
+    candidates and placements (prerot included) bit-exact; the packing is valid
+    under the validator, which applies step 0 to the original outlines."""
+    import oracle
+    from paper_2602_07782_b200 import F_PREROTATE, spec_of
+    _compare_pack(orc, ctx, cs, check_profiles=4, flags=F_PREROTATE)
+    _, pl, _ = ctx.pack(cs.xy, cs.start, spec_of(cs, flags=F_PREROTATE))
+    assert (pl["prerot"] > 0).any()
+    assert oracle.validate(cs, pl) == {"overlap": 0, "gutter": 0, "oob": 0}
 
 
 def test_unsnapped_input_with_resolution(orc, ctx):
