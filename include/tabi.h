@@ -38,16 +38,19 @@ enum {
   TABI_F_NO_HC = 1u,                 /* ablation: never compact horizontally */
   TABI_F_NO_BALANCE = 2u,            /* ablation: no knees, static L/R alternation    */
   TABI_F_ADJACENT_LOCKS_ONLY = 4u,   /* paper-literal Alg. 1 (adjacent pairs only)    */
-  TABI_F_PREROTATE = 8u              /* UV pre-rotation to the OBB angle (for UV
+  TABI_F_PREROTATE = 8u,             /* UV pre-rotation to the OBB angle (for UV
                                         charts, not TSS -- rotation by non-90-degree angles
                                         resamples the texture); see tabi_placement step 0 */
+  TABI_F_NO_OBB = 16u                /* ablation: no OBB bound on the footprints (D6/D11);
+                                        with local_aabb_count = 1 the proxy is the plain AABB
+                                        (Chameleon / balanced-only) */
 };
 
 typedef struct tabi_ctx tabi_ctx;    /* opaque: device workspace + stream, one per host thread */
 
 /* Atlas + knobs (SPEC AtlasSpec S:33-36).  Invariants, else TABI_EINVAL:
  *   1 <= atlas_w, atlas_h <= 16384;  0 <= gutter <= 64;  1 <= scale_count <= 256;
- *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_* (0..15). */
+ *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_* (0..31). */
 typedef struct {
   int32_t atlas_w, atlas_h;   /* texels */
   int32_t gutter;             /* texels around every chart, none at atlas edges; paper 1 */

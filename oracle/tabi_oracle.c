@@ -173,9 +173,9 @@ static void orientation(int k, int64_t w, int64_t h, const int32_t* top, const i
 }
 
 /* ---- D6: approximate OBB. -------------------------------- */
-static void obb(const int64_t* X, const int64_t* Y, int nv, or_proxy* p) {
+static void obb(const int64_t* X, const int64_t* Y, int nv, int nj, or_proxy* p) {
   i128 best = -1;
-  for (int j = 0; j < 8; j++) {
+  for (int j = 0; j < nj; j++) { /* nj = 1 under OR_F_NO_OBB: the AABB (j = 0) */
     int64_t umin = INT64_MAX, umax = INT64_MIN, vmin = INT64_MAX, vmax = INT64_MIN;
     for (int v = 0; v < nv; v++) {
       int64_t u = X[v] * OR_QC[j] + Y[v] * OR_QS[j];
@@ -232,8 +232,9 @@ static void prerotate(int64_t* X, int64_t* Y, int nv, int j) {
 }
 
 /* ---- A1-A5: one chart's proxy ------------------------------------------ */
-static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, int prerot_on,
+static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, uint32_t flags,
                        or_proxy* p) {
+  const int prerot_on = (flags & OR_F_PREROTATE) != 0;
   memset(p, 0, sizeof(*p));
   if (nv < 3) return 0;
   int64_t* X = malloc(sizeof(int64_t) * nv);
@@ -287,7 +288,7 @@ static int chart_proxy(const float* xy, int nv, float rx, float ry, int k, int p
     if (p->fy) Y[v] = h - Y[v];
   }
   merged_slices(X, Y, nv, w, h, k, p->top, p->bot, p->left, p->right);
-  obb(X, Y, nv, p);
+  obb(X, Y, nv, (flags & OR_F_NO_OBB) ? 1 : 8, p);
   free(X);
   free(Y);
   return 1;
@@ -299,8 +300,7 @@ int or_build_proxies(const float* xy, const int32_t* start, int32_t n, float res
   if (n < 1 || k < 1 || k > OR_KMAX) return OR_EINVAL;
   for (int32_t c = 0; c < n; c++) {
     int nv = start[c + 1] - start[c];
-    if (!chart_proxy(xy + 2 * (int64_t)start[c], nv, res_x, res_y, k,
-                     (flags & OR_F_PREROTATE) != 0, &out[c])) {
+    if (!chart_proxy(xy + 2 * (int64_t)start[c], nv, res_x, res_y, k, flags, &out[c])) {
       *bad_chart = c;
       return OR_EINVAL;
     }
@@ -895,7 +895,7 @@ static int spec_ok(const or_spec* s) {
   return s->atlas_w >= 1 && s->atlas_h >= 1 && s->atlas_w <= 16384 && s->atlas_h <= 16384 &&
          s->gutter >= 0 && s->gutter <= 64 && s->scale_count >= 1 && s->scale_count <= 256 &&
          s->local_aabb_count >= 1 && s->local_aabb_count <= OR_KMAX && s->t_opt_bp >= -1 &&
-         s->t_opt_bp <= 10000 && (s->flags & ~15u) == 0;
+         s->t_opt_bp <= 10000 && (s->flags & ~31u) == 0;
 }
 
 /* ---- scale search + output ("return the largest scale and

@@ -196,7 +196,7 @@ __device__ __forceinline__ int64_t q30_round(int64_t a) {
 // S.ob and lane 0 picks.  Returns the same j in every lane.
 template <int G>
 __device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, int nv,
-                         const Slices& S) {
+                         const Slices& S, int nj = 8) {
   constexpr int VG = G / 8;
   const int j = g.gl / VG, vg = g.gl % VG;
   const int64_t C = kQC[j], Sn = kQS[j];
@@ -221,7 +221,7 @@ __device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, 
   int bj = 0;
   if (g.gl == 0) {
     i128 best = -1;
-    for (int a = 0; a < 8; a++) {
+    for (int a = 0; a < nj; a++) {
       const i128 area = (i128)(S.ob[4 * a + 1] - S.ob[4 * a]) * (i128)(S.ob[4 * a + 3] - S.ob[4 * a + 2]);
       if (best < 0 || area < best) { best = area; bj = a; }
     }
@@ -234,7 +234,7 @@ __device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, 
 template <int G>
 __global__ void __launch_bounds__(kBlock)
 proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
-             float ry, int k, bool prerot_on, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
+             float ry, int k, uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, gib = threadIdx.x / G;
   Group<G> g;
@@ -283,7 +283,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     return;
   }
   int prerot = 0;
-  if (prerot_on) {
+  if (flags & TABI_F_PREROTATE) {
     // R4 pre-rotation (TABI_F_PREROTATE): the D6 minimum-area angle
     // of the snapped polygon, then every vertex moves to that OBB frame,
     // rounded half to even to 1/256 texel (tabi_placement step 0).
@@ -408,7 +408,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   }
   // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j.
   g.sync();
-  const int bj = obb_angle(g, X, Y, nv, S);
+  const int bj = obb_angle(g, X, Y, nv, S, (flags & TABI_F_NO_OBB) ? 1 : 8);
   if (gl == 0) {
     P.w[c] = (int32_t)w;
     P.h[c] = (int32_t)h;
@@ -427,7 +427,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
 
 template <int G>
 void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-              bool prerot, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+              uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
   constexpr int per_block = kBlock / G;
   const int blocks = (n + per_block - 1) / per_block;
   const size_t smem = slice_bytes(k) * per_block;
@@ -437,20 +437,20 @@ void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float 
                          (int)(slice_bytes(TABI_KMAX) * per_block));
     attr = true;
   }
-  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st);
+  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, flags, qx, qy, P, st);
 }
 
 }  // namespace
 
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-                    bool prerot, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+                    uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
   const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
   const int forced = genv ? atoi(genv) : 0;
   const int G = forced == 8 || forced == 16 || forced == 32 ? forced
                 : n < 4096 ? 32 : n < 8192 ? 16 : 8;  // measured: C3 (1572) 32, C4 (20000) 8
-  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st, s);
-  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st, s);
-  else launch_g<8>(xy, start, n, rx, ry, k, prerot, qx, qy, P, st, s);
+  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, P, st, s);
+  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, P, st, s);
+  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, P, st, s);
 }
 
 }  // namespace tabi

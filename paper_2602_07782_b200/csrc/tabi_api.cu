@@ -269,7 +269,7 @@ static bool spec_ok(const tabi_spec* s) {
          s->atlas_h <= TABI_MAX_ATLAS_SIDE && s->gutter >= 0 && s->gutter <= 64 &&
          s->scale_count >= 1 && s->scale_count <= TABI_MAX_SCALES && s->local_aabb_count >= 1 &&
          s->local_aabb_count <= TABI_MAX_LOCAL_AABBS && s->t_opt_bp >= -1 &&
-         s->t_opt_bp <= 10000 && (s->flags & ~15u) == 0;
+         s->t_opt_bp <= 10000 && (s->flags & ~31u) == 0;
 }
 
 namespace {
@@ -422,7 +422,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
                  nrdy, s);
     nl++;
     if (prologue) {
-      launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, (pp.flags & TABI_F_PREROTATE) != 0,
+      launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
                      ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
       nl++;
       tm.mark(s);

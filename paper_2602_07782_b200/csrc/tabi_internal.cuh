@@ -386,7 +386,7 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
 // Launch wrappers (defined in the .cu files)
 namespace tabi {
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-                    bool prerot, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
+                    uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
 // Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
 void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
                   int32_t* rdy, int64_t nrdy, cudaStream_t s);

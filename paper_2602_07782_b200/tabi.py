@@ -20,7 +20,20 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtabi.so")
 
 OK, EINVAL, NO_FIT, ECUDA, ECAPACITY = 0, 1, 2, 3, 4
-F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE = 1, 2, 4, 8
+F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE, F_NO_OBB = 1, 2, 4, 8, 16
+# Ablation / baseline modes on the same kernels (the ablation table after
+# P:1060): spec overrides for spec_of(cs, **ABLATIONS[name]).
+#   tight_only    = horizontal + vertical compacting, no balance (no knees,
+#                   static L/R alternation);
+#   balanced_only = balance without tightening: plain AABB proxies (k = 1, no
+#                   OBB bound), no horizontal compacting;
+#   chameleon     = Chameleon: AABBs, fold + push, strict alternation.
+ABLATIONS = {
+    "tabi": dict(flags=0),
+    "tight_only": dict(flags=F_NO_BALANCE),
+    "balanced_only": dict(flags=F_NO_HC | F_NO_OBB, local_aabb_count=1),
+    "chameleon": dict(flags=F_NO_HC | F_NO_BALANCE | F_NO_OBB, local_aabb_count=1),
+}
 STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "no candidate scale fits", 3: "CUDA error",
                 4: "capacity exceeded"}
 

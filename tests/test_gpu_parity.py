@@ -145,7 +145,8 @@ def test_quality_knob_parity(orc, ctx, k):
 
 @pytest.mark.parametrize("kw", [dict(gutter=0), dict(gutter=3), dict(scale_count=1),
                                 dict(scale_count=17), dict(scale_count=256),
-                                dict(flags=1), dict(flags=2), dict(flags=4)],
+                                dict(flags=1), dict(flags=2), dict(flags=4), dict(flags=16),
+                                dict(flags=16, local_aabb_count=1)],
                          ids=lambda d: "-".join(f"{a}{b}" for a, b in d.items()))
 def test_spec_variants_parity(orc, ctx, kw):
     _compare_pack(orc, ctx, chartgen.small_case(5, n=50, family="mixed", rho=0.8),
@@ -168,6 +169,17 @@ def test_prerotate_parity(orc, ctx, cs):
     _, pl, _ = ctx.pack(cs.xy, cs.start, spec_of(cs, flags=F_PREROTATE))
     assert (pl["prerot"] > 0).any()
     assert oracle.validate(cs, pl) == {"overlap": 0, "gutter": 0, "oob": 0}
+
+
+@pytest.mark.parametrize("mode", ["tight_only", "balanced_only", "chameleon"])
+@pytest.mark.parametrize("cs", [chartgen.config2(1),
+                                chartgen.small_case(0, n=300, family="tss", side=512, rho=0.6)],
+                         ids=lambda c: c.name)
+def test_ablation_modes_parity(orc, ctx, cs, mode):
+    """the paper's ablation / baseline modes run on the
+    same kernels, bit-exact against the oracle."""
+    from paper_2602_07782_b200 import ABLATIONS
+    _compare_pack(orc, ctx, cs, check_profiles=4, **ABLATIONS[mode])
 
 
 def test_unsnapped_input_with_resolution(orc, ctx):
