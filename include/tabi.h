@@ -155,6 +155,45 @@ tabi_status tabi_pack_batch(tabi_ctx* const* ctxs, int32_t n_gpus, int32_t n_atl
                             const int32_t* n_charts, const float* res_xy, const tabi_spec* specs,
                             tabi_placement* const* out, tabi_info* infos);
 
+/* ---- validation and metrics on the GPU ----
+ * P:85 / P:353: "texels covered by two or more charts ... with 1 pixel gutter
+ * dilation"; S:545-553 fix the conservative raster rule: texel (i, r) is
+ * covered by chart c iff the OPEN square (i, i+1) x (r, r+1) meets the closed
+ * outline of c mapped by placements[c] (tabi_placement steps 0-6, exact
+ * integer arithmetic).  Counts:
+ *   overlap  atlas texels covered by >= 2 charts;
+ *   gutter   atlas texels covered by >= 2 charts after a Chebyshev dilation of
+ *            each chart's in-atlas coverage by `gutter` texels (atlas edges
+ *            exempt);
+ *   oob      covered texels outside [0, atlas_w) x [0, atlas_h);
+ *   covered  atlas texels covered by >= 1 chart; occupancy = covered / (W H).
+ * l2_stretch: every chart map is a similarity of scale
+ * s_c = scale_num / scale_den, so per-triangle stretch is 1/s_c and the
+ * area-weighted RMS is sqrt(sum_c A_c / s_c^2 / sum_c A_c), A_c the area of the
+ * snapped outline (before step 0).  Deterministic. */
+typedef struct {
+  int64_t overlap, gutter, oob, covered;
+  double occupancy, l2_stretch;
+  int32_t bad_chart;     /* on TABI_EINVAL: first chart whose outline does not snap
+                            (|coord * res| * 256 > 2^24, non-finite, < 3 vertices) or
+                            whose placement is malformed (scale <= 0, prerot > 7); else -1 */
+  int32_t gpu_launches;  /* kernels launched by this call */
+} tabi_validation;
+
+/* Validate n_charts placements (e.g. the `out` of a tabi_pack) against their
+ * outlines.  xy / chart_start / res as for tabi_pack; placements n_charts
+ * entries.  on_device 0: host pointers (copied in); 1: device pointers.
+ * Device scratch is one byte per texel of every chart's g-dilated texel box
+ * plus 2 bits per atlas texel; it grows on demand and is kept on ctx.  Returns
+ * TABI_EINVAL on bad arguments (atlas side outside [1, 65536], gutter outside
+ * [0, 64], n_charts < 1 or above the context's max_charts), TABI_ECUDA on a
+ * CUDA error.  Independent of the last tabi_pack (its introspection state is
+ * untouched). */
+tabi_status tabi_validate(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                          int32_t n_charts, float res_x, float res_y, int32_t atlas_w,
+                          int32_t atlas_h, int32_t gutter, const tabi_placement* placements,
+                          tabi_validation* out, int on_device, void* stream);
+
 /* ---- introspection of the last tabi_pack on ctx (parity tests; host outputs) ---- */
 
 /* Final-pose proxy of one chart, 1088 bytes (D3-D8 of SURVEY.md §8(c)). */

@@ -268,7 +268,7 @@ def validate(cs, placements, res=(1.0, 1.0), gutter=None):
     xy = np.ascontiguousarray(cs.xy, dtype=np.float32)
     start = _i32(cs.start)
     n = start.shape[0] - 1
-    counts = np.zeros(3, dtype=np.int64)
+    counts = np.zeros(4, dtype=np.int64)
     pl = np.ascontiguousarray(placements, dtype=PLACEMENT_DTYPE)
     g = cs.gutter if gutter is None else gutter
     ok = lib().or_validate(_ptr(xy), _ptr(start), n, res[0], res[1], cs.atlas_w, cs.atlas_h, g,
@@ -276,6 +276,43 @@ def validate(cs, placements, res=(1.0, 1.0), gutter=None):
     if not ok:
         raise RuntimeError("validator could not snap input")
     return {"overlap": int(counts[0]), "gutter": int(counts[1]), "oob": int(counts[2])}
+
+
+def metrics(cs, placements, res=(1.0, 1.0), gutter=None):
+    """Validator counts plus the atlas metrics:
+    covered texels, occupancy = covered / (W H), and the L2 stretch
+    (P:1027-1028): each chart map is a similarity of scale
+    s_c = scale_num / scale_den, every triangle's stretch is 1/s_c, so the
+    area-weighted RMS is sqrt(sum A_c / s_c^2 / sum A_c), A_c the snapped
+    outline area (exact rationals here, one rounding at the end)."""
+    from fractions import Fraction
+    import math
+    xy = np.ascontiguousarray(cs.xy, dtype=np.float32)
+    start = _i32(cs.start)
+    n = start.shape[0] - 1
+    counts = np.zeros(4, dtype=np.int64)
+    pl = np.ascontiguousarray(placements, dtype=PLACEMENT_DTYPE)
+    g = cs.gutter if gutter is None else gutter
+    ok = lib().or_validate(_ptr(xy), _ptr(start), n, res[0], res[1], cs.atlas_w, cs.atlas_h, g,
+                           _ptr(pl), _ptr(counts))
+    if not ok:
+        raise RuntimeError("validator could not snap input")
+    num = Fraction(0)
+    den = 0
+    for c in range(n):
+        a, b = int(start[c]), int(start[c + 1])
+        q = np.rint(xy[2 * a:2 * b].astype(np.float64).reshape(-1, 2) *
+                    np.array([res[0], res[1]]) * 256.0).astype(np.int64)
+        x, y = q[:, 0].tolist(), q[:, 1].tolist()
+        a2 = abs(sum(x[i] * y[(i + 1) % len(x)] - x[(i + 1) % len(x)] * y[i]
+                     for i in range(len(x))))
+        s = Fraction(int(pl["scale_num"][c]), int(pl["scale_den"][c]))
+        num += Fraction(a2) / (s * s)
+        den += a2
+    return {"overlap": int(counts[0]), "gutter": int(counts[1]), "oob": int(counts[2]),
+            "covered": int(counts[3]),
+            "occupancy": int(counts[3]) / (cs.atlas_w * cs.atlas_h),
+            "l2_stretch": math.sqrt(num / den)}
 
 
 def raster_chart(poly_xy, placement, x0, y0, nx, ny, res=(1.0, 1.0)):

@@ -94,7 +94,7 @@ int or_pack(const float* xy, const int32_t* start, int32_t n, float res_x, float
             const or_spec* spec, or_placement* out, or_info* info, or_cand* cands);
 int or_validate(const float* xy, const int32_t* start, int32_t n, float res_x, float res_y,
                 int32_t atlas_w, int32_t atlas_h, int32_t gutter, const or_placement* pl,
-                int64_t* counts /* [overlap, gutter_violation, out_of_bounds] */);
+                int64_t* counts /* [overlap, gutter_violation, out_of_bounds, covered] */);
 int or_raster_chart(const float* xy, int32_t nv, float res_x, float res_y,
                     const or_proxy* p, const or_placement* pl, int32_t x0, int32_t y0,
                     int32_t nx, int32_t ny, uint8_t* mask);

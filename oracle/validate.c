@@ -11,7 +11,8 @@
  *   overlap    texels covered by >= 2 charts,
  *   gutter     texels covered by >= 2 charts after a g-Chebyshev dilation of
  *              each chart's coverage (atlas edges exempt),
- *   oob        covered texels outside [0, W) x [0, H).
+ *   oob        covered texels outside [0, W) x [0, H),
+ *   covered    atlas texels covered by >= 1 chart (occupancy metric).
  */
 #include <math.h>
 #include <stdlib.h>
@@ -174,7 +175,7 @@ static int64_t ceildiv(int64_t a, int64_t b) {
 
 int or_validate(const float* xy, const int32_t* start, int32_t n, float res_x, float res_y,
                 int32_t W, int32_t H, int32_t g, const or_placement* pl, int64_t* counts) {
-  counts[0] = counts[1] = counts[2] = 0;
+  counts[0] = counts[1] = counts[2] = counts[3] = 0;
   size_t A = (size_t)W * H;
   int32_t* last0 = malloc(sizeof(int32_t) * A);
   int32_t* lastg = malloc(sizeof(int32_t) * A);
@@ -223,6 +224,7 @@ int or_validate(const float* xy, const int32_t* start, int32_t n, float res_x, f
     free(mask);
   }
   for (size_t i = 0; i < A; i++) {
+    if (cnt0[i] >= 1) counts[3]++; /* covered: occupancy = covered / (W H) */
     if (cnt0[i] >= 2) counts[0]++;
     if (cntg[i] >= 2) counts[1]++;
   }

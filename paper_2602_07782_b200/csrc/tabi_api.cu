@@ -110,6 +110,7 @@ struct tabi_ctx {
   int64_t alloc_gen = 0;
   cudaError_t last_cuda = cudaSuccess;
   bool fused_off = false;  // the cooperative launch was refused once: split kernels from now on
+  Validator val;           // tabi_validate scratch (N3)
 };
 
 #define CK(call)                                              \
@@ -142,6 +143,7 @@ static void dfree_all(tabi_ctx* ctx) {
                 ctx->drow, ctx->scratch};  // cands / h_cands live inside the status blocks
   for (void* p : ps)
     if (p) cudaFree(p);
+  ctx->val.release();
   void* hs[] = {ctx->h_status, ctx->h_xy, ctx->h_start, ctx->h_out};
   for (void* p : hs)
     if (p) cudaFreeHost(p);
@@ -320,6 +322,41 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     st = pack_impl(ctx, xy, chart_start, n, res_x, res_y, spec, out, info, on_device, stream);
   }
   return st;
+}
+
+extern "C" tabi_status tabi_validate(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                                     int32_t n, float res_x, float res_y, int32_t W, int32_t H,
+                                     int32_t g, const tabi_placement* placements,
+                                     tabi_validation* out, int on_device, void* stream) {
+  if (!ctx || !out) return TABI_EINVAL;
+  memset(out, 0, sizeof(*out));
+  out->bad_chart = -1;
+  if (!xy || !chart_start || !placements || n < 1 || W < 1 || H < 1 || W > 65536 ||
+      H > 65536 || g < 0 || g > 64)
+    return TABI_EINVAL;
+  if (n > ctx->max_n) return TABI_ECAPACITY;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+  int64_t V = 0;
+  if (on_device) {
+    int32_t v = 0;
+    CK(cudaMemcpyAsync(&v, chart_start + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    V = v;
+  } else {
+    V = chart_start[n];
+    for (int32_t c = 0; c < n; c++)
+      if (chart_start[c + 1] - chart_start[c] < 3) {
+        out->bad_chart = c;
+        return TABI_EINVAL;
+      }
+  }
+  if (V < 3) return TABI_EINVAL;
+  int launches = 0;
+  const int st = ctx->val.run(xy, chart_start, n, res_x, res_y, W, H, g, placements,
+                              on_device != 0, V, s, out, &launches, &ctx->err);
+  out->gpu_launches = launches;
+  return (tabi_status)st;
 }
 
 static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,

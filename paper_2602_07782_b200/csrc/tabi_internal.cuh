@@ -434,3 +434,29 @@ void launch_tail_prepare(const PackParams& pp, const int32_t* perm, const int64_
 void launch_tail_layout(const PackParams& pp, const int32_t* wd, const int32_t* off,
                         int32_t* scratch, int64_t pair_cap, const Status* st, cudaStream_t s);
 }  // namespace tabi
+
+#include <string>
+namespace tabi {
+// N3 GPU validator (k_validate.cu): device scratch that grows on demand and
+// persists across calls on one context.
+struct Validator {
+  float* xy = nullptr;
+  int32_t* start = nullptr;
+  tabi_placement* pl = nullptr;
+  int64_t *AX = nullptr, *AY = nullptr;
+  void* ch = nullptr;
+  int64_t* ofs = nullptr;
+  uint8_t *mask = nullptr, *rows = nullptr;
+  uint32_t* grid = nullptr;
+  unsigned char* misc = nullptr;
+  unsigned char* h_misc = nullptr;  // pinned
+  int64_t cap_xy = 0, cap_s = 0, cap_pl = 0, cap_ax = 0, cap_ay = 0, cap_ch = 0, cap_ofs = 0;
+  int64_t cap_m = 0, cap_r = 0, cap_g = 0;
+  void release();
+  // counts for n charts placed by pl (host or device pointers); returns a
+  // tabi_status; fills out (bad_chart on EINVAL) and the launch count
+  int run(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int32_t W,
+          int32_t H, int32_t g, const tabi_placement* pl, bool on_device, int64_t nverts,
+          cudaStream_t s, tabi_validation* out, int* launches, std::string* err);
+};
+}  // namespace tabi

@@ -58,6 +58,12 @@ class Info(C.Structure):
                 ("work_profile", C.c_int64)]
 
 
+class Validation(C.Structure):
+    _fields_ = [("overlap", C.c_int64), ("gutter", C.c_int64), ("oob", C.c_int64),
+                ("covered", C.c_int64), ("occupancy", C.c_double), ("l2_stretch", C.c_double),
+                ("bad_chart", C.c_int32), ("gpu_launches", C.c_int32)]
+
+
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
                             ("scale_den", "<i4"), ("box_w", "<i4"), ("box_h", "<i4"),
                             ("rot90", "u1"), ("flip_x", "u1"), ("flip_y", "u1"),
@@ -105,6 +111,8 @@ def lib():
         L.tabi_debug_trace_raster.argtypes = [P, P]
         L.tabi_shard_plan.argtypes = [i32, P, i32, P]
         L.tabi_pack_batch.argtypes = [P, i32, i32, P, P, P, P, P, P, P]
+        L.tabi_validate.argtypes = [P, P, P, i32, C.c_float, C.c_float, i32, i32, i32, P,
+                                    C.POINTER(Validation), C.c_int, P]
         _lib = L
     return _lib
 
@@ -112,7 +120,7 @@ def lib():
 EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
            "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace",
-           "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch"]
+           "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch", "tabi_validate"]
 
 
 def shard_plan(n_charts, n_gpus: int) -> np.ndarray:
@@ -216,6 +224,35 @@ class Context:
         if raise_on_error and st not in (OK, NO_FIT):
             raise TabiError(st, f"bad_chart={info.bad_chart} {self.last_error()}")
         return st, out, info
+
+    def validate(self, xy, start, placements, atlas_w, atlas_h, gutter=1, res=(1.0, 1.0),
+                 stream=None, raise_on_error=True):
+        """GPU validator + metrics (tabi_validate): overlap / gutter / oob /
+        covered texel counts, occupancy and L2 stretch of ``placements``.
+        Host numpy inputs, or CUDA tensors (placements as uint8[32*N]).
+        Returns a dict."""
+        on_device = hasattr(xy, "is_cuda") and xy.is_cuda
+        n = int(start.shape[0]) - 1
+        v = Validation()
+        if on_device:
+            import torch
+            if stream is None:
+                stream = torch.cuda.current_stream(xy.device).cuda_stream
+            st = lib().tabi_validate(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], atlas_w,
+                                     atlas_h, gutter, _ptr(placements), C.byref(v), 1,
+                                     C.c_void_p(stream))
+        else:
+            xy = np.ascontiguousarray(xy, dtype=np.float32)
+            start = np.ascontiguousarray(start, dtype=np.int32)
+            pl = np.ascontiguousarray(placements, dtype=PLACEMENT_DTYPE)
+            st = lib().tabi_validate(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], atlas_w,
+                                     atlas_h, gutter, _ptr(pl), C.byref(v), 0,
+                                     C.c_void_p(stream) if stream else None)
+        if raise_on_error and st != OK:
+            raise TabiError(st, f"bad_chart={v.bad_chart} {self.last_error()}")
+        return dict(status=st, overlap=v.overlap, gutter=v.gutter, oob=v.oob, covered=v.covered,
+                    occupancy=v.occupancy, l2_stretch=v.l2_stretch, bad_chart=v.bad_chart,
+                    gpu_launches=v.gpu_launches)
 
     def pack_set(self, cs, res=None, **spec_kw):
         r = (cs.res, cs.res) if res is None else res
