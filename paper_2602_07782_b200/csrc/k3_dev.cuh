@@ -43,27 +43,25 @@ __device__ __forceinline__ void slice_job(int32_t* tab, const int32_t* blo, cons
 //  bottom y_bot(x)   = min((Umax - xC)/S, (Vmax + xS)/C)
 //  left   x_left(y)  = max((Umin - yS)/C, (yC - Vmax)/S)
 //  right  x_right(y) = min((Umax - yS)/C, (yC - Vmin)/S)
-__device__ inline void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i128 UXN, i128 VMN, i128 VXN,
-                        int64_t SC, int64_t nw, int64_t nh) {
+// The 8 jobs of a chart run on 8 lanes of one warp, so the job index only
+// selects operands: every lane then runs the same three divisions (no 8-way
+// divergence through per-job branches).
+__device__ inline void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i128 UXN, i128 VMN,
+                               i128 VXN, int64_t SC, int64_t nw, int64_t nh) {
   const int64_t N2 = C * C + S * S, DS = S * SC, DC = C * SC;
   const i128 N2SC = (i128)N2 * SC;
   const double rDS = rcp_approx((double)DS), rDC = rcp_approx((double)DC);
   const double rN2SC = rcp_approx(i128_to_double(N2SC));
   const int64_t SCS = SC * S, SCC = SC * C;
-  {  // LinDiv r
-    i128 A;
-    int64_t B, D;
-    double rD;
-    switch (r) {
-      case 0: A = VMN; B = SCS; D = DC; rD = rDC; break;          // top, increasing line at P0
-      case 1: A = UMN - SCC; B = -SCC; D = DS; rD = rDS; break;   // top, decreasing line at P1
-      case 2: A = -UXN; B = SCC; D = DS; rD = rDS; break;         // bottom, decreasing at P0 (neg)
-      case 3: A = -VXN - SCS; B = -SCS; D = DC; rD = rDC; break;  // bottom, increasing at P1 (neg)
-      case 4: A = -VXN; B = SCC; D = DS; rD = rDS; break;         // left, increasing at Q0
-      case 5: A = UMN - SCS; B = -SCS; D = DC; rD = rDC; break;   // left, decreasing at Q1
-      case 6: A = -UXN; B = SCS; D = DC; rD = rDC; break;         // right, decreasing at Q0 (neg)
-      default: A = VMN - SCC; B = -SCC; D = DS; rD = rDS; break;  // right, increasing at Q1 (neg)
-    }
+  const int q = r & 3;
+  {  // LinDiv r: f(i) = floor((A + i B) / D)
+    const bool dc = r == 0 || r == 3 || r == 5 || r == 6;
+    const int64_t D = dc ? DC : DS;
+    const double rD = dc ? rDC : rDS;
+    const i128 A0 = (r == 0 || r == 7) ? VMN : (r == 1 || r == 5) ? UMN : (r == 2 || r == 6) ? -UXN : -VXN;
+    const int64_t Aoff = (r == 1 || r == 7) ? -SCC : (r == 3 || r == 5) ? -SCS : 0;
+    const int64_t B = (r == 0 || r == 6) ? SCS : (r == 2 || r == 4) ? SCC : (r == 3 || r == 5) ? -SCS : -SCC;
+    const i128 A = A0 + Aoff;
     LinDiv L;
     L.D = D;
     L.rcp = rD;
@@ -73,38 +71,44 @@ __device__ inline void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i
     L.rB = B - L.qB * D;
     O.lin[r] = L;
   }
-  const int q = r & 3;
-  if (r < 4) {  // value at the last cell's clipped edge
-    int64_t v;
-    switch (q) {
-      case 0: v = fdiv_r128(UMN - mul_wide(nw, C), (i128)DS, rDS, false); break;
-      case 1: v = -fdiv_r128(-(VXN + mul_wide(nw, S)), (i128)DC, rDC, false); break;
-      case 2: v = fdiv_r128(UMN - mul_wide(nh, S), (i128)DC, rDC, false); break;
-      default: v = -fdiv_r128(-(mul_wide(nh, C) - VMN), (i128)DS, rDS, false); break;
+  // jobs 0-3: value at the last cell's clipped edge; 4-7: value at the
+  // crossing.  Even q rounds down, odd q up: v = sg * floor(sg * num / den).
+  {
+    const int64_t sg = (q & 1) ? -1 : 1;
+    i128 nm, den;
+    double rden;
+    if (r < 4) {
+      const i128 X = q == 0 ? UMN : q == 1 ? VXN : q == 2 ? UMN : -VMN;
+      const int64_t f = q < 2 ? nw : nh;
+      const int64_t P = q == 0 ? -C : q == 1 ? S : q == 2 ? -S : C;
+      nm = X + mul_wide(f, P);
+      const bool ds = q == 0 || q == 3;
+      den = ds ? DS : DC;
+      rden = ds ? rDS : rDC;
+    } else {
+      const int64_t m1 = q < 2 ? S : C, m2 = q < 2 ? C : -S;
+      const i128 X1 = (q & 1) ? UXN : UMN;
+      const i128 X2 = q == 0 ? VMN : q == 1 ? VXN : q == 2 ? VXN : VMN;
+      nm = (i128)m1 * X1 + (i128)m2 * X2;
+      den = N2SC;
+      rden = rN2SC;
     }
-    O.last[q] = v;
-  } else {  // value at the crossing
-    int64_t v;
-    switch (q) {
-      case 0: v = fdiv_r128((i128)S * UMN + (i128)C * VMN, N2SC, rN2SC, false); break;
-      case 1: v = -fdiv_r128(-((i128)S * UXN + (i128)C * VXN), N2SC, rN2SC, false); break;
-      case 2: v = fdiv_r128((i128)C * UMN - (i128)S * VXN, N2SC, rN2SC, false); break;
-      default: v = -fdiv_r128(-((i128)C * UXN - (i128)S * VMN), N2SC, rN2SC, false); break;
+    const int64_t v = sg * fdiv_r128(sg > 0 ? nm : -nm, den, rden, false);
+    if (r < 4) O.last[q] = v;
+    else O.star[q] = v;
+  }
+  {  // crossing x* / x** / y* / y**: i <= iA  (jobs 0-3), i >= iB (jobs 4-7)
+    const int64_t m1 = q < 2 ? C : S;
+    const int64_t m2 = q < 2 ? -S : C;
+    const i128 X1 = (q & 1) ? UXN : UMN;
+    const i128 X2 = q == 0 ? VMN : q == 1 ? VXN : q == 2 ? VXN : VMN;
+    const i128 cross = (i128)m1 * X1 + (i128)m2 * X2;
+    if (r < 4) {
+      O.iA[q] = fdiv_r128(cross, N2SC, rN2SC, true);
+      O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
+    } else {
+      O.iB[q] = -fdiv_r128(-cross, N2SC, rN2SC, true) - 1;
     }
-    O.star[q] = v;
-  }
-  i128 cross;
-  switch (q) {
-    case 0: cross = (i128)C * UMN - (i128)S * VMN; break;   // x* of the top boundary
-    case 1: cross = (i128)C * UXN - (i128)S * VXN; break;   // x** of the bottom
-    case 2: cross = (i128)S * UMN + (i128)C * VXN; break;   // y* of the left
-    default: cross = (i128)S * UXN + (i128)C * VMN; break;  // y** of the right
-  }
-  if (r < 4) {
-    O.iA[q] = fdiv_r128(cross, N2SC, rN2SC, true);
-    O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
-  } else {
-    O.iB[q] = -fdiv_r128(-cross, N2SC, rN2SC, true) - 1;
   }
 }
 

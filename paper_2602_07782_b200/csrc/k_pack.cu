@@ -37,6 +37,18 @@ constexpr int kNT = 512;
 constexpr int kNW = kNT / 32;
 constexpr int kRW = 2048;          // charts per row window
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for static Smem
+#ifndef TABI_PACK_NT
+#define TABI_PACK_NT 512
+#endif
+// The packer role runs on the first kPT threads of its CTA with a named
+// barrier (the other threads of a kNT-thread CTA leave at once).
+constexpr int kPT = TABI_PACK_NT;
+constexpr int kPW = kPT / 32;
+static_assert(kPT % 32 == 0 && kPT <= kNT, "packer threads");
+__device__ __forceinline__ void pk_sync() {
+  if (kPT == kNT) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"n"(kPT) : "memory");
+}
 
 struct Smem {
   int32_t scan[2][kNW + 1];
@@ -96,19 +108,19 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int32_t ia = warp_incl_sum(a, lane), ib = warp_incl_sum(b, lane);
   if (lane == 31) { S.scan[0][wid] = ia; S.scan[1][wid] = ib; }
-  __syncthreads();
+  pk_sync();
   if (wid == 0) {
-    const int32_t va = lane < kNW ? S.scan[0][lane] : 0, vb = lane < kNW ? S.scan[1][lane] : 0;
+    const int32_t va = lane < kPW ? S.scan[0][lane] : 0, vb = lane < kPW ? S.scan[1][lane] : 0;
     const int32_t xa = warp_incl_sum(va, lane), xb = warp_incl_sum(vb, lane);
-    if (lane < kNW) { S.scan[0][lane] = xa - va; S.scan[1][lane] = xb - vb; }
-    if (lane == 31) { S.scan[0][kNW] = xa; S.scan[1][kNW] = xb; }
+    if (lane < kPW) { S.scan[0][lane] = xa - va; S.scan[1][lane] = xb - vb; }
+    if (lane == 31) { S.scan[0][kPW] = xa; S.scan[1][kPW] = xb; }
   }
-  __syncthreads();
+  pk_sync();
   ea = S.scan[0][wid] + ia - a;
   eb = S.scan[1][wid] + ib - b;
-  ta = S.scan[0][kNW];
-  tb = S.scan[1][kNW];
-  __syncthreads();
+  ta = S.scan[0][kPW];
+  tb = S.scan[1][kPW];
+  pk_sync();
 }
 
 struct Win {                 // shared-memory window of one row
@@ -131,7 +143,7 @@ __device__ __forceinline__ void walk(const Win& w, int nwin, Enter enter, Body b
   const int32_t T = w.rx0[nwin - 1] - base0 + w.rwd[nwin - 1];
   // run length per thread, forced odd: lanes then hit F / the staged footprints
   // at addresses C apart, i.e. 32 distinct shared-memory banks per warp access
-  const int32_t C = ((T + kNT - 1) / kNT) | 1;
+  const int32_t C = ((T + kPT - 1) / kPT) | 1;
   int32_t t = threadIdx.x * C;
   const int32_t tend = min(T, t + C);
   if (t >= tend) return;
@@ -191,6 +203,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   __shared__ Smem S;
   __shared__ int32_t ready_upto;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid >= kPT) return;
   const int m = wave_m(pp, st->pad[2], jslot);
   if (m == 0) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
@@ -219,7 +232,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
       atomicAdd(&st->tr[3], gtime() - t0);
     }
-    __syncthreads();
+    pk_sync();
   };
   // Fold-side readiness: block until position s (and its pair offset) is
   // published, then take whatever further tiles are already published (no
@@ -273,7 +286,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         if (up < t_need) { S.abort = 1; ready_lim = -2; }  // beaten while waiting
       }
     }
-    __syncthreads();
+    pk_sync();
     return ready_lim;
   };
   const int64_t cb = (int64_t)(m - 1) * n;
@@ -321,12 +334,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   }
   if (!prefix_mode && !rd.flags) {  // work accounting: footprint entries K3 produced
     unsigned long long pe = 0;
-    for (int s = tid; s < n; s += kNT) pe += (unsigned long long)(wd[s] + hd[s]);
+    for (int s = tid; s < n; s += kPT) pe += (unsigned long long)(wd[s] + hd[s]);
     for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
     if (lane == 0) atomicAdd(&st->work_prof, pe);
   }
   int32_t* fsave = pp.T.fsave + (int64_t)(m - 1) * pp.T.fstride;
-  for (int x = tid; x < Wp; x += kNT) F[x] = prefix_mode ? fsave[x] : 0;  // top
+  for (int x = tid; x < Wp; x += kPT) F[x] = prefix_mode ? fsave[x] : 0;  // top
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
     S.next_a0 = 0; S.fold_hi = 0; S.pf_out = 0; S.abort = 0;
@@ -342,7 +355,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     }
     mbar_init(&S.mbar);
   }
-  __syncthreads();
+  pk_sync();
   uint32_t phase = 0;
   unsigned long long wk = 0;  // frontline column visits by this thread
   // row-phase timing (thread 0, SM clock cycles), compiled in only for the
@@ -381,8 +394,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t a0 = c0 & ~3, a1 = (c1 + 3) & ~3;
     const bool pg = (a1 - a0) > W.prof_cap;
     const bool hit = pf_pending && c0 >= S.pf_a0 && c1 <= S.pf_a1;
-    __syncthreads();  // previous readers of the window buffers are done
-    for (int k = tid; k < nwin && !have; k += kNT) {
+    pk_sync();  // previous readers of the window buffers are done
+    for (int k = tid; k < nwin && !have; k += kPT) {
       const int s = ws0 + k;
       W.rx0[k] = xs0[s];
       W.rx1[k] = xs1[s];
@@ -404,7 +417,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       mbar_wait(&S.mbar, phase);
       phase ^= 1u;
     }
-    __syncthreads();
+    pk_sync();
   };
 
   while (true) {
@@ -421,11 +434,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           wait_upto(n - 1);
           if (__ldcg(cand_bad + m - 1)) {
             if (tid == 0) S.fail = 1;
-            __syncthreads();
+            pk_sync();
             break;
           }
         }
-        for (int x = tid; x < Wp; x += kNT) fsave[x] = F[x];
+        for (int x = tid; x < Wp; x += kPT) fsave[x] = F[x];
         if (tid == 0) {
           pp.T.state[m - 1] = TAIL_LAYOUT;
           pp.T.r0[m - 1] = rs;
@@ -434,7 +447,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
                               0ull, 0ull};
           S.switched = 1;
         }
-        __syncthreads();
+        pk_sync();
         break;
       }
     }
@@ -466,17 +479,17 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       const int32_t left = S.knee_left, right = S.knee_right, ltr = S.knee_ltr;
       const bool degenerate = ltr ? (right >= Wp) : (left <= 0);
       if (tid == 0) S.nk = ltr ? left - 1 : right;
-      __syncthreads();
+      pk_sync();
       if (!degenerate) {
         const int32_t ref = ltr ? F[right] : F[left - 1];
-        for (int x = left + tid; x < right; x += kNT) {
+        for (int x = left + tid; x < right; x += kPT) {
           if (F[x] >= ref) {
             if (ltr) atomicMax(&S.nk, x);
             else atomicMin(&S.nk, x);
           }
         }
       }
-      __syncthreads();
+      pk_sync();
       if (tid == 0) {
         if (degenerate) {
           S.knee_valid = 0;
@@ -489,7 +502,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         }
         S.conc_max = INT32_MIN;
       }
-      __syncthreads();
+      pk_sync();
     }
     phase_mark(0);
     const int32_t kv = S.knee_valid;
@@ -497,32 +510,32 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t kb = kv ? (S.knee_ltr ? Wp : S.knee_left) : 0;
     if (kv) {
       int32_t mx = INT32_MIN;
-      for (int x = ka + tid; x < kb; x += kNT) mx = max(mx, F[x]);
+      for (int x = ka + tid; x < kb; x += kPT) mx = max(mx, F[x]);
       mx = warp_max(mx);
       if (lane == 0) atomicMax(&S.conc_max, mx);
     }
     // ---- Alg. 3 FoldRow for both HC settings and both folds --------------
     if (tid < 4) S.endv[tid] = INT32_MIN;
     if (tid == 0) { S.done = 0; S.win_s0 = -1; S.win_e = -1; }
-    __syncthreads();
+    pk_sync();
     pf_pending = S.pf_out != 0 && !prefix_mode;
     if (prefix_mode) {
       // prefix rows were laid out by the tail kernels (positions in xs0/xs1);
       // the row is the run of equal row ids starting at rs
       const int32_t qr = qrow[rs];
-      for (int base = rs; !S.done; base += kNT) {
+      for (int base = rs; !S.done; base += kPT) {
         if (tid == 0) S.fmin[0] = INT32_MAX;
-        __syncthreads();
+        pk_sync();
         const int s = base + tid;
         if (s < n && qrow[s] != qr) atomicMin(&S.fmin[0], s);
-        __syncthreads();
-        if (tid == 0 && (S.fmin[0] != INT32_MAX || base + kNT >= n)) {
+        pk_sync();
+        if (tid == 0 && (S.fmin[0] != INT32_MAX || base + kPT >= n)) {
           const int32_t e = S.fmin[0] != INT32_MAX ? S.fmin[0] - 1 : n - 1;
           S.endv[0] = S.endv[1] = e;
           S.endv[2] = S.endv[3] = rs - 1;
           S.done = 1;
         }
-        __syncthreads();
+        pk_sync();
       }
     } else {
       int32_t carry0 = 0, carry1 = 0;
@@ -532,7 +545,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
 #ifdef TABI_PHASE_TRACE
         if (rd.flags && jslot == 0 && rs == 0 && base == 0 && tid == 0) st->tfirst[2] = gtime();
 #endif
-        const int cnt = min(kNT, lim - base + 1);  // positions [base, base + cnt)
+        const int cnt = min(kPT, lim - base + 1);  // positions [base, base + cnt)
         if (tid < 4) S.fmin[tid] = INT32_MAX;
         const int s = base + tid;
         const bool valid = tid < cnt;
@@ -558,7 +571,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           if (x0 + w_s > kb - ka) atomicMin(&S.fmin[2], s);
           if (x1 + w_s > kb - ka) atomicMin(&S.fmin[3], s);
         }
-        __syncthreads();
+        pk_sync();
         if (tid == 0) {
           for (int q = 0; q < 4; q++)
             if (S.endv[q] == INT32_MIN && S.fmin[q] != INT32_MAX) S.endv[q] = S.fmin[q] - 1;
@@ -569,7 +582,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             S.fold_hi = base + cnt;  // W.* hold positions [rs, min(fold_hi, rs + kRW))
           }
         }
-        __syncthreads();
+        pk_sync();
         if (S.done) break;
         carry0 += t0;
         carry1 += t1;
@@ -593,7 +606,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       S.npairs = 0;
       S.pair_overflow = 0;
     }
-    __syncthreads();
+    pk_sync();
     if (S.fail) break;
     const int32_t knee_ok = S.knee_ok;
     const int32_t hc0 = S.hcsel[0], hc1 = S.hcsel[1];
@@ -609,7 +622,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t R = max(hc0 ? endA : -1, (knee_ok && hc1) ? endK : -1);
     if (!adj_only && R > rs) {
       int32_t carry = 0;
-      for (int base = rs; base <= R; base += kNT) {
+      for (int base = rs; base <= R; base += kPT) {
         const int a = base + tid;
         int32_t cnt = 0;
         if (a <= R && useW) {
@@ -640,21 +653,21 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           atomicMax(&st->pad[0], carry);
         }
       }
-      __syncthreads();
+      pk_sync();
       if (S.pair_overflow) {
         if (tid == 0) S.fail = 1;
-        __syncthreads();
+        pk_sync();
         break;
       }
       const int32_t np = S.npairs;
-      for (int p = wid; p < np; p += kNW) {
+      for (int p = wid; p < np; p += kPW) {
         const int a = pa[p], b = pb[p];
         bool la, lb;
         const int32_t dx = useW ? W.rx1[b - rs] - W.rx1[a - rs] : xs1[b] - xs1[a];
         warp_locks(row + rowofs[a], row + rowofs[b], hd[a], hd[b], dx, lane, la, lb);
         if (lane == 0) plk[p] = (la ? 1 : 0) | (lb ? 2 : 0);
       }
-      __syncthreads();
+      pk_sync();
     }
     const int32_t np = S.npairs;
     phase_mark(2);
@@ -672,8 +685,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
       stage(ws0, we);
-      for (int k = tid; k < 5 * nwin; k += kNT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
-      __syncthreads();  // (index 4 of rY is rbot)
+      for (int k = tid; k < 5 * nwin; k += kPT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
+      pk_sync();  // (index 4 of rY is rbot)
       phase_mark(8);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       // flattened (chart, column) runs (see walk()); per chart segment the
@@ -683,7 +696,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       {
         const int32_t base0 = W.rx0[0];
         const int32_t T = W.rx0[nwin - 1] - base0 + W.rwd[nwin - 1];
-        const int32_t C = ((T + kNT - 1) / kNT) | 1;
+        const int32_t C = ((T + kPT - 1) / kPT) | 1;
         int32_t t = tid * C;
         const int32_t tend = min(T, t + C);
         int i = 0;
@@ -740,14 +753,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           i++;
         }
       }
-      __syncthreads();
+      pk_sync();
       if (one) continue;  // Y stays in shared memory for Alg. 1, score and commit
-      for (int k = tid; k < nwin; k += kNT) {
+      for (int k = tid; k < nwin; k += kPT) {
         const int s = ws0 + k;
         const int na = (knee_ok && s <= endK) ? 4 : 2;
         for (int q = 0; q < na; q++) __stcg(&Yc[(int64_t)q * n + s], W.rY[q * kRW + k]);
       }
-      __syncthreads();
+      pk_sync();
     }
     phase_mark(3);
     // ---- Alg. 1 CorrectYOffsets over adjacent + non-adjacent pairs ---------
@@ -785,18 +798,18 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           if ((bits & 1) && ya < yb) { atomicMax(Ya, yb); S.changed3[flag] = 1; }
           if ((bits & 2) && yb < ya) { atomicMax(Yb, ya); S.changed3[flag] = 1; }
         };
-        const bool cached = nitems <= 2 * kNT;
+        const bool cached = nitems <= 2 * kPT;
         int32_t *ya0 = nullptr, *yb0 = nullptr, *ya1 = nullptr, *yb1 = nullptr;
         int bits0 = 0, bits1 = 0;
         bool v0 = false, v1 = false;
         if (cached) {
           if (tid < nitems) v0 = item(tid, ya0, yb0, bits0);
-          if (tid + kNT < nitems) v1 = item(tid + kNT, ya1, yb1, bits1);
+          if (tid + kPT < nitems) v1 = item(tid + kPT, ya1, yb1, bits1);
         }
         // one barrier per iteration: iteration i raises flag i % 3 and clears
         // flag (i + 1) % 3, last read two barriers ago
         if (tid == 0) { S.changed3[0] = 0; S.changed3[1] = 0; }
-        __syncthreads();
+        pk_sync();
         for (int iter = 0;; iter++) {
           const int fl = iter % 3;
           if (tid == 0) S.changed3[(iter + 1) % 3] = 0;
@@ -804,13 +817,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             if (v0) relax(ya0, yb0, bits0, fl);
             if (v1) relax(ya1, yb1, bits1, fl);
           } else {
-            for (int it = tid; it < nitems; it += kNT) {
+            for (int it = tid; it < nitems; it += kPT) {
               int32_t *Ya, *Yb;
               int bits;
               if (item(it, Ya, Yb, bits)) relax(Ya, Yb, bits, fl);
             }
           }
-          __syncthreads();
+          pk_sync();
 #ifdef TABI_PHASE_TRACE
           if (tid == 0 && jslot == 0) atomicAdd(&st->rph[7], 1ull);  // Alg. 1 passes
 #endif
@@ -827,7 +840,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       int32_t nm[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
       if (one) {
         const int nwin = endA - rs + 1;
-        for (int k = tid; k < nwin; k += kNT) {
+        for (int k = tid; k < nwin; k += kPT) {
           const int na = (knee_ok && rs + k <= endK) ? 4 : 2;
           for (int q = 0; q < na; q++) nm[q] = max(nm[q], W.rY[q * kRW + k] + W.rbot[k]);
         }
@@ -835,12 +848,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       for (int ws0 = rs; ws0 <= endA && !one; ws0 += kRW) {
         const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
         stage(ws0, we);
-        for (int k = tid; k < nwin && !one; k += kNT) {
+        for (int k = tid; k < nwin && !one; k += kPT) {
           const int s = ws0 + k;
           const int na = (knee_ok && s <= endK) ? 4 : 2;
           for (int q = 0; q < na; q++) W.rY[q * kRW + k] = __ldcg(&Yc[(int64_t)q * n + s]);
         }
-        __syncthreads();
+        pk_sync();
         const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
         int32_t Yv[4];
         int nact = 0;
@@ -858,14 +871,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               wk += nact;
             },
             [&](int) {});
-        __syncthreads();
+        pk_sync();
       }
       for (int q = 0; q < ncfg; q++) {
         const int32_t v = warp_max(nm[q]);
         if (lane == 0) atomicMax(&S.newmax[q], v);
       }
     }
-    __syncthreads();
+    pk_sync();
     phase_mark(5);
     // ---- hierarchical selection -----------------------------------
     if (tid == 0) {
@@ -885,7 +898,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       S.fmax = max(S.fmax, S.newmax[cfg]);
       S.knee_key = 0ull;
     }
-    __syncthreads();
+    pk_sync();
     // ---- commit: F <- max(F, Y + BottomEdge); record placements ------------
     const int cfg = S.sel_cfg;
     const int f = cfg >> 1, dir = cfg & 1;
@@ -894,7 +907,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // drops of the row's charts, issued here so their loads overlap the commit
     // walk (the commit's last barrier publishes S.knee_key) ------------------
     if (f == 0 && !no_bal && !prefix_mode) {
-      for (int t = rs + tid; t < endS; t += kNT) {
+      for (int t = rs + tid; t < endS; t += kPT) {
         const int64_t d = (int64_t)hsorted[t] - hsorted[t + 1];
         if (10 * d >= (int64_t)pp.H * TABI_UNITS && 5 * d >= hsorted[t]) {
           const unsigned long long key =
@@ -906,9 +919,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int ws0 = rs; ws0 <= endS; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = min(we, endS + 1) - ws0;
       stage(ws0, we);
-      for (int k = tid; k < nwin && !one; k += kNT)
+      for (int k = tid; k < nwin && !one; k += kPT)
         W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
-      __syncthreads();
+      pk_sync();
       phase_mark(9);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
@@ -937,7 +950,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             wk += (unsigned long long)(j1 - j0);
           },
           [&](int, int32_t) {}, [&](int) {});
-      __syncthreads();
+      pk_sync();
     }
     phase_mark(6);
     if (tid == 0) {
@@ -965,7 +978,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
       S.next_a0 = (!prefix_mode && nx < n && nx < S.fold_hi && nx - rs < kRW) ? W.rco[nx - rs] : -1;
     }
-    __syncthreads();
+    pk_sync();
     phase_mark(7);
   }
   if (pf_pending) {  // a failed row left its prefetch in flight: let it land first

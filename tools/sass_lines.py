@@ -68,6 +68,23 @@ def main():
         tot[0] += n
         tot[1] += s
     print(f"total warp instructions {tot[0]:.0f}, stall samples {tot[1]:.0f}, mapped lines {len(agg)}")
+    # optional phase buckets over line ranges of <file.cu>: PHASES="name:lo-hi,..."
+    if os.environ.get("PHASES"):
+        ph = []
+        for item in os.environ["PHASES"].split(","):
+            name, rng = item.split(":")
+            fn = os.path.basename(cu)
+            if "@" in rng:  # name:file@lo-hi
+                fn, rng = rng.split("@")
+            lo, hi = map(int, rng.split("-"))
+            ph.append((name, fn, lo, hi))
+        bk = collections.defaultdict(lambda: [0.0, 0.0])
+        for (f, l), (n, s) in agg.items():
+            nm = next((name for name, fn, lo, hi in ph if fn == f and lo <= l <= hi), "other:" + f)
+            bk[nm][0] += n
+            bk[nm][1] += s
+        for nm, (n, s) in sorted(bk.items(), key=lambda kv: -kv[1][0]):
+            print(f"  phase {nm:24s} {n / tot[0] * 100:5.1f}% inst {s / max(tot[1], 1) * 100:5.1f}% stall")
     for (f, l), (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:topn]:
         fp = os.path.join(ROOT, "paper_2602_07782_b200", "csrc", f)
         lines = src if f == os.path.basename(cu) else (
