@@ -130,6 +130,8 @@ struct Win {                 // shared-memory window of one row
   int32_t* rco;              // footprint offset (colofs, absolute; see pr_base)
   int32_t* rY;               // [4][kRW] vertical offsets per configuration
   int32_t* rbot;             // max over the chart's columns of BottomEdge (push walk)
+  int32_t* rhs;              // unscaled heights (FindKnee), written by the fold
+  uint8_t* rlk;              // adjacent-pair lock bits (Alg. 1), written by the fold
   uint32_t* prof;            // staged column footprints
   int32_t prof_cap;
 };
@@ -321,7 +323,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   W.rco = W.rwd + kRW;
   W.rY = W.rco + kRW;
   W.rbot = W.rY + 4 * kRW;
-  W.prof = (uint32_t*)(W.rbot + kRW);
+  W.rhs = W.rbot + kRW;
+  W.rlk = (uint8_t*)(W.rhs + kRW);
+  W.prof = (uint32_t*)(W.rlk + kRW);
   W.prof_cap = prof_cap;
 
   const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
@@ -565,6 +569,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             W.rx1[s - rs] = x1;
             W.rwd[s - rs] = w_s;
             W.rco[s - rs] = colofs[s];
+            W.rhs[s - rs] = hsorted[s];
+            W.rlk[s - rs] = lk[s];
           }
           if (x0 + w_s > Wp) atomicMin(&S.fmin[0], s);
           if (x1 + w_s > Wp) atomicMin(&S.fmin[1], s);
@@ -685,7 +691,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
       stage(ws0, we);
-      for (int k = tid; k < 5 * nwin; k += kPT) W.rY[(k / nwin) * kRW + k % nwin] = INT32_MIN;
+      for (int k = tid; k < nwin; k += kPT) {
+#pragma unroll
+        for (int q = 0; q < 5; q++) W.rY[q * kRW + k] = INT32_MIN;
+      }
       pk_sync();  // (index 4 of rY is rbot)
       phase_mark(8);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
@@ -780,7 +789,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             a = rs + q;
             b = a + 1;
             if (b > endc) return false;
-            bits = lk[a];
+            bits = useW ? W.rlk[a - rs] : lk[a];
           } else {
             const int p = q - (endA - rs);
             a = pa[p];
@@ -908,8 +917,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // walk (the commit's last barrier publishes S.knee_key) ------------------
     if (f == 0 && !no_bal && !prefix_mode) {
       for (int t = rs + tid; t < endS; t += kPT) {
-        const int64_t d = (int64_t)hsorted[t] - hsorted[t + 1];
-        if (10 * d >= (int64_t)pp.H * TABI_UNITS && 5 * d >= hsorted[t]) {
+        const int32_t h0 = useW ? W.rhs[t - rs] : hsorted[t];
+        const int32_t h1 = useW ? W.rhs[t + 1 - rs] : hsorted[t + 1];
+        const int64_t d = (int64_t)h0 - h1;
+        if (10 * d >= (int64_t)pp.H * TABI_UNITS && 5 * d >= h0) {
           const unsigned long long key =
               ((unsigned long long)d << 32) | (unsigned long long)(0x7fffffff - t);
           atomicMax(&S.knee_key, key);
@@ -965,8 +976,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           const int t = 0x7fffffff - (int)(S.knee_key & 0xffffffffull);
           S.knee_valid = 1;
           S.knee_ltr = dir == 0;
-          S.knee_left = Xo[t];
-          S.knee_right = Xo[t] + wd[t];
+          const int32_t xk = useW ? cfgX(cfg, t - rs) : Xo[t];
+          S.knee_left = xk;
+          S.knee_right = xk + (useW ? W.rwd[t - rs] : wd[t]);
           S.knees_found++;
         } else {
           S.knee_valid = 0;
@@ -1339,7 +1351,7 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
     attr = true;
   }
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 9 * (size_t)kRW);
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW) + kRW;
   const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   pack_kernel<<<pp.B, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
                                              hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
@@ -1377,7 +1389,7 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s) {
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 9 * (size_t)kRW);
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW) + kRW;
   int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy, tstart, tix};
   PackParams p = pp;
