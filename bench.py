@@ -34,6 +34,10 @@ PAPER_CONTEXT = ("paper (RTX 4090, OpenGL): 5.31 ms mean pack for 1,001-5,000 ch
                  "Ryzen 7 1800X (P:39)")
 
 
+# spec overrides per workload (beyond the chart set's own fields)
+WORKLOAD_SPEC = {"C4X": {"flags": 32}}
+
+
 def workload(name: str, seed: int, rho: float):
     import chartgen
     if name == "C3":
@@ -46,6 +50,10 @@ def workload(name: str, seed: int, rho: float):
     elif name == "C4":
         cs = chartgen.config4(seed, t_opt_bp=0)
         desc = f"C4 configs[3]: 20000 lightmap charts (seed={seed}, rho=0.8) into 8192x8192, t_opt=0"
+    elif name == "C4X":
+        cs = chartgen.config4(seed, t_opt_bp=-1)
+        desc = (f"C4 configs[3]: 20000 lightmap charts (seed={seed}, rho=0.8) into 8192x8192, "
+                f"paper t_opt policy with the exact-greedy tail (TABI_F_EXACT_TAIL, SURVEY N4)")
     elif name == "C4P":
         cs = chartgen.config4(seed, t_opt_bp=-1)
         desc = (f"C4 configs[3]: 20000 lightmap charts (seed={seed}, rho=0.8) into 8192x8192, "
@@ -138,14 +146,14 @@ def barrier(ws):
         dist.barrier()
 
 
-def cpu_oracle_rate(cs, budget_s=15.0, max_candidates=None):
+def cpu_oracle_rate(cs, budget_s=15.0, max_candidates=None, **spec_kw):
     """Time the oracle (as it stands) on host cores: full packs until ~budget_s."""
     import oracle
     oracle.build()
     t0 = time.perf_counter()
     n = 0
     while True:
-        st, pl, info, _ = oracle.pack(cs)
+        st, pl, info, _ = oracle.pack(cs, **spec_kw)
         n += 1
         if time.perf_counter() - t0 > budget_s or n >= 64:
             break
@@ -159,19 +167,20 @@ def run_reference(args, ws, rank):
     import oracle
     oracle.build()
     cs, desc = workload(args.workload, 0, args.rho)
+    kw = WORKLOAD_SPEC.get(args.workload, {})
     sample_cands = args.steps > 20
     M = cs.scale_count
 
     def step(i):
         if not sample_cands:
             t = time.perf_counter()
-            oracle.pack(cs)
+            oracle.pack(cs, **kw)
             return time.perf_counter() - t
         # bounded sample: proxies+sort+8 of the 64 candidate scales (rotating), scaled to 64
         ms = [M - ((i % 8) + 8 * j) for j in range(8)]
         t = time.perf_counter()
         for m in ms:
-            oracle.pack_candidate(cs, m)
+            oracle.pack_candidate(cs, m, **kw)
         return (time.perf_counter() - t) * M / len(ms)
 
     for i in range(args.warmup):
@@ -239,7 +248,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sets, desc, units_per_step, scaling = rank_atlases(args.workload, rank, ws, args.rho)
-    specs = [spec_of(cs) for cs in sets]
+    specs = [spec_of(cs, **WORKLOAD_SPEC.get(args.workload, {})) for cs in sets]
     ctx = Context(local, max_charts=max(max(cs.n_charts for cs in sets), 1024),
                   max_vertices=max(cs.n_vertices for cs in sets) + 16,
                   max_atlas_side=max(max(cs.atlas_w, cs.atlas_h) for cs in sets))
@@ -390,7 +399,7 @@ def main():
             "clocks": clk.summary(),
             "paper_context": PAPER_CONTEXT}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, n, dt, m = cpu_oracle_rate(sets[0])
+        rate, n, dt, m = cpu_oracle_rate(sets[0], **WORKLOAD_SPEC.get(args.workload, {}))
         line["cpu_baseline"] = {"value": rate, "unit": "atlases/s", "cores": 1, "kind": "oracle",
                                 "sample": f"{n} full oracle packs of the first chart set "
                                           f"(all candidates) in {dt:.1f} s, 1 thread",

@@ -41,16 +41,19 @@ enum {
   TABI_F_PREROTATE = 8u,             /* UV pre-rotation to the OBB angle (for UV
                                         charts, not TSS -- rotation by non-90-degree angles
                                         resamples the texture); see tabi_placement step 0 */
-  TABI_F_NO_OBB = 16u                /* ablation: no OBB bound on the footprints (D6/D11);
+  TABI_F_NO_OBB = 16u,               /* ablation: no OBB bound on the footprints (D6/D11);
                                         with local_aabb_count = 1 the proxy is the plain AABB
                                         (Chameleon / balanced-only) */
+  TABI_F_EXACT_TAIL = 32u            /* hybrid tail variant (DESIGN R6): the tail is
+                                        folded exactly by Alg. 3 with compaction at m/M -- no
+                                        intermediate downscale; tail charts keep scale m/M */
 };
 
 typedef struct tabi_ctx tabi_ctx;    /* opaque: device workspace + stream, one per host thread */
 
 /* Atlas + knobs (SPEC AtlasSpec S:33-36).  Invariants, else TABI_EINVAL:
  *   1 <= atlas_w, atlas_h <= 16384;  0 <= gutter <= 64;  1 <= scale_count <= 256;
- *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_* (0..31). */
+ *   1 <= local_aabb_count <= 64;  -1 <= t_opt_bp <= 10000;  flags in TABI_F_* (0..63). */
 typedef struct {
   int32_t atlas_w, atlas_h;   /* texels */
   int32_t gutter;             /* texels around every chart, none at atlas edges; paper 1 */
@@ -85,8 +88,9 @@ typedef struct {
   int32_t scale_num, scale_den;   /* scale = scale_num / scale_den = m / M */
   int32_t box_w, box_h;
   uint8_t rot90, flip_x, flip_y, mirror_x;
-  uint8_t mode;                   /* 0 = sequential row, 1 = prefix-tail row (scale
-                                     scale_num / scale_den = p / 2^20) */
+  uint8_t mode;                   /* 0 = sequential row, 1 = hybrid-tail row: prefix rows
+                                     at scale p / 2^20, or exact rows at m / M
+                                     under TABI_F_EXACT_TAIL (R6) */
   uint8_t prerot;                 /* pre-rotation angle index j (step 0), 0 = none */
   uint8_t pad[2];
 } tabi_placement;

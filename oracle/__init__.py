@@ -21,7 +21,8 @@ SRCS = [os.path.join(HERE, f) for f in ("tabi_oracle.c", "validate.c")]
 KMAX = 64
 
 OK, EINVAL, NO_FIT = 0, 1, 2
-F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE, F_NO_OBB = 1, 2, 4, 8, 16
+F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE, F_NO_OBB, F_EXACT_TAIL = (1, 2, 4, 8, 16,
+                                                                            32)
 
 
 def build(force: bool = False) -> str:

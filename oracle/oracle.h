@@ -20,7 +20,8 @@
 enum { OR_OK = 0, OR_EINVAL = 1, OR_NO_FIT = 2 };
 enum { OR_F_NO_HC = 1u, OR_F_NO_BALANCE = 2u, OR_F_ADJACENT_LOCKS_ONLY = 4u,
        OR_F_PREROTATE = 8u, /* UV pre-rotation to the OBB angle (DESIGN R4) */
-       OR_F_NO_OBB = 16u /* ablation: footprints without the OBB bound */ };
+       OR_F_NO_OBB = 16u, /* ablation: footprints without the OBB bound */
+       OR_F_EXACT_TAIL = 32u /* R6: exact Alg. 3 fold of the hybrid tail */ };
 
 /* Per-chart proxy in its final pre-packing pose ("two parallel passes
  * which compute our shape approximations ... and determine each chart's

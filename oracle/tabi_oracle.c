@@ -628,6 +628,10 @@ static void eval_config(or_config* cf, const or_prof* pr, const int32_t* wd, con
     if (cf->F[x] > cf->score_knee) cf->score_knee = cf->F[x];
 }
 
+static int tail_rows(const or_prof* pt, const int32_t* q, const int32_t* xl, int32_t n,
+                     int32_t r0, const or_spec* spec, int32_t* F, int32_t* X, int32_t* Y,
+                     uint8_t* mir, or_cand* cand);
+
 /* ---- D24 prefix-sum tail ("Performance Optimization") --------
  * Remaining sorted charts [r0, n) at candidate m: FastAtlas-style fold of the
  * prefix sum of the horizontal OFFSETS (HC always on), rows cut at
@@ -678,8 +682,21 @@ static int prefix_tail(const or_proxy* px, const int32_t* perm, int32_t n, int32
   }
   cand->p = (int32_t)p;
   cand->switched_at = r0;
-  if (!ok) { free(q); free(xl); return 0; }
-  /* steps 3-4: rows in order, L->R iff row index % 3 == 0, push with locks */
+  if (ok) ok = tail_rows(pt, q, xl, n, r0, spec, F, X, Y, mir, cand);
+  free(q);
+  free(xl);
+  return ok;
+}
+
+/* D24 steps 3-4 (and R6): the tail rows q[] in order, L->R iff row index % 3
+ * == 0 (FastAtlas), positions xl[] in the row, pushed with locks (D15,
+ * Alg. 1), no knees; fails if the frontline passes the atlas bottom. */
+static int tail_rows(const or_prof* pt, const int32_t* q, const int32_t* xl, int32_t n,
+                     int32_t r0, const or_spec* spec, int32_t* F, int32_t* X, int32_t* Y,
+                     uint8_t* mir, or_cand* cand) {
+  const int32_t g = spec->gutter;
+  const int64_t Wp = spec->atlas_w + 2 * g, Hp = spec->atlas_h + 2 * g;
+  int ok = 1;
   int32_t row_idx = 0;
   int32_t cap = 1, np;
   int32_t *qa = malloc(sizeof(int32_t)), *qb = malloc(sizeof(int32_t));
@@ -724,6 +741,33 @@ static int prefix_tail(const or_proxy* px, const int32_t* perm, int32_t n, int32
     a = b + 1;
   }
   free(qa); free(qb); free(la); free(lb);
+  return ok;
+}
+
+/* ---- R6 exact-greedy tail (TABI_F_EXACT_TAIL) ----------
+ * Same switch (D23) and the same row placement as D24 steps 3-4, but the
+ * remaining charts [r0, n) are folded exactly by Alg. 3 with horizontal
+ * compaction (HC always on in the tail) at the candidate
+ * scale m/M itself: a row never overflows, so there is no intermediate
+ * downscale and every chart keeps scale m/M. */
+static int exact_tail(int32_t n, int32_t r0, int32_t m, const or_spec* spec, const or_prof* pr,
+                      const int32_t* wd, const int32_t* off, int32_t* F, int32_t* X, int32_t* Y,
+                      uint8_t* mir, or_cand* cand) {
+  const int32_t g = spec->gutter, M = spec->scale_count;
+  const int32_t Wp = spec->atlas_w + 2 * g;
+  int32_t* q = malloc(sizeof(int32_t) * n);
+  int32_t* xl = malloc(sizeof(int32_t) * n);
+  int ok = 1;
+  int32_t row = 0;
+  for (int32_t a = r0; a < n; row++) {
+    const int32_t end = or_fold_row(n, a, Wp, 1, wd, off, xl);
+    if (end < a) { ok = 0; break; } /* D22: the first chart does not fit */
+    for (int32_t c = a; c <= end; c++) q[c] = row;
+    a = end + 1;
+  }
+  cand->p = (int32_t)(((int64_t)m << 20) / M); /* informational: every chart keeps m/M */
+  cand->switched_at = r0;
+  if (ok) ok = tail_rows(pr, q, xl, n, r0, spec, F, X, Y, mir, cand);
   free(q);
   free(xl);
   return ok;
@@ -783,7 +827,10 @@ int or_pack_candidate(const or_proxy* px, const int32_t* perm, int32_t n, const 
         cdiv64(hu[row_start] * m, (int64_t)M * 256) * 10000 < (int64_t)t_opt * spec->atlas_h) {
       r0 = row_start;
       cand->score = score;
-      if (!prefix_tail(px, perm, n, r0, m, spec, pr, off, F, X, Y, mir, pt, cand)) fail = 1;
+      const int okt = (flags & OR_F_EXACT_TAIL)
+                          ? exact_tail(n, r0, m, spec, pr, wd, off, F, X, Y, mir, cand)
+                          : prefix_tail(px, perm, n, r0, m, spec, pr, off, F, X, Y, mir, pt, cand);
+      if (!okt) fail = 1;
       score = cand->score;
       break;
     }
@@ -861,13 +908,14 @@ int or_pack_candidate(const or_proxy* px, const int32_t* perm, int32_t n, const 
       int32_t c = perm[s];
       or_placement* o = &out[c];
       memset(o, 0, sizeof(*o));
-      const int tail = s >= r0;  /* prefix-folded chart: final scale p / 2^20 */
+      const int tail = s >= r0;  /* tail chart: final scale p / 2^20 (D24) */
+      const int ptail = tail && !(flags & OR_F_EXACT_TAIL);  /* R6 keeps m/M */
       o->tx = X[s];
       o->ty = Y[s];
-      o->scale_num = tail ? cand->p : m;
-      o->scale_den = tail ? (1 << 20) : M;
-      o->box_w = tail ? pt[s].ws : pr[s].ws;
-      o->box_h = tail ? pt[s].hs : pr[s].hs;
+      o->scale_num = ptail ? cand->p : m;
+      o->scale_den = ptail ? (1 << 20) : M;
+      o->box_w = ptail ? pt[s].ws : pr[s].ws;
+      o->box_h = ptail ? pt[s].hs : pr[s].hs;
       o->rot90 = (uint8_t)px[c].rot90;
       o->prerot = (uint8_t)px[c].prerot;
       o->flip_x = (uint8_t)px[c].fx;
@@ -895,7 +943,7 @@ static int spec_ok(const or_spec* s) {
   return s->atlas_w >= 1 && s->atlas_h >= 1 && s->atlas_w <= 16384 && s->atlas_h <= 16384 &&
          s->gutter >= 0 && s->gutter <= 64 && s->scale_count >= 1 && s->scale_count <= 256 &&
          s->local_aabb_count >= 1 && s->local_aabb_count <= OR_KMAX && s->t_opt_bp >= -1 &&
-         s->t_opt_bp <= 10000 && (s->flags & ~31u) == 0;
+         s->t_opt_bp <= 10000 && (s->flags & ~63u) == 0;
 }
 
 /* ---- scale search + output ("return the largest scale and
@@ -932,7 +980,9 @@ int or_pack(const float* xy, const int32_t* start, int32_t n, float res_x, float
      * scale factor S that maximizes the average final scale weighted by chart
      * area"); sequential candidates reduce to the largest m.  Exact:
      * V = A_seq * m * 2^20 + A_pre * p * M; ties go to the larger m. */
-    const int32_t r0 = cd.switched_at >= 0 ? cd.switched_at : n;
+    /* R6: every chart keeps m/M, so the whole area counts at m */
+    const int32_t r0 =
+        (cd.switched_at >= 0 && !(spec->flags & OR_F_EXACT_TAIL)) ? cd.switched_at : n;
     const i128 V = apre[r0] * m * P20 + (apre[n] - apre[r0]) * (i128)cd.p * M;
     if (V >= bestV) { bestV = V; best = m; bc = cd; }
   }
@@ -943,7 +993,8 @@ int or_pack(const float* xy, const int32_t* start, int32_t n, float res_x, float
   {
     /* D26: every map is a similarity, so the per-triangle L2 stretch is 1/s;
      * area-weighted RMS over the charts. */
-    const int32_t r0 = bc.switched_at >= 0 ? bc.switched_at : n;
+    const int32_t r0 =
+        (bc.switched_at >= 0 && !(spec->flags & OR_F_EXACT_TAIL)) ? bc.switched_at : n;
     if (r0 == n) {
       info->l2_stretch = (double)M / (double)best;
     } else {

@@ -1320,12 +1320,13 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
   const int64_t b = (int64_t)(m - 1) * pp.n + s;
   const int c = perm[s];
   const uint8_t ps = pose[c];
-  const bool tail = s >= wr0;  // prefix-folded chart: final scale p / 2^20 (D24)
+  const bool tail = s >= wr0;  // tail chart: final scale p / 2^20 (D24) ...
+  const bool ptail = tail && !(pp.flags & TABI_F_EXACT_TAIL);  // ... or m/M (R6)
   tabi_placement p;
   p.tx = Xo[b];
   p.ty = Yo[b];
-  p.scale_num = tail ? wp : m;
-  p.scale_den = tail ? (1 << 20) : pp.M;
+  p.scale_num = ptail ? wp : m;
+  p.scale_den = ptail ? (1 << 20) : pp.M;
   p.box_w = wd_all[b] - 2 * pp.g;
   p.box_h = hd_all[b] - 2 * pp.g;
   p.rot90 = ps & 1;

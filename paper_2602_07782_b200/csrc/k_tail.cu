@@ -87,6 +87,65 @@ tail_prepare_kernel(PackParams pp, const int32_t* __restrict__ perm, const int64
   int32_t* sc = scratch + (int64_t)(m - 1) * (6 * (int64_t)n + 3 * pair_cap);
   int32_t* qrow = sc + 5 * (int64_t)n;
   int32_t* start = sc + 4 * (int64_t)n;  // temporary: prefix sum at scale m
+  if (pp.flags & TABI_F_EXACT_TAIL) {
+    // R6: Alg. 3 with compaction at m/M, row by row.  Exclusive
+    // prefix sums of the offsets (positions) and of the widths (the packer's
+    // flattened column index) over [r0, n); then each row ends before the first
+    // chart c with start(c) - start(a) + Wd(c) > W' -- one block-wide
+    // first-violation search per row.  Every chart keeps scale m/M.
+    __shared__ int32_t row_end[2], row_a;  // row_end alternates by pass (no reset race)
+    int32_t* pwd = sc + 3 * (int64_t)n;
+    int32_t* xs0 = sc;
+    int32_t* xs1 = sc + n;
+    int32_t c0 = 0, c1 = 0;
+    for (int base = r0; base < n; base += kT) {
+      const int s = base + tid;
+      const int32_t a = (s < n && s + 1 < n) ? off[s] : 0;
+      const int32_t b = s < n ? wd[s] : 0;
+      int32_t ea, eb, ic, ta, tb, mc;
+      block_scan3(a, b, 0, ea, eb, ic, ta, tb, mc, S);
+      if (s < n) { start[s] = c0 + ea; pwd[s] = c1 + eb; }
+      c0 += ta;
+      c1 += tb;
+    }
+    if (tid == 0) row_a = r0;
+    __syncthreads();
+    int32_t row = 0;
+    bool ok = true;
+    while (true) {
+      const int32_t a = row_a;
+      if (a >= n) break;
+      const int32_t sa = start[a], wa = pwd[a];
+      int32_t end = n - 1;
+      for (int base = a, pass = 0;; base += kT, pass ^= 1) {
+        if (tid == 0) row_end[pass] = INT32_MAX;
+        __syncthreads();
+        const int s = base + tid;
+        if (s < n && start[s] - sa + wd[s] > Wp) atomicMin(&row_end[pass], s);
+        __syncthreads();
+        const int32_t e = row_end[pass];
+        if (e != INT32_MAX) { end = e - 1; break; }
+        if (base + kT >= n) break;
+      }
+      if (end < a) { ok = false; break; }  // D22: the first chart does not fit
+      for (int s = a + tid; s <= end; s += kT) {
+        qrow[s] = row;
+        xs1[s] = start[s] - sa;
+        xs0[s] = pwd[s] - wa;
+      }
+      row++;
+      __syncthreads();
+      if (tid == 0) row_a = end + 1;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      pp.T.p[m - 1] = (int32_t)(((int64_t)m << 20) / pp.M);  // informational
+      pp.T.state[m - 1] = ok ? TAIL_READY : TAIL_FAIL;
+      cands[m - 1].apre_lo = 0ull;  // every chart keeps m/M: no area at another scale
+      cands[m - 1].apre_hi = 0ull;
+    }
+    return;
+  }
   // pass 1: start = exclusive scan of off over [r0, n); q = floor(start / W')
   int32_t carry = 0;
   for (int base = r0; base < n; base += kT) {

@@ -271,7 +271,7 @@ static bool spec_ok(const tabi_spec* s) {
          s->atlas_h <= TABI_MAX_ATLAS_SIDE && s->gutter >= 0 && s->gutter <= 64 &&
          s->scale_count >= 1 && s->scale_count <= TABI_MAX_SCALES && s->local_aabb_count >= 1 &&
          s->local_aabb_count <= TABI_MAX_LOCAL_AABBS && s->t_opt_bp >= -1 &&
-         s->t_opt_bp <= 10000 && (s->flags & ~31u) == 0;
+         s->t_opt_bp <= 10000 && (s->flags & ~63u) == 0;
 }
 
 namespace {
@@ -503,7 +503,9 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       nl++;
       PackParams pt = pp;
       pt.tail = 1;
-      for (int r = 0; r <= 8; r++) {
+      // (the exact tail, R6, keeps the footprints at m/M: no re-rasterization)
+      const int rounds = (pp.flags & TABI_F_EXACT_TAIL) ? 0 : 9;
+      for (int r = 0; r < rounds; r++) {
         CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));
         launch_profiles(ctx->P, ctx->perm, pt, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
                         (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,

@@ -20,7 +20,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtabi.so")
 
 OK, EINVAL, NO_FIT, ECUDA, ECAPACITY = 0, 1, 2, 3, 4
-F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE, F_NO_OBB = 1, 2, 4, 8, 16
+F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE, F_NO_OBB, F_EXACT_TAIL = (1, 2, 4, 8, 16,
+                                                                            32)
 # Ablation / baseline modes on the same kernels (the ablation table after
 # P:1060): spec overrides for spec_of(cs, **ABLATIONS[name]).
 #   tight_only    = horizontal + vertical compacting, no balance (no knees,

@@ -210,6 +210,25 @@ def test_config4_policy_full_size(orc, ctx):
     _compare_pack(orc, ctx, chartgen.config4(0), check_profiles=0)
 
 
+@pytest.mark.parametrize("t", [100, 1000, 10000])
+@pytest.mark.parametrize("cs", HYBRID, ids=lambda c: c.name)
+def test_exact_tail_parity(orc, ctx, cs, t):
+    """R6 exact-greedy tail: rows, placements (tail charts at
+    m/M, mode 1) and the candidate choice bit-exact against the oracle."""
+    from paper_2602_07782_b200 import F_EXACT_TAIL
+    _compare_pack(orc, ctx, cs, check_profiles=2, t_opt_bp=t, flags=F_EXACT_TAIL)
+
+
+def test_exact_tail_config4_full_size(orc, ctx):
+    from paper_2602_07782_b200 import F_EXACT_TAIL, spec_of
+    cs = chartgen.config4(0)
+    _compare_pack(orc, ctx, cs, check_profiles=0, flags=F_EXACT_TAIL)
+    _, pl, info = ctx.pack(cs.xy, cs.start, spec_of(cs, flags=F_EXACT_TAIL))
+    assert info.prefix_rows > 0 and (pl["mode"] == 1).any()
+    m = ctx.validate(cs.xy, cs.start, pl, cs.atlas_w, cs.atlas_h, gutter=cs.gutter)
+    assert m["overlap"] == m["gutter"] == m["oob"] == 0
+
+
 @pytest.mark.parametrize("wave", ["1", "3", "256"])
 def test_wave_sizes(orc, ctx, wave, monkeypatch):
     """Candidate waves of any size give the exhaustive result: 1 = one candidate
