@@ -10,7 +10,11 @@ charts into a 4096^2 atlas, k = 10, t_opt = 0) with inputs resident in HBM.
 Each rank packs its own atlas per step (seed = rank): weak scaling, no data-path
 collective; value = atlases/s over all ranks = N*K / max-over-
 ranks device time.  L2 is flushed (256 MB write) between steps, outside the
-timed events.  `e2e` repeats the measurement through the public host-pointer
+timed events.  Device time per step = the CUDA-event span tabi_pack records on
+the timed stream around its own enqueued work (tabi_info.device_ms); the
+outer per-step events (which also see the host return from the synchronous
+call) are reported as stream_ms_per_step.  Everything timed runs on one
+dedicated stream, so the flush is complete before a pack starts.  `e2e` repeats the measurement through the public host-pointer
 call (H2D of the chart set and D2H of the placements inside the timed region).
 `--impl reference` times the CPU oracle (the only reference this paper has:
 no code) on the box's host cores.
@@ -252,7 +256,11 @@ def main():
     ctx = Context(local, max_charts=max(max(cs.n_charts for cs in sets), 1024),
                   max_vertices=max(cs.n_vertices for cs in sets) + 16,
                   max_atlas_side=max(max(cs.atlas_w, cs.atlas_h) for cs in sets))
-    stream = torch.cuda.current_stream(dev)
+    # one dedicated stream for everything timed: the L2 flush, the CUDA events and
+    # the packs (torch's default stream is the legacy NULL stream, handle 0,
+    # which the C ABI would read as "the context's own stream")
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     dev_in = [(torch.from_numpy(cs.xy).to(dev), torch.from_numpy(cs.start).to(dev),
                torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)) for cs in sets]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -281,6 +289,7 @@ def main():
     launches = 0
     work_pack = work_prof = 0
     infos = None
+    span_ms = []  # per step: the library's own device span (tabi_info.device_ms)
     barrier(ws)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -289,6 +298,7 @@ def main():
             ev[i][0].record(stream)
             infos = step_dev()
             ev[i][1].record(stream)
+            span_ms.append(sum(info.device_ms for info in infos))
             for info in infos:
                 launches += info.gpu_launches
                 work_pack += info.work_pack
@@ -306,8 +316,14 @@ def main():
             stage += np.array(info.stage_ms[:8])
     torch.cuda.synchronize()
     os.environ["TABI_TIMING"] = "0"
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    # device time per step = the pack's own span on the timed stream (CUDA events
+    # recorded by tabi_pack around its enqueued work, tabi_info.device_ms); the
+    # outer events bracketing each step additionally see the host returning from
+    # the synchronous call (reported as stream_ms_per_step)
+    outer_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms = span_ms
     total_ms = allmax(sum(step_ms), ws)
+    outer_total = allmax(sum(outer_ms), ws)
     ms_per_step = total_ms / args.steps
     value = units_per_step * args.steps / (total_ms / 1000.0)
     p50 = statistics.median(step_ms)
@@ -384,6 +400,7 @@ def main():
                                        if scaling == "weak" else
                                        f"512 atlases per step sharded over {ws} GPU(s)")},
             "p50_ms": p50, "p99_ms": p99,
+            "stream_ms_per_step": outer_total / args.steps,
             "l2_stretch": (info.l2_stretch if len(sets) == 1 else
                            float(np.mean([i.l2_stretch for i in infos]))),
             "scale_index": info.scale_index, "rows": info.rows,

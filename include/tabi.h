@@ -109,6 +109,10 @@ typedef struct {
   int64_t work_pack;              /* fold&push: frontline column visits, all candidates
                                      (push + score per evaluated configuration, + commit) */
   int64_t work_profile;           /* footprint entries evaluated, sum over m, s of Wd + Hd */
+  float device_ms;                /* device time of this call on its stream (CUDA events):
+                                     from the first enqueued operation to the last copy of
+                                     the last wave, host-side call overhead excluded */
+  int32_t reserved;
 } tabi_info;
 
 /* Create a context on `cuda_device`.  max_charts / max_vertices bound every
@@ -131,7 +135,8 @@ void tabi_ctx_destroy(tabi_ctx* ctx);
  *               copies out and returns when `out`/`info` are final.
  *               1: xy, chart_start, out are device pointers; the call still returns
  *               after completion (info needs the winner) but does no bulk copies.
- *   stream      cudaStream_t to run on, or NULL for the context's stream.
+ *   stream      cudaStream_t to run on, or NULL for the context's own (non-blocking)
+ *               stream; cudaStreamLegacy orders the call with the legacy default stream.
  * Ownership: the caller owns every pointer; nothing is retained after return.
  * Deterministic: identical inputs give bit-identical outputs. */
 tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,

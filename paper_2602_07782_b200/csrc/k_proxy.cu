@@ -125,6 +125,11 @@ __device__ void accumulate_slices(const Group<G>& g, const int32_t* A, const int
 }
 
 // D5 merge: x-slice j tightened by y-slices whose x-range meets strip j.
+// The (j, i) tests are spread over the group: with k <= G, lane = part * k + j
+// scans i = part, part + P, ... (P = G / k parts) and the parts' min / max
+// meet by shuffles; with k > G lanes stride over j.  Only min / max, so the
+// order is immaterial.  The strip bounds floor(i ext / k), ceil((i+1) ext / k)
+// are below 2^25: int32.
 template <int G>
 __device__ void merge_slices(const Group<G>& g, const Slices& S, int64_t w, int64_t h, int k) {
   for (int i = g.gl; i < k; i += G) {
@@ -134,37 +139,52 @@ __device__ void merge_slices(const Group<G>& g, const Slices& S, int64_t w, int6
     S.cl1[i] = cdiv_fast((int64_t)(i + 1) * w, k);
   }
   g.sync();
-  for (int j = g.gl; j < k; j += G) {
-    // x-slices
-    int64_t mn = INT64_MAX, mx = INT64_MIN;
-    for (int i = 0; i < k; i++) {
-      if ((int64_t)k * S.lo1[i] <= (int64_t)(j + 1) * w && (int64_t)k * S.hi1[i] >= (int64_t)j * w) {
-        const int64_t f = S.fl0[i], c = S.cl0[i];
-        mn = f < mn ? f : mn;
-        mx = c > mx ? c : mx;
+  const bool split = k <= G;
+  const int P = split ? G / k : 1;
+  const int part = split ? g.gl / k : 0;
+  const int jstep = split ? k : G;
+  for (int jb = 0; jb < k; jb += jstep) {
+    const int j = jb + (split ? g.gl % k : g.gl);
+    const bool act = j < k && part < P;
+    int32_t mn0 = INT32_MAX, mx0 = INT32_MIN, mn1 = INT32_MAX, mx1 = INT32_MIN;
+    if (act) {
+      const int64_t jw0 = (int64_t)j * w, jw1 = (int64_t)(j + 1) * w;
+      const int64_t jh0 = (int64_t)j * h, jh1 = (int64_t)(j + 1) * h;
+      for (int i = part; i < k; i += P) {
+        // x-slices: y-slice i's x-range meets strip j
+        if ((int64_t)k * S.lo1[i] <= jw1 && (int64_t)k * S.hi1[i] >= jw0) {
+          mn0 = min(mn0, (int32_t)S.fl0[i]);
+          mx0 = max(mx0, (int32_t)S.cl0[i]);
+        }
+        // y-slices: x-slice i's y-range meets strip j
+        if ((int64_t)k * S.lo0[i] <= jh1 && (int64_t)k * S.hi0[i] >= jh0) {
+          mn1 = min(mn1, (int32_t)S.fl1[i]);
+          mx1 = max(mx1, (int32_t)S.cl1[i]);
+        }
       }
     }
-    int64_t t = S.lo0[j], b = S.hi0[j];
-    if (mn != INT64_MAX && mn > t) t = mn;
-    if (mx != INT64_MIN && mx < b) b = mx;
-    S.mlo0[j] = (int32_t)t;
-    S.mhi0[j] = (int32_t)b;
-    // y-slices
-    mn = INT64_MAX;
-    mx = INT64_MIN;
-    for (int i = 0; i < k; i++) {
-      if ((int64_t)k * S.lo0[i] <= (int64_t)(j + 1) * h && (int64_t)k * S.hi0[i] >= (int64_t)j * h) {
-        const int64_t f = S.fl1[i], c = S.cl1[i];
-        mn = f < mn ? f : mn;
-        mx = c > mx ? c : mx;
+    for (int q = 1; q < P; q++) {  // uniform: every lane of the group shuffles
+      const int o = q * k;
+      const int32_t a = __shfl_down_sync(g.mask, mn0, o, G), b = __shfl_down_sync(g.mask, mx0, o, G);
+      const int32_t c = __shfl_down_sync(g.mask, mn1, o, G), d = __shfl_down_sync(g.mask, mx1, o, G);
+      if (part == 0 && g.gl + o < P * k) {
+        mn0 = min(mn0, a); mx0 = max(mx0, b);
+        mn1 = min(mn1, c); mx1 = max(mx1, d);
       }
     }
-    t = S.lo1[j];
-    b = S.hi1[j];
-    if (mn != INT64_MAX && mn > t) t = mn;
-    if (mx != INT64_MIN && mx < b) b = mx;
-    S.mlo1[j] = (int32_t)t;
-    S.mhi1[j] = (int32_t)b;
+    if (act && part == 0) {
+      int32_t t = S.lo0[j], b = S.hi0[j];
+      if (mn0 != INT32_MAX && mn0 > t) t = mn0;
+      if (mx0 != INT32_MIN && mx0 < b) b = mx0;
+      S.mlo0[j] = t;
+      S.mhi0[j] = b;
+      t = S.lo1[j];
+      b = S.hi1[j];
+      if (mn1 != INT32_MAX && mn1 > t) t = mn1;
+      if (mx1 != INT32_MIN && mx1 < b) b = mx1;
+      S.mlo1[j] = t;
+      S.mhi1[j] = b;
+    }
   }
 }
 
@@ -217,17 +237,19 @@ __device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, 
   if (vg == 0) {
     S.ob[4 * j + 0] = u0; S.ob[4 * j + 1] = u1; S.ob[4 * j + 2] = v0; S.ob[4 * j + 3] = v1;
   }
-  g.sync();
-  int bj = 0;
-  if (g.gl == 0) {
-    i128 best = -1;
-    for (int a = 0; a < nj; a++) {
-      const i128 area = (i128)(S.ob[4 * a + 1] - S.ob[4 * a]) * (i128)(S.ob[4 * a + 3] - S.ob[4 * a + 2]);
-      if (best < 0 || area < best) { best = area; bj = a; }
-    }
+  // arg-min over the angle lanes (lane j * VG), ties to the smaller j
+  i128 area = (i128)(u1 - u0) * (i128)(v1 - v0);
+  int bj = j;
+  if (j >= nj) area = ~((i128)1 << 127);  // excluded angles: +infinity
+#pragma unroll
+  for (int o = VG; o < G; o <<= 1) {
+    const uint64_t lo = g.xorv((uint64_t)area, o), hi = g.xorv((uint64_t)(area >> 64), o);
+    const int oj = g.xorv(bj, o);
+    const i128 oa = (i128)(((unsigned __int128)hi << 64) | lo);
+    if (oa < area || (oa == area && oj < bj)) { area = oa; bj = oj; }
   }
   bj = __shfl_sync(g.mask, bj, 0, G);
-  g.sync();  // S.ob is reused
+  g.sync();  // S.ob complete before any reader
   return bj;
 }
 

@@ -111,6 +111,7 @@ struct tabi_ctx {
   cudaError_t last_cuda = cudaSuccess;
   bool fused_off = false;  // the cooperative launch was refused once: split kernels from now on
   Validator val;           // tabi_validate scratch (N3)
+  cudaEvent_t span[2] = {nullptr, nullptr};  // tabi_info.device_ms
 };
 
 #define CK(call)                                              \
@@ -144,6 +145,8 @@ static void dfree_all(tabi_ctx* ctx) {
   for (void* p : ps)
     if (p) cudaFree(p);
   ctx->val.release();
+  for (auto& e : ctx->span)
+    if (e) cudaEventDestroy(e);
   void* hs[] = {ctx->h_status, ctx->h_xy, ctx->h_start, ctx->h_out};
   for (void* p : hs)
     if (p) cudaFreeHost(p);
@@ -180,6 +183,8 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
   };
   if (cudaSetDevice(cuda_device) != cudaSuccess) return fail();
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail();
+  if (cudaEventCreate(&ctx->span[0]) != cudaSuccess || cudaEventCreate(&ctx->span[1]) != cudaSuccess)
+    return fail();
   const size_t N = (size_t)max_charts, V = (size_t)max_vertices;
   // d_xy / h_xy: outline (2V floats) followed by the chart offsets (N + 1 ints)
   bool ok = dalloc(&ctx->d_xy, 2 * V + N + 1) == cudaSuccess &&
@@ -559,9 +564,16 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         ctx->gexec = nullptr;
         cudaGraph_t g = nullptr;
         int nl = 0;
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        // capture on the context's own stream (the caller's may be the legacy
+        // default stream, which cannot be captured); launched on the caller's
+        const cudaStream_t user_s = s;
+        s = ctx->stream;
+        const cudaError_t be = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+        if (be != cudaSuccess) s = user_s;
+        CK(be);
         const tabi_status es = enqueue_wave(true, nl);
         const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        s = user_s;
         if (es != TABI_OK) {
           if (g) cudaGraphDestroy(g);
           return es;
@@ -573,14 +585,17 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         ctx->gkey = key;
         ctx->g_launches = nl;
       }
+      CK(cudaEventRecord(ctx->span[0], s));
       CK(cudaGraphLaunch(ctx->gexec, s));
       launches += ctx->g_launches;
     } else {
       int nl = 0;
+      if (prologue) CK(cudaEventRecord(ctx->span[0], s));
       const tabi_status es = enqueue_wave(prologue, nl);
       if (es != TABI_OK) return es;
       launches += nl;
     }
+    CK(cudaEventRecord(ctx->span[1], s));  // device span: first enqueued op .. last copy
     CK(cudaStreamSynchronize(s));
     const Status st = *ctx->h_status;
     if (st.bad_chart != INT32_MAX) {
@@ -635,6 +650,8 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   if (!on_device) memcpy(out, ctx->h_out, sizeof(tabi_placement) * n);  // copied with the status
   tm.finish(info);
   if (info) {
+    float dms = 0.f;
+    if (cudaEventElapsedTime(&dms, ctx->span[0], ctx->span[1]) == cudaSuccess) info->device_ms = dms;
     const Cand& c = ctx->h_cands[win - 1];
     info->scale_index = win;
     // D26: every map is a similarity, so the per-triangle L2 stretch is 1/s

@@ -56,7 +56,7 @@ class Info(C.Structure):
                 ("rows", C.c_int32), ("knees_found", C.c_int32), ("knee_rows", C.c_int32),
                 ("prefix_rows", C.c_int32), ("bad_chart", C.c_int32), ("gpu_launches", C.c_int32),
                 ("stage_ms", C.c_float * 8), ("work_pack", C.c_int64),
-                ("work_profile", C.c_int64)]
+                ("work_profile", C.c_int64), ("device_ms", C.c_float), ("reserved", C.c_int32)]
 
 
 class Validation(C.Structure):
@@ -172,6 +172,16 @@ def spec_of(cs, **kw) -> Spec:
     return make_spec(cs.atlas_w, cs.atlas_h, **d)
 
 
+def _torch_stream(device):
+    """Handle of torch's current stream on `device` for the C ABI.  torch's
+    default stream is the legacy NULL stream (handle 0), which the ABI reads as
+    "the context's own stream"; pass cudaStreamLegacy (1) instead so the pack
+    stays ordered with the torch work that produced its inputs."""
+    import torch
+    h = torch.cuda.current_stream(device).cuda_stream
+    return h if h else 1
+
+
 class Context:
     """One device workspace + stream (``tabi_ctx``)."""
 
@@ -211,7 +221,7 @@ class Context:
             if out is None:
                 out = torch.empty(n * PLACEMENT_DTYPE.itemsize, dtype=torch.uint8, device=xy.device)
             if stream is None:
-                stream = torch.cuda.current_stream(xy.device).cuda_stream
+                stream = _torch_stream(xy.device)
             st = lib().tabi_pack(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], C.byref(spec),
                                  _ptr(out), C.byref(info), 1, C.c_void_p(stream))
         else:
@@ -238,7 +248,7 @@ class Context:
         if on_device:
             import torch
             if stream is None:
-                stream = torch.cuda.current_stream(xy.device).cuda_stream
+                stream = _torch_stream(xy.device)
             st = lib().tabi_validate(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], atlas_w,
                                      atlas_h, gutter, _ptr(placements), C.byref(v), 1,
                                      C.c_void_p(stream))
