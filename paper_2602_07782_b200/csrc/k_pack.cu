@@ -1346,11 +1346,8 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
                  const int32_t* off, const uint8_t* lockbits, const int32_t* hsorted,
                  const int32_t* cand_bad, int32_t* scratch, int64_t pair_cap, int32_t* X,
                  int32_t* Y, uint8_t* mir, Cand* cands, Status* st, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_dyn_smem((const void*)pack_kernel, kMaxDynSmem, attr);
   const int f_words = (pp.Wp + 3) & ~3;
   const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW) + kRW;
   const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;

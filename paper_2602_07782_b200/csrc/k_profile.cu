@@ -117,12 +117,8 @@ void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp
                      int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
                      cudaStream_t s) {
   const size_t dyn = sizeof(int32_t) * (size_t)(kTC * 4 * pp.k) + sizeof(uint32_t) * kRaw;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(profile_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(int32_t) * (kTC * 4 * TABI_KMAX) + sizeof(uint32_t) * kRaw));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_dyn_smem((const void*)profile_tile_kernel, (int)(sizeof(int32_t) * (kTC * 4 * TABI_KMAX) + sizeof(uint32_t) * kRaw), attr);
   dim3 grid((pp.n + kTC - 1) / kTC, pp.B);
   profile_tile_kernel<<<grid, kTT, dyn, s>>>(P, perm, pp, colofs, rowofs, (uint32_t*)dcol,
                                              (uint32_t*)drow, wd, hd, cand_bad, big_list, st);

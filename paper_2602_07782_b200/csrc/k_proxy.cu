@@ -453,12 +453,8 @@ void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float 
   constexpr int per_block = kBlock / G;
   const int blocks = (n + per_block - 1) / per_block;
   const size_t smem = slice_bytes(k) * per_block;
-  static bool attr = false;
-  if (!attr) {  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
-    cudaFuncSetAttribute(proxy_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(slice_bytes(TABI_KMAX) * per_block));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
+  ensure_dyn_smem((const void*)proxy_kernel<G>, (int)(slice_bytes(TABI_KMAX) * per_block), attr);
   proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, flags, qx, qy, P, st);
 }
 

@@ -2,10 +2,13 @@
 //
 // P:139 "sorted in decreasing height order"; ties by the wider chart, then by
 // chart index.  Three exact paths by N:
-//   N <= 4096    bitonic sort in one CTA's shared memory of the packed unique
-//                keys (h, w, index) -- a few microseconds;
-//   N <= 2^17    rank sort: rank(i) = #{j : (key_j, j) < (key_i, i)} over a
-//                2-D grid of (key block, key tile), then a scatter;
+//   N <= 2048    bitonic network in registers of one CTA (shuffles below
+//                distance 64) on the packed unique keys (h, w, index);
+//   N <= 2^17    chunked: every CTA sorts 2048 (key, index) pairs the same way,
+//                then each element's rank = its rank in its chunk + binary-
+//                search counts in the other chunks, and a scatter;
+//                (test knobs: the smem bitonic for N <= 4096 and an O(N^2)
+//                rank count, both exact);
 //   larger       STABLE LSD radix sort on ((hmax - h) << bw) | (wmax - w) with
 //                the chart index as payload, one CTA of 1024 threads: per-tile
 //                digit ranks from warp match masks + per-warp digit counts.
@@ -230,6 +233,115 @@ bitonic_reg_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ w
   }
 }
 
+// 2048 < N <= 2^17: each CTA sorts a chunk of 2048 (key, index) pairs with the
+// register bitonic network above, then every element's final position is its
+// rank in its own chunk plus, for every other chunk, the number of pairs
+// below it (binary searches, 16 chunks at a time in lockstep so their loads
+// overlap).  Pairs are unique (the index), so the ranks are a permutation.
+constexpr int kChunk = 2 * kT;
+__device__ __forceinline__ bool pair_lt(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(kT, 1)
+chunk_sort_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n,
+                  uint64_t* ck, int32_t* ci, const Status* st) {
+  __shared__ uint64_t key[kChunk];
+  __shared__ int32_t idx[kChunk];
+  if (st->bad_chart != INT32_MAX) return;
+  const int t = threadIdx.x, base = blockIdx.x * kChunk, cn = min(kChunk, n - base);
+  uint64_t v[2];
+  int32_t x[2];
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const int i = 2 * t + s;
+    v[s] = i < cn ? order_key(hh[base + i], ww[base + i]) : ~0ull;
+    x[s] = i < cn ? base + i : INT32_MAX;
+  }
+  int P = 2;
+  while (P < cn) P <<= 1;
+  for (int size = 2; size <= P; size <<= 1) {
+    int stride = size >> 1;
+    if (stride >= 64) {
+      key[2 * t] = v[0]; key[2 * t + 1] = v[1];
+      idx[2 * t] = x[0]; idx[2 * t + 1] = x[1];
+      __syncthreads();
+      for (; stride >= 64; stride >>= 1) {
+        const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const uint64_t a = key[lo], b = key[hi];
+        const int32_t ia = idx[lo], ib = idx[hi];
+        if (pair_lt(b, ib, a, ia) == ((lo & size) == 0)) {
+          key[lo] = b; key[hi] = a;
+          idx[lo] = ib; idx[hi] = ia;
+        }
+        __syncthreads();
+      }
+      v[0] = key[2 * t]; v[1] = key[2 * t + 1];
+      x[0] = idx[2 * t]; x[1] = idx[2 * t + 1];
+      __syncthreads();
+    }
+    const bool asc = ((2 * t) & size) == 0;
+    for (; stride >= 2; stride >>= 1) {
+      const int d = stride >> 1;
+      const bool keep_min = (((2 * t) & stride) == 0) == asc;
+#pragma unroll
+      for (int s = 0; s < 2; s++) {
+        const uint64_t p = __shfl_xor_sync(0xffffffffu, v[s], d);
+        const int32_t px = __shfl_xor_sync(0xffffffffu, x[s], d);
+        const bool plt = pair_lt(p, px, v[s], x[s]);
+        if (keep_min == plt) { v[s] = p; x[s] = px; }
+      }
+    }
+    if (pair_lt(v[1], x[1], v[0], x[0]) == asc) {
+      const uint64_t tv = v[0]; v[0] = v[1]; v[1] = tv;
+      const int32_t tx = x[0]; x[0] = x[1]; x[1] = tx;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const int i = 2 * t + s;
+    if (i < cn) { ck[base + i] = v[s]; ci[base + i] = x[s]; }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+chunk_rank_kernel(const uint64_t* __restrict__ ck, const int32_t* __restrict__ ci, int32_t n,
+                  int32_t* perm, const Status* st) {
+  if (st->bad_chart != INT32_MAX) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const uint64_t k = ck[e];
+  const int32_t i = ci[e];
+  const int c = e / kChunk, nch = (n + kChunk - 1) / kChunk;
+  int rank = e - c * kChunk;
+  for (int g0 = 0; g0 < nch; g0 += 16) {
+    int lo[16], hi[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int c2 = g0 + q;
+      lo[q] = c2 < nch && c2 != c ? c2 * kChunk : 0;
+      hi[q] = c2 < nch && c2 != c ? min(n, c2 * kChunk + kChunk) : 0;
+    }
+    // lower bound: first position whose pair is not below (k, i)
+    for (int step = 0; step < 12; step++) {
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        if (lo[q] < hi[q]) {
+          const int mid = (lo[q] + hi[q]) >> 1;
+          if (pair_lt(ck[mid], ci[mid], k, i)) lo[q] = mid + 1;
+          else hi[q] = mid;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int c2 = g0 + q;
+      if (c2 < nch && c2 != c) rank += lo[q] - c2 * kChunk;
+    }
+  }
+  perm[rank] = i;
+}
+
 // N <= 2^17: rank of key i = #{j : (key_j, j) < (key_i, i)}, counted over a 2-D
 // grid of (i block, j tile) with one atomicAdd per thread and tile, then a
 // scatter perm[rank[i]] = i.
@@ -396,17 +508,26 @@ void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* 
 
 int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
                 int32_t* perm2, const Status* st, cudaStream_t s) {
-  // TABI_SORT=bitonic|rank|radix forces a path (tests cover all three)
+  // TABI_SORT=bitonic|chunk|rank|radix forces a path (tests cover all four)
   const char* force = getenv("TABI_SORT");
   const bool want_rank = force && strcmp(force, "rank") == 0;
   const bool want_radix = force && strcmp(force, "radix") == 0;
-  if (n <= 2 * kT && !want_rank && !want_radix && !(force && strcmp(force, "bitonic") == 0)) {
+  const bool want_chunk = force && strcmp(force, "chunk") == 0;
+  if (n <= 2 * kT && !want_rank && !want_radix && !want_chunk &&
+      !(force && strcmp(force, "bitonic") == 0)) {
     bitonic_reg_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, perm, st);
     return 1;
   }
-  if (n <= kBitonicMax && !want_rank && !want_radix) {
+  if (n <= kBitonicMax && force && strcmp(force, "bitonic") == 0) {
     bitonic_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, perm, st);
     return 1;
+  }
+  if (n <= kRankMax && !want_radix && !want_rank) {
+    // chunked bitonic + merge ranks (ck in keys, ci in perm2)
+    const int nch = (n + kChunk - 1) / kChunk;
+    chunk_sort_kernel<<<nch, kT, 0, s>>>(P.h, P.w, n, keys, perm2, st);
+    chunk_rank_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, perm2, n, perm, st);
+    return 2;
   }
   if (n <= kRankMax && !want_radix) {
     int32_t* rank = (int32_t*)keys2;

@@ -435,8 +435,21 @@ void launch_tail_layout(const PackParams& pp, const int32_t* wd, const int32_t* 
                         int32_t* scratch, int64_t pair_cap, const Status* st, cudaStream_t s);
 }  // namespace tabi
 
+#include <atomic>
 #include <string>
 namespace tabi {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, and batch mode drives several devices from
+// several host threads.
+inline void ensure_dyn_smem(const void* fn, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 // N3 GPU validator (k_validate.cu): device scratch that grows on demand and
 // persists across calls on one context.
 struct Validator {

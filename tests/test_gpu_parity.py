@@ -326,12 +326,13 @@ def test_pack_batch_equals_single_packs(ctx):
     c3.close()
 
 
-@pytest.mark.parametrize("path", ["default", "bitonic", "rank", "radix"])
+@pytest.mark.parametrize("path", ["default", "bitonic", "chunk", "rank", "radix"])
 def test_sort_paths_with_ties(orc, ctx, path, monkeypatch):
     """D9 order (h desc, w desc, index asc) through each sort path (default:
-    the register bitonic network for N <= 2048; TABI_SORT forces the smem
-    bitonic, rank or radix path), on inputs full of exact (h, w) ties: index
-    order must decide them."""
+    the register bitonic network for N <= 2048, the chunked bitonic + merge
+    ranks above; TABI_SORT forces the smem bitonic (N <= 4096), chunked, rank or
+    radix path), on inputs full of exact (h, w) ties: index order must decide
+    them.  N = 900 (one chunk) and 5000 (three chunks, ties across chunks)."""
     import oracle
     from paper_2602_07782_b200 import spec_of
     if path == "default":
@@ -339,16 +340,17 @@ def test_sort_paths_with_ties(orc, ctx, path, monkeypatch):
     else:
         monkeypatch.setenv("TABI_SORT", path)
     rng = np.random.default_rng(5)
-    polys = []
-    for i in range(900):
-        w, h = [(8, 8), (8, 12), (12, 8), (5, 20)][rng.integers(0, 4)]
-        if rng.random() < 0.2:
-            w, h = int(rng.integers(3, 30)), int(rng.integers(3, 30))
-        polys.append([(0, 0), (w, 0), (w, h), (0, h)])
-    cs = chartgen.from_polygons(polys, 512, 512)
-    ctx.pack(cs.xy, cs.start, spec_of(cs, scale_count=4))
-    _, px, _ = oracle.build_proxies(cs.xy, cs.start, cs.local_aabb_count, (1.0, 1.0))
-    assert np.array_equal(ctx.perm(cs.n_charts), oracle.sort_order(px))
+    for n in (900, 5000):
+        polys = []
+        for i in range(n):
+            w, h = [(8, 8), (8, 12), (12, 8), (5, 20)][rng.integers(0, 4)]
+            if rng.random() < 0.2:
+                w, h = int(rng.integers(3, 30)), int(rng.integers(3, 30))
+            polys.append([(0, 0), (w, 0), (w, h), (0, h)])
+        cs = chartgen.from_polygons(polys, 2048, 2048)
+        ctx.pack(cs.xy, cs.start, spec_of(cs, scale_count=4))
+        _, px, _ = oracle.build_proxies(cs.xy, cs.start, cs.local_aabb_count, (1.0, 1.0))
+        assert np.array_equal(ctx.perm(cs.n_charts), oracle.sort_order(px)), n
     _compare_pack(orc, ctx, chartgen.config2(2), check_profiles=0)
 
 
