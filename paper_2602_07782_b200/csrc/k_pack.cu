@@ -36,6 +36,7 @@ namespace {
 constexpr int kNT = 512;
 constexpr int kNW = kNT / 32;
 constexpr int kRW = 2048;          // charts per row window
+constexpr int kPWN = 1024;         // sorted positions in the fold's position window
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for static Smem
 #ifndef TABI_PACK_NT
 #define TABI_PACK_NT 512
@@ -67,6 +68,8 @@ struct Smem {
   int32_t fold_hi, next_a0;      // fold's scanned end; colofs of the next row start (or -1)
   int32_t changed3[3];           // Alg. 1 rotating change flags
   int32_t abort;                 // sequential fused mode: a higher candidate won
+  int32_t pw_b, pw_e, pw_c0, pw_c1;  // fold position window (see pw_fill)
+  int32_t w_fold;                    // W.* hold the fold's scalars of the row start
   int32_t prefix_rows, switched;
   unsigned long long knee_key;
   unsigned long long work;
@@ -325,7 +328,17 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   W.rbot = W.rY + 4 * kRW;
   W.rhs = W.rbot + kRW;
   W.rlk = (uint8_t*)(W.rhs + kRW);
-  W.prof = (uint32_t*)(W.rlk + kRW);
+  struct {
+    int32_t *p0, *p1, *wd, *co, *hs;
+    uint8_t* lk;
+  } PW;
+  PW.p0 = (int32_t*)(W.rlk + kRW);
+  PW.p1 = PW.p0 + kPWN;
+  PW.wd = PW.p1 + kPWN;
+  PW.co = PW.wd + kPWN;
+  PW.hs = PW.co + kPWN;
+  PW.lk = (uint8_t*)(PW.hs + kPWN);
+  W.prof = (uint32_t*)(PW.lk + kPWN);
   W.prof_cap = prof_cap;
 
   const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
@@ -347,6 +360,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
     S.next_a0 = 0; S.fold_hi = 0; S.pf_out = 0; S.abort = 0;
+    S.pw_b = 0; S.pw_e = 0; S.pw_c0 = 0; S.pw_c1 = 0; S.w_fold = 0;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
     S.prefix_rows = 0;
@@ -391,7 +405,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // the fold already wrote the scalars of the row's first kRW charts
     // (positions below S.fold_hi), footprint offsets included
     const bool fw = !prefix_mode && ws0 == S.row_start;
-    const bool have = fw && nwin <= kRW;
+    // (only while W still holds the fold's scalars: a later window of a long
+    // row overwrites them)
+    const bool have = fw && nwin <= kRW && S.w_fold != 0;
     const int32_t c0 = have ? W.rco[0] : colofs[ws0];
     const int32_t c1 = we >= n ? cols_total
                                : (fw && we < S.fold_hi && nwin < kRW) ? W.rco[nwin] : colofs[we];
@@ -413,6 +429,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     }
     if (!hit && !pg && tid == 0) bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
     if (tid == 0) {
+      if (!have) S.w_fold = 0;
       S.win_s0 = ws0; S.win_e = we;
       S.pglobal = hit ? 0 : pg;
       S.a0 = hit ? S.pf_a0 : a0;
@@ -422,6 +439,66 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       phase ^= 1u;
     }
     pk_sync();
+  };
+
+  // Position window for the fold (non-prefix mode): sorted positions
+  // [S.pw_b, S.pw_e) with the exclusive prefix sums of widths (p0) and of the
+  // compaction offsets (p1) from S.pw_b, and the per-position scalars the row
+  // window needs.  Filled (or appended to) by block scans over published
+  // positions only; only its first chunk may wait for the rasterizers.
+  // mode 0: a new window at `from` (prefix frame restarts at 0); 1: append at
+  // S.pw_e; 2: slide -- a new window at `from` = S.pw_e that keeps the prefix
+  // frame (a row longer than the window continues in the same frame).
+  auto pw_fill = [&](int from, int mode) -> bool {
+    const bool append = mode == 1;
+    int count = append ? S.pw_e - S.pw_b : 0;
+    const int count0 = count;
+    const int b0 = append ? S.pw_b : from;
+    int32_t c0 = mode ? S.pw_c0 : 0, c1 = mode ? S.pw_c1 : 0;
+    int base = append ? S.pw_e : from;
+    int lim = -1;
+    while (count < kPWN && base < n) {
+      if (base > lim) {
+        if (count > count0) break;  // only the first chunk waits
+        lim = wait_ready(base);
+        if (lim == -2) return false;  // beaten (S.abort)
+#ifdef TABI_PHASE_TRACE
+        if (rd.flags && jslot == 0 && base == 0 && tid == 0) st->tfirst[2] = gtime();
+#endif
+      }
+      const int cnt = min(min(kPT, lim - base + 1), kPWN - count);
+      const int s = base + tid;
+      const bool valid = tid < cnt;
+      const int32_t w_s = valid ? wd[s] : 0;
+      const int32_t a1 = valid ? off[s] : 0;
+      // fused mode: a chart that cannot fit the dilated atlas at this scale
+      // makes the candidate fail (it must be placed in some row)
+      if (rd.flags && valid && (w_s > Wp || hd[s] > Hp)) S.fail = 1;
+      int32_t e0, e1, t0, t1;
+      block_scan2(w_s, a1, e0, e1, t0, t1, S);
+      if (valid) {
+        const int i = count + tid;
+        PW.p0[i] = c0 + e0;
+        PW.p1[i] = c1 + e1;
+        PW.wd[i] = w_s;
+        PW.co[i] = colofs[s];
+        PW.hs[i] = hsorted[s];
+        PW.lk[i] = lk[s];
+      }
+      c0 += t0;
+      c1 += t1;
+      count += cnt;
+      base += cnt;
+    }
+    pk_sync();
+    if (tid == 0) {
+      S.pw_b = b0;
+      S.pw_e = b0 + count;
+      S.pw_c0 = c0;
+      S.pw_c1 = c1;
+    }
+    pk_sync();
+    return true;
   };
 
   while (true) {
@@ -542,57 +619,59 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         pk_sync();
       }
     } else {
-      int32_t carry0 = 0, carry1 = 0;
-      for (int base = rs;;) {
-        const int lim = wait_ready(base);
-        if (lim == -2) break;  // beaten (S.abort): leave the row loop below
-#ifdef TABI_PHASE_TRACE
-        if (rd.flags && jslot == 0 && rs == 0 && base == 0 && tid == 0) st->tfirst[2] = gtime();
-#endif
-        const int cnt = min(kPT, lim - base + 1);  // positions [base, base + cnt)
-        if (tid < 4) S.fmin[tid] = INT32_MAX;
-        const int s = base + tid;
-        const bool valid = tid < cnt;
-        const int32_t w_s = valid ? wd[s] : 0;
-        const int32_t a1 = valid ? off[s] : 0;
-        // fused mode: a chart that cannot fit the dilated atlas at this scale
-        // makes the candidate fail (it must be placed in some row)
-        if (rd.flags && valid && (w_s > Wp || hd[s] > Hp)) S.fail = 1;
-        int32_t e0, e1, t0, t1;
-        block_scan2(w_s, a1, e0, e1, t0, t1, S);
-        const int32_t x0 = carry0 + e0, x1 = carry1 + e1;
-        if (valid) {
-          xs0[s] = x0;
-          xs1[s] = x1;
-          if (s - rs < kRW) {  // the row's window scalars, straight into smem
-            W.rx0[s - rs] = x0;
-            W.rx1[s - rs] = x1;
-            W.rwd[s - rs] = w_s;
-            W.rco[s - rs] = colofs[s];
-            W.rhs[s - rs] = hsorted[s];
-            W.rlk[s - rs] = lk[s];
+      // Fold over the position window: its exclusive prefix sums of widths
+      // and offsets were scanned when the window was filled, so a row's fold
+      // positions are differences (x(s) = P(s) - P(rs)) -- no block scan and no
+      // global loads while the row start stays inside the window.
+      bool beaten = false;
+      if (rs < S.pw_b || rs >= S.pw_e) beaten = !pw_fill(rs, 0);
+      // the row start's prefixes (the frame stays fixed while the row is folded)
+      const int32_t r0 = beaten ? 0 : PW.p0[rs - S.pw_b], r1 = beaten ? 0 : PW.p1[rs - S.pw_b];
+      int sc = rs;  // next position to examine
+      while (!beaten) {
+        const int pb = S.pw_b, pe = S.pw_e;
+        for (; sc < pe; sc = min(sc + kPT, pe)) {  // (sc ends at pe: an append resumes there)
+          if (tid < 4) S.fmin[tid] = INT32_MAX;
+          pk_sync();
+          const int s = sc + tid;
+          if (s < pe) {
+            const int i = s - pb;
+            const int32_t w_s = PW.wd[i], x0 = PW.p0[i] - r0, x1 = PW.p1[i] - r1;
+            xs0[s] = x0;
+            xs1[s] = x1;
+            if (s - rs < kRW) {  // the row's window scalars, straight into smem
+              W.rx0[s - rs] = x0;
+              W.rx1[s - rs] = x1;
+              W.rwd[s - rs] = w_s;
+              W.rco[s - rs] = PW.co[i];
+              W.rhs[s - rs] = PW.hs[i];
+              W.rlk[s - rs] = PW.lk[i];
+            }
+            if (x0 + w_s > Wp) atomicMin(&S.fmin[0], s);
+            if (x1 + w_s > Wp) atomicMin(&S.fmin[1], s);
+            if (x0 + w_s > kb - ka) atomicMin(&S.fmin[2], s);
+            if (x1 + w_s > kb - ka) atomicMin(&S.fmin[3], s);
           }
-          if (x0 + w_s > Wp) atomicMin(&S.fmin[0], s);
-          if (x1 + w_s > Wp) atomicMin(&S.fmin[1], s);
-          if (x0 + w_s > kb - ka) atomicMin(&S.fmin[2], s);
-          if (x1 + w_s > kb - ka) atomicMin(&S.fmin[3], s);
-        }
-        pk_sync();
-        if (tid == 0) {
-          for (int q = 0; q < 4; q++)
-            if (S.endv[q] == INT32_MIN && S.fmin[q] != INT32_MAX) S.endv[q] = S.fmin[q] - 1;
-          if (S.endv[1] != INT32_MIN || base + cnt >= n) {
+          pk_sync();
+          if (tid == 0) {
             for (int q = 0; q < 4; q++)
-              if (S.endv[q] == INT32_MIN) S.endv[q] = n - 1;
-            S.done = 1;
-            S.fold_hi = base + cnt;  // W.* hold positions [rs, min(fold_hi, rs + kRW))
+              if (S.endv[q] == INT32_MIN && S.fmin[q] != INT32_MAX) S.endv[q] = S.fmin[q] - 1;
+            const int hi = min(sc + kPT, pe);
+            if (S.endv[1] != INT32_MIN || hi >= n) {
+              for (int q = 0; q < 4; q++)
+                if (S.endv[q] == INT32_MIN) S.endv[q] = n - 1;
+              S.done = 1;
+              S.fold_hi = hi;  // W.* hold positions [rs, min(fold_hi, rs + kRW))
+              S.w_fold = 1;
+            }
           }
+          pk_sync();
+          if (S.done) break;
         }
-        pk_sync();
         if (S.done) break;
-        carry0 += t0;
-        carry1 += t1;
-        base += cnt;
+        // the row reaches past the window: append, or slide it on when full
+        const bool full = S.pw_e - S.pw_b >= kPWN;
+        beaten = !pw_fill(S.pw_e, full ? 2 : 1);
       }
     }  // !prefix_mode
     if (S.abort) break;  // beaten while waiting for tiles (set before a barrier)
@@ -988,7 +1067,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       S.row_start = endS + 1;
       if (rd.flags && pp.early && wj < jslot) S.abort = 1;  // checked at the next row start
       const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
-      S.next_a0 = (!prefix_mode && nx < n && nx < S.fold_hi && nx - rs < kRW) ? W.rco[nx - rs] : -1;
+      S.next_a0 = (!prefix_mode && S.w_fold && nx < n && nx < S.fold_hi && nx - rs < kRW)
+                      ? W.rco[nx - rs] : -1;
     }
     pk_sync();
     phase_mark(7);
@@ -1349,7 +1429,8 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
   static std::atomic<unsigned long long> attr{0};
   ensure_dyn_smem((const void*)pack_kernel, kMaxDynSmem, attr);
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW) + kRW;
+  const size_t fixed =
+      sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN) + kRW + kPWN;
   const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   pack_kernel<<<pp.B, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
                                              hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
@@ -1387,7 +1468,8 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s) {
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW) + kRW;
+  const size_t fixed =
+      sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN) + kRW + kPWN;
   int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy, tstart, tix};
   PackParams p = pp;

@@ -262,6 +262,20 @@ def test_large_chart_path(orc, ctx):
     _compare_pack(orc, ctx, cs, check_profiles=4, scale_count=8)
 
 
+def test_long_row_window(orc, ctx):
+    """Rows longer than the fold's position window (1,024 sorted positions):
+    3,000 small charts fit one 16,384-wide row, so the fold slides its window
+    on within the row (same prefix frame); also ragged chart sizes."""
+    rng = np.random.default_rng(3)
+    polys = []
+    for _ in range(3000):
+        a, b = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        polys.append([(0, 0), (a, 0), (a, b), (0, b)])
+    cs = chartgen.from_polygons(polys, 16384, 64)
+    _compare_pack(orc, ctx, cs, check_profiles=0)
+    _compare_pack(orc, ctx, cs, check_profiles=0, scale_count=8)
+
+
 def test_lock1_both_modes(orc, ctx):
     A = [(0, 0), (20, 0), (20, 150), (0, 150)]
     c0 = [(0, 0), (10, 0), (10, 45), (40, 45), (40, 47), (10, 47), (10, 100), (0, 100)]
