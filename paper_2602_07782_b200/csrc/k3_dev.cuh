@@ -269,8 +269,8 @@ struct Scale {
 // TT threads (8 per chart during setup).  Charts that fit the dilated atlas but
 // have more than kRaw raw cells are left for a warp-per-chart pass: their tile
 // index is flagged in big[ci].  Writes wd/hd, the footprint slots, cand_bad.
-struct NoMark {
-  __device__ void operator()() const {}
+struct NoMark {  // mark(0): setup done; mark(1): a chunk's raw pass done
+  __device__ void operator()(int) const {}
 };
 
 template <int TC, int TT, int RAW, class Sync, class Mark = NoMark>
@@ -318,7 +318,7 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   sync();
   if (ci < nt && CH[ci].small) chart_setup(CH[ci], tabs + ci * 4 * k, P, k, num, SC, r);
   sync();
-  setup_done();
+  setup_done(0);
   uint32_t* colb = dcol + (int64_t)(m - 1) * pp.col_cap;
   uint32_t* rowb = drow + (int64_t)(m - 1) * pp.row_cap;
   int cb = 0;
@@ -382,6 +382,7 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
       }
     }
     sync();
+    setup_done(1);
     for (int o = tid; o < nout; o += TT) {  // dilation over the flattened outputs
       int lo = 0, hi = nc - 1;
       while (lo < hi) {

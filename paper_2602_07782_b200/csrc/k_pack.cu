@@ -1225,18 +1225,24 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 #else
   auto rmark = [](int) {};
 #endif
+  // the first G items go to the G raster groups statically (no queue round
+  // trip before the first -- most urgent -- tiles); the queue hands out the rest
+  const int G = ((int)gridDim.x - pp.B) * kRG;
+  int first_it = ((int)blockIdx.x - pp.B) * kRG + grp;
   while (true) {
     // (fetching the next item ahead would hide this round trip, but lets a
     // busy CTA sit on an early tile the packers are waiting for)
     if (gt == 0) {
-      const int it0 = atomicAdd(&st->work_next, 1);
+      const int it0 = first_it >= 0 ? first_it : G + atomicAdd(&st->work_next, 1);
       misc[0] = it0;
       // sequential mode: drop items of candidates below a successful one
-      // (decided once, by the leader, so the group branches uniformly)
+      // (decided once, by the leader, so the group branches uniformly); the
+      // top candidate's items (slot 0) can never be beaten
       const int j0 = !pp.early || pp.B == 1 ? it0 % pp.B
                      : it0 < T ? 0 : 1 + (it0 - T) % (pp.B - 1);  // item -> slot, as below
-      misc[4] = pp.early && *(volatile int32_t*)&st->win_j < j0;
+      misc[4] = pp.early && j0 > 0 && *(volatile int32_t*)&st->win_j < j0;
     }
+    first_it = -1;
     gsync();
     const int it = misc[0];
     const bool dropped = misc[4] != 0;
@@ -1273,10 +1279,11 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
                                        ra.hd, ra.cand_bad, m, s0, sc, CH, cells, cpre, opre,
                                        &misc[1], big, tabs, raw, nt, gt, gsync,
-                                       [&]() {
-                                         rmark(6);
+                                       [&](int w) {
+                                         if (w == 0) rmark(6);
 #ifdef TABI_PHASE_TRACE
-                                         if (gt == 0 && t == 0 && j == 0) st->tfirst[5] = gtime();
+                                         if (gt == 0 && t == 0 && j == 0)
+                                           st->tfirst[w == 0 ? 5 : 4] = gtime();
 #endif
                                        });
     rmark(1);

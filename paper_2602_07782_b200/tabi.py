@@ -313,7 +313,7 @@ class Context:
                                        "publish", "setup"), (int(v) for v in r16[:7])))
         d["alg1_passes"] = int(r16[7])  # trace build: Alg. 1 passes of wave slot 0
         d["first_row_ns"] = dict(zip(("tile0_cells", "tile0_published", "fold_unblocked",
-                                      "row0_done", "-", "tile0_setup", "tile0_pairs_start",
+                                      "row0_done", "tile0_raw", "tile0_setup", "tile0_pairs_start",
                                       "tile0_pairs_end"), (int(v) for v in r16[8:16])))
         d["phases"] = dict(zip(("knee", "fold", "hc_locks", "push", "alg1", "score", "commit",
                                 "findknee", "push_stage", "commit_stage"),
