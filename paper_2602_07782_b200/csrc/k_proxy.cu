@@ -47,21 +47,10 @@ struct Group {
   __device__ void sync() const { __syncwarp(mask); }
   template <class T>
   __device__ T xorv(T v, int o) const { return __shfl_xor_sync(mask, v, o, G); }
-  __device__ int32_t min32(int32_t v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v = min(v, xorv(v, o));
-    return v;
-  }
-  __device__ int32_t max32(int32_t v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v = max(v, xorv(v, o));
-    return v;
-  }
-  __device__ uint32_t sumu(uint32_t v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v += xorv(v, o);
-    return v;
-  }
+  // 32-bit group reductions: one REDUX over the group's lanes (the mask)
+  __device__ int32_t min32(int32_t v) const { return __reduce_min_sync(mask, v); }
+  __device__ int32_t max32(int32_t v) const { return __reduce_max_sync(mask, v); }
+  __device__ uint32_t sumu(uint32_t v) const { return __reduce_add_sync(mask, v); }
   __device__ int64_t sum64(int64_t v) const {
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) v += xorv(v, o);
