@@ -361,6 +361,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
     S.next_a0 = 0; S.fold_hi = 0; S.pf_out = 0; S.abort = 0;
     S.pw_b = 0; S.pw_e = 0; S.pw_c0 = 0; S.pw_c1 = 0; S.w_fold = 0;
+    for (int q = 0; q < 4; q++) S.fmin[q] = INT32_MAX;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
     S.prefix_rows = 0;
@@ -595,11 +596,28 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       mx = warp_max(mx);
       if (lane == 0) atomicMax(&S.conc_max, mx);
     }
+    // ---- level 1 of the hierarchical choice: HC iff it fits more,
+    // by thread 0 once the fold's row ends are known ---------------------------
+    auto hc_select = [&]() {
+      S.hcsel[0] = (!no_hc && S.endv[1] > S.endv[0]) ? 1 : 0;
+      S.hcsel[1] = (!no_hc && S.endv[3] > S.endv[2]) ? 1 : 0;
+      if (prefix_mode) { S.hcsel[0] = 1; S.hcsel[1] = 0; }  // HC always on in the tail (P:322)
+      const int32_t ea = S.endv[S.hcsel[0]];
+      const int32_t ek = S.endv[2 + S.hcsel[1]];
+      S.knee_ok = kv && ek >= rs;
+      S.end_cfg[0] = S.end_cfg[1] = ea;
+      S.end_cfg[2] = S.end_cfg[3] = ek;
+      if (ea < rs) S.fail = 1;  // first chart wider than the atlas (D22)
+      for (int q = 0; q < 4; q++) S.newmax[q] = INT32_MIN;
+      S.npairs = 0;
+      S.pair_overflow = 0;
+    };
     // ---- Alg. 3 FoldRow for both HC settings and both folds --------------
+    // (no barrier here: in the non-prefix fold only thread 0 reads these
+    // before the fold's own barriers)
     if (tid < 4) S.endv[tid] = INT32_MIN;
     if (tid == 0) { S.done = 0; S.win_s0 = -1; S.win_e = -1; }
-    pk_sync();
-    pf_pending = S.pf_out != 0 && !prefix_mode;
+    if (prefix_mode) pk_sync();
     if (prefix_mode) {
       // prefix rows were laid out by the tail kernels (positions in xs0/xs1);
       // the row is the run of equal row ids starting at rs
@@ -630,9 +648,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       int sc = rs;  // next position to examine
       while (!beaten) {
         const int pb = S.pw_b, pe = S.pw_e;
+        // (S.fmin[] are INT32_MAX here: reset by thread 0 after each use)
         for (; sc < pe; sc = min(sc + kPT, pe)) {  // (sc ends at pe: an append resumes there)
-          if (tid < 4) S.fmin[tid] = INT32_MAX;
-          pk_sync();
           const int s = sc + tid;
           if (s < pe) {
             const int i = s - pb;
@@ -646,6 +663,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               W.rco[s - rs] = PW.co[i];
               W.rhs[s - rs] = PW.hs[i];
               W.rlk[s - rs] = PW.lk[i];
+#pragma unroll
+              for (int q = 0; q < 5; q++) W.rY[q * kRW + (s - rs)] = INT32_MIN;  // push init
             }
             if (x0 + w_s > Wp) atomicMin(&S.fmin[0], s);
             if (x1 + w_s > Wp) atomicMin(&S.fmin[1], s);
@@ -654,8 +673,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           }
           pk_sync();
           if (tid == 0) {
-            for (int q = 0; q < 4; q++)
+            for (int q = 0; q < 4; q++) {
               if (S.endv[q] == INT32_MIN && S.fmin[q] != INT32_MAX) S.endv[q] = S.fmin[q] - 1;
+              S.fmin[q] = INT32_MAX;
+            }
             const int hi = min(sc + kPT, pe);
             if (S.endv[1] != INT32_MIN || hi >= n) {
               for (int q = 0; q < 4; q++)
@@ -663,6 +684,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               S.done = 1;
               S.fold_hi = hi;  // W.* hold positions [rs, min(fold_hi, rs + kRW))
               S.w_fold = 1;
+              hc_select();  // published by the barrier below
             }
           }
           pk_sync();
@@ -674,24 +696,16 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         beaten = !pw_fill(S.pw_e, full ? 2 : 1);
       }
     }  // !prefix_mode
+    // (the row-top prefetch flag: published by the fold's barriers; set before
+    // any exit so the end of the packer drains a copy still in flight)
+    pf_pending = S.pf_out != 0 && !prefix_mode;
     if (S.abort) break;  // beaten while waiting for tiles (set before a barrier)
     phase_mark(1);
-    // ---- level 1 of the hierarchical choice: HC iff it fits more --
-    if (tid == 0) {
-      S.hcsel[0] = (!no_hc && S.endv[1] > S.endv[0]) ? 1 : 0;
-      S.hcsel[1] = (!no_hc && S.endv[3] > S.endv[2]) ? 1 : 0;
-      if (prefix_mode) { S.hcsel[0] = 1; S.hcsel[1] = 0; }  // HC always on in the tail (P:322)
-      const int32_t ea = S.endv[S.hcsel[0]];
-      const int32_t ek = S.endv[2 + S.hcsel[1]];
-      S.knee_ok = kv && ek >= rs;
-      S.end_cfg[0] = S.end_cfg[1] = ea;
-      S.end_cfg[2] = S.end_cfg[3] = ek;
-      if (ea < rs) S.fail = 1;  // first chart wider than the atlas (D22)
-      for (int q = 0; q < 4; q++) S.newmax[q] = INT32_MIN;
-      S.npairs = 0;
-      S.pair_overflow = 0;
+    // (the non-prefix fold ran hc_select in its last step, before a barrier)
+    if (prefix_mode) {
+      if (tid == 0) hc_select();
+      pk_sync();
     }
-    pk_sync();
     if (S.fail) break;
     const int32_t knee_ok = S.knee_ok;
     const int32_t hc0 = S.hcsel[0], hc1 = S.hcsel[1];
@@ -770,11 +784,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
       stage(ws0, we);
-      for (int k = tid; k < nwin; k += kPT) {
+      if (!(ws0 == rs && one && !prefix_mode)) {  // (else the fold initialised them)
+        for (int k = tid; k < nwin; k += kPT) {
 #pragma unroll
-        for (int q = 0; q < 5; q++) W.rY[q * kRW + k] = INT32_MIN;
+          for (int q = 0; q < 5; q++) W.rY[q * kRW + k] = INT32_MIN;
+        }
+        pk_sync();  // (index 4 of rY is rbot)
       }
-      pk_sync();  // (index 4 of rY is rbot)
       phase_mark(8);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       // flattened (chart, column) runs (see walk()); per chart segment the
@@ -1009,9 +1025,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int ws0 = rs; ws0 <= endS; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = min(we, endS + 1) - ws0;
       stage(ws0, we);
-      for (int k = tid; k < nwin && !one; k += kPT)
-        W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
-      pk_sync();
+      if (!one) {
+        for (int k = tid; k < nwin; k += kPT) W.rY[k] = __ldcg(&Yc[(int64_t)cfg * n + ws0 + k]);
+        pk_sync();
+      }
       phase_mark(9);
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
