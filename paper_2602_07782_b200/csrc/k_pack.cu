@@ -188,6 +188,11 @@ __device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
 __device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int32_t atom_add_release(int32_t* p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -542,6 +547,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // is published)
     if (!prefix_mode && tid == 0) {
       S.pf_out = 0;
+      // every tile of this candidate published?  (one acquire load of the
+      // slot's completed-tile count; the fold's window fills probe far less
+      // often than once a row)
+      if (rd.flags && ready_lim != n - 1 && ld_acquire(rd.flags + 2 * (int64_t)pp.B * n + jslot) >= rd.T) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
+        ready_upto = rd.T - 1;
+        ready_lim = n - 1;
+      }
 #ifdef TABI_NO_PREFETCH
       const bool all = false;  // experiment: measure the row without the prefetch
 #else
@@ -1368,8 +1381,12 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     if (gt == 0 && t == 0 && j == 0) st->tfirst[7] = gtime();
 #endif
     if (gt == 0) {
-      red_add_release(fl + t, (t == T - 1 || needR) ? 2 : 1);
-      if (needL) red_add_release(fl + t - 1, 1);
+      // a tile whose flag reaches 2 here is complete: count it for its slot
+      // (the packers' all-published test)
+      int32_t* done_cnt = ra.rdy + 2 * (int64_t)pp.B * pp.n + j;
+      const int32_t v = (t == T - 1 || needR) ? 2 : 1;
+      if (atom_add_release(fl + t, v) + v == 2) red_add_release(done_cnt, 1);
+      if (needL && atom_add_release(fl + t - 1, 1) + 1 == 2) red_add_release(done_cnt, 1);
 #ifdef TABI_PHASE_TRACE
       if (j == 0 && (t == 0 || (t == 1 && needL))) atomicMax(&st->tfirst[1], gtime());
 #endif
