@@ -214,7 +214,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   __shared__ int32_t ready_upto;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid >= kPT) return;
-  const int m = wave_m(pp, st->pad[2], jslot);
+  const int m = wave_m(pp, st->pad[2], st->b0, jslot);
   if (m == 0) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
@@ -1213,8 +1213,11 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
              int32_t prof_cap, RasterArgs ra) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int T = st->ntiles;
+  // wave slots in use: prep_kernel narrows wave 0 (Status::b0); the CTAs of
+  // unused slots rasterize instead
+  const int Bw = pp.wave == 0 ? st->b0 : pp.B;
   if (threadIdx.x == 0) atomicMin(&st->tr[0], gtime());
-  if ((int)blockIdx.x < pp.B) {
+  if ((int)blockIdx.x < Bw) {
     packer(pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, hsorted,
            ra.cand_bad, scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap,
            blockIdx.x, Ready{ra.rdy, T, ra.tstart, ra.tix}, dsm);
@@ -1240,7 +1243,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   k3::ChartK3* CW = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kNW);
   int32_t* wtab = (int32_t*)carve(p, (size_t)4 * kNW * 4 * k);
   const int32_t m_hi = st->pad[2];
-  const int NB = T * pp.B;
+  const int NB = T * Bw;
   const int64_t SCm = (int64_t)pp.M * TABI_UNITS;
 #ifdef TABI_PHASE_TRACE
   unsigned long long rph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1257,8 +1260,8 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 #endif
   // the first G items go to the G raster groups statically (no queue round
   // trip before the first -- most urgent -- tiles); the queue hands out the rest
-  const int G = ((int)gridDim.x - pp.B) * kRG;
-  int first_it = ((int)blockIdx.x - pp.B) * kRG + grp;
+  const int G = ((int)gridDim.x - Bw) * kRG;
+  int first_it = ((int)blockIdx.x - Bw) * kRG + grp;
   while (true) {
     // (fetching the next item ahead would hide this round trip, but lets a
     // busy CTA sit on an early tile the packers are waiting for)
@@ -1268,8 +1271,8 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       // sequential mode: drop items of candidates below a successful one
       // (decided once, by the leader, so the group branches uniformly); the
       // top candidate's items (slot 0) can never be beaten
-      const int j0 = !pp.early || pp.B == 1 ? it0 % pp.B
-                     : it0 < T ? 0 : 1 + (it0 - T) % (pp.B - 1);  // item -> slot, as below
+      const int j0 = !pp.early || Bw == 1 ? it0 % Bw
+                     : it0 < T ? 0 : 1 + (it0 - T) % (Bw - 1);  // item -> slot, as below
       misc[4] = pp.early && j0 > 0 && *(volatile int32_t*)&st->win_j < j0;
     }
     first_it = -1;
@@ -1291,18 +1294,18 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     // below a successful one are dropped (its packer exits too).  Hybrid mode:
     // tile-major for all.
     int t, j;
-    if (!pp.early || pp.B == 1) {
-      t = it / pp.B;
-      j = it % pp.B;
+    if (!pp.early || Bw == 1) {
+      t = it / Bw;
+      j = it % Bw;
     } else if (it < T) {
       t = it;
       j = 0;
     } else {
-      t = (it - T) / (pp.B - 1);
-      j = 1 + (it - T) % (pp.B - 1);
+      t = (it - T) / (Bw - 1);
+      j = 1 + (it - T) % (Bw - 1);
     }
     if (dropped) continue;
-    const int m = wave_m(pp, m_hi, j);
+    const int m = wave_m(pp, m_hi, st->b0, j);
     if (m == 0) continue;
     const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
     const k3::Scale sc{m, SCm, 0};

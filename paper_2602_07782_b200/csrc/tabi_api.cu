@@ -608,7 +608,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       // Continue while an unevaluated (lower) candidate could still beat the
       // best area-weighted scale found: V(m) <= A_tot * m * 2^20 (p <= m 2^20/M);
       // in sequential mode any success stops the search.
-      const int next_m = st.pad[2] - (wave + 1) * B;
+      const int next_m = st.pad[2] - (st.b0 + wave * B);  // top of wave + 1 (see wave_m)
       if (next_m < 1) break;
       if (st.winner > 0) {
         const i128 Atot = (i128)(((unsigned __int128)st.atot_hi << 64) | st.atot_lo);

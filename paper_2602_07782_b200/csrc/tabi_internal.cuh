@@ -315,7 +315,7 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t work_next;  // fused kernel: raster work-queue head
   int32_t ntiles;     // fused kernel: raster tiles (prep_kernel)
   int32_t win_j;      // fused, sequential mode: smallest wave slot that succeeded
-  int32_t pad3;
+  int32_t b0;         // wave 0's candidate slots in use (prep_kernel; <= B)
   unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
   unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
   unsigned long long atot_lo, atot_hi;  // total 2 x area (int128) for D25 / D26
@@ -376,8 +376,11 @@ struct PackParams {
 
 // Candidate j of the current wave (0 if below 1).  m_hi = st->pad[2] is the
 // area bound computed by prep_kernel.
-__host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_hi, int j) {
-  const int m = m_hi - pp.wave * pp.B - j;
+// Candidate of wave slot j: wave 0 evaluates the b0 candidates m_hi, m_hi - 1,
+// ... (b0 <= B, chosen by prep_kernel); wave w >= 1 the next B below.
+__host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_hi, int32_t b0, int j) {
+  if (pp.wave == 0 && j >= b0) return 0;
+  const int m = m_hi - (pp.wave == 0 ? 0 : b0 + (pp.wave - 1) * pp.B) - j;
   return m >= 1 ? m : 0;
 }
 
