@@ -1418,7 +1418,16 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
     const i128 Atot = (i128)(((unsigned __int128)st->atot_hi << 64) | st->atot_lo);
     int32_t w = 0, r0 = pp.n, pw = 0;
     i128 bestV = -1;
-    for (int m = 1; m <= pp.M; m++) {
+    // without a tail anywhere V is increasing in m: the largest success wins
+    // (the common, sequential case -- no int128 products)
+    bool any_tail = false;
+    for (int m = pp.M; m >= 1; m--) {
+      const Cand& cd = sc[m - 1];
+      any_tail |= cd.switched_at >= 0;
+      if (!any_tail && cd.success && w == 0) w = m;
+    }
+    if (any_tail) w = 0;
+    for (int m = any_tail ? 1 : pp.M + 1; m <= pp.M; m++) {
       const Cand& cd = sc[m - 1];
       if (!cd.success) continue;
       const bool tail = cd.switched_at >= 0;
