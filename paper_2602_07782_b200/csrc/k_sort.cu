@@ -181,11 +181,10 @@ bitonic_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, i
 // and 2t + 1 in registers: the compare-exchange stages of element distance
 // <= 32 are warp shuffles (partner thread t ^ (stride / 2), same slot) with no
 // barrier; only distances >= 64 go through shared memory.
-__global__ void __launch_bounds__(kT, 1)
-bitonic_reg_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n,
-                   int32_t* perm, const Status* st) {
+__device__ __forceinline__ void bitonic_reg_body(const int32_t* __restrict__ hh,
+                                                 const int32_t* __restrict__ ww, int32_t n,
+                                                 int32_t* perm) {
   __shared__ uint64_t key[2 * kT];
-  if (st->bad_chart != INT32_MAX) return;
   const int t = threadIdx.x;
   uint64_t v[2];
 #pragma unroll
@@ -231,6 +230,13 @@ bitonic_reg_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ w
     const int i = 2 * t + s;
     if (i < n) perm[i] = (int32_t)(v[s] & 0xfffu);
   }
+}
+
+__global__ void __launch_bounds__(kT, 1)
+bitonic_reg_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, int32_t n,
+                   int32_t* perm, const Status* st) {
+  if (st->bad_chart != INT32_MAX) return;
+  bitonic_reg_body(hh, ww, n, perm);
 }
 
 // 2048 < N <= 2^17: each CTA sorts a chunk of 2048 (key, index) pairs with the
@@ -374,14 +380,14 @@ __global__ void rank_scatter_kernel(const int32_t* __restrict__ rank, int32_t n,
 // Footprint slots: column slot of sorted position s = min(ceil(w/256) + 2g, W'),
 // row slot = min(ceil(h/256) + 2g, H') -- the footprint at the largest scale
 // (m = M, scale 1) bounds every candidate's (w_s is monotone in m).
-__global__ void __launch_bounds__(kT, 1)
-prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int64_t* area2,
-            const int32_t* perm, PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
-            int32_t* tstart, int32_t* tix, Status* st) {
+__device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
+                                          const int32_t* __restrict__ ww, const int64_t* area2,
+                                          const int32_t* perm, const PackParams& pp, int32_t* colofs,
+                                          int32_t* rowofs, int32_t* hsorted, int32_t* tstart,
+                                          int32_t* tix, Status* st) {
   __shared__ int32_t sh[2][kW + 1];
   __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
-  if (st->bad_chart != INT32_MAX) return;
   // Area bound on the candidate scales: the packed charts are disjoint and
   // inside the atlas, so (m/M)^2 * sum(area) <= W*H for any candidate that can
   // succeed; in units (2*area, 1/256 texel): m^2 * A2 <= 2 * 65536 * W * H * M^2.
@@ -477,6 +483,26 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
   }
 }
 
+__global__ void __launch_bounds__(kT, 1)
+prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int64_t* area2,
+            const int32_t* perm, PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
+            int32_t* tstart, int32_t* tix, Status* st) {
+  if (st->bad_chart != INT32_MAX) return;
+  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st);
+}
+
+// N <= 2048: order and slot layout in one launch (the block that sorted reads
+// its own permutation after a barrier).
+__global__ void __launch_bounds__(kT, 1)
+sort_prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww,
+                 const int64_t* area2, int32_t* perm, PackParams pp, int32_t* colofs,
+                 int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st) {
+  if (st->bad_chart != INT32_MAX) return;
+  bitonic_reg_body(hh, ww, pp.n, perm);
+  __syncthreads();
+  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st);
+}
+
 // One launch instead of a status upload plus a string of memsets.
 // mode 2: initialise the status block (bad_chart = none, trace start = max);
 // mode >= 1: zero the candidate records and hybrid-tail states;
@@ -551,6 +577,15 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
   }
   sort_kernel<<<1, kT, 0, s>>>(P.h, P.w, n, keys, keys2, perm, perm2, st);
   return 1;
+}
+
+bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int32_t* colofs,
+                      int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
+                      cudaStream_t s) {
+  if (pp.n > 2 * kT || getenv("TABI_SORT")) return false;
+  sort_prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart,
+                                    tix, st);
+  return true;
 }
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,

@@ -459,6 +459,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   // One wave's work, enqueued on s: [H2D + reset + proxies + sort] for the
   // first wave, the candidate wave, select, [placements D2H], status D2H.
   auto enqueue_wave = [&](bool prologue, int& nl) -> tabi_status {
+    bool prep_done = false;
     if (prologue && !on_device)
       CK(cudaMemcpyAsync(ctx->d_xy, ctx->h_xy, sizeof(float) * 2 * V_in + sizeof(int32_t) * (n + 1),
                          cudaMemcpyHostToDevice, s));
@@ -470,10 +471,16 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
                      ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
       nl++;
       tm.mark(s);
-      nl += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
+      if (wave == 0 && launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs,
+                                        ctx->hsorted, ctx->tstart, ctx->tix, ctx->d_status, s)) {
+        nl++;
+        prep_done = true;
+      } else {
+        nl += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
+      }
       tm.mark(s);
     }
-    if (wave == 0) {
+    if (wave == 0 && !prep_done) {
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
                   ctx->tix, ctx->d_status, s);
       nl++;

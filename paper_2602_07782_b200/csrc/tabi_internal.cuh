@@ -397,6 +397,10 @@ void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* 
 // Returns the number of kernels launched.
 int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
                 int32_t* perm2, const Status* st, cudaStream_t s);
+// N <= 2048 and no TABI_SORT knob: sort + prep in one launch (returns false otherwise)
+bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int32_t* colofs,
+                      int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
+                      cudaStream_t s);
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
                  cudaStream_t s);
