@@ -302,7 +302,11 @@ constexpr int kFusedTileCharts = 64 / kFusedGroups;
 #endif
 constexpr int kFusedTileCells = TABI_TILE_CELLS / kFusedGroups;
 #ifndef TABI_HEAD_CELLS
-#define TABI_HEAD_CELLS 0  // measured: quarter-size head tiles do not shorten the first wait
+// quarter-size tiles for the first 16 K footprint cells (the tallest charts,
+// which the first rows need): with a narrow first wave most raster CTAs are
+// free at the start, and the first row's wait drops (C3: -10 us; measured
+// 16 K < 32 K < 64 K < 128 K; with 16 candidates per wave it did not pay)
+#define TABI_HEAD_CELLS 16384
 #endif
 constexpr int kFusedHeadCells = TABI_HEAD_CELLS;  // quarter-size tiles below this prefix
 
