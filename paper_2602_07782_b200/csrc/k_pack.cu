@@ -37,6 +37,7 @@ constexpr int kNT = 512;
 constexpr int kNW = kNT / 32;
 constexpr int kRW = 2048;          // charts per row window
 constexpr int kPWN = 1024;         // sorted positions in the fold's position window
+constexpr int kPairSm = 512;       // lock pairs of a row kept in shared memory
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;  // leave room for static Smem
 #ifndef TABI_PACK_NT
 #define TABI_PACK_NT 512
@@ -343,7 +344,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   PW.co = PW.wd + kPWN;
   PW.hs = PW.co + kPWN;
   PW.lk = (uint8_t*)(PW.hs + kPWN);
-  W.prof = (uint32_t*)(PW.lk + kPWN);
+  struct {  // the row's first kPairSm lock pairs (D15) in shared memory
+    int32_t *a, *b;
+    uint8_t* lk;
+  } SP;
+  SP.a = (int32_t*)(PW.lk + kPWN);
+  SP.b = SP.a + kPairSm;
+  SP.lk = (uint8_t*)(SP.b + kPairSm);
+  W.prof = (uint32_t*)(SP.lk + kPairSm);
   W.prof_cap = prof_cap;
 
   const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
@@ -749,7 +757,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         if (a <= R && cnt > 0) {
           int32_t p = carry + ex;
           for (int b = a + 2; b < a + 2 + cnt; b++, p++) {
-            if (p < pair_cap) {
+            if (p < kPairSm) {  // the row's first pairs stay in shared memory
+              SP.a[p] = a;
+              SP.b[p] = b;
+            } else if (p < pair_cap) {
               pa[p] = a;
               pb[p] = b;
             }
@@ -773,11 +784,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       }
       const int32_t np = S.npairs;
       for (int p = wid; p < np; p += kPW) {
-        const int a = pa[p], b = pb[p];
+        const int a = p < kPairSm ? SP.a[p] : pa[p], b = p < kPairSm ? SP.b[p] : pb[p];
         bool la, lb;
         const int32_t dx = useW ? W.rx1[b - rs] - W.rx1[a - rs] : xs1[b] - xs1[a];
         warp_locks(row + rowofs[a], row + rowofs[b], hd[a], hd[b], dx, lane, la, lb);
-        if (lane == 0) plk[p] = (la ? 1 : 0) | (lb ? 2 : 0);
+        if (lane == 0) {
+          const uint8_t bits = (la ? 1 : 0) | (lb ? 2 : 0);
+          if (p < kPairSm) SP.lk[p] = bits;
+          else plk[p] = bits;
+        }
       }
       pk_sync();
     }
@@ -900,10 +915,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             bits = useW ? W.rlk[a - rs] : lk[a];
           } else {
             const int p = q - (endA - rs);
-            a = pa[p];
-            b = pb[p];
+            a = p < kPairSm ? SP.a[p] : pa[p];
+            b = p < kPairSm ? SP.b[p] : pb[p];
             if (b > endc) return false;
-            bits = plk[p];
+            bits = p < kPairSm ? SP.lk[p] : plk[p];
           }
           Ya = one ? &W.rY[cfg * kRW + (a - rs)] : &Yc[(int64_t)cfg * n + a];
           Yb = one ? &W.rY[cfg * kRW + (b - rs)] : &Yc[(int64_t)cfg * n + b];
@@ -1482,8 +1497,8 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
   static std::atomic<unsigned long long> attr{0};
   ensure_dyn_smem((const void*)pack_kernel, kMaxDynSmem, attr);
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed =
-      sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN) + kRW + kPWN;
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN +
+                                         2 * (size_t)kPairSm) + kRW + kPWN + kPairSm;
   const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   pack_kernel<<<pp.B, kNT, kMaxDynSmem, s>>>(pp, colofs, rowofs, dcol, drow, wd, hd, off, lockbits,
                                              hsorted, cand_bad, scratch, pair_cap, X, Y, mir,
@@ -1521,8 +1536,8 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s) {
   const int f_words = (pp.Wp + 3) & ~3;
-  const size_t fixed =
-      sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN) + kRW + kPWN;
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN +
+                                         2 * (size_t)kPairSm) + kRW + kPWN + kPairSm;
   int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
   RasterArgs ra{P, perm, wd, hd, off, lockbits, cand_bad, dcol, drow, rdy, tstart, tix};
   PackParams p = pp;
