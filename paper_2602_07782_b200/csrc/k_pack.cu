@@ -364,11 +364,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   }
   if (!prefix_mode && !rd.flags) {  // work accounting: footprint entries K3 produced
     unsigned long long pe = 0;
+    #pragma unroll 1  // (cold or short: keep the code small)
     for (int s = tid; s < n; s += kPT) pe += (unsigned long long)(wd[s] + hd[s]);
     for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
     if (lane == 0) atomicAdd(&st->work_prof, pe);
   }
   int32_t* fsave = pp.T.fsave + (int64_t)(m - 1) * pp.T.fstride;
+  #pragma unroll 1  // (cold or short: keep the code small)
   for (int x = tid; x < Wp; x += kPT) F[x] = prefix_mode ? fsave[x] : 0;  // top
   if (tid == 0) {
     S.row_start = 0; S.fmax = 0; S.fail = 0; S.rows = 0; S.knees_found = 0; S.knee_rows = 0;
@@ -429,6 +431,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const bool pg = (a1 - a0) > W.prof_cap;
     const bool hit = pf_pending && c0 >= S.pf_a0 && c1 <= S.pf_a1;
     pk_sync();  // previous readers of the window buffers are done
+    #pragma unroll 1  // (cold or short: keep the code small)
     for (int k = tid; k < nwin && !have; k += kPT) {
       const int s = ws0 + k;
       W.rx0[k] = xs0[s];
@@ -533,6 +536,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             break;
           }
         }
+        #pragma unroll 1  // (cold or short: keep the code small)
         for (int x = tid; x < Wp; x += kPT) fsave[x] = F[x];
         if (tid == 0) {
           pp.T.state[m - 1] = TAIL_LAYOUT;
@@ -585,6 +589,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       pk_sync();
       if (!degenerate) {
         const int32_t ref = ltr ? F[right] : F[left - 1];
+        #pragma unroll 1  // (cold or short: keep the code small)
         for (int x = left + tid; x < right; x += kPT) {
           if (F[x] >= ref) {
             if (ltr) atomicMax(&S.nk, x);
@@ -613,6 +618,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t kb = kv ? (S.knee_ltr ? Wp : S.knee_left) : 0;
     if (kv) {
       int32_t mx = INT32_MIN;
+      #pragma unroll 1  // (cold or short: keep the code small)
       for (int x = ka + tid; x < kb; x += kPT) mx = max(mx, F[x]);
       mx = warp_max(mx);
       if (lane == 0) atomicMax(&S.conc_max, mx);
