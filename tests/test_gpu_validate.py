@@ -146,3 +146,19 @@ def test_errors(ctx):
     assert m["status"] == EINVAL
     m = ctx.validate(cs.xy, cs.start, pl, cs.atlas_w, cs.atlas_h, gutter=65, raise_on_error=False)
     assert m["status"] == EINVAL
+
+
+def test_maximum_sizes_self_consistent(ctx):
+    """The largest configuration the context allows (25,000 charts, M = 256
+    candidate scales, k = 64, a 16,384^2 atlas): too large for the CPU oracle
+    in a test, so the GPU result is checked against the GPU validator (no
+    overlap, gutter or out-of-bounds texel) and the stretch closed form M/m."""
+    from paper_2602_07782_b200 import spec_of
+    cs = chartgen.generate("lightmap", 25000, 16384, 16384, 11, rho=0.8, name="max")
+    spec = spec_of(cs, scale_count=256, local_aabb_count=64)
+    st, pl, info = ctx.pack(cs.xy, cs.start, spec)
+    assert st == 0 and info.scale_index >= 1
+    assert info.l2_stretch == pytest.approx(256 / info.scale_index, rel=1e-12)
+    m = ctx.validate(cs.xy, cs.start, pl, cs.atlas_w, cs.atlas_h, gutter=cs.gutter)
+    assert m["overlap"] == m["gutter"] == m["oob"] == 0
+    assert m["l2_stretch"] == pytest.approx(info.l2_stretch, rel=1e-9)
