@@ -51,6 +51,18 @@ __device__ __forceinline__ void pk_sync() {
   if (kPT == kNT) __syncthreads();
   else asm volatile("bar.sync 1, %0;" ::"n"(kPT) : "memory");
 }
+// barrier + OR of a per-thread predicate over the packer's threads
+__device__ __forceinline__ bool pk_sync_or(bool v) {
+  if (kPT == kNT) return __syncthreads_or(v ? 1 : 0) != 0;
+  unsigned r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, 1, %2, p;\n"
+      " selp.u32 %0, 1, 0, q;\n}\n"
+      : "=r"(r)
+      : "r"(v ? 1u : 0u), "n"(kPT)
+      : "memory");
+  return r != 0;
+}
 
 struct Smem {
   int32_t scan[2][kNW + 1];
@@ -933,8 +945,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         auto relax = [&](int32_t* Ya, int32_t* Yb, int bits, int flag) {
           const int32_t ya = one ? *(volatile int32_t*)Ya : __ldcg(Ya);
           const int32_t yb = one ? *(volatile int32_t*)Yb : __ldcg(Yb);
-          if ((bits & 1) && ya < yb) { atomicMax(Ya, yb); S.changed3[flag] = 1; }
-          if ((bits & 2) && yb < ya) { atomicMax(Yb, ya); S.changed3[flag] = 1; }
+          bool ch = false;
+          if ((bits & 1) && ya < yb) { atomicMax(Ya, yb); ch = true; }
+          if ((bits & 2) && yb < ya) { atomicMax(Yb, ya); ch = true; }
+          return ch;
         };
         const bool cached = nitems <= 2 * kPT;
         int32_t *ya0 = nullptr, *yb0 = nullptr, *ya1 = nullptr, *yb1 = nullptr;
@@ -944,28 +958,25 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           if (tid < nitems) v0 = item(tid, ya0, yb0, bits0);
           if (tid + kPT < nitems) v1 = item(tid + kPT, ya1, yb1, bits1);
         }
-        // one barrier per iteration: iteration i raises flag i % 3 and clears
-        // flag (i + 1) % 3, last read two barriers ago
-        if (tid == 0) { S.changed3[0] = 0; S.changed3[1] = 0; }
-        pk_sync();
+        // one barrier per pass, which also ORs the threads' "raised something"
+        // (the items read only values published before Alg. 1: no setup barrier)
         for (int iter = 0;; iter++) {
-          const int fl = iter % 3;
-          if (tid == 0) S.changed3[(iter + 1) % 3] = 0;
+          bool ch = false;
           if (cached) {
-            if (v0) relax(ya0, yb0, bits0, fl);
-            if (v1) relax(ya1, yb1, bits1, fl);
+            if (v0) ch |= relax(ya0, yb0, bits0, 0);
+            if (v1) ch |= relax(ya1, yb1, bits1, 0);
           } else {
             for (int it = tid; it < nitems; it += kPT) {
               int32_t *Ya, *Yb;
               int bits;
-              if (item(it, Ya, Yb, bits)) relax(Ya, Yb, bits, fl);
+              if (item(it, Ya, Yb, bits)) ch |= relax(Ya, Yb, bits, 0);
             }
           }
-          pk_sync();
+          const bool any = pk_sync_or(ch);
 #ifdef TABI_PHASE_TRACE
           if (tid == 0 && jslot == 0) atomicAdd(&st->rph[7], 1ull);  // Alg. 1 passes
 #endif
-          if (!S.changed3[fl]) break;
+          if (!any) break;
         }
       }
     }
