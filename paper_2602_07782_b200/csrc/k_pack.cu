@@ -759,7 +759,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // ---- D15: non-adjacent lock pairs of the row (HC folds only) ----------
     const int32_t R = max(hc0 ? endA : -1, (knee_ok && hc1) ? endK : -1);
     if (!adj_only && R > rs) {
-      int32_t carry = 0;
+      // pair-list slots by warp-aggregated atomics: the list's order is
+      // immaterial (each pair's lock bits and Alg. 1's fixpoint do not depend
+      // on it), so no block scan
       for (int base = rs; base <= R; base += kPT) {
         const int a = base + tid;
         int32_t cnt = 0;
@@ -770,10 +772,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           const int32_t xa = xs1[a], wa = wd[a];
           for (int b = a + 2; b <= R && xs1[b] - xa < wa; b++) cnt++;
         }
-        int32_t ex, dummy, tot, tot2;
-        block_scan2(cnt, 0, ex, dummy, tot, tot2, S);
+        const int32_t inc = warp_incl_sum(cnt, lane);
+        const int32_t wtot = __shfl_sync(0xffffffffu, inc, 31);
+        int32_t wbase = 0;
+        if (lane == 31 && wtot > 0) wbase = atomicAdd(&S.npairs, wtot);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
         if (a <= R && cnt > 0) {
-          int32_t p = carry + ex;
+          int32_t p = wbase + inc - cnt;
           for (int b = a + 2; b < a + 2 + cnt; b++, p++) {
             if (p < kPairSm) {  // the row's first pairs stay in shared memory
               SP.a[p] = a;
@@ -784,19 +789,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             }
           }
         }
-        carry += tot;
-      }
-      if (tid == 0) {
-        S.npairs = carry;
-        if (carry > pair_cap) {
-          S.pair_overflow = 1;
-          atomicOr(&st->capacity, 2);
-          atomicMax(&st->pad[0], carry);
-        }
       }
       pk_sync();
-      if (S.pair_overflow) {
-        if (tid == 0) S.fail = 1;
+      if (S.npairs > pair_cap) {  // (uniform)
+        if (tid == 0) {
+          S.pair_overflow = 1;
+          S.fail = 1;
+          atomicOr(&st->capacity, 2);
+          atomicMax(&st->pad[0], S.npairs);
+        }
         pk_sync();
         break;
       }
