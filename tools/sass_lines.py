@@ -32,6 +32,12 @@ def main():
     ia, ie, ws = h.index("Address"), h.index("Instructions Executed"), h.index(
         "Warp Stall Sampling (All Samples)")
     prof = [(int(r[ia], 16), float(r[ie] or 0), float(r[ws] or 0)) for r in rows[hi + 1:] if r and r[ia].startswith("0x")]
+    # optional per-line stall reasons / shared-memory excess (REASONS=1)
+    rcols = [(i, c) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+    xcol = h.index("L1 Wavefronts Shared Excessive") if "L1 Wavefronts Shared Excessive" in h else None
+    extra = {int(r[ia], 16): ([float(r[i] or 0) for i, _ in rcols],
+                              float(r[xcol] or 0) if xcol is not None else 0.0)
+             for r in rows[hi + 1:] if r and r[ia].startswith("0x")}
     base = min(a for a, _, _ in prof)
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_2602_07782_b200", "libtabi.so")],
@@ -85,6 +91,20 @@ def main():
             bk[nm][1] += s
         for nm, (n, s) in sorted(bk.items(), key=lambda kv: -kv[1][0]):
             print(f"  phase {nm:24s} {n / tot[0] * 100:5.1f}% inst {s / max(tot[1], 1) * 100:5.1f}% stall")
+    if os.environ.get("REASONS"):
+        lr = collections.defaultdict(lambda: [[0.0] * len(rcols), 0.0])
+        for a, _, _ in prof:
+            key = off2line.get(a - base, ("?", 0))
+            v, x = extra[a]
+            acc = lr[key]
+            acc[0] = [p + q for p, q in zip(acc[0], v)]
+            acc[1] += x
+        for (f, l), (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:topn]:
+            v, x = lr[(f, l)]
+            top = sorted(((val, c) for val, (_, c) in zip(v, rcols) if val > 0), reverse=True)[:3]
+            print(f"{s:6.0f} samples  {f}:{l}  smem-excess {x:.0f}  " +
+                  ", ".join(f"{c[6:]} {val:.0f}" for val, c in top))
+        return
     for (f, l), (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:topn]:
         fp = os.path.join(ROOT, "paper_2602_07782_b200", "csrc", f)
         lines = src if f == os.path.basename(cu) else (
