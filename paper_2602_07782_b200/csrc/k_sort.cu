@@ -384,7 +384,7 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
                                           const int32_t* __restrict__ ww, const int64_t* area2,
                                           const int32_t* perm, const PackParams& pp, int32_t* colofs,
                                           int32_t* rowofs, int32_t* hsorted, int32_t* tstart,
-                                          int32_t* tix, Status* st) {
+                                          int32_t* tix, Status* st, int32_t* rdy) {
   __shared__ int32_t sh[2][kW + 1];
   __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
@@ -481,14 +481,23 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
     // +4: the TMA bulk copy of a row window rounds its end up to 16 bytes
     if ((int64_t)carry_c + 4 > pp.col_cap || (int64_t)carry_r + 4 > pp.row_cap) st->capacity |= 1;
   }
+  if (rdy) {  // fused wave 0: the ready flags, arrival counters and completed-tile
+              // counts of the T tiles (the reset kernel leaves them to us)
+    const int64_t bt = (int64_t)pp.B * carry_t, bn = (int64_t)pp.B * pp.n;
+    for (int64_t q = threadIdx.x; q < bt; q += kT) {
+      rdy[q] = 0;
+      rdy[bn + q] = 0;
+    }
+    for (int q = threadIdx.x; q < pp.B; q += kT) rdy[2 * bn + q] = 0;
+  }
 }
 
 __global__ void __launch_bounds__(kT, 1)
 prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int64_t* area2,
             const int32_t* perm, PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
-            int32_t* tstart, int32_t* tix, Status* st) {
+            int32_t* tstart, int32_t* tix, Status* st, int32_t* rdy) {
   if (st->bad_chart != INT32_MAX) return;
-  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st);
+  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy);
 }
 
 // N <= 2048: order and slot layout in one launch (the block that sorted reads
@@ -496,11 +505,12 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
 __global__ void __launch_bounds__(kT, 1)
 sort_prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww,
                  const int64_t* area2, int32_t* perm, PackParams pp, int32_t* colofs,
-                 int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st) {
+                 int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
+                 int32_t* rdy) {
   if (st->bad_chart != INT32_MAX) return;
   bitonic_reg_body(hh, ww, pp.n, perm);
   __syncthreads();
-  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st);
+  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy);
 }
 
 // One launch instead of a status upload plus a string of memsets.
@@ -581,18 +591,18 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
 
 bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int32_t* colofs,
                       int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                      cudaStream_t s) {
+                      int32_t* rdy, cudaStream_t s) {
   if (pp.n > 2 * kT || getenv("TABI_SORT")) return false;
   sort_prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart,
-                                    tix, st);
+                                    tix, st, rdy);
   return true;
 }
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                 cudaStream_t s) {
+                 int32_t* rdy, cudaStream_t s) {
   prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart, tix,
-                               st);
+                               st, rdy);
 }
 
 }  // namespace tabi

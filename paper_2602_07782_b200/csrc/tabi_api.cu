@@ -463,8 +463,10 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     if (prologue && !on_device)
       CK(cudaMemcpyAsync(ctx->d_xy, ctx->h_xy, sizeof(float) * 2 * V_in + sizeof(int32_t) * (n + 1),
                          cudaMemcpyHostToDevice, s));
+    // (wave 0: prep_kernel zeroes the fused kernel's flags for the T tiles it
+    // lays out; later waves reuse the tiles and need the reset here)
     launch_reset(ctx->d_status, reset_mode, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy,
-                 nrdy, s);
+                 wave == 0 ? 0 : nrdy, s);
     nl++;
     if (prologue) {
       launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
@@ -472,7 +474,8 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       nl++;
       tm.mark(s);
       if (wave == 0 && launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs,
-                                        ctx->hsorted, ctx->tstart, ctx->tix, ctx->d_status, s)) {
+                                        ctx->hsorted, ctx->tstart, ctx->tix, ctx->d_status,
+                                        fused ? ctx->rdy : nullptr, s)) {
         nl++;
         prep_done = true;
       } else {
@@ -482,7 +485,8 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     }
     if (wave == 0 && !prep_done) {
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
-                  ctx->tix, ctx->d_status, s);
+                  ctx->tix, ctx->d_status,
+                  fused ? ctx->rdy : nullptr, s);
       nl++;
     }
     if (fused) {

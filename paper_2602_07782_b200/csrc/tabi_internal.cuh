@@ -404,10 +404,10 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
 // N <= 2048 and no TABI_SORT knob: sort + prep in one launch (returns false otherwise)
 bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int32_t* colofs,
                       int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                      cudaStream_t s);
+                      int32_t* rdy, cudaStream_t s);  // rdy: zeroed for the fused wave, or nullptr
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                 cudaStream_t s);
+                 int32_t* rdy, cudaStream_t s);
 void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
                      int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
