@@ -219,6 +219,18 @@ def test_exact_tail_parity(orc, ctx, cs, t):
     _compare_pack(orc, ctx, cs, check_profiles=2, t_opt_bp=t, flags=F_EXACT_TAIL)
 
 
+@pytest.mark.parametrize("kw", [dict(flags=8 | 1), dict(flags=8 | 32, t_opt_bp=300),
+                                dict(flags=2 | 4), dict(flags=16 | 2, local_aabb_count=1),
+                                dict(flags=32 | 4, t_opt_bp=1000, gutter=0),
+                                dict(flags=8 | 16, scale_count=17, gutter=2)],
+                         ids=lambda d: "-".join(f"{a}{b}" for a, b in d.items()))
+def test_flag_combinations_parity(orc, ctx, kw):
+    """Flags together (pre-rotation, exact tail, ablations, paper-literal
+    locks) with other spec knobs: bit-exact against the oracle."""
+    _compare_pack(orc, ctx, chartgen.small_case(2, n=300, family="tss", side=512, rho=0.6),
+                  check_profiles=2, **kw)
+
+
 def test_exact_tail_config4_full_size(orc, ctx):
     from paper_2602_07782_b200 import F_EXACT_TAIL, spec_of
     cs = chartgen.config4(0)
