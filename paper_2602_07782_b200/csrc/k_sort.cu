@@ -144,6 +144,9 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
 // 2^26 units (|coordinate| <= 2^24), so (2^26-1-h, 2^26-1-w, index) packs in
 // 64 bits for N <= 4096 and the packed keys are unique: any correct sort gives
 // the stable order.
+#ifndef TABI_B0_FILL
+#define TABI_B0_FILL 60  // wave 0 reaches down to the scale filling this % of the atlas
+#endif
 constexpr int kBitonicMax = 4096;
 constexpr int kRankMax = 1 << 17;
 constexpr int kRankT = 256;   // rank sort: keys i per block
@@ -418,7 +421,7 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
       int b0 = pp.B;
       if (pp.early && pp.B > 2 && m_hi >= 1) {
         int m_lo = m_hi;
-        while (m_lo > 1 && (i128)10 * (m_lo - 1) * (m_lo - 1) * tot >= (i128)6 * rhs) m_lo--;
+        while (m_lo > 1 && (i128)100 * (m_lo - 1) * (m_lo - 1) * tot >= (i128)TABI_B0_FILL * rhs) m_lo--;
         b0 = min(pp.B, max(2, m_hi - m_lo + 1));
       }
       st->b0 = b0;
