@@ -201,11 +201,6 @@ __device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
 __device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ int32_t atom_add_release(int32_t* p, int32_t v) {
-  int32_t old;
-  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1421,8 +1416,12 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       // (the packers' all-published test)
       int32_t* done_cnt = ra.rdy + 2 * (int64_t)pp.B * pp.n + j;
       const int32_t v = (t == T - 1 || needR) ? 2 : 1;
-      if (atom_add_release(fl + t, v) + v == 2) red_add_release(done_cnt, 1);
-      if (needL && atom_add_release(fl + t - 1, 1) + 1 == 2) red_add_release(done_cnt, 1);
+      // acq_rel: the group that completes a flag (2 increments from two raster
+      // groups) acquires the other group's writes before it releases the
+      // completed-tile count, so the packers' one-load "all published" test
+      // (an acquire of done_cnt) happens-after both contributors
+      if (atom_add_acq_rel(fl + t, v) + v == 2) red_add_release(done_cnt, 1);
+      if (needL && atom_add_acq_rel(fl + t - 1, 1) + 1 == 2) red_add_release(done_cnt, 1);
 #ifdef TABI_PHASE_TRACE
       if (j == 0 && (t == 0 || (t == 1 && needL))) atomicMax(&st->tfirst[1], gtime());
 #endif
@@ -1524,19 +1523,22 @@ void launch_pack(const PackParams& pp, const int32_t* colofs, const int32_t* row
 }
 
 int fused_grid(int device) {
-  static int cached[64];
-  static bool have[64];
+  // per-device cache, filled once; several host threads (tabi_pack_batch)
+  // may race here, so the value is an atomic (-1 = not yet known) and the
+  // computation is idempotent
+  static std::atomic<int> cached[64] = {};
+  static std::atomic<bool> have[64] = {};
   if (device < 0 || device >= 64) return 0;
-  if (!have[device]) {
+  if (!have[device].load(std::memory_order_acquire)) {
     cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     int sms = 0, per = 0, coop = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fused_kernel, kNT, kMaxDynSmem);
-    cached[device] = coop ? sms * per : 0;
-    have[device] = true;
+    cached[device].store(coop ? sms * per : 0, std::memory_order_relaxed);
+    have[device].store(true, std::memory_order_release);
   }
-  return cached[device];
+  return cached[device].load(std::memory_order_relaxed);
 }
 
 

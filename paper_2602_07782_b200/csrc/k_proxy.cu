@@ -245,7 +245,8 @@ __device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, 
 template <int G>
 __global__ void __launch_bounds__(kBlock)
 proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
-             float ry, int k, uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st) {
+             float ry, int k, uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P,
+             Status* st) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, gib = threadIdx.x / G;
   Group<G> g;
@@ -266,6 +267,13 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   const int gl = g.gl;
   const int32_t a0 = start[c];
   const int nv = start[c + 1] - a0;
+  // device-pointer inputs are not checked on the host: a vertex range outside
+  // the context's snapped-coordinate scratch is a capacity error (bit 2),
+  // raised before any write (tabi.h: TABI_ECAPACITY beyond max_vertices)
+  if (a0 < 0 || (int64_t)a0 + (nv > 0 ? nv : 0) > max_v) {
+    if (gl == 0) atomicOr(&st->capacity, 4);
+    return;
+  }
   if (nv < 3) {
     if (gl == 0) atomicMin(&st->bad_chart, c);
     return;
@@ -438,26 +446,29 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
 
 template <int G>
 void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-              uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+              uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
+              cudaStream_t s) {
   constexpr int per_block = kBlock / G;
   const int blocks = (n + per_block - 1) / per_block;
   const size_t smem = slice_bytes(k) * per_block;
   static std::atomic<unsigned long long> attr{0};  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
   ensure_dyn_smem((const void*)proxy_kernel<G>, (int)(slice_bytes(TABI_KMAX) * per_block), attr);
-  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, flags, qx, qy, P, st);
+  proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P,
+                                                st);
 }
 
 }  // namespace
 
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-                    uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s) {
+                    uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
+                    cudaStream_t s) {
   const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
   const int forced = genv ? atoi(genv) : 0;
   const int G = forced == 8 || forced == 16 || forced == 32 ? forced
                 : n < 4096 ? 32 : n < 8192 ? 16 : 8;  // measured: C3 (1572) 32, C4 (20000) 8
-  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, P, st, s);
-  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, P, st, s);
-  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, P, st, s);
+  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, s);
+  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, s);
+  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, s);
 }
 
 }  // namespace tabi

@@ -470,7 +470,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     nl++;
     if (prologue) {
       launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
-                     ctx->d_qx, ctx->d_qy, ctx->P, ctx->d_status, s);
+                     ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s);
       nl++;
       tm.mark(s);
       if (wave == 0 && launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs,
@@ -560,7 +560,11 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   // with one call: no per-kernel launch overhead on the critical path.
   const char* genv = getenv("TABI_GRAPH");
   const bool use_graph = !tm.on && !(genv && genv[0] == '0');
-  for (int attempt = 0; attempt < 64; attempt++) {
+  // bound: every wave but the last evaluates >= 1 candidate (<= M waves), plus
+  // at most 8 capacity retries; reaching it is an internal error, not NO_FIT
+  const int max_attempts = M + 10;
+  bool finished = false;
+  for (int attempt = 0; attempt < max_attempts; attempt++) {
     pp.col_cap = ctx->col_cap;
     pp.row_cap = ctx->row_cap;
     pp.wave = wave;
@@ -570,7 +574,10 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       for (const char* p = getenv("TABI_SORT"); p && *p; p++) sort_env = (char)(sort_env * 31 + *p);
       for (const char* p = getenv("TABI_PROXY_LANES"); p && *p; p++)
         sort_env = (char)(sort_env * 37 + *p);
-      GraphKey key{xy, chart_start, out, n, V_in, on_device, res_x, res_y, *spec, B,
+      // host mode: the graph reads the context's own staging buffers, so the
+      // caller's pointers are not part of what it bakes in
+      GraphKey key{on_device ? (const void*)xy : nullptr, on_device ? (const void*)chart_start : nullptr,
+                   on_device ? (const void*)out : nullptr, n, V_in, on_device, res_x, res_y, *spec, B,
                    fused ? 1 : 0, ctx->alloc_gen, sort_env};
       if (!ctx->gexec || !(key == ctx->gkey)) {
         if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
@@ -615,11 +622,13 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       if (info) info->bad_chart = st.bad_chart;
       return TABI_EINVAL;
     }
+    if (st.capacity & 4) return TABI_ECAPACITY;  // vertex range beyond max_vertices
     if (!st.capacity) {
       // Continue while an unevaluated (lower) candidate could still beat the
       // best area-weighted scale found: V(m) <= A_tot * m * 2^20 (p <= m 2^20/M);
       // in sequential mode any success stops the search.
       const int next_m = st.pad[2] - (st.b0 + wave * B);  // top of wave + 1 (see wave_m)
+      finished = true;
       if (next_m < 1) break;
       if (st.winner > 0) {
         const i128 Atot = (i128)(((unsigned __int128)st.atot_hi << 64) | st.atot_lo);
@@ -629,6 +638,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         const i128 bestV = (Atot - Ap) * st.winner * ((i128)1 << 20) + Ap * c.p * M;
         if (Atot * next_m * ((i128)1 << 20) <= bestV) break;
       }
+      finished = false;
       wave++;
       reset_mode = 0;
       continue;
@@ -650,6 +660,10 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     reset_mode = 2;  // fresh status (prep recomputes its fields), records, wave state
     tm.n = 3;  // re-time the retried stages
     if (attempt >= 8) return TABI_ECAPACITY;
+  }
+  if (!finished) {
+    ctx->err = "candidate wave loop did not terminate";
+    return TABI_ECUDA;
   }
   ctx->last_n = n;
   ctx->last_M = M;

@@ -312,7 +312,8 @@ constexpr int kFusedHeadCells = TABI_HEAD_CELLS;  // quarter-size tiles below th
 
 struct Status {       // device-side status block, copied back once per pack
   int32_t bad_chart;  // INT32_MAX if none
-  int32_t capacity;   // required column/row slot totals exceeded capacity
+  int32_t capacity;   // bit 0: footprint slots, bit 1: lock-pair lists exceed the buffers
+                      // (grow + retry); bit 2: a vertex range beyond max_vertices
   int32_t winner;     // winning m (0 = none)
   int32_t cols_total, rows_total;
   int32_t pad[3];
@@ -392,8 +393,11 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
 
 // Launch wrappers (defined in the .cu files)
 namespace tabi {
+// max_v: capacity of qx/qy; a chart's vertex range outside [0, max_v) sets
+// Status::capacity bit 2 (-> TABI_ECAPACITY) before anything is written
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
-                    uint32_t flags, int32_t* qx, int32_t* qy, Proxies P, Status* st, cudaStream_t s);
+                    uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
+                    cudaStream_t s);
 // Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
 void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
                   int32_t* rdy, int64_t nrdy, cudaStream_t s);
