@@ -146,6 +146,52 @@ tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start
 const char* tabi_status_str(tabi_status s);
 const char* tabi_last_error(tabi_ctx* ctx);   /* last CUDA error text, or "" */
 
+/* ---- many independent atlases on ONE GPU as one device pipeline ----
+ * SURVEY §3(iii) / §8(e); "one work group per scale factor" is the unit
+ * of work.  The atlases' charts are stored back to back:
+ *   xy           all outlines, 2*V floats;
+ *   chart_start  N + 1 int32 GLOBAL vertex offsets into xy (chart_start[0] = 0),
+ *                N = atlas_start[n_atlases]; chart c owns [chart_start[c], chart_start[c+1]);
+ *   atlas_start  n_atlases + 1 int32 chart offsets (HOST pointer always): atlas a owns the
+ *                global charts [atlas_start[a], atlas_start[a+1]); chart indices in
+ *                infos[a].bad_chart are atlas-local;
+ *   res_xy       2 * n_atlases floats (host) or NULL (1, 1 for every atlas);
+ *   spec         one spec for every atlas;
+ *   out          N placements, global chart order (host or device, as on_device);
+ *                entries of an atlas whose status is not TABI_OK are unspecified;
+ *   infos        n_atlases entries or NULL (scale_index, l2_stretch, rows, knees,
+ *                bad_chart as for tabi_pack; stage_ms / device_ms are 0);
+ *   atlas_status n_atlases tabi_status or NULL;
+ *   binfo        batch totals or NULL.
+ * Pipeline (one stream, 4 kernels, one sync): batched proxies over every chart
+ * -> one CTA per atlas for its sort + slot layout -> a persistent kernel whose
+ * CTAs take (atlas, candidate) items from a device work queue: each item
+ * rasterizes the atlas's footprints at that scale, computes its pair offsets
+ * and runs Alg. 4 in the CTA's own buffers; a failed candidate queues the next
+ * lower scale, a success writes the atlas's placements.  The candidates of one
+ * atlas are evaluated top-down from its area bound, so the result of every
+ * atlas is bit-identical to tabi_pack's.  Atlases with more than 2048 charts,
+ * with a hybrid tail (t_opt resolving to > 0), or that overflow the batch's
+ * per-CTA buffers are packed afterwards by tabi_pack on the same context
+ * (binfo->solo_atlases counts them; the context's max_charts / max_vertices
+ * must cover them).  Workspace grows to the largest batch seen.
+ * Returns TABI_OK if every atlas is OK or NO_FIT, else the first other error
+ * (per-atlas detail in atlas_status). */
+typedef struct {
+  float device_ms;                /* batch device span on the stream (CUDA events) */
+  int32_t gpu_launches;           /* kernels launched (batch + solo packs) */
+  int32_t candidates_evaluated;   /* (atlas, candidate) items run by the batch kernel */
+  int32_t batched_atlases;        /* atlases packed by the device batch */
+  int32_t solo_atlases;           /* atlases packed by tabi_pack afterwards */
+  int32_t reserved[3];
+} tabi_batch_info;
+
+tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t n_atlases, const float* xy,
+                           const int32_t* chart_start, const int32_t* atlas_start,
+                           const float* res_xy, const tabi_spec* spec, tabi_placement* out,
+                           tabi_info* infos, int32_t* atlas_status, tabi_batch_info* binfo,
+                           int on_device, void* stream);
+
 /* ---- batches of independent atlases over several GPUs ----
  * A single pack never shards; a batch shards by atlas.  tabi_shard_plan
  * assigns atlas i to GPU assignment[i] by LPT (longest processing time first):

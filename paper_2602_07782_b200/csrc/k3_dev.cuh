@@ -265,7 +265,8 @@ struct Scale {
   int32_t r0;  // first sorted position rasterized (tail mode), else 0
 };
 
-// Rasterize the footprints of the TC charts [s0, s0 + TC) of candidate m with
+// Rasterize the footprints of the TC charts [s0, s0 + TC) at scale sc into the
+// per-candidate arrays of index `slot` (m - 1 for a single pack) with
 // TT threads (8 per chart during setup).  Charts that fit the dilated atlas but
 // have more than kRaw raw cells are left for a warp-per-chart pass: their tile
 // index is flagged in big[ci].  Writes wd/hd, the footprint slots, cand_bad.
@@ -277,7 +278,7 @@ template <int TC, int TT, int RAW, class Sync, class Mark = NoMark>
 __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, const PackParams& pp,
                             const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
                             uint32_t* dcol, uint32_t* drow, int32_t* wd_all, int32_t* hd_all,
-                            int32_t* cand_bad, int m, int s0, Scale sc, ChartK3* CH,
+                            int32_t* cand_bad, int slot, int s0, Scale sc, ChartK3* CH,
                             int32_t* cells, int32_t* cpre, int32_t* opre, int32_t* chunk_end,
                             int32_t* big, int32_t* tabs, uint32_t* raw, int nt, int tid,
                             Sync sync, Mark setup_done = Mark()) {
@@ -304,11 +305,11 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
     H.rnw = rcp_approx((double)H.nw);
     H.rnh = rcp_approx((double)H.nh);
     H.j8 = P.obb_j[c];
-    const int64_t b = (int64_t)(m - 1) * pp.n + s;
+    const int64_t b = (int64_t)slot * pp.n + s;
     wd_all[b] = H.ws + 2 * g;
     hd_all[b] = H.hs + 2 * g;
     const bool fits = H.ws + 2 * g <= pp.Wp && H.hs + 2 * g <= pp.Hp;
-    if (!fits) cand_bad[m - 1] = 1;
+    if (!fits) cand_bad[slot] = 1;
     H.small = fits && (H.ws + H.hs <= RAW);
     big[ci] = fits && !H.small;
     H.col_o = colofs[s];
@@ -319,8 +320,8 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   if (ci < nt && CH[ci].small) chart_setup(CH[ci], tabs + ci * 4 * k, P, k, num, SC, r);
   sync();
   setup_done(0);
-  uint32_t* colb = dcol + (int64_t)(m - 1) * pp.col_cap;
-  uint32_t* rowb = drow + (int64_t)(m - 1) * pp.row_cap;
+  uint32_t* colb = dcol + (int64_t)slot * pp.col_cap;
+  uint32_t* rowb = drow + (int64_t)slot * pp.row_cap;
   int cb = 0;
   while (cb < nt && cells[cb] == 0) cb++;
   while (cb < nt) {
@@ -417,7 +418,7 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
 // straight into the HBM slot, then an in-place dilation.
 __device__ inline void big_chart(const Proxies& P, const int32_t* __restrict__ perm, const PackParams& pp,
                           const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
-                          uint32_t* dcol, uint32_t* drow, int m, int s, Scale sc, ChartK3& H,
+                          uint32_t* dcol, uint32_t* drow, int slot, int s, Scale sc, ChartK3& H,
                           int32_t* tab, int lane) {
   const int k = pp.k;
   const int64_t num = sc.num, SC = sc.SC;
@@ -437,8 +438,8 @@ __device__ inline void big_chart(const Proxies& P, const int32_t* __restrict__ p
   __syncwarp();
   if (lane < 8) chart_setup(H, tab, P, k, num, SC, lane);
   __syncwarp();
-  uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap + colofs[s];
-  uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
+  uint32_t* col = dcol + (int64_t)slot * pp.col_cap + colofs[s];
+  uint32_t* row = drow + (int64_t)slot * pp.row_cap + rowofs[s];
   for (int64_t e = lane; e < (int64_t)H.ws + H.hs; e += 32) {
     const int ax = e >= H.ws;
     const int64_t i = ax ? e - H.ws : e;
@@ -456,15 +457,15 @@ __device__ inline void big_chart(const Proxies& P, const int32_t* __restrict__ p
 __device__ __forceinline__ void pair_offset(const PackParams& pp, const int32_t* __restrict__ rowofs,
                                             const uint32_t* drow, const int32_t* wd_all,
                                             const int32_t* hd_all, int32_t* off_all,
-                                            uint8_t* lock_all, int m, int s, int lane) {
-  const int64_t base = (int64_t)(m - 1) * pp.n;
+                                            uint8_t* lock_all, int slot, int s, int lane) {
+  const int64_t base = (int64_t)slot * pp.n;
   if (s == pp.n - 1) {
     if (lane == 0) { off_all[base + s] = 0; lock_all[base + s] = 0; }
     return;
   }
   const int32_t Hda = hd_all[base + s], Hdb = hd_all[base + s + 1], Wda = wd_all[base + s];
-  const uint32_t* ra = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-  const uint32_t* rb = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s + 1];
+  const uint32_t* ra = drow + (int64_t)slot * pp.row_cap + rowofs[s];
+  const uint32_t* rb = drow + (int64_t)slot * pp.row_cap + rowofs[s + 1];
   const int rows = min(Hda, Hdb);
   int32_t off = 0;
   for (int j = lane; j < rows; j += 32) off = max(off, hi16(ra[j]) - lo16(rb[j]));
@@ -487,13 +488,13 @@ template <int TT, class Sync>
 __device__ void pair_offset_group(const PackParams& pp, const int32_t* __restrict__ rowofs,
                                   const uint32_t* drow, const int32_t* wd_all,
                                   const int32_t* hd_all, int32_t* off_all, uint8_t* lock_all,
-                                  int m, int s, int tid, Sync sync, int32_t* red) {
+                                  int slot, int s, int tid, Sync sync, int32_t* red) {
   constexpr int NW = TT / 32;
   const int lane = tid & 31, w = tid >> 5;
-  const int64_t base = (int64_t)(m - 1) * pp.n;
+  const int64_t base = (int64_t)slot * pp.n;
   const int32_t Hda = hd_all[base + s], Hdb = hd_all[base + s + 1], Wda = wd_all[base + s];
-  const uint32_t* ra = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s];
-  const uint32_t* rb = drow + (int64_t)(m - 1) * pp.row_cap + rowofs[s + 1];
+  const uint32_t* ra = drow + (int64_t)slot * pp.row_cap + rowofs[s];
+  const uint32_t* rb = drow + (int64_t)slot * pp.row_cap + rowofs[s + 1];
   const int rows = min(Hda, Hdb);
   int32_t off = 0;
   for (int j = tid; j < rows; j += TT) off = max(off, hi16(ra[j]) - lo16(rb[j]));

@@ -217,13 +217,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             const int32_t* off_all, const uint8_t* lock_all,
             const int32_t* __restrict__ hsorted, const int32_t* cand_bad,
             int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
-            Cand* cands, Status* st, int32_t prof_cap, int jslot, Ready rd, unsigned char* dsm) {
+            Cand* cands, Status* st, int32_t prof_cap, int m, int slot, int jslot, Ready rd,
+            unsigned char* dsm) {
+  // m: the candidate scale m/M; slot: its index in the per-candidate arrays
+  // (m - 1 for a single pack, the CTA's own buffers in batch mode); jslot: its
+  // wave slot (ready flags, early exit)
   __shared__ Smem S;
   __shared__ int32_t ready_upto;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid >= kPT) return;
-  const int m = wave_m(pp, st->pad[2], st->b0, jslot);
-  if (m == 0) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
   // wait until every sorted position <= s_hi has its footprints, width/height
@@ -307,14 +309,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     pk_sync();
     return ready_lim;
   };
-  const int64_t cb = (int64_t)(m - 1) * n;
+  const int64_t cb = (int64_t)slot * n;
   const int32_t* wd = wd_all + cb;
   const int32_t* hd = hd_all + cb;
   const int32_t* off = off_all + cb;
   const uint8_t* lk = lock_all + cb;
-  const uint32_t* col = dcol + (int64_t)(m - 1) * pp.col_cap;
-  const uint32_t* row = drow + (int64_t)(m - 1) * pp.row_cap;
-  int32_t* sc = scratch + (int64_t)(m - 1) * (6 * (int64_t)n + 3 * pair_cap);
+  const uint32_t* col = dcol + (int64_t)slot * pp.col_cap;
+  const uint32_t* row = drow + (int64_t)slot * pp.row_cap;
+  int32_t* sc = scratch + (int64_t)slot * (6 * (int64_t)n + 3 * pair_cap);
   int32_t* xs0 = sc;
   int32_t* xs1 = sc + n;
   int32_t* Yc = sc + 2 * (int64_t)n;  // [4][n]
@@ -364,9 +366,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
   int32_t* qrow = sc + 5 * (int64_t)n;    // prefix row id per sorted position (tail)
   if (prefix_mode) {
-    if (pp.T.state[m - 1] != TAIL_READY) return;
-  } else if (!rd.flags && cand_bad[m - 1]) {  // a chart exceeds the dilated atlas at this scale
-    if (tid == 0) cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
+    if (pp.T.state[slot] != TAIL_READY) return;
+  } else if (!rd.flags && cand_bad[slot]) {  // a chart exceeds the dilated atlas at this scale
+    if (tid == 0) cands[slot] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
     return;
   }
   if (!prefix_mode && !rd.flags) {  // work accounting: footprint entries K3 produced
@@ -376,7 +378,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
     if (lane == 0) atomicAdd(&st->work_prof, pe);
   }
-  int32_t* fsave = pp.T.fsave + (int64_t)(m - 1) * pp.T.fstride;
+  int32_t* fsave = pp.T.fsave + (int64_t)slot * pp.T.fstride;
   #pragma unroll 1  // (cold or short: keep the code small)
   for (int x = tid; x < Wp; x += kPT) F[x] = prefix_mode ? fsave[x] : 0;  // top
   if (tid == 0) {
@@ -389,8 +391,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     S.prefix_rows = 0;
     S.switched = 0;
     if (prefix_mode) {  // continue from the state saved at the switch
-      const Cand cd = cands[m - 1];
-      S.row_start = pp.T.r0[m - 1];
+      const Cand cd = cands[slot];
+      S.row_start = pp.T.r0[slot];
       S.fmax = cd.score; S.rows = cd.rows; S.knees_found = cd.knees_found;
       S.knee_rows = cd.knee_rows;
     }
@@ -537,7 +539,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       if (hs0 * 10000 < (int64_t)pp.t_opt * pp.H) {
         if (rd.flags) {  // fused: the split path never switches a candidate with a bad chart
           wait_upto(n - 1);
-          if (__ldcg(cand_bad + m - 1)) {
+          if (__ldcg(cand_bad + slot)) {
             if (tid == 0) S.fail = 1;
             pk_sync();
             break;
@@ -546,10 +548,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         #pragma unroll 1  // (cold or short: keep the code small)
         for (int x = tid; x < Wp; x += kPT) fsave[x] = F[x];
         if (tid == 0) {
-          pp.T.state[m - 1] = TAIL_LAYOUT;
-          pp.T.r0[m - 1] = rs;
-          pp.T.iter[m - 1] = 0;
-          cands[m - 1] = Cand{0, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1, rs, 0,
+          pp.T.state[slot] = TAIL_LAYOUT;
+          pp.T.r0[slot] = rs;
+          pp.T.iter[slot] = 0;
+          cands[slot] = Cand{0, S.fmax, S.rows, S.knees_found, S.knee_rows, 0, 0, 1, rs, 0,
                               0ull, 0ull};
           S.switched = 1;
         }
@@ -1144,8 +1146,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // fused mode: report a chart that exceeds the dilated atlas the way the
     // split path does (the whole candidate's footprints must be in first)
     wait_upto(n - 1);
-    if (tid == 0 && !S.abort && __ldcg(cand_bad + m - 1)) {
-      cands[m - 1] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
+    if (tid == 0 && !S.abort && __ldcg(cand_bad + slot)) {
+      cands[slot] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
       return;
     }
   }
@@ -1155,14 +1157,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // sequential fused mode: announce the success so lower candidates stop
     if (!S.fail && rd.flags && pp.early) atomicMin(&st->win_j, jslot);
     if (prefix_mode) {  // keep the tail's area (written by the layout kernel)
-      const Cand prev = cands[m - 1];
+      const Cand prev = cands[slot];
       cd.prefix_rows = S.prefix_rows;
-      cd.p = pp.T.p[m - 1];
-      cd.switched_at = pp.T.r0[m - 1];
+      cd.p = pp.T.p[slot];
+      cd.switched_at = pp.T.r0[slot];
       cd.apre_lo = prev.apre_lo;
       cd.apre_hi = prev.apre_hi;
     }
-    cands[m - 1] = cd;
+    cands[slot] = cd;
   }
 }
 
@@ -1175,8 +1177,10 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
             int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
             Cand* cands, Status* st, int32_t prof_cap) {
   extern __shared__ __align__(16) unsigned char dsm[];
+  const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.x);
+  if (m == 0) return;
   packer(pp, colofs, rowofs, dcol, drow, wd_all, hd_all, off_all, lock_all, hsorted, cand_bad,
-         scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, blockIdx.x,
+         scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, m, m - 1, blockIdx.x,
          Ready{nullptr, 0, nullptr, nullptr}, dsm);
 }
 
@@ -1246,8 +1250,10 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   const int Bw = pp.wave == 0 ? st->b0 : pp.B;
   if (threadIdx.x == 0) atomicMin(&st->tr[0], gtime());
   if ((int)blockIdx.x < Bw) {
+    const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.x);
+    if (m == 0) return;
     packer(pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, hsorted,
-           ra.cand_bad, scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap,
+           ra.cand_bad, scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, m, m - 1,
            blockIdx.x, Ready{ra.rdy, T, ra.tstart, ra.tix}, dsm);
     return;
   }
@@ -1338,7 +1344,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
     const k3::Scale sc{m, SCm, 0};
     k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
-                                       ra.hd, ra.cand_bad, m, s0, sc, CH, cells, cpre, opre,
+                                       ra.hd, ra.cand_bad, m - 1, s0, sc, CH, cells, cpre, opre,
                                        &misc[1], big, tabs, raw, nt, gt, gsync,
                                        [&](int w) {
                                          if (w == 0) rmark(6);
@@ -1353,7 +1359,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 #endif
     for (int ci = gw; ci < nt; ci += kRGW)
       if (big[ci])
-        k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m, s0 + ci, sc, CW[wid],
+        k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m - 1, s0 + ci, sc, CW[wid],
                       wtab + wid * 4 * k, lane);
     if (gt < 32) {  // work accounting: footprint entries of the tile (from smem)
       unsigned long long pe = 0;
@@ -1401,10 +1407,10 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     };
     for (int s = lo + gw; s <= hi; s += kRGW)
       if (!big_pair(s))
-        k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, lane);
+        k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s, lane);
     for (int s = lo; s <= hi; s++)
       if (big_pair(s))
-        k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m, s, gt,
+        k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s, gt,
                                     gsync, red);
     gsync();
     rmark(4);
@@ -1427,6 +1433,179 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 #endif
     }
     rmark(5);
+  }
+}
+
+// ---- batch mode (tabi_pack_many): a persistent work queue of (atlas,
+// candidate) items, one CTA per item, no cross-CTA waiting --------------------
+// Item (a, r) evaluates m = m_hi(a) - r, m_hi the atlas's area bound.  The CTA
+// rasterizes all of the atlas's footprints at m/M (tile_raster over 64-chart
+// tiles, large charts warp by warp) into its own buffers, computes every
+// adjacent pair's offset and locks (warp per pair), then runs the packer (the
+// same Alg. 4 code as a single pack).  Success: m is the largest successful
+// scale (every higher one was evaluated and failed, or is above the exact area
+// bound -- SURVEY §3(iii)'s top-down order), so the CTA scatters the
+// placements.  Failure: the item (a, r + 1) is appended to the queue.  A CTA
+// that draws a ticket past the queue's end waits until the ticket is filled
+// or every atlas is decided; items are only ever produced by running CTAs, so
+// the queue cannot deadlock.  P:307 "one work group per scale factor" is the
+// unit; the batch gives each GPU hundreds of them in flight.
+__device__ __forceinline__ int32_t ld_acquire_i(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kNT, 1)
+many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ int32_t item_s, outcome_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gcta = blockIdx.x;
+  const int64_t nm = A.nmax;
+  uint32_t* dcol = A.dcol + (int64_t)gcta * pp0.col_cap;
+  uint32_t* drow = A.drow + (int64_t)gcta * pp0.row_cap;
+  int32_t* wd = A.wd + gcta * nm;
+  int32_t* hd = A.hd + gcta * nm;
+  int32_t* off = A.off + gcta * nm;
+  uint8_t* lock = A.lock + gcta * nm;
+  int32_t* scr = A.scratch + (int64_t)gcta * (6 * nm + 3 * A.pair_cap);
+  int32_t* X = A.X + gcta * nm;
+  int32_t* Y = A.Y + gcta * nm;
+  uint8_t* mir = A.mir + gcta * nm;
+  Cand* cand = A.cands + gcta;
+  int32_t* cbad = A.cand_bad + gcta;
+  const int k = pp0.k, g = pp0.g;
+  const int64_t SCm = (int64_t)pp0.M * TABI_UNITS;
+  while (true) {
+    if (tid == 0) {
+      const int i = atomicAdd(&A.qctl[0], 1);
+      int v = -1;
+      if (i < A.qcap) {
+        while ((v = ld_acquire_i(A.q + i)) < 0) {
+          if (ld_acquire_i(A.qctl + 2) == 0) break;  // every atlas decided
+          __nanosleep(256);
+        }
+      }
+      item_s = v;
+    }
+    __syncthreads();
+    const int item = item_s;
+    if (item < 0) break;
+    const int a = item & 0xfffff, r = item >> 20;
+    Status* st = A.sts + a;
+    const int c0 = A.abase[a], n = A.abase[a + 1] - c0;
+    const int m = st->pad[2] - r;
+    const bool dead = st->bad_chart != INT32_MAX || st->capacity || m < 1 || n < 1 || n > A.nmax;
+    PackParams pp = pp0;
+    pp.n = n;
+    Proxies P = A.P;
+    P.w += c0; P.h += c0; P.area2 += c0; P.xmin += c0; P.ymin += c0; P.pose += c0;
+    P.prerot += c0; P.sl += (int64_t)c0 * 4 * k; P.obb_j += c0; P.obb += 4 * (int64_t)c0;
+    const int32_t* perm = A.perm + c0;
+    const int32_t* colofs = A.colofs + c0;
+    const int32_t* rowofs = A.rowofs + c0;
+    if (!dead) {
+      // ---- footprints of every chart at m/M (K3, D11 + D13) ----------------
+      if (tid == 0) { *cbad = 0; *cand = Cand{}; }
+      __syncthreads();
+      {
+        unsigned char* p = dsm;
+        k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kTCF);
+        int32_t* cells = (int32_t*)carve(p, 4 * kTCF);
+        int32_t* cpre = (int32_t*)carve(p, 4 * (kTCF + 1));
+        int32_t* opre = (int32_t*)carve(p, 4 * (kTCF + 1));
+        int32_t* big = (int32_t*)carve(p, 4 * kTCF);
+        int32_t* misc = (int32_t*)carve(p, 32);
+        carve(p, 4 * (2 * kRGW + 4));
+        int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kTCF * 4 * k);
+        uint32_t* raw = (uint32_t*)carve(p, 4 * (size_t)kRawF);
+        p = dsm + group_bytes(k) * kRG;
+        k3::ChartK3* CW = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kNW);
+        int32_t* wtab = (int32_t*)carve(p, (size_t)4 * kNW * 4 * k);
+        const k3::Scale sc{m, SCm, 0};
+        for (int s0 = 0; s0 < n; s0 += kTCF) {
+          const int nt = min(kTCF, n - s0);
+          k3::tile_raster<kTCF, kNT, kRawF>(P, perm, pp, colofs, rowofs, dcol, drow, wd, hd, cbad,
+                                            0, s0, sc, CH, cells, cpre, opre, &misc[1], big, tabs,
+                                            raw, nt, tid, [] { __syncthreads(); });
+          for (int ci = wid; ci < nt; ci += kNW)
+            if (big[ci])
+              k3::big_chart(P, perm, pp, colofs, rowofs, dcol, drow, 0, s0 + ci, sc, CW[wid],
+                            wtab + wid * 4 * k, lane);
+          __syncthreads();
+        }
+      }
+      // ---- adjacent pairs: compaction advance + locks (K3b, D14 + D15) ------
+      if (!*(volatile int32_t*)cbad)
+        for (int s = wid; s < n; s += kNW)
+          k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, 0, s, lane);
+      __syncthreads();
+      // ---- Alg. 4 for this candidate (K4) -----------------------------------
+      packer(pp, colofs, rowofs, dcol, drow, wd, hd, off, lock, A.hsorted + c0, cbad, scr,
+             A.pair_cap, X, Y, mir, cand, st, prof_cap, m, 0, 0, Ready{nullptr, 0, nullptr, nullptr},
+             dsm);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const Cand cd = *cand;  // (written by this CTA before the barrier)
+      int oc;  // 0 failed -> next candidate, 1 succeeded, 2 decided without success
+      if (dead) oc = 2;
+      else if (cd.success) oc = 1;
+      else oc = m > 1 ? 0 : 2;
+      AtlasRes& R = A.res[a];
+      if (!dead) R.evaluated++;
+      if (oc == 1) {
+        R.winner = m;
+        R.rows = cd.rows;
+        R.knees_found = cd.knees_found;
+        R.knee_rows = cd.knee_rows;
+      }
+      outcome_s = oc;
+    }
+    __syncthreads();
+    const int oc = outcome_s;
+    if (oc == 1) {  // K5 for this atlas: placements in input order
+      for (int s = tid; s < n; s += kNT) {
+        const int c = perm[s];
+        const uint8_t ps = P.pose[c];
+        tabi_placement pl;
+        pl.tx = X[s];
+        pl.ty = Y[s];
+        pl.scale_num = m;
+        pl.scale_den = pp.M;
+        pl.box_w = wd[s] - 2 * g;
+        pl.box_h = hd[s] - 2 * g;
+        pl.rot90 = ps & 1;
+        pl.flip_x = (ps >> 1) & 1;
+        pl.flip_y = (ps >> 2) & 1;
+        pl.mirror_x = mir[s];
+        pl.mode = 0;
+        pl.prerot = P.prerot[c];
+        pl.pad[0] = pl.pad[1] = 0;
+        A.out[c0 + c] = pl;
+      }
+    }
+    __syncthreads();  // (placements written before the atlas is announced)
+    if (tid == 0) {
+      if (oc == 0) {
+        const int slot = atomicAdd(&A.qctl[1], 1);
+        if (slot < A.qcap) {
+          st_release_i(A.q + slot, a | ((r + 1) << 20));
+        } else {  // (cannot happen: the queue holds M items per atlas)
+          atomicOr(&st->capacity, 8);
+          __threadfence();
+          atomicSub(&A.qctl[2], 1);
+        }
+      } else {
+        A.res[a].done = 1;
+        __threadfence();
+        atomicSub(&A.qctl[2], 1);
+      }
+    }
   }
 }
 
@@ -1566,6 +1745,32 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                   &ra};
   return cudaLaunchCooperativeKernel((const void*)fused_kernel, dim3(grid), dim3(kNT), args,
                                      kMaxDynSmem, s);
+}
+
+int many_grid(int device) {
+  static std::atomic<int> cached[64] = {};
+  static std::atomic<bool> have[64] = {};
+  if (device < 0 || device >= 64) return 0;
+  if (!have[device].load(std::memory_order_acquire)) {
+    cudaFuncSetAttribute(many_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, many_kernel, kNT, kMaxDynSmem);
+    cached[device].store(sms * (per > 0 ? per : 1), std::memory_order_relaxed);
+    have[device].store(true, std::memory_order_release);
+  }
+  return cached[device].load(std::memory_order_relaxed);
+}
+
+cudaError_t launch_many(int grid, const PackParams& pp, const ManyArgs& a, cudaStream_t s) {
+  static std::atomic<unsigned long long> attr{0};
+  ensure_dyn_smem((const void*)many_kernel, kMaxDynSmem, attr);
+  const int f_words = (pp.Wp + 3) & ~3;
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN +
+                                         2 * (size_t)kPairSm) + kRW + kPWN + kPairSm;
+  const int32_t prof_cap = (int32_t)(((size_t)kMaxDynSmem - fixed) / 4) & ~3;
+  many_kernel<<<grid, kNT, kMaxDynSmem, s>>>(pp, a, prof_cap);
+  return cudaGetLastError();
 }
 
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,

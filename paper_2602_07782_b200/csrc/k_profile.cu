@@ -66,7 +66,7 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   }
   int32_t* tabs = dyn;  // [kTC][2 axes][k][2]
   uint32_t* raw = (uint32_t*)(dyn + kTC * 4 * pp.k);
-  tile_raster<kTC, kTT, kRaw>(P, perm, pp, colofs, rowofs, dcol, drow, wd_all, hd_all, cand_bad, m,
+  tile_raster<kTC, kTT, kRaw>(P, perm, pp, colofs, rowofs, dcol, drow, wd_all, hd_all, cand_bad, m - 1,
                               s0, sc, CH, cells, cpre, opre, &chunk_end, big, tabs, raw,
                               min(kTC, pp.n - s0), (int)threadIdx.x, [] { __syncthreads(); });
   if (threadIdx.x == 0) {
@@ -89,7 +89,7 @@ profile_big_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   for (int it = blockIdx.x * kWarps + wib; it < nbig; it += gridDim.x * kWarps) {
     const int item = big_list[it];
     const int m = item / pp.n + 1, s = item % pp.n;
-    big_chart(P, perm, pp, colofs, rowofs, dcol, drow, m, s, scale_of(pp, m), CH[wib], tab, lane);
+    big_chart(P, perm, pp, colofs, rowofs, dcol, drow, m - 1, s, scale_of(pp, m), CH[wib], tab, lane);
   }
 }
 
@@ -107,7 +107,7 @@ offsets_kernel(PackParams pp, const int32_t* __restrict__ rowofs, const uint32_t
   const int s = (int)(item % pp.n);
   if (cand_bad[m - 1]) return;
   if (pp.tail && (pp.T.state[m - 1] != TAIL_LAYOUT || s < pp.T.r0[m - 1])) return;
-  pair_offset(pp, rowofs, drow, wd_all, hd_all, off_all, lock_all, m, s, lane);
+  pair_offset(pp, rowofs, drow, wd_all, hd_all, off_all, lock_all, m - 1, s, lane);
 }
 
 }  // namespace

@@ -246,7 +246,7 @@ template <int G>
 __global__ void __launch_bounds__(kBlock)
 proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
              float ry, int k, uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P,
-             Status* st) {
+             Status* st, AtlasMap am) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, gib = threadIdx.x / G;
   Group<G> g;
@@ -254,6 +254,21 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   g.mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane / G * G));
   const int c = blockIdx.x * (kBlock / G) + gib;
   if (c >= n) return;  // the whole group leaves together
+  // batch mode (tabi_pack_many): chart c is global; its atlas a is the last
+  // with abase[a] <= c (uniform per group), which owns the status block, the
+  // resolution and the chart index reported on EINVAL
+  int32_t cl = c;
+  if (am.abase) {
+    int lo = 0, hi = am.na - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (am.abase[mid] <= c) lo = mid;
+      else hi = mid - 1;
+    }
+    st += lo;
+    cl = c - am.abase[lo];
+    if (am.res) { rx = am.res[2 * lo]; ry = am.res[2 * lo + 1]; }
+  }
   Slices S;
   {
     unsigned char* p = dsm + slice_bytes(k) * gib;
@@ -275,7 +290,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     return;
   }
   if (nv < 3) {
-    if (gl == 0) atomicMin(&st->bad_chart, c);
+    if (gl == 0) atomicMin(&st->bad_chart, cl);
     return;
   }
   int32_t* X = qx + a0;
@@ -298,7 +313,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     ymn = min(ymn, iy); ymx = max(ymx, iy);
   }
   if (__ballot_sync(g.mask, !ok) != 0u) {
-    if (gl == 0) atomicMin(&st->bad_chart, c);
+    if (gl == 0) atomicMin(&st->bad_chart, cl);
     return;
   }
   int prerot = 0;
@@ -337,7 +352,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   s2 = g.sum128(s2);
   if (s2 < 0) s2 = -s2;
   if (s2 == 0) {
-    if (gl == 0) atomicMin(&st->bad_chart, c);
+    if (gl == 0) atomicMin(&st->bad_chart, cl);
     return;
   }
   // D3 90-degree normalization: (x, y) -> (h - y, x) iff w > h
@@ -447,28 +462,28 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
 template <int G>
 void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
               uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-              cudaStream_t s) {
+              AtlasMap am, cudaStream_t s) {
   constexpr int per_block = kBlock / G;
   const int blocks = (n + per_block - 1) / per_block;
   const size_t smem = slice_bytes(k) * per_block;
   static std::atomic<unsigned long long> attr{0};  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
   ensure_dyn_smem((const void*)proxy_kernel<G>, (int)(slice_bytes(TABI_KMAX) * per_block), attr);
   proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P,
-                                                st);
+                                                st, am);
 }
 
 }  // namespace
 
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-                    cudaStream_t s) {
+                    cudaStream_t s, AtlasMap am) {
   const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
   const int forced = genv ? atoi(genv) : 0;
   const int G = forced == 8 || forced == 16 || forced == 32 ? forced
                 : n < 4096 ? 32 : n < 8192 ? 16 : 8;  // measured: C3 (1572) 32, C4 (20000) 8
-  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, s);
-  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, s);
-  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, s);
+  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
+  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
+  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
 }
 
 }  // namespace tabi

@@ -516,6 +516,47 @@ sort_prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww,
   prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy);
 }
 
+// Batch mode (tabi_pack_many): one CTA per atlas -- its order (register
+// bitonic, N <= 2048) and slot layout, written at the atlas's chart offset
+// (tile arrays at offset + atlas index: one more tstart entry per atlas).
+__global__ void __launch_bounds__(kT, 1)
+many_sort_prep_kernel(Proxies P, const int32_t* __restrict__ abase, int32_t* perm, PackParams pp,
+                      int32_t* colofs, int32_t* rowofs, int32_t* hsorted, int32_t* tstart,
+                      int32_t* tix, Status* sts) {
+  const int a = blockIdx.x;
+  const int c0 = abase[a], n = abase[a + 1] - c0;
+  Status* st = sts + a;
+  if (n < 1 || n > 2 * kT || st->bad_chart != INT32_MAX || st->capacity) return;
+  PackParams q = pp;
+  q.n = n;
+  bitonic_reg_body(P.h + c0, P.w + c0, n, perm + c0);
+  __syncthreads();
+  prep_body(P.h + c0, P.w + c0, P.area2 + c0, perm + c0, q, colofs + c0, rowofs + c0,
+            hsorted + c0, tstart + c0 + a, tix + c0, st, nullptr);
+}
+
+// Batch mode: per-atlas status blocks and results, and the pack work queue
+// (items [0, E) = the batched atlases in `order`, candidate offset 0; the
+// rest empty).
+__global__ void many_reset_kernel(Status* sts, AtlasRes* res, int32_t A, const int32_t* order,
+                                  int32_t E, int32_t* q, int32_t qcap, int32_t* qctl) {
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t a = t0; a < A; a += stride) {
+    uint32_t* w = (uint32_t*)(sts + a);
+    for (size_t i = 0; i < sizeof(Status) / 4; i++) w[i] = 0;
+    sts[a].bad_chart = INT32_MAX;
+    sts[a].win_j = INT32_MAX;
+    res[a] = AtlasRes{0, 0, 0, 0, 0, 0};
+  }
+  for (int64_t i = t0; i < qcap; i += stride) q[i] = i < E ? order[i] : -1;
+  if (t0 == 0) {
+    qctl[0] = 0;  // head
+    qctl[1] = E;  // tail
+    qctl[2] = E;  // atlases not yet decided
+  }
+}
+
 // One launch instead of a status upload plus a string of memsets.
 // mode 2: initialise the status block (bad_chart = none, trace start = max);
 // mode >= 1: zero the candidate records and hybrid-tail states;
@@ -599,6 +640,22 @@ bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int
   sort_prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart,
                                     tix, st, rdy);
   return true;
+}
+
+void launch_many_sort_prep(const Proxies& P, const int32_t* abase, int32_t A, int32_t* perm,
+                          const PackParams& pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
+                          int32_t* tstart, int32_t* tix, Status* sts, cudaStream_t s) {
+  many_sort_prep_kernel<<<A, kT, 0, s>>>(P, abase, perm, pp, colofs, rowofs, hsorted, tstart, tix,
+                                         sts);
+}
+
+void launch_many_reset(Status* sts, AtlasRes* res, int32_t A, const int32_t* order, int32_t E,
+                       int32_t* q, int32_t qcap, int32_t* qctl, cudaStream_t s) {
+  const int64_t work = qcap > A ? qcap : A;
+  int blocks = (int)((work + 255) / 256);
+  if (blocks > 296) blocks = 296;
+  if (blocks < 1) blocks = 1;
+  many_reset_kernel<<<blocks, 256, 0, s>>>(sts, res, A, order, E, q, qcap, qctl);
 }
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,

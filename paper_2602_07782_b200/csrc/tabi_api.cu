@@ -46,6 +46,58 @@ struct GraphKey {
   }
 };
 
+// Batch-mode workspace (tabi_pack_many): chart-indexed arrays for every atlas
+// of the batch, per-atlas status / results, the work queue, and one set of
+// per-candidate buffers per persistent CTA.  Grows to the largest batch seen.
+struct ManyWs {
+  int64_t cap_N = 0, cap_V = 0, cap_A = 0, cap_q = 0;
+  int32_t cap_k = 0, nmax = 0, G = 0;
+  int64_t col_cap = 0, row_cap = 0, pair_cap = 0;
+  // chart-indexed
+  float* d_xy = nullptr;          // staging for host-mode outlines (2V floats)
+  int32_t* d_start = nullptr;     // staging for host-mode chart offsets (N + 1)
+  int32_t* qx = nullptr;
+  int32_t* qy = nullptr;
+  Proxies P{};
+  int32_t *perm = nullptr, *colofs = nullptr, *rowofs = nullptr, *hsorted = nullptr;
+  int32_t *tstart = nullptr, *tix = nullptr;
+  tabi_placement* d_out = nullptr;
+  // atlas-indexed: abase (A + 1) | order (A) | res (2A floats) in one upload
+  int32_t* d_small = nullptr;
+  int32_t* h_small = nullptr;     // pinned
+  Status* sts = nullptr;
+  AtlasRes* res = nullptr;        // device; followed by nothing
+  Status* h_sts = nullptr;        // pinned copies
+  AtlasRes* h_res = nullptr;
+  int32_t* q = nullptr;           // [cap_q] queue + [4] control words at the end
+  // per persistent CTA
+  uint32_t *dcol = nullptr, *drow = nullptr;
+  int32_t *wd = nullptr, *hd = nullptr, *off = nullptr, *scratch = nullptr, *X = nullptr, *Y = nullptr;
+  uint8_t *lock = nullptr, *mir = nullptr;
+  Cand* cands = nullptr;
+  int32_t* cand_bad = nullptr;
+  int32_t* solo_start = nullptr;  // rebased chart offsets of a solo atlas (device mode)
+  // pinned host staging for host-mode inputs / outputs
+  float* h_xy = nullptr;          // 2V floats + N + 1 ints
+  int64_t h_cap = 0;
+  tabi_placement* h_out = nullptr;
+  int64_t h_out_cap = 0;
+  cudaEvent_t span[2] = {nullptr, nullptr};
+  void release() {
+    void* ds[] = {d_xy, d_start, qx, qy, P.w, P.h, P.area2, P.xmin, P.ymin, P.pose, P.prerot, P.sl,
+                  P.obb_j, P.obb, perm, colofs, rowofs, hsorted, tstart, tix, d_out, d_small, sts,
+                  res, q, dcol, drow, wd, hd, off, scratch, X, Y, lock, mir, cands, cand_bad,
+                  solo_start};
+    for (void* p : ds)
+      if (p) cudaFree(p);
+    void* hs[] = {h_small, h_sts, h_res, h_xy, h_out};
+    for (void* p : hs)
+      if (p) cudaFreeHost(p);
+    for (auto& e : span)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 struct tabi_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -112,6 +164,7 @@ struct tabi_ctx {
   bool fused_off = false;  // the cooperative launch was refused once: split kernels from now on
   Validator val;           // tabi_validate scratch (N3)
   cudaEvent_t span[2] = {nullptr, nullptr};  // tabi_info.device_ms
+  ManyWs many;             // tabi_pack_many
 };
 
 #define CK(call)                                              \
@@ -145,6 +198,7 @@ static void dfree_all(tabi_ctx* ctx) {
   for (void* p : ps)
     if (p) cudaFree(p);
   ctx->val.release();
+  ctx->many.release();
   for (auto& e : ctx->span)
     if (e) cudaEventDestroy(e);
   void* hs[] = {ctx->h_status, ctx->h_xy, ctx->h_start, ctx->h_out};
@@ -703,6 +757,348 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   return TABI_OK;
 }
 
+// ---- many atlases on one GPU: one device pipeline (tabi_pack_many) ----------
+
+template <class T>
+static cudaError_t grow(T** p, int64_t count) {
+  return dalloc(p, (size_t)(count > 0 ? count : 1));
+}
+
+static tabi_status many_ensure(tabi_ctx* ctx, int64_t N, int64_t V, int32_t A, int32_t k,
+                               int32_t nmax, int32_t M, int32_t side) {
+  ManyWs& w = ctx->many;
+  if (!w.span[0]) {
+    CK(cudaEventCreate(&w.span[0]));
+    CK(cudaEventCreate(&w.span[1]));
+  }
+  const int32_t G = many_grid(ctx->device);
+  if (G < 1) {
+    ctx->err = "batch kernel cannot be resident";
+    return TABI_ECUDA;
+  }
+  if (N > w.cap_N || k > w.cap_k || A > w.cap_A) {
+    const int64_t n = std::max(N, w.cap_N), kk = std::max<int64_t>(k, w.cap_k);
+    const int64_t a = std::max<int64_t>(A, w.cap_A);
+    CK(grow(&w.P.w, n)); CK(grow(&w.P.h, n)); CK(grow(&w.P.area2, n));
+    CK(grow(&w.P.xmin, n)); CK(grow(&w.P.ymin, n)); CK(grow(&w.P.pose, n));
+    CK(grow(&w.P.prerot, n)); CK(grow(&w.P.sl, n * 4 * kk)); CK(grow(&w.P.obb_j, n));
+    CK(grow(&w.P.obb, 4 * n)); CK(grow(&w.perm, n)); CK(grow(&w.colofs, n));
+    CK(grow(&w.rowofs, n)); CK(grow(&w.hsorted, n)); CK(grow(&w.tix, n));
+    CK(grow(&w.tstart, n + a + 1)); CK(grow(&w.d_out, n)); CK(grow(&w.d_start, n + 1));
+    w.cap_N = n;
+    w.cap_k = (int32_t)kk;
+  }
+  if (V > w.cap_V) {
+    CK(grow(&w.qx, V)); CK(grow(&w.qy, V)); CK(grow(&w.d_xy, 2 * V));
+    w.cap_V = V;
+  }
+  if (A > w.cap_A || (int64_t)A * M > w.cap_q) {
+    const int64_t a = std::max<int64_t>(A, w.cap_A);
+    const int64_t qc = std::max<int64_t>((int64_t)A * M, w.cap_q);
+    CK(grow(&w.d_small, 4 * a + 1));
+    CK(grow(&w.sts, a));
+    CK(grow(&w.res, a));
+    CK(grow(&w.q, qc + 4));
+    CK(grow(&w.tstart, w.cap_N + a + 1));
+    if (w.h_small) cudaFreeHost(w.h_small);
+    if (w.h_sts) cudaFreeHost(w.h_sts);
+    if (w.h_res) cudaFreeHost(w.h_res);
+    w.h_small = nullptr; w.h_sts = nullptr; w.h_res = nullptr;
+    CK(cudaMallocHost((void**)&w.h_small, sizeof(int32_t) * (4 * a + 1)));
+    CK(cudaMallocHost((void**)&w.h_sts, sizeof(Status) * a));
+    CK(cudaMallocHost((void**)&w.h_res, sizeof(AtlasRes) * a));
+    w.cap_A = a;
+    w.cap_q = qc;
+  }
+  const int64_t col0 = ((int64_t)nmax * 96 + 4 * (int64_t)side + 1024) & ~(int64_t)3;
+  const int64_t pair0 = 2 * (int64_t)nmax + 1024;
+  const bool cta = nmax > w.nmax || G != w.G || col0 > w.col_cap || pair0 > w.pair_cap;
+  if (cta || !w.dcol) {
+    w.nmax = std::max(nmax, w.nmax);
+    w.G = G;
+    w.col_cap = std::max(col0, w.col_cap);
+    w.row_cap = std::max(col0, w.row_cap);
+    w.pair_cap = std::max(pair0, w.pair_cap);
+    const int64_t nm = w.nmax;
+    CK(grow(&w.dcol, (int64_t)G * w.col_cap));
+    CK(grow(&w.drow, (int64_t)G * w.row_cap));
+    CK(grow(&w.wd, G * nm)); CK(grow(&w.hd, G * nm)); CK(grow(&w.off, G * nm));
+    CK(grow(&w.X, G * nm)); CK(grow(&w.Y, G * nm));
+    CK(grow(&w.lock, G * nm)); CK(grow(&w.mir, G * nm));
+    CK(grow(&w.scratch, (int64_t)G * (6 * nm + 3 * w.pair_cap)));
+    CK(grow(&w.cands, G)); CK(grow(&w.cand_bad, G));
+  }
+  return TABI_OK;
+}
+
+// Grow the per-CTA footprint slots / pair lists to what a capacity-flagged
+// atlas needed (the slot totals are in its status block).
+static tabi_status many_grow_cta(tabi_ctx* ctx, const Status& st) {
+  ManyWs& w = ctx->many;
+  const int64_t G = w.G, nm = w.nmax;
+  if (st.capacity & 1) {
+    w.col_cap = std::max<int64_t>(w.col_cap, ((int64_t)st.cols_total + (st.cols_total >> 2) + 1024) & ~(int64_t)3);
+    w.row_cap = std::max<int64_t>(w.row_cap, ((int64_t)st.rows_total + (st.rows_total >> 2) + 1024) & ~(int64_t)3);
+    CK(grow(&w.dcol, G * w.col_cap));
+    CK(grow(&w.drow, G * w.row_cap));
+  }
+  if (st.capacity & 2) {
+    w.pair_cap = std::max<int64_t>(w.pair_cap, (int64_t)st.pad[0] * 2 + 1024);
+    CK(grow(&w.scratch, G * (6 * nm + 3 * w.pair_cap)));
+  }
+  return TABI_OK;
+}
+
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
+                                      const int32_t* chart_start, const int32_t* atlas_start,
+                                      const float* res_xy, const tabi_spec* spec,
+                                      tabi_placement* out, tabi_info* infos,
+                                      int32_t* atlas_status, tabi_batch_info* binfo, int on_device,
+                                      void* stream) {
+  if (!ctx) return TABI_EINVAL;
+  if (binfo) memset(binfo, 0, sizeof(*binfo));
+  if (A < 1 || !xy || !chart_start || !atlas_start || !out || !spec_ok(spec)) return TABI_EINVAL;
+  if (atlas_start[0] != 0) return TABI_EINVAL;
+  for (int32_t a = 0; a < A; a++)
+    if (atlas_start[a + 1] < atlas_start[a]) return TABI_EINVAL;
+  const int64_t N = atlas_start[A];
+  if (N < 1 || spec->atlas_w > ctx->max_side || spec->atlas_h > ctx->max_side) {
+    return N < 1 ? TABI_EINVAL : TABI_ECAPACITY;
+  }
+  ctx->last_cuda = cudaSuccess;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+  std::vector<tabi_status> stv(A, TABI_OK);
+  std::vector<tabi_info> inf(A);
+  for (auto& i : inf) {
+    memset(&i, 0, sizeof(i));
+    i.bad_chart = -1;
+  }
+  // atlases the device batch takes: 1 <= n <= kManyMaxCharts and a sequential
+  // search (t_opt resolves to 0; P:418 gives 0 for every atlas this small);
+  // the others ("solo") go through tabi_pack one by one, largest first
+  std::vector<int32_t> order, solo;
+  int32_t nmax = 1;
+  for (int32_t a = 0; a < A; a++) {
+    const int32_t n = atlas_start[a + 1] - atlas_start[a];
+    const int32_t t = spec->t_opt_bp >= 0 ? spec->t_opt_bp : (n > 10000 ? 100 : 0);
+    if (n < 1) {
+      stv[a] = TABI_EINVAL;
+    } else if (n <= kManyMaxCharts && t == 0) {
+      order.push_back(a);
+      nmax = std::max(nmax, n);
+    } else {
+      solo.push_back(a);
+    }
+  }
+  // LPT: the largest atlases first, so the queue's tail holds small items
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    return atlas_start[x + 1] - atlas_start[x] > atlas_start[y + 1] - atlas_start[y];
+  });
+  const int32_t E = (int32_t)order.size();
+  int launches = 0;
+  float dev_ms = 0.f;
+  int32_t evaluated = 0;
+  if (E > 0) {
+    int64_t V = 0;
+    if (on_device) {
+      int32_t v = 0;
+      CK(cudaMemcpyAsync(&v, chart_start + N, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      V = v;
+    } else {
+      V = chart_start[N];
+      if (chart_start[0] != 0) return TABI_EINVAL;
+    }
+    if (V < 3) return TABI_EINVAL;
+    const int32_t M = spec->scale_count;
+    tabi_status ts = many_ensure(ctx, N, V, A, spec->local_aabb_count, nmax, M,
+                                 std::max(spec->atlas_w, spec->atlas_h));
+    if (ts != TABI_OK) return ts;
+    ManyWs& w = ctx->many;
+    CK(cudaEventRecord(w.span[0], s));
+    const float* d_xy = xy;
+    const int32_t* d_start = chart_start;
+    if (!on_device) {
+      // pinned caller memory is copied directly; pageable memory via staging
+      if (host_pinned(xy)) {
+        CK(cudaMemcpyAsync(w.d_xy, xy, sizeof(float) * 2 * V, cudaMemcpyHostToDevice, s));
+      } else {
+        if (w.h_cap < 2 * V) {
+          if (w.h_xy) cudaFreeHost(w.h_xy);
+          w.h_xy = nullptr;
+          CK(cudaMallocHost((void**)&w.h_xy, sizeof(float) * 2 * V));
+          w.h_cap = 2 * V;
+        }
+        memcpy(w.h_xy, xy, sizeof(float) * 2 * V);
+        CK(cudaMemcpyAsync(w.d_xy, w.h_xy, sizeof(float) * 2 * V, cudaMemcpyHostToDevice, s));
+      }
+      CK(cudaMemcpyAsync(w.d_start, chart_start, sizeof(int32_t) * (N + 1), cudaMemcpyHostToDevice, s));
+      d_xy = w.d_xy;
+      d_start = w.d_start;
+    }
+    // abase (A + 1) | order (E) | res (2A floats): one upload
+    int32_t* hs = w.h_small;
+    memcpy(hs, atlas_start, sizeof(int32_t) * (A + 1));
+    for (int32_t i = 0; i < E; i++) hs[A + 1 + i] = order[i];  // item (a, r = 0)
+    float* hr = (float*)(hs + 2 * A + 1);
+    for (int32_t a = 0; a < A; a++) {
+      hr[2 * a] = res_xy ? res_xy[2 * a] : 1.0f;
+      hr[2 * a + 1] = res_xy ? res_xy[2 * a + 1] : 1.0f;
+    }
+    CK(cudaMemcpyAsync(w.d_small, hs, sizeof(int32_t) * (4 * (size_t)A + 1), cudaMemcpyHostToDevice, s));
+    const int32_t* d_abase = w.d_small;
+    const int32_t* d_order = w.d_small + A + 1;
+    const float* d_res = (const float*)(w.d_small + 2 * A + 1);
+    const int32_t qcap = (int32_t)std::min<int64_t>(w.cap_q, (int64_t)E * M);
+    int32_t* qctl = w.q + w.cap_q;
+    PackParams pp;
+    memset(&pp, 0, sizeof(pp));
+    pp.n = 0;
+    pp.k = spec->local_aabb_count;
+    pp.M = M;
+    pp.g = spec->gutter;
+    pp.W = spec->atlas_w;
+    pp.H = spec->atlas_h;
+    pp.Wp = spec->atlas_w + 2 * spec->gutter;
+    pp.Hp = spec->atlas_h + 2 * spec->gutter;
+    pp.flags = spec->flags;
+    pp.B = 1;
+    pp.col_cap = w.col_cap;
+    pp.row_cap = w.row_cap;
+    launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, s);
+    launch_proxies(d_xy, d_start, (int32_t)N, 1.0f, 1.0f, pp.k, pp.flags, w.qx, w.qy, w.cap_V, w.P,
+                   w.sts, s, AtlasMap{d_abase, A, d_res});
+    launch_many_sort_prep(w.P, d_abase, A, w.perm, pp, w.colofs, w.rowofs, w.hsorted, w.tstart,
+                          w.tix, w.sts, s);
+    ManyArgs ma;
+    ma.P = w.P;
+    ma.abase = d_abase;
+    ma.perm = w.perm;
+    ma.colofs = w.colofs;
+    ma.rowofs = w.rowofs;
+    ma.hsorted = w.hsorted;
+    ma.sts = w.sts;
+    ma.res = w.res;
+    ma.out = on_device ? out : w.d_out;
+    ma.q = w.q;
+    ma.qctl = qctl;
+    ma.qcap = qcap;
+    ma.dcol = w.dcol;
+    ma.drow = w.drow;
+    ma.wd = w.wd;
+    ma.hd = w.hd;
+    ma.off = w.off;
+    ma.lock = w.lock;
+    ma.scratch = w.scratch;
+    ma.X = w.X;
+    ma.Y = w.Y;
+    ma.mir = w.mir;
+    ma.cands = w.cands;
+    ma.cand_bad = w.cand_bad;
+    ma.nmax = w.nmax;
+    ma.pair_cap = w.pair_cap;
+    CK(launch_many(w.G, pp, ma, s));
+    launches = 4;
+    if (!on_device) {
+      tabi_placement* dst = out;
+      if (!host_pinned(out)) {
+        if (w.h_out_cap < N) {
+          if (w.h_out) cudaFreeHost(w.h_out);
+          w.h_out = nullptr;
+          CK(cudaMallocHost((void**)&w.h_out, sizeof(tabi_placement) * N));
+          w.h_out_cap = N;
+        }
+        dst = w.h_out;
+      }
+      CK(cudaMemcpyAsync(dst, w.d_out, sizeof(tabi_placement) * N, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaMemcpyAsync(w.h_sts, w.sts, sizeof(Status) * A, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(AtlasRes) * A, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(w.span[1], s));
+    CK(cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&dev_ms, w.span[0], w.span[1]);
+    const bool staged = !on_device && !host_pinned(out);
+    for (int32_t i = 0; i < E; i++) {
+      const int32_t a = order[i];
+      const Status& st = w.h_sts[a];
+      const AtlasRes& R = w.h_res[a];
+      evaluated += R.evaluated;
+      if (st.bad_chart != INT32_MAX) {
+        stv[a] = TABI_EINVAL;
+        inf[a].bad_chart = st.bad_chart;
+      } else if (st.capacity & 4) {
+        stv[a] = TABI_ECAPACITY;
+      } else if (st.capacity) {  // slots / pair lists too small: grow, then solo
+        ts = many_grow_cta(ctx, st);
+        if (ts != TABI_OK) return ts;
+        solo.push_back(a);
+      } else if (R.winner > 0) {
+        tabi_info& f = inf[a];
+        f.scale_index = R.winner;
+        f.l2_stretch = (double)M / (double)R.winner;  // D26: uniform scale m/M
+        f.rows = R.rows;
+        f.knees_found = R.knees_found;
+        f.knee_rows = R.knee_rows;
+        const int32_t c0 = atlas_start[a], n = atlas_start[a + 1] - c0;
+        if (staged) memcpy(out + c0, w.h_out + c0, sizeof(tabi_placement) * n);
+      } else {
+        stv[a] = TABI_NO_FIT;
+      }
+    }
+  }
+  // solo atlases (hybrid tail, more than kManyMaxCharts charts, or a capacity
+  // retry) through the single-pack path, atlas-local chart offsets
+  for (int32_t a : solo) {
+    const int32_t c0 = atlas_start[a], n = atlas_start[a + 1] - c0;
+    const float rx = res_xy ? res_xy[2 * a] : 1.0f, ry = res_xy ? res_xy[2 * a + 1] : 1.0f;
+    std::vector<int32_t> loc(n + 1);
+    if (on_device) {
+      CK(cudaMemcpyAsync(loc.data(), chart_start + c0, sizeof(int32_t) * (n + 1),
+                         cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    } else {
+      memcpy(loc.data(), chart_start + c0, sizeof(int32_t) * (n + 1));
+    }
+    const int32_t v0 = loc[0];
+    for (auto& v : loc) v -= v0;
+    if (on_device) {
+      ManyWs& w = ctx->many;
+      if (!w.solo_start || w.cap_N < n + 1) CK(grow(&w.solo_start, std::max<int64_t>(n + 1, w.cap_N + 1)));
+      CK(cudaMemcpyAsync(w.solo_start, loc.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
+      stv[a] = tabi_pack(ctx, xy + 2 * (int64_t)v0, w.solo_start, n, rx, ry, spec, out + c0, &inf[a],
+                         1, s);
+    } else {
+      stv[a] = tabi_pack(ctx, xy + 2 * (int64_t)v0, loc.data(), n, rx, ry, spec, out + c0, &inf[a],
+                         0, s);
+    }
+    launches += inf[a].gpu_launches;
+  }
+  tabi_status ret = TABI_OK;
+  for (int32_t a = 0; a < A; a++) {
+    if (atlas_status) atlas_status[a] = stv[a];
+    if (infos) infos[a] = inf[a];
+    if (ret == TABI_OK && stv[a] != TABI_OK && stv[a] != TABI_NO_FIT) ret = stv[a];
+  }
+  if (binfo) {
+    binfo->device_ms = dev_ms;
+    binfo->gpu_launches = launches;
+    binfo->candidates_evaluated = evaluated;
+    binfo->solo_atlases = (int32_t)solo.size();
+    binfo->batched_atlases = E;
+  }
+  return ret;
+}
+
 // ---- batches over several GPUs --------------------------------
 
 extern "C" tabi_status tabi_shard_plan(int32_t n_atlases, const int32_t* n_charts, int32_t n_gpus,
@@ -735,22 +1131,106 @@ extern "C" tabi_status tabi_pack_batch(tabi_ctx* const* ctxs, int32_t n_gpus, in
                                        const tabi_spec* specs, tabi_placement* const* out,
                                        tabi_info* infos) {
   if (!ctxs || n_gpus < 1 || n_atlases < 0) return TABI_EINVAL;
+  if (n_atlases == 0) return TABI_OK;
+  if (!xy || !chart_start || !n_charts || !specs || !out) return TABI_EINVAL;
   std::vector<int32_t> asg(n_atlases);
   tabi_status st = tabi_shard_plan(n_atlases, n_charts, n_gpus, asg.data());
   if (st != TABI_OK) return st;
   std::vector<tabi_status> res(n_atlases, TABI_OK);
+  std::vector<tabi_status> gst(n_gpus, TABI_OK);
+  // One host thread per GPU.  Its atlases are grouped by spec; each group is
+  // gathered back to back into the context's pinned staging and packed by
+  // ONE tabi_pack_many call (device batch pipeline), then scattered to out[i].
   std::vector<std::thread> th;
   for (int32_t g = 0; g < n_gpus; g++) {
     th.emplace_back([&, g]() {
-      for (int32_t i = 0; i < n_atlases; i++) {
-        if (asg[i] != g) continue;
-        const float rx = res_xy ? res_xy[2 * i] : 1.0f, ry = res_xy ? res_xy[2 * i + 1] : 1.0f;
-        res[i] = tabi_pack(ctxs[g], xy[i], chart_start[i], n_charts[i], rx, ry, &specs[i], out[i],
-                           infos ? &infos[i] : nullptr, 0, nullptr);
+      tabi_ctx* ctx = ctxs[g];
+      std::vector<int32_t> mine;
+      for (int32_t i = 0; i < n_atlases; i++)
+        if (asg[i] == g) mine.push_back(i);
+      std::vector<char> used(mine.size(), 0);
+      for (size_t u = 0; u < mine.size(); u++) {
+        if (used[u]) continue;
+        std::vector<int32_t> grp;  // atlases with the same spec as mine[u]
+        for (size_t v = u; v < mine.size(); v++)
+          if (!used[v] && memcmp(&specs[mine[v]], &specs[mine[u]], sizeof(tabi_spec)) == 0) {
+            grp.push_back(mine[v]);
+            used[v] = 1;
+          }
+        const int32_t A = (int32_t)grp.size();
+        std::vector<int32_t> abase(A + 1, 0);
+        std::vector<float> rxy(2 * (size_t)A);
+        int64_t V = 0;
+        bool bad = false;
+        for (int32_t j = 0; j < A; j++) {
+          const int32_t i = grp[j];
+          abase[j + 1] = abase[j] + n_charts[i];
+          if (n_charts[i] < 1 || chart_start[i][0] != 0) bad = true;
+          else V += chart_start[i][n_charts[i]];
+          rxy[2 * j] = res_xy ? res_xy[2 * i] : 1.0f;
+          rxy[2 * j + 1] = res_xy ? res_xy[2 * i + 1] : 1.0f;
+        }
+        if (bad) {  // malformed atlas: pack one by one so each gets its own status
+          for (int32_t i : grp) {
+            const float rx = res_xy ? res_xy[2 * i] : 1.0f, ry = res_xy ? res_xy[2 * i + 1] : 1.0f;
+            res[i] = tabi_pack(ctx, xy[i], chart_start[i], n_charts[i], rx, ry, &specs[i], out[i],
+                               infos ? &infos[i] : nullptr, 0, nullptr);
+          }
+          continue;
+        }
+        const int64_t N = abase[A];
+        ManyWs& w = ctx->many;
+        if (cudaSetDevice(ctx->device) != cudaSuccess) { gst[g] = TABI_ECUDA; return; }
+        if (w.h_cap < 2 * V) {
+          if (w.h_xy) cudaFreeHost(w.h_xy);
+          w.h_xy = nullptr;
+          w.h_cap = 0;
+          if (cudaMallocHost((void**)&w.h_xy, sizeof(float) * 2 * V) != cudaSuccess) {
+            gst[g] = TABI_ECUDA;
+            return;
+          }
+          w.h_cap = 2 * V;
+        }
+        if (w.h_out_cap < N) {
+          if (w.h_out) cudaFreeHost(w.h_out);
+          w.h_out = nullptr;
+          w.h_out_cap = 0;
+          if (cudaMallocHost((void**)&w.h_out, sizeof(tabi_placement) * N) != cudaSuccess) {
+            gst[g] = TABI_ECUDA;
+            return;
+          }
+          w.h_out_cap = N;
+        }
+        std::vector<int32_t> cs(N + 1);
+        int64_t vo = 0;
+        for (int32_t j = 0; j < A; j++) {
+          const int32_t i = grp[j], n = n_charts[i];
+          const int32_t nv = chart_start[i][n];
+          memcpy(w.h_xy + 2 * vo, xy[i], sizeof(float) * 2 * (size_t)nv);
+          for (int32_t c = 0; c < n; c++) cs[abase[j] + c] = (int32_t)vo + chart_start[i][c];
+          vo += nv;
+        }
+        cs[N] = (int32_t)vo;
+        std::vector<tabi_info> inf(A);
+        std::vector<int32_t> ast(A);
+        tabi_placement* hout = w.h_out;
+        const tabi_status r = tabi_pack_many(ctx, A, w.h_xy, cs.data(), abase.data(), rxy.data(),
+                                             &specs[grp[0]], hout, inf.data(), ast.data(), nullptr,
+                                             0, nullptr);
+        if (r == TABI_ECUDA) { gst[g] = r; return; }
+        for (int32_t j = 0; j < A; j++) {
+          const int32_t i = grp[j];
+          res[i] = (tabi_status)ast[j];
+          if (infos) infos[i] = inf[j];
+          if (ast[j] == TABI_OK)
+            memcpy(out[i], hout + abase[j], sizeof(tabi_placement) * (size_t)n_charts[i]);
+        }
       }
     });
   }
   for (auto& t : th) t.join();
+  for (int32_t g = 0; g < n_gpus; g++)
+    if (gst[g] != TABI_OK) return gst[g];
   for (int32_t i = 0; i < n_atlases; i++)
     if (res[i] != TABI_OK && res[i] != TABI_NO_FIT) return res[i];
   return TABI_OK;

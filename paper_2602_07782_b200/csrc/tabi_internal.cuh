@@ -355,6 +355,15 @@ struct Cand {
   unsigned long long apre_lo, apre_hi;  // 2 x area of the prefix-folded tail (D25), int128
 };
 
+// Batch mode (tabi_pack_many): the outcome of one atlas.
+struct AtlasRes {
+  int32_t winner;      // largest successful m, 0 = none (NO_FIT or not decided)
+  int32_t rows, knees_found, knee_rows;
+  int32_t evaluated;   // candidates evaluated (top-down from the area bound)
+  int32_t done;        // 1 once decided (success or every candidate failed)
+};
+constexpr int kManyMaxCharts = 2048;  // per atlas in the device batch (one-CTA sort)
+
 // Hybrid prefix tail state per candidate (DESIGN.md §1 A12).
 enum { TAIL_NONE = 0, TAIL_LAYOUT = 1, TAIL_READY = 2, TAIL_FAIL = 3 };
 struct TailBufs {
@@ -393,11 +402,19 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
 
 // Launch wrappers (defined in the .cu files)
 namespace tabi {
+// Batch mode (tabi_pack_many): charts of na atlases back to back, atlas a owning
+// the global charts [abase[a], abase[a+1]) with status block st[a] and
+// resolution res[2a..2a+1] (nullptr: rx, ry).  abase == nullptr: one atlas.
+struct AtlasMap {
+  const int32_t* abase;
+  int32_t na;
+  const float* res;
+};
 // max_v: capacity of qx/qy; a chart's vertex range outside [0, max_v) sets
 // Status::capacity bit 2 (-> TABI_ECAPACITY) before anything is written
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-                    cudaStream_t s);
+                    cudaStream_t s, AtlasMap am = AtlasMap{nullptr, 1, nullptr});
 // Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
 void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
                   int32_t* rdy, int64_t nrdy, cudaStream_t s);
@@ -437,6 +454,48 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                          const int32_t* tstart, const int32_t* tix, int32_t* scratch,
                          int64_t pair_cap, int32_t* X, int32_t* Y, uint8_t* mir, Cand* cands,
                          Status* st, cudaStream_t s);
+// Batch mode (tabi_pack_many): sort + slot layout per atlas
+// (one CTA each), queue reset, and the persistent pack kernel in which each
+// CTA takes (atlas, candidate) items -- rasterizes the atlas's footprints at
+// that scale, computes its pair offsets and runs Alg. 4, all in its own
+// buffers -- pushing the next lower candidate on failure (top-down search,
+// exact) and scattering the placements on success.
+struct ManyArgs {
+  Proxies P;                      // global (chart-indexed)
+  const int32_t* abase;           // [A + 1] first global chart of each atlas
+  const int32_t* perm;            // per atlas at abase[a]: sorted position -> atlas-local chart
+  const int32_t* colofs;
+  const int32_t* rowofs;
+  const int32_t* hsorted;
+  Status* sts;                    // [A]
+  AtlasRes* res;                  // [A]
+  tabi_placement* out;            // global (chart-indexed)
+  int32_t* q;                     // [qcap] items a | r << 20 (r = candidates below m_hi), -1 empty
+  int32_t* qctl;                  // head, tail, atlases pending
+  int32_t qcap;
+  // per-CTA buffers, CTA g at g * (stride)
+  uint32_t* dcol;                 // [G][col_cap]
+  uint32_t* drow;                 // [G][row_cap]
+  int32_t* wd;                    // [G][nmax] (also hd, off, X, Y below)
+  int32_t* hd;
+  int32_t* off;
+  uint8_t* lock;
+  int32_t* scratch;               // [G][6 nmax + 3 pair_cap]
+  int32_t* X;
+  int32_t* Y;
+  uint8_t* mir;
+  Cand* cands;                    // [G]
+  int32_t* cand_bad;              // [G]
+  int32_t nmax;
+  int64_t pair_cap;
+};
+void launch_many_reset(Status* sts, AtlasRes* res, int32_t A, const int32_t* order, int32_t E,
+                       int32_t* q, int32_t qcap, int32_t* qctl, cudaStream_t s);
+void launch_many_sort_prep(const Proxies& P, const int32_t* abase, int32_t A, int32_t* perm,
+                          const PackParams& pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
+                          int32_t* tstart, int32_t* tix, Status* sts, cudaStream_t s);
+int many_grid(int device);  // persistent CTAs (one per SM)
+cudaError_t launch_many(int grid, const PackParams& pp, const ManyArgs& a, cudaStream_t s);
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
                    const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s);

@@ -65,6 +65,12 @@ class Validation(C.Structure):
                 ("bad_chart", C.c_int32), ("gpu_launches", C.c_int32)]
 
 
+class BatchInfo(C.Structure):
+    _fields_ = [("device_ms", C.c_float), ("gpu_launches", C.c_int32),
+                ("candidates_evaluated", C.c_int32), ("batched_atlases", C.c_int32),
+                ("solo_atlases", C.c_int32), ("reserved", C.c_int32 * 3)]
+
+
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
                             ("scale_den", "<i4"), ("box_w", "<i4"), ("box_h", "<i4"),
                             ("rot90", "u1"), ("flip_x", "u1"), ("flip_y", "u1"),
@@ -112,6 +118,8 @@ def lib():
         L.tabi_debug_trace_raster.argtypes = [P, P]
         L.tabi_shard_plan.argtypes = [i32, P, i32, P]
         L.tabi_pack_batch.argtypes = [P, i32, i32, P, P, P, P, P, P, P]
+        L.tabi_pack_many.argtypes = [P, i32, P, P, P, P, C.POINTER(Spec), P, P, P,
+                                     C.POINTER(BatchInfo), C.c_int, P]
         L.tabi_validate.argtypes = [P, P, P, i32, C.c_float, C.c_float, i32, i32, i32, P,
                                     C.POINTER(Validation), C.c_int, P]
         _lib = L
@@ -121,7 +129,28 @@ def lib():
 EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
            "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace",
-           "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch", "tabi_validate"]
+           "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch", "tabi_pack_many",
+           "tabi_validate"]
+
+
+def concat_chart_sets(chart_sets):
+    """Marshal independent chart sets into tabi_pack_many's layout: outlines
+    back to back, GLOBAL vertex offsets, per-atlas chart offsets and
+    resolutions.  Returns (xy float32[2V], chart_start int32[N+1],
+    atlas_start int32[A+1], res_xy float32[2A])."""
+    xys, starts, abase, res = [], [], [0], []
+    vo = 0
+    for cs in chart_sets:
+        st = np.asarray(cs.start, dtype=np.int64)
+        xys.append(np.asarray(cs.xy, dtype=np.float32))
+        starts.append((st[:-1] + vo).astype(np.int32))
+        vo += int(st[-1])
+        abase.append(abase[-1] + cs.n_charts)
+        r = getattr(cs, "res", 1.0)
+        res.extend((r, r))
+    starts.append(np.array([vo], dtype=np.int32))
+    return (np.concatenate(xys), np.concatenate(starts), np.asarray(abase, dtype=np.int32),
+            np.asarray(res, dtype=np.float32))
 
 
 def shard_plan(n_charts, n_gpus: int) -> np.ndarray:
@@ -264,6 +293,45 @@ class Context:
         return dict(status=st, overlap=v.overlap, gutter=v.gutter, oob=v.oob, covered=v.covered,
                     occupancy=v.occupancy, l2_stretch=v.l2_stretch, bad_chart=v.bad_chart,
                     gpu_launches=v.gpu_launches)
+
+    def pack_many(self, xy, chart_start, atlas_start, spec: Spec, res_xy=None, out=None,
+                  stream=None, raise_on_error=True):
+        """Pack many independent atlases as one device pipeline (tabi_pack_many).
+        xy / chart_start (global vertex offsets) / out: host numpy arrays or CUDA
+        tensors (out uint8[32*N]); atlas_start and res_xy are host arrays.
+        Returns (status, placements, [Info], atlas_status int32[A], BatchInfo)."""
+        on_device = hasattr(xy, "is_cuda") and xy.is_cuda
+        abase = np.ascontiguousarray(atlas_start, dtype=np.int32)
+        A = abase.shape[0] - 1
+        N = int(abase[-1])
+        infos = (Info * A)()
+        ast = np.zeros(A, dtype=np.int32)
+        bi = BatchInfo()
+        rp = None
+        if res_xy is not None:
+            res_xy = np.ascontiguousarray(res_xy, dtype=np.float32)
+            rp = _ptr(res_xy)
+        if on_device:
+            import torch
+            if out is None:
+                out = torch.empty(N * PLACEMENT_DTYPE.itemsize, dtype=torch.uint8, device=xy.device)
+            if stream is None:
+                stream = _torch_stream(xy.device)
+            st = lib().tabi_pack_many(self.h, A, _ptr(xy), _ptr(chart_start), _ptr(abase), rp,
+                                      C.byref(spec), _ptr(out), infos, _ptr(ast), C.byref(bi), 1,
+                                      C.c_void_p(stream))
+        else:
+            if not (isinstance(xy, np.ndarray) and xy.dtype == np.float32 and xy.flags.c_contiguous):
+                xy = np.ascontiguousarray(xy, dtype=np.float32)
+            chart_start = np.ascontiguousarray(chart_start, dtype=np.int32)
+            if out is None:
+                out = np.zeros(N, dtype=PLACEMENT_DTYPE)
+            st = lib().tabi_pack_many(self.h, A, _ptr(xy), _ptr(chart_start), _ptr(abase), rp,
+                                      C.byref(spec), _ptr(out), infos, _ptr(ast), C.byref(bi), 0,
+                                      C.c_void_p(stream) if stream else None)
+        if raise_on_error and st not in (OK, NO_FIT):
+            raise TabiError(st, self.last_error())
+        return st, out, list(infos), ast, bi
 
     def pack_set(self, cs, res=None, **spec_kw):
         r = (cs.res, cs.res) if res is None else res
