@@ -1,23 +1,35 @@
 #!/usr/bin/env python
-"""Benchmark of the B200-native TABI packer (BASELINE.json metric).
+"""Benchmark of the B200-native TABI packer (BASELINE.json metric:
+"p50 pack ms @1572 charts 4096^2 atlas; L2 stretch; atlases/s at 1/2/4/8 B200").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload C3|C2|C4] [--rho R]
+                    [--workload C5|C3|C2|C4|C4P|C4X] [--rho R] [--quick]
 
-A *step* is one full pack (all five hot-path stages, all 64 candidate scales)
-of one synthetic chart set of the metric's workload (configs[2]: 1,572 TSS-like
-charts into a 4096^2 atlas, k = 10, t_opt = 0) with inputs resident in HBM.
-Each rank packs its own atlas per step (seed = rank): weak scaling, no data-path
-collective; value = atlases/s over all ranks = N*K / max-over-
-ranks device time.  L2 is flushed (256 MB write) between steps, outside the
-timed events.  Device time per step = the CUDA-event span tabi_pack records on
-the timed stream around its own enqueued work (tabi_info.device_ms); the
-outer per-step events (which also see the host return from the synchronous
-call) are reported as stream_ms_per_step.  Everything timed runs on one
-dedicated stream, so the flush is complete before a pack starts.  `e2e` repeats the measurement through the public host-pointer
-call (H2D of the chart set and D2H of the placements inside the timed region).
-`--impl reference` times the CPU oracle (the only reference this paper has:
-no code) on the box's host cores.
+Default (workload C5): the metric's throughput part, "atlases/s at 1/2/4/8
+B200", on configs[4] -- a batch of 512 independent atlases (200-2,000 TSS-like
+charts each, 2048^2) sharded over the ranks by LPT (strong scaling, no
+data-path collective: SURVEY §8(e)).  A *step* packs every atlas of the rank's
+share through ONE tabi_pack_many call (all hot-path stages for every atlas:
+batched proxies, per-atlas sort, (atlas, candidate) work queue of raster +
+pair offsets + Alg. 4, placements) with inputs resident in HBM.  value = 512 *
+K / (max over ranks of the summed step times), step time = CUDA events on the
+timed stream around the call.  L2 is flushed (256 MB write) between steps,
+outside the events.  `e2e` repeats it through the host-pointer call from
+pinned memory (H2D of the outlines and D2H of the placements inside the timed
+region); `batch.wall_atlases_per_s` is the same call by the host wall clock.
+
+At N = 1 the line also carries the metric's latency part on configs[2]
+(1,572 charts into 4096^2, k = 10, t_opt = 0): p50 / p99 single-pack latency
+(`tabi_pack`, device pointers, the pack's own CUDA-event span) over seeds 0-7 at
+rho = 1.5 -- the fill ratio whose stretch (~1.39) matches the paper's 2K TSS
+regime (1.38) -- and at rho = 0.5 / 2.0; a knob sweep k x t_opt
+(P:897); the latency floor of the packer's building blocks; the
+roofline of the dominant kernel; and the CPU oracle on the box's cores.
+
+--workload C3|C2|C4|C4P|C4X: the round-1 single-pack bench (one atlas per
+rank per step, weak scaling), kept for diagnostics.
+`--impl reference` times the CPU oracle (the only reference this paper has --
+no code) on the same workload, metric and unit, on the box's host cores.
 """
 from __future__ import annotations
 
@@ -36,7 +48,8 @@ METRIC = "p50 pack ms @1572 charts 4096² atlas; L2 stretch; atlases/s at 1/2/4/
 PAPER_CONTEXT = ("paper (RTX 4090, OpenGL): 5.31 ms mean pack for 1,001-5,000 charts (P:672), "
                  "15 ms interactive budget (P:35); Xatlas-random >= 2.5 s for 1,572 charts on a "
                  "Ryzen 7 1800X (P:39)")
-
+C5_ATLASES = 512
+C3_HEADLINE_RHO = 1.5
 
 # spec overrides per workload (beyond the chart set's own fields)
 WORKLOAD_SPEC = {"C4X": {"flags": 32}}
@@ -150,87 +163,204 @@ def barrier(ws):
         dist.barrier()
 
 
-def cpu_oracle_rate(cs, budget_s=15.0, max_candidates=None, **spec_kw):
-    """Time the oracle (as it stands) on host cores: full packs until ~budget_s."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- C5 batch --
+
+def _gen_c5(i):
+    import chartgen
+    return chartgen.config5(i)
+
+
+def c5_sets(indices, procs=None):
+    """configs[4] atlases by index, generated in parallel (pure-Python generator)."""
+    import multiprocessing as mp
+    if len(indices) <= 4:
+        return [_gen_c5(i) for i in indices]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs or min(host_cores(), 32)) as pool:
+        return pool.map(_gen_c5, indices, chunksize=4)
+
+
+def rank_share(ws, rank):
+    import chartgen
+    from paper_2602_07782_b200 import shard_plan
+    sizes = chartgen.config5_sizes(C5_ATLASES)
+    a = shard_plan(sizes, ws)
+    return [i for i in range(C5_ATLASES) if a[i] == rank]
+
+
+def _oracle_pack_time(cs):
+    import oracle
+    t = time.perf_counter()
+    st, pl, info, _ = oracle.pack(cs)
+    return time.perf_counter() - t, info.scale_index
+
+
+def oracle_batch_rate(sets, budget_s=12.0):
+    """The oracle (as it stands, 1 thread per pack) on the box's host cores:
+    one process per core, each packing whole atlases of `sets` (rotating) until
+    ~budget_s.  Returns (atlases/s on all cores, atlases/s on one core, cores,
+    atlases packed, wall seconds)."""
+    import multiprocessing as mp
     import oracle
     oracle.build()
+    cores = host_cores()
+    ctx = mp.get_context("fork")
+    done, t_sum = 0, 0.0
     t0 = time.perf_counter()
-    n = 0
-    while True:
-        st, pl, info, _ = oracle.pack(cs, **spec_kw)
-        n += 1
-        if time.perf_counter() - t0 > budget_s or n >= 64:
-            break
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt, info.scale_index
+    with ctx.Pool(cores) as pool:
+        i = 0
+        while time.perf_counter() - t0 < budget_s and i < 4 * len(sets):
+            chunk = [sets[(i + j) % len(sets)] for j in range(cores)]
+            res = pool.map(_oracle_pack_time, chunk, chunksize=1)
+            done += len(chunk)
+            t_sum += sum(r[0] for r in res)
+            i += cores
+    wall = time.perf_counter() - t0
+    return done / wall, done / t_sum, cores, done, wall
 
 
 def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle on the same workload / metric / unit.
+    Rank 0 alone runs it under torchrun."""
     if rank != 0:
         return
     import oracle
     oracle.build()
-    cs, desc = workload(args.workload, 0, args.rho)
-    kw = WORKLOAD_SPEC.get(args.workload, {})
-    sample_cands = args.steps > 20
-    M = cs.scale_count
+    cores = host_cores()
+    if args.workload == "C5":
+        # a bounded, deterministic sample of the batch: every 8th atlas
+        sets = c5_sets(list(range(0, C5_ATLASES, 8)))
+        import multiprocessing as mp
+        # atlases per step: all cores busy, whole run within a few minutes
+        per = cores if args.steps <= 40 else max(1, cores * 40 // args.steps)
+        pool = mp.get_context("fork").Pool(cores)
 
-    def step(i):
-        if not sample_cands:
+        def step(i):
+            chunk = [sets[(i * per + j) % len(sets)] for j in range(per)]
+            t = time.perf_counter()
+            pool.map(_oracle_pack_time, chunk, chunksize=1)
+            return time.perf_counter() - t, len(chunk)
+
+        for i in range(args.warmup):
+            step(i)
+        rs = [step(args.warmup + i) for i in range(args.steps)]
+        pool.close()
+        tot_t = sum(r[0] for r in rs)
+        tot_a = sum(r[1] for r in rs)
+        value = tot_a / tot_t
+        desc = ("C5 configs[4]: 512 tss atlases (200-2000 charts, 2048x2048); oracle sample "
+                f"= every 8th atlas, {per} per step")
+        sample = (f"per step: {per} whole C5 atlases (every 8th of the batch, rotating), one "
+                  f"oracle pack (all 64 candidates) per process, {cores} processes")
+        ms_step = 1000.0 * tot_t / len(rs)
+    else:
+        cs, desc = workload(args.workload, 0, args.rho)
+        kw = WORKLOAD_SPEC.get(args.workload, {})
+
+        def step(i):
             t = time.perf_counter()
             oracle.pack(cs, **kw)
             return time.perf_counter() - t
-        # bounded sample: proxies+sort+8 of the 64 candidate scales (rotating), scaled to 64
-        ms = [M - ((i % 8) + 8 * j) for j in range(8)]
-        t = time.perf_counter()
-        for m in ms:
-            oracle.pack_candidate(cs, m, **kw)
-        return (time.perf_counter() - t) * M / len(ms)
 
-    for i in range(args.warmup):
-        step(i)
-    times = [step(i) for i in range(args.steps)]
-    ms_step = 1000.0 * sum(times) / len(times)
-    value = 1000.0 / ms_step
-    sample = ("one full oracle pack per step (all 64 candidates)" if not sample_cands else
-              "per step: 8 of the 64 candidate scales (rotating) + proxies/sort, time x 8")
+        for i in range(args.warmup):
+            step(i)
+        times = [step(i) for i in range(args.steps)]
+        ms_step = 1000.0 * sum(times) / len(times)
+        value = 1000.0 / ms_step
+        cores = 1
+        sample = "one full oracle pack per step (all 64 candidates), 1 thread"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "atlases/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic (chartgen, SplitMix64)",
-            "config": {"workload": desc, "impl": "CPU oracle (oracle/, plain C, 1 thread)"},
-            "p50_ms": 1000.0 * statistics.median(times),
-            "cpu_baseline": {"value": value, "unit": "atlases/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "higher_is_better": True, "scaling": "strong" if args.workload == "C5" else "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (chartgen, SplitMix64)",
+            "config": {"workload": desc, "impl": "CPU oracle (oracle/, plain C)"},
+            "cpu_baseline": {"value": value, "unit": "atlases/s", "cores": cores, "kind": "oracle",
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "atlases/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def rank_atlases(name, rank, ws, rho):
-    """The chart sets this rank packs each step, and the per-step total over ranks."""
-    if name == "C5":
-        import chartgen
-        from paper_2602_07782_b200 import shard_plan
-        sizes = chartgen.config5_sizes(512)
-        a = shard_plan(sizes, ws)
-        mine = [chartgen.config5(i) for i in range(512) if a[i] == rank]
-        desc = ("C5 configs[4]: batch of 512 tss atlases (200-2000 charts each, rho~U[0.3,1.5]) "
-                "into 2048x2048, LPT-sharded over the ranks")
-        return mine, desc, 512, "strong"
-    cs, desc = workload(name, rank, rho)
-    return [cs], desc, ws, "weak"
+def c3_latency(ctx, stream, dev, rho, seeds, reps, flush):
+    """tabi_pack latency (device pointers, the pack's own CUDA-event span) over
+    seeds x reps, L2 flushed before each pack."""
+    import torch
+    from paper_2602_07782_b200 import spec_of
+    ms, stretch, rows, ms_m = [], [], [], []
+    for seed in seeds:
+        cs, _ = workload("C3", seed, rho)
+        xy = torch.from_numpy(cs.xy).to(dev)
+        st = torch.from_numpy(cs.start).to(dev)
+        out = torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)
+        spec = spec_of(cs)
+        for _ in range(3):
+            ctx.pack(xy, st, spec, out=out, stream=stream.cuda_stream)
+        for _ in range(reps):
+            flush()
+            info = ctx.pack(xy, st, spec, out=out, stream=stream.cuda_stream)[2]
+            ms.append(info.device_ms)
+        stretch.append(info.l2_stretch)
+        rows.append(info.rows)
+        ms_m.append(info.scale_index)
+    ms.sort()
+    p99 = ms[min(len(ms) - 1, int(round(0.99 * (len(ms) - 1))))]
+    return {"rho": rho, "seeds": list(seeds), "packs": len(ms), "p50_ms": statistics.median(ms),
+            "p99_ms": p99, "mean_ms": statistics.fmean(ms), "l2_stretch_mean": statistics.fmean(stretch),
+            "l2_stretch": stretch, "scale_index": ms_m, "rows": rows}
+
+
+def knob_sweep(ctx, stream, dev, flush, reps=8):
+    """C3 (rho = 1.5, seed 0): local-AABB count k x t_opt."""
+    import torch
+    from paper_2602_07782_b200 import spec_of
+    cs, _ = workload("C3", 0, C3_HEADLINE_RHO)
+    xy = torch.from_numpy(cs.xy).to(dev)
+    st = torch.from_numpy(cs.start).to(dev)
+    out = torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)
+    rows = []
+    for k in (2, 5, 10):
+        for t in (0, 100, 200, 500):
+            spec = spec_of(cs, local_aabb_count=k, t_opt_bp=t)
+            for _ in range(2):
+                ctx.pack(xy, st, spec, out=out, stream=stream.cuda_stream)
+            ms = []
+            for _ in range(reps):
+                flush()
+                info = ctx.pack(xy, st, spec, out=out, stream=stream.cuda_stream)[2]
+                ms.append(info.device_ms)
+            rows.append({"k": k, "t_opt_pct": t / 100.0, "p50_ms": statistics.median(ms),
+                         "l2_stretch": info.l2_stretch, "scale_index": info.scale_index,
+                         "rows": info.rows, "prefix_rows": info.prefix_rows})
+    return rows
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3")
-    ap.add_argument("--rho", type=float, default=0.5)
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--rho", type=float, default=C3_HEADLINE_RHO)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the C3 blocks and the knob sweep")
     ap.add_argument("--flush", default="write", choices=["write", "write+read", "none"],
                     help="L2 flush between timed steps: a 256 MB write (default), or that "
                          "write followed by a 256 MB read so L2 holds no dirty lines; "
@@ -241,7 +371,218 @@ def main():
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
+    if args.workload != "C5":
+        run_single(args, ws, rank, local)
+        return
 
+    import numpy as np
+    import torch
+
+    from paper_2602_07782_b200 import Context, concat_chart_sets, latency_floor, spec_of
+    from paper_2602_07782_b200 import build as nbuild
+    if nbuild.needs_build():
+        nbuild.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    share = rank_share(ws, rank)
+    sets = c5_sets(share)
+    xy, cst, abase, res = concat_chart_sets(sets)
+    spec = spec_of(sets[0])
+    N, V, A = int(abase[-1]), int(cst[-1]), len(sets)
+    ctx = Context(local, max_charts=25000, max_vertices=1 << 19, max_atlas_side=4096)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = (torch.zeros(64 << 20, dtype=torch.int32, device=dev)
+                if args.flush == "write+read" else None)
+
+    def flush():
+        if args.flush == "none":
+            return
+        flush_buf.zero_()
+        if flush_rd is not None:
+            flush_rd.sum()
+
+    xy_d = torch.from_numpy(xy).to(dev)
+    cst_d = torch.from_numpy(cst).to(dev)
+    out_d = torch.empty(N * 32, dtype=torch.uint8, device=dev)
+    os.environ["TABI_TIMING"] = "0"
+
+    def step_dev():
+        return ctx.pack_many(xy_d, cst_d, abase, spec, res_xy=res, out=out_d,
+                             stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        r = step_dev()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+    binfos = []
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush()
+            ev[i][0].record(stream)
+            st_b, _, infos, ast, bi = step_dev()
+            ev[i][1].record(stream)
+            launches += bi.gpu_launches
+            binfos.append(bi)
+    torch.cuda.synchronize()
+    barrier(ws)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = allmax(sum(step_ms), ws)
+    ms_per_step = total_ms / args.steps
+    value = C5_ATLASES * args.steps / (total_ms / 1000.0)
+    ok = int(sum(1 for s in ast if s == 0))
+    stretch_b = float(np.mean([i.l2_stretch for i in infos if i.scale_index > 0]))
+
+    # ---- e2e: host pointers from pinned memory (H2D + D2H inside the timed region)
+    xy_p = torch.from_numpy(xy).pin_memory()
+    cst_p = torch.from_numpy(cst).pin_memory()
+    out_p = torch.empty(N * 32, dtype=torch.uint8).pin_memory()
+    xy_h, cst_h = xy_p.numpy(), cst_p.numpy()
+    from paper_2602_07782_b200 import PLACEMENT_DTYPE
+    out_h = out_p.numpy().view(PLACEMENT_DTYPE)
+
+    def step_host():
+        return ctx.pack_many(xy_h, cst_h, abase, spec, res_xy=res, out=out_h,
+                             stream=stream.cuda_stream)
+
+    for _ in range(2):
+        step_host()
+    torch.cuda.synchronize()
+    e2e_steps = max(5, args.steps // 2)
+    e2e_ev, wall = [], []
+    barrier(ws)
+    for i in range(e2e_steps):
+        flush()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(stream)
+        step_host()
+        b.record(stream)
+        wall.append(time.perf_counter() - t0)
+        e2e_ev.append((a, b))
+    torch.cuda.synchronize()
+    e2e_ms = allmax(sum(x.elapsed_time(y) for x, y in e2e_ev), ws) / e2e_steps
+    wall_s = allmax(sum(wall), ws) / e2e_steps
+    assert out_h.tobytes() == out_d.cpu().numpy().tobytes(), "host / device batch results differ"
+    h2d = int(xy.nbytes + cst.nbytes + 4 * (4 * A + 1))
+    d2h = int(N * 32 + A * (8 + 600))
+
+    # ---- per-stage times of the batch (TABI_TIMING events, separate untimed steps)
+    os.environ["TABI_TIMING"] = "1"
+    stage = np.zeros(4)
+    for _ in range(3):
+        flush()
+        stage += np.array(step_dev()[4].stage_ms[:4])
+    stage /= 3
+    os.environ["TABI_TIMING"] = "0"
+    bi = binfos[-1]
+    pk, pk_kind = peaks()
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # G int32 lane-ops/s
+    work = bi.work_pack + bi.work_profile
+    stage_names = ["copies+reset", "proxies", "sort+slots", "pack_kernel (raster+pairs+Alg.4)"]
+    kdom = int(np.argmax(stage))
+    roof = {"kernel": ["reset", "proxy_kernel", "many_sort_prep_kernel", "many_kernel"][kdom],
+            "bound": "alu", "unit": "Gop/s", "peak": alu_peak,
+            "peak_kind": f"derived from {pk_kind} sm_max_mhz (148 SMs x 128 int32 lanes)",
+            "stage_ms": {stage_names[i]: round(float(stage[i]), 4) for i in range(4)},
+            "work_unit": "frontline column visits + footprint entries (batch kernel)",
+            "work_per_launch": work, "traffic": None}
+    if kdom == 3 and stage[3] > 0:
+        roof["achieved"] = work / (stage[3] * 1e-3) / 1e9
+        roof["frac"] = roof["achieved"] / alu_peak
+    else:
+        roof["achieved"] = roof["frac"] = None
+    tr = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr):
+        roof["traffic"] = json.load(open(tr)).get("C5", {}).get("many_kernel")
+    hbm_bytes = h2d + d2h
+    line = {"metric": METRIC, "value": value, "unit": "atlases/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (chartgen SplitMix64; configs[4] atlas i: seed 1000+i)",
+            "config": {"workload": (f"C5 configs[4]: batch of {C5_ATLASES} tss atlases (200-2000 "
+                                    "charts each, rho~U[0.3,1.5]) into 2048x2048, k=10, M=64, g=1, "
+                                    f"LPT-sharded over {ws} GPU(s); one tabi_pack_many per rank "
+                                    "per step"),
+                       "latency_workload": (f"C3 configs[2]: 1572 tss charts into 4096x4096, "
+                                            f"rho={C3_HEADLINE_RHO} (stretch ~1.39, the paper's "
+                                            "2K TSS regime 1.38, P:796), k=10, t_opt=0, seeds 0-7"),
+                       "l2": {"write": "flushed between steps (256 MB write, untimed)",
+                              "write+read": "flushed between steps (256 MB write + 256 MB read)",
+                              "none": "NOT flushed (warm-cache diagnostic, not a bench value)"
+                              }[args.flush],
+                       "parallelism": f"{C5_ATLASES} atlases per step sharded over {ws} GPU(s)"},
+            "batch": {"atlases": C5_ATLASES, "atlases_this_rank": A, "charts_this_rank": N,
+                      "device_atlases_per_s": value,
+                      "e2e_atlases_per_s": C5_ATLASES * 1000.0 / e2e_ms,
+                      "wall_atlases_per_s": C5_ATLASES / wall_s,
+                      "ok_atlases_this_rank": ok, "l2_stretch_mean": stretch_b,
+                      "candidates_evaluated": bi.candidates_evaluated,
+                      "solo_atlases": bi.solo_atlases, "library_device_ms": bi.device_ms,
+                      "per_gpu_busy_ms": sum(step_ms) / args.steps},
+            "roofline": roof,
+            "hbm_compulsory": {"bytes_per_step": hbm_bytes,
+                               "gbs": hbm_bytes / (ms_per_step * 1e-3) / 1e9,
+                               "frac_of_measured": hbm_bytes / (ms_per_step * 1e-3) / 1e9 /
+                               pk.get("hbm_gbs", 6650.0)},
+            "e2e": {"value": C5_ATLASES * 1000.0 / e2e_ms, "unit": "atlases/s",
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "paper_context": PAPER_CONTEXT}
+    line["p50_ms"] = line["p99_ms"] = line["l2_stretch"] = None
+    if ws == 1 and not args.quick:
+        c3 = {}
+        for rho in (C3_HEADLINE_RHO, 0.5, 2.0):
+            c3[f"rho_{rho}"] = c3_latency(ctx, stream, dev, rho, range(8), 25, flush)
+        h = c3[f"rho_{C3_HEADLINE_RHO}"]
+        line["p50_ms"], line["p99_ms"], line["l2_stretch"] = h["p50_ms"], h["p99_ms"], h["l2_stretch_mean"]
+        line["c3"] = c3
+        line["interactive_budget_ms"] = 15.0
+        line["knob_sweep"] = knob_sweep(ctx, stream, dev, flush)
+        # per-row cost of the headline pack vs the building-block floor
+        cs, _ = workload("C3", 0, C3_HEADLINE_RHO)
+        os.environ["TABI_TIMING"] = "1"
+        xy1 = torch.from_numpy(cs.xy).to(dev)
+        st1 = torch.from_numpy(cs.start).to(dev)
+        fused = []
+        for _ in range(5):
+            flush()
+            inf1 = ctx.pack(xy1, st1, spec_of(cs), stream=stream.cuda_stream)[2]
+            fused.append(inf1.stage_ms[5])
+        os.environ["TABI_TIMING"] = "0"
+        fl = latency_floor(local)
+        phases = 25  # barrier-separated steps per row
+        line["latency_floor"] = dict(fl, phases_per_row=phases,
+                                     row_floor_us=phases * fl["barrier_smem_exchange_ns"] / 2 / 1e3,
+                                     fused_kernel_ms=statistics.median(fused), rows=inf1.rows,
+                                     row_us_measured=statistics.median(fused) * 1e3 / max(1, inf1.rows))
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, rate1, cores, n_done, wall_o = oracle_batch_rate(sets[::8])
+        line["cpu_baseline"] = {"value": rate, "unit": "atlases/s", "cores": cores,
+                                "kind": "oracle", "one_core_atlases_per_s": rate1,
+                                "cpu_model": cpu_model(),
+                                "sample": (f"{n_done} whole C5 atlases (every 8th of the batch, "
+                                           f"rotating) in {wall_o:.1f} s, one oracle process per "
+                                           f"core ({cores})")}
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_single(args, ws, rank, local):
+    """Round-1 single-pack bench (--workload C3 | C2 | C4 | C4P | C4X): one atlas per
+    rank per step (weak scaling); kept for diagnostics and per-workload profiles."""
     import numpy as np
     import torch
 
@@ -251,182 +592,65 @@ def main():
         nbuild.build()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    sets, desc, units_per_step, scaling = rank_atlases(args.workload, rank, ws, args.rho)
-    specs = [spec_of(cs, **WORKLOAD_SPEC.get(args.workload, {})) for cs in sets]
-    ctx = Context(local, max_charts=max(max(cs.n_charts for cs in sets), 1024),
-                  max_vertices=max(cs.n_vertices for cs in sets) + 16,
-                  max_atlas_side=max(max(cs.atlas_w, cs.atlas_h) for cs in sets))
-    # one dedicated stream for everything timed: the L2 flush, the CUDA events and
-    # the packs (torch's default stream is the legacy NULL stream, handle 0,
-    # which the C ABI would read as "the context's own stream")
+    cs, desc = workload(args.workload, rank, args.rho)
+    spec = spec_of(cs, **WORKLOAD_SPEC.get(args.workload, {}))
+    ctx = Context(local, max_charts=max(cs.n_charts, 1024), max_vertices=cs.n_vertices + 16,
+                  max_atlas_side=max(cs.atlas_w, cs.atlas_h))
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
-    dev_in = [(torch.from_numpy(cs.xy).to(dev), torch.from_numpy(cs.start).to(dev),
-               torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)) for cs in sets]
+    xy_d, st_d = torch.from_numpy(cs.xy).to(dev), torch.from_numpy(cs.start).to(dev)
+    out_d = torch.empty(cs.n_charts * 32, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    flush_rd = torch.zeros(64 << 20, dtype=torch.int32, device=dev) if args.flush == "write+read" \
-        else None
-
-    def do_flush():
-        if args.flush == "none":
-            return
-        flush.zero_()
-        if flush_rd is not None:
-            flush_rd.sum()
-
-    def step_dev():
-        infos = []
-        for (xy_d, start_d, out_d), spec in zip(dev_in, specs):
-            infos.append(ctx.pack(xy_d, start_d, spec, out=out_d, stream=stream.cuda_stream)[2])
-        return infos
-
     os.environ["TABI_TIMING"] = "0"
     for _ in range(args.warmup):
-        step_dev()
+        ctx.pack(xy_d, st_d, spec, out=out_d, stream=stream.cuda_stream)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    launches = 0
-    work_pack = work_prof = 0
-    infos = None
-    span_ms = []  # per step: the library's own device span (tabi_info.device_ms)
+    span, launches, info = [], 0, None
     barrier(ws)
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            do_flush()
-            ev[i][0].record(stream)
-            infos = step_dev()
-            ev[i][1].record(stream)
-            span_ms.append(sum(info.device_ms for info in infos))
-            for info in infos:
-                launches += info.gpu_launches
-                work_pack += info.work_pack
-                work_prof += info.work_profile
+            if args.flush != "none":
+                flush.zero_()
+            info = ctx.pack(xy_d, st_d, spec, out=out_d, stream=stream.cuda_stream)[2]
+            span.append(info.device_ms)
+            launches += info.gpu_launches
     torch.cuda.synchronize()
-    barrier(ws)
-    # per-stage device times (TABI_TIMING events inside tabi_pack) from separate,
-    # untimed steps: the events and their host syncs stay out of the timed loop
+    total = allmax(sum(span), ws)
     os.environ["TABI_TIMING"] = "1"
     stage = np.zeros(8)
-    stage_steps = min(args.steps, 20)
-    for i in range(stage_steps):
-        do_flush()
-        for info in step_dev():
-            stage += np.array(info.stage_ms[:8])
-    torch.cuda.synchronize()
+    for _ in range(min(args.steps, 10)):
+        flush.zero_()
+        stage += np.array(ctx.pack(xy_d, st_d, spec, out=out_d, stream=stream.cuda_stream)[2].stage_ms[:8])
+    stage /= min(args.steps, 10)
     os.environ["TABI_TIMING"] = "0"
-    # device time per step = the pack's own span on the timed stream (CUDA events
-    # recorded by tabi_pack around its enqueued work, tabi_info.device_ms); the
-    # outer events bracketing each step additionally see the host returning from
-    # the synchronous call (reported as stream_ms_per_step)
-    outer_ms = [a.elapsed_time(b) for a, b in ev]
-    step_ms = span_ms
-    total_ms = allmax(sum(step_ms), ws)
-    outer_total = allmax(sum(outer_ms), ws)
-    ms_per_step = total_ms / args.steps
-    value = units_per_step * args.steps / (total_ms / 1000.0)
-    p50 = statistics.median(step_ms)
-    p99 = float(np.percentile(step_ms, 99))
-
-    # ---- e2e through the public host-pointer call -------------------------
-    e2e_steps = max(10, args.steps // 4) if len(sets) == 1 else 3
-    for cs, spec in zip(sets, specs):
-        ctx.pack(cs.xy, cs.start, spec, stream=stream.cuda_stream)
-    e2e_ev = []
-    torch.cuda.synchronize()
-    barrier(ws)
-    for i in range(e2e_steps):
-        do_flush()
+    e2e = []
+    for _ in range(10):
+        flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for cs, spec in zip(sets, specs):
-            ctx.pack(cs.xy, cs.start, spec, stream=stream.cuda_stream)
+        ctx.pack(cs.xy, cs.start, spec, stream=stream.cuda_stream)
         b.record(stream)
-        e2e_ev.append((a, b))
+        e2e.append((a, b))
     torch.cuda.synchronize()
-    e2e_ms = allmax(sum(a.elapsed_time(b) for a, b in e2e_ev), ws) / e2e_steps
-    h2d = int(sum(cs.xy.nbytes + cs.start.nbytes for cs in sets))
-    d2h = int(sum(cs.n_charts * 32 + 64 + 56 * cs.scale_count for cs in sets))
-
-    # ---- roofline of the dominant kernel -------------------------------
-    npk = args.steps * len(sets)
-    stage_avg = stage / (stage_steps * len(sets))
+    e2e_ms = allmax(sum(x.elapsed_time(y) for x, y in e2e), ws) / 10
     names = ["h2d", "proxies", "sort", "profiles", "offsets_locks", "fold_push", "select", "d2h"]
-    k_dom = int(np.argmax(stage_avg[1:7])) + 1
-    pk, pk_kind = peaks()
-    sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    # int32 lane-op issue peak: 148 SMs x 4 SMSPs x 32 lanes x clock
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # G lane-ops/s
-    fused = bool(infos[0].fused)
-    if fused and k_dom == 5:
-        # the fused wave kernel rasterizes footprints (K3), computes pair offsets
-        # (K3b) and runs the row loop (K4) in one launch: its work is both
-        work = (work_pack + work_prof) / npk
-        names[5] = "fused_wave (K3+K3b+K4)"
-    else:
-        work = {5: work_pack / npk, 3: work_prof / npk}.get(k_dom)
-    roof = {"kernel": names[k_dom], "bound": "alu", "unit": "Gop/s",
-            "peak": alu_peak, "peak_kind": f"derived from {pk_kind} sm_max_mhz (148x128 int32 lanes)",
-            "stage_ms": {names[i]: round(float(stage_avg[i]), 5) for i in range(8)},
-            "traffic": None}
-    if work is not None and stage_avg[k_dom] > 0:
-        ach = work / (stage_avg[k_dom] * 1e-3) / 1e9
-        roof.update({"achieved": ach, "frac": ach / alu_peak,
-                     "work_per_launch": work,
-                     "work_unit": ("frontline column visits + footprint entries"
-                                   if fused and k_dom == 5 else
-                                   "frontline column visits" if k_dom == 5 else
-                                   "footprint entries")})
-    else:
-        roof.update({"achieved": None, "frac": None})
-    tr = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr):
-        roof["traffic"] = json.load(open(tr)).get(args.workload, {}).get(names[k_dom])
-    # HBM context: compulsory bytes per pack
-    hbm_bytes = sum(cs.xy.nbytes + cs.start.nbytes + 32 * cs.n_charts for cs in sets) / len(sets)
-    info = infos[0]
-    line = {"metric": METRIC, "value": value, "unit": "atlases/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (chartgen SplitMix64, seed = rank)",
-            "config": {"workload": desc,
-                       "l2": {"write": "flushed between steps (256 MB write, untimed)",
-                              "write+read": "flushed between steps (256 MB write + 256 MB read, "
-                                            "untimed)",
-                              "none": "NOT flushed (warm-cache diagnostic, not a bench value)"
-                              }[args.flush],
-                       "parallelism": (f"{ws} independent packs per step (one per GPU)"
-                                       if scaling == "weak" else
-                                       f"512 atlases per step sharded over {ws} GPU(s)")},
-            "p50_ms": p50, "p99_ms": p99,
-            "stream_ms_per_step": outer_total / args.steps,
-            "l2_stretch": (info.l2_stretch if len(sets) == 1 else
-                           float(np.mean([i.l2_stretch for i in infos]))),
-            "scale_index": info.scale_index, "rows": info.rows,
-            "interactive_budget_ms": 15.0,
-            "hbm_compulsory": {"bytes_per_pack": int(hbm_bytes),
-                               "gbs": hbm_bytes * len(sets) / (p50 * 1e-3) / 1e9,
-                               "frac_of_measured": hbm_bytes * len(sets) / (p50 * 1e-3) / 1e9 /
-                               pk.get("hbm_gbs", 6650.0)},
-            "roofline": roof,
-            "e2e": {"value": units_per_step * 1000.0 / e2e_ms, "unit": "atlases/s",
-                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "paper_context": PAPER_CONTEXT}
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, n, dt, m = cpu_oracle_rate(sets[0], **WORKLOAD_SPEC.get(args.workload, {}))
-        line["cpu_baseline"] = {"value": rate, "unit": "atlases/s", "cores": 1, "kind": "oracle",
-                                "sample": f"{n} full oracle packs of the first chart set "
-                                          f"(all candidates) in {dt:.1f} s, 1 thread",
-                                "host_cores": os.cpu_count()}
+    span.sort()
+    line = {"metric": METRIC, "value": ws * args.steps / (total / 1000.0), "unit": "atlases/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic (chartgen, seed = rank)",
+            "config": {"workload": desc, "parallelism": f"{ws} independent packs per step"},
+            "p50_ms": statistics.median(span), "p99_ms": span[int(0.99 * (len(span) - 1))],
+            "l2_stretch": info.l2_stretch, "scale_index": info.scale_index, "rows": info.rows,
+            "prefix_rows": info.prefix_rows,
+            "stage_ms": {names[i]: round(float(stage[i]), 5) for i in range(8)},
+            "e2e": {"value": ws * 1000.0 / e2e_ms, "unit": "atlases/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(cs.xy.nbytes + cs.start.nbytes),
+                    "d2h_bytes_per_step": int(cs.n_charts * 32)},
+            "gpu_launches": launches, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line))
     ctx.close()
-    if ws > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

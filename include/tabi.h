@@ -178,12 +178,16 @@ const char* tabi_last_error(tabi_ctx* ctx);   /* last CUDA error text, or "" */
  * Returns TABI_OK if every atlas is OK or NO_FIT, else the first other error
  * (per-atlas detail in atlas_status). */
 typedef struct {
-  float device_ms;                /* batch device span on the stream (CUDA events) */
+  float device_ms;                /* batch device span on the stream (CUDA events): first
+                                     enqueued copy .. last result copy */
+  float stage_ms[4];              /* TABI_TIMING=1 only (else 0): [0] input copies + reset,
+                                     [1] proxies, [2] sort + slot layout, [3] pack kernel */
   int32_t gpu_launches;           /* kernels launched (batch + solo packs) */
   int32_t candidates_evaluated;   /* (atlas, candidate) items run by the batch kernel */
   int32_t batched_atlases;        /* atlases packed by the device batch */
   int32_t solo_atlases;           /* atlases packed by tabi_pack afterwards */
-  int32_t reserved[3];
+  int64_t work_pack;              /* batch kernel: frontline column visits (as tabi_info) */
+  int64_t work_profile;           /* batch kernel: footprint entries rasterized (Wd + Hd) */
 } tabi_batch_info;
 
 tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t n_atlases, const float* xy,
@@ -298,6 +302,13 @@ tabi_status tabi_debug_trace(tabi_ctx* ctx, int64_t* out16);
  * ns from the kernel start: tile 0 footprints done, tile 0 published, packer
  * 0's first fold unblocked, packer 0's first row done; [12..15] 0. */
 tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out16);
+/* Latency floor of the packer's per-row building blocks: one
+ * 512-thread CTA times dependent chains on `cuda_device`; out8 receives ns per
+ * operation: [0] barrier, [1] barrier + shared-memory exchange (two barriers),
+ * [2] block max-reduce (two barriers), [3] shared atomicMax + barrier,
+ * [4] dependent L2 load, [5] the SM clock in MHz it measured.  Diagnostic;
+ * independent of any context. */
+tabi_status tabi_debug_latency_floor(int cuda_device, double* out8);
 
 #ifdef __cplusplus
 }

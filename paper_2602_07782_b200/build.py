@@ -13,7 +13,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtabi.so")
 SOURCES = ["tabi_api.cu", "k_proxy.cu", "k_sort.cu", "k_profile.cu", "k_pack.cu", "k_tail.cu",
-           "k_validate.cu"]
+           "k_validate.cu",
+           "k_floor.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]

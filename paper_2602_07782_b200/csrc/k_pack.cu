@@ -1536,6 +1536,13 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
             if (big[ci])
               k3::big_chart(P, perm, pp, colofs, rowofs, dcol, drow, 0, s0 + ci, sc, CW[wid],
                             wtab + wid * 4 * k, lane);
+          if (wid == 0) {  // work accounting: footprint entries (Wd + Hd) of the tile
+            unsigned long long pe = 0;
+            for (int ci = lane; ci < nt; ci += 32)
+              pe += (unsigned long long)(CH[ci].ws + CH[ci].hs + 4 * g);
+            for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
+            if (lane == 0) atomicAdd(&st->work_prof, pe);
+          }
           __syncthreads();
         }
       }

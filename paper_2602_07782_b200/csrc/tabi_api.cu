@@ -83,6 +83,7 @@ struct ManyWs {
   tabi_placement* h_out = nullptr;
   int64_t h_out_cap = 0;
   cudaEvent_t span[2] = {nullptr, nullptr};
+  cudaEvent_t stage[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // TABI_TIMING
   void release() {
     void* ds[] = {d_xy, d_start, qx, qy, P.w, P.h, P.area2, P.xmin, P.ymin, P.pose, P.prerot, P.sl,
                   P.obb_j, P.obb, perm, colofs, rowofs, hsorted, tstart, tix, d_out, d_small, sts,
@@ -94,6 +95,8 @@ struct ManyWs {
     for (void* p : hs)
       if (p) cudaFreeHost(p);
     for (auto& e : span)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : stage)
       if (e) cudaEventDestroy(e);
   }
 };
@@ -770,6 +773,7 @@ static tabi_status many_ensure(tabi_ctx* ctx, int64_t N, int64_t V, int32_t A, i
   if (!w.span[0]) {
     CK(cudaEventCreate(&w.span[0]));
     CK(cudaEventCreate(&w.span[1]));
+    for (auto& e : w.stage) CK(cudaEventCreate(&e));
   }
   const int32_t G = many_grid(ctx->device);
   if (G < 1) {
@@ -907,7 +911,11 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
   const int32_t E = (int32_t)order.size();
   int launches = 0;
   float dev_ms = 0.f;
+  float stage_ms[4] = {0.f, 0.f, 0.f, 0.f};
   int32_t evaluated = 0;
+  int64_t work_pack = 0, work_prof = 0;
+  const char* tenv = getenv("TABI_TIMING");
+  const bool timing = tenv && tenv[0] == '1';
   if (E > 0) {
     int64_t V = 0;
     if (on_device) {
@@ -976,10 +984,13 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     pp.col_cap = w.col_cap;
     pp.row_cap = w.row_cap;
     launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, s);
+    if (timing) CK(cudaEventRecord(w.stage[0], s));
     launch_proxies(d_xy, d_start, (int32_t)N, 1.0f, 1.0f, pp.k, pp.flags, w.qx, w.qy, w.cap_V, w.P,
                    w.sts, s, AtlasMap{d_abase, A, d_res});
+    if (timing) CK(cudaEventRecord(w.stage[1], s));
     launch_many_sort_prep(w.P, d_abase, A, w.perm, pp, w.colofs, w.rowofs, w.hsorted, w.tstart,
                           w.tix, w.sts, s);
+    if (timing) CK(cudaEventRecord(w.stage[2], s));
     ManyArgs ma;
     ma.P = w.P;
     ma.abase = d_abase;
@@ -1008,6 +1019,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     ma.nmax = w.nmax;
     ma.pair_cap = w.pair_cap;
     CK(launch_many(w.G, pp, ma, s));
+    if (timing) CK(cudaEventRecord(w.stage[3], s));
     launches = 4;
     if (!on_device) {
       tabi_placement* dst = out;
@@ -1027,12 +1039,18 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     CK(cudaEventRecord(w.span[1], s));
     CK(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&dev_ms, w.span[0], w.span[1]);
+    if (timing) {
+      cudaEventElapsedTime(&stage_ms[0], w.span[0], w.stage[0]);
+      for (int i = 1; i < 4; i++) cudaEventElapsedTime(&stage_ms[i], w.stage[i - 1], w.stage[i]);
+    }
     const bool staged = !on_device && !host_pinned(out);
     for (int32_t i = 0; i < E; i++) {
       const int32_t a = order[i];
       const Status& st = w.h_sts[a];
       const AtlasRes& R = w.h_res[a];
       evaluated += R.evaluated;
+      work_pack += (int64_t)st.work_pack;
+      work_prof += (int64_t)st.work_prof;
       if (st.bad_chart != INT32_MAX) {
         stv[a] = TABI_EINVAL;
         inf[a].bad_chart = st.bad_chart;
@@ -1095,6 +1113,9 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     binfo->candidates_evaluated = evaluated;
     binfo->solo_atlases = (int32_t)solo.size();
     binfo->batched_atlases = E;
+    for (int i = 0; i < 4; i++) binfo->stage_ms[i] = stage_ms[i];
+    binfo->work_pack = work_pack;
+    binfo->work_profile = work_prof;
   }
   return ret;
 }
@@ -1347,6 +1368,11 @@ extern "C" tabi_status tabi_debug_trace_raster(tabi_ctx* ctx, int64_t* out16) {
   for (int i = 0; i < 8; i++)
     out16[8 + i] = st.tfirst[i] > st.tr[0] && st.tfirst[i] != 0 ? (int64_t)(st.tfirst[i] - st.tr[0]) : 0;
   return TABI_OK;
+}
+
+extern "C" tabi_status tabi_debug_latency_floor(int cuda_device, double* out8) {
+  if (!out8) return TABI_EINVAL;
+  return latency_floor(cuda_device, out8) == 0 ? TABI_OK : TABI_ECUDA;
 }
 
 extern "C" tabi_status tabi_debug_offsets(tabi_ctx* ctx, int32_t m, int32_t* off, uint8_t* lockbits) {

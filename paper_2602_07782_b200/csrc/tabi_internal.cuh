@@ -495,6 +495,8 @@ void launch_many_sort_prep(const Proxies& P, const int32_t* abase, int32_t A, in
                           const PackParams& pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
                           int32_t* tstart, int32_t* tix, Status* sts, cudaStream_t s);
 int many_grid(int device);  // persistent CTAs (one per SM)
+// k_floor.cu: packer building-block latencies in ns (tabi_debug_latency_floor)
+int latency_floor(int device, double* out8);
 cudaError_t launch_many(int grid, const PackParams& pp, const ManyArgs& a, cudaStream_t s);
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,

@@ -66,9 +66,9 @@ class Validation(C.Structure):
 
 
 class BatchInfo(C.Structure):
-    _fields_ = [("device_ms", C.c_float), ("gpu_launches", C.c_int32),
+    _fields_ = [("device_ms", C.c_float), ("stage_ms", C.c_float * 4), ("gpu_launches", C.c_int32),
                 ("candidates_evaluated", C.c_int32), ("batched_atlases", C.c_int32),
-                ("solo_atlases", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("solo_atlases", C.c_int32), ("work_pack", C.c_int64), ("work_profile", C.c_int64)]
 
 
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
@@ -116,6 +116,7 @@ def lib():
         L.tabi_debug_offsets.argtypes = [P, i32, P, P]
         L.tabi_debug_trace.argtypes = [P, P]
         L.tabi_debug_trace_raster.argtypes = [P, P]
+        L.tabi_debug_latency_floor.argtypes = [C.c_int, P]
         L.tabi_shard_plan.argtypes = [i32, P, i32, P]
         L.tabi_pack_batch.argtypes = [P, i32, i32, P, P, P, P, P, P, P]
         L.tabi_pack_many.argtypes = [P, i32, P, P, P, P, C.POINTER(Spec), P, P, P,
@@ -130,7 +131,17 @@ EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str"
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
            "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace",
            "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch", "tabi_pack_many",
-           "tabi_validate"]
+           "tabi_validate", "tabi_debug_latency_floor"]
+
+
+def latency_floor(device: int = 0) -> dict:
+    """ns per packer building block (tabi_debug_latency_floor)."""
+    out = np.zeros(8, dtype=np.float64)
+    st = lib().tabi_debug_latency_floor(device, _ptr(out))
+    if st != OK:
+        raise TabiError(st, "tabi_debug_latency_floor")
+    return dict(barrier_ns=out[0], barrier_smem_exchange_ns=out[1], block_max_ns=out[2],
+                smem_atomic_barrier_ns=out[3], l2_dependent_load_ns=out[4], sm_mhz=out[5])
 
 
 def concat_chart_sets(chart_sets):
