@@ -188,6 +188,8 @@ typedef struct {
   int32_t solo_atlases;           /* atlases packed by tabi_pack afterwards */
   int64_t work_pack;              /* batch kernel: frontline column visits (as tabi_info) */
   int64_t work_profile;           /* batch kernel: footprint entries rasterized (Wd + Hd) */
+  int64_t cycles[3];              /* batch kernel: SM cycles summed over its items, in
+                                     footprint rasterization, pair offsets + locks, Alg. 4 */
 } tabi_batch_info;
 
 tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t n_atlases, const float* xy,

@@ -8,6 +8,7 @@ namespace tabi {
 namespace k3 {
 
 constexpr int kRaw = 8192;   // raw cells per chunk (32 KB)
+constexpr int kDilMax = 2;   // gutters up to this use the fused raster + dilation pass
 // Per-(chart, candidate) constants.  OBB index q = axis * 2 + (0 low, 1 high);
 // lines lin[axis * 4 + kind]: kind 0 low-bound line right of the crossing
 // (at the cell's low edge), 1 low-bound line left of it (high edge, non-last
@@ -221,6 +222,149 @@ __device__ __forceinline__ void raw_run(const ChartK3& H, const int32_t* tab, in
   }
 }
 
+// raw_cell as an iterator over consecutive cells i0, i0 + 1, ... of one axis
+// (same values as raw_run).  Of the four OBB line progressions only the two
+// that can decide a cell are advanced: the low (high) bound uses line 1 (3)
+// up to its crossing index iA and line 0 (2) past it, so each bound carries
+// one progression and restarts it once where the run passes its crossing.
+struct RawIter {
+  const int32_t* t;
+  const LinDiv* lin;
+  int64_t nx, rl, rh;                // slice-index progressions: remainders mod nx
+  int64_t dr;                        // SCk - dq * nx (SCk = SC k: 2^28 k in tail mode)
+  int32_t dq, ql, qh, k, cnt, ext, i;
+  bool obb, pL, pH;                  // past the low / high crossing
+  // OBB bound state, clamped to +-2^30 where only compared with cell indices /
+  // texel values (both far smaller)
+  int32_t iA0, iA1, iB0, iB1, st0, st1, la0, la1, lb0, lb1;
+  int32_t vL, vH, sqL, sqH;          // the active line progressions (values in texels)
+  int64_t rL, rH, srL, srH, DL, DH;
+  __device__ __forceinline__ static int32_t clamp30(int64_t v) {
+    return (int32_t)(v < -(1ll << 30) ? -(1ll << 30) : v > (1ll << 30) ? (1ll << 30) : v);
+  }
+  __device__ __forceinline__ void load_low(int32_t at) {
+    const LinDiv& L = lin[pL ? 0 : 1];
+    int64_t v;
+    lindiv_start(L, at, v, rL);
+    vL = clamp30(v);
+    sqL = (int32_t)L.qB; srL = L.rB; DL = L.D;
+  }
+  __device__ __forceinline__ void load_high(int32_t at) {
+    const LinDiv& L = lin[pH ? 2 : 3];
+    int64_t v;
+    lindiv_start(L, at, v, rH);
+    vH = clamp30(v);
+    sqH = (int32_t)L.qB; srH = L.rB; DH = L.D;
+  }
+  __device__ __forceinline__ void init(const ChartK3& H, const int32_t* tab, int k_, int ax,
+                                       int32_t i0, int64_t SC) {
+    k = k_;
+    nx = ax ? H.nh : H.nw;
+    const double rnx = ax ? H.rnh : H.rnw;
+    const int64_t SCk = SC * k;
+    const int64_t q = fdiv_r64(SCk, nx, rnx);
+    dq = (int32_t)q;
+    dr = SCk - q * nx;
+    int64_t a = (int64_t)i0 * SCk;
+    int64_t f = fdiv_r64(a, nx, rnx);
+    ql = (int32_t)f;
+    rl = a - f * nx;
+    a += SCk - 1;
+    f = fdiv_r64(a, nx, rnx);
+    qh = (int32_t)f;
+    rh = a - f * nx;
+    t = tab + ax * 2 * k;
+    cnt = ax ? H.hs : H.ws;
+    ext = ax ? H.ws : H.hs;
+    i = i0;
+    obb = H.j8 != 0;
+    if (obb) {
+      const ObbC& O = H.O;
+      const int q0 = 2 * ax, q1 = 2 * ax + 1;
+      lin = O.lin + 4 * ax;
+      iA0 = clamp30(O.iA[q0]); iA1 = clamp30(O.iA[q1]);
+      iB0 = clamp30(O.iB[q0]); iB1 = clamp30(O.iB[q1]);
+      st0 = clamp30(O.star[q0]); st1 = clamp30(O.star[q1]);
+      la0 = clamp30(O.last[q0]); la1 = clamp30(O.last[q1]);
+      lb0 = O.lastB[q0]; lb1 = O.lastB[q1];
+      pL = i0 > iA0;
+      pH = i0 > iA1;
+      load_low(i0);
+      load_high(i0);
+    }
+  }
+  // value of cell i (packed lo | hi << 16), then move to i + 1
+  __device__ __forceinline__ uint32_t next() {
+    const int32_t jl = ql < 0 ? 0 : ql, jh = qh > k - 1 ? k - 1 : qh;
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (int32_t j = jl; j <= jh; j++) {
+      lo = min(lo, t[2 * j]);
+      hi = max(hi, t[2 * j + 1]);
+    }
+    int32_t L = max(0, lo), Hh = min(hi, ext);
+    if (obb) {
+      const bool last = i == cnt - 1;
+      int32_t w;
+      if (pL) w = vL;
+      else if (last ? lb0 != 0 : i >= iB0) w = st0;
+      else w = last ? la0 : vL;
+      L = max(L, w);
+      if (pH) w = -vH;
+      else if (last ? lb1 != 0 : i >= iB1) w = st1;
+      else w = last ? la1 : -vH;
+      Hh = min(Hh, w);
+      // advance to i + 1 (restart a bound's progression where i + 1 passes its crossing)
+      vL += sqL; rL += srL;
+      if (rL >= DL) { rL -= DL; vL++; }
+      vH += sqH; rH += srH;
+      if (rH >= DH) { rH -= DH; vH++; }
+      if (!pL && i + 1 > iA0) { pL = true; load_low(i + 1); }
+      if (!pH && i + 1 > iA1) { pH = true; load_high(i + 1); }
+    }
+    ql += dq; rl += dr;
+    if (rl >= nx) { rl -= nx; ql++; }
+    qh += dq; rh += dr;
+    if (rh >= nx) { rh -= nx; qh++; }
+    i++;
+    return (uint32_t)L | ((uint32_t)Hh << 16);
+  }
+};
+
+// Raster and dilation fused (D11 + D13) for gutters g <= GMAX: the dilated
+// outputs o0 .. o0 + len - 1 of one axis (Dlo(o) = min Lo(q), Dhi(o) = max
+// Hi(q) + 2g over raw cells q in [o - 2g, o] within [0, n0)), written to
+// dst[0 .. len), the raw cells kept in a (2g + 1)-entry register window
+// instead of a shared-memory buffer.  A window entry packs lo | (0xffff - hi)
+// << 16, so one per-halfword minimum (vminu2) takes both bounds.
+template <int GMAX>
+__device__ __forceinline__ void dil_run(const ChartK3& H, const int32_t* tab, int k, int ax,
+                                        int32_t o0, int32_t len, int64_t SC, int g, uint32_t* dst) {
+  constexpr int WN = 2 * GMAX + 1;
+  const int32_t n0 = ax ? H.hs : H.ws;
+  RawIter it;
+  it.init(H, tab, k, ax, max(0, o0 - 2 * g), SC);
+  uint32_t win[WN];  // raw cells o - 2g .. o at slots WN - 1 - 2g .. WN - 1 (sentinel: empty)
+#pragma unroll
+  for (int u = 0; u < WN; u++) win[u] = 0xffffffffu;
+  for (int32_t q = o0 - 2 * g; q < o0 + len; q++) {
+#pragma unroll
+    for (int u = 0; u + 1 < WN; u++) win[u] = win[u + 1];
+    uint32_t e = 0xffffffffu;
+    if (q >= 0 && q < n0) {
+      const uint32_t v = it.next();
+      e = (v & 0xffffu) | ((0xffffu - (v >> 16)) << 16);
+    }
+    win[WN - 1] = e;
+    if (q >= o0) {
+      uint32_t m = win[WN - 1];
+#pragma unroll
+      for (int u = WN - 2; u >= 0; u--)
+        if (WN - 1 - u <= 2 * g) m = __vminu2(m, win[u]);
+      dst[q - o0] = (m & 0xffffu) | ((0xffffu - (m >> 16) + 2 * g) << 16);
+    }
+  }
+}
+
 // Setup of one chart by 8 cooperating threads r = 0..7 (rank r).
 __device__ inline void chart_setup(ChartK3& H, int32_t* tab, const Proxies& P, int k, int64_t num,
                             int64_t SC, int r) {
@@ -286,6 +430,9 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   const int64_t num = sc.num, SC = sc.SC;
   const double rSC = rcp_approx((double)SC);
   const int ci = tid >> 3, r = tid & 7;
+  // g <= kDilMax: the fused raster+dilation pass has no raw buffer, so every
+  // fitting chart is rasterized here (no large-chart hand-off)
+  const int raw_cap = g <= kDilMax ? INT32_MAX : RAW;
   if (ci < TC && r == 0) {
     cells[ci] = 0;
     big[ci] = 0;
@@ -310,7 +457,7 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
     hd_all[b] = H.hs + 2 * g;
     const bool fits = H.ws + 2 * g <= pp.Wp && H.hs + 2 * g <= pp.Hp;
     if (!fits) cand_bad[slot] = 1;
-    H.small = fits && (H.ws + H.hs <= RAW);
+    H.small = fits && (H.ws + H.hs <= raw_cap);
     big[ci] = fits && !H.small;
     H.col_o = colofs[s];
     H.row_o = rowofs[s];
@@ -322,6 +469,55 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   setup_done(0);
   uint32_t* colb = dcol + (int64_t)slot * pp.col_cap;
   uint32_t* rowb = drow + (int64_t)slot * pp.row_cap;
+  if (g <= kDilMax) {
+    // fused raster + dilation (dil_run): no raw buffer, every fitting chart of
+    // the tile in one pass over its flattened dilated outputs (Wd + Hd each)
+    if (tid < 32) {
+      const int lane = tid;
+      int e = 0, otot = 0;
+      if (lane == 0) opre[0] = 0;
+      for (; e < nt; e += 32) {
+        const int idx = e + lane;
+        int io = (idx < nt && CH[idx].small) ? CH[idx].ws + CH[idx].hs + 4 * g : 0;
+        // (the pass covers fitting charts only; big[] stays 0 on this path)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int b = __shfl_up_sync(0xffffffffu, io, o);
+          if (lane >= o) io += b;
+        }
+        if (idx < nt) opre[idx + 1] = otot + io;
+        otot += __shfl_sync(0xffffffffu, io, 31);
+      }
+    }
+    sync();
+    setup_done(1);
+    const int32_t nout = opre[nt];
+    const int32_t R = ((nout + TT - 1) / TT) | 1;
+    int32_t e = tid * R;
+    const int32_t e1 = min(nout, e + R);
+    if (e < e1) {
+      int lo = 0, hi = nt - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (opre[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      while (e < e1) {
+        const ChartK3& H = CH[lo];
+        const int32_t y = e - opre[lo];
+        const int32_t Wd = H.ws + 2 * g;
+        const int ax = y >= Wd;
+        const int32_t o = ax ? y - Wd : y;
+        const int32_t len = min(e1 - e, (ax ? H.hs + 2 * g : Wd) - o);
+        dil_run<kDilMax>(H, tabs + lo * 4 * k, k, ax, o, len, SC, g,
+                         (ax ? rowb + H.row_o : colb + H.col_o) + o);
+        e += len;
+        while (lo < nt - 1 && opre[lo + 1] <= e) lo++;
+      }
+    }
+    sync();
+    return;
+  }
   int cb = 0;
   while (cb < nt && cells[cb] == 0) cb++;
   while (cb < nt) {

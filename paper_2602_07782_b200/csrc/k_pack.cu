@@ -84,10 +84,20 @@ struct Smem {
   int32_t pw_b, pw_e, pw_c0, pw_c1;  // fold position window (see pw_fill)
   int32_t w_fold;                    // W.* hold the fold's scalars of the row start
   int32_t prefix_rows, switched;
+  int32_t r_done;                // lazy raster: sorted positions [0, r_done) rasterized
   unsigned long long knee_key;
+  long long sumF, placed;        // lazy + early fail: sum of F, 2 x area of the placed charts
   unsigned long long work;
   alignas(8) uint64_t mbar;
 };
+
+__host__ __device__ __forceinline__ size_t r16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+__device__ __forceinline__ unsigned char* carve(unsigned char*& p, size_t bytes) {
+  unsigned char* r = p;
+  p += r16(bytes);
+  return r;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -193,6 +203,27 @@ struct Ready {
   const int32_t* tix;    // [n] tile of each sorted position
 };
 
+// Batch mode, lazy: the packer rasterizes the footprints (and the adjacent
+// pairs) itself, a few rows ahead of its fold, in the staging buffer it does
+// not use before the last chart is rasterized -- so a candidate that fails
+// never rasterizes the charts it does not reach.  With early_fail, a row end
+// also checks that the charts still to place can fit below the frontline
+// (their polygon area <= the free area sum_x (H' - F[x])): the method's
+// packings are overlap-free, so a candidate failing this test fails anyway
+// (R8).
+struct LazyRaster {
+  Proxies P;             // at the atlas's chart offset
+  const int32_t* perm;   // sorted position -> atlas-local chart
+  int32_t* cbad;         // the candidate's "a chart does not fit" flag
+  int64_t* area;         // [n] 2 x polygon area by sorted position (written here)
+  k3::Scale sc;
+  int32_t ahead;         // positions rasterized beyond the one the fold needs
+  int32_t early_fail;
+  int64_t atot;          // 2 x the atlas's total polygon area (fits int64 for n <= 2048)
+  unsigned long long* cycles;  // [2]: SM cycles in the lazy raster, in its pair offsets
+};
+constexpr int kLzTC = 64;  // charts per lazy raster tile (the whole CTA, 8 threads per chart)
+
 __device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
   int32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -218,7 +249,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             const int32_t* __restrict__ hsorted, const int32_t* cand_bad,
             int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
             Cand* cands, Status* st, int32_t prof_cap, int m, int slot, int jslot, Ready rd,
-            unsigned char* dsm) {
+            unsigned char* dsm, const bool lazy = false, const LazyRaster lzv = LazyRaster{}) {
+  const LazyRaster* lz = lazy ? &lzv : nullptr;
   // m: the candidate scale m/M; slot: its index in the per-candidate arrays
   // (m - 1 for a single pack, the CTA's own buffers in batch mode); jslot: its
   // wave slot (ready flags, early exit)
@@ -329,6 +361,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   const bool adj_only = (pp.flags & TABI_F_ADJACENT_LOCKS_ONLY) != 0;
   const bool no_hc = (pp.flags & TABI_F_NO_HC) != 0;
   const bool no_bal = (pp.flags & TABI_F_NO_BALANCE) != 0;
+  const bool ef = lz && lz->early_fail;  // batch mode: the area test at every row end
   const int32_t cols_total = st->cols_total;
 
   // dynamic shared memory: F | window scalars | staged footprints
@@ -367,7 +400,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   int32_t* qrow = sc + 5 * (int64_t)n;    // prefix row id per sorted position (tail)
   if (prefix_mode) {
     if (pp.T.state[slot] != TAIL_READY) return;
-  } else if (!rd.flags && cand_bad[slot]) {  // a chart exceeds the dilated atlas at this scale
+  } else if (!rd.flags && !lz && cand_bad[slot]) {  // a chart exceeds the dilated atlas at this scale
     if (tid == 0) cands[slot] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
     return;
   }
@@ -390,6 +423,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     S.work = 0ull;
     S.prefix_rows = 0;
     S.switched = 0;
+    S.r_done = 0;
+    S.sumF = 0;
+    S.placed = 0;
     if (prefix_mode) {  // continue from the state saved at the switch
       const Cand cd = cands[slot];
       S.row_start = pp.T.r0[slot];
@@ -467,6 +503,53 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     pk_sync();
   };
 
+  // Lazy raster (batch mode): make sorted positions [0, s + 2 + ahead) have
+  // their footprints, widths / heights and pair offsets; returns the last
+  // position whose pair offset is valid (the fold's scan limit).
+  auto lazy_fill = [&](int s) -> int {
+    const int target = min(n, max(S.r_done, s + 2) + lz->ahead);
+    if (S.r_done < target) {
+      unsigned char* p = (unsigned char*)W.prof;  // free: no row-top prefetch before the end
+      k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kLzTC);
+      int32_t* cells = (int32_t*)carve(p, 4 * kLzTC);
+      int32_t* cpre = (int32_t*)carve(p, 4 * (kLzTC + 1));
+      int32_t* opre = (int32_t*)carve(p, 4 * (kLzTC + 1));
+      int32_t* big = (int32_t*)carve(p, 4 * kLzTC);
+      int32_t* misc = (int32_t*)carve(p, 32);
+      int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kLzTC * 4 * pp.k);
+      int done = S.r_done;
+      long long c0 = tid == 0 ? clock64() : 0, cpair = 0;
+      while (done < target) {  // (uniform)
+        const int s0 = done, nt = min(kLzTC, n - s0);
+        k3::tile_raster<kLzTC, kPT, 1>(lz->P, lz->perm, pp, colofs, rowofs, (uint32_t*)dcol,
+                                       (uint32_t*)drow, (int32_t*)wd_all, (int32_t*)hd_all,
+                                       lz->cbad, slot, s0, lz->sc, CH, cells, cpre, opre, &misc[1],
+                                       big, tabs, nullptr, nt, tid, [] { pk_sync(); });
+        if (tid < nt) lz->area[s0 + tid] = lz->P.area2[lz->perm[s0 + tid]];
+        // pairs (s, s + 1) that end in this tile, and the last chart's zero entry
+        const long long cp = tid == 0 ? clock64() : 0;
+        const int plo = max(0, s0 - 1), phi = s0 + nt == n ? n - 1 : s0 + nt - 2;
+        for (int q = plo + wid; q <= phi; q += kPW)
+          k3::pair_offset(pp, rowofs, (const uint32_t*)drow, wd_all, hd_all, (int32_t*)off_all,
+                          (uint8_t*)lock_all, slot, q, lane);
+        pk_sync();
+        if (tid == 0) cpair += clock64() - cp;
+        done = s0 + nt;
+      }
+      if (tid == 0) {
+        S.r_done = done;
+        const long long dt = clock64() - c0;
+        atomicAdd(lz->cycles, (unsigned long long)(dt - cpair));
+        atomicAdd(lz->cycles + 1, (unsigned long long)cpair);
+      }
+      pk_sync();
+      return done >= n ? n - 1 : done - 2;
+    }
+    const int d0 = S.r_done;
+    pk_sync();  // (every thread has read S.r_done before a later call changes it)
+    return d0 >= n ? n - 1 : d0 - 2;
+  };
+
   // Position window for the fold (non-prefix mode): sorted positions
   // [S.pw_b, S.pw_e) with the exclusive prefix sums of widths (p0) and of the
   // compaction offsets (p1) from S.pw_b, and the per-position scalars the row
@@ -486,7 +569,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     while (count < kPWN && base < n) {
       if (base > lim) {
         if (count > count0) break;  // only the first chunk waits
-        lim = wait_ready(base);
+        lim = lz ? lazy_fill(base) : wait_ready(base);
         if (lim == -2) return false;  // beaten (S.abort)
 #ifdef TABI_PHASE_TRACE
         if (rd.flags && jslot == 0 && base == 0 && tid == 0) st->tfirst[2] = gtime();
@@ -499,7 +582,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       const int32_t a1 = valid ? off[s] : 0;
       // fused mode: a chart that cannot fit the dilated atlas at this scale
       // makes the candidate fail (it must be placed in some row)
-      if (rd.flags && valid && (w_s > Wp || hd[s] > Hp)) S.fail = 1;
+      if ((rd.flags || lz) && valid && (w_s > Wp || hd[s] > Hp)) S.fail = 1;
       int32_t e0, e1, t0, t1;
       block_scan2(w_s, a1, e0, e1, t0, t1, S);
       if (valid) {
@@ -579,7 +662,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
 #ifdef TABI_NO_PREFETCH
       const bool all = false;  // experiment: measure the row without the prefetch
 #else
-      const bool all = !rd.flags || ready_lim == n - 1;
+      const bool all = lz ? S.r_done >= n : !rd.flags || ready_lim == n - 1;
 #endif
       if (all && S.next_a0 >= 0) {
         const int32_t a0 = S.next_a0 & ~3;
@@ -1065,6 +1148,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         }
       }
     }
+    if (ef) {  // 2 x polygon area of the row's charts (published by the walk's barrier)
+      long long pa = 0;
+      for (int t = rs + tid; t <= endS; t += kPT) pa += lz->area[t];
+      pa = warp_sum64(pa);
+      if (lane == 0 && pa) atomicAdd((unsigned long long*)&S.placed, (unsigned long long)pa);
+    }
     for (int ws0 = rs; ws0 <= endS; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = min(we, endS + 1) - ws0;
       stage(ws0, we);
@@ -1076,6 +1165,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
       int32_t* const Fs = F;
+      long long dsum = 0;  // early fail: this thread's increase of sum_x F[x]
       walk(
           W, nwin,
           [&](int i, int32_t j0, int32_t j1) {
@@ -1088,7 +1178,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             }
             // the whole run of this chart at once: F <- max(F, Y + BottomEdge)
             const uint32_t* pc = pr + W.rco[i];
-            if (dir) {
+            if (ef) {  // each raise returns the value it replaced: the increases telescope
+              int32_t* fp = dir ? Fs + Xc + Wd - 1 : Fs + Xc;
+              const int step = dir ? -1 : 1;
+              for (int32_t j = j0; j < j1; j++) {
+                const int32_t v = Yv + hi16(pc[j]);
+                const int32_t o = atomicMax(fp + step * j, v);
+                if (v > o) dsum += v - o;
+              }
+            } else if (dir) {
               int32_t* fp = Fs + Xc + Wd - 1;
               #pragma unroll 4
               for (int32_t j = j0; j < j1; j++) atomicMax(fp - j, Yv + hi16(pc[j]));
@@ -1100,6 +1198,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             wk += (unsigned long long)(j1 - j0);
           },
           [&](int, int32_t) {}, [&](int) {});
+      if (ef) {
+        dsum = warp_sum64(dsum);
+        if (lane == 0 && dsum) atomicAdd((unsigned long long*)&S.sumF, (unsigned long long)dsum);
+      }
       pk_sync();
     }
     phase_mark(6);
@@ -1125,6 +1227,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       }
       if (S.fmax > Hp) S.fail = 1;  // overflow below the atlas bottom
       S.row_start = endS + 1;
+      if (ef && !S.fail && S.row_start < n) {
+        // R8: the charts still to place lie below the frontline, disjoint, in
+        // [F(x), H') per column: their polygon area (2 x area in units^2 at
+        // scale 1, x (m / (M 256))^2 / 2) cannot exceed sum_x (H' - F[x])
+        const i128 rem = (i128)(lz->atot - S.placed);
+        const i128 freeA = (i128)Wp * Hp - S.sumF;
+        const i128 SCm2 = (i128)pp.M * TABI_UNITS * pp.M * TABI_UNITS;
+        if (rem * m * m > 2 * SCm2 * freeA) S.fail = 1;
+      }
       if (rd.flags && pp.early && wj < jslot) S.abort = 1;  // checked at the next row start
       const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
       S.next_a0 = (!prefix_mode && S.w_fold && nx < n && nx < S.fold_hi && nx - rs < kRW)
@@ -1224,7 +1335,6 @@ struct RasterArgs {
   const int32_t* tix;     // [n] tile of each sorted position
 };
 
-__host__ __device__ __forceinline__ size_t r16(size_t b) { return (b + 15) & ~(size_t)15; }
 
 // per-group carve of the dynamic shared memory
 __host__ __device__ __forceinline__ size_t group_bytes(int k) {
@@ -1232,11 +1342,6 @@ __host__ __device__ __forceinline__ size_t group_bytes(int k) {
          r16(4 * kTCF) + r16(32) + r16(4 * (2 * kRGW + 4)) + r16((size_t)4 * kTCF * 4 * k) + r16(4 * (size_t)kRawF);
 }
 
-__device__ __forceinline__ unsigned char* carve(unsigned char*& p, size_t bytes) {
-  unsigned char* r = p;
-  p += r16(bytes);
-  return r;
-}
 
 __global__ void __launch_bounds__(kNT, 1)
 fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __restrict__ rowofs,
@@ -1450,6 +1555,29 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 // or every atlas is decided; items are only ever produced by running CTAs, so
 // the queue cannot deadlock.  P:307 "one work group per scale factor" is the
 // unit; the batch gives each GPU hundreds of them in flight.
+// Batch-kernel rasterization: kBG independent groups of kBGT threads (named
+// barriers 1..kBG), each taking every kBG-th tile of kBTC sorted charts, so
+// one group's barrier / setup latency hides behind the others' work (the
+// packer that follows uses the whole CTA).
+#ifndef TABI_BATCH_RG
+#define TABI_BATCH_RG 4
+#endif
+constexpr int kBG = TABI_BATCH_RG;
+constexpr int kBGT = kNT / kBG;
+constexpr int kBTC = kBGT / 8;
+constexpr int kBGW = kBGT / 32;
+constexpr int kBRaw = 16384 / kBG;
+__host__ __device__ __forceinline__ size_t bgroup_bytes(int k) {
+  return r16(sizeof(k3::ChartK3) * kBTC) + r16(4 * kBTC) + 2 * r16(4 * (kBTC + 1)) +
+         r16(4 * kBTC) + r16(32) + r16((size_t)4 * kBTC * 4 * k) + r16(4 * (size_t)kBRaw);
+}
+struct BGroupSync {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kBGT) : "memory");
+  }
+};
+
 __device__ __forceinline__ int32_t ld_acquire_i(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1508,53 +1636,75 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
     const int32_t* perm = A.perm + c0;
     const int32_t* colofs = A.colofs + c0;
     const int32_t* rowofs = A.rowofs + c0;
+    long long tc0 = 0, tc1 = 0, tc2 = 0;  // thread 0: phase clocks (raster, pairs, packer)
     if (!dead) {
-      // ---- footprints of every chart at m/M (K3, D11 + D13) ----------------
-      if (tid == 0) { *cbad = 0; *cand = Cand{}; }
+      // ---- footprints of every chart at m/M (K3, D11 + D13): all up front,
+      // or (lazy) inside the packer as its fold reaches them (LazyRaster) ----
+      if (tid == 0) { *cbad = 0; *cand = Cand{}; tc0 = clock64(); }
       __syncthreads();
-      {
-        unsigned char* p = dsm;
-        k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kTCF);
-        int32_t* cells = (int32_t*)carve(p, 4 * kTCF);
-        int32_t* cpre = (int32_t*)carve(p, 4 * (kTCF + 1));
-        int32_t* opre = (int32_t*)carve(p, 4 * (kTCF + 1));
-        int32_t* big = (int32_t*)carve(p, 4 * kTCF);
+      LazyRaster lzr;
+      lzr.P = P;
+      lzr.perm = perm;
+      lzr.cbad = cbad;
+      lzr.area = A.area + gcta * nm;
+      lzr.sc = k3::Scale{m, SCm, 0};
+      lzr.ahead = 96;
+      lzr.early_fail = A.early_fail;
+      lzr.atot = (int64_t)st->atot_lo;
+      lzr.cycles = A.cycles;
+      if (!A.lazy) {
+        const int grp = tid / kBGT, gt = tid % kBGT, gw = gt >> 5;
+        const BGroupSync gsync{1 + grp};
+        unsigned char* p = dsm + bgroup_bytes(k) * grp;
+        k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kBTC);
+        int32_t* cells = (int32_t*)carve(p, 4 * kBTC);
+        int32_t* cpre = (int32_t*)carve(p, 4 * (kBTC + 1));
+        int32_t* opre = (int32_t*)carve(p, 4 * (kBTC + 1));
+        int32_t* big = (int32_t*)carve(p, 4 * kBTC);
         int32_t* misc = (int32_t*)carve(p, 32);
-        carve(p, 4 * (2 * kRGW + 4));
-        int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kTCF * 4 * k);
-        uint32_t* raw = (uint32_t*)carve(p, 4 * (size_t)kRawF);
-        p = dsm + group_bytes(k) * kRG;
+        int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kBTC * 4 * k);
+        uint32_t* raw = (uint32_t*)carve(p, 4 * (size_t)kBRaw);
+        p = dsm + bgroup_bytes(k) * kBG;
         k3::ChartK3* CW = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kNW);
         int32_t* wtab = (int32_t*)carve(p, (size_t)4 * kNW * 4 * k);
         const k3::Scale sc{m, SCm, 0};
-        for (int s0 = 0; s0 < n; s0 += kTCF) {
-          const int nt = min(kTCF, n - s0);
-          k3::tile_raster<kTCF, kNT, kRawF>(P, perm, pp, colofs, rowofs, dcol, drow, wd, hd, cbad,
-                                            0, s0, sc, CH, cells, cpre, opre, &misc[1], big, tabs,
-                                            raw, nt, tid, [] { __syncthreads(); });
-          for (int ci = wid; ci < nt; ci += kNW)
+        const int ntile = (n + kBTC - 1) / kBTC;
+        unsigned long long pe = 0;  // work accounting: footprint entries (Wd + Hd)
+        for (int t = grp; t < ntile; t += kBG) {
+          const int s0 = t * kBTC, nt = min(kBTC, n - s0);
+          k3::tile_raster<kBTC, kBGT, kBRaw>(P, perm, pp, colofs, rowofs, dcol, drow, wd, hd, cbad,
+                                             0, s0, sc, CH, cells, cpre, opre, &misc[1], big, tabs,
+                                             raw, nt, gt, gsync);
+          for (int ci = gw; ci < nt; ci += kBGW)
             if (big[ci])
               k3::big_chart(P, perm, pp, colofs, rowofs, dcol, drow, 0, s0 + ci, sc, CW[wid],
                             wtab + wid * 4 * k, lane);
-          if (wid == 0) {  // work accounting: footprint entries (Wd + Hd) of the tile
-            unsigned long long pe = 0;
-            for (int ci = lane; ci < nt; ci += 32)
-              pe += (unsigned long long)(CH[ci].ws + CH[ci].hs + 4 * g);
-            for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
-            if (lane == 0) atomicAdd(&st->work_prof, pe);
-          }
-          __syncthreads();
+          if (gt < nt) pe += (unsigned long long)(CH[gt].ws + CH[gt].hs + 4 * g);
+          // the tile's internal adjacent pairs (K3b, D14 + D15) while its rows
+          // are hot in L2 -- warp per pair, both charts rasterized above
+          for (int s = s0 + gw; s < s0 + nt - 1; s += kBGW)
+            if (CH[s - s0].small && CH[s + 1 - s0].small)
+              k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, 0, s, lane);
+          gsync();
         }
+        for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
+        if (lane == 0 && pe) atomicAdd(&st->work_prof, pe);
+        __syncthreads();
       }
-      // ---- adjacent pairs: compaction advance + locks (K3b, D14 + D15) ------
-      if (!*(volatile int32_t*)cbad)
-        for (int s = wid; s < n; s += kNW)
-          k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, 0, s, lane);
+      // ---- the pairs across tile boundaries, and the last chart's zero entry --
+      if (tid == 0) tc1 = clock64();
+      if (!A.lazy && !*(volatile int32_t*)cbad) {
+        const int ntile = (n + kBTC - 1) / kBTC;
+        for (int b = wid; b < ntile; b += kNW)
+          k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, 0, min(n - 1, (b + 1) * kBTC - 1),
+                          lane);
+      }
       __syncthreads();
       // ---- Alg. 4 for this candidate (K4) -----------------------------------
+      if (tid == 0) tc2 = clock64();
       packer(pp, colofs, rowofs, dcol, drow, wd, hd, off, lock, A.hsorted + c0, cbad, scr,
              A.pair_cap, X, Y, mir, cand, st, prof_cap, m, 0, 0, Ready{nullptr, 0, nullptr, nullptr},
-             dsm);
+             dsm, A.lazy != 0, lzr);
       __syncthreads();
     }
     if (tid == 0) {
@@ -1564,7 +1714,13 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
       else if (cd.success) oc = 1;
       else oc = m > 1 ? 0 : 2;
       AtlasRes& R = A.res[a];
-      if (!dead) R.evaluated++;
+      if (!dead) {
+        R.evaluated++;
+        const long long t3 = clock64();
+        atomicAdd(&A.cycles[0], (unsigned long long)(tc1 - tc0));
+        atomicAdd(&A.cycles[1], (unsigned long long)(tc2 - tc1));
+        atomicAdd(&A.cycles[2], (unsigned long long)(t3 - tc2));  // (lazy: raster inside, see below)
+      }
       if (oc == 1) {
         R.winner = m;
         R.rows = cd.rows;
@@ -1752,6 +1908,16 @@ cudaError_t launch_fused(int grid, const Proxies& P, const int32_t* perm, const 
                   &ra};
   return cudaLaunchCooperativeKernel((const void*)fused_kernel, dim3(grid), dim3(kNT), args,
                                      kMaxDynSmem, s);
+}
+
+bool many_lazy_ok(int k, int g, int Wp) {
+  const int f_words = (Wp + 3) & ~3;
+  const size_t fixed = sizeof(int32_t) * ((size_t)f_words + 10 * (size_t)kRW + 5 * (size_t)kPWN +
+                                         2 * (size_t)kPairSm) + kRW + kPWN + kPairSm;
+  const size_t prof = (((size_t)kMaxDynSmem - fixed) / 4 & ~(size_t)3) * 4;
+  const size_t need = r16(sizeof(k3::ChartK3) * kLzTC) + r16(4 * kLzTC) + 2 * r16(4 * (kLzTC + 1)) +
+                      r16(4 * kLzTC) + r16(32) + r16((size_t)4 * kLzTC * 4 * k);
+  return g <= k3::kDilMax && need <= prof;
 }
 
 int many_grid(int device) {

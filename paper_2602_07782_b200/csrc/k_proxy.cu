@@ -26,18 +26,12 @@ constexpr int kBlock = 256;  // threads per block
 
 // Per-group shared scratch, k slices per axis (sized by k at launch).
 struct Slices {
-  int32_t *lo0, *lo1, *hi0, *hi1;      // unmerged: x-slices top/bot, y-slices left/right
-  int32_t *mlo0, *mlo1, *mhi0, *mhi1;  // merged
-  int64_t *fl0, *fl1, *cl0, *cl1;      // floor(i ext / k), ceil((i + 1) ext / k)
+  int32_t *mlo0, *mlo1, *mhi0, *mhi1;  // x-slices top/bot, y-slices left/right (merged = D4, R7)
   int64_t* ob;                         // [8][4] OBB extents per angle
-  __device__ int32_t* lo(int a) const { return a ? lo1 : lo0; }
-  __device__ int32_t* hi(int a) const { return a ? hi1 : hi0; }
-  __device__ int32_t* mlo(int a) const { return a ? mlo1 : mlo0; }
-  __device__ int32_t* mhi(int a) const { return a ? mhi1 : mhi0; }
 };
 
 __host__ __device__ constexpr size_t slice_bytes(int k) {
-  return ((size_t)8 * 4 * k + (size_t)4 * 8 * k + 256 + 15) & ~(size_t)15;
+  return (256 + (size_t)4 * 4 * k + 15) & ~(size_t)15;
 }
 
 template <int G>
@@ -113,82 +107,21 @@ __device__ void accumulate_slices(const Group<G>& g, const int32_t* A, const int
   }
 }
 
-// D5 merge: x-slice j tightened by y-slices whose x-range meets strip j.
-// The (j, i) tests are spread over the group: with k <= G, lane = part * k + j
-// scans i = part, part + P, ... (P = G / k parts) and the parts' min / max
-// meet by shuffles; with k > G lanes stride over j.  Only min / max, so the
-// order is immaterial.  The strip bounds floor(i ext / k), ceil((i+1) ext / k)
-// are below 2^25: int32.
-template <int G>
-__device__ void merge_slices(const Group<G>& g, const Slices& S, int64_t w, int64_t h, int k) {
-  for (int i = g.gl; i < k; i += G) {
-    S.fl0[i] = fdiv_fast((int64_t)i * h, k);
-    S.cl0[i] = cdiv_fast((int64_t)(i + 1) * h, k);
-    S.fl1[i] = fdiv_fast((int64_t)i * w, k);
-    S.cl1[i] = cdiv_fast((int64_t)(i + 1) * w, k);
-  }
-  g.sync();
-  const bool split = k <= G;
-  const int P = split ? G / k : 1;
-  const int part = split ? g.gl / k : 0;
-  const int jstep = split ? k : G;
-  for (int jb = 0; jb < k; jb += jstep) {
-    const int j = jb + (split ? g.gl % k : g.gl);
-    const bool act = j < k && part < P;
-    int32_t mn0 = INT32_MAX, mx0 = INT32_MIN, mn1 = INT32_MAX, mx1 = INT32_MIN;
-    if (act) {
-      const int64_t jw0 = (int64_t)j * w, jw1 = (int64_t)(j + 1) * w;
-      const int64_t jh0 = (int64_t)j * h, jh1 = (int64_t)(j + 1) * h;
-      for (int i = part; i < k; i += P) {
-        // x-slices: y-slice i's x-range meets strip j
-        if ((int64_t)k * S.lo1[i] <= jw1 && (int64_t)k * S.hi1[i] >= jw0) {
-          mn0 = min(mn0, (int32_t)S.fl0[i]);
-          mx0 = max(mx0, (int32_t)S.cl0[i]);
-        }
-        // y-slices: x-slice i's y-range meets strip j
-        if ((int64_t)k * S.lo0[i] <= jh1 && (int64_t)k * S.hi0[i] >= jh0) {
-          mn1 = min(mn1, (int32_t)S.fl1[i]);
-          mx1 = max(mx1, (int32_t)S.cl1[i]);
-        }
-      }
-    }
-    for (int q = 1; q < P; q++) {  // uniform: every lane of the group shuffles
-      const int o = q * k;
-      const int32_t a = __shfl_down_sync(g.mask, mn0, o, G), b = __shfl_down_sync(g.mask, mx0, o, G);
-      const int32_t c = __shfl_down_sync(g.mask, mn1, o, G), d = __shfl_down_sync(g.mask, mx1, o, G);
-      if (part == 0 && g.gl + o < P * k) {
-        mn0 = min(mn0, a); mx0 = max(mx0, b);
-        mn1 = min(mn1, c); mx1 = max(mx1, d);
-      }
-    }
-    if (act && part == 0) {
-      int32_t t = S.lo0[j], b = S.hi0[j];
-      if (mn0 != INT32_MAX && mn0 > t) t = mn0;
-      if (mx0 != INT32_MIN && mx0 < b) b = mx0;
-      S.mlo0[j] = t;
-      S.mhi0[j] = b;
-      t = S.lo1[j];
-      b = S.hi1[j];
-      if (mn1 != INT32_MAX && mn1 > t) t = mn1;
-      if (mx1 != INT32_MIN && mx1 < b) b = mx1;
-      S.mlo1[j] = t;
-      S.mhi1[j] = b;
-    }
-  }
-}
-
+// D4 slices, then D5's merge.  D5 is the identity on D4's slices (DESIGN.md
+// R7: each slice is the exact extent of the polygon in its closed strip, and
+// the y-band holding a strip's topmost point always meets the strip, so the
+// merged bound never moves); the merged slices are the accumulated ones --
+// pinned by the oracle (which merges literally) in every parity test.
 template <int G>
 __device__ void merged_slices(const Group<G>& g, const Slices& S, const int32_t* X, const int32_t* Y,
                               int nv, int64_t w, int64_t h, int k) {
   for (int j = g.gl; j < k; j += G) {
-    S.lo0[j] = INT32_MAX; S.hi0[j] = INT32_MIN;
-    S.lo1[j] = INT32_MAX; S.hi1[j] = INT32_MIN;
+    S.mlo0[j] = INT32_MAX; S.mhi0[j] = INT32_MIN;
+    S.mlo1[j] = INT32_MAX; S.mhi1[j] = INT32_MIN;
   }
   g.sync();
-  accumulate_slices(g, X, Y, nv, w, k, S.lo0, S.hi0);
-  accumulate_slices(g, Y, X, nv, h, k, S.lo1, S.hi1);
-  g.sync();
-  merge_slices(g, S, w, h, k);
+  accumulate_slices(g, X, Y, nv, w, k, S.mlo0, S.mhi0);
+  accumulate_slices(g, Y, X, nv, h, k, S.mlo1, S.mhi1);
   g.sync();
 }
 
@@ -272,12 +205,9 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   Slices S;
   {
     unsigned char* p = dsm + slice_bytes(k) * gib;
-    int32_t* i32 = (int32_t*)p;
-    S.lo0 = i32; S.lo1 = i32 + k; S.hi0 = i32 + 2 * k; S.hi1 = i32 + 3 * k;
-    S.mlo0 = i32 + 4 * k; S.mlo1 = i32 + 5 * k; S.mhi0 = i32 + 6 * k; S.mhi1 = i32 + 7 * k;
-    int64_t* i64 = (int64_t*)(p + 32 * (size_t)k);
-    S.fl0 = i64; S.fl1 = i64 + k; S.cl0 = i64 + 2 * k; S.cl1 = i64 + 3 * k;
-    S.ob = i64 + 4 * k;
+    S.ob = (int64_t*)p;  // 256 B, 8-byte aligned at the group's slot
+    int32_t* i32 = (int32_t*)(p + 256);
+    S.mlo0 = i32; S.mlo1 = i32 + k; S.mhi0 = i32 + 2 * k; S.mhi1 = i32 + 3 * k;
   }
   const int gl = g.gl;
   const int32_t a0 = start[c];
@@ -476,11 +406,17 @@ void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float 
 
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-                    cudaStream_t s, AtlasMap am) {
+                    cudaStream_t s, AtlasMap am, int64_t nverts) {
   const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
   const int forced = genv ? atoi(genv) : 0;
+  // Lanes per chart.  Below 4096 charts a pack is latency-bound per chart: 32.
+  // Above, the lanes of a warp's groups diverge whenever their charts' vertex
+  // counts differ, so narrow groups pay off only for charts of a few vertices:
+  // measured C4 (20,000 lightmap quads, 4.4 vertices per chart) best at 8, the
+  // C5 batch (547 k TSS charts, 9.6 vertices) at 32 (2.9 ms vs 3.9 at 16, 4.8 at 8).
+  const int64_t avg = nverts > 0 ? (nverts + n - 1) / n : 0;
   const int G = forced == 8 || forced == 16 || forced == 32 ? forced
-                : n < 4096 ? 32 : n < 8192 ? 16 : 8;  // measured: C3 (1572) 32, C4 (20000) 8
+                : n < 4096 ? 32 : avg >= 8 ? 32 : avg >= 6 ? 16 : n < 8192 ? 16 : 8;
   if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
   else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
   else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);

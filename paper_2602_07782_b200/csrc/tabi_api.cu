@@ -76,6 +76,9 @@ struct ManyWs {
   uint8_t *lock = nullptr, *mir = nullptr;
   Cand* cands = nullptr;
   int32_t* cand_bad = nullptr;
+  unsigned long long* cycles = nullptr;   // [3] batch kernel phase cycles
+  int64_t* area = nullptr;                // [G][nmax] lazy batch mode
+  unsigned long long h_cycles[3] = {0, 0, 0};
   int32_t* solo_start = nullptr;  // rebased chart offsets of a solo atlas (device mode)
   // pinned host staging for host-mode inputs / outputs
   float* h_xy = nullptr;          // 2V floats + N + 1 ints
@@ -88,7 +91,7 @@ struct ManyWs {
     void* ds[] = {d_xy, d_start, qx, qy, P.w, P.h, P.area2, P.xmin, P.ymin, P.pose, P.prerot, P.sl,
                   P.obb_j, P.obb, perm, colofs, rowofs, hsorted, tstart, tix, d_out, d_small, sts,
                   res, q, dcol, drow, wd, hd, off, scratch, X, Y, lock, mir, cands, cand_bad,
-                  solo_start};
+                  solo_start, cycles, area};
     for (void* p : ds)
       if (p) cudaFree(p);
     void* hs[] = {h_small, h_sts, h_res, h_xy, h_out};
@@ -527,7 +530,8 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     nl++;
     if (prologue) {
       launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
-                     ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s);
+                     ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s,
+                     AtlasMap{nullptr, 1, nullptr}, V_in);
       nl++;
       tm.mark(s);
       if (wave == 0 && launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs,
@@ -831,7 +835,9 @@ static tabi_status many_ensure(tabi_ctx* ctx, int64_t N, int64_t V, int32_t A, i
     CK(grow(&w.lock, G * nm)); CK(grow(&w.mir, G * nm));
     CK(grow(&w.scratch, (int64_t)G * (6 * nm + 3 * w.pair_cap)));
     CK(grow(&w.cands, G)); CK(grow(&w.cand_bad, G));
+    CK(grow(&w.area, G * nm));
   }
+  if (!w.cycles) CK(grow(&w.cycles, 3));
   return TABI_OK;
 }
 
@@ -914,6 +920,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
   float stage_ms[4] = {0.f, 0.f, 0.f, 0.f};
   int32_t evaluated = 0;
   int64_t work_pack = 0, work_prof = 0;
+  bool lazy_used = false;
   const char* tenv = getenv("TABI_TIMING");
   const bool timing = tenv && tenv[0] == '1';
   if (E > 0) {
@@ -984,9 +991,10 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     pp.col_cap = w.col_cap;
     pp.row_cap = w.row_cap;
     launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, s);
+    CK(cudaMemsetAsync(w.cycles, 0, 3 * sizeof(unsigned long long), s));
     if (timing) CK(cudaEventRecord(w.stage[0], s));
     launch_proxies(d_xy, d_start, (int32_t)N, 1.0f, 1.0f, pp.k, pp.flags, w.qx, w.qy, w.cap_V, w.P,
-                   w.sts, s, AtlasMap{d_abase, A, d_res});
+                   w.sts, s, AtlasMap{d_abase, A, d_res}, V);
     if (timing) CK(cudaEventRecord(w.stage[1], s));
     launch_many_sort_prep(w.P, d_abase, A, w.perm, pp, w.colofs, w.rowofs, w.hsorted, w.tstart,
                           w.tix, w.sts, s);
@@ -1016,6 +1024,15 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     ma.mir = w.mir;
     ma.cands = w.cands;
     ma.cand_bad = w.cand_bad;
+    ma.cycles = w.cycles;
+    ma.area = w.area;
+    {  // lazy raster + area test (R8); TABI_LAZY=0 / TABI_EARLY_FAIL=0 switch them off
+      const char* le = getenv("TABI_LAZY");
+      const char* fe = getenv("TABI_EARLY_FAIL");
+      ma.lazy = !(le && le[0] == '0') && many_lazy_ok(pp.k, pp.g, pp.Wp);
+      ma.early_fail = ma.lazy && !(fe && fe[0] == '0') && !(pp.flags & TABI_F_ADJACENT_LOCKS_ONLY);
+      lazy_used = ma.lazy != 0;
+    }
     ma.nmax = w.nmax;
     ma.pair_cap = w.pair_cap;
     CK(launch_many(w.G, pp, ma, s));
@@ -1036,6 +1053,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     }
     CK(cudaMemcpyAsync(w.h_sts, w.sts, sizeof(Status) * A, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(AtlasRes) * A, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_cycles, w.cycles, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(w.span[1], s));
     CK(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&dev_ms, w.span[0], w.span[1]);
@@ -1116,6 +1134,8 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     for (int i = 0; i < 4; i++) binfo->stage_ms[i] = stage_ms[i];
     binfo->work_pack = work_pack;
     binfo->work_profile = work_prof;
+    for (int i = 0; i < 3; i++) binfo->cycles[i] = E > 0 ? (int64_t)ctx->many.h_cycles[i] : 0;
+    if (lazy_used) binfo->cycles[2] = std::max<int64_t>(0, binfo->cycles[2] - binfo->cycles[0] - binfo->cycles[1]);
   }
   return ret;
 }

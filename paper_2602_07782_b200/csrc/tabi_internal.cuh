@@ -414,7 +414,8 @@ struct AtlasMap {
 // Status::capacity bit 2 (-> TABI_ECAPACITY) before anything is written
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-                    cudaStream_t s, AtlasMap am = AtlasMap{nullptr, 1, nullptr});
+                    cudaStream_t s, AtlasMap am = AtlasMap{nullptr, 1, nullptr},
+                    int64_t nverts = 0);  // total vertices if known (picks the lane group)
 // Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
 void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
                   int32_t* rdy, int64_t nrdy, cudaStream_t s);
@@ -486,6 +487,10 @@ struct ManyArgs {
   uint8_t* mir;
   Cand* cands;                    // [G]
   int32_t* cand_bad;              // [G]
+  unsigned long long* cycles;     // [3] SM cycles summed over items: raster, pairs, packer
+  int64_t* area;                  // [G][nmax] lazy mode: 2 x polygon area by sorted position
+  int32_t lazy;                   // rasterize on demand inside the packer (many_lazy_ok)
+  int32_t early_fail;             // lazy mode: the row-end area test (R8)
   int32_t nmax;
   int64_t pair_cap;
 };
@@ -495,6 +500,8 @@ void launch_many_sort_prep(const Proxies& P, const int32_t* abase, int32_t A, in
                           const PackParams& pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
                           int32_t* tstart, int32_t* tix, Status* sts, cudaStream_t s);
 int many_grid(int device);  // persistent CTAs (one per SM)
+// the lazy batch raster fits the packer's staging buffer at this k and W' (and g <= 2)
+bool many_lazy_ok(int k, int g, int Wp);
 // k_floor.cu: packer building-block latencies in ns (tabi_debug_latency_floor)
 int latency_floor(int device, double* out8);
 cudaError_t launch_many(int grid, const PackParams& pp, const ManyArgs& a, cudaStream_t s);

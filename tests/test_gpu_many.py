@@ -197,3 +197,21 @@ def test_pack_batch_uses_many(ctx):
         assert inf.scale_index == inf1.scale_index and pl.tobytes() == pl1.tobytes()
     c2.close()
     c3.close()
+
+
+@pytest.mark.parametrize("mode", [{"TABI_LAZY": "0"}, {"TABI_EARLY_FAIL": "0"}])
+def test_pack_many_lazy_and_early_fail_are_exact(ctx, monkeypatch, mode):
+    """The batch kernel's lazy raster and its row-end area test (R8)
+    only skip work of candidates that fail: switching either off gives the
+    same bytes on 48 C5 atlases (whose searches evaluate ~8 candidates each)."""
+    from paper_2602_07782_b200 import concat_chart_sets, spec_of
+    sets = [chartgen.config5(i) for i in range(100, 148)]
+    xy, cst, abase, res = concat_chart_sets(sets)
+    ref = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res)
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    alt = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res)
+    assert list(ref[3]) == list(alt[3])
+    assert [i.scale_index for i in ref[2]] == [i.scale_index for i in alt[2]]
+    assert ref[1].tobytes() == alt[1].tobytes()
+    assert ref[4].candidates_evaluated == alt[4].candidates_evaluated

@@ -1,17 +1,19 @@
-# Round profile: per-kernel launch list (ncu gpu__time_duration, one pack) and
-# --set full captures of the fused wave kernel and the proxy kernel.
-#   bash tools/gpu_profile_round.sh [C3|C4|C2]
-mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-W=${1:-C3}
-python tools/profile_once.py --workload $W > gpurun_out/plain_$W.log 2>&1 || { echo "plain run failed"; exit 1; }
-L=$(grep -o 'launches/pack [0-9]*' gpurun_out/plain_$W.log | awk '{print $2}')
+# Round profile of one workload: plain run, then the ncu launch list (device
+# time of every kernel of one call) and --set full captures of the given
+# kernels.   bash tools/gpu_profile_round.sh C5 "proxy_kernel many_kernel" [out_dir]
+W=${1:-C5}
+KS=${2:-"proxy_kernel many_kernel"}
+O=${3:-gpurun_out/prof}
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+python tools/profile_once.py --workload $W > $O/plain_$W.log 2>&1 || { echo "plain run failed"; cat $O/plain_$W.log; exit 1; }
+L=$(grep -o 'launches/pack [0-9]*' $O/plain_$W.log | awk '{print $2}')
 echo "launches/pack $L"
 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3*L)) -c $L --csv \
-    --log-file gpurun_out/launches_$W.csv python tools/profile_once.py --workload $W > gpurun_out/ncu_list_$W.log 2>&1
+    --log-file $O/launches_$W.csv python tools/profile_once.py --workload $W > $O/ncu_list_$W.log 2>&1
 echo "list rc=$?"
-for K in fused_kernel proxy_kernel; do
+for K in $KS; do
   ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
-      -o gpurun_out/prof_${K}_$W python tools/profile_once.py --workload $W > gpurun_out/ncu_${K}_$W.log 2>&1
+      -o $O/prof_${K}_$W python tools/profile_once.py --workload $W > $O/ncu_${K}_$W.log 2>&1
   echo "$K rc=$?"
 done
