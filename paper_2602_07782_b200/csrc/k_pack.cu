@@ -238,6 +238,50 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   return v;
 }
 
+// Lazy raster step (batch mode): the packer's threads rasterize the sorted
+// positions [done, target) in kLzTC-chart tiles into the candidate's buffers
+// (footprints, widths / heights, 2 x polygon areas) and compute the adjacent
+// pairs that end in them.  Not inlined: its register working set then does
+// not add to the packer's (no spills in the row loop).  Returns the new end.
+__device__ __noinline__ int lazy_tiles(const LazyRaster& lz, const PackParams& pp,
+                                       const int32_t* __restrict__ colofs,
+                                       const int32_t* __restrict__ rowofs, uint32_t* dcol,
+                                       uint32_t* drow, int32_t* wd, int32_t* hd, int32_t* off,
+                                       uint8_t* lock, int slot, int done, int target,
+                                       unsigned char* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, n = pp.n;
+  unsigned char* p = scratch;  // the packer's staging buffer (idle until the last tile)
+  k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kLzTC);
+  int32_t* cells = (int32_t*)carve(p, 4 * kLzTC);
+  int32_t* cpre = (int32_t*)carve(p, 4 * (kLzTC + 1));
+  int32_t* opre = (int32_t*)carve(p, 4 * (kLzTC + 1));
+  int32_t* big = (int32_t*)carve(p, 4 * kLzTC);
+  int32_t* misc = (int32_t*)carve(p, 32);
+  int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kLzTC * 4 * pp.k);
+  long long c0 = tid == 0 ? clock64() : 0, cpair = 0;
+  while (done < target) {  // (uniform)
+    const int s0 = done, nt = min(kLzTC, n - s0);
+    k3::tile_raster<kLzTC, kPT, 1>(lz.P, lz.perm, pp, colofs, rowofs, dcol, drow, wd, hd, lz.cbad,
+                                   slot, s0, lz.sc, CH, cells, cpre, opre, &misc[1], big, tabs,
+                                   nullptr, nt, tid, [] { pk_sync(); });
+    if (tid < nt) lz.area[s0 + tid] = lz.P.area2[lz.perm[s0 + tid]];
+    // pairs (s, s + 1) that end in this tile, and the last chart's zero entry
+    const long long cp = tid == 0 ? clock64() : 0;
+    const int plo = max(0, s0 - 1), phi = s0 + nt == n ? n - 1 : s0 + nt - 2;
+    for (int q = plo + wid; q <= phi; q += kPW)
+      k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, slot, q, lane);
+    pk_sync();
+    if (tid == 0) cpair += clock64() - cp;
+    done = s0 + nt;
+  }
+  if (tid == 0) {
+    const long long dt = clock64() - c0;
+    atomicAdd(lz.cycles, (unsigned long long)(dt - cpair));
+    atomicAdd(lz.cycles + 1, (unsigned long long)cpair);
+  }
+  return done;
+}
+
 // The footprint/offset arrays are not __restrict__ here: in fused mode other
 // CTAs write them during the launch, so they must not go through the
 // non-coherent load path.
@@ -421,6 +465,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     for (int q = 0; q < 4; q++) S.fmin[q] = INT32_MAX;
     S.knee_valid = 0; S.knee_ltr = 0; S.knee_left = 0; S.knee_right = 0;
     S.work = 0ull;
+    S.knee_key = 0ull;
     S.prefix_rows = 0;
     S.switched = 0;
     S.r_done = 0;
@@ -460,8 +505,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   // if its window lies inside (else drains it and copies the exact window).
   bool pf_pending = false;  // uniform: a prefetch copy is in flight
   int32_t wj = INT32_MAX;   // thread 0: last seen st->win_j
+  // the staged window and where its footprints are (every thread keeps the
+  // same copy: no shared-memory handshake)
+  int32_t win_s0 = -1, win_e = -1, g_a0 = 0;
+  bool g_pg = false;
   auto stage = [&](int ws0, int we) {
-    if (S.win_s0 == ws0 && S.win_e == we) return;
+    if (win_s0 == ws0 && win_e == we) return;
     const int nwin = we - ws0;
     // the fold already wrote the scalars of the row's first kRW charts
     // (positions below S.fold_hi), footprint offsets included
@@ -475,6 +524,19 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t a0 = c0 & ~3, a1 = (c1 + 3) & ~3;
     const bool pg = (a1 - a0) > W.prof_cap;
     const bool hit = pf_pending && c0 >= S.pf_a0 && c1 <= S.pf_a1;
+    win_s0 = ws0;
+    win_e = we;
+    g_pg = hit ? false : pg;
+    g_a0 = hit ? S.pf_a0 : a0;
+    if (have && hit) {
+      // the fold wrote the window's scalars and the row-top prefetch holds its
+      // footprints: nothing in shared memory changes, so no barrier -- every
+      // thread waits for the copy on the mbarrier
+      mbar_wait(&S.mbar, phase);
+      phase ^= 1u;
+      pf_pending = false;
+      return;
+    }
     pk_sync();  // previous readers of the window buffers are done
     #pragma unroll 1  // (cold or short: keep the code small)
     for (int k = tid; k < nwin && !have; k += kPT) {
@@ -490,12 +552,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       pf_pending = false;
     }
     if (!hit && !pg && tid == 0) bulk_g2s(W.prof, col + a0, (uint32_t)(a1 - a0) * 4u, &S.mbar);
-    if (tid == 0) {
-      if (!have) S.w_fold = 0;
-      S.win_s0 = ws0; S.win_e = we;
-      S.pglobal = hit ? 0 : pg;
-      S.a0 = hit ? S.pf_a0 : a0;
-    }
+    if (tid == 0 && !have) S.w_fold = 0;
     if (!hit && !pg) {
       mbar_wait(&S.mbar, phase);
       phase ^= 1u;
@@ -509,39 +566,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   auto lazy_fill = [&](int s) -> int {
     const int target = min(n, max(S.r_done, s + 2) + lz->ahead);
     if (S.r_done < target) {
-      unsigned char* p = (unsigned char*)W.prof;  // free: no row-top prefetch before the end
-      k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kLzTC);
-      int32_t* cells = (int32_t*)carve(p, 4 * kLzTC);
-      int32_t* cpre = (int32_t*)carve(p, 4 * (kLzTC + 1));
-      int32_t* opre = (int32_t*)carve(p, 4 * (kLzTC + 1));
-      int32_t* big = (int32_t*)carve(p, 4 * kLzTC);
-      int32_t* misc = (int32_t*)carve(p, 32);
-      int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kLzTC * 4 * pp.k);
-      int done = S.r_done;
-      long long c0 = tid == 0 ? clock64() : 0, cpair = 0;
-      while (done < target) {  // (uniform)
-        const int s0 = done, nt = min(kLzTC, n - s0);
-        k3::tile_raster<kLzTC, kPT, 1>(lz->P, lz->perm, pp, colofs, rowofs, (uint32_t*)dcol,
-                                       (uint32_t*)drow, (int32_t*)wd_all, (int32_t*)hd_all,
-                                       lz->cbad, slot, s0, lz->sc, CH, cells, cpre, opre, &misc[1],
-                                       big, tabs, nullptr, nt, tid, [] { pk_sync(); });
-        if (tid < nt) lz->area[s0 + tid] = lz->P.area2[lz->perm[s0 + tid]];
-        // pairs (s, s + 1) that end in this tile, and the last chart's zero entry
-        const long long cp = tid == 0 ? clock64() : 0;
-        const int plo = max(0, s0 - 1), phi = s0 + nt == n ? n - 1 : s0 + nt - 2;
-        for (int q = plo + wid; q <= phi; q += kPW)
-          k3::pair_offset(pp, rowofs, (const uint32_t*)drow, wd_all, hd_all, (int32_t*)off_all,
-                          (uint8_t*)lock_all, slot, q, lane);
-        pk_sync();
-        if (tid == 0) cpair += clock64() - cp;
-        done = s0 + nt;
-      }
-      if (tid == 0) {
-        S.r_done = done;
-        const long long dt = clock64() - c0;
-        atomicAdd(lz->cycles, (unsigned long long)(dt - cpair));
-        atomicAdd(lz->cycles + 1, (unsigned long long)cpair);
-      }
+      const int done = lazy_tiles(*lz, pp, colofs, rowofs, (uint32_t*)dcol, (uint32_t*)drow,
+                                  (int32_t*)wd_all, (int32_t*)hd_all, (int32_t*)off_all,
+                                  (uint8_t*)lock_all, slot, S.r_done, target,
+                                  (unsigned char*)W.prof);
+      if (tid == 0) S.r_done = done;
       pk_sync();
       return done >= n ? n - 1 : done - 2;
     }
@@ -735,7 +764,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // (no barrier here: in the non-prefix fold only thread 0 reads these
     // before the fold's own barriers)
     if (tid < 4) S.endv[tid] = INT32_MIN;
-    if (tid == 0) { S.done = 0; S.win_s0 = -1; S.win_e = -1; }
+    if (tid == 0) S.done = 0;
+    win_s0 = win_e = -1;
+    bool anylock = true;   // some adjacent pair the row may hold has a lock bit (else Alg. 1 is a no-op)
+    bool anypl = false;    // some non-adjacent (D15) pair of the row is locked
     if (prefix_mode) pk_sync();
     if (prefix_mode) {
       // prefix rows were laid out by the tail kernels (positions in xs0/xs1);
@@ -765,6 +797,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       // the row start's prefixes (the frame stays fixed while the row is folded)
       const int32_t r0 = beaten ? 0 : PW.p0[rs - S.pw_b], r1 = beaten ? 0 : PW.p1[rs - S.pw_b];
       int sc = rs;  // next position to examine
+      bool lockv = false;  // this thread saw a lock bit among the row's candidate pairs
       while (!beaten) {
         const int pb = S.pw_b, pe = S.pw_e;
         // (S.fmin[] are INT32_MAX here: reset by thread 0 after each use)
@@ -782,6 +815,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               W.rco[s - rs] = PW.co[i];
               W.rhs[s - rs] = PW.hs[i];
               W.rlk[s - rs] = PW.lk[i];
+              lockv |= PW.lk[i] != 0;
 #pragma unroll
               for (int q = 0; q < 5; q++) W.rY[q * kRW + (s - rs)] = INT32_MIN;  // push init
             }
@@ -790,7 +824,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             if (x0 + w_s > kb - ka) atomicMin(&S.fmin[2], s);
             if (x1 + w_s > kb - ka) atomicMin(&S.fmin[3], s);
           }
-          pk_sync();
+          anylock = pk_sync_or(lockv);  // (lockv is sticky: the last chunk's OR covers all)
           if (tid == 0) {
             for (int q = 0; q < 4; q++) {
               if (S.endv[q] == INT32_MIN && S.fmin[q] != INT32_MAX) S.endv[q] = S.fmin[q] - 1;
@@ -882,6 +916,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         break;
       }
       const int32_t np = S.npairs;
+      bool plv = false;
       for (int p = wid; p < np; p += kPW) {
         const int a = p < kPairSm ? SP.a[p] : pa[p], b = p < kPairSm ? SP.b[p] : pb[p];
         bool la, lb;
@@ -891,9 +926,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           const uint8_t bits = (la ? 1 : 0) | (lb ? 2 : 0);
           if (p < kPairSm) SP.lk[p] = bits;
           else plk[p] = bits;
+          plv |= bits != 0;
         }
       }
-      pk_sync();
+      if (np > 0) anypl = pk_sync_or(plv);  // (np is uniform: no pairs, no barrier)
     }
     const int32_t np = S.npairs;
     phase_mark(2);
@@ -919,7 +955,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         pk_sync();  // (index 4 of rY is rbot)
       }
       phase_mark(8);
-      const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
+      const uint32_t* pr = g_pg ? col : W.prof - g_a0;
       // flattened (chart, column) runs (see walk()); per chart segment the
       // configurations' frontline pointers are set once and the column loop is
       // specialised on 2 / 4 configurations (L->R reads F[X + j], R->L reads
@@ -997,7 +1033,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // ---- Alg. 1 CorrectYOffsets over adjacent + non-adjacent pairs ---------
     {
       const int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // HC configs [c0, c1)
-      if (c1 > c0) {
+      // (no lock bit among the row's pairs: every pass would change nothing)
+      if (!one || prefix_mode) anylock = true;
+      if (c1 > c0 && (anylock || anypl)) {
         const int32_t per = (endA - rs) + (adj_only ? 0 : np);  // adjacent pairs + list
         const int nitems = (c1 - c0) * per;
         // item -> (Ya, Yb, lock bits); with <= 2 items per thread they are
@@ -1084,7 +1122,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           for (int q = 0; q < na; q++) W.rY[q * kRW + k] = __ldcg(&Yc[(int64_t)q * n + s]);
         }
         pk_sync();
-        const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
+        const uint32_t* pr = g_pg ? col : W.prof - g_a0;
         int32_t Yv[4];
         int nact = 0;
         walk(
@@ -1111,26 +1149,26 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     pk_sync();
     phase_mark(5);
     // ---- hierarchical selection -----------------------------------
-    if (tid == 0) {
+    // (every thread: the inputs were published by the score's barrier and stay
+    // unchanged until the row end, where thread 0 stores the new maximum)
+    int cfg;
+    int32_t fmax_new;
+    {
       const int32_t sw0 = max(S.fmax, S.newmax[0]), sw1 = max(S.fmax, S.newmax[1]);
       int d0 = sw1 < sw0 ? 1 : 0;   // ties -> left to right
       if (no_bal) d0 = S.rows & 1;  // static alternation (ablation)
       // prefix rows: FastAtlas alternation, one L->R row then two R->L
       if (prefix_mode) d0 = (S.prefix_rows % 3 == 0) ? 0 : 1;
-      int cfg = d0;
+      cfg = d0;
       if (knee_ok) {
         const int32_t sk0 = max(S.conc_max, S.newmax[2]), sk1 = max(S.conc_max, S.newmax[3]);
         const int d1 = sk1 < sk0 ? 1 : 0;
         const int32_t swk = max(S.fmax, S.newmax[2 + d1]);
         if (swk <= (d0 ? sw1 : sw0) - 1) cfg = 2 + d1;  // "at least marginally smaller"
       }
-      S.sel_cfg = cfg;
-      S.fmax = max(S.fmax, S.newmax[cfg]);
-      S.knee_key = 0ull;
+      fmax_new = max(S.fmax, S.newmax[cfg]);
     }
-    pk_sync();
     // ---- commit: F <- max(F, Y + BottomEdge); record placements ------------
-    const int cfg = S.sel_cfg;
     const int f = cfg >> 1, dir = cfg & 1;
     const int32_t endS = S.end_cfg[cfg];
     // ---- FindKnee after an atlas-fold row: the height
@@ -1162,7 +1200,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         pk_sync();
       }
       phase_mark(9);
-      const uint32_t* pr = S.pglobal ? col : W.prof - S.a0;
+      const uint32_t* pr = g_pg ? col : W.prof - g_a0;
       const int32_t* rYc = one ? W.rY + cfg * kRW : W.rY;
       int32_t* const Fs = F;
       long long dsum = 0;  // early fail: this thread's increase of sum_x F[x]
@@ -1212,6 +1250,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       if (rd.flags && jslot == 0 && S.rows == 1 && !prefix_mode) st->tfirst[3] = gtime();
 #endif
       if (f == 1) S.knee_rows++;
+      S.fmax = fmax_new;
       if (f == 0 && !no_bal && !prefix_mode) {
         if (S.knee_key != 0ull) {
           const int t = 0x7fffffff - (int)(S.knee_key & 0xffffffffull);
@@ -1224,6 +1263,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         } else {
           S.knee_valid = 0;
         }
+        S.knee_key = 0ull;  // (consumed: the next FindKnee starts from zero)
       }
       if (S.fmax > Hp) S.fail = 1;  // overflow below the atlas bottom
       S.row_start = endS + 1;
