@@ -210,6 +210,21 @@ def test_config4_policy_full_size(orc, ctx):
     _compare_pack(orc, ctx, chartgen.config4(0), check_profiles=0)
 
 
+def test_config4_sequential_full_size(orc, ctx):
+    """C4 as bench.py's --workload C4 times it: 20,000 lightmap charts into
+    8192^2 with t_opt = 0 (sequential rows only): full oracle comparison
+    (proxies, order, every evaluated candidate, placements)."""
+    _compare_pack(orc, ctx, chartgen.config4(0, t_opt_bp=0), check_profiles=0)
+
+
+@pytest.mark.parametrize("i", [0, 311])
+def test_config5_atlas_single_pack(orc, ctx, i):
+    """One atlas of the C5 batch workload (200-2,000 tss charts, 2048^2) by
+    tabi_pack against the oracle (the batch path is compared in
+    test_gpu_many.py)."""
+    _compare_pack(orc, ctx, chartgen.config5(i), check_profiles=2)
+
+
 @pytest.mark.parametrize("t", [100, 1000, 10000])
 @pytest.mark.parametrize("cs", HYBRID, ids=lambda c: c.name)
 def test_exact_tail_parity(orc, ctx, cs, t):
