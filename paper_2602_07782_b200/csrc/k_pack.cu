@@ -304,31 +304,12 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   if (tid >= kPT) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  // wait until every sorted position <= s_hi has its footprints, width/height
-  // and the offset of the pair (s, s+1) published (fused mode only)
+  // fused mode: tiles [0, ready_upto] of this slot are known to be published
   if (tid == 0) ready_upto = -1;
   // sequential mode: a higher candidate already succeeded, so this one cannot
   // win -- its remaining tiles may never be rasterized; stop
   auto beaten = [&]() -> bool {
     return pp.early && *(volatile int32_t*)&st->win_j < jslot;
-  };
-  auto wait_upto = [&](int s_hi) {
-    if (!rd.flags) return;
-    const int t_req = rd.tix[min(s_hi + 1, n - 1)];
-    if (tid == 0 && ready_upto < t_req) {
-      int32_t* fl = rd.flags + (int64_t)jslot * rd.T;
-      const unsigned long long t0 = gtime();
-      while (ready_upto < t_req && !S.abort) {
-        while (ld_acquire(fl + ready_upto + 1) < 2) {
-          if (beaten()) { S.abort = 1; break; }
-          __nanosleep(64);
-        }
-        if (!S.abort) ready_upto++;
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
-      atomicAdd(&st->tr[3], gtime() - t0);
-    }
-    pk_sync();
   };
   // Fold-side readiness: block until position s (and its pair offset) is
   // published, then take whatever further tiles are already published (no
@@ -444,8 +425,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   int32_t* qrow = sc + 5 * (int64_t)n;    // prefix row id per sorted position (tail)
   if (prefix_mode) {
     if (pp.T.state[slot] != TAIL_READY) return;
-  } else if (!rd.flags && !lz && cand_bad[slot]) {  // a chart exceeds the dilated atlas at this scale
-    if (tid == 0) cands[slot] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
+  } else if ((!rd.flags && !lz && cand_bad[slot]) || (rd.flags && cand_too_big(pp, st, m))) {
+    // a chart exceeds the dilated atlas at this scale (fused mode: decided
+    // from the largest chart at once, and the rasterizers drop the slot)
+    if (tid == 0) {
+      cands[slot] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
+      if (rd.flags) *(volatile int32_t*)(rd.flags + 2 * (int64_t)pp.B * n + pp.B + jslot) = 1;
+    }
     return;
   }
   if (!prefix_mode && !rd.flags) {  // work accounting: footprint entries K3 produced
@@ -649,14 +635,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     if (!prefix_mode && pp.t_opt > 0 && !S.knee_valid) {
       const int64_t hs0 = ceildiv((int64_t)hsorted[rs] * m, (int64_t)pp.M * TABI_UNITS);
       if (hs0 * 10000 < (int64_t)pp.t_opt * pp.H) {
-        if (rd.flags) {  // fused: the split path never switches a candidate with a bad chart
-          wait_upto(n - 1);
-          if (__ldcg(cand_bad + slot)) {
-            if (tid == 0) S.fail = 1;
-            pk_sync();
-            break;
-          }
-        }
+        // (a candidate with a chart too big for the atlas never gets here: the
+        // split path checks cand_bad first, the fused packer cand_too_big)
         #pragma unroll 1  // (cold or short: keep the code small)
         for (int x = tid; x < Wp; x += kPT) fsave[x] = F[x];
         if (tid == 0) {
@@ -1293,14 +1273,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
   if (lane == 0) atomicAdd(&st->work_pack, wk);
   if (rd.flags && tid == 0) atomicMax(&st->tr[2], gtime());
-  if (rd.flags && S.fail && !S.abort) {
-    // fused mode: report a chart that exceeds the dilated atlas the way the
-    // split path does (the whole candidate's footprints must be in first)
-    wait_upto(n - 1);
-    if (tid == 0 && !S.abort && __ldcg(cand_bad + slot)) {
-      cands[slot] = Cand{0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0ull, 0ull};
-      return;
-    }
+  if (rd.flags && S.fail && tid == 0) {
+    // fused mode: this candidate's remaining tiles are no longer needed -- the
+    // rasterizers drop them (a hint: a relaxed flag read at each item fetch)
+    *(volatile int32_t*)(rd.flags + 2 * (int64_t)pp.B * n + pp.B + jslot) = 1;
   }
   // a beaten candidate stays "not evaluated" (its record keeps the reset zeros)
   if (tid == 0 && !S.switched && !S.abort) {
@@ -1345,6 +1321,12 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
 // overlap with the row loop; no host round trip inside the wave.  Several
 // groups per SM hide the latency of one group's setup / barrier phases the
 // way several resident CTAs do in the split kernels.
+#ifndef TABI_TOP_FIRST
+#define TABI_TOP_FIRST 1
+#endif
+// sequential mode: the top candidate's tiles before the others' (0: tile-major
+// for every slot, as in hybrid mode)
+constexpr bool kTopFirst = TABI_TOP_FIRST != 0;
 constexpr int kRG = kFusedGroups;   // raster groups per CTA
 constexpr int kRGT = kNT / kRG;     // threads per group (8 per chart in setup)
 constexpr int kTCF = kRGT / 8;      // charts per raster tile
@@ -1447,12 +1429,14 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     if (gt == 0) {
       const int it0 = first_it >= 0 ? first_it : G + atomicAdd(&st->work_next, 1);
       misc[0] = it0;
-      // sequential mode: drop items of candidates below a successful one
-      // (decided once, by the leader, so the group branches uniformly); the
-      // top candidate's items (slot 0) can never be beaten
-      const int j0 = !pp.early || Bw == 1 ? it0 % Bw
+      // drop items of a candidate that failed (its packer has exited), and in
+      // sequential mode of candidates below a successful one (decided once, by
+      // the leader, so the group branches uniformly); the top candidate's
+      // items (slot 0) can never be beaten
+      const int j0 = !(kTopFirst && pp.early) || Bw == 1 ? it0 % Bw
                      : it0 < T ? 0 : 1 + (it0 - T) % (Bw - 1);  // item -> slot, as below
-      misc[4] = pp.early && j0 > 0 && *(volatile int32_t*)&st->win_j < j0;
+      misc[4] = (pp.early && j0 > 0 && *(volatile int32_t*)&st->win_j < j0) ||
+                *(volatile int32_t*)(ra.rdy + 2 * (int64_t)pp.B * pp.n + pp.B + j0) != 0;
     }
     first_it = -1;
     gsync();
@@ -1473,7 +1457,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     // below a successful one are dropped (its packer exits too).  Hybrid mode:
     // tile-major for all.
     int t, j;
-    if (!pp.early || Bw == 1) {
+    if (!(kTopFirst && pp.early) || Bw == 1) {
       t = it / Bw;
       j = it % Bw;
     } else if (it < T) {
@@ -1821,28 +1805,31 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
                               const int32_t* __restrict__ Yo, const uint8_t* __restrict__ mir,
                               const Cand* __restrict__ cands, tabi_placement* out, Status* st) {
   __shared__ int32_t win, wr0, wp;
-  __shared__ Cand sc[TABI_MAX_SCALES];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  for (int i = threadIdx.x; i < pp.M; i += blockDim.x) sc[i] = cands[i];  // one parallel load
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  // Without a prefix tail anywhere V (below) is increasing in m, so the
+  // winner is the largest successful m: one parallel pass (thread m - 1 reads
+  // its candidate's two flags) and a shared max -- no serial loop, no int128.
+  if (threadIdx.x == 0) win = 0;
+  bool tl = false;
+  int32_t best = 0;
+  for (int i = threadIdx.x; i < pp.M; i += blockDim.x) {
+    const Cand& cd = cands[i];
+    tl |= cd.switched_at >= 0;
+    if (cd.success) best = i + 1;
+  }
+  const bool any_tail = __syncthreads_or(tl ? 1 : 0) != 0;
+  if (!any_tail) {
+    if (best) atomicMax(&win, best);
+    if (threadIdx.x == 0) { wr0 = pp.n; wp = 0; }
+  } else if (threadIdx.x == 0) {
     // D25: the candidate with the largest area-weighted mean final scale,
     // V = A_seq * m * 2^20 + A_pre * p * M (exact, int128), ties -> larger m;
     // without a prefix tail this is the largest successful m.
     const i128 Atot = (i128)(((unsigned __int128)st->atot_hi << 64) | st->atot_lo);
     int32_t w = 0, r0 = pp.n, pw = 0;
     i128 bestV = -1;
-    // without a tail anywhere V is increasing in m: the largest success wins
-    // (the common, sequential case -- no int128 products)
-    bool any_tail = false;
-    for (int m = pp.M; m >= 1; m--) {
-      const Cand& cd = sc[m - 1];
-      any_tail |= cd.switched_at >= 0;
-      if (!any_tail && cd.success && w == 0) w = m;
-    }
-    if (any_tail) w = 0;
-    for (int m = any_tail ? 1 : pp.M + 1; m <= pp.M; m++) {
-      const Cand& cd = sc[m - 1];
+    for (int m = 1; m <= pp.M; m++) {
+      const Cand& cd = cands[m - 1];
       if (!cd.success) continue;
       const bool tail = cd.switched_at >= 0;
       const i128 Ap = tail ? (i128)(((unsigned __int128)cd.apre_hi << 64) | cd.apre_lo) : 0;
@@ -1857,10 +1844,10 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
     win = w;
     wr0 = r0;
     wp = pw;
-    if (blockIdx.x == 0) st->winner = w;
   }
   __syncthreads();
   const int32_t m = win;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->winner = m;
   if (m == 0) return;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= pp.n) return;

@@ -8,9 +8,11 @@
 //   snap to 1/256 texel -> AABB -> 90-degree normalization -> local AABBs
 //    + merge -> orientation -> final pose (the
 //   slices reflected, D8) -> approximate OBB over 8 angles.
-// Lanes stride over vertices / edges; slice bounds are accumulated with
-// shared-memory atomicMin/Max (commutative, so schedule-independent), merges
-// and reductions use shuffles within the group.  The group size trades
+// Lanes stride over vertices / edges (lane v: vertex v and edge (v, v+1));
+// the snapped vertices stay in shared memory (charts of <= 64 vertices; larger
+// ones use the HBM scratch); slice bounds are accumulated with shared-memory
+// atomicMin/Max (commutative, so schedule-independent); reductions are REDUX
+// instructions (64-bit sums as four 16-bit-chunk REDUX sums) or shuffles.  The group size trades
 // per-chart latency (wide groups, few charts) against charts in flight (narrow
 // groups, many small charts): 32 lanes below 4096 charts (a pack of a few
 // thousand charts is latency-bound per chart), 16 below 8192, else 8.
@@ -23,15 +25,17 @@ namespace tabi {
 namespace {
 
 constexpr int kBlock = 256;  // threads per block
+constexpr int kVCap = 64;    // vertices per group kept in shared memory (larger charts: HBM scratch)
 
 // Per-group shared scratch, k slices per axis (sized by k at launch).
 struct Slices {
   int32_t *mlo0, *mlo1, *mhi0, *mhi1;  // x-slices top/bot, y-slices left/right (merged = D4, R7)
   int64_t* ob;                         // [8][4] OBB extents per angle
+  int32_t *vx, *vy;                    // [kVCap] the chart's vertices (nv <= kVCap)
 };
 
 __host__ __device__ constexpr size_t slice_bytes(int k) {
-  return (256 + (size_t)4 * 4 * k + 15) & ~(size_t)15;
+  return (256 + (size_t)4 * 4 * k + (size_t)8 * kVCap + 15) & ~(size_t)15;
 }
 
 template <int G>
@@ -45,60 +49,69 @@ struct Group {
   __device__ int32_t min32(int32_t v) const { return __reduce_min_sync(mask, v); }
   __device__ int32_t max32(int32_t v) const { return __reduce_max_sync(mask, v); }
   __device__ uint32_t sumu(uint32_t v) const { return __reduce_add_sync(mask, v); }
-  __device__ int64_t sum64(int64_t v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v += xorv(v, o);
-    return v;
-  }
-  __device__ i128 sum128(i128 v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-      const uint64_t lo = xorv((uint64_t)v, o), hi = xorv((uint64_t)(v >> 64), o);
-      v += (i128)(((unsigned __int128)hi << 64) | lo);
-    }
-    return v;
+  // 64-bit sum modulo 2^64 from four independent 16-bit-chunk REDUX sums (each
+  // chunk sum < 2^21): exact whenever the true sum fits int64, whatever the
+  // lanes' partial sums did
+  __device__ int64_t sum64_wrap(int64_t v) const {
+    const uint64_t u = (uint64_t)v;
+    const uint64_t c0 = sumu((uint32_t)(u & 0xffffu)), c1 = sumu((uint32_t)((u >> 16) & 0xffffu));
+    const uint64_t c2 = sumu((uint32_t)((u >> 32) & 0xffffu)), c3 = sumu((uint32_t)(u >> 48));
+    return (int64_t)(c0 + (c1 << 16) + (c2 << 32) + (c3 << 48));
   }
 };
 
+// floor(a / e) and the remainder, for 0 <= a <= 2^31, 1 <= e <= 2^25 and a
+// quotient <= 64 (a = k * coordinate, e = the extent): the double estimate
+// from e's reciprocal is off by far less than 1 / e, so truncation gives the
+// quotient or one less, and one exact correction step settles it.
+__device__ __forceinline__ uint32_t strip_div(uint32_t a, uint32_t e, double re, uint32_t& r) {
+  uint32_t q = (uint32_t)((double)a * re);
+  int64_t rr = (int64_t)a - (int64_t)((uint64_t)q * e);
+  if (rr < 0) { q--; rr += e; }
+  else if (rr >= (int64_t)e) { q++; rr -= e; }
+  r = (uint32_t)rr;
+  return q;
+}
+
 // D4: slice bounds along one axis.  A = coordinate that is sliced (x for
-// x-slices), B = the bounded coordinate.  Strip j = closed range k*A in
-// [j*ext, (j+1)*ext].
+// x-slices, in [0, ext]), B = the bounded coordinate.  Strip j = closed range
+// k*A in [j*ext, (j+1)*ext].  Lane v takes vertex v and edge (v, v+1): the
+// vertex updates the strips holding it, the edge its crossings of the strip
+// boundary lines strictly inside it (floored into top, ceiled into bottom).
 template <int G>
 __device__ void accumulate_slices(const Group<G>& g, const int32_t* A, const int32_t* B, int nv,
                                   int64_t ext, int k, int32_t* lo, int32_t* hi) {
-  const double rext = rcp_approx((double)ext);
+  const uint32_t e = (uint32_t)ext;
+  const double re = rcp_approx((double)ext);
   for (int v = g.gl; v < nv; v += G) {
-    int64_t ka = (int64_t)k * A[v];
-    int64_t jh = fdiv_r64(ka, ext, rext);            // floor(k*a/ext), a >= 0
-    int64_t jl = -fdiv_r64(-ka, ext, rext) - 1;      // ceil(k*a/ext) - 1
-    if (jl < 0) jl = 0;
-    if (jh > k - 1) jh = k - 1;
-    for (int64_t j = jl; j <= jh; j++) {
-      if (j * ext <= ka && ka <= (j + 1) * ext) {
-        atomicMin(&lo[j], B[v]);
-        atomicMax(&hi[j], B[v]);
-      }
-    }
-  }
-  for (int v = g.gl; v < nv; v += G) {
-    int a = v, b = (v + 1 == nv) ? 0 : v + 1;
-    int64_t xa = A[a], xb = A[b], ya = B[a], yb = B[b];
-    if (xa == xb) continue;
-    if (xa > xb) {
-      int64_t t = xa; xa = xb; xb = t;
-      t = ya; ya = yb; yb = t;
-    }
-    int64_t L0 = fdiv_r64((int64_t)k * xa, ext, rext) + 1;       // first line strictly right of xa
-    int64_t L1 = -fdiv_r64(-(int64_t)k * xb, ext, rext) - 1;     // last line strictly left of xb
-    if (L0 < 1) L0 = 1;
-    if (L1 > k - 1) L1 = k - 1;
-    for (int64_t L = L0; L <= L1; L++) {
-      int64_t line = L * ext;
-      if (!((int64_t)k * xa < line && line < (int64_t)k * xb)) continue;
-      int64_t num = (line - (int64_t)k * xa) * (yb - ya);
-      int64_t den = (int64_t)k * (xb - xa);
-      int32_t yf = (int32_t)(ya + fdiv_fast(num, den));
-      int32_t yc = (int32_t)(ya + cdiv_fast(num, den));
+    const int u = v + 1 == nv ? 0 : v + 1;
+    const int32_t av = A[v], bv = B[v], au = A[u], bu = B[u];
+    uint32_t rv, ru;
+    const int32_t qv = (int32_t)strip_div((uint32_t)k * (uint32_t)av, e, re, rv);
+    const int32_t qu = (int32_t)strip_div((uint32_t)k * (uint32_t)au, e, re, ru);
+    // closed strips holding vertex v: q (unless q = k) and q - 1 when on a line
+    if (qv <= k - 1) { atomicMin(&lo[qv], bv); atomicMax(&hi[qv], bv); }
+    if (rv == 0 && qv >= 1) { atomicMin(&lo[qv - 1], bv); atomicMax(&hi[qv - 1], bv); }
+    if (av == au) continue;
+    const bool fw = av < au;
+    const int64_t xa = fw ? av : au, xb = fw ? au : av, ya = fw ? bv : bu, yb = fw ? bu : bv;
+    const int32_t qa = fw ? qv : qu, qb = fw ? qu : qv;
+    const uint32_t rb = fw ? ru : rv;
+    // lines L*ext with k*xa < L*ext < k*xb, L in [1, k-1]
+    const int32_t L0 = max(qa + 1, 1);
+    const int32_t L1 = min(rb == 0 ? qb - 1 : qb, k - 1);
+    if (L0 > L1) continue;
+    const int64_t dy = yb - ya, den = (int64_t)k * (xb - xa);
+    const double rd = rcp_approx((double)den);
+    const int64_t kxa = (int64_t)k * xa;
+    for (int32_t L = L0; L <= L1; L++) {
+      // crossing y = ya + (L*ext - k*xa) * dy / den, |num| <= den * 2^25 < 2^57
+      const int64_t num = ((int64_t)L * e - kxa) * dy;
+      int64_t q = (int64_t)floor((double)num * rd);
+      int64_t r = num - q * den;
+      while (r < 0) { q--; r += den; }
+      while (r >= den) { q++; r -= den; }
+      const int32_t yf = (int32_t)(ya + q), yc = yf + (r != 0 ? 1 : 0);
       atomicMin(&lo[L - 1], yf);
       atomicMax(&hi[L - 1], yc);
       atomicMin(&lo[L], yf);
@@ -133,19 +146,22 @@ __device__ __forceinline__ int64_t q30_round(int64_t a) {
   return q;
 }
 
-// D6's minimum-area angle (ties to the smaller j) of the group's polygon:
-// lane = (G / 8) * angle + vertex subgroup; the per-angle extents go through
-// S.ob and lane 0 picks.  Returns the same j in every lane.
+// D6's minimum-area angle (ties to the smaller j) of the group's polygon,
+// reflected on the fly (x -> w - x if fx, y -> h - y if fy): lane = (G / 8) *
+// angle + vertex subgroup; the per-angle extents go through S.ob and lane 0
+// picks.  Returns the same j in every lane.
 template <int G>
 __device__ int obb_angle(const Group<G>& g, const int32_t* X, const int32_t* Y, int nv,
-                         const Slices& S, int nj = 8) {
+                         const Slices& S, int nj = 8, bool fx = false, bool fy = false,
+                         int32_t w = 0, int32_t h = 0) {
   constexpr int VG = G / 8;
   const int j = g.gl / VG, vg = g.gl % VG;
-  const int64_t C = kQC[j], Sn = kQS[j];
+  const int32_t C = (int32_t)kQC[j], Sn = (int32_t)kQS[j];
   int64_t u0 = INT64_MAX, u1 = INT64_MIN, v0 = INT64_MAX, v1 = INT64_MIN;
   for (int v = vg; v < nv; v += VG) {
-    const int64_t x = X[v], y = Y[v];
-    const int64_t u = x * C + y * Sn, vv = -x * Sn + y * C;
+    const int32_t x = fx ? w - X[v] : X[v], y = fy ? h - Y[v] : Y[v];
+    // |x|, |y| <= 2^25, C, Sn <= 2^30: 32 x 32 -> 64-bit products
+    const int64_t u = (int64_t)x * C + (int64_t)y * Sn, vv = (int64_t)y * C - (int64_t)x * Sn;
     u0 = u < u0 ? u : u0; u1 = u > u1 ? u : u1;
     v0 = vv < v0 ? vv : v0; v1 = vv > v1 ? vv : v1;
   }
@@ -208,6 +224,8 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     S.ob = (int64_t*)p;  // 256 B, 8-byte aligned at the group's slot
     int32_t* i32 = (int32_t*)(p + 256);
     S.mlo0 = i32; S.mlo1 = i32 + k; S.mhi0 = i32 + 2 * k; S.mhi1 = i32 + 3 * k;
+    S.vx = i32 + 4 * k;
+    S.vy = S.vx + kVCap;
   }
   const int gl = g.gl;
   const int32_t a0 = start[c];
@@ -223,14 +241,20 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     if (gl == 0) atomicMin(&st->bad_chart, cl);
     return;
   }
-  int32_t* X = qx + a0;
-  int32_t* Y = qy + a0;
+  // the chart's vertices: shared memory when they fit, else the HBM scratch
+  const bool in_smem = nv <= kVCap;
+  int32_t* X = in_smem ? S.vx : qx + a0;
+  int32_t* Y = in_smem ? S.vy : qy + a0;
   // A1 snap: q = round_half_even(x * res * 256), exact product in double (D2)
   bool ok = true;
   int32_t xmn = INT32_MAX, xmx = INT32_MIN, ymn = INT32_MAX, ymx = INT32_MIN;
+  // (one 8-byte load per vertex when the caller's buffer allows it)
+  const bool al8 = ((uintptr_t)xy & 7u) == 0;
+  const float2* xy2 = reinterpret_cast<const float2*>(xy) + a0;
   for (int v = gl; v < nv; v += G) {
-    double fx = (double)xy[2 * (int64_t)(a0 + v)] * (double)rx * 256.0;
-    double fy = (double)xy[2 * (int64_t)(a0 + v) + 1] * (double)ry * 256.0;
+    const float2 p = al8 ? xy2[v] : make_float2(xy[2 * ((int64_t)a0 + v)], xy[2 * ((int64_t)a0 + v) + 1]);
+    double fx = (double)p.x * (double)rx * 256.0;
+    double fy = (double)p.y * (double)ry * 256.0;
     if (!isfinite(fx) || !isfinite(fy) || fabs(fx) > (double)TABI_QMAX ||
         fabs(fy) > (double)TABI_QMAX) {
       ok = false;
@@ -270,32 +294,30 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   xmn = g.min32(xmn); xmx = g.max32(xmx);
   ymn = g.min32(ymn); ymx = g.max32(ymx);
   int64_t w = (int64_t)xmx - xmn, h = (int64_t)ymx - ymn;
-  g.sync();
-  for (int v = gl; v < nv; v += G) { X[v] -= xmn; Y[v] -= ymn; }
-  g.sync();
-  // D3 shoelace (2 x area), exact
-  i128 s2 = 0;
+  // D3 90-degree normalization, (x, y) -> (h - y, x) iff w > h, folded into
+  // the translation of the AABB to the origin (one pass; each lane rewrites
+  // only its own vertices)
+  const bool rot = w > h;
   for (int v = gl; v < nv; v += G) {
-    int u = (v + 1 == nv) ? 0 : v + 1;
-    s2 += (i128)((int64_t)X[v] * Y[u] - (int64_t)X[u] * Y[v]);
+    const int32_t x = X[v] - xmn, y = Y[v] - ymn;
+    X[v] = rot ? (int32_t)(h - y) : x;
+    Y[v] = rot ? x : y;
   }
-  s2 = g.sum128(s2);
+  if (rot) { const int64_t t = w; w = h; h = t; }
+  g.sync();
+  // D3 shoelace (2 x area), exact: |x|, |y| <= 2^25, so each term fits int64
+  // and the sum (|2A| <= 2^51) is exact modulo 2^64; a rotation keeps |area|
+  int64_t s2 = 0;
+  for (int v = gl; v < nv; v += G) {
+    const int u = (v + 1 == nv) ? 0 : v + 1;
+    s2 += (int64_t)X[v] * Y[u] - (int64_t)X[u] * Y[v];
+  }
+  s2 = g.sum64_wrap(s2);
   if (s2 < 0) s2 = -s2;
   if (s2 == 0) {
     if (gl == 0) atomicMin(&st->bad_chart, cl);
     return;
   }
-  // D3 90-degree normalization: (x, y) -> (h - y, x) iff w > h
-  const bool rot = w > h;
-  if (rot) {
-    for (int v = gl; v < nv; v += G) {
-      int32_t nx = (int32_t)(h - Y[v]), ny = X[v];
-      X[v] = nx;
-      Y[v] = ny;
-    }
-    int64_t t = w; w = h; h = t;
-  }
-  g.sync();
   // D4/D5 in the normalized pose, D7 orientation
   merged_slices(g, S, X, Y, nv, w, h, k);
   // empty-area sums: every term is in [0, 2^25] and k <= 64, so the sums fit
@@ -310,23 +332,23 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   const int64_t TOP = g.sumu(top), BOT = g.sumu(bot);
   const int64_t LEFT = g.sumu(left), RIGHT = g.sumu(right);
   const bool fy = TOP > BOT;
-  const int64_t D = LEFT - RIGHT;
+  const int64_t D = LEFT - RIGHT;  // |10 D| < 2^35, k w <= 2^31: int64
   bool fx;
-  if ((i128)10 * D > (i128)k * w) {
+  if (10 * D > (int64_t)k * w) {
     fx = true;
-  } else if ((i128)10 * (-D) > (i128)k * w) {
+  } else if (10 * (-D) > (int64_t)k * w) {
     fx = false;
   } else {
-    int64_t BL2 = 0, BR2 = 0;
+    // bottom-left vs bottom-right (D7): BL2 = 2 S_L + mid, BR2 = 2 S_R + mid
+    // with the odd-k middle slice split 50/50, so BL2 > BR2 iff S_L > S_R
+    // (each a sum of < 32 gaps <= 2^25: 32 bits)
+    uint32_t sl = 0, sr = 0;
     for (int j = gl; j < k; j += G) {
-      int64_t gap = fy ? S.mlo0[j] : (h - S.mhi0[j]);
-      if (2 * j + 1 < k) BL2 += 2 * gap;
-      else if (2 * j + 1 > k) BR2 += 2 * gap;
-      else { BL2 += gap; BR2 += gap; }
+      const uint32_t gap = (uint32_t)(fy ? S.mlo0[j] : (h - S.mhi0[j]));
+      if (2 * j + 1 < k) sl += gap;
+      else if (2 * j + 1 > k) sr += gap;
     }
-    BL2 = g.sum64(BL2);
-    BR2 = g.sum64(BR2);
-    fx = BL2 > BR2;
+    fx = g.sumu(sl) > g.sumu(sr);
   }
   // D8 final pose.  The slices of the reflected chart are the reflected
   // slices: x -> w - x maps x-strip j to strip k-1-j (closed strips, the same
@@ -334,12 +356,8 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   // commutes with both maps.  So the final-pose merged slices are an index
   // mirror plus a value reflection of the ones just computed -- no second
   // slicing pass (tests compare every slice with the oracle, which re-slices).
+  // The vertices are reflected on the fly by the OBB pass below.
   if (fx || fy) {
-    g.sync();
-    for (int v = gl; v < nv; v += G) {
-      if (fx) X[v] = (int32_t)(w - X[v]);
-      if (fy) Y[v] = (int32_t)(h - Y[v]);
-    }
     constexpr int U = TABI_KMAX / G;  // slices per lane (k <= 64)
     int32_t t0[U], b0[U], l1[U], r1[U];
 #pragma unroll
@@ -370,13 +388,14 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
     sl[2 * k + j] = S.mlo1[j];
     sl[3 * k + j] = S.mhi1[j];
   }
-  // D6 OBB: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles, ties -> smaller j.
-  g.sync();
-  const int bj = obb_angle(g, X, Y, nv, S, (flags & TABI_F_NO_OBB) ? 1 : 8);
+  // D6 OBB of the final pose: minimum (Umax-Umin)(Vmax-Vmin) over 8 angles,
+  // ties -> smaller j
+  const int bj = obb_angle(g, X, Y, nv, S, (flags & TABI_F_NO_OBB) ? 1 : 8, fx, fy, (int32_t)w,
+                           (int32_t)h);
   if (gl == 0) {
     P.w[c] = (int32_t)w;
     P.h[c] = (int32_t)h;
-    P.area2[c] = (int64_t)s2;
+    P.area2[c] = s2;
     P.xmin[c] = xmn;
     P.ymin[c] = ymn;
     P.pose[c] = (uint8_t)((rot ? 1 : 0) | (fx ? 2 : 0) | (fy ? 4 : 0));

@@ -391,23 +391,39 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
   __shared__ int32_t sh[2][kW + 1];
   __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
+  __shared__ int32_t ext_max[2][kW];
   // Area bound on the candidate scales: the packed charts are disjoint and
   // inside the atlas, so (m/M)^2 * sum(area) <= W*H for any candidate that can
   // succeed; in units (2*area, 1/256 texel): m^2 * A2 <= 2 * 65536 * W * H * M^2.
   {
     i128 a = 0;
-    for (int i = threadIdx.x; i < pp.n; i += kT) a += area2[i];
+    int32_t wm = 0, hm = 0;
+    for (int i = threadIdx.x; i < pp.n; i += kT) {
+      a += area2[i];
+      wm = max(wm, ww[i]);
+      hm = max(hm, hh[i]);
+    }
     a = warp_sum128(a);
+    wm = warp_max(wm);
+    hm = warp_max(hm);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (lane == 0) {
       asum[0][wid] = (unsigned long long)(uint64_t)a;
       asum[1][wid] = (unsigned long long)(uint64_t)(a >> 64);
+      ext_max[0][wid] = wm;
+      ext_max[1][wid] = hm;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       i128 tot = 0;
-      for (int w = 0; w < kW; w++)
+      int32_t wmx = 0, hmx = 0;
+      for (int w = 0; w < kW; w++) {
         tot += (i128)(((unsigned __int128)asum[1][w] << 64) | asum[0][w]);
+        wmx = max(wmx, ext_max[0][w]);
+        hmx = max(hmx, ext_max[1][w]);
+      }
+      st->wmax = wmx;
+      st->hmax = hmx;
       const i128 rhs = (i128)2 * 65536 * pp.W * pp.H * (i128)pp.M * pp.M;
       int m_hi = 0;
       for (int m = pp.M; m >= 1; m--)
@@ -484,14 +500,14 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
     // +4: the TMA bulk copy of a row window rounds its end up to 16 bytes
     if ((int64_t)carry_c + 4 > pp.col_cap || (int64_t)carry_r + 4 > pp.row_cap) st->capacity |= 1;
   }
-  if (rdy) {  // fused wave 0: the ready flags, arrival counters and completed-tile
-              // counts of the T tiles (the reset kernel leaves them to us)
+  if (rdy) {  // fused wave 0: the ready flags, arrival counters, completed-tile
+              // counts and failed flags of the T tiles (the reset kernel leaves them to us)
     const int64_t bt = (int64_t)pp.B * carry_t, bn = (int64_t)pp.B * pp.n;
     for (int64_t q = threadIdx.x; q < bt; q += kT) {
       rdy[q] = 0;
       rdy[bn + q] = 0;
     }
-    for (int q = threadIdx.x; q < pp.B; q += kT) rdy[2 * bn + q] = 0;
+    for (int q = threadIdx.x; q < 2 * pp.B; q += kT) rdy[2 * bn + q] = 0;
   }
 }
 

@@ -296,7 +296,7 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
     CK(dalloc(&ctx->cand_bad, (size_t)M));
     CK(dalloc(&ctx->big_list, (size_t)M * N));
     // ready flags + boundary arrival counters + per-slot completed-tile counts
-    CK(dalloc(&ctx->rdy, 2 * (size_t)M * N + (size_t)M));
+    CK(dalloc(&ctx->rdy, 2 * (size_t)M * N + 2 * (size_t)M));
     ctx->fstride = ((ctx->max_side + 2 * 64 + 4) + 31) & ~31;
     CK(dalloc(&ctx->t_state, (size_t)M));
     CK(dalloc(&ctx->t_r0, (size_t)M));
@@ -509,8 +509,9 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
                      fused_fits(pp.k);
   if (info) info->fused = fused ? 1 : 0;
   ctx->last_fused = fused ? 1 : 0;
-  // ready flags + arrival counters + per-slot completed-tile counts
-  const int64_t nrdy = fused ? 2 * (int64_t)B * n + B : 0;
+  // ready flags + arrival counters + per-slot completed-tile counts + per-slot
+  // "failed" flags (rasterizers drop a failed candidate's remaining tiles)
+  const int64_t nrdy = fused ? 2 * (int64_t)B * n + 2 * B : 0;
 
   tabi_placement* d_out = on_device ? out : ctx->d_out;
   const int64_t V_in = on_device ? 0 : (int64_t)chart_start[n];

@@ -321,6 +321,9 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t ntiles;     // fused kernel: raster tiles (prep_kernel)
   int32_t win_j;      // fused, sequential mode: smallest wave slot that succeeded
   int32_t b0;         // wave 0's candidate slots in use (prep_kernel; <= B)
+  int32_t wmax, hmax; // largest chart width / height (units; prep_kernel): a
+                      // candidate whose scaled largest chart exceeds the dilated
+                      // atlas fails at once (cand_too_big)
   unsigned long long work_pack;  // K4 frontline column visits (push + score + commit)
   unsigned long long work_prof;  // K3 footprint entries (sum over candidates of Wd + Hd)
   unsigned long long atot_lo, atot_hi;  // total 2 x area (int128) for D25 / D26
@@ -396,6 +399,16 @@ __host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_h
   if (pp.wave == 0 && j >= b0) return 0;
   const int m = m_hi - (pp.wave == 0 ? 0 : b0 + (pp.wave - 1) * pp.B) - j;
   return m >= 1 ? m : 0;
+}
+
+// Does candidate m's largest chart exceed the dilated atlas?  The rasterizers'
+// per-chart test (cand_bad: ceil(w m / (M 256)) + 2g > W' or the same for h)
+// on the largest width and height, which decides it for every chart.
+__device__ __forceinline__ bool cand_too_big(const PackParams& pp, const Status* st, int m) {
+  const int64_t SC = (int64_t)pp.M * TABI_UNITS;
+  const int64_t ws = ((int64_t)st->wmax * m + SC - 1) / SC;
+  const int64_t hs = ((int64_t)st->hmax * m + SC - 1) / SC;
+  return ws + 2 * pp.g > pp.Wp || hs + 2 * pp.g > pp.Hp;
 }
 
 }  // namespace tabi

@@ -18,8 +18,10 @@ os.environ["TABI_TIMING"] = "1"
 ctx = Context(0, max_charts=25000, max_vertices=1 << 21, max_atlas_side=16384)
 us = lambda v: round(v / 1000, 1)  # noqa: E731
 only = os.environ.get("TRACE_MODES", "1,0").split(",")
-for name, cs in (("C3", chartgen.config3(0, rho=0.5)), ("C2", chartgen.config2(0)),
-                 ("C4", chartgen.config4(0, t_opt_bp=0))):
+SETS = {"C3": lambda: chartgen.config3(0, rho=0.5), "C3r15": lambda: chartgen.config3(0, rho=1.5),
+        "C2": lambda: chartgen.config2(0), "C4": lambda: chartgen.config4(0, t_opt_bp=0)}
+for name in os.environ.get("TRACE_SETS", "C3,C2,C4").split(","):
+    cs = SETS[name]()
     for f in only:
         os.environ["TABI_FUSED"] = f
         for _ in range(3):

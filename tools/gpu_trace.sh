@@ -1,7 +1,12 @@
-# fused-kernel trace for raster group counts 1, 2, 4 (stage + timeline only)
-mkdir -p gpurun_out
-for RG in 1 2 4; do
-  TABI_NVCC_EXTRA="-DTABI_FUSED_RG=$RG" python -c "from paper_2602_07782_b200 import build as b; b.build(force=True)" > gpurun_out/build_rg$RG.log 2>&1
-  echo "=== RG=$RG"
-  TRACE_MODES=1 timeout 300 python tools/fused_trace.py 2>&1 | sed 's/rows.*//'
-done
+# K4 row-phase trace (a -DTABI_PHASE_TRACE build) of the winner's chain alone
+# (one candidate per wave) and with the default waves.
+#   bash tools/gpu_trace.sh [sets] [out]      sets: comma list of C3,C3r15,C2,C4
+S=${1:-C3r15,C3}
+O=${2:-gpurun_out/trace}
+mkdir -p $O
+TABI_NVCC_EXTRA=-DTABI_PHASE_TRACE python -c "from paper_2602_07782_b200 import build as b; b.build(force=True)" > $O/build_trace.log 2>&1
+echo "== TABI_WAVE=1"
+TABI_WAVE=1 TRACE_SETS=$S TRACE_MODES=1 timeout 300 python tools/fused_trace.py 2>&1 | tee $O/trace_wave1.txt
+echo "== default waves"
+TRACE_SETS=$S TRACE_MODES=1 timeout 300 python tools/fused_trace.py 2>&1 | tee $O/trace_default.txt
+python -c "from paper_2602_07782_b200 import build as b; b.build(force=True)" > $O/build.log 2>&1

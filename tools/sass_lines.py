@@ -56,7 +56,7 @@ def main():
         if m:
             fn = m.group(1)
             continue
-        if fn is None or kname not in fn:
+        if fn is None or (os.environ.get("MANGLED", kname)) not in fn:
             continue
         m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
         if m:
