@@ -9,6 +9,10 @@ namespace k3 {
 
 constexpr int kRaw = 8192;   // raw cells per chunk (32 KB)
 constexpr int kDilMax = 2;   // gutters up to this use the fused raster + dilation pass
+#ifndef TABI_RUN_MIN
+#define TABI_RUN_MIN 1
+#endif
+constexpr int kRunMin = TABI_RUN_MIN | 1;  // shortest dilated-output run per thread
 // Per-(chart, candidate) constants.  OBB index q = axis * 2 + (0 low, 1 high);
 // lines lin[axis * 4 + kind]: kind 0 low-bound line right of the crossing
 // (at the cell's low edge), 1 low-bound line left of it (high edge, non-last
@@ -37,6 +41,7 @@ __device__ __forceinline__ void slice_job(int32_t* tab, const int32_t* blo, cons
   tab[2 * j] = (int32_t)fdiv_r64(num * blo[j], SC, rSC);
   tab[2 * j + 1] = (int32_t)(-fdiv_r64(-num * bhi[j], SC, rSC));
 }
+
 
 // OBB job r (0..7) of a chart: LinDiv r, one of last/star, one of iA/iB.  The
 // box is {Umin <= xC + yS <= Umax, Vmin <= -xS + yC <= Vmax}; with num/SC:
@@ -338,7 +343,8 @@ struct RawIter {
 // << 16, so one per-halfword minimum (vminu2) takes both bounds.
 template <int GMAX>
 __device__ __forceinline__ void dil_run(const ChartK3& H, const int32_t* tab, int k, int ax,
-                                        int32_t o0, int32_t len, int64_t SC, int g, uint32_t* dst) {
+                                        int32_t o0, int32_t len, int64_t SC, int g, uint32_t* dst,
+                                        uint32_t* dst2 = nullptr) {
   constexpr int WN = 2 * GMAX + 1;
   const int32_t n0 = ax ? H.hs : H.ws;
   RawIter it;
@@ -360,7 +366,9 @@ __device__ __forceinline__ void dil_run(const ChartK3& H, const int32_t* tab, in
 #pragma unroll
       for (int u = WN - 2; u >= 0; u--)
         if (WN - 1 - u <= 2 * g) m = __vminu2(m, win[u]);
-      dst[q - o0] = (m & 0xffffu) | ((0xffffu - (m >> 16) + 2 * g) << 16);
+      const uint32_t val = (m & 0xffffu) | ((0xffffu - (m >> 16) + 2 * g) << 16);
+      dst[q - o0] = val;
+      if (dst2) dst2[q - o0] = val;
     }
   }
 }
@@ -425,7 +433,8 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
                             int32_t* cand_bad, int slot, int s0, Scale sc, ChartK3* CH,
                             int32_t* cells, int32_t* cpre, int32_t* opre, int32_t* chunk_end,
                             int32_t* big, int32_t* tabs, uint32_t* raw, int nt, int tid,
-                            Sync sync, Mark setup_done = Mark()) {
+                            Sync sync, Mark setup_done = Mark(), uint32_t* rstash = nullptr,
+                            int32_t rstash_cap = 0) {
   const int k = pp.k, g = pp.g;  // tile = sorted positions [s0, s0 + nt), nt <= TC
   const int64_t num = sc.num, SC = sc.SC;
   const double rSC = rcp_approx((double)SC);
@@ -472,27 +481,38 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
   if (g <= kDilMax) {
     // fused raster + dilation (dil_run): no raw buffer, every fitting chart of
     // the tile in one pass over its flattened dilated outputs (Wd + Hd each)
+    // (with rstash: cpre = the prefix of the dilated row counts, and each
+    // chart's row outputs also go to rstash + cpre[ci] -- the caller's pair
+    // offsets then read shared memory; only if they all fit rstash_cap)
     if (tid < 32) {
       const int lane = tid;
-      int e = 0, otot = 0;
-      if (lane == 0) opre[0] = 0;
+      int e = 0, otot = 0, rtot = 0;
+      if (lane == 0) { opre[0] = 0; cpre[0] = 0; }
       for (; e < nt; e += 32) {
         const int idx = e + lane;
-        int io = (idx < nt && CH[idx].small) ? CH[idx].ws + CH[idx].hs + 4 * g : 0;
+        const bool sm = idx < nt && CH[idx].small;
+        int io = sm ? CH[idx].ws + CH[idx].hs + 4 * g : 0;
+        int ir = sm ? CH[idx].hs + 2 * g : 0;
         // (the pass covers fitting charts only; big[] stays 0 on this path)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int b = __shfl_up_sync(0xffffffffu, io, o);
-          if (lane >= o) io += b;
+          const int br = __shfl_up_sync(0xffffffffu, ir, o);
+          if (lane >= o) { io += b; ir += br; }
         }
-        if (idx < nt) opre[idx + 1] = otot + io;
+        if (idx < nt) { opre[idx + 1] = otot + io; cpre[idx + 1] = rtot + ir; }
         otot += __shfl_sync(0xffffffffu, io, 31);
+        rtot += __shfl_sync(0xffffffffu, ir, 31);
       }
     }
     sync();
     setup_done(1);
+    if (rstash && cpre[nt] > rstash_cap) rstash = nullptr;  // (uniform)
     const int32_t nout = opre[nt];
-    const int32_t R = ((nout + TT - 1) / TT) | 1;
+    // run length per thread (odd: the runs' stores hit distinct banks); each
+    // run pays one iterator start, so short runs spend most of their
+    // instructions there
+    const int32_t R = max(((nout + TT - 1) / TT) | 1, kRunMin);
     int32_t e = tid * R;
     const int32_t e1 = min(nout, e + R);
     if (e < e1) {
@@ -510,7 +530,8 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
         const int32_t o = ax ? y - Wd : y;
         const int32_t len = min(e1 - e, (ax ? H.hs + 2 * g : Wd) - o);
         dil_run<kDilMax>(H, tabs + lo * 4 * k, k, ax, o, len, SC, g,
-                         (ax ? rowb + H.row_o : colb + H.col_o) + o);
+                         (ax ? rowb + H.row_o : colb + H.col_o) + o,
+                         ax && rstash ? rstash + cpre[lo] + o : nullptr);
         e += len;
         while (lo < nt - 1 && opre[lo + 1] <= e) lo++;
       }
@@ -650,6 +671,23 @@ __device__ inline void big_chart(const Proxies& P, const int32_t* __restrict__ p
 // Compaction advance off(s, s+1) and CannotMoveAbove bits of the adjacent
 // pair, by one warp (D14, D15).  The footprint arrays
 // are plain (coherent) loads: in the fused kernel another CTA wrote chart s.
+// The pair from its two dilated row footprints ra, rb (HBM or shared memory)
+// and sizes; stores off and the lock bits at *off_o, *lock_o.
+__device__ __forceinline__ void pair_rows(const uint32_t* ra, const uint32_t* rb, int32_t Hda,
+                                          int32_t Hdb, int32_t Wda, int32_t* off_o, uint8_t* lock_o,
+                                          int lane) {
+  const int rows = min(Hda, Hdb);
+  int32_t off = 0;
+  for (int j = lane; j < rows; j += 32) off = max(off, hi16(ra[j]) - lo16(rb[j]));
+  off = warp_max(off);
+  bool la = false, lb = false;
+  if (off < Wda) warp_locks(ra, rb, Hda, Hdb, off, lane, la, lb);
+  if (lane == 0) {
+    *off_o = off;
+    *lock_o = (uint8_t)((la ? 1 : 0) | (lb ? 2 : 0));
+  }
+}
+
 __device__ __forceinline__ void pair_offset(const PackParams& pp, const int32_t* __restrict__ rowofs,
                                             const uint32_t* drow, const int32_t* wd_all,
                                             const int32_t* hd_all, int32_t* off_all,
@@ -662,16 +700,7 @@ __device__ __forceinline__ void pair_offset(const PackParams& pp, const int32_t*
   const int32_t Hda = hd_all[base + s], Hdb = hd_all[base + s + 1], Wda = wd_all[base + s];
   const uint32_t* ra = drow + (int64_t)slot * pp.row_cap + rowofs[s];
   const uint32_t* rb = drow + (int64_t)slot * pp.row_cap + rowofs[s + 1];
-  const int rows = min(Hda, Hdb);
-  int32_t off = 0;
-  for (int j = lane; j < rows; j += 32) off = max(off, hi16(ra[j]) - lo16(rb[j]));
-  off = warp_max(off);
-  bool la = false, lb = false;
-  if (off < Wda) warp_locks(ra, rb, Hda, Hdb, off, lane, la, lb);
-  if (lane == 0) {
-    off_all[base + s] = off;
-    lock_all[base + s] = (uint8_t)((la ? 1 : 0) | (lb ? 2 : 0));
-  }
+  pair_rows(ra, rb, Hda, Hdb, Wda, off_all + base + s, lock_all + base + s, lane);
 }
 
 // pair_offset for a pair with many shared rows, by a whole group of TT

@@ -248,7 +248,7 @@ __device__ __noinline__ int lazy_tiles(const LazyRaster& lz, const PackParams& p
                                        const int32_t* __restrict__ rowofs, uint32_t* dcol,
                                        uint32_t* drow, int32_t* wd, int32_t* hd, int32_t* off,
                                        uint8_t* lock, int slot, int done, int target,
-                                       unsigned char* scratch) {
+                                       unsigned char* scratch, int32_t scratch_words) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, n = pp.n;
   unsigned char* p = scratch;  // the packer's staging buffer (idle until the last tile)
   k3::ChartK3* CH = (k3::ChartK3*)carve(p, sizeof(k3::ChartK3) * kLzTC);
@@ -258,18 +258,33 @@ __device__ __noinline__ int lazy_tiles(const LazyRaster& lz, const PackParams& p
   int32_t* big = (int32_t*)carve(p, 4 * kLzTC);
   int32_t* misc = (int32_t*)carve(p, 32);
   int32_t* tabs = (int32_t*)carve(p, (size_t)4 * kLzTC * 4 * pp.k);
+  // the rest of the staging buffer holds a tile's dilated row footprints, so
+  // its internal pairs read shared memory (g <= kDilMax)
+  uint32_t* rstash = (uint32_t*)p;
+  const int32_t rcap = scratch_words - (int32_t)((p - scratch) / 4);
+  const bool stash = pp.g <= k3::kDilMax && rcap > 0;
   long long c0 = tid == 0 ? clock64() : 0, cpair = 0;
   while (done < target) {  // (uniform)
     const int s0 = done, nt = min(kLzTC, n - s0);
     k3::tile_raster<kLzTC, kPT, 1>(lz.P, lz.perm, pp, colofs, rowofs, dcol, drow, wd, hd, lz.cbad,
                                    slot, s0, lz.sc, CH, cells, cpre, opre, &misc[1], big, tabs,
-                                   nullptr, nt, tid, [] { pk_sync(); });
+                                   nullptr, nt, tid, [] { pk_sync(); }, k3::NoMark(),
+                                   stash ? rstash : nullptr, rcap);
+    const bool stashed = stash && cpre[nt] <= rcap;
     if (tid < nt) lz.area[s0 + tid] = lz.P.area2[lz.perm[s0 + tid]];
     // pairs (s, s + 1) that end in this tile, and the last chart's zero entry
     const long long cp = tid == 0 ? clock64() : 0;
     const int plo = max(0, s0 - 1), phi = s0 + nt == n ? n - 1 : s0 + nt - 2;
-    for (int q = plo + wid; q <= phi; q += kPW)
-      k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, slot, q, lane);
+    for (int q = plo + wid; q <= phi; q += kPW) {
+      const int a = q - s0;
+      if (stashed && a >= 0 && a + 1 < nt && CH[a].small && CH[a + 1].small) {
+        const int64_t b = (int64_t)slot * n + q;
+        k3::pair_rows(rstash + cpre[a], rstash + cpre[a + 1], CH[a].hs + 2 * pp.g,
+                      CH[a + 1].hs + 2 * pp.g, CH[a].ws + 2 * pp.g, off + b, lock + b, lane);
+      } else {
+        k3::pair_offset(pp, rowofs, drow, wd, hd, off, lock, slot, q, lane);
+      }
+    }
     pk_sync();
     if (tid == 0) cpair += clock64() - cp;
     done = s0 + nt;
@@ -555,7 +570,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       const int done = lazy_tiles(*lz, pp, colofs, rowofs, (uint32_t*)dcol, (uint32_t*)drow,
                                   (int32_t*)wd_all, (int32_t*)hd_all, (int32_t*)off_all,
                                   (uint8_t*)lock_all, slot, S.r_done, target,
-                                  (unsigned char*)W.prof);
+                                  (unsigned char*)W.prof, W.prof_cap);
       if (tid == 0) S.r_done = done;
       pk_sync();
       return done >= n ? n - 1 : done - 2;
@@ -1322,10 +1337,11 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
 // groups per SM hide the latency of one group's setup / barrier phases the
 // way several resident CTAs do in the split kernels.
 #ifndef TABI_TOP_FIRST
-#define TABI_TOP_FIRST 1
+#define TABI_TOP_FIRST 0
 #endif
-// sequential mode: the top candidate's tiles before the others' (0: tile-major
-// for every slot, as in hybrid mode)
+// sequential mode: 1 queues the top candidate's tiles before the others'; 0
+// (default) tile-major for every slot, as in hybrid mode -- the top
+// candidate often fails (C3 at rho 1.5: 0.303 -> 0.292 ms)
 constexpr bool kTopFirst = TABI_TOP_FIRST != 0;
 constexpr int kRG = kFusedGroups;   // raster groups per CTA
 constexpr int kRGT = kNT / kRG;     // threads per group (8 per chart in setup)
@@ -1423,11 +1439,14 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   // trip before the first -- most urgent -- tiles); the queue hands out the rest
   const int G = ((int)gridDim.x - Bw) * kRG;
   int first_it = ((int)blockIdx.x - Bw) * kRG + grp;
+  int next_it = -1;  // (leader) an item claimed during the previous tile's pair phase
   while (true) {
     // (fetching the next item ahead would hide this round trip, but lets a
     // busy CTA sit on an early tile the packers are waiting for)
     if (gt == 0) {
-      const int it0 = first_it >= 0 ? first_it : G + atomicAdd(&st->work_next, 1);
+      const int it0 = first_it >= 0 ? first_it
+                      : next_it >= 0 ? next_it : G + atomicAdd(&st->work_next, 1);
+      next_it = -1;
       misc[0] = it0;
       // drop items of a candidate that failed (its packer has exited), and in
       // sequential mode of candidates below a successful one (decided once, by
@@ -1452,10 +1471,10 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 #endif
       break;
     }
-    // sequential mode: the highest candidate's tiles first (it wins whenever
-    // it succeeds), then the other candidates tile-major; items of a candidate
-    // below a successful one are dropped (its packer exits too).  Hybrid mode:
-    // tile-major for all.
+    // Tile-major over the wave's slots (kTopFirst: in sequential mode the
+    // highest candidate's tiles first, then the others tile-major); items of
+    // a failed candidate, or of one below a successful one, are dropped (its
+    // packer has exited).
     int t, j;
     if (!(kTopFirst && pp.early) || Bw == 1) {
       t = it / Bw;
@@ -1472,6 +1491,9 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
     if (m == 0) continue;
     const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
     const k3::Scale sc{m, SCm, 0};
+    // (g <= kDilMax: the raw buffer is free and holds the tile's dilated row
+    // footprints for its internal pair offsets)
+    const bool stash = pp.g <= k3::kDilMax;
     k3::tile_raster<kTCF, kRGT, kRawF>(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd,
                                        ra.hd, ra.cand_bad, m - 1, s0, sc, CH, cells, cpre, opre,
                                        &misc[1], big, tabs, raw, nt, gt, gsync,
@@ -1481,7 +1503,9 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
                                          if (gt == 0 && t == 0 && j == 0)
                                            st->tfirst[w == 0 ? 5 : 4] = gtime();
 #endif
-                                       });
+                                       },
+                                       stash ? raw : nullptr, kRawF);
+    const bool stashed = stash && cpre[nt] <= kRawF;
     rmark(1);
 #ifdef TABI_PHASE_TRACE
     if (gt == 0 && t == 0 && j == 0) atomicMax(&st->tfirst[0], gtime());
@@ -1515,6 +1539,8 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       misc[2 + gt] = ours;
       if (gt == 0) atomicAdd(&st->tr[5], 1ull);
     }
+    // claim the next item now: its queue round trip overlaps the pair offsets
+    if (gt == 0) next_it = G + atomicAdd(&st->work_next, 1);
     gsync();
     rmark(3);
 #ifdef TABI_PHASE_TRACE
@@ -1534,10 +1560,23 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       const int32_t hb = s + 1 < s0 + nt ? CH[s + 1 - s0].hs : ra.hd[b + s + 1] - 2 * pp.g;
       return min(ha, hb) >= 512;
     };
-    for (int s = lo + gw; s <= hi; s += kRGW)
-      if (!big_pair(s))
+    // (only tiles of fewer than kRGW / 2 charts can hold a big pair: the test
+    // is skipped for the rest -- it used to cost every thread a loop over all
+    // of the tile's pairs)
+    const bool may_big = 2 * nt <= kRGW;
+    for (int s = lo + gw; s <= hi; s += kRGW) {
+      if (may_big && big_pair(s)) continue;
+      const int a = s - s0;
+      if (stashed && a >= 0 && a + 1 < nt && CH[a].small && CH[a + 1].small) {
+        // both charts in this tile: their row footprints from shared memory
+        const int64_t b = (int64_t)(m - 1) * pp.n + s;
+        k3::pair_rows(raw + cpre[a], raw + cpre[a + 1], CH[a].hs + 2 * pp.g, CH[a + 1].hs + 2 * pp.g,
+                      CH[a].ws + 2 * pp.g, ra.off + b, ra.lock + b, lane);
+      } else {
         k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s, lane);
-    for (int s = lo; s <= hi; s++)
+      }
+    }
+    for (int s = lo; s <= hi && may_big; s++)
       if (big_pair(s))
         k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s, gt,
                                     gsync, red);
