@@ -31,7 +31,8 @@ typedef enum {
   TABI_EINVAL = 1,      /* bad spec or chart (info->bad_chart names the chart) */
   TABI_NO_FIT = 2,      /* no candidate scale packs: out untouched     */
   TABI_ECUDA = 3,       /* CUDA runtime failure; see tabi_last_error()         */
-  TABI_ECAPACITY = 4    /* input larger than the context was created for      */
+  TABI_ECAPACITY = 4,   /* input larger than the context was created for      */
+  TABI_PENDING = 5      /* tabi_pack_query: the asynchronous pack is still running */
 } tabi_status;
 
 enum {
@@ -134,7 +135,10 @@ void tabi_ctx_destroy(tabi_ctx* ctx);
  *   on_device   0: xy, chart_start, out are host pointers; the call copies in, runs,
  *               copies out and returns when `out`/`info` are final.
  *               1: xy, chart_start, out are device pointers; the call still returns
- *               after completion (info needs the winner) but does no bulk copies.
+ *               after completion (info needs the winner) but does no bulk copies
+ *               (tabi_pack_async returns after enqueueing).
+ * The whole scale search (every candidate wave) is one CUDA-graph launch with a
+ * device-side wave loop and a single host synchronisation.
  *   stream      cudaStream_t to run on, or NULL for the context's own (non-blocking)
  *               stream; cudaStreamLegacy orders the call with the legacy default stream.
  * Ownership: the caller owns every pointer; nothing is retained after return.
@@ -142,6 +146,33 @@ void tabi_ctx_destroy(tabi_ctx* ctx);
 tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
                       int32_t n_charts, float res_x, float res_y, const tabi_spec* spec,
                       tabi_placement* out, tabi_info* info, int on_device, void* stream);
+
+/* Asynchronous pack (SURVEY §8(b) "returns after enqueueing, completion is
+ * stream-ordered"): the same pack as tabi_pack with on_device = 1, enqueued on
+ * `stream` as ONE CUDA graph launch -- the proxies, the sort, every candidate
+ * wave of the scale search (a WHILE node whose body ends in a device-side
+ * decision, so no host round trip between waves) and the result copy --
+ * and returns without waiting.  xy, chart_start and out are device pointers;
+ * the caller keeps them valid and unmodified until tabi_pack_wait returns.
+ * `out` is final once the stream passes the pack (when the pack succeeds);
+ * status and statistics come from tabi_pack_wait.  One pack per context may be
+ * in flight; use several contexts to overlap packs.  Errors found before
+ * enqueueing (bad spec, capacity, CUDA) are returned at once and nothing is
+ * pending; TABI_EINVAL also if TABI_GRAPH=0 or TABI_TIMING=1 is set. */
+tabi_status tabi_pack_async(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                            int32_t n_charts, float res_x, float res_y, const tabi_spec* spec,
+                            tabi_placement* out, void* stream);
+/* Wait for the context's pending asynchronous pack and return its status
+ * (TABI_OK, TABI_NO_FIT, TABI_EINVAL with info->bad_chart, ...) with `info` as
+ * tabi_pack fills it.  If the device-side capacity check failed (footprint
+ * slots or lock-pair lists larger than the context's buffers), the buffers grow
+ * and the pack re-runs synchronously from the same arguments.  TABI_EINVAL if
+ * nothing is pending. */
+tabi_status tabi_pack_wait(tabi_ctx* ctx, tabi_info* info);
+/* Non-blocking completion check of the pending asynchronous pack: TABI_PENDING
+ * while its device work runs, TABI_OK once tabi_pack_wait would not block,
+ * TABI_EINVAL if nothing is pending, TABI_ECUDA on a device error. */
+tabi_status tabi_pack_query(tabi_ctx* ctx);
 
 const char* tabi_status_str(tabi_status s);
 const char* tabi_last_error(tabi_ctx* ctx);   /* last CUDA error text, or "" */

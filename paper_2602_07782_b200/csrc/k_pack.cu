@@ -1319,7 +1319,7 @@ pack_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* __
             int32_t* scratch, int64_t pair_cap, int32_t* Xo_all, int32_t* Yo_all, uint8_t* mir_all,
             Cand* cands, Status* st, int32_t prof_cap) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.x);
+  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
   if (m == 0) return;
   packer(pp, colofs, rowofs, dcol, drow, wd_all, hd_all, off_all, lock_all, hsorted, cand_bad,
          scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, m, m - 1, blockIdx.x,
@@ -1390,10 +1390,10 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   const int T = st->ntiles;
   // wave slots in use: prep_kernel narrows wave 0 (Status::b0); the CTAs of
   // unused slots rasterize instead
-  const int Bw = pp.wave == 0 ? st->b0 : pp.B;
+  const int Bw = st->wave == 0 ? st->b0 : pp.B;
   if (threadIdx.x == 0) atomicMin(&st->tr[0], gtime());
   if ((int)blockIdx.x < Bw) {
-    const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.x);
+    const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
     if (m == 0) return;
     packer(pp, colofs, rowofs, ra.dcol, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, hsorted,
            ra.cand_bad, scratch, pair_cap, Xo_all, Yo_all, mir_all, cands, st, prof_cap, m, m - 1,
@@ -1487,7 +1487,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       j = 1 + (it - T) % (Bw - 1);
     }
     if (dropped) continue;
-    const int m = wave_m(pp, m_hi, st->b0, j);
+    const int m = wave_m(pp, st->wave, m_hi, st->b0, j);
     if (m == 0) continue;
     const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
     const k3::Scale sc{m, SCm, 0};
@@ -1842,9 +1842,13 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
                               const int32_t* __restrict__ wd_all,
                               const int32_t* __restrict__ hd_all, const int32_t* __restrict__ Xo,
                               const int32_t* __restrict__ Yo, const uint8_t* __restrict__ mir,
-                              const Cand* __restrict__ cands, tabi_placement* out, Status* st) {
+                              const Cand* __restrict__ cands, tabi_placement* out, Status* st,
+                              cudaGraphConditionalHandle h, int use_h) {
   __shared__ int32_t win, wr0, wp;
-  if (st->bad_chart != INT32_MAX || st->capacity) return;
+  if (st->bad_chart != INT32_MAX || st->capacity) {
+    if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0u);
+    return;
+  }
   // Without a prefix tail anywhere V (below) is increasing in m, so the
   // winner is the largest successful m: one parallel pass (thread m - 1 reads
   // its candidate's two flags) and a shared max -- no serial loop, no int128.
@@ -1886,7 +1890,28 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
   }
   __syncthreads();
   const int32_t m = win;
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->winner = m;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->winner = m;
+    // Device-side candidate-wave loop (a CUDA-graph WHILE node whose body is
+    // the next wave, so a multi-wave scale search has no host round trip):
+    // continue while an unevaluated lower candidate could still win.
+    // Sequential mode: any success ends the search (the largest successful m
+    // wins).  Hybrid mode (D25): a lower m can win only if its V(m) <= A_tot m
+    // 2^20 (p <= m 2^20 / M) can exceed the best V found.
+    if (use_h) {
+      const int next_m = st->pad[2] - (st->b0 + st->wave * pp.B);  // top of the next wave
+      bool go = next_m >= 1 && st->wave < pp.M;
+      if (go && m > 0) {
+        const i128 Atot = (i128)(((unsigned __int128)st->atot_hi << 64) | st->atot_lo);
+        const Cand& c = cands[m - 1];
+        const bool tail = c.switched_at >= 0;
+        const i128 Ap = tail ? (i128)(((unsigned __int128)c.apre_hi << 64) | c.apre_lo) : 0;
+        const i128 bestV = (Atot - Ap) * m * ((i128)1 << 20) + Ap * c.p * pp.M;
+        if (Atot * next_m * ((i128)1 << 20) <= bestV) go = false;
+      }
+      cudaGraphSetConditional(h, go ? 1u : 0u);
+    }
+  }
   if (m == 0) return;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= pp.n) return;
@@ -2014,9 +2039,11 @@ cudaError_t launch_many(int grid, const PackParams& pp, const ManyArgs& a, cudaS
 
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
-                   const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s) {
+                   const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s,
+                   cudaGraphConditionalHandle h, int use_h) {
   const int blocks = (pp.n + 255) / 256;
-  select_kernel<<<blocks, 256, 0, s>>>(pp, perm, P.pose, P.prerot, wd, hd, X, Y, mir, cands, out, st);
+  select_kernel<<<blocks, 256, 0, s>>>(pp, perm, P.pose, P.prerot, wd, hd, X, Y, mir, cands, out, st,
+                                       h, use_h);
 }
 
 }  // namespace tabi

@@ -56,7 +56,7 @@ profile_tile_kernel(Proxies P, const int32_t* __restrict__ perm, PackParams pp,
   __shared__ int32_t chunk_end;
   extern __shared__ __align__(16) int32_t dyn[];
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.y);
+  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.y);
   if (m == 0) return;
   const int s0 = blockIdx.x * kTC;
   const Scale sc = scale_of(pp, m);
@@ -102,7 +102,7 @@ offsets_kernel(PackParams pp, const int32_t* __restrict__ rowofs, const uint32_t
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (item >= (int64_t)pp.n * pp.B) return;
-  const int m = wave_m(pp, st->pad[2], st->b0, (int)(item / pp.n));
+  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, (int)(item / pp.n));
   if (m == 0) return;
   const int s = (int)(item % pp.n);
   if (cand_bad[m - 1]) return;

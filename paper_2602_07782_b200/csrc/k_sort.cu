@@ -574,12 +574,13 @@ __global__ void many_reset_kernel(Status* sts, AtlasRes* res, int32_t A, const i
 }
 
 // One launch instead of a status upload plus a string of memsets.
-// mode 2: initialise the status block (bad_chart = none, trace start = max);
-// mode >= 1: zero the candidate records and hybrid-tail states;
+// mode 2: initialise the status block (bad_chart = none, trace start = max)
+// and zero the candidate records and hybrid-tail states;
 // always: zero per-wave state (cand_bad, large-chart list, raster queue head,
 // fused ready flags / arrival counters).
 __global__ void reset_kernel(Status* st, int mode, Cand* cands, int32_t* t_state,
                              int32_t* cand_bad, int M, int32_t* rdy, int64_t nrdy) {
+  // mode 2: fresh status (wave 0); 0: the next wave (the wave index advances)
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (t0 == 0) {
@@ -590,12 +591,13 @@ __global__ void reset_kernel(Status* st, int mode, Cand* cands, int32_t* t_state
       st->tr[0] = ~0ull;
       st->win_j = INT32_MAX;
     } else {
+      if (mode == 0) st->wave++;
       st->pad[1] = 0;
       st->work_next = 0;
       st->win_j = INT32_MAX;
     }
   }
-  if (mode >= 1) {
+  if (mode == 1 || mode == 2) {
     int32_t* cw = (int32_t*)cands;
     for (int64_t i = t0; i < (int64_t)M * (int64_t)(sizeof(Cand) / 4); i += stride) cw[i] = 0;
     for (int64_t i = t0; i < M; i += stride) t_state[i] = 0;

@@ -76,7 +76,7 @@ tail_prepare_kernel(PackParams pp, const int32_t* __restrict__ perm, const int64
                     int32_t* scratch, int64_t pair_cap, Cand* cands, const Status* st) {
   __shared__ ScanSmem S;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.x);
+  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
   if (m == 0 || pp.T.state[m - 1] != TAIL_LAYOUT) return;
   const int n = pp.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t Wp = pp.Wp;
@@ -203,7 +203,7 @@ tail_layout_kernel(PackParams pp, const int32_t* __restrict__ wd_all,
                    const Status* st) {
   __shared__ ScanSmem S;
   if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int m = wave_m(pp, st->pad[2], st->b0, blockIdx.x);
+  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
   if (m == 0 || pp.T.state[m - 1] != TAIL_LAYOUT) return;
   const int n = pp.n, tid = threadIdx.x;
   const int64_t Wp = pp.Wp;

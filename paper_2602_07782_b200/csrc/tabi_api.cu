@@ -6,8 +6,10 @@
 // pair offsets + K4 fold & push of a wave of candidates, one cooperative
 // launch; split K3/K3b/K4 kernels with TABI_FUSED=0) -> [hybrid tail] -> K5
 // select/scatter -> [D2H placements] + D2H status/records -> one sync.  The
-// first wave is captured once as a CUDA graph and replayed.  Further waves
-// (only when every candidate of a wave fails) cost one host round trip each.
+// whole search is captured once as a CUDA graph and replayed: further waves
+// (only when every candidate of a wave fails) run in a WHILE node whose
+// condition select_kernel sets on the device -- no host round trip between
+// waves.  tabi_pack_async returns right after the graph launch.
 // If a device-side capacity check fails (footprint slots or lock-pair lists
 // larger than the current buffers), the context grows those buffers and
 // re-runs from the slot layout; sizes persist, so steady-state calls never
@@ -44,6 +46,18 @@ struct GraphKey {
            on_device == o.on_device && rx == o.rx && ry == o.ry && B == o.B && fused == o.fused &&
            gen == o.gen && sort_env == o.sort_env && memcmp(&spec, &o.spec, sizeof(tabi_spec)) == 0;
   }
+};
+
+// The arguments of a pending asynchronous pack (tabi_pack_async), kept for
+// tabi_pack_wait's re-run after a capacity overflow.
+struct PendArgs {
+  const float* xy;
+  const int32_t* start;
+  int32_t n;
+  float rx, ry;
+  tabi_spec spec;
+  tabi_placement* out;
+  void* stream;
 };
 
 // Batch-mode workspace (tabi_pack_many): chart-indexed arrays for every atlas
@@ -171,6 +185,11 @@ struct tabi_ctx {
   Validator val;           // tabi_validate scratch (N3)
   cudaEvent_t span[2] = {nullptr, nullptr};  // tabi_info.device_ms
   ManyWs many;             // tabi_pack_many
+  cudaStream_t cap_stream = nullptr;  // captures the graph's wave-loop body
+  int g_body = 0;                     // kernels per wave of the graph's loop body
+  bool loop_off = false;              // the graph's device wave loop failed once
+  bool pend = false;                  // an asynchronous pack is in flight
+  PendArgs pend_args{};
 };
 
 #define CK(call)                                              \
@@ -219,6 +238,7 @@ extern "C" const char* tabi_status_str(tabi_status s) {
     case TABI_NO_FIT: return "no candidate scale fits";
     case TABI_ECUDA: return "CUDA error";
     case TABI_ECAPACITY: return "capacity exceeded";
+    case TABI_PENDING: return "pending";
   }
   return "unknown";
 }
@@ -283,6 +303,7 @@ extern "C" void tabi_ctx_destroy(tabi_ctx* ctx) {
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   dfree_all(ctx);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
 }
 
@@ -332,6 +353,22 @@ static tabi_status ensure_candidates(tabi_ctx* ctx, int32_t M, bool regrow_cols,
   return TABI_OK;
 }
 
+// A wave hit the device-side capacity check: grow the footprint slots and / or
+// the lock-pair lists to what it reported (with headroom; sizes persist).
+static tabi_status grow_for(tabi_ctx* ctx, const Status& st, int32_t M) {
+  bool cols = false, pairs = false;
+  if (st.capacity & 1) {
+    ctx->col_cap = ((int64_t)st.cols_total + (st.cols_total >> 2) + 1024) & ~(int64_t)3;
+    ctx->row_cap = ((int64_t)st.rows_total + (st.rows_total >> 2) + 1024) & ~(int64_t)3;
+    cols = true;
+  }
+  if (st.capacity & 2) {
+    ctx->pair_cap = (int64_t)st.pad[0] * 2 + 1024;
+    pairs = true;
+  }
+  return ensure_candidates(ctx, M, cols, pairs);
+}
+
 static bool spec_ok(const tabi_spec* s) {
   return s && s->atlas_w >= 1 && s->atlas_h >= 1 && s->atlas_w <= TABI_MAX_ATLAS_SIDE &&
          s->atlas_h <= TABI_MAX_ATLAS_SIDE && s->gutter >= 0 && s->gutter <= 64 &&
@@ -368,13 +405,21 @@ struct Timer {
 
 static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
                              int32_t n, float res_x, float res_y, const tabi_spec* spec,
-                             tabi_placement* out, tabi_info* info, int on_device, void* stream);
+                             tabi_placement* out, tabi_info* info, int on_device, void* stream,
+                             bool async = false);
+static tabi_status finish_pack(tabi_ctx* ctx, int32_t n, int32_t M, int32_t k, int32_t g,
+                               int on_device, tabi_placement* out, tabi_info* info, int launches,
+                               Timer& tm);
 
 extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
                                  int32_t n, float res_x, float res_y, const tabi_spec* spec,
                                  tabi_placement* out, tabi_info* info, int on_device,
                                  void* stream) {
   if (!ctx) return TABI_EINVAL;
+  if (ctx->pend) {
+    ctx->err = "an asynchronous pack is pending on this context (tabi_pack_wait first)";
+    return TABI_EINVAL;
+  }
   ctx->last_cuda = cudaSuccess;
   tabi_status st = pack_impl(ctx, xy, chart_start, n, res_x, res_y, spec, out, info, on_device,
                              stream);
@@ -388,6 +433,56 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
     st = pack_impl(ctx, xy, chart_start, n, res_x, res_y, spec, out, info, on_device, stream);
   }
   return st;
+}
+
+extern "C" tabi_status tabi_pack_async(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
+                                       int32_t n, float res_x, float res_y, const tabi_spec* spec,
+                                       tabi_placement* out, void* stream) {
+  if (!ctx) return TABI_EINVAL;
+  if (ctx->pend) {
+    ctx->err = "an asynchronous pack is already pending on this context";
+    return TABI_EINVAL;
+  }
+  ctx->last_cuda = cudaSuccess;
+  return pack_impl(ctx, xy, chart_start, n, res_x, res_y, spec, out, nullptr, 1, stream, true);
+}
+
+extern "C" tabi_status tabi_pack_query(tabi_ctx* ctx) {
+  if (!ctx || !ctx->pend) return TABI_EINVAL;
+  const cudaError_t e = cudaEventQuery(ctx->span[1]);
+  if (e == cudaErrorNotReady) return TABI_PENDING;
+  if (e != cudaSuccess) {
+    ctx->err = std::string("cudaEventQuery: ") + cudaGetErrorString(e);
+    return TABI_ECUDA;
+  }
+  return TABI_OK;
+}
+
+extern "C" tabi_status tabi_pack_wait(tabi_ctx* ctx, tabi_info* info) {
+  if (!ctx || !ctx->pend) return TABI_EINVAL;
+  ctx->pend = false;
+  const PendArgs a = ctx->pend_args;
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->bad_chart = -1;
+    info->fused = ctx->last_fused;
+  }
+  CK(cudaEventSynchronize(ctx->span[1]));
+  const Status st = *ctx->h_status;
+  if (st.bad_chart != INT32_MAX) {
+    if (info) info->bad_chart = st.bad_chart;
+    return TABI_EINVAL;
+  }
+  if (st.capacity & 4) return TABI_ECAPACITY;
+  if (st.capacity) {  // grow, then the same pack synchronously
+    const tabi_status ts = grow_for(ctx, st, a.spec.scale_count);
+    if (ts != TABI_OK) return ts;
+    return tabi_pack(ctx, a.xy, a.start, a.n, a.rx, a.ry, &a.spec, a.out, info, 1, a.stream);
+  }
+  const int launches = ctx->g_launches + ctx->g_body * st.wave;
+  Timer tm;
+  return finish_pack(ctx, a.n, a.spec.scale_count, a.spec.local_aabb_count, a.spec.gutter, 1, a.out,
+                     info, launches, tm);
 }
 
 extern "C" tabi_status tabi_validate(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
@@ -427,7 +522,8 @@ extern "C" tabi_status tabi_validate(tabi_ctx* ctx, const float* xy, const int32
 
 static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
                              int32_t n, float res_x, float res_y, const tabi_spec* spec,
-                             tabi_placement* out, tabi_info* info, int on_device, void* stream) {
+                             tabi_placement* out, tabi_info* info, int on_device, void* stream,
+                             bool async) {
   if (!ctx) return TABI_EINVAL;
   if (info) {
     memset(info, 0, sizeof(*info));
@@ -516,28 +612,29 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   tabi_placement* d_out = on_device ? out : ctx->d_out;
   const int64_t V_in = on_device ? 0 : (int64_t)chart_start[n];
   int wave = 0;
-  int reset_mode = 2;  // 2: fresh status; 0: next wave
-  // One wave's work, enqueued on s: [H2D + reset + proxies + sort] for the
-  // first wave, the candidate wave, select, [placements D2H], status D2H.
-  auto enqueue_wave = [&](bool prologue, int& nl) -> tabi_status {
+  // The pack is enqueued in three parts on s:
+  //  prologue  [H2D] + fresh status + proxies + sort + slot layout (full), or
+  //            fresh status + slot layout only (a capacity retry keeps the
+  //            proxies and the order);
+  //  body      one candidate wave: [reset] + the fused wave kernel (or the
+  //            split K3/K3b/K4 kernels) + [hybrid tail] + select;
+  //  epilogue  [D2H placements] + D2H status and candidate records.
+  auto enqueue_prologue = [&](bool full, int& nl) -> tabi_status {
     bool prep_done = false;
-    if (prologue && !on_device)
+    if (full && !on_device)
       CK(cudaMemcpyAsync(ctx->d_xy, ctx->h_xy, sizeof(float) * 2 * V_in + sizeof(int32_t) * (n + 1),
                          cudaMemcpyHostToDevice, s));
-    // (wave 0: prep_kernel zeroes the fused kernel's flags for the T tiles it
-    // lays out; later waves reuse the tiles and need the reset here)
-    launch_reset(ctx->d_status, reset_mode, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy,
-                 wave == 0 ? 0 : nrdy, s);
+    // (prep_kernel zeroes the fused kernel's flags for the T tiles it lays out)
+    launch_reset(ctx->d_status, 2, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy, 0, s);
     nl++;
-    if (prologue) {
+    if (full) {
       launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
                      ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s,
                      AtlasMap{nullptr, 1, nullptr}, V_in);
       nl++;
       tm.mark(s);
-      if (wave == 0 && launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs,
-                                        ctx->hsorted, ctx->tstart, ctx->tix, ctx->d_status,
-                                        fused ? ctx->rdy : nullptr, s)) {
+      if (launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted,
+                           ctx->tstart, ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s)) {
         nl++;
         prep_done = true;
       } else {
@@ -545,10 +642,20 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       }
       tm.mark(s);
     }
-    if (wave == 0 && !prep_done) {
+    if (!prep_done) {
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
-                  ctx->tix, ctx->d_status,
-                  fused ? ctx->rdy : nullptr, s);
+                  ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s);
+      nl++;
+    }
+    return TABI_OK;
+  };
+  // reset_mode: -1 none (wave 0 after the prologue), 0 the next wave; with
+  // use_h, select also sets the graph's wave-loop condition h
+  auto enqueue_body = [&](int reset_mode, int& nl, cudaGraphConditionalHandle h,
+                          int use_h) -> tabi_status {
+    if (reset_mode >= 0) {
+      launch_reset(ctx->d_status, reset_mode, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy,
+                   nrdy, s);
       nl++;
     }
     if (fused) {
@@ -604,11 +711,14 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     }
     tm.mark(s);
     launch_select(pp, ctx->P, ctx->perm, ctx->wd, ctx->hd, ctx->X, ctx->Y, ctx->mir, ctx->cands,
-                  d_out, ctx->d_status, s);
+                  d_out, ctx->d_status, s, h, use_h);
     nl++;
     tm.mark(s);
     CK(cudaGetLastError());
-    if (!on_device)  // placements (used only if this wave holds the winner)
+    return TABI_OK;
+  };
+  auto enqueue_epilogue = [&]() -> tabi_status {
+    if (!on_device)  // placements (valid if some wave held the winner)
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(tabi_placement) * n, cudaMemcpyDeviceToHost,
                          s));
     // status + candidate records: one contiguous block, one copy
@@ -617,11 +727,21 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     return TABI_OK;
   };
 
-  // The first wave (the only one in the common case) runs as a CUDA graph,
-  // captured once per (pointers, sizes, spec, buffer generation) and relaunched
-  // with one call: no per-kernel launch overhead on the critical path.
+  // The common case runs as ONE CUDA graph, captured once per (pointers,
+  // sizes, spec, buffer generation) and relaunched with one call: the
+  // prologue, candidate wave 0, a WHILE node whose body is one further wave,
+  // and the epilogue.  Each wave's select_kernel decides on the device
+  // whether another wave is needed (it sets the node's condition), so a
+  // multi-wave scale search has no host round trip and the host syncs once;
+  // in the common case the loop body never runs.  Test knobs (TABI_GRAPH=0,
+  // TABI_TIMING=1) and capacity retries use the host-driven loop below, which
+  // enqueues the same kernels wave by wave.
   const char* genv = getenv("TABI_GRAPH");
   const bool use_graph = !tm.on && !(genv && genv[0] == '0');
+  if (async && !use_graph) {
+    ctx->err = "asynchronous packs need the graph path (TABI_GRAPH / TABI_TIMING unset)";
+    return TABI_EINVAL;
+  }
   // bound: every wave but the last evaluates >= 1 candidate (<= M waves), plus
   // at most 8 capacity retries; reaching it is an internal error, not NO_FIT
   const int max_attempts = M + 10;
@@ -629,9 +749,9 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   for (int attempt = 0; attempt < max_attempts; attempt++) {
     pp.col_cap = ctx->col_cap;
     pp.row_cap = ctx->row_cap;
-    pp.wave = wave;
-    const bool prologue = attempt == 0;
-    if (prologue && use_graph) {
+    const bool first = attempt == 0;
+    const bool device_loop = first && use_graph && !ctx->loop_off;
+    if (device_loop) {
       char sort_env = 0;  // test knobs read while enqueuing: part of the key
       for (const char* p = getenv("TABI_SORT"); p && *p; p++) sort_env = (char)(sort_env * 31 + *p);
       for (const char* p = getenv("TABI_PROXY_LANES"); p && *p; p++)
@@ -644,53 +764,119 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       if (!ctx->gexec || !(key == ctx->gkey)) {
         if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
         ctx->gexec = nullptr;
+        if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
         cudaGraph_t g = nullptr;
-        int nl = 0;
-        // capture on the context's own stream (the caller's may be the legacy
+        int npro = 0, nbody = 0;
+        // capture on the context's own streams (the caller's may be the legacy
         // default stream, which cannot be captured); launched on the caller's
         const cudaStream_t user_s = s;
         s = ctx->stream;
         const cudaError_t be = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
         if (be != cudaSuccess) s = user_s;
         CK(be);
-        const tabi_status es = enqueue_wave(true, nl);
-        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        tabi_status es = enqueue_prologue(true, npro);
+        cudaError_t ce = cudaSuccess;
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        cudaGraphConditionalHandle h = 0;
+        if (es == TABI_OK) {
+          ce = cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, nullptr, nullptr);
+          // (default 0 at every launch: a wave that stops early leaves it so)
+          if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault);
+          if (ce == cudaSuccess) es = enqueue_body(-1, npro, h, 1);
+        }
+        if (es == TABI_OK && ce == cudaSuccess) {
+          // WHILE node after wave 0; its body captured from a second stream
+          const cudaGraphNode_t* deps = nullptr;
+          size_t ndeps = 0;
+          ce = cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &ndeps);
+          cudaGraphNodeParams cp = {};
+          cp.type = cudaGraphNodeTypeConditional;
+          cp.conditional.handle = h;
+          cp.conditional.type = cudaGraphCondTypeWhile;
+          cp.conditional.size = 1;
+          cudaGraphNode_t cn = nullptr;
+          if (ce == cudaSuccess) ce = cudaGraphAddNode(&cn, cg, deps, ndeps, &cp);
+          if (ce == cudaSuccess)
+            ce = cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies);
+          if (ce == cudaSuccess) {
+            const cudaStream_t ms = s;
+            s = ctx->cap_stream;
+            ce = cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal);
+            if (ce == cudaSuccess) {
+              es = enqueue_body(0, nbody, h, 1);
+              cudaGraph_t bg = nullptr;
+              const cudaError_t e2 = cudaStreamEndCapture(s, &bg);
+              if (ce == cudaSuccess) ce = e2;
+            }
+            s = ms;
+          }
+          if (es == TABI_OK && ce == cudaSuccess) es = enqueue_epilogue();
+        }
+        const cudaError_t ee = cudaStreamEndCapture(s, &g);
         s = user_s;
+        if (ce == cudaSuccess) ce = ee;
         if (es != TABI_OK) {
           if (g) cudaGraphDestroy(g);
           return es;
         }
-        CK(ce);
-        const cudaError_t ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
-        cudaGraphDestroy(g);
-        CK(ie);
+        cudaError_t ie = ce;
+        if (ie == cudaSuccess) ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+          // no conditional-node graph here (driver, cooperative launch in a
+          // loop body, ...): the host-driven loop from now on
+          cudaGetLastError();
+          ctx->gexec = nullptr;
+          ctx->loop_off = true;
+          ctx->err = std::string("device wave loop unavailable: ") + cudaGetErrorString(ie);
+          if (async) return TABI_ECUDA;
+          attempt--;
+          continue;
+        }
         ctx->gkey = key;
-        ctx->g_launches = nl;
+        ctx->g_launches = npro;
+        ctx->g_body = nbody;
       }
       CK(cudaEventRecord(ctx->span[0], s));
       CK(cudaGraphLaunch(ctx->gexec, s));
-      launches += ctx->g_launches;
     } else {
       int nl = 0;
-      if (prologue) CK(cudaEventRecord(ctx->span[0], s));
-      const tabi_status es = enqueue_wave(prologue, nl);
+      if (first) CK(cudaEventRecord(ctx->span[0], s));
+      if (wave == 0) {
+        const tabi_status es = enqueue_prologue(first, nl);
+        if (es != TABI_OK) return es;
+      }
+      const tabi_status es = enqueue_body(wave == 0 ? -1 : 0, nl, 0, 0);
       if (es != TABI_OK) return es;
+      const tabi_status ee = enqueue_epilogue();
+      if (ee != TABI_OK) return ee;
       launches += nl;
     }
     CK(cudaEventRecord(ctx->span[1], s));  // device span: first enqueued op .. last copy
+    if (device_loop && async) {
+      // return after enqueueing; tabi_pack_wait finishes (or re-runs on a
+      // capacity overflow) -- the caller keeps its buffers until then
+      ctx->pend = true;
+      ctx->pend_args = PendArgs{xy, chart_start, n, res_x, res_y, *spec, out, stream};
+      return TABI_OK;
+    }
     CK(cudaStreamSynchronize(s));
     const Status st = *ctx->h_status;
+    if (device_loop) launches += ctx->g_launches + ctx->g_body * st.wave;
     if (st.bad_chart != INT32_MAX) {
       if (info) info->bad_chart = st.bad_chart;
       return TABI_EINVAL;
     }
     if (st.capacity & 4) return TABI_ECAPACITY;  // vertex range beyond max_vertices
     if (!st.capacity) {
+      finished = true;
+      if (device_loop) break;  // the device decided the waves
       // Continue while an unevaluated (lower) candidate could still beat the
       // best area-weighted scale found: V(m) <= A_tot * m * 2^20 (p <= m 2^20/M);
-      // in sequential mode any success stops the search.
+      // in sequential mode any success stops the search (select_kernel's rule).
       const int next_m = st.pad[2] - (st.b0 + wave * B);  // top of wave + 1 (see wave_m)
-      finished = true;
       if (next_m < 1) break;
       if (st.winner > 0) {
         const i128 Atot = (i128)(((unsigned __int128)st.atot_hi << 64) | st.atot_lo);
@@ -702,24 +888,12 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       }
       finished = false;
       wave++;
-      reset_mode = 0;
       continue;
     }
     wave = 0;
     // grow and retry from the slot layout (proxies and order are kept)
-    bool cols = false, pairs = false;
-    if (st.capacity & 1) {
-      ctx->col_cap = ((int64_t)st.cols_total + (st.cols_total >> 2) + 1024) & ~(int64_t)3;
-      ctx->row_cap = ((int64_t)st.rows_total + (st.rows_total >> 2) + 1024) & ~(int64_t)3;
-      cols = true;
-    }
-    if (st.capacity & 2) {
-      ctx->pair_cap = (int64_t)st.pad[0] * 2 + 1024;
-      pairs = true;
-    }
-    ts = ensure_candidates(ctx, M, cols, pairs);
+    ts = grow_for(ctx, st, M);
     if (ts != TABI_OK) return ts;
-    reset_mode = 2;  // fresh status (prep recomputes its fields), records, wave state
     tm.n = 3;  // re-time the retried stages
     if (attempt >= 8) return TABI_ECAPACITY;
   }
@@ -727,10 +901,18 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     ctx->err = "candidate wave loop did not terminate";
     return TABI_ECUDA;
   }
+  return finish_pack(ctx, n, M, pp.k, pp.g, on_device, out, info, launches, tm);
+}
+
+// After the last wave: the winner's record -> tabi_info, placements (host mode)
+// -> the caller's buffer.
+static tabi_status finish_pack(tabi_ctx* ctx, int32_t n, int32_t M, int32_t k, int32_t g,
+                               int on_device, tabi_placement* out, tabi_info* info, int launches,
+                               Timer& tm) {
   ctx->last_n = n;
   ctx->last_M = M;
-  ctx->last_k = pp.k;
-  ctx->last_g = pp.g;
+  ctx->last_k = k;
+  ctx->last_g = g;
   const int32_t win = ctx->h_status->winner;
   if (win == 0) {
     if (info) info->gpu_launches = launches;

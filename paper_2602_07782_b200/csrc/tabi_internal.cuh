@@ -321,6 +321,8 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t ntiles;     // fused kernel: raster tiles (prep_kernel)
   int32_t win_j;      // fused, sequential mode: smallest wave slot that succeeded
   int32_t b0;         // wave 0's candidate slots in use (prep_kernel; <= B)
+  int32_t wave;       // current candidate wave (reset_kernel / wave_ctl_kernel advance it)
+  int32_t wave_pad;
   int32_t wmax, hmax; // largest chart width / height (units; prep_kernel): a
                       // candidate whose scaled largest chart exceeds the dilated
                       // atlas fails at once (cand_too_big)
@@ -381,7 +383,8 @@ struct TailBufs {
 struct PackParams {
   int32_t n, k, M, g, W, H, Wp, Hp;
   uint32_t flags;
-  int32_t wave, B;            // candidate wave: m = m_hi - wave * B - j, j < B
+  int32_t B;                  // candidates per wave: m = m_hi - wave * B - j, j < B (wave:
+                              // Status::wave)
   int32_t t_opt;              // effective t_opt (basis points of H), 0 = sequential only
   int32_t mode;               // K4: 0 sequential rows (may switch), 1 prefix rows
   int32_t tail;               // K3 / K3b: 1 = rasterize tail charts at p / 2^20
@@ -395,9 +398,12 @@ struct PackParams {
 // area bound computed by prep_kernel.
 // Candidate of wave slot j: wave 0 evaluates the b0 candidates m_hi, m_hi - 1,
 // ... (b0 <= B, chosen by prep_kernel); wave w >= 1 the next B below.
-__host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t m_hi, int32_t b0, int j) {
-  if (pp.wave == 0 && j >= b0) return 0;
-  const int m = m_hi - (pp.wave == 0 ? 0 : b0 + (pp.wave - 1) * pp.B) - j;
+// The wave index lives in the status block (Status::wave): the device-side
+// wave loop advances it without a host round trip.
+__host__ __device__ __forceinline__ int wave_m(const PackParams& pp, int32_t wave, int32_t m_hi,
+                                               int32_t b0, int j) {
+  if (wave == 0 && j >= b0) return 0;
+  const int m = m_hi - (wave == 0 ? 0 : b0 + (wave - 1) * pp.B) - j;
   return m >= 1 ? m : 0;
 }
 
@@ -518,9 +524,12 @@ bool many_lazy_ok(int k, int g, int Wp);
 // k_floor.cu: packer building-block latencies in ns (tabi_debug_latency_floor)
 int latency_floor(int device, double* out8);
 cudaError_t launch_many(int grid, const PackParams& pp, const ManyArgs& a, cudaStream_t s);
+// K5; with use_h it also sets the graph's wave-loop condition (see
+// select_kernel)
 void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, const int32_t* wd,
                    const int32_t* hd, const int32_t* X, const int32_t* Y, const uint8_t* mir,
-                   const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s);
+                   const Cand* cands, tabi_placement* out, Status* st, cudaStream_t s,
+                   cudaGraphConditionalHandle h = 0, int use_h = 0);
 }  // namespace tabi
 
 namespace tabi {

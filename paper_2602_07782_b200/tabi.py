@@ -19,7 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtabi.so")
 
-OK, EINVAL, NO_FIT, ECUDA, ECAPACITY = 0, 1, 2, 3, 4
+OK, EINVAL, NO_FIT, ECUDA, ECAPACITY, PENDING = 0, 1, 2, 3, 4, 5
 F_NO_HC, F_NO_BALANCE, F_ADJACENT_LOCKS_ONLY, F_PREROTATE, F_NO_OBB, F_EXACT_TAIL = (1, 2, 4, 8, 16,
                                                                             32)
 # Ablation / baseline modes on the same kernels (the ablation table after
@@ -106,6 +106,9 @@ def lib():
         L.tabi_ctx_destroy.argtypes = [P]
         L.tabi_pack.argtypes = [P, P, P, i32, C.c_float, C.c_float, C.POINTER(Spec), P,
                                 C.POINTER(Info), C.c_int, P]
+        L.tabi_pack_async.argtypes = [P, P, P, i32, C.c_float, C.c_float, C.POINTER(Spec), P, P]
+        L.tabi_pack_wait.argtypes = [P, C.POINTER(Info)]
+        L.tabi_pack_query.argtypes = [P]
         L.tabi_status_str.restype = C.c_char_p
         L.tabi_status_str.argtypes = [C.c_int]
         L.tabi_last_error.restype = C.c_char_p
@@ -128,7 +131,8 @@ def lib():
     return _lib
 
 
-EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_status_str",
+EXPORTS = ["tabi_ctx_create", "tabi_ctx_destroy", "tabi_pack", "tabi_pack_async",
+           "tabi_pack_wait", "tabi_pack_query", "tabi_status_str",
            "tabi_last_error", "tabi_debug_proxies", "tabi_debug_perm", "tabi_debug_candidates",
            "tabi_debug_profile", "tabi_debug_offsets", "tabi_debug_trace",
            "tabi_debug_trace_raster", "tabi_shard_plan", "tabi_pack_batch", "tabi_pack_many",
@@ -273,6 +277,37 @@ class Context:
             st = lib().tabi_pack(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], C.byref(spec),
                                  _ptr(out), C.byref(info), 0,
                                  C.c_void_p(stream) if stream else None)
+        if raise_on_error and st not in (OK, NO_FIT):
+            raise TabiError(st, f"bad_chart={info.bad_chart} {self.last_error()}")
+        return st, out, info
+
+    def pack_async(self, xy, start, spec: Spec, res=(1.0, 1.0), out=None, stream=None):
+        """Enqueue one pack (tabi_pack_async) from CUDA tensors and return the
+        device placement buffer at once; the inputs must stay alive and unchanged
+        until ``wait()``.  Raises on errors found before enqueueing."""
+        import torch
+        n = int(start.shape[0]) - 1
+        if out is None:
+            out = torch.empty(n * PLACEMENT_DTYPE.itemsize, dtype=torch.uint8, device=xy.device)
+        if stream is None:
+            stream = _torch_stream(xy.device)
+        st = lib().tabi_pack_async(self.h, _ptr(xy), _ptr(start), n, res[0], res[1], C.byref(spec),
+                                   _ptr(out), C.c_void_p(stream))
+        if st != OK:
+            raise TabiError(st, self.last_error())
+        self._pending = (xy, start, out)  # keep the buffers alive until wait()
+        return out
+
+    def query(self) -> int:
+        """tabi_pack_query: PENDING while the asynchronous pack runs, OK once done."""
+        return lib().tabi_pack_query(self.h)
+
+    def wait(self, raise_on_error=True):
+        """tabi_pack_wait: (status, device placements, Info) of the pending pack."""
+        info = Info()
+        st = lib().tabi_pack_wait(self.h, C.byref(info))
+        out = (getattr(self, "_pending", None) or (None, None, None))[2]
+        self._pending = None
         if raise_on_error and st not in (OK, NO_FIT):
             raise TabiError(st, f"bad_chart={info.bad_chart} {self.last_error()}")
         return st, out, info
