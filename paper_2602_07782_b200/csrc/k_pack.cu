@@ -859,6 +859,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     const int32_t hc0 = S.hcsel[0], hc1 = S.hcsel[1];
     const int32_t endA = S.end_cfg[0], endK = S.end_cfg[2];
     const int ncfg = knee_ok ? 4 : 2;
+    // prefix rows: FastAtlas fixes the direction in advance (one L->R row,
+    // then two R->L) and HC is on, so a prefix row pushes,
+    // relaxes and scores ONE configuration (pdir) instead of both directions
+    const int pdir = prefix_mode ? ((S.prefix_rows % 3 == 0) ? 0 : 1) : -1;
     // A row of at most kRW charts (the normal case) is one window: its Y
     // values then live in shared memory from push to commit, and the fold's
     // window scalars (W.rx1, W.rwd) serve the lock-pair scan; longer rows
@@ -993,6 +997,15 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               m2 = max(m2, f2[j] - top);
               m3 = max(m3, f3[-j] - top);
             }
+          } else if (pdir >= 0) {  // prefix row: its one direction (m0 holds it)
+            const int32_t* fp = pdir ? f1 : f0;
+            const int32_t step = pdir ? -1 : 1;
+            #pragma unroll 4
+            for (int32_t j = j0; j < j1; j++) {
+              const uint32_t v = pc[j];
+              bm = max(bm, hi16(v));
+              m0 = max(m0, fp[step * j] - lo16(v));
+            }
           } else {
             #pragma unroll 4
             for (int32_t j = j0; j < j1; j++) {
@@ -1003,9 +1016,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               m1 = max(m1, f1[-j] - top);
             }
           }
-          wk += (unsigned long long)((four ? 4 : 2) * (j1 - j0));
-          atomicMax(&W.rY[i], m0);
-          atomicMax(&W.rY[kRW + i], m1);
+          wk += (unsigned long long)((four ? 4 : pdir >= 0 ? 1 : 2) * (j1 - j0));
+          if (pdir >= 0) {
+            atomicMax(&W.rY[pdir * kRW + i], m0);
+          } else {
+            atomicMax(&W.rY[i], m0);
+            atomicMax(&W.rY[kRW + i], m1);
+          }
           if (four) {
             atomicMax(&W.rY[2 * kRW + i], m2);
             atomicMax(&W.rY[3 * kRW + i], m3);
@@ -1027,7 +1044,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     phase_mark(3);
     // ---- Alg. 1 CorrectYOffsets over adjacent + non-adjacent pairs ---------
     {
-      const int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // HC configs [c0, c1)
+      int c0 = hc0 ? 0 : 2, c1 = (knee_ok && hc1) ? 4 : 2;  // HC configs [c0, c1)
+      if (pdir >= 0) { c0 = pdir; c1 = pdir + 1; }  // (prefix rows: HC on, one direction)
       // (no lock bit among the row's pairs: every pass would change nothing)
       if (!one || prefix_mode) anylock = true;
       if (c1 > c0 && (anylock || anypl)) {

@@ -429,13 +429,14 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
       for (int m = pp.M; m >= 1; m--)
         if ((i128)m * m * tot <= rhs) { m_hi = m; break; }
       st->pad[2] = m_hi;
-      // Wave 0's width (sequential mode): the candidates from m_hi down to the
-      // scale at which the charts would fill 60 % of the atlas -- below that a
-      // success is unlikely, and a narrower first wave leaves the top
-      // candidate's chain with less contention.  Later waves take B each, so
-      // the result is the exhaustive search's either way.
+      // Wave 0's width: the candidates from m_hi down to the scale at which
+      // the charts would fill 60 % of the atlas -- below that a success is
+      // unlikely, and a narrower first wave leaves the top candidate's chain
+      // with less contention.  Later waves take B each and the wave loop's
+      // stopping rule (select_kernel; hybrid mode: the V bound of D25) is
+      // unchanged, so the result is the exhaustive search's either way.
       int b0 = pp.B;
-      if (pp.early && pp.B > 2 && m_hi >= 1) {
+      if (pp.B > 2 && m_hi >= 1) {
         int m_lo = m_hi;
         while (m_lo > 1 && (i128)100 * (m_lo - 1) * (m_lo - 1) * tot >= (i128)TABI_B0_FILL * rhs) m_lo--;
         b0 = min(pp.B, max(2, m_hi - m_lo + 1));

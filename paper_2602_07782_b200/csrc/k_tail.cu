@@ -70,14 +70,36 @@ __device__ __forceinline__ int32_t block_max(int32_t v, ScanSmem& S) {
   return r;
 }
 
-__global__ void __launch_bounds__(kT, 1)
-tail_prepare_kernel(PackParams pp, const int32_t* __restrict__ perm, const int64_t* __restrict__ area2,
-                    const int32_t* __restrict__ wd_all, const int32_t* __restrict__ off_all,
-                    int32_t* scratch, int64_t pair_cap, Cand* cands, const Status* st) {
+// Device-side stop of the re-layout rounds (a CUDA-graph WHILE node around
+// K3 + K3b + tail_layout): the last CTA of the grid to finish (fence +
+// counter, the threadFenceReduction pattern) sets the node's condition to
+// "some candidate of the wave still needs a round" -- TAIL_LAYOUT, whose
+// iteration count tail_layout bounds by 8.
+__device__ __forceinline__ void rounds_decide(const PackParams& pp, Status* st,
+                                              cudaGraphConditionalHandle h, bool round) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(&st->tail_cnt, 1) != (int)gridDim.x - 1) return;
+  st->tail_cnt = 0;
+  if (round) st->rounds_run++;
+  __threadfence();
+  bool go = false;
+  if (st->bad_chart == INT32_MAX && !st->capacity) {
+    for (int j = 0; j < (int)gridDim.x; j++) {
+      const int m = wave_m(pp, st->wave, st->pad[2], st->b0, j);
+      if (m != 0 && *(volatile int32_t*)&pp.T.state[m - 1] == TAIL_LAYOUT) go = true;
+    }
+  }
+  cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+__device__ __noinline__ void tail_prepare(const PackParams& pp, const int32_t* __restrict__ perm,
+                                          const int64_t* __restrict__ area2,
+                                          const int32_t* __restrict__ wd_all,
+                                          const int32_t* __restrict__ off_all, int32_t* scratch,
+                                          int64_t pair_cap, Cand* cands, int m) {
   __shared__ ScanSmem S;
-  if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
-  if (m == 0 || pp.T.state[m - 1] != TAIL_LAYOUT) return;
   const int n = pp.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t Wp = pp.Wp;
   const int32_t r0 = pp.T.r0[m - 1];
@@ -198,13 +220,21 @@ tail_prepare_kernel(PackParams pp, const int32_t* __restrict__ perm, const int64
 }
 
 __global__ void __launch_bounds__(kT, 1)
-tail_layout_kernel(PackParams pp, const int32_t* __restrict__ wd_all,
-                   const int32_t* __restrict__ off_all, int32_t* scratch, int64_t pair_cap,
-                   const Status* st) {
+tail_prepare_kernel(PackParams pp, const int32_t* __restrict__ perm, const int64_t* __restrict__ area2,
+                    const int32_t* __restrict__ wd_all, const int32_t* __restrict__ off_all,
+                    int32_t* scratch, int64_t pair_cap, Cand* cands, Status* st,
+                    cudaGraphConditionalHandle h, int use_h) {
+  if (st->bad_chart == INT32_MAX && !st->capacity) {
+    const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
+    if (m != 0 && pp.T.state[m - 1] == TAIL_LAYOUT) tail_prepare(pp, perm, area2, wd_all, off_all, scratch, pair_cap, cands, m);
+  }
+  if (use_h) rounds_decide(pp, st, h, false);
+}
+
+__device__ __noinline__ void tail_layout(const PackParams& pp, const int32_t* __restrict__ wd_all,
+                                         const int32_t* __restrict__ off_all, int32_t* scratch,
+                                         int64_t pair_cap, int m) {
   __shared__ ScanSmem S;
-  if (st->bad_chart != INT32_MAX || st->capacity) return;
-  const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
-  if (m == 0 || pp.T.state[m - 1] != TAIL_LAYOUT) return;
   const int n = pp.n, tid = threadIdx.x;
   const int64_t Wp = pp.Wp;
   const int32_t r0 = pp.T.r0[m - 1];
@@ -263,17 +293,31 @@ tail_layout_kernel(PackParams pp, const int32_t* __restrict__ wd_all,
   }
 }
 
+__global__ void __launch_bounds__(kT, 1)
+tail_layout_kernel(PackParams pp, const int32_t* __restrict__ wd_all,
+                   const int32_t* __restrict__ off_all, int32_t* scratch, int64_t pair_cap,
+                   Status* st, cudaGraphConditionalHandle h, int use_h) {
+  if (st->bad_chart == INT32_MAX && !st->capacity) {
+    const int m = wave_m(pp, st->wave, st->pad[2], st->b0, blockIdx.x);
+    if (m != 0 && pp.T.state[m - 1] == TAIL_LAYOUT) tail_layout(pp, wd_all, off_all, scratch, pair_cap, m);
+  }
+  if (use_h) rounds_decide(pp, st, h, true);
+}
+
 }  // namespace
 
 void launch_tail_prepare(const PackParams& pp, const int32_t* perm, const int64_t* area2,
                          const int32_t* wd, const int32_t* off, int32_t* scratch, int64_t pair_cap,
-                         Cand* cands, const Status* st, cudaStream_t s) {
-  tail_prepare_kernel<<<pp.B, kT, 0, s>>>(pp, perm, area2, wd, off, scratch, pair_cap, cands, st);
+                         Cand* cands, Status* st, cudaStream_t s, cudaGraphConditionalHandle h,
+                         int use_h) {
+  tail_prepare_kernel<<<pp.B, kT, 0, s>>>(pp, perm, area2, wd, off, scratch, pair_cap, cands, st, h,
+                                          use_h);
 }
 
 void launch_tail_layout(const PackParams& pp, const int32_t* wd, const int32_t* off,
-                        int32_t* scratch, int64_t pair_cap, const Status* st, cudaStream_t s) {
-  tail_layout_kernel<<<pp.B, kT, 0, s>>>(pp, wd, off, scratch, pair_cap, st);
+                        int32_t* scratch, int64_t pair_cap, Status* st, cudaStream_t s,
+                        cudaGraphConditionalHandle h, int use_h) {
+  tail_layout_kernel<<<pp.B, kT, 0, s>>>(pp, wd, off, scratch, pair_cap, st, h, use_h);
 }
 
 }  // namespace tabi

@@ -186,6 +186,7 @@ struct tabi_ctx {
   cudaEvent_t span[2] = {nullptr, nullptr};  // tabi_info.device_ms
   ManyWs many;             // tabi_pack_many
   cudaStream_t cap_stream = nullptr;  // captures the graph's wave-loop body
+  cudaStream_t cap_stream2 = nullptr; // captures the hybrid tail's rounds-loop body
   int g_body = 0;                     // kernels per wave of the graph's loop body
   bool loop_off = false;              // the graph's device wave loop failed once
   bool pend = false;                  // an asynchronous pack is in flight
@@ -304,6 +305,7 @@ extern "C" void tabi_ctx_destroy(tabi_ctx* ctx) {
   dfree_all(ctx);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
   delete ctx;
 }
 
@@ -479,7 +481,7 @@ extern "C" tabi_status tabi_pack_wait(tabi_ctx* ctx, tabi_info* info) {
     if (ts != TABI_OK) return ts;
     return tabi_pack(ctx, a.xy, a.start, a.n, a.rx, a.ry, &a.spec, a.out, info, 1, a.stream);
   }
-  const int launches = ctx->g_launches + ctx->g_body * st.wave;
+  const int launches = ctx->g_launches + ctx->g_body * st.wave + 4 * st.rounds_run;
   Timer tm;
   return finish_pack(ctx, a.n, a.spec.scale_count, a.spec.local_aabb_count, a.spec.gutter, 1, a.out,
                      info, launches, tm);
@@ -619,6 +621,27 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
   //  body      one candidate wave: [reset] + the fused wave kernel (or the
   //            split K3/K3b/K4 kernels) + [hybrid tail] + select;
   //  epilogue  [D2H placements] + D2H status and candidate records.
+  // Append a WHILE node with condition h to the graph being captured on
+  // stream sm (after everything captured so far); returns its body graph.
+  auto add_while = [&](cudaStream_t sm, cudaGraphConditionalHandle h,
+                       cudaGraph_t& body) -> cudaError_t {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cg = nullptr;
+    cudaError_t ce = cudaStreamGetCaptureInfo(sm, &cs, nullptr, &cg, &deps, &ndeps);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn = nullptr;
+    if (ce == cudaSuccess) ce = cudaGraphAddNode(&cn, cg, deps, ndeps, &cp);
+    if (ce == cudaSuccess)
+      ce = cudaStreamUpdateCaptureDependencies(sm, &cn, 1, cudaStreamSetCaptureDependencies);
+    body = ce == cudaSuccess ? cp.conditional.phGraph_out[0] : nullptr;
+    return ce;
+  };
   auto enqueue_prologue = [&](bool full, int& nl) -> tabi_status {
     bool prep_done = false;
     if (full && !on_device)
@@ -684,23 +707,63 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     }
     if (t_opt > 0) {
       // hybrid prefix tail for the candidates K4 switched: rows and
-      // sigma, then up to 9 re-rasterize / re-lay rounds, then the prefix rows
-      launch_tail_prepare(pp, ctx->perm, ctx->P.area2, ctx->wd, ctx->off, ctx->scratch,
-                          ctx->pair_cap, ctx->cands, ctx->d_status, s);
-      nl++;
+      // sigma, then re-rasterize / re-lay rounds until every row fits (at most
+      // 9), then the prefix rows.  In the graph the rounds are a WHILE node
+      // whose condition the last CTA of tail_prepare / tail_layout sets, so
+      // they stop at the round that fits; the host-driven loop enqueues 9
+      // (the kernels of a finished candidate exit at once).
       PackParams pt = pp;
       pt.tail = 1;
       // (the exact tail, R6, keeps the footprints at m/M: no re-rasterization)
-      const int rounds = (pp.flags & TABI_F_EXACT_TAIL) ? 0 : 9;
-      for (int r = 0; r < rounds; r++) {
+      const bool exact = (pp.flags & TABI_F_EXACT_TAIL) != 0;
+      const bool rloop = use_h && !exact;
+      cudaGraphConditionalHandle hr = 0;
+      if (rloop) {
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, nullptr, nullptr));
+        CK(cudaGraphConditionalHandleCreate(&hr, cg, 0, cudaGraphCondAssignDefault));
+      }
+      launch_tail_prepare(pp, ctx->perm, ctx->P.area2, ctx->wd, ctx->off, ctx->scratch,
+                          ctx->pair_cap, ctx->cands, ctx->d_status, s, hr, rloop ? 1 : 0);
+      nl++;
+      auto round = [&](int use_r) -> tabi_status {
         CK(cudaMemsetAsync(&ctx->d_status->pad[1], 0, sizeof(int32_t), s));
         launch_profiles(ctx->P, ctx->perm, pt, ctx->colofs, ctx->rowofs, (int16_t*)ctx->dcol,
                         (int16_t*)ctx->drow, ctx->wd, ctx->hd, ctx->cand_bad, ctx->big_list,
                         ctx->d_status, s);
         launch_offsets(pt, ctx->colofs, ctx->rowofs, (const int16_t*)ctx->drow, ctx->wd, ctx->hd,
                        ctx->off, ctx->lockbits, ctx->cand_bad, ctx->d_status, s);
-        launch_tail_layout(pt, ctx->wd, ctx->off, ctx->scratch, ctx->pair_cap, ctx->d_status, s);
-        nl += 4;
+        launch_tail_layout(pt, ctx->wd, ctx->off, ctx->scratch, ctx->pair_cap, ctx->d_status, s, hr,
+                           use_r);
+        return TABI_OK;
+      };
+      if (rloop) {
+        if (!ctx->cap_stream2) CK(cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking));
+        const cudaStream_t ms = s;
+        cudaGraph_t body = nullptr;
+        CK(add_while(s, hr, body));
+        s = ctx->cap_stream2;
+        cudaError_t ce = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeThreadLocal);
+        tabi_status es = TABI_OK;
+        if (ce == cudaSuccess) {
+          es = round(1);
+          cudaGraph_t bg = nullptr;
+          const cudaError_t e2 = cudaStreamEndCapture(s, &bg);
+          if (ce == cudaSuccess) ce = e2;
+        }
+        s = ms;
+        if (es != TABI_OK) return es;
+        CK(ce);
+        // (the rounds' 4 kernels each are counted from Status::rounds_run)
+      } else {
+        const int rounds = exact ? 0 : 9;
+        for (int r = 0; r < rounds; r++) {
+          const tabi_status es = round(0);
+          if (es != TABI_OK) return es;
+          nl += 4;
+        }
       }
       PackParams pm = pp;
       pm.mode = 1;
@@ -787,22 +850,12 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         }
         if (es == TABI_OK && ce == cudaSuccess) {
           // WHILE node after wave 0; its body captured from a second stream
-          const cudaGraphNode_t* deps = nullptr;
-          size_t ndeps = 0;
-          ce = cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &ndeps);
-          cudaGraphNodeParams cp = {};
-          cp.type = cudaGraphNodeTypeConditional;
-          cp.conditional.handle = h;
-          cp.conditional.type = cudaGraphCondTypeWhile;
-          cp.conditional.size = 1;
-          cudaGraphNode_t cn = nullptr;
-          if (ce == cudaSuccess) ce = cudaGraphAddNode(&cn, cg, deps, ndeps, &cp);
-          if (ce == cudaSuccess)
-            ce = cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies);
+          cudaGraph_t body = nullptr;
+          ce = add_while(s, h, body);
           if (ce == cudaSuccess) {
             const cudaStream_t ms = s;
             s = ctx->cap_stream;
-            ce = cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+            ce = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeThreadLocal);
             if (ce == cudaSuccess) {
               es = enqueue_body(0, nbody, h, 1);
@@ -817,11 +870,13 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         const cudaError_t ee = cudaStreamEndCapture(s, &g);
         s = user_s;
         if (ce == cudaSuccess) ce = ee;
-        if (es != TABI_OK) {
+        if (es != TABI_OK && es != TABI_ECUDA) {
           if (g) cudaGraphDestroy(g);
           return es;
         }
         cudaError_t ie = ce;
+        if (es == TABI_ECUDA && ie == cudaSuccess)
+          ie = ctx->last_cuda != cudaSuccess ? ctx->last_cuda : cudaErrorUnknown;
         if (ie == cudaSuccess) ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
         if (g) cudaGraphDestroy(g);
         if (ie != cudaSuccess) {
@@ -864,7 +919,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     }
     CK(cudaStreamSynchronize(s));
     const Status st = *ctx->h_status;
-    if (device_loop) launches += ctx->g_launches + ctx->g_body * st.wave;
+    if (device_loop) launches += ctx->g_launches + ctx->g_body * st.wave + 4 * st.rounds_run;
     if (st.bad_chart != INT32_MAX) {
       if (info) info->bad_chart = st.bad_chart;
       return TABI_EINVAL;

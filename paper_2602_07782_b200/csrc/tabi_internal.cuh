@@ -322,7 +322,9 @@ struct Status {       // device-side status block, copied back once per pack
   int32_t win_j;      // fused, sequential mode: smallest wave slot that succeeded
   int32_t b0;         // wave 0's candidate slots in use (prep_kernel; <= B)
   int32_t wave;       // current candidate wave (reset_kernel / wave_ctl_kernel advance it)
-  int32_t wave_pad;
+  int32_t tail_cnt;   // hybrid tail kernels: CTAs done (the last one decides the rounds loop)
+  int32_t rounds_run; // hybrid tail: re-layout rounds run by the graph's rounds loop
+  int32_t st_pad2;
   int32_t wmax, hmax; // largest chart width / height (units; prep_kernel): a
                       // candidate whose scaled largest chart exceeds the dilated
                       // atlas fails at once (cand_too_big)
@@ -533,11 +535,15 @@ void launch_select(const PackParams& pp, const Proxies& P, const int32_t* perm, 
 }  // namespace tabi
 
 namespace tabi {
+// (with use_h: the last CTA sets the rounds loop's condition h -- "some
+// candidate still needs a re-layout round")
 void launch_tail_prepare(const PackParams& pp, const int32_t* perm, const int64_t* area2,
                          const int32_t* wd, const int32_t* off, int32_t* scratch, int64_t pair_cap,
-                         Cand* cands, const Status* st, cudaStream_t s);
+                         Cand* cands, Status* st, cudaStream_t s, cudaGraphConditionalHandle h = 0,
+                         int use_h = 0);
 void launch_tail_layout(const PackParams& pp, const int32_t* wd, const int32_t* off,
-                        int32_t* scratch, int64_t pair_cap, const Status* st, cudaStream_t s);
+                        int32_t* scratch, int64_t pair_cap, Status* st, cudaStream_t s,
+                        cudaGraphConditionalHandle h = 0, int use_h = 0);
 }  // namespace tabi
 
 #include <atomic>

@@ -3,7 +3,7 @@
     python tools/profile_once.py [--workload C5|C3|C2|C4|...] [--rho 1.5] [--warmup 3] [--atlases 512]
 C5: one tabi_pack_many of the batch (4 kernels: reset, proxies, sort+slots,
 pack queue); single-pack workloads: one tabi_pack (reset, proxy, sort+prep,
-fused wave, select).
+fused wave, select; with TABI_GRAPH=0, see below).
 """
 import argparse
 import os
@@ -32,12 +32,16 @@ if a.workload == "C5":
     torch.cuda.synchronize()
     print("atlases", len(sets), "evaluated", bi.candidates_evaluated, "launches/pack", bi.gpu_launches)
 else:
+    # ncu cannot profile the kernel nodes of a graph that holds a conditional
+    # node (the device-side wave loop): the host-driven loop enqueues the same
+    # kernels one by one
+    os.environ["TABI_GRAPH"] = "0"
     cs, _ = bench.workload(a.workload, 0, a.rho)
     ctx = Context(0, max_charts=max(cs.n_charts, 1024), max_vertices=cs.n_vertices + 16,
                   max_atlas_side=max(cs.atlas_w, cs.atlas_h))
     xy = torch.from_numpy(cs.xy).cuda()
     st = torch.from_numpy(cs.start).cuda()
     for _ in range(a.warmup + 1):
-        s, _, info = ctx.pack(xy, st, spec_of(cs))
+        s, _, info = ctx.pack(xy, st, spec_of(cs, **bench.WORKLOAD_SPEC.get(a.workload, {})))
     torch.cuda.synchronize()
     print("m", info.scale_index, "launches/pack", info.gpu_launches)
