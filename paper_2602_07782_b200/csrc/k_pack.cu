@@ -1863,6 +1863,11 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
                               const Cand* __restrict__ cands, tabi_placement* out, Status* st,
                               cudaGraphConditionalHandle h, int use_h) {
   __shared__ int32_t win, wr0, wp;
+  // this thread's chart and pose do not depend on the winner: their loads go
+  // out first, beside the status and candidate loads (one latency, not three)
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = s < pp.n ? perm[s] : 0;
+  const uint8_t ps = s < pp.n ? pose[c] : 0, prr = s < pp.n ? prerot[c] : 0;
   if (st->bad_chart != INT32_MAX || st->capacity) {
     if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0u);
     return;
@@ -1931,11 +1936,8 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
     }
   }
   if (m == 0) return;
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= pp.n) return;
   const int64_t b = (int64_t)(m - 1) * pp.n + s;
-  const int c = perm[s];
-  const uint8_t ps = pose[c];
   const bool tail = s >= wr0;  // tail chart: final scale p / 2^20 (D24) ...
   const bool ptail = tail && !(pp.flags & TABI_F_EXACT_TAIL);  // ... or m/M (R6)
   tabi_placement p;
@@ -1950,7 +1952,7 @@ __global__ void select_kernel(PackParams pp, const int32_t* __restrict__ perm,
   p.flip_y = (ps >> 2) & 1;
   p.mirror_x = mir[b];
   p.mode = tail ? 1 : 0;
-  p.prerot = prerot[c];
+  p.prerot = prr;
   p.pad[0] = p.pad[1] = 0;
   out[c] = p;
 }

@@ -184,9 +184,12 @@ bitonic_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, i
 // and 2t + 1 in registers: the compare-exchange stages of element distance
 // <= 32 are warp shuffles (partner thread t ^ (stride / 2), same slot) with no
 // barrier; only distances >= 64 go through shared memory.
-__device__ __forceinline__ void bitonic_reg_body(const int32_t* __restrict__ hh,
-                                                 const int32_t* __restrict__ ww, int32_t n,
-                                                 int32_t* perm) {
+// Returns the sorted keys in shared memory (valid after a barrier): a
+// following slot layout reads each position's (h, w, chart) from them instead
+// of a dependent perm -> proxy load chain.
+__device__ __forceinline__ const uint64_t* bitonic_reg_body(const int32_t* __restrict__ hh,
+                                                            const int32_t* __restrict__ ww,
+                                                            int32_t n, int32_t* perm) {
   __shared__ uint64_t key[2 * kT];
   const int t = threadIdx.x;
   uint64_t v[2];
@@ -232,7 +235,9 @@ __device__ __forceinline__ void bitonic_reg_body(const int32_t* __restrict__ hh,
   for (int s = 0; s < 2; s++) {
     const int i = 2 * t + s;
     if (i < n) perm[i] = (int32_t)(v[s] & 0xfffu);
+    key[i] = v[s];  // (own slots only: the last smem pass read just these)
   }
+  return key;
 }
 
 __global__ void __launch_bounds__(kT, 1)
@@ -387,7 +392,8 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
                                           const int32_t* __restrict__ ww, const int64_t* area2,
                                           const int32_t* perm, const PackParams& pp, int32_t* colofs,
                                           int32_t* rowofs, int32_t* hsorted, int32_t* tstart,
-                                          int32_t* tix, Status* st, int32_t* rdy) {
+                                          int32_t* tix, Status* st, int32_t* rdy,
+                                          const uint64_t* skey = nullptr) {
   __shared__ int32_t sh[2][kW + 1];
   __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
@@ -451,12 +457,21 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
     const int s = t0 + threadIdx.x;
     int32_t cw = 0, rh = 0;
     if (s < pp.n) {
-      const int c = perm[s];
-      const int64_t wd = ceildiv(ww[c], TABI_UNITS) + 2 * pp.g;
-      const int64_t hd = ceildiv(hh[c], TABI_UNITS) + 2 * pp.g;
+      int32_t w, h;
+      if (skey) {  // the sorted key holds (h, w): no dependent global loads
+        const uint64_t k = skey[s];
+        h = (int32_t)(0x3ffffffu - (uint32_t)((k >> 38) & 0x3ffffffu));
+        w = (int32_t)(0x3ffffffu - (uint32_t)((k >> 12) & 0x3ffffffu));
+      } else {
+        const int c = perm[s];
+        w = ww[c];
+        h = hh[c];
+      }
+      const int64_t wd = ceildiv(w, TABI_UNITS) + 2 * pp.g;
+      const int64_t hd = ceildiv(h, TABI_UNITS) + 2 * pp.g;
       cw = (int32_t)(wd < pp.Wp ? wd : pp.Wp);
       rh = (int32_t)(hd < pp.Hp ? hd : pp.Hp);
-      hsorted[s] = hh[c];
+      hsorted[s] = h;
     }
     int32_t ec, er, tc, tr;
     block_scan2(cw, rh, ec, er, tc, tr, sh);
@@ -528,9 +543,9 @@ sort_prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
                  int32_t* rdy) {
   if (st->bad_chart != INT32_MAX) return;
-  bitonic_reg_body(hh, ww, pp.n, perm);
+  const uint64_t* skey = bitonic_reg_body(hh, ww, pp.n, perm);
   __syncthreads();
-  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy);
+  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy, skey);
 }
 
 // Batch mode (tabi_pack_many): one CTA per atlas -- its order (register
@@ -546,10 +561,10 @@ many_sort_prep_kernel(Proxies P, const int32_t* __restrict__ abase, int32_t* per
   if (n < 1 || n > 2 * kT || st->bad_chart != INT32_MAX || st->capacity) return;
   PackParams q = pp;
   q.n = n;
-  bitonic_reg_body(P.h + c0, P.w + c0, n, perm + c0);
+  const uint64_t* skey = bitonic_reg_body(P.h + c0, P.w + c0, n, perm + c0);
   __syncthreads();
   prep_body(P.h + c0, P.w + c0, P.area2 + c0, perm + c0, q, colofs + c0, rowofs + c0,
-            hsorted + c0, tstart + c0 + a, tix + c0, st, nullptr);
+            hsorted + c0, tstart + c0 + a, tix + c0, st, nullptr, skey);
 }
 
 // Batch mode: per-atlas status blocks and results, and the pack work queue

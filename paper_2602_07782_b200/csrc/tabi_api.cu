@@ -23,9 +23,18 @@
 #include <cstring>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "tabi_internal.cuh"
 
 using namespace tabi;
+
+// NVTX range for the host-side phases of a call (header-only NVTX3: free
+// unless a profiler is attached)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 // Everything a captured first-wave graph bakes in: if any of it changes, the
 // graph is re-captured.
@@ -417,6 +426,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
                                  int32_t n, float res_x, float res_y, const tabi_spec* spec,
                                  tabi_placement* out, tabi_info* info, int on_device,
                                  void* stream) {
+  Nvtx nv_("tabi_pack");
   if (!ctx) return TABI_EINVAL;
   if (ctx->pend) {
     ctx->err = "an asynchronous pack is pending on this context (tabi_pack_wait first)";
@@ -440,6 +450,7 @@ extern "C" tabi_status tabi_pack(tabi_ctx* ctx, const float* xy, const int32_t* 
 extern "C" tabi_status tabi_pack_async(tabi_ctx* ctx, const float* xy, const int32_t* chart_start,
                                        int32_t n, float res_x, float res_y, const tabi_spec* spec,
                                        tabi_placement* out, void* stream) {
+  Nvtx nv_("tabi_pack_async");
   if (!ctx) return TABI_EINVAL;
   if (ctx->pend) {
     ctx->err = "an asynchronous pack is already pending on this context";
@@ -461,6 +472,7 @@ extern "C" tabi_status tabi_pack_query(tabi_ctx* ctx) {
 }
 
 extern "C" tabi_status tabi_pack_wait(tabi_ctx* ctx, tabi_info* info) {
+  Nvtx nv_("tabi_pack_wait");
   if (!ctx || !ctx->pend) return TABI_EINVAL;
   ctx->pend = false;
   const PendArgs a = ctx->pend_args;
@@ -491,6 +503,7 @@ extern "C" tabi_status tabi_validate(tabi_ctx* ctx, const float* xy, const int32
                                      int32_t n, float res_x, float res_y, int32_t W, int32_t H,
                                      int32_t g, const tabi_placement* placements,
                                      tabi_validation* out, int on_device, void* stream) {
+  Nvtx nv_("tabi_validate");
   if (!ctx || !out) return TABI_EINVAL;
   memset(out, 0, sizeof(*out));
   out->bad_chart = -1;
@@ -825,8 +838,20 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
                    on_device ? (const void*)out : nullptr, n, V_in, on_device, res_x, res_y, *spec, B,
                    fused ? 1 : 0, ctx->alloc_gen, sort_env};
       if (!ctx->gexec || !(key == ctx->gkey)) {
-        if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-        ctx->gexec = nullptr;
+        // Only the caller's device pointers changed (same sizes, spec and
+        // buffers): the re-captured graph has the same topology, so the
+        // instantiated graph is updated in place (cudaGraphExecUpdate) rather
+        // than re-instantiated.
+        GraphKey kp = key;
+        kp.xy = ctx->gkey.xy;
+        kp.start = ctx->gkey.start;
+        kp.out = ctx->gkey.out;
+        const bool try_update = ctx->gexec && kp == ctx->gkey;
+        if (ctx->gexec && !try_update) {
+          cudaGraphExecDestroy(ctx->gexec);
+          ctx->gexec = nullptr;
+        }
+        Nvtx nv_cap(try_update ? "graph capture + update" : "graph capture + instantiate");
         if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
         cudaGraph_t g = nullptr;
         int npro = 0, nbody = 0;
@@ -877,12 +902,24 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         cudaError_t ie = ce;
         if (es == TABI_ECUDA && ie == cudaSuccess)
           ie = ctx->last_cuda != cudaSuccess ? ctx->last_cuda : cudaErrorUnknown;
-        if (ie == cudaSuccess) ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
+        if (ie == cudaSuccess && try_update) {
+          cudaGraphExecUpdateResultInfo ui;
+          if (cudaGraphExecUpdate(ctx->gexec, g, &ui) != cudaSuccess) {
+            cudaGetLastError();  // (topology not updatable here: instantiate anew)
+            cudaGraphExecDestroy(ctx->gexec);
+            ctx->gexec = nullptr;
+          }
+        } else if (ctx->gexec) {
+          cudaGraphExecDestroy(ctx->gexec);
+          ctx->gexec = nullptr;
+        }
+        if (ie == cudaSuccess && !ctx->gexec) ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
         if (g) cudaGraphDestroy(g);
         if (ie != cudaSuccess) {
           // no conditional-node graph here (driver, cooperative launch in a
           // loop body, ...): the host-driven loop from now on
           cudaGetLastError();
+          if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
           ctx->gexec = nullptr;
           ctx->loop_off = true;
           ctx->err = std::string("device wave loop unavailable: ") + cudaGetErrorString(ie);
@@ -894,9 +931,12 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         ctx->g_launches = npro;
         ctx->g_body = nbody;
       }
+      Nvtx nv_l("graph launch: proxies, sort, every candidate wave, results");
       CK(cudaEventRecord(ctx->span[0], s));
       CK(cudaGraphLaunch(ctx->gexec, s));
     } else {
+      Nvtx nv_w(wave == 0 ? (first ? "host-driven wave 0" : "capacity retry, wave 0")
+                          : "host-driven further wave");
       int nl = 0;
       if (first) CK(cudaEventRecord(ctx->span[0], s));
       if (wave == 0) {
@@ -917,7 +957,10 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
       ctx->pend_args = PendArgs{xy, chart_start, n, res_x, res_y, *spec, out, stream};
       return TABI_OK;
     }
-    CK(cudaStreamSynchronize(s));
+    {
+      Nvtx nv_s("wait for the device");
+      CK(cudaStreamSynchronize(s));
+    }
     const Status st = *ctx->h_status;
     if (device_loop) launches += ctx->g_launches + ctx->g_body * st.wave + 4 * st.rounds_run;
     if (st.bad_chart != INT32_MAX) {
@@ -1112,6 +1155,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
                                       tabi_placement* out, tabi_info* infos,
                                       int32_t* atlas_status, tabi_batch_info* binfo, int on_device,
                                       void* stream) {
+  Nvtx nv_("tabi_pack_many");
   if (!ctx) return TABI_EINVAL;
   if (binfo) memset(binfo, 0, sizeof(*binfo));
   if (A < 1 || !xy || !chart_start || !atlas_start || !out || !spec_ok(spec)) return TABI_EINVAL;
@@ -1178,6 +1222,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
                                  std::max(spec->atlas_w, spec->atlas_h));
     if (ts != TABI_OK) return ts;
     ManyWs& w = ctx->many;
+    Nvtx nv_b("tabi_pack_many: enqueue inputs, proxies, sort + slots, batch kernel, results");
     CK(cudaEventRecord(w.span[0], s));
     const float* d_xy = xy;
     const int32_t* d_start = chart_start;
@@ -1332,6 +1377,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
   }
   // solo atlases (hybrid tail, more than kManyMaxCharts charts, or a capacity
   // retry) through the single-pack path, atlas-local chart offsets
+  Nvtx nv_solo("tabi_pack_many: solo atlases via tabi_pack");
   for (int32_t a : solo) {
     const int32_t c0 = atlas_start[a], n = atlas_start[a + 1] - c0;
     const float rx = res_xy ? res_xy[2 * a] : 1.0f, ry = res_xy ? res_xy[2 * a + 1] : 1.0f;
@@ -1409,6 +1455,7 @@ extern "C" tabi_status tabi_pack_batch(tabi_ctx* const* ctxs, int32_t n_gpus, in
                                        const int32_t* n_charts, const float* res_xy,
                                        const tabi_spec* specs, tabi_placement* const* out,
                                        tabi_info* infos) {
+  Nvtx nv_("tabi_pack_batch");
   if (!ctxs || n_gpus < 1 || n_atlases < 0) return TABI_EINVAL;
   if (n_atlases == 0) return TABI_OK;
   if (!xy || !chart_start || !n_charts || !specs || !out) return TABI_EINVAL;
@@ -1423,6 +1470,7 @@ extern "C" tabi_status tabi_pack_batch(tabi_ctx* const* ctxs, int32_t n_gpus, in
   std::vector<std::thread> th;
   for (int32_t g = 0; g < n_gpus; g++) {
     th.emplace_back([&, g]() {
+      Nvtx nv_g("tabi_pack_batch: one GPU's atlases");
       tabi_ctx* ctx = ctxs[g];
       std::vector<int32_t> mine;
       for (int32_t i = 0; i < n_atlases; i++)

@@ -156,3 +156,33 @@ def test_async_capacity_growth_and_errors():
     assert st == EINVAL and info.bad_chart == 5
     c.close()
     ref.close()
+
+
+def test_new_device_pointers_update_the_graph(ctx):
+    """Device-pointer packs whose buffers move between calls (same sizes and
+    spec): the graph is re-captured and updated in place -- every call still
+    reads its own inputs and writes its own output."""
+    import torch
+    from paper_2602_07782_b200 import OK, spec_of
+    cs = chartgen.config2(3)
+    ref = None
+    for i in range(4):
+        xy, start = _dev(cs)
+        pad = torch.zeros(1024 * (i + 1), device="cuda")  # (moves later allocations)
+        st, out, info = ctx.pack(xy, start, spec_of(cs))
+        torch.cuda.synchronize()
+        assert st == OK
+        b = out.cpu().numpy().tobytes()
+        ref = ref or b
+        assert b == ref
+        del pad
+    # another chart set with the same chart count (other vertex count): the
+    # updated graph must read the new buffers, not the previous call's
+    cs2 = chartgen.config2(4)
+    assert cs2.n_charts == cs.n_charts
+    xy2, start2 = _dev(cs2)
+    st, out2, _ = ctx.pack(xy2, start2, spec_of(cs2))
+    st_h, pl_h, _ = ctx.pack(cs2.xy, cs2.start, spec_of(cs2))
+    torch.cuda.synchronize()
+    assert st == st_h == OK
+    assert out2.cpu().numpy().tobytes() == pl_h.tobytes()
