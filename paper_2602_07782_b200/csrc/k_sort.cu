@@ -145,7 +145,7 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
 // 64 bits for N <= 4096 and the packed keys are unique: any correct sort gives
 // the stable order.
 #ifndef TABI_B0_FILL
-#define TABI_B0_FILL 60  // wave 0 reaches down to the scale filling this % of the atlas
+#define TABI_B0_FILL 55  // wave 0 reaches down to the scale filling this % of the atlas
 #endif
 constexpr int kBitonicMax = 4096;
 constexpr int kRankMax = 1 << 17;
@@ -436,7 +436,7 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
         if ((i128)m * m * tot <= rhs) { m_hi = m; break; }
       st->pad[2] = m_hi;
       // Wave 0's width: the candidates from m_hi down to the scale at which
-      // the charts would fill 60 % of the atlas -- below that a success is
+      // the charts would fill 55 % of the atlas (TSS sets pack at ~60 %) -- below that a success is
       // unlikely, and a narrower first wave leaves the top candidate's chain
       // with less contention.  Later waves take B each and the wave loop's
       // stopping rule (select_kernel; hybrid mode: the V bound of D25) is
