@@ -5,7 +5,7 @@ and the batch kernel draws (atlas, candidate) items from a device queue, so
 the order in which CTAs run differs from call to call.  The method's result
 must not (P:85 / P:1025: one overlap-free packing per input; BASELINE
 north_star: "deterministic tie-breaking").  compute-sanitizer is not
-available on the GPU pool (DESIGN.md §5 "race evidence"), so races are hunted
+available on the GPU pool (DESIGN.md §6 "Race evidence"), so races are hunted
 by repetition here: 100 packs of C3 at rho = 2.0 (the knee-rich case, several
 candidates per wave) must return identical bytes, the same bytes as the split
 (non-fused) path and as one-candidate waves, and a batch must be identical
