@@ -201,7 +201,7 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   Group<G> g;
   g.gl = lane % G;
   g.mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane / G * G));
-  const int c = blockIdx.x * (kBlock / G) + gib;
+  const int c = am.c0 + blockIdx.x * (kBlock / G) + gib;
   if (c >= n) return;  // the whole group leaves together
   // batch mode (tabi_pack_many): chart c is global; its atlas a is the last
   // with abase[a] <= c (uniform per group), which owns the status block, the
@@ -413,7 +413,8 @@ void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float 
               uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
               AtlasMap am, cudaStream_t s) {
   constexpr int per_block = kBlock / G;
-  const int blocks = (n + per_block - 1) / per_block;
+  const int blocks = (n - am.c0 + per_block - 1) / per_block;
+  if (blocks < 1) return;
   const size_t smem = slice_bytes(k) * per_block;
   static std::atomic<unsigned long long> attr{0};  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
   ensure_dyn_smem((const void*)proxy_kernel<G>, (int)(slice_bytes(TABI_KMAX) * per_block), attr);

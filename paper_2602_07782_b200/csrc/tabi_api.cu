@@ -110,6 +110,8 @@ struct ManyWs {
   int64_t h_out_cap = 0;
   cudaEvent_t span[2] = {nullptr, nullptr};
   cudaEvent_t stage[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // TABI_TIMING
+  cudaStream_t copy_stream = nullptr;  // host mode: chunked outline upload
+  cudaEvent_t chunk_ev[9] = {};
   void release() {
     void* ds[] = {d_xy, d_start, qx, qy, P.w, P.h, P.area2, P.xmin, P.ymin, P.pose, P.prerot, P.sl,
                   P.obb_j, P.obb, perm, colofs, rowofs, hsorted, tstart, tix, d_out, d_small, sts,
@@ -124,6 +126,9 @@ struct ManyWs {
       if (e) cudaEventDestroy(e);
     for (auto& e : stage)
       if (e) cudaEventDestroy(e);
+    for (auto& e : chunk_ev)
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
   }
 };
 
@@ -1226,11 +1231,18 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     CK(cudaEventRecord(w.span[0], s));
     const float* d_xy = xy;
     const int32_t* d_start = chart_start;
+    // host mode: the outlines go up in chunks on a copy stream, each chunk's
+    // proxies starting as soon as it lands (the copy of chunk j + 1 overlaps
+    // the proxies of chunk j); pinned caller memory is copied directly,
+    // pageable memory via staging
+    const float* xy_src = xy;
+    const char* chenv = getenv("TABI_UPLOAD_CHUNKS");  // test knob: 1..8 (default 8)
+    const int nch_max = chenv ? std::min(8, std::max(1, atoi(chenv))) : 8;
+    const int nch = on_device ? 1 : (N >= 8 * 2048 ? nch_max : 1);
+    int32_t cbound[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j <= nch; j++) cbound[j] = (int32_t)((int64_t)N * j / nch);
     if (!on_device) {
-      // pinned caller memory is copied directly; pageable memory via staging
-      if (host_pinned(xy)) {
-        CK(cudaMemcpyAsync(w.d_xy, xy, sizeof(float) * 2 * V, cudaMemcpyHostToDevice, s));
-      } else {
+      if (!host_pinned(xy)) {
         if (w.h_cap < 2 * V) {
           if (w.h_xy) cudaFreeHost(w.h_xy);
           w.h_xy = nullptr;
@@ -1238,11 +1250,25 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
           w.h_cap = 2 * V;
         }
         memcpy(w.h_xy, xy, sizeof(float) * 2 * V);
-        CK(cudaMemcpyAsync(w.d_xy, w.h_xy, sizeof(float) * 2 * V, cudaMemcpyHostToDevice, s));
+        xy_src = w.h_xy;
       }
       CK(cudaMemcpyAsync(w.d_start, chart_start, sizeof(int32_t) * (N + 1), cudaMemcpyHostToDevice, s));
       d_xy = w.d_xy;
       d_start = w.d_start;
+      if (!w.copy_stream) {
+        CK(cudaStreamCreateWithFlags(&w.copy_stream, cudaStreamNonBlocking));
+        for (auto& e : w.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      // (the copy stream starts after everything before this call on s)
+      CK(cudaEventRecord(w.chunk_ev[8], s));
+      CK(cudaStreamWaitEvent(w.copy_stream, w.chunk_ev[8], 0));
+      for (int j = 0; j < nch; j++) {
+        const int64_t v0 = chart_start[cbound[j]], v1 = chart_start[cbound[j + 1]];
+        if (v1 > v0)
+          CK(cudaMemcpyAsync(w.d_xy + 2 * v0, xy_src + 2 * v0, sizeof(float) * 2 * (v1 - v0),
+                             cudaMemcpyHostToDevice, w.copy_stream));
+        CK(cudaEventRecord(w.chunk_ev[j], w.copy_stream));
+      }
     }
     // abase (A + 1) | order (E) | res (2A floats): one upload
     int32_t* hs = w.h_small;
@@ -1276,8 +1302,13 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, s);
     CK(cudaMemsetAsync(w.cycles, 0, 3 * sizeof(unsigned long long), s));
     if (timing) CK(cudaEventRecord(w.stage[0], s));
-    launch_proxies(d_xy, d_start, (int32_t)N, 1.0f, 1.0f, pp.k, pp.flags, w.qx, w.qy, w.cap_V, w.P,
-                   w.sts, s, AtlasMap{d_abase, A, d_res}, V);
+    for (int j = 0; j < nch; j++) {
+      if (!on_device) CK(cudaStreamWaitEvent(s, w.chunk_ev[j], 0));
+      // (nverts scaled to the chunk's end keeps the lane-group choice of the whole batch)
+      launch_proxies(d_xy, d_start, cbound[j + 1], 1.0f, 1.0f, pp.k, pp.flags, w.qx, w.qy, w.cap_V,
+                     w.P, w.sts, s, AtlasMap{d_abase, A, d_res, cbound[j]},
+                     V * cbound[j + 1] / N);
+    }
     if (timing) CK(cudaEventRecord(w.stage[1], s));
     launch_many_sort_prep(w.P, d_abase, A, w.perm, pp, w.colofs, w.rowofs, w.hsorted, w.tstart,
                           w.tix, w.sts, s);

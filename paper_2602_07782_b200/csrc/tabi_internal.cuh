@@ -430,6 +430,7 @@ struct AtlasMap {
   const int32_t* abase;
   int32_t na;
   const float* res;
+  int32_t c0;  // first chart of this launch (charts [c0, n)); 0 for one launch
 };
 // max_v: capacity of qx/qy; a chart's vertex range outside [0, max_v) sets
 // Status::capacity bit 2 (-> TABI_ECAPACITY) before anything is written

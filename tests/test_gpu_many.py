@@ -215,3 +215,40 @@ def test_pack_many_lazy_and_early_fail_are_exact(ctx, monkeypatch, mode):
     assert [i.scale_index for i in ref[2]] == [i.scale_index for i in alt[2]]
     assert ref[1].tobytes() == alt[1].tobytes()
     assert ref[4].candidates_evaluated == alt[4].candidates_evaluated
+
+
+def test_pack_many_host_pinned_chunked_upload(ctx):
+    """Host-pointer batch from pinned memory, large enough for the chunked
+    outline upload (8 chunks on a copy stream, each chunk's proxies behind its
+    copy): the same bytes as the device-pointer batch, with one chunk, and
+    from pageable host buffers."""
+    import torch
+    from paper_2602_07782_b200 import OK, PLACEMENT_DTYPE, concat_chart_sets, spec_of
+    sets = [chartgen.config5(i) for i in range(24)]
+    xy, cst, abase, res = concat_chart_sets(sets)
+    assert abase[-1] >= 8 * 2048
+    st_d, out_d, _, ast_d, _ = ctx.pack_many(torch.from_numpy(xy).cuda(),
+                                             torch.from_numpy(cst).cuda(), abase,
+                                             spec_of(sets[0]), res_xy=res)
+    torch.cuda.synchronize()
+    ref = out_d.cpu().numpy().tobytes()
+    xy_p = torch.from_numpy(xy).pin_memory().numpy()
+    cst_p = torch.from_numpy(cst).pin_memory().numpy()
+    out_p = torch.empty(int(abase[-1]) * 32, dtype=torch.uint8).pin_memory().numpy().view(PLACEMENT_DTYPE)
+    for _ in range(2):
+        out_p[:] = np.zeros(1, dtype=PLACEMENT_DTYPE)
+        st, pl, _, ast, _ = ctx.pack_many(xy_p, cst_p, abase, spec_of(sets[0]), res_xy=res, out=out_p)
+        assert st == st_d == OK and list(ast) == list(ast_d)
+        assert pl.tobytes() == ref
+    st, pl, _, ast, _ = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res)  # pageable
+    assert pl.tobytes() == ref
+
+
+def test_pack_many_one_upload_chunk(ctx, monkeypatch):
+    from paper_2602_07782_b200 import concat_chart_sets, spec_of
+    sets = [chartgen.config5(i) for i in range(24)]
+    xy, cst, abase, res = concat_chart_sets(sets)
+    _, a, _, _, _ = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res)
+    monkeypatch.setenv("TABI_UPLOAD_CHUNKS", "1")
+    _, b, _, _, _ = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res)
+    assert a.tobytes() == b.tobytes()
