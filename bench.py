@@ -526,7 +526,10 @@ def main():
                       "ok_atlases_this_rank": ok, "l2_stretch_mean": stretch_b,
                       "candidates_evaluated": bi.candidates_evaluated,
                       "solo_atlases": bi.solo_atlases, "library_device_ms": bi.device_ms,
-                      "per_gpu_busy_ms": sum(step_ms) / args.steps},
+                      "per_gpu_busy_ms": sum(step_ms) / args.steps,
+                      # batch-kernel load balance: last CTA's end after the
+                      # median CTA's last item; mean CTA busy fraction
+                      "kernel_tail_ms": bi.tail_ms, "kernel_busy_frac": bi.busy_frac},
             "roofline": roof,
             "hbm_compulsory": {"bytes_per_step": hbm_bytes,
                                "gbs": hbm_bytes / (ms_per_step * 1e-3) / 1e9,

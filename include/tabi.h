@@ -221,6 +221,9 @@ typedef struct {
   int64_t work_profile;           /* batch kernel: footprint entries rasterized (Wd + Hd) */
   int64_t cycles[3];              /* batch kernel: SM cycles summed over its items, in
                                      footprint rasterization, pair offsets + locks, Alg. 4 */
+  float tail_ms;                  /* batch kernel load balance: time from the median CTA's
+                                     last item end to the last CTA's */
+  float busy_frac;                /* mean over CTAs of (last item end - start) / kernel span */
 } tabi_batch_info;
 
 tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t n_atlases, const float* xy,

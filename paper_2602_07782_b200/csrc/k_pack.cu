@@ -1689,6 +1689,8 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
   int32_t* cbad = A.cand_bad + gcta;
   const int k = pp0.k, g = pp0.g;
   const int64_t SCm = (int64_t)pp0.M * TABI_UNITS;
+  // per-CTA timeline (globaltimer ns): start, end of its last item
+  if (tid == 0) A.cycles[3 + 2 * gcta] = A.cycles[3 + 2 * gcta + 1] = gtime();
   while (true) {
     if (tid == 0) {
       const int i = atomicAdd(&A.qctl[0], 1);
@@ -1849,6 +1851,7 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
         __threadfence();
         atomicSub(&A.qctl[2], 1);
       }
+      A.cycles[3 + 2 * gcta + 1] = gtime();
     }
   }
 }

@@ -102,6 +102,8 @@ struct ManyWs {
   unsigned long long* cycles = nullptr;   // [3] batch kernel phase cycles
   int64_t* area = nullptr;                // [G][nmax] lazy batch mode
   unsigned long long h_cycles[3] = {0, 0, 0};
+  int64_t cycles_cap = 0;
+  std::vector<unsigned long long> h_cta;  // per CTA: start, last item end (ns)
   int32_t* solo_start = nullptr;  // rebased chart offsets of a solo atlas (device mode)
   // pinned host staging for host-mode inputs / outputs
   float* h_xy = nullptr;          // 2V floats + N + 1 ints
@@ -1123,7 +1125,11 @@ static tabi_status many_ensure(tabi_ctx* ctx, int64_t N, int64_t V, int32_t A, i
     CK(grow(&w.cands, G)); CK(grow(&w.cand_bad, G));
     CK(grow(&w.area, G * nm));
   }
-  if (!w.cycles) CK(grow(&w.cycles, 3));
+  if (w.cycles_cap < 3 + 2 * (int64_t)w.G) {
+    CK(grow(&w.cycles, 3 + 2 * (int64_t)w.G));
+    w.cycles_cap = 3 + 2 * (int64_t)w.G;
+    w.h_cta.assign(2 * (size_t)w.G, 0ull);
+  }
   return TABI_OK;
 }
 
@@ -1368,6 +1374,8 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     CK(cudaMemcpyAsync(w.h_sts, w.sts, sizeof(Status) * A, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_res, w.res, sizeof(AtlasRes) * A, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_cycles, w.cycles, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_cta.data(), w.cycles + 3, 2 * (size_t)w.G * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(w.span[1], s));
     CK(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&dev_ms, w.span[0], w.span[1]);
@@ -1450,6 +1458,25 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     binfo->work_pack = work_pack;
     binfo->work_profile = work_prof;
     for (int i = 0; i < 3; i++) binfo->cycles[i] = E > 0 ? (int64_t)ctx->many.h_cycles[i] : 0;
+    // load balance of the batch kernel: how long the last CTAs ran after the
+    // median CTA finished its last item, and the mean busy fraction
+    const ManyWs& w = ctx->many;
+    if (E > 0 && w.G > 0 && (int64_t)w.h_cta.size() >= 2 * (int64_t)w.G) {
+      unsigned long long t0 = ~0ull, t1 = 0;
+      std::vector<unsigned long long> ends(w.G);
+      for (int g = 0; g < w.G; g++) {
+        t0 = std::min(t0, w.h_cta[2 * g]);
+        t1 = std::max(t1, w.h_cta[2 * g + 1]);
+        ends[g] = w.h_cta[2 * g + 1];
+      }
+      std::sort(ends.begin(), ends.end());
+      double busy = 0.0;
+      for (int g = 0; g < w.G; g++) busy += (double)(w.h_cta[2 * g + 1] - w.h_cta[2 * g]);
+      if (t1 > t0) {
+        binfo->tail_ms = (float)((double)(t1 - ends[w.G / 2]) * 1e-6);
+        binfo->busy_frac = (float)(busy / ((double)w.G * (double)(t1 - t0)));
+      }
+    }
     if (lazy_used) binfo->cycles[2] = std::max<int64_t>(0, binfo->cycles[2] - binfo->cycles[0] - binfo->cycles[1]);
   }
   return ret;

@@ -509,7 +509,8 @@ struct ManyArgs {
   uint8_t* mir;
   Cand* cands;                    // [G]
   int32_t* cand_bad;              // [G]
-  unsigned long long* cycles;     // [3] SM cycles summed over items: raster, pairs, packer
+  unsigned long long* cycles;     // [3] SM cycles summed over items: raster, pairs, packer;
+                                  // then [G][2] per CTA: start, end of its last item (ns)
   int64_t* area;                  // [G][nmax] lazy mode: 2 x polygon area by sorted position
   int32_t lazy;                   // rasterize on demand inside the packer (many_lazy_ok)
   int32_t early_fail;             // lazy mode: the row-end area test (R8)

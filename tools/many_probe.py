@@ -34,4 +34,5 @@ for _ in range(a.reps):
     print(f"device {bi.device_ms:.3f} ms  stages " + " ".join(f"{v:.3f}" for v in bi.stage_ms) +
           f"  items {bi.candidates_evaluated}  cycles raster/pairs/pack " +
           " / ".join(f"{100.0 * c / tot:.1f}%" for c in cyc) +
-          f"  per item us {tot / bi.candidates_evaluated / 1965.0:.1f}", flush=True)
+          f"  per item us {tot / bi.candidates_evaluated / 1965.0:.1f}"
+          f"  tail {bi.tail_ms:.3f} ms  busy {100 * bi.busy_frac:.1f}%", flush=True)
