@@ -414,3 +414,14 @@ def test_determinism_and_capacity_growth():
     outs = [small.pack(cs.xy, cs.start, spec_of(cs))[1].tobytes() for _ in range(3)]
     assert outs[0] == outs[1] == outs[2]
     small.close()
+
+
+@pytest.mark.parametrize("a,n,W,g,M", [(30, 400, 1024, 1, 64), (30, 10, 1024, 1, 64),
+                                       (17, 700, 512, 2, 32), (9, 900, 256, 1, 16)])
+def test_prefix_tail_equal_squares_parity(orc, ctx, a, n, W, g, M):
+    """The closed-form tail family of tests/test_oracle_tail_closed_form.py
+    (every chart in the D24 tail; sigma rule, its cap, re-layout rounds, the
+    D25 choice) through the GPU: graph rounds loop, tail kernels, prefix rows."""
+    polys = [[(0, 0), (a, 0), (a, a), (0, a)] for _ in range(n)]
+    cs = chartgen.from_polygons(polys, W, W)
+    _compare_pack(orc, ctx, cs, check_profiles=3, t_opt_bp=1000, gutter=g, scale_count=M)
