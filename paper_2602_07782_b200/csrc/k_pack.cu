@@ -862,7 +862,10 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // prefix rows: FastAtlas fixes the direction in advance (one L->R row,
     // then two R->L) and HC is on, so a prefix row pushes,
     // relaxes and scores ONE configuration (pdir) instead of both directions
-    const int pdir = prefix_mode ? ((S.prefix_rows % 3 == 0) ? 0 : 1) : -1;
+#ifndef TABI_PREFIX_ONECFG
+#define TABI_PREFIX_ONECFG 1
+#endif
+    const int pdir = TABI_PREFIX_ONECFG && prefix_mode ? ((S.prefix_rows % 3 == 0) ? 0 : 1) : -1;
     // A row of at most kRW charts (the normal case) is one window: its Y
     // values then live in shared memory from push to commit, and the fold's
     // window scalars (W.rx1, W.rwd) serve the lock-pair scan; longer rows

@@ -431,9 +431,13 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
       st->wmax = wmx;
       st->hmax = hmx;
       const i128 rhs = (i128)2 * 65536 * pp.W * pp.H * (i128)pp.M * pp.M;
+      // R2: sequential mode only -- every chart keeps m/M, so a successful
+      // (overlap-free, in-bounds) packing needs (m/M)^2 A <= W H.  In hybrid
+      // mode the prefix tail's intermediate downscale (D24) can make a
+      // candidate above that bound succeed, so the search starts at M.
       int m_hi = 0;
       for (int m = pp.M; m >= 1; m--)
-        if ((i128)m * m * tot <= rhs) { m_hi = m; break; }
+        if (pp.t_opt > 0 || (i128)m * m * tot <= rhs) { m_hi = m; break; }
       st->pad[2] = m_hi;
       // Wave 0's width: the candidates from m_hi down to the scale at which
       // the charts would fill 55 % of the atlas (TSS sets pack at ~60 %) -- below that a success is

@@ -139,22 +139,23 @@ __device__ __forceinline__ int64_t fdiv_r128(i128 a, i128 b, double rcp, bool cl
 }
 // Start a running evaluation at i: v = f(i), r = (rA + i*rB) mod D; then
 // lindiv_step moves to i + 1 with one add and one conditional carry (rB < D).
+// rA + i rB is formed in 128 bits: in the hybrid tail the scale denominator is
+// 2^20 x 256, so D = S x 2^28 reaches 2^58 and i rB overflows int64 from a
+// few dozen cells on (the prefix tail's large charts, found by the random
+// parity sweep tests/test_gpu_fuzz.py).
 __device__ __forceinline__ void lindiv_start(const LinDiv& L, int64_t i, int64_t& v, int64_t& r) {
-  const int64_t N = L.rA + i * L.rB;
-  int64_t t = (int64_t)((double)N * L.rcp);
-  int64_t rr = N - t * L.D;
+  const i128 N = (i128)L.rA + (i128)i * L.rB;
+  int64_t t = (int64_t)(i128_to_double(N) * L.rcp);
+  i128 rr = N - (i128)t * L.D;
   while (rr < 0) { t--; rr += L.D; }
   while (rr >= L.D) { t++; rr -= L.D; }
   v = L.qA + i * L.qB + t;
-  r = rr;
+  r = (int64_t)rr;
 }
 __device__ __forceinline__ int64_t lindiv_eval(const LinDiv& L, int64_t i) {
-  const int64_t N = L.rA + i * L.rB;
-  int64_t t = (int64_t)((double)N * L.rcp);
-  int64_t r = N - t * L.D;
-  while (r < 0) { t--; r += L.D; }
-  while (r >= L.D) { t++; r -= L.D; }
-  return L.qA + i * L.qB + t;
+  int64_t v, r;
+  lindiv_start(L, i, v, r);
+  return v;
 }
 
 // ---- warp reductions (full warp) ------------------------------------------

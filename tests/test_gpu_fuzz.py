@@ -1,0 +1,56 @@
+"""Seeded random parity sweep: the CUDA path against the oracle over the spec
+space a user can reach -- chart families (UV, TSS, lightmap, mixed), counts
+and atlas sizes that span one to many rows and several raster tiles, fill
+ratios from trivial fits to heavy downscaling, the quality knob k, gutters,
+M, the hybrid threshold t_opt and every flag combination that the method
+defines (pre-rotation, exact tail, ablations, paper-literal locks).  Each case
+is compared element by element (proxies, order, every evaluated candidate,
+placements; stretch within 1e-6) by test_gpu_parity._compare_pack, and every
+packing is checked overlap-free by the GPU validator (P:85 / P:1025).
+
+The parameters are drawn from chartgen.SplitMix64 with a fixed seed, so the
+sweep is the same on every run; NTABI_FUZZ=<n> widens it locally.
+"""
+import os
+
+import pytest
+
+import chartgen
+from test_gpu_parity import _compare_pack, ctx  # noqa: F401  (the module-scoped context fixture)
+
+pytestmark = pytest.mark.gpu
+
+N = int(os.environ.get("NTABI_FUZZ", "160"))
+FAMILIES = ["uv", "tss", "lightmap", "mixed"]
+FLAG_SETS = [0, 0, 0, 8, 32, 1, 2, 3, 16, 8 | 2, 4, 32 | 8]
+
+
+def case(i):
+    r = chartgen.SplitMix64(0xF00D + i)
+    fam = FAMILIES[r.randint(0, len(FAMILIES) - 1)]
+    side = [128, 256, 512, 1024][r.randint(0, 3)]
+    n = r.randint(8, 260 if side >= 512 else 140)
+    rho = 0.2 + 1.6 * r.uniform()
+    cs = chartgen.small_case(i, n=n, side=side, family=fam, rho=rho)
+    kw = dict(local_aabb_count=[1, 2, 5, 10, 17][r.randint(0, 4)],
+              gutter=[0, 1, 1, 1, 2][r.randint(0, 4)],
+              scale_count=[16, 32, 64, 64, 64][r.randint(0, 4)],
+              flags=FLAG_SETS[r.randint(0, len(FLAG_SETS) - 1)])
+    if r.uniform() < 0.3 or kw["flags"] & 32:
+        kw["t_opt_bp"] = [50, 300, 1000, 3000][r.randint(0, 3)]
+    if kw["flags"] & 16:   # NO_OBB is an ablation of the plain-AABB modes
+        kw["local_aabb_count"] = 1
+    return cs, kw
+
+
+@pytest.mark.parametrize("i", range(N))
+def test_random_spec_parity(orc, ctx, i):
+    cs, kw = case(i)
+    st = _compare_pack(orc, ctx, cs, check_profiles=2, **kw)
+    if st == orc.OK:
+        from paper_2602_07782_b200 import spec_of
+        _, pl, _ = ctx.pack(cs.xy, cs.start, spec_of(cs, **kw))
+        g = kw.get("gutter", cs.gutter)
+        m = ctx.validate(cs.xy, cs.start, pl, cs.atlas_w, cs.atlas_h, gutter=g)
+        if not kw["flags"] & 4:  # (the paper-literal locks admit overlaps, LOCK-1)
+            assert m["overlap"] == m["gutter"] == m["oob"] == 0, (cs.name, kw, m)

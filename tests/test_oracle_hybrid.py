@@ -98,3 +98,26 @@ def test_hybrid_switch_rule(orc):
     assert orc.validate(cs, pl) == {"overlap": 0, "gutter": 0, "oob": 0}
     st0, pl0, info0, _ = orc.pack(cs, t_opt_bp=0, with_cands=True)
     assert info0.prefix_rows == 0
+
+
+def test_area_bound_does_not_hold_with_a_prefix_tail(orc):
+    """Reading R2 prunes candidates whose scaled total area exceeds
+    the atlas -- exact in sequential mode only.  With a hybrid tail the prefix
+    rows are downscaled by sigma < 1 (D24), so a candidate above the
+    bound can succeed and win (D25): here m = 63 and 64 lie above it and 64 is
+    the oracle's winner (found by the random parity sweep; the CUDA path now
+    starts its hybrid search at M)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "fz", os.path.join(os.path.dirname(__file__), "test_gpu_fuzz.py"))
+    fz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fz)
+    cs, kw = fz.case(105)
+    st, pl, info, cands = orc.pack(cs, with_cands=True, **kw)
+    a2 = sum(_area2(cs.polygon(c)) for c in range(cs.n_charts))
+    M = kw["scale_count"]
+    above = [m for m in range(1, M + 1) if m * m * a2 > 2 * 65536 * cs.atlas_w * cs.atlas_h * M * M]
+    assert above and info.scale_index in above and cands[info.scale_index - 1].success
+    assert cands[info.scale_index - 1].switched_at >= 0 and cands[info.scale_index - 1].p < (1 << 20)
+    assert orc.validate(cs, pl) == {"overlap": 0, "gutter": 0, "oob": 0}
