@@ -54,3 +54,59 @@ def test_random_spec_parity(orc, ctx, i):
         m = ctx.validate(cs.xy, cs.start, pl, cs.atlas_w, cs.atlas_h, gutter=g)
         if not kw["flags"] & 4:  # (the paper-literal locks admit overlaps, LOCK-1)
             assert m["overlap"] == m["gutter"] == m["oob"] == 0, (cs.name, kw, m)
+
+
+def large_case(i):
+    r = chartgen.SplitMix64(0xB16 + i)
+    fam = FAMILIES[r.randint(0, len(FAMILIES) - 1)]
+    side = [2048, 4096][r.randint(0, 1)]
+    n = r.randint(400, 3000)
+    rho = 0.3 + 1.4 * r.uniform()
+    cs = chartgen.generate(fam, n, side, side, 7000 + i, rho=rho, side_limit=side / 4,
+                           name=f"large-{fam}-n{n}-s{i}")
+    kw = dict(local_aabb_count=[2, 5, 10, 10][r.randint(0, 3)],
+              flags=[0, 0, 8, 32, 3][r.randint(0, 4)])
+    if r.uniform() < 0.4 or kw["flags"] & 32:
+        kw["t_opt_bp"] = [100, 500, 2000][r.randint(0, 2)]
+    return cs, kw
+
+
+@pytest.mark.parametrize("i", range(10))
+def test_random_large_parity(orc, ctx, i):
+    """Larger random sets (400-3,000 charts, 2048^2 / 4096^2): many raster
+    tiles per candidate, several position windows per fold, long rows."""
+    cs, kw = large_case(i)
+    _compare_pack(orc, ctx, cs, check_profiles=1, **kw)
+
+
+def batch_case(i):
+    r = chartgen.SplitMix64(0xBA7C + i)
+    side = [256, 512, 1024][r.randint(0, 2)]
+    sets = []
+    for j in range(r.randint(2, 24)):
+        fam = FAMILIES[r.randint(0, len(FAMILIES) - 1)]
+        sets.append(chartgen.small_case(100 * i + j, n=r.randint(1, 180), side=side, family=fam,
+                                        rho=0.2 + 1.8 * r.uniform()))
+    kw = dict(local_aabb_count=[1, 5, 10][r.randint(0, 2)], flags=[0, 0, 8, 3][r.randint(0, 3)])
+    if r.uniform() < 0.2:
+        kw["t_opt_bp"] = 500  # hybrid atlases go through tabi_pack ("solo")
+    return sets, kw
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_batch_parity(orc, ctx, i):
+    """tabi_pack_many on random batches (1-180 charts per atlas, mixed
+    families, fill ratios from trivial to NO_FIT): every atlas's status and
+    placements equal the oracle's pack of that atlas alone."""
+    import numpy as np
+    from paper_2602_07782_b200 import OK, concat_chart_sets, spec_of
+    sets, kw = batch_case(i)
+    xy, cst, abase, res = concat_chart_sets(sets)
+    st, pl, infos, ast, bi = ctx.pack_many(xy, cst, abase, spec_of(sets[0], **kw), res_xy=res,
+                                           raise_on_error=False)
+    for a, cs in enumerate(sets):
+        st_o, pl_o, info_o, _ = orc.pack(cs, **kw)
+        assert ast[a] == st_o, (i, a, ast[a], st_o)
+        if st_o == OK:
+            assert infos[a].scale_index == info_o.scale_index, (i, a)
+            assert pl[abase[a]:abase[a + 1]].tobytes() == np.ascontiguousarray(pl_o).tobytes(), (i, a)
