@@ -110,3 +110,55 @@ def test_random_batch_parity(orc, ctx, i):
         if st_o == OK:
             assert infos[a].scale_index == info_o.scale_index, (i, a)
             assert pl[abase[a]:abase[a + 1]].tobytes() == np.ascontiguousarray(pl_o).tobytes(), (i, a)
+
+
+def edge_case(i):
+    """Hand-shaped extremes mixed at random: slivers (aspect up to 1:200),
+    sub-texel and one-texel charts, charts close to the atlas size, stars with
+    up to 300 vertices (beyond the proxy kernel's shared-memory vertex cache),
+    far-off-origin coordinates, both windings, duplicate consecutive vertices
+    and collinear runs (valid simple outlines)."""
+    import math
+    r = chartgen.SplitMix64(0xED6E + i)
+    side = [64, 256, 1024][r.randint(0, 2)]
+    polys = []
+    for _ in range(r.randint(1, 60)):
+        kind = r.randint(0, 6)
+        ox, oy = r.uniform(-5000, 5000), r.uniform(-5000, 5000)
+        if kind == 0:    # sliver
+            L, t = r.uniform(4, side * 0.9), r.uniform(0.05, 2.0)
+            p = [(0, 0), (L, 0), (L, t), (0, t)]
+        elif kind == 1:  # sub-texel / one-texel
+            a = r.uniform(0.02, 1.0)
+            p = [(0, 0), (a, 0), (a, a), (0, a)]
+        elif kind == 2:  # near the atlas size
+            a, b = r.uniform(0.3, 0.95) * side, r.uniform(0.1, 0.9) * side
+            p = [(0, 0), (a, 0), (a, b), (0, b)]
+        elif kind == 3:  # star with many vertices
+            nv = r.randint(60, 300)
+            R = r.uniform(3, side * 0.3)
+            p = [(R * (0.4 + 0.6 * r.uniform()) * math.cos(2 * math.pi * j / nv),
+                  R * (0.4 + 0.6 * r.uniform()) * math.sin(2 * math.pi * j / nv)) for j in range(nv)]
+        elif kind == 4:  # triangle, clockwise
+            a, b = r.uniform(2, side * 0.4), r.uniform(2, side * 0.4)
+            p = [(0, 0), (0, b), (a, 0)]
+        elif kind == 5:  # collinear runs and a repeated vertex
+            a = r.uniform(4, side * 0.3)
+            p = [(0, 0), (a / 3, 0), (2 * a / 3, 0), (a, 0), (a, a), (a, a), (0, a)]
+        else:            # rotated rectangle
+            a, b, th = r.uniform(2, side * 0.3), r.uniform(2, side * 0.3), r.uniform(0, math.pi)
+            c, s = math.cos(th), math.sin(th)
+            p = [(x * c - y * s, x * s + y * c) for x, y in [(0, 0), (a, 0), (a, b), (0, b)]]
+        polys.append([(x + ox, y + oy) for x, y in p])
+    cs = chartgen.from_polygons(polys, side, side, name=f"edge-{i}")
+    kw = dict(local_aabb_count=[1, 3, 10, 64][r.randint(0, 3)], gutter=[0, 1, 2][r.randint(0, 2)],
+              flags=[0, 0, 8, 3, 32][r.randint(0, 4)])
+    if r.uniform() < 0.3 or kw["flags"] & 32:
+        kw["t_opt_bp"] = [300, 3000][r.randint(0, 1)]
+    return cs, kw
+
+
+@pytest.mark.parametrize("i", range(40))
+def test_random_edge_parity(orc, ctx, i):
+    cs, kw = edge_case(i)
+    _compare_pack(orc, ctx, cs, check_profiles=2, **kw)

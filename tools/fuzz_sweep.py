@@ -3,7 +3,7 @@ tests/test_gpu_fuzz.py (seeded random specs, families, flags) packed by the
 CUDA path and the oracle, placements compared byte for byte; prints the
 mismatching cases.
 
-    python tools/fuzz_sweep.py [N=160]
+    python tools/fuzz_sweep.py [N=160] [case|edge|large]
 """
 import sys, os
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), 'tests'))
@@ -16,7 +16,8 @@ from paper_2602_07782_b200 import Context, spec_of
 ctx = Context(0, max_charts=25000, max_vertices=1 << 19, max_atlas_side=16384)
 bad = []
 for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 160):
-    cs, kw = fz.case(i)
+    kind = sys.argv[2] if len(sys.argv) > 2 else "case"
+    cs, kw = {"case": fz.case, "edge": fz.edge_case, "large": fz.large_case}[kind](i)
     st_o, pl_o, info_o, _ = oracle.pack(cs, with_cands=True, **kw)
     st_g, pl_g, info_g = ctx.pack(cs.xy, cs.start, spec_of(cs, **kw))
     same = st_o == st_g and (st_o != 0 or pl_g.tobytes() == np.ascontiguousarray(pl_o).tobytes())
