@@ -162,3 +162,80 @@ def edge_case(i):
 def test_random_edge_parity(orc, ctx, i):
     cs, kw = edge_case(i)
     _compare_pack(orc, ctx, cs, check_profiles=2, **kw)
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_validator_parity(orc, ctx, i):
+    """N3 validator on random packings, valid and corrupted (random shifts,
+    mirror flips, pre-rotation indices, scales): overlap / gutter / oob /
+    covered counts bit-exact against oracle/validate.c, occupancy exact,
+    stretch to 1e-12."""
+    import numpy as np
+    from paper_2602_07782_b200 import spec_of
+    cs, kw = case(1000 + i)
+    st, pl, _ = ctx.pack(cs.xy, cs.start, spec_of(cs, **kw), raise_on_error=False)
+    if st != orc.OK:
+        pytest.skip("no packing")
+    rng = np.random.default_rng(i)
+    g = kw.get("gutter", cs.gutter)
+    for trial in range(3):
+        bad = pl.copy()
+        if trial:
+            k = rng.choice(len(bad), size=max(1, len(bad) // (2 + trial)), replace=False)
+            bad["tx"][k] += rng.integers(-9, 10, size=len(k))
+            bad["ty"][k] += rng.integers(-9, 10, size=len(k))
+            bad["mirror_x"][k] ^= rng.integers(0, 2, size=len(k)).astype(bad["mirror_x"].dtype)
+            if trial == 2:
+                bad["prerot"][k] = rng.integers(0, 8, size=len(k)).astype(bad["prerot"].dtype)
+        mo = orc.metrics(cs, bad, gutter=g)
+        mg = ctx.validate(cs.xy, cs.start, bad, cs.atlas_w, cs.atlas_h, gutter=g)
+        for key in ("overlap", "gutter", "oob", "covered"):
+            assert mg[key] == mo[key], (i, trial, key, mg[key], mo[key])
+        assert mg["occupancy"] == mo["occupancy"]
+        assert mg["l2_stretch"] == pytest.approx(mo["l2_stretch"], rel=1e-12)
+        if trial == 0 and not kw["flags"] & 4:
+            assert mg["overlap"] == mg["gutter"] == mg["oob"] == 0
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_random_async_parity(orc, ctx, i):
+    """tabi_pack_async + tabi_pack_wait on random specs: the bytes and the
+    statistics of the synchronous pack (and so of the oracle)."""
+    import torch
+    from paper_2602_07782_b200 import spec_of
+    cs, kw = case(2000 + i)
+    xy, start = torch.from_numpy(cs.xy).cuda(), torch.from_numpy(cs.start).cuda()
+    st_s, out_s, info_s = ctx.pack(xy, start, spec_of(cs, **kw), raise_on_error=False)
+    torch.cuda.synchronize()
+    ref = out_s.cpu().numpy().tobytes()
+    out = ctx.pack_async(xy, start, spec_of(cs, **kw))
+    st, out2, info = ctx.wait(raise_on_error=False)
+    torch.cuda.synchronize()
+    assert st == st_s and info.scale_index == info_s.scale_index
+    if st == orc.OK:
+        assert out.cpu().numpy().tobytes() == ref
+
+
+def test_two_contexts_async_on_two_streams(orc):
+    """Distinct contexts may run concurrently (tabi.h): two asynchronous packs
+    in flight at once on two streams of one GPU, each equal to the oracle."""
+    import numpy as np
+    import torch
+    from paper_2602_07782_b200 import Context, spec_of
+    cases = [case(3000 + j) for j in range(2)]
+    ctxs = [Context(0, max_charts=4096, max_vertices=1 << 16, max_atlas_side=4096) for _ in cases]
+    streams = [torch.cuda.Stream() for _ in cases]
+    outs = []
+    for c, s, (cs, kw) in zip(ctxs, streams, cases):
+        xy, start = torch.from_numpy(cs.xy).cuda(), torch.from_numpy(cs.start).cuda()
+        torch.cuda.synchronize()
+        outs.append((xy, start, c.pack_async(xy, start, spec_of(cs, **kw), stream=s.cuda_stream)))
+    for c, (xy, start, out), (cs, kw) in zip(ctxs, outs, cases):
+        st, _, info = c.wait(raise_on_error=False)
+        st_o, pl_o, info_o, _ = orc.pack(cs, with_cands=True, **kw)
+        assert st == st_o
+        if st == orc.OK:
+            torch.cuda.synchronize()
+            assert out.cpu().numpy().tobytes() == np.ascontiguousarray(pl_o).tobytes()
+    for c in ctxs:
+        c.close()
