@@ -320,7 +320,7 @@ chunk_sort_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww
 
 __global__ void __launch_bounds__(256)
 chunk_rank_kernel(const uint64_t* __restrict__ ck, const int32_t* __restrict__ ci, int32_t n,
-                  int32_t* perm, const Status* st) {
+                  int32_t* perm, uint64_t* skeys, const Status* st) {
   if (st->bad_chart != INT32_MAX) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
@@ -354,7 +354,9 @@ chunk_rank_kernel(const uint64_t* __restrict__ ck, const int32_t* __restrict__ c
     }
   }
   perm[rank] = i;
+  skeys[rank] = k;  // the keys in sorted order: the slot layout reads (h, w) from them
 }
+
 
 // N <= 2^17: rank of key i = #{j : (key_j, j) < (key_i, i)}, counted over a 2-D
 // grid of (i block, j tile) with one atomicAdd per thread and tile, then a
@@ -393,7 +395,7 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
                                           const int32_t* perm, const PackParams& pp, int32_t* colofs,
                                           int32_t* rowofs, int32_t* hsorted, int32_t* tstart,
                                           int32_t* tix, Status* st, int32_t* rdy,
-                                          const uint64_t* skey = nullptr) {
+                                          const uint64_t* skey = nullptr, int skey_shift = 12) {
   __shared__ int32_t sh[2][kW + 1];
   __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
@@ -463,9 +465,9 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
     if (s < pp.n) {
       int32_t w, h;
       if (skey) {  // the sorted key holds (h, w): no dependent global loads
-        const uint64_t k = skey[s];
-        h = (int32_t)(0x3ffffffu - (uint32_t)((k >> 38) & 0x3ffffffu));
-        w = (int32_t)(0x3ffffffu - (uint32_t)((k >> 12) & 0x3ffffffu));
+        const uint64_t k = skey[s] >> skey_shift;  // order_key(h, w) [<< 12 | index]
+        h = (int32_t)(0x3ffffffu - (uint32_t)((k >> 26) & 0x3ffffffu));
+        w = (int32_t)(0x3ffffffu - (uint32_t)(k & 0x3ffffffu));
       } else {
         const int c = perm[s];
         w = ww[c];
@@ -534,9 +536,9 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
 __global__ void __launch_bounds__(kT, 1)
 prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, const int64_t* area2,
             const int32_t* perm, PackParams pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
-            int32_t* tstart, int32_t* tix, Status* st, int32_t* rdy) {
+            int32_t* tstart, int32_t* tix, Status* st, int32_t* rdy, const uint64_t* skeys) {
   if (st->bad_chart != INT32_MAX) return;
-  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy);
+  prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy, skeys, 0);
 }
 
 // N <= 2048: order and slot layout in one launch (the block that sorted reads
@@ -637,7 +639,8 @@ void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* 
 }
 
 int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
-                int32_t* perm2, const Status* st, cudaStream_t s) {
+                int32_t* perm2, const Status* st, cudaStream_t s, const uint64_t** sorted_keys) {
+  if (sorted_keys) *sorted_keys = nullptr;
   // TABI_SORT=bitonic|chunk|rank|radix forces a path (tests cover all four)
   const char* force = getenv("TABI_SORT");
   const bool want_rank = force && strcmp(force, "rank") == 0;
@@ -656,7 +659,8 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
     // chunked bitonic + merge ranks (ck in keys, ci in perm2)
     const int nch = (n + kChunk - 1) / kChunk;
     chunk_sort_kernel<<<nch, kT, 0, s>>>(P.h, P.w, n, keys, perm2, st);
-    chunk_rank_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, perm2, n, perm, st);
+    chunk_rank_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, perm2, n, perm, keys2, st);
+    if (sorted_keys) *sorted_keys = keys2;
     return 2;
   }
   if (n <= kRankMax && !want_radix) {
@@ -698,9 +702,9 @@ void launch_many_reset(Status* sts, AtlasRes* res, int32_t A, const int32_t* ord
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                 int32_t* rdy, cudaStream_t s) {
+                 int32_t* rdy, cudaStream_t s, const uint64_t* sorted_keys) {
   prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart, tix,
-                               st, rdy);
+                               st, rdy, sorted_keys);
 }
 
 }  // namespace tabi

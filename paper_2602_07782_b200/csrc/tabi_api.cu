@@ -153,6 +153,7 @@ struct tabi_ctx {
   int32_t* colofs = nullptr;
   int32_t* rowofs = nullptr;
   int32_t* hsorted = nullptr;
+  const uint64_t* sorted_keys = nullptr;  // keys in sorted order (chunked sort), else nullptr
   tabi_placement* d_out = nullptr;
   Status* d_status = nullptr;
   Status* h_status = nullptr;  // pinned
@@ -671,6 +672,7 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     launch_reset(ctx->d_status, 2, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy, 0, s);
     nl++;
     if (full) {
+      ctx->sorted_keys = nullptr;  // (set by launch_sort when its ranks write them)
       launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
                      ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s,
                      AtlasMap{nullptr, 1, nullptr}, V_in);
@@ -681,13 +683,14 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
         nl++;
         prep_done = true;
       } else {
-        nl += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s);
+        nl += launch_sort(ctx->P, n, ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->d_status, s,
+                          &ctx->sorted_keys);
       }
       tm.mark(s);
     }
     if (!prep_done) {
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
-                  ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s);
+                  ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s, ctx->sorted_keys);
       nl++;
     }
     return TABI_OK;

@@ -445,14 +445,15 @@ void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* 
 // D9 sort: bitonic in smem (N <= 4096), rank sort (N <= 2^17), else radix.
 // Returns the number of kernels launched.
 int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, int32_t* perm,
-                int32_t* perm2, const Status* st, cudaStream_t s);
+                int32_t* perm2, const Status* st, cudaStream_t s,
+                const uint64_t** sorted_keys = nullptr);
 // N <= 2048 and no TABI_SORT knob: sort + prep in one launch (returns false otherwise)
 bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int32_t* colofs,
                       int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
                       int32_t* rdy, cudaStream_t s);  // rdy: zeroed for the fused wave, or nullptr
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                 int32_t* rdy, cudaStream_t s);
+                 int32_t* rdy, cudaStream_t s, const uint64_t* sorted_keys = nullptr);
 void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
                      int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,
