@@ -144,6 +144,9 @@ __device__ __forceinline__ void block_scan2(int32_t a, int32_t b, int32_t& ea, i
 // 2^26 units (|coordinate| <= 2^24), so (2^26-1-h, 2^26-1-w, index) packs in
 // 64 bits for N <= 4096 and the packed keys are unique: any correct sort gives
 // the stable order.
+#ifndef TABI_B0_HYBRID
+#define TABI_B0_HYBRID 4
+#endif
 #ifndef TABI_B0_FILL
 #define TABI_B0_FILL 55  // wave 0 reaches down to the scale filling this % of the atlas
 #endif
@@ -452,6 +455,11 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
         int m_lo = m_hi;
         while (m_lo > 1 && (i128)100 * (m_lo - 1) * (m_lo - 1) * tot >= (i128)TABI_B0_FILL * rhs) m_lo--;
         b0 = min(pp.B, max(2, m_hi - m_lo + 1));
+        // hybrid mode: the prefix tail's downscale absorbs the overflow that
+        // fails a sequential candidate, so the top candidates usually succeed
+        // and then win (D25) -- a first wave of TABI_B0_HYBRID; the device
+        // loop's V bound decides whether lower ones still need a wave
+        if (pp.t_opt > 0) b0 = min(b0, TABI_B0_HYBRID);
       }
       st->b0 = b0;
       st->atot_lo = (unsigned long long)(uint64_t)tot;

@@ -144,6 +144,19 @@ __device__ __forceinline__ int64_t fdiv_r128(i128 a, i128 b, double rcp, bool cl
 // few dozen cells on (the prefix tail's large charts, found by the random
 // parity sweep tests/test_gpu_fuzz.py).
 __device__ __forceinline__ void lindiv_start(const LinDiv& L, int64_t i, int64_t& v, int64_t& r) {
+  // int64 whenever i D < 2^62 (then rA + i rB < 2^63): every sequential-mode
+  // scale, and the tail's small charts
+  const uint64_t iD = (uint64_t)i * (uint64_t)L.D;
+  if (i >= 0 && __umul64hi((uint64_t)i, (uint64_t)L.D) == 0 && iD < (1ull << 62)) {
+    const int64_t N = L.rA + i * L.rB;
+    int64_t t = (int64_t)((double)N * L.rcp);
+    int64_t rr = N - t * L.D;
+    while (rr < 0) { t--; rr += L.D; }
+    while (rr >= L.D) { t++; rr -= L.D; }
+    v = L.qA + i * L.qB + t;
+    r = rr;
+    return;
+  }
   const i128 N = (i128)L.rA + (i128)i * L.rB;
   int64_t t = (int64_t)(i128_to_double(N) * L.rcp);
   i128 rr = N - (i128)t * L.D;
