@@ -59,6 +59,43 @@ __device__ __forceinline__ void block_scan3(int32_t a, int32_t b, int32_t c, int
   __syncthreads();
 }
 
+// Like block_scan3 but c's result is the EXCLUSIVE max over the threads
+// before this one (INT32_MIN for thread 0 of the block).
+__device__ __forceinline__ void block_scan3x(int32_t a, int32_t b, int32_t c, int32_t& ea,
+                                             int32_t& eb, int32_t& xc_ex, int32_t& ta, int32_t& tb,
+                                             int32_t& mc, ScanSmem& S) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t ia = warp_incl_sum(a, lane), ib = warp_incl_sum(b, lane);
+  const int32_t xc = warp_incl_max(c, lane);
+  int32_t xprev = __shfl_up_sync(0xffffffffu, xc, 1);
+  if (lane == 0) xprev = INT32_MIN;
+  if (lane == 31) { S.s[0][wid] = ia; S.s[1][wid] = ib; S.s[2][wid] = xc; }
+  __syncthreads();
+  if (wid == 0) {
+    const int32_t va = lane < kW ? S.s[0][lane] : 0, vb = lane < kW ? S.s[1][lane] : 0;
+    const int32_t vc = lane < kW ? S.s[2][lane] : INT32_MIN;
+    const int32_t xa = warp_incl_sum(va, lane), xb = warp_incl_sum(vb, lane);
+    const int32_t yc = warp_incl_max(vc, lane);
+    int32_t pc = __shfl_up_sync(0xffffffffu, yc, 1);
+    if (lane == 0) pc = INT32_MIN;
+    if (lane < kW) { S.s[0][lane] = xa - va; S.s[1][lane] = xb - vb; S.s[2][lane] = pc; }
+    if (lane == 31) { S.s[0][kW] = xa; S.s[1][kW] = xb; S.s[2][kW] = yc; }
+  }
+  __syncthreads();
+  ea = S.s[0][wid] + ia - a;
+  eb = S.s[1][wid] + ib - b;
+  xc_ex = max(S.s[2][wid], xprev);
+  ta = S.s[0][kW];
+  tb = S.s[1][kW];
+  mc = S.s[2][kW];
+  __syncthreads();
+}
+
+// Scans over the tail [r0, n) take kIT consecutive positions per thread (a
+// sequential scan in registers, then one block scan of the thread totals):
+// kIT x fewer barrier-separated block scans than one position per thread.
+constexpr int kIT = 8;
+
 __device__ __forceinline__ int32_t block_max(int32_t v, ScanSmem& S) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_max(v);
@@ -170,14 +207,24 @@ __device__ __noinline__ void tail_prepare(const PackParams& pp, const int32_t* _
   }
   // pass 1: start = exclusive scan of off over [r0, n); q = floor(start / W')
   int32_t carry = 0;
-  for (int base = r0; base < n; base += kT) {
-    const int s = base + tid;
-    const int32_t a = (s < n && s + 1 < n) ? off[s] : 0;
+  for (int base = r0; base < n; base += kT * kIT) {
+    const int s0 = base + tid * kIT;
+    int32_t lx[kIT], tot = 0;
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      lx[u] = tot;
+      tot += (s < n && s + 1 < n) ? off[s] : 0;
+    }
     int32_t ea, eb, ic, ta, tb, mc;
-    block_scan3(a, 0, 0, ea, eb, ic, ta, tb, mc, S);
-    if (s < n) {
-      start[s] = carry + ea;
-      qrow[s] = (int32_t)((int64_t)(carry + ea) / Wp);
+    block_scan3(tot, 0, 0, ea, eb, ic, ta, tb, mc, S);
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      if (s < n) {
+        start[s] = carry + ea + lx[u];
+        qrow[s] = (int32_t)((int64_t)(carry + ea + lx[u]) / Wp);
+      }
     }
     carry += ta;
   }
@@ -185,16 +232,25 @@ __device__ __noinline__ void tail_prepare(const PackParams& pp, const int32_t* _
   // pass 2: E = max over charts of (start - start of the row's first chart + Wd)
   int32_t fcarry = INT32_MIN, emax = INT32_MIN;
   i128 apre = 0;
-  for (int base = r0; base < n; base += kT) {
-    const int s = base + tid;
-    const bool valid = s < n;
-    const bool first = valid && (s == r0 || qrow[s] != qrow[s - 1]);
-    int32_t ea, eb, f, ta, tb, mc;
-    block_scan3(0, 0, first ? s : INT32_MIN, ea, eb, f, ta, tb, mc, S);
-    f = max(f, fcarry);
-    if (valid) {
-      emax = max(emax, start[s] - start[f] + wd[s]);
-      apre += area2[perm[s]];
+  for (int base = r0; base < n; base += kT * kIT) {
+    const int s0 = base + tid * kIT;
+    int32_t lf = INT32_MIN;  // the thread's last row start among its positions
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      if (s < n && (s == r0 || qrow[s] != qrow[s - 1])) lf = s;
+    }
+    int32_t ea, eb, fx, ta, tb, mc;
+    block_scan3x(0, 0, lf, ea, eb, fx, ta, tb, mc, S);
+    int32_t f = max(fcarry, fx);
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      if (s < n) {
+        if (s == r0 || qrow[s] != qrow[s - 1]) f = s;
+        emax = max(emax, start[s] - start[f] + wd[s]);
+        apre += area2[perm[s]];
+      }
     }
     fcarry = max(fcarry, mc);
   }
@@ -249,31 +305,51 @@ __device__ __noinline__ void tail_layout(const PackParams& pp, const int32_t* __
   const int32_t* qrow = sc + 5 * (int64_t)n;
   // global exclusive prefix sums of the new offsets and widths over [r0, n)
   int32_t c0 = 0, c1 = 0;
-  for (int base = r0; base < n; base += kT) {
-    const int s = base + tid;
-    const int32_t a = (s < n && s + 1 < n) ? off[s] : 0;
-    const int32_t b = s < n ? wd[s] : 0;
+  for (int base = r0; base < n; base += kT * kIT) {
+    const int s0 = base + tid * kIT;
+    int32_t la[kIT], lb[kIT], sa = 0, sb = 0;
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      la[u] = sa;
+      lb[u] = sb;
+      sa += (s < n && s + 1 < n) ? off[s] : 0;
+      sb += s < n ? wd[s] : 0;
+    }
     int32_t ea, eb, ic, ta, tb, mc;
-    block_scan3(a, b, 0, ea, eb, ic, ta, tb, mc, S);
-    if (s < n) { poff[s] = c0 + ea; pwd[s] = c1 + eb; }
+    block_scan3(sa, sb, 0, ea, eb, ic, ta, tb, mc, S);
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      if (s < n) { poff[s] = c0 + ea + la[u]; pwd[s] = c1 + eb + lb[u]; }
+    }
     c0 += ta;
     c1 += tb;
   }
   __syncthreads();
   // row-relative positions: subtract the value at the row's first chart
   int32_t fcarry = INT32_MIN, emax = INT32_MIN;
-  for (int base = r0; base < n; base += kT) {
-    const int s = base + tid;
-    const bool valid = s < n;
-    const bool first = valid && (s == r0 || qrow[s] != qrow[s - 1]);
-    int32_t ea, eb, f, ta, tb, mc;
-    block_scan3(0, 0, first ? s : INT32_MIN, ea, eb, f, ta, tb, mc, S);
-    f = max(f, fcarry);
-    if (valid) {
-      const int32_t x = poff[s] - poff[f];
-      xs1[s] = x;                // position with compaction (D24 step 2 re-lay)
-      xs0[s] = pwd[s] - pwd[f];  // prefix of widths in the row (flattened index)
-      emax = max(emax, x + wd[s]);
+  for (int base = r0; base < n; base += kT * kIT) {
+    const int s0 = base + tid * kIT;
+    int32_t lf = INT32_MIN;
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      if (s < n && (s == r0 || qrow[s] != qrow[s - 1])) lf = s;
+    }
+    int32_t ea, eb, fx, ta, tb, mc;
+    block_scan3x(0, 0, lf, ea, eb, fx, ta, tb, mc, S);
+    int32_t f = max(fcarry, fx);
+#pragma unroll
+    for (int u = 0; u < kIT; u++) {
+      const int s = s0 + u;
+      if (s < n) {
+        if (s == r0 || qrow[s] != qrow[s - 1]) f = s;
+        const int32_t x = poff[s] - poff[f];
+        xs1[s] = x;                // position with compaction (D24 step 2 re-lay)
+        xs0[s] = pwd[s] - pwd[f];  // prefix of widths in the row (flattened index)
+        emax = max(emax, x + wd[s]);
+      }
     }
     fcarry = max(fcarry, mc);
   }
