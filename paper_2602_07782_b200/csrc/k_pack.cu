@@ -438,6 +438,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
 
   const bool prefix_mode = pp.mode == 1;  // D24 steps 3-4: push the prefix-folded rows
   int32_t* qrow = sc + 5 * (int64_t)n;    // prefix row id per sorted position (tail)
+  const int32_t* rend = sc + 4 * (int64_t)n;  // prefix row: last position, by its first (tail)
   if (prefix_mode) {
     if (pp.T.state[slot] != TAIL_READY) return;
   } else if ((!rd.flags && !lz && cand_bad[slot]) || (rd.flags && cand_too_big(pp, st, m))) {
@@ -765,22 +766,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     bool anypl = false;    // some non-adjacent (D15) pair of the row is locked
     if (prefix_mode) pk_sync();
     if (prefix_mode) {
-      // prefix rows were laid out by the tail kernels (positions in xs0/xs1);
-      // the row is the run of equal row ids starting at rs
-      const int32_t qr = qrow[rs];
-      for (int base = rs; !S.done; base += kPT) {
-        if (tid == 0) S.fmin[0] = INT32_MAX;
-        pk_sync();
-        const int s = base + tid;
-        if (s < n && qrow[s] != qr) atomicMin(&S.fmin[0], s);
-        pk_sync();
-        if (tid == 0 && (S.fmin[0] != INT32_MAX || base + kPT >= n)) {
-          const int32_t e = S.fmin[0] != INT32_MAX ? S.fmin[0] - 1 : n - 1;
-          S.endv[0] = S.endv[1] = e;
-          S.endv[2] = S.endv[3] = rs - 1;
-          S.done = 1;
-        }
-        pk_sync();
+      // prefix rows were laid out by the tail kernels (positions in xs0/xs1,
+      // and each row's last position by its first: rend, written by
+      // tail_layout / the exact tail's row search)
+      if (tid == 0) {
+        const int32_t e = rend[rs];
+        S.endv[0] = S.endv[1] = e;
+        S.endv[2] = S.endv[3] = rs - 1;
+        S.done = 1;
       }
     } else {
       // Fold over the position window: its exclusive prefix sums of widths

@@ -192,6 +192,7 @@ __device__ __noinline__ void tail_prepare(const PackParams& pp, const int32_t* _
         xs1[s] = start[s] - sa;
         xs0[s] = pwd[s] - wa;
       }
+      if (tid == 0) start[a] = end;  // (rend, read by the packer's prefix rows; start[a] is dead)
       row++;
       __syncthreads();
       if (tid == 0) row_a = end + 1;
@@ -303,6 +304,7 @@ __device__ __noinline__ void tail_layout(const PackParams& pp, const int32_t* __
   int32_t* poff = sc + 2 * (int64_t)n;  // temporary global prefix sums
   int32_t* pwd = sc + 3 * (int64_t)n;
   const int32_t* qrow = sc + 5 * (int64_t)n;
+  int32_t* rend = sc + 4 * (int64_t)n;  // row's last position by its first (the packer's prefix rows)
   // global exclusive prefix sums of the new offsets and widths over [r0, n)
   int32_t c0 = 0, c1 = 0;
   for (int base = r0; base < n; base += kT * kIT) {
@@ -349,6 +351,7 @@ __device__ __noinline__ void tail_layout(const PackParams& pp, const int32_t* __
         xs1[s] = x;                // position with compaction (D24 step 2 re-lay)
         xs0[s] = pwd[s] - pwd[f];  // prefix of widths in the row (flattened index)
         emax = max(emax, x + wd[s]);
+        if (s == n - 1 || qrow[s + 1] != qrow[s]) rend[f] = s;  // the row's last position
       }
     }
     fcarry = max(fcarry, mc);
