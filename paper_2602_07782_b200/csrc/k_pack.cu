@@ -476,6 +476,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     if (prefix_mode) {  // continue from the state saved at the switch
       const Cand cd = cands[slot];
       S.row_start = pp.T.r0[slot];
+      S.next_a0 = S.row_start < n ? colofs[S.row_start] : -1;  // the first prefix row's prefetch
       S.fmax = cd.score; S.rows = cd.rows; S.knees_found = cd.knees_found;
       S.knee_rows = cd.knee_rows;
     }
@@ -674,7 +675,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // (no global loads on thread 0's path: the row start's slot offset was
     // kept from the previous row's fold; in fused mode only once every tile
     // is published)
-    if (!prefix_mode && tid == 0) {
+    if (tid == 0) {
       S.pf_out = 0;
       // every tile of this candidate published?  (one acquire load of the
       // slot's completed-tile count; the fold's window fills probe far less
@@ -839,7 +840,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     }  // !prefix_mode
     // (the row-top prefetch flag: published by the fold's barriers; set before
     // any exit so the end of the packer drains a copy still in flight)
-    pf_pending = S.pf_out != 0 && !prefix_mode;
+    pf_pending = S.pf_out != 0;
     if (S.abort) break;  // beaten while waiting for tiles (set before a barrier)
     phase_mark(1);
     // (the non-prefix fold ran hc_select in its last step, before a barrier)
@@ -1180,6 +1181,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     // ---- commit: F <- max(F, Y + BottomEdge); record placements ------------
     const int f = cfg >> 1, dir = cfg & 1;
     const int32_t endS = S.end_cfg[cfg];
+    // prefix rows: the next row's slot offset for its row-top prefetch (the
+    // load's latency hides behind the commit walk)
+    const int32_t pf_next = (prefix_mode && tid == 0 && endS + 1 < n) ? colofs[endS + 1] : -1;
     // ---- FindKnee after an atlas-fold row: the height
     // drops of the row's charts, issued here so their loads overlap the commit
     // walk (the commit's last barrier publishes S.knee_key) ------------------
@@ -1287,8 +1291,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       }
       if (rd.flags && pp.early && wj < jslot) S.abort = 1;  // checked at the next row start
       const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
-      S.next_a0 = (!prefix_mode && S.w_fold && nx < n && nx < S.fold_hi && nx - rs < kRW)
-                      ? W.rco[nx - rs] : -1;
+      S.next_a0 = prefix_mode ? pf_next
+                  : (S.w_fold && nx < n && nx < S.fold_hi && nx - rs < kRW) ? W.rco[nx - rs] : -1;
     }
     pk_sync();
     phase_mark(7);
