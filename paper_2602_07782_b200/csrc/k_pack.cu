@@ -155,7 +155,7 @@ struct Win {                 // shared-memory window of one row
   int32_t* rwd;              // dilated width
   int32_t* rco;              // footprint offset (colofs, absolute; see pr_base)
   int32_t* rY;               // [4][kRW] vertical offsets per configuration
-  int32_t* rbot;             // max over the chart's columns of BottomEdge (push walk)
+  int32_t* rbot;             // (unused: a chart's largest BottomEdge is its Hd, see the push)
   int32_t* rhs;              // unscaled heights (FindKnee), written by the fold
   uint8_t* rlk;              // adjacent-pair lock bits (Alg. 1), written by the fold
   uint32_t* prof;            // staged column footprints
@@ -806,7 +806,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
               W.rlk[s - rs] = PW.lk[i];
               lockv |= PW.lk[i] != 0;
 #pragma unroll
-              for (int q = 0; q < 5; q++) W.rY[q * kRW + (s - rs)] = INT32_MIN;  // push init
+              for (int q = 0; q < 4; q++) W.rY[q * kRW + (s - rs)] = INT32_MIN;  // push init
             }
             if (x0 + w_s > Wp) atomicMin(&S.fmin[0], s);
             if (x1 + w_s > Wp) atomicMin(&S.fmin[1], s);
@@ -939,6 +939,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       return dir ? (f ? kb : Wp) - xl - Wd : (f ? ka : 0) + xl;
     };
 
+    // A chart's largest BottomEdge is its dilated height Hd (the footprint
+    // contains the chart, whose lowest point lies in some column, and never
+    // exceeds Hd; D11, D13 -- checked on the oracle's footprints), so the
+    // score max_j (Y + BottomEdge_j) of a chart is Y + Hd: the push needs no
+    // BottomEdge reduction.  One-window rows load Hd here, consumed by the
+    // score (the load's latency hides behind the push).
+    const int32_t hd_mine = (one && tid <= endA - rs) ? hd[rs + tid] : 0;
     // ---- push: Y = max over covered columns of F - TopEdge ----
     for (int ws0 = rs; ws0 <= endA; ws0 += kRW) {
       const int we = min(endA + 1, ws0 + kRW), nwin = we - ws0;
@@ -946,9 +953,9 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       if (!(ws0 == rs && one && !prefix_mode)) {  // (else the fold initialised them)
         for (int k = tid; k < nwin; k += kPT) {
 #pragma unroll
-          for (int q = 0; q < 5; q++) W.rY[q * kRW + k] = INT32_MIN;
+          for (int q = 0; q < 4; q++) W.rY[q * kRW + k] = INT32_MIN;
         }
-        pk_sync();  // (index 4 of rY is rbot)
+        pk_sync();
       }
       phase_mark(8);
       const uint32_t* pr = g_pg ? col : W.prof - g_a0;
@@ -979,16 +986,14 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
           const uint32_t* pc = pr + W.rco[i];
           const int32_t* f0 = F + cfgX(0, i);
           const int32_t* f1 = F + cfgX(1, i) + Wd - 1;
-          int32_t m0 = INT32_MIN, m1 = INT32_MIN, m2 = INT32_MIN, m3 = INT32_MIN, bm = INT32_MIN;
+          int32_t m0 = INT32_MIN, m1 = INT32_MIN, m2 = INT32_MIN, m3 = INT32_MIN;
           const bool four = knee_ok && ws0 + i <= endK;
           if (four) {
             const int32_t* f2 = F + cfgX(2, i);
             const int32_t* f3 = F + cfgX(3, i) + Wd - 1;
             #pragma unroll 4
             for (int32_t j = j0; j < j1; j++) {
-              const uint32_t v = pc[j];
-              const int32_t top = lo16(v);
-              bm = max(bm, hi16(v));  // the score needs only max_j BottomEdge per chart
+              const int32_t top = lo16(pc[j]);
               m0 = max(m0, f0[j] - top);
               m1 = max(m1, f1[-j] - top);
               m2 = max(m2, f2[j] - top);
@@ -998,17 +1003,11 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             const int32_t* fp = pdir ? f1 : f0;
             const int32_t step = pdir ? -1 : 1;
             #pragma unroll 4
-            for (int32_t j = j0; j < j1; j++) {
-              const uint32_t v = pc[j];
-              bm = max(bm, hi16(v));
-              m0 = max(m0, fp[step * j] - lo16(v));
-            }
+            for (int32_t j = j0; j < j1; j++) m0 = max(m0, fp[step * j] - lo16(pc[j]));
           } else {
             #pragma unroll 4
             for (int32_t j = j0; j < j1; j++) {
-              const uint32_t v = pc[j];
-              const int32_t top = lo16(v);
-              bm = max(bm, hi16(v));
+              const int32_t top = lo16(pc[j]);
               m0 = max(m0, f0[j] - top);
               m1 = max(m1, f1[-j] - top);
             }
@@ -1024,7 +1023,6 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
             atomicMax(&W.rY[2 * kRW + i], m2);
             atomicMax(&W.rY[3 * kRW + i], m3);
           }
-          atomicMax(&W.rbot[i], bm);
           t += j1 - j0;
           i++;
         }
@@ -1112,15 +1110,16 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     phase_mark(4);
     // ---- score: max over covered columns of Y + BottomEdge ----
     // Y is constant per chart, so the max over its columns is Y + the chart's
-    // largest BottomEdge, which the push walk recorded (rbot): one pass over
-    // the row's charts instead of a column walk.  Multi-window rows walk.
+    // largest BottomEdge = Y + Hd (see the push): one pass over the row's
+    // charts instead of a column walk.  Multi-window rows walk.
     {
       int32_t nm[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
       if (one) {
         const int nwin = endA - rs + 1;
         for (int k = tid; k < nwin; k += kPT) {
           const int na = (knee_ok && rs + k <= endK) ? 4 : 2;
-          for (int q = 0; q < na; q++) nm[q] = max(nm[q], W.rY[q * kRW + k] + W.rbot[k]);
+          const int32_t hdk = k == tid ? hd_mine : hd[rs + k];
+          for (int q = 0; q < na; q++) nm[q] = max(nm[q], W.rY[q * kRW + k] + hdk);
         }
       }
       for (int ws0 = rs; ws0 <= endA && !one; ws0 += kRW) {
