@@ -284,3 +284,26 @@ def test_invalid_inputs(orc):
     cs = chartgen.from_polygons([[(0, 0), (1, 0), (0, 1)]], 0, 64)
     st, _, _, _ = orc.pack(cs)
     assert st == orc.EINVAL
+
+
+def test_footprint_extremes_equal_the_dilated_box(orc):
+    """Every dilated footprint reaches its box: max_j BottomEdge = Hd,
+    min_j TopEdge = 0, max_i Right = Wd, min_i Left = 0 (D11: the footprint
+    contains the chart, whose extreme points lie in some column / row, and is
+    clipped to the chart extent; D13: the dilation adds 2g).  The CUDA push
+    relies on it (the score of a chart is Y + Hd)."""
+    cases = [chartgen.small_case(s, n=40, family=f, rho=r)
+             for s, (f, r) in enumerate([("uv", 0.8), ("tss", 1.2), ("mixed", 0.5),
+                                         ("lightmap", 1.0)])]
+    checked = 0
+    for cs in cases:
+        for k in (1, 3, 10):
+            st, px, _ = orc.build_proxies(cs.xy, cs.start, k)
+            assert st == orc.OK
+            for p in px:
+                for num, den, g in ((64, 64, 1), (37, 64, 0), (5, 16, 2), (912345, 1 << 20, 1)):
+                    pr = orc.Profile(p, num, den, g)
+                    assert max(pr.Dbot) == pr.Hd and min(pr.Dtop) == 0
+                    assert max(pr.Dright) == pr.Wd and min(pr.Dleft) == 0
+                    checked += 1
+    assert checked > 1000
