@@ -318,7 +318,13 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid >= kPT) return;
   const int n = pp.n, Wp = pp.Wp, Hp = pp.Hp;
-  if (st->bad_chart != INT32_MAX || st->capacity) return;
+  // (decided by thread 0 for the whole packer: in batch mode another CTA
+  // evaluating a rank of the same atlas may set the capacity bits meanwhile)
+  __shared__ int32_t pk_bad;
+  if (tid == 0) pk_bad = (*(volatile int32_t*)&st->bad_chart != INT32_MAX ||
+                          *(volatile int32_t*)&st->capacity != 0) ? 1 : 0;
+  pk_sync();
+  if (pk_bad) return;
   // fused mode: tiles [0, ready_upto] of this slot are known to be published
   if (tid == 0) ready_upto = -1;
   // sequential mode: a higher candidate already succeeded, so this one cannot
@@ -670,7 +676,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
     }
     // sequential fused mode: has a higher candidate won?  Loaded here, used at
     // the row end, so the load's latency hides behind the row
-    if (tid == 0 && rd.flags && pp.early) wj = *(volatile int32_t*)&st->win_j;
+    // (batch mode: a lower rank of the same atlas, i.e. a larger m, won)
+    if (tid == 0 && (rd.flags || lz) && pp.early) wj = *(volatile int32_t*)&st->win_j;
     // ---- footprint prefetch for this row (consumed by the push's stage) ----
     // (no global loads on thread 0's path: the row start's slot offset was
     // kept from the previous row's fold; in fused mode only once every tile
@@ -1288,7 +1295,7 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
         const i128 SCm2 = (i128)pp.M * TABI_UNITS * pp.M * TABI_UNITS;
         if (rem * m * m > 2 * SCm2 * freeA) S.fail = 1;
       }
-      if (rd.flags && pp.early && wj < jslot) S.abort = 1;  // checked at the next row start
+      if ((rd.flags || lz) && pp.early && wj < jslot) S.abort = 1;  // checked at the next row start
       const int nx = endS + 1;  // the next row's slot offset, if this fold saw it
       S.next_a0 = prefix_mode ? pf_next
                   : (S.w_fold && nx < n && nx < S.fold_hi && nx - rs < kRW) ? W.rco[nx - rs] : -1;
@@ -1670,9 +1677,10 @@ __device__ __forceinline__ void st_release_i(int32_t* p, int32_t v) {
 __global__ void __launch_bounds__(kNT, 1)
 many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ int32_t item_s, outcome_s;
+  __shared__ int32_t item_s, outcome_s, skip_s;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gcta = blockIdx.x;
+  int carry = -1;  // thread 0: the next rank of the atlas this CTA just failed
   const int64_t nm = A.nmax;
   uint32_t* dcol = A.dcol + (int64_t)gcta * pp0.col_cap;
   uint32_t* drow = A.drow + (int64_t)gcta * pp0.row_cap;
@@ -1692,24 +1700,44 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
   if (tid == 0) A.cycles[3 + 2 * gcta] = A.cycles[3 + 2 * gcta + 1] = gtime();
   while (true) {
     if (tid == 0) {
-      const int i = atomicAdd(&A.qctl[0], 1);
-      int v = -1;
-      if (i < A.qcap) {
-        while ((v = ld_acquire_i(A.q + i)) < 0) {
-          if (ld_acquire_i(A.qctl + 2) == 0) break;  // every atlas decided
-          __nanosleep(256);
+      int v = carry;
+      if (v < 0) {
+        const int i = atomicAdd(&A.qctl[0], 1);
+        if (i < A.qcap) {
+          while ((v = ld_acquire_i(A.q + i)) < 0) {
+            if (ld_acquire_i(A.qctl + 2) == 0) break;  // every atlas decided
+            __nanosleep(256);
+          }
         }
       }
       item_s = v;
+      // a rank of an atlas already decided, or above a lower rank that won, is
+      // skipped -- decided HERE, once, for the whole CTA (other CTAs change
+      // these words concurrently, so per-thread reads could disagree)
+      if (v >= 0) {
+        const int a = v & 0xfffff, r = v >> 20;
+        const Status* sa = A.sts + a;
+        const int na = A.abase[a + 1] - A.abase[a];
+        const bool bad_a = *(volatile int32_t*)&sa->bad_chart != INT32_MAX ||
+                           *(volatile int32_t*)&sa->capacity != 0 || na < 1 || na > A.nmax;
+        skip_s = bad_a ? 2
+                 : (*(volatile int32_t*)&sa->win_j < r || *(volatile int32_t*)&A.res[a].done != 0) ? 1
+                                                                                                  : 0;
+      }
     }
     __syncthreads();
     const int item = item_s;
     if (item < 0) break;
     const int a = item & 0xfffff, r = item >> 20;
     Status* st = A.sts + a;
+    AtlasRes& R = A.res[a];
     const int c0 = A.abase[a], n = A.abase[a + 1] - c0;
     const int m = st->pad[2] - r;
-    const bool dead = st->bad_chart != INT32_MAX || st->capacity || m < 1 || n < 1 || n > A.nmax;
+    // an atlas problem (bad chart, capacity) decides the atlas; a rank past the
+    // last candidate (m < 1), one above an already successful rank, or of a
+    // decided atlas is not evaluated (m is fixed for the atlas)
+    const bool bad = skip_s == 2;
+    const bool dead = bad || m < 1 || skip_s != 0;
     PackParams pp = pp0;
     pp.n = n;
     Proxies P = A.P;
@@ -1785,29 +1813,71 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
       // ---- Alg. 4 for this candidate (K4) -----------------------------------
       if (tid == 0) tc2 = clock64();
       packer(pp, colofs, rowofs, dcol, drow, wd, hd, off, lock, A.hsorted + c0, cbad, scr,
-             A.pair_cap, X, Y, mir, cand, st, prof_cap, m, 0, 0, Ready{nullptr, 0, nullptr, nullptr},
+             A.pair_cap, X, Y, mir, cand, st, prof_cap, m, 0, r, Ready{nullptr, 0, nullptr, nullptr},
              dsm, A.lazy != 0, lzr);
       __syncthreads();
     }
     if (tid == 0) {
+      // Outcome.  Several ranks of one atlas may be in flight (A.inflight
+      // initial items per atlas; a CTA whose rank failed continues with the
+      // atlas's next unissued rank): the winner is the lowest successful rank
+      // all of whose lower ranks failed -- the top-down search's result.
       const Cand cd = *cand;  // (written by this CTA before the barrier)
-      int oc;  // 0 failed -> next candidate, 1 succeeded, 2 decided without success
-      if (dead) oc = 2;
-      else if (cd.success) oc = 1;
-      else oc = m > 1 ? 0 : 2;
-      AtlasRes& R = A.res[a];
+      int oc;  // 0 failed, 1 won, 2 atlas decided as bad, 3 not needed
+      if (bad) oc = 2;
+      else if (m < 1) oc = 0;
+      else if (dead || *(volatile int32_t*)&st->win_j < r) oc = 3;  // (beaten)
+      else oc = cd.success ? 1 : 0;
       if (!dead) {
-        R.evaluated++;
+        atomicAdd(&R.evaluated, 1);
         const long long t3 = clock64();
         atomicAdd(&A.cycles[0], (unsigned long long)(tc1 - tc0));
         atomicAdd(&A.cycles[1], (unsigned long long)(tc2 - tc1));
         atomicAdd(&A.cycles[2], (unsigned long long)(t3 - tc2));  // (lazy: raster inside, see below)
       }
       if (oc == 1) {
-        R.winner = m;
-        R.rows = cd.rows;
-        R.knees_found = cd.knees_found;
-        R.knee_rows = cd.knee_rows;
+        // announce (higher ranks in flight stop at their next row), then wait
+        // until every lower rank has failed -- or a lower rank won
+        atomicMin(&st->win_j, r);
+        while (true) {
+          __threadfence();
+          if (*(volatile int32_t*)&st->win_j < r || *(volatile int32_t*)&R.done != 0) { oc = 3; break; }
+          bool all = true;
+          for (int w = 0; w * 32 < r; w++) {
+            const uint32_t mk = r - w * 32 >= 32 ? 0xffffffffu : ((1u << (r - w * 32)) - 1u);
+            if ((*(volatile uint32_t*)&R.fail[w] & mk) != mk) all = false;
+          }
+          if (all) break;
+          __nanosleep(256);
+        }
+        if (oc == 1) {
+          R.winner = m;
+          R.rows = cd.rows;
+          R.knees_found = cd.knees_found;
+          R.knee_rows = cd.knee_rows;
+        }
+      }
+      carry = -1;
+      if (oc == 0) {
+        __threadfence();
+        if (r < 256) atomicOr(&R.fail[r >> 5], 1u << (r & 31));
+        // no rank has succeeded yet: this CTA continues with the atlas's next
+        // rank (issued before this rank's completion is counted, below)
+        if (*(volatile int32_t*)&st->win_j == INT32_MAX && *(volatile int32_t*)&R.done == 0) {
+          const int nr = atomicAdd(&R.next_r, 1);
+          if (st->pad[2] - nr >= 1 && nr < 256) {
+            atomicAdd(&R.issued, 1);
+            if (A.carry) {
+              carry = a | (nr << 20);
+            } else {
+              // one rank in flight (many atlases per CTA): the next rank goes
+              // to the queue's tail, so the atlases' chains interleave
+              const int slot = atomicAdd(&A.qctl[1], 1);
+              if (slot < A.qcap) st_release_i(A.q + slot, a | (nr << 20));
+              else atomicOr(&st->capacity, 8);  // (cannot happen: E * M slots)
+            }
+          }
+        }
       }
       outcome_s = oc;
     }
@@ -1836,17 +1906,16 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
     }
     __syncthreads();  // (placements written before the atlas is announced)
     if (tid == 0) {
-      if (oc == 0) {
-        const int slot = atomicAdd(&A.qctl[1], 1);
-        if (slot < A.qcap) {
-          st_release_i(A.q + slot, a | ((r + 1) << 20));
-        } else {  // (cannot happen: the queue holds M items per atlas)
-          atomicOr(&st->capacity, 8);
-          __threadfence();
-          atomicSub(&A.qctl[2], 1);
-        }
-      } else {
-        A.res[a].done = 1;
+      // the atlas is decided once: by its winner, by a bad chart / capacity
+      // overflow, or -- no rank succeeded -- by the completion that finds
+      // every issued rank done (a rank issues its successor before its own
+      // completion is counted, so nothing is issued after that point)
+      bool decide = oc == 1 || oc == 2;
+      const int done_now = atomicAdd(&R.completed, 1) + 1;
+      if (!decide && carry < 0 && done_now == *(volatile int32_t*)&R.issued &&
+          *(volatile int32_t*)&st->win_j == INT32_MAX)
+        decide = true;
+      if (decide && atomicCAS(&R.done, 0, 1) == 0) {
         __threadfence();
         atomicSub(&A.qctl[2], 1);
       }

@@ -585,7 +585,7 @@ many_sort_prep_kernel(Proxies P, const int32_t* __restrict__ abase, int32_t* per
 // (items [0, E) = the batched atlases in `order`, candidate offset 0; the
 // rest empty).
 __global__ void many_reset_kernel(Status* sts, AtlasRes* res, int32_t A, const int32_t* order,
-                                  int32_t E, int32_t* q, int32_t qcap, int32_t* qctl) {
+                                  int32_t E, int32_t* q, int32_t qcap, int32_t* qctl, int32_t K) {
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t a = t0; a < A; a += stride) {
@@ -593,13 +593,19 @@ __global__ void many_reset_kernel(Status* sts, AtlasRes* res, int32_t A, const i
     for (size_t i = 0; i < sizeof(Status) / 4; i++) w[i] = 0;
     sts[a].bad_chart = INT32_MAX;
     sts[a].win_j = INT32_MAX;
-    res[a] = AtlasRes{0, 0, 0, 0, 0, 0};
+    AtlasRes z{};
+    z.next_r = K;
+    z.issued = K;
+    res[a] = z;
   }
-  for (int64_t i = t0; i < qcap; i += stride) q[i] = i < E ? order[i] : -1;
+  // item i: atlas order[i / K], rank i % K (the largest atlases first, each
+  // with K ranks in flight)
+  for (int64_t i = t0; i < qcap; i += stride)
+    q[i] = i < (int64_t)E * K ? order[i / K] | (int32_t)((i % K) << 20) : -1;
   if (t0 == 0) {
-    qctl[0] = 0;  // head
-    qctl[1] = E;  // tail
-    qctl[2] = E;  // atlases not yet decided
+    qctl[0] = 0;      // head
+    qctl[1] = E * K;  // tail
+    qctl[2] = E;      // atlases not yet decided
   }
 }
 
@@ -700,12 +706,12 @@ void launch_many_sort_prep(const Proxies& P, const int32_t* abase, int32_t A, in
 }
 
 void launch_many_reset(Status* sts, AtlasRes* res, int32_t A, const int32_t* order, int32_t E,
-                       int32_t* q, int32_t qcap, int32_t* qctl, cudaStream_t s) {
+                       int32_t* q, int32_t qcap, int32_t* qctl, int32_t inflight, cudaStream_t s) {
   const int64_t work = qcap > A ? qcap : A;
   int blocks = (int)((work + 255) / 256);
   if (blocks > 296) blocks = 296;
   if (blocks < 1) blocks = 1;
-  many_reset_kernel<<<blocks, 256, 0, s>>>(sts, res, A, order, E, q, qcap, qctl);
+  many_reset_kernel<<<blocks, 256, 0, s>>>(sts, res, A, order, E, q, qcap, qctl, inflight);
 }
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,

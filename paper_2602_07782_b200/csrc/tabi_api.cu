@@ -1292,7 +1292,6 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     const int32_t* d_abase = w.d_small;
     const int32_t* d_order = w.d_small + A + 1;
     const float* d_res = (const float*)(w.d_small + 2 * A + 1);
-    const int32_t qcap = (int32_t)std::min<int64_t>(w.cap_q, (int64_t)E * M);
     int32_t* qctl = w.q + w.cap_q;
     PackParams pp;
     memset(&pp, 0, sizeof(pp));
@@ -1308,7 +1307,23 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     pp.B = 1;
     pp.col_cap = w.col_cap;
     pp.row_cap = w.row_cap;
-    launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, s);
+    pp.early = 1;  // a rank stops at its next row once a lower rank (larger m) won
+    // Ranks in flight per atlas: one atlas's top-down chain is sequential (up
+    // to 16 candidates of a 2,000-chart atlas in C5), which sets the batch's
+    // critical path when the GPU has more CTAs than the batch has atlases to
+    // keep them busy.  K = floor(3 G / E) ranks of each atlas start at once
+    // (1 for the 512- and 256-atlas shares of C5 on one / two GPUs, 3 for
+    // 128, 6 for 64), a CTA whose rank failed then continuing with the
+    // atlas's next rank; a rank above the winner is wasted work, so K stays
+    // 1 while the atlases alone fill the GPU (failures then requeue at the
+    // tail).  Measured on C5 subsets: 128 atlases 7.1 -> 4.7 ms, 64 atlases
+    // 7.0 -> 3.0 ms; 256: 7.5 vs 7.7 ms with K = 2.  TABI_MANY_INFLIGHT
+    // overrides.
+    const char* ienv = getenv("TABI_MANY_INFLIGHT");
+    int32_t inflight = ienv ? atoi(ienv) : (int32_t)((3 * (int64_t)w.G) / std::max(E, 1));
+    inflight = std::max<int32_t>(1, std::min<int32_t>(inflight, std::min<int32_t>(8, M)));
+    const int32_t qcap = (int32_t)std::min<int64_t>(w.cap_q, (int64_t)E * M);
+    launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, inflight, s);
     CK(cudaMemsetAsync(w.cycles, 0, 3 * sizeof(unsigned long long), s));
     if (timing) CK(cudaEventRecord(w.stage[0], s));
     for (int j = 0; j < nch; j++) {
@@ -1335,6 +1350,16 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     ma.q = w.q;
     ma.qctl = qctl;
     ma.qcap = qcap;
+    {
+      const char* cenv = getenv("TABI_MANY_CARRY");  // test knob: 1 = continue the atlas even at K = 1
+      ma.inflight = inflight;
+      // a CTA continues its atlas's chain itself while the batch has fewer
+      // atlases than 2 G (measured: 256 C5 atlases 8.1 -> 7.4 ms); with more,
+      // failures requeue at the tail so the chains interleave (512: 13.2 ->
+      // 12.9 ms)
+      ma.carry = (inflight > 1 || E < 2 * w.G || (cenv && cenv[0] == '1')) ? 1 : 0;
+      if (cenv && cenv[0] == '0') ma.carry = inflight > 1 ? 1 : 0;
+    }
     ma.dcol = w.dcol;
     ma.drow = w.drow;
     ma.wd = w.wd;

@@ -382,6 +382,11 @@ struct AtlasRes {
   int32_t rows, knees_found, knee_rows;
   int32_t evaluated;   // candidates evaluated (top-down from the area bound)
   int32_t done;        // 1 once decided (success or every candidate failed)
+  int32_t next_r;      // next rank (m = m_hi - r) to issue
+  int32_t issued;      // ranks issued (the initial in-flight ones + continuations)
+  int32_t completed;   // ranks finished (failed, won, or not needed)
+  int32_t pad;
+  uint32_t fail[8];    // bit r: rank r failed (r < 256)
 };
 constexpr int kManyMaxCharts = 2048;  // per atlas in the device batch (one-CTA sort)
 
@@ -528,12 +533,16 @@ struct ManyArgs {
                                   // then [G][2] per CTA: start, end of its last item (ns)
   int64_t* area;                  // [G][nmax] lazy mode: 2 x polygon area by sorted position
   int32_t lazy;                   // rasterize on demand inside the packer (many_lazy_ok)
+  int32_t inflight;               // ranks of one atlas in flight at once (K >= 1)
+  int32_t carry;                  // a CTA whose rank failed continues with the next rank
+                                  // (else the next rank goes to the queue's tail)
   int32_t early_fail;             // lazy mode: the row-end area test (R8)
   int32_t nmax;
   int64_t pair_cap;
 };
+// queue: ranks 0 .. inflight - 1 of every atlas, interleaved in `order`
 void launch_many_reset(Status* sts, AtlasRes* res, int32_t A, const int32_t* order, int32_t E,
-                       int32_t* q, int32_t qcap, int32_t* qctl, cudaStream_t s);
+                       int32_t* q, int32_t qcap, int32_t* qctl, int32_t inflight, cudaStream_t s);
 void launch_many_sort_prep(const Proxies& P, const int32_t* abase, int32_t A, int32_t* perm,
                           const PackParams& pp, int32_t* colofs, int32_t* rowofs, int32_t* hsorted,
                           int32_t* tstart, int32_t* tix, Status* sts, cudaStream_t s);
