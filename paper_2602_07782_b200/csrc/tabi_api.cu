@@ -1311,17 +1311,21 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     // Ranks in flight per atlas: one atlas's top-down chain is sequential (up
     // to 16 candidates of a 2,000-chart atlas in C5), which sets the batch's
     // critical path when the GPU has more CTAs than the batch has atlases to
-    // keep them busy.  K = floor(3 G / E) ranks of each atlas start at once
-    // (1 for the 512- and 256-atlas shares of C5 on one / two GPUs, 3 for
-    // 128, 6 for 64), a CTA whose rank failed then continuing with the
-    // atlas's next rank; a rank above the winner is wasted work, so K stays
-    // 1 while the atlases alone fill the GPU (failures then requeue at the
-    // tail).  Measured on C5 subsets: 128 atlases 7.1 -> 4.7 ms, 64 atlases
-    // 7.0 -> 3.0 ms; 256: 7.5 vs 7.7 ms with K = 2.  TABI_MANY_INFLIGHT
+    // keep them busy.  K = round(sqrt(6 G / E)) ranks of each atlas start at
+    // once when E < 4 G / 3, else 1 (1 for the 512- and 256-atlas shares of
+    // C5 on one / two GPUs, 3 for 128, 4 for 64, 5 for 32), a CTA whose rank
+    // failed then continuing with the atlas's next rank; a rank above the
+    // winner is wasted work, so more is not better.  Measured on C5 subsets
+    // (kernel ms by K): 128 atlases 7.1 / 4.7 / 5.6 / 6.7 (K = 1 / 3 / 4 /
+    // 6), 64: 7.0 / 3.4 / 3.2 / 3.7 (1 / 3 / 4 / 6), 32: 2.9 / 2.5 / 2.3 /
+    // 2.7 (3 / 4 / 6 / 8); 256: 7.4 / 7.7 (1 / 2).  TABI_MANY_INFLIGHT
     // overrides.
     const char* ienv = getenv("TABI_MANY_INFLIGHT");
-    int32_t inflight = ienv ? atoi(ienv) : (int32_t)((3 * (int64_t)w.G) / std::max(E, 1));
-    inflight = std::max<int32_t>(1, std::min<int32_t>(inflight, std::min<int32_t>(8, M)));
+    int32_t inflight = 1;
+    if (ienv) inflight = atoi(ienv);
+    else if (3 * (int64_t)E < 4 * (int64_t)w.G)
+      inflight = (int32_t)lround(sqrt(6.0 * w.G / std::max(E, 1)));
+    inflight = std::max<int32_t>(1, std::min<int32_t>(inflight, std::min<int32_t>(16, M)));
     const int32_t qcap = (int32_t)std::min<int64_t>(w.cap_q, (int64_t)E * M);
     launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, inflight, s);
     CK(cudaMemsetAsync(w.cycles, 0, 3 * sizeof(unsigned long long), s));
