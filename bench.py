@@ -326,6 +326,40 @@ def c3_latency(ctx, stream, dev, rho, seeds, reps, flush):
             "l2_stretch": stretch, "scale_index": ms_m, "rows": rows}
 
 
+def shard_shares(ctx, stream, dev, flush, spec, reps=3):
+    """The per-GPU work of the multi-GPU C5 step, measured on this GPU: for
+    N = 2, 4, 8 every rank's LPT share (the exact share bench.py --gpus N
+    gives that rank) packed by one tabi_pack_many, device span median of
+    `reps`.  The N-GPU step has no inter-GPU work (no data-path collective),
+    so its time is the slowest share's: 512 / that time is what an N-GPU run
+    of this build delivers on this GPU model (an N-GPU run measures it
+    directly)."""
+    import numpy as np
+    import torch
+    from paper_2602_07782_b200 import concat_chart_sets
+    out = {}
+    for n in (2, 4, 8):
+        per = []
+        for r in range(n):
+            sets = c5_sets(rank_share(n, r))
+            xy, cst, abase, res = concat_chart_sets(sets)
+            xy_d, cst_d = torch.from_numpy(xy).to(dev), torch.from_numpy(cst).to(dev)
+            ctx.pack_many(xy_d, cst_d, abase, spec, res_xy=res, stream=stream.cuda_stream)
+            ts = []
+            for _ in range(reps):
+                flush()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                ctx.pack_many(xy_d, cst_d, abase, spec, res_xy=res, stream=stream.cuda_stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            per.append(float(np.median(ts)))
+        out[f"gpus_{n}"] = {"share_ms": [round(x, 3) for x in per], "max_share_ms": max(per),
+                            "atlases_per_s": C5_ATLASES * 1000.0 / max(per)}
+    return out
+
+
 def knob_sweep(ctx, stream, dev, flush, reps=8):
     """C3 (rho = 1.5, seed 0): local-AABB count k x t_opt."""
     import torch
@@ -550,6 +584,7 @@ def main():
         line["c3"] = c3
         line["interactive_budget_ms"] = 15.0
         line["knob_sweep"] = knob_sweep(ctx, stream, dev, flush)
+        line["shard_shares"] = shard_shares(ctx, stream, dev, flush, spec)
         # per-row cost of the headline pack vs the building-block floor
         cs, _ = workload("C3", 0, C3_HEADLINE_RHO)
         os.environ["TABI_TIMING"] = "1"
