@@ -563,7 +563,8 @@ def main():
                       "per_gpu_busy_ms": sum(step_ms) / args.steps,
                       # batch-kernel load balance: last CTA's end after the
                       # median CTA's last item; mean CTA busy fraction
-                      "kernel_tail_ms": bi.tail_ms, "kernel_busy_frac": bi.busy_frac},
+                      "kernel_tail_ms": bi.tail_ms, "kernel_busy_frac": bi.busy_frac,
+                      "ranks_in_flight": bi.ranks_in_flight},
             "roofline": roof,
             "hbm_compulsory": {"bytes_per_step": hbm_bytes,
                                "gbs": hbm_bytes / (ms_per_step * 1e-3) / 1e9,

@@ -224,6 +224,9 @@ typedef struct {
   float tail_ms;                  /* batch kernel load balance: time from the median CTA's
                                      last item end to the last CTA's */
   float busy_frac;                /* mean over CTAs of (last item end - start) / kernel span */
+  int32_t ranks_in_flight;        /* candidate ranks of one atlas evaluated at once (K >= 1:
+                                     more when the batch has few atlases for the GPU) */
+  int32_t reserved;
 } tabi_batch_info;
 
 tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t n_atlases, const float* xy,

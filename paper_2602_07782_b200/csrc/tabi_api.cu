@@ -1328,6 +1328,7 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
     inflight = std::max<int32_t>(1, std::min<int32_t>(inflight, std::min<int32_t>(16, M)));
     const int32_t qcap = (int32_t)std::min<int64_t>(w.cap_q, (int64_t)E * M);
     launch_many_reset(w.sts, w.res, A, d_order, E, w.q, qcap, qctl, inflight, s);
+    if (binfo) binfo->ranks_in_flight = inflight;
     CK(cudaMemsetAsync(w.cycles, 0, 3 * sizeof(unsigned long long), s));
     if (timing) CK(cudaEventRecord(w.stage[0], s));
     for (int j = 0; j < nch; j++) {

@@ -69,7 +69,8 @@ class BatchInfo(C.Structure):
     _fields_ = [("device_ms", C.c_float), ("stage_ms", C.c_float * 4), ("gpu_launches", C.c_int32),
                 ("candidates_evaluated", C.c_int32), ("batched_atlases", C.c_int32),
                 ("solo_atlases", C.c_int32), ("work_pack", C.c_int64), ("work_profile", C.c_int64),
-                ("cycles", C.c_int64 * 3), ("tail_ms", C.c_float), ("busy_frac", C.c_float)]
+                ("cycles", C.c_int64 * 3), ("tail_ms", C.c_float), ("busy_frac", C.c_float),
+                ("ranks_in_flight", C.c_int32), ("reserved", C.c_int32)]
 
 
 PLACEMENT_DTYPE = np.dtype([("tx", "<i4"), ("ty", "<i4"), ("scale_num", "<i4"),
