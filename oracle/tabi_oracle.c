@@ -12,6 +12,11 @@
  * No blocking, fusion or reordering: every candidate, every configuration
  * (all 4 or 8 of P:301) and every frontline copy (Alg. 4 line "Copy frontLine
  * to localFrontLine[j]") is evaluated literally.
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC / paper worked examples,
+ * hand-derived goldens for every tightening step, closed forms (single chart,
+ * equal-square prefix tails, exact-tail squares), brute-force optimal
+ * packings, exact-rational clipping, invariants; no function is left
+ * "parity unpinned".
  */
 #include "oracle.h"
 

@@ -425,3 +425,15 @@ def test_prefix_tail_equal_squares_parity(orc, ctx, a, n, W, g, M):
     polys = [[(0, 0), (a, 0), (a, a), (0, a)] for _ in range(n)]
     cs = chartgen.from_polygons(polys, W, W)
     _compare_pack(orc, ctx, cs, check_profiles=3, t_opt_bp=1000, gutter=g, scale_count=M)
+
+
+def test_obb_angle_ties_parity(orc, ctx):
+    """D6's tie rule on the GPU: shapes whose two best OBB angles tie exactly
+    (tests/test_oracle_properties.py::D6_TIES), packed together with a few
+    scaled copies -- proxies (obb_j, extents) and placements bit-exact."""
+    from test_oracle_properties import D6_TIES
+    polys = []
+    for s in (1, 2, 3):
+        polys += [[(x * s, y * s) for x, y in p] for p in D6_TIES]
+    cs = chartgen.from_polygons(polys, 1024, 1024)
+    _compare_pack(orc, ctx, cs, check_profiles=4)

@@ -307,3 +307,37 @@ def test_footprint_extremes_equal_the_dilated_box(orc):
                     assert max(pr.Dright) == pr.Wd and min(pr.Dleft) == 0
                     checked += 1
     assert checked > 1000
+
+
+# Polygons symmetric about the diagonal x = y whose minimum-area boxes over
+# the 8 angles of D6 are tied between j and 8 - j (the Q30 table has
+# C_{8-j} = S_j, so the mirror image ties exactly in integers).
+D6_TIES = [[(0, 0), (27, 10), (37, 37), (10, 27)],
+           [(0, 0), (14, 9), (23, 23), (9, 14)],
+           [(0, 0), (71, 18), (89, 89), (18, 71)],
+           [(0, 0), (41, 19), (80, 40), (90, 90), (40, 80), (19, 41)],
+           [(0, 0), (33, 23), (66, 46), (105, 63), (112, 112), (63, 105), (46, 66), (23, 33)]]
+_QC = [1073741824, 1053110176, 992008094, 892783698, 759250125, 596538995, 410903207, 209476638]
+_QS = [0, 209476638, 410903207, 596538995, 759250125, 892783698, 992008094, 1053110176]
+
+
+def test_obb_angle_tie_takes_the_smaller_angle(orc):
+    """D6 tie rule ('ties -> smaller j'): on shapes whose two best
+    angles give exactly equal box areas, the oracle's OBB is the smaller j --
+    the areas recomputed here from the snapped outline (any reflection of the
+    final pose maps j to 8 - j, which the symmetry leaves tied)."""
+    for poly in D6_TIES:
+        q = [(x * 256, y * 256) for x, y in poly]
+        areas = []
+        for j in range(8):
+            us = [x * _QC[j] + y * _QS[j] for x, y in q]
+            vs = [-x * _QS[j] + y * _QC[j] for x, y in q]
+            areas.append((max(us) - min(us)) * (max(vs) - min(vs)))
+        best = min(areas)
+        tied = [j for j in range(8) if areas[j] == best]
+        assert len(tied) == 2 and tied[0] + tied[1] == 8 and tied[0] in (1, 2, 3), (poly, tied)
+        cs = chartgen.from_polygons([poly], 512, 512)
+        st, px, _ = orc.build_proxies(cs.xy, cs.start, 10)
+        assert st == orc.OK and px[0].obb_j == tied[0], (poly, px[0].obb_j, tied)
+        # and the box is that angle's: its extents give the minimum area
+        assert (px[0].umax - px[0].umin) * (px[0].vmax - px[0].vmin) == best
