@@ -232,6 +232,12 @@ __device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
 __device__ __forceinline__ void red_add_release(int32_t* p, int32_t v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// a release pattern: one fence, then relaxed adds (a release per add would
+// fence each one)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_add_relaxed(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -687,7 +693,8 @@ __device__ __forceinline__ void packer(PackParams pp, const int32_t* __restrict_
       // every tile of this candidate published?  (one acquire load of the
       // slot's completed-tile count; the fold's window fills probe far less
       // often than once a row)
-      if (rd.flags && ready_lim != n - 1 && ld_acquire(rd.flags + 2 * (int64_t)pp.B * n + jslot) >= rd.T) {
+      if (rd.flags && ready_lim != n - 1 &&
+          ld_acquire(rd.flags + 2 * (int64_t)pp.B * n + jslot) >= 2 * rd.T) {
         asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads follow
         ready_upto = rd.T - 1;
         ready_lim = n - 1;
@@ -1462,44 +1469,13 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
   // the first G items go to the G raster groups statically (no queue round
   // trip before the first -- most urgent -- tiles); the queue hands out the rest
   const int G = ((int)gridDim.x - Bw) * kRG;
-  int first_it = ((int)blockIdx.x - Bw) * kRG + grp;
-  int next_it = -1;  // (leader) an item claimed during the previous tile's pair phase
-  while (true) {
-    // (fetching the next item ahead would hide this round trip, but lets a
-    // busy CTA sit on an early tile the packers are waiting for)
-    if (gt == 0) {
-      const int it0 = first_it >= 0 ? first_it
-                      : next_it >= 0 ? next_it : G + atomicAdd(&st->work_next, 1);
-      next_it = -1;
-      misc[0] = it0;
-      // drop items of a candidate that failed (its packer has exited), and in
-      // sequential mode of candidates below a successful one (decided once, by
-      // the leader, so the group branches uniformly); the top candidate's
-      // items (slot 0) can never be beaten
-      const int j0 = !(kTopFirst && pp.early) || Bw == 1 ? it0 % Bw
-                     : it0 < T ? 0 : 1 + (it0 - T) % (Bw - 1);  // item -> slot, as below
-      misc[4] = (pp.early && j0 > 0 && *(volatile int32_t*)&st->win_j < j0) ||
-                *(volatile int32_t*)(ra.rdy + 2 * (int64_t)pp.B * pp.n + pp.B + j0) != 0;
-    }
-    first_it = -1;
-    gsync();
-    const int it = misc[0];
-    const bool dropped = misc[4] != 0;
-    gsync();
-    rmark(0);
-    if (it >= NB) {
-      if (gt == 0) atomicMax(&st->tr[1], gtime());
-#ifdef TABI_PHASE_TRACE
-      if (gt == 0)
-        for (int i = 0; i < 8; i++) atomicAdd(&st->rph[i], rph[i]);
-#endif
-      break;
-    }
-    // Tile-major over the wave's slots (kTopFirst: in sequential mode the
-    // highest candidate's tiles first, then the others tile-major); items of
-    // a failed candidate, or of one below a successful one, are dropped (its
-    // packer has exited).
-    int t, j;
+  // (constant for the launch: loaded once -- the loop's atomics would make
+  // the compiler reload them every tile)
+  const int32_t wave = st->wave, b0 = st->b0;
+  int32_t* const done_cnt0 = ra.rdy + 2 * (int64_t)pp.B * pp.n;
+  // Tile-major over the wave's slots (kTopFirst: in sequential mode the
+  // highest candidate's tiles first, then the others tile-major).
+  auto item_tj = [&](int it, int& t, int& j) {
     if (!(kTopFirst && pp.early) || Bw == 1) {
       t = it / Bw;
       j = it % Bw;
@@ -1510,10 +1486,64 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       t = (it - T) / (Bw - 1);
       j = 1 + (it - T) % (Bw - 1);
     }
-    if (dropped) continue;
-    const int m = wave_m(pp, st->wave, m_hi, st->b0, j);
-    if (m == 0) continue;
-    const int s0 = ra.tstart[t], nt = ra.tstart[t + 1] - s0;
+  };
+  // (leader) an item's drop hint and tile bounds: items of a candidate that
+  // failed (its packer has exited), and in sequential mode of candidates below
+  // a successful one, are dropped -- the top candidate's (slot 0) never are
+  auto probe = [&](int it, int& drop, int32_t& ts0, int32_t& ts1) {
+    drop = 1;
+    ts0 = ts1 = 0;
+    if (it >= NB) return;
+    int t, j;
+    item_tj(it, t, j);
+    drop = (pp.early && j > 0 && *(volatile int32_t*)&st->win_j < j) ||
+           *(volatile int32_t*)(done_cnt0 + pp.B + j) != 0;
+    ts0 = ra.tstart[t];
+    ts1 = ra.tstart[t + 1];
+  };
+  int first_it = ((int)blockIdx.x - Bw) * kRG + grp;
+  // the claimer (lane 0 of the group's last warp) claims the next item during
+  // a tile's pair phase and leaves it, its drop hint and its tile bounds in
+  // misc[0], misc[4..6] with misc[7] = 1; the leader (gt == 0) claims at the
+  // loop top only when nothing was left there
+  const int gclaim = 32 * (kRGW - 1);
+  static_assert(kRGW >= 2, "pair phase: warp 0 boundary pairs, the rest internal pairs");
+  if (gt == 0) misc[7] = 0;
+  while (true) {
+    if (gt == 0) {
+      if (misc[7] == 0) {  // the first item, or the one after a dropped item
+        const int it0 = first_it >= 0 ? first_it : G + atomicAdd(&st->work_next, 1);
+        int drop;
+        int32_t ts0, ts1;
+        probe(it0, drop, ts0, ts1);
+        misc[0] = it0;
+        misc[4] = drop;
+        misc[5] = ts0;
+        misc[6] = ts1;
+      }
+      misc[7] = 0;
+    }
+    first_it = -1;
+    gsync();
+    const int it = misc[0];
+    const bool dropped = misc[4] != 0;
+    const int s0 = misc[5], nt = misc[6] - s0;
+    rmark(0);
+    if (it >= NB) {
+      if (gt == 0) atomicMax(&st->tr[1], gtime());
+#ifdef TABI_PHASE_TRACE
+      if (gt == 0)
+        for (int i = 0; i < 8; i++) atomicAdd(&st->rph[i], rph[i]);
+#endif
+      break;
+    }
+    int t, j;
+    item_tj(it, t, j);
+    const int m = dropped ? 0 : wave_m(pp, wave, m_hi, b0, j);
+    if (m == 0) {
+      gsync();  // (everyone has read misc before the leader rewrites it)
+      continue;
+    }
     const k3::Scale sc{m, SCm, 0};
     // (g <= kDilMax: the raw buffer is free and holds the tile's dilated row
     // footprints for its internal pair offsets)
@@ -1534,45 +1564,41 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
 #ifdef TABI_PHASE_TRACE
     if (gt == 0 && t == 0 && j == 0) atomicMax(&st->tfirst[0], gtime());
 #endif
-    for (int ci = gw; ci < nt; ci += kRGW)
-      if (big[ci])
-        k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m - 1, s0 + ci, sc, CW[wid],
-                      wtab + wid * 4 * k, lane);
-    if (gt < 32) {  // work accounting: footprint entries of the tile (from smem)
-      unsigned long long pe = 0;
-      for (int ci = gt; ci < nt; ci += 32)
-        pe += (unsigned long long)(CH[ci].ws + CH[ci].hs + 4 * pp.g);
-      for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
-      if (gt == 0) atomicAdd(&st->work_prof, pe);
+    if (pp.g > k3::kDilMax) {  // (uniform; g <= kDilMax hands no chart to this pass)
+      for (int ci = gw; ci < nt; ci += kRGW)
+        if (big[ci])
+          k3::big_chart(ra.P, ra.perm, pp, colofs, rowofs, ra.dcol, ra.drow, m - 1, s0 + ci, sc,
+                        CW[wid], wtab + wid * 4 * k, lane);
+      gsync();
     }
-    gsync();
     rmark(2);
     // Adjacent pairs: the tile's internal pairs here; a boundary pair with a
     // neighbour tile is done by whichever of the two tiles publishes its
     // footprints second (arrival counter per boundary, acq_rel), so no tile
     // waits for another.  rdy[t] reaches 2 once the pairs (s, s + 1) of all
     // s in tile t are done: its internal pairs (+1) and its right boundary (+1;
-    // the last tile adds its own zero entry instead).
+    // the last tile adds its own zero entry instead).  Every contribution is
+    // also added to the slot's done count (2 T once all of its tiles are
+    // complete): each is a release pattern (fence + relaxed adds), so the
+    // packers' one acquire load of the count that reads 2 T happens-after all
+    // of them.
     int32_t* fl = ra.rdy + (int64_t)j * T;
     int32_t* arr = ra.rdy + (int64_t)pp.B * pp.n + (int64_t)j * T;  // boundary t | t+1
-    if (gt < 2) {  // both arrivals in one instruction: lane 0 left, lane 1 right boundary
-      const bool has = gt == 0 ? t > 0 : t < T - 1;
-      int32_t* a = arr + t - 1 + gt;
-      int ours = 0;
-      if (has) ours = atom_add_acq_rel(a, 1) == 1;  // second to arrive computes the pair
-      misc[2 + gt] = ours;
-      if (gt == 0) atomicAdd(&st->tr[5], 1ull);
-    }
+    int32_t* done_cnt = done_cnt0 + j;
+    // both arrivals in one instruction (lane 0 left, lane 1 right boundary)
+    int32_t arrived = 0;
+    if (gt < 2 && (gt == 0 ? t > 0 : t < T - 1)) arrived = atom_add_acq_rel(arr + t - 1 + gt, 1);
     // claim the next item now: its queue round trip overlaps the pair offsets
-    if (gt == 0) next_it = G + atomicAdd(&st->work_next, 1);
-    gsync();
-    rmark(3);
-#ifdef TABI_PHASE_TRACE
-    if (gt == 0 && t == 0 && j == 0) st->tfirst[6] = gtime();
-#endif
-    const bool needL = misc[2] != 0, needR = misc[3] != 0;
-    const int lo = needL ? s0 - 1 : s0;
-    const int hi = (t == T - 1) ? pp.n - 1 : (needR ? s0 + nt - 1 : s0 + nt - 2);
+    int nx_it = -1;
+    if (gt == gclaim) nx_it = G + atomicAdd(&st->work_next, 1);
+    if (gt == 0) atomicAdd(&st->tr[5], 1ull);  // tiles rasterized
+    if (gw == kRGW - 1) {  // work accounting: footprint entries of the tile (from smem)
+      unsigned long long pe = 0;
+      for (int ci = lane; ci < nt; ci += 32)
+        pe += (unsigned long long)(CH[ci].ws + CH[ci].hs + 4 * pp.g);
+      for (int o = 16; o > 0; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
+      if (lane == 0) atomicAdd(&st->work_prof, pe);
+    }
     // pairs with many shared rows (the tallest charts, first in the order and
     // first needed by the packers) go to the whole group, one after another;
     // the rest one warp each.  Only in tiles with fewer charts than half the
@@ -1584,12 +1610,7 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       const int32_t hb = s + 1 < s0 + nt ? CH[s + 1 - s0].hs : ra.hd[b + s + 1] - 2 * pp.g;
       return min(ha, hb) >= 512;
     };
-    // (only tiles of fewer than kRGW / 2 charts can hold a big pair: the test
-    // is skipped for the rest -- it used to cost every thread a loop over all
-    // of the tile's pairs)
-    const bool may_big = 2 * nt <= kRGW;
-    for (int s = lo + gw; s <= hi; s += kRGW) {
-      if (may_big && big_pair(s)) continue;
+    auto warp_pair = [&](int s) {
       const int a = s - s0;
       if (stashed && a >= 0 && a + 1 < nt && CH[a].small && CH[a + 1].small) {
         // both charts in this tile: their row footprints from shared memory
@@ -1599,31 +1620,90 @@ fused_kernel(PackParams pp, const int32_t* __restrict__ colofs, const int32_t* _
       } else {
         k3::pair_offset(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s, lane);
       }
+    };
+    auto leave_next = [&]() {  // (claimer) the next item for the loop top
+      if (gt == gclaim) {
+        int drop;
+        int32_t ts0, ts1;
+        probe(nx_it, drop, ts0, ts1);
+        misc[0] = nx_it;
+        misc[4] = drop;
+        misc[5] = ts0;
+        misc[6] = ts1;
+        misc[7] = 1;
+      }
+    };
+    // (only tiles of fewer than kRGW / 2 charts can hold a big pair)
+    const bool may_big = 2 * nt <= kRGW;
+    // internal pairs (s, s + 1) of the tile (the last tile: up to the zero
+    // entry of position n - 1)
+    const int hi = (t == T - 1) ? pp.n - 1 : s0 + nt - 2;
+    const int32_t vint = t == T - 1 ? 2 : 1;
+    if (!may_big) {
+      // warp 0: the boundary pairs this tile arrived second at (its lanes 0 / 1
+      // hold the arrivals), each published as soon as it is done; the other
+      // warps: the internal pairs, published together after the group barrier
+      if (gw == 0) {
+        const bool needL = t > 0 && __shfl_sync(0xffffffffu, arrived, 0) == 1;
+        const bool needR = t < T - 1 && __shfl_sync(0xffffffffu, arrived, 1) == 1;
+        __syncwarp();  // (orders the lanes' neighbour reads after lanes 0 / 1's acquires)
+        for (int q = 0; q < 2; q++) {
+          if (!(q == 0 ? needL : needR)) continue;
+          warp_pair(q == 0 ? s0 - 1 : s0 + nt - 1);
+          __syncwarp();
+          if (lane == 0) {
+            fence_acq_rel_gpu();
+            red_add_relaxed(fl + (q == 0 ? t - 1 : t), 1);
+            red_add_relaxed(done_cnt, 1);
+          }
+        }
+      } else {
+        for (int s = s0 + gw - 1; s <= hi; s += kRGW - 1) warp_pair(s);
+      }
+      leave_next();
+      gsync();
+      rmark(3);
+#ifdef TABI_PHASE_TRACE
+      if (gt == 0 && t == 0 && j == 0) st->tfirst[6] = gtime();
+#endif
+      if (gt == 0) {
+        fence_acq_rel_gpu();
+        red_add_relaxed(fl + t, vint);
+        red_add_relaxed(done_cnt, vint);
+      }
+    } else {
+      // few (tall) charts: wait for the arrivals, then every pair -- a tall
+      // one by the whole group -- and publish them together
+      if (gt < 2) misc[2 + gt] = arrived == 1 && (gt == 0 ? t > 0 : t < T - 1);
+      leave_next();
+      gsync();
+      rmark(3);
+#ifdef TABI_PHASE_TRACE
+      if (gt == 0 && t == 0 && j == 0) st->tfirst[6] = gtime();
+#endif
+      const bool needL = misc[2] != 0, needR = misc[3] != 0;
+      const int lo = needL ? s0 - 1 : s0;
+      const int hh = needR ? s0 + nt - 1 : hi;
+      for (int s = lo + gw; s <= hh; s += kRGW)
+        if (!big_pair(s)) warp_pair(s);
+      for (int s = lo; s <= hh; s++)
+        if (big_pair(s))
+          k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s,
+                                      gt, gsync, red);
+      gsync();
+      if (gt == 0) {
+        const int32_t v = vint + (needR ? 1 : 0);
+        fence_acq_rel_gpu();
+        red_add_relaxed(fl + t, v);
+        if (needL) red_add_relaxed(fl + t - 1, 1);
+        red_add_relaxed(done_cnt, v + (needL ? 1 : 0));
+      }
     }
-    for (int s = lo; s <= hi && may_big; s++)
-      if (big_pair(s))
-        k3::pair_offset_group<kRGT>(pp, rowofs, ra.drow, ra.wd, ra.hd, ra.off, ra.lock, m - 1, s, gt,
-                                    gsync, red);
-    gsync();
     rmark(4);
 #ifdef TABI_PHASE_TRACE
     if (gt == 0 && t == 0 && j == 0) st->tfirst[7] = gtime();
+    if (gt == 0 && j == 0 && t <= 1) atomicMax(&st->tfirst[1], gtime());
 #endif
-    if (gt == 0) {
-      // a tile whose flag reaches 2 here is complete: count it for its slot
-      // (the packers' all-published test)
-      int32_t* done_cnt = ra.rdy + 2 * (int64_t)pp.B * pp.n + j;
-      const int32_t v = (t == T - 1 || needR) ? 2 : 1;
-      // acq_rel: the group that completes a flag (2 increments from two raster
-      // groups) acquires the other group's writes before it releases the
-      // completed-tile count, so the packers' one-load "all published" test
-      // (an acquire of done_cnt) happens-after both contributors
-      if (atom_add_acq_rel(fl + t, v) + v == 2) red_add_release(done_cnt, 1);
-      if (needL && atom_add_acq_rel(fl + t - 1, 1) + 1 == 2) red_add_release(done_cnt, 1);
-#ifdef TABI_PHASE_TRACE
-      if (j == 0 && (t == 0 || (t == 1 && needL))) atomicMax(&st->tfirst[1], gtime());
-#endif
-    }
     rmark(5);
   }
 }

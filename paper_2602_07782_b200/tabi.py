@@ -425,7 +425,7 @@ class Context:
         d = dict(zip(keys, (int(v) for v in out[:6])))
         r16 = np.zeros(16, dtype=np.int64)
         self._chk(lib().tabi_debug_trace_raster(self.h, _ptr(r16)))
-        d["raster_phases"] = dict(zip(("fetch", "cells", "big_acct", "arrivals", "pairs",
+        d["raster_phases"] = dict(zip(("fetch", "cells", "big", "pairs_int", "pairs_bnd",
                                        "publish", "setup"), (int(v) for v in r16[:7])))
         d["alg1_passes"] = int(r16[7])  # trace build: Alg. 1 passes of wave slot 0
         d["first_row_ns"] = dict(zip(("tile0_cells", "tile0_published", "fold_unblocked",
