@@ -321,45 +321,58 @@ chunk_sort_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww
   }
 }
 
-__global__ void __launch_bounds__(256)
+// Each block holds kT consecutive pairs of one chunk; the other chunks pass
+// through shared memory one after another (the next one's loads are issued
+// before the current one is searched), and every pair adds its lower bound in
+// each of them -- an 11-step binary search in shared memory instead of global
+// loads.
+__global__ void __launch_bounds__(kT)
 chunk_rank_kernel(const uint64_t* __restrict__ ck, const int32_t* __restrict__ ci, int32_t n,
                   int32_t* perm, uint64_t* skeys, const Status* st) {
+  __shared__ uint64_t sk[kChunk];
+  __shared__ int32_t si[kChunk];
   if (st->bad_chart != INT32_MAX) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  const uint64_t k = ck[e];
-  const int32_t i = ci[e];
-  const int c = e / kChunk, nch = (n + kChunk - 1) / kChunk;
+  const int e = blockIdx.x * kT + threadIdx.x;
+  const bool valid = e < n;
+  const uint64_t k = valid ? ck[e] : 0ull;
+  const int32_t i = valid ? ci[e] : 0;
+  const int c = (int)(blockIdx.x * kT) / kChunk;  // (kChunk = 2 kT: one chunk per block)
+  const int nother = (n + kChunk - 1) / kChunk - 1;
   int rank = e - c * kChunk;
-  for (int g0 = 0; g0 < nch; g0 += 16) {
-    int lo[16], hi[16];
+  uint64_t rk[2];
+  int32_t ri[2];
+  auto fetch = [&](int q) {  // the q-th chunk other than c, padded with sentinels
+    const int b = (q < c ? q : q + 1) * kChunk, len = min(kChunk, n - b);
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-      const int c2 = g0 + q;
-      lo[q] = c2 < nch && c2 != c ? c2 * kChunk : 0;
-      hi[q] = c2 < nch && c2 != c ? min(n, c2 * kChunk + kChunk) : 0;
+    for (int u = 0; u < 2; u++) {
+      const int x = threadIdx.x + u * kT;
+      rk[u] = x < len ? ck[b + x] : ~0ull;
+      ri[u] = x < len ? ci[b + x] : INT32_MAX;
     }
-    // lower bound: first position whose pair is not below (k, i)
-    for (int step = 0; step < 12; step++) {
+  };
+  if (nother > 0) fetch(0);
+  for (int q = 0; q < nother; q++) {
+    __syncthreads();  // (the previous chunk's searches are done)
 #pragma unroll
-      for (int q = 0; q < 16; q++) {
-        if (lo[q] < hi[q]) {
-          const int mid = (lo[q] + hi[q]) >> 1;
-          if (pair_lt(ck[mid], ci[mid], k, i)) lo[q] = mid + 1;
-          else hi[q] = mid;
-        }
-      }
+    for (int u = 0; u < 2; u++) {
+      sk[threadIdx.x + u * kT] = rk[u];
+      si[threadIdx.x + u * kT] = ri[u];
     }
+    __syncthreads();
+    if (q + 1 < nother) fetch(q + 1);
+    // number of pairs below (k, i): binary lifting over the 2,048 sorted slots
+    int pos = 0;
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-      const int c2 = g0 + q;
-      if (c2 < nch && c2 != c) rank += lo[q] - c2 * kChunk;
-    }
+    for (int stp = kChunk / 2; stp >= 1; stp >>= 1)
+      if (pair_lt(sk[pos + stp - 1], si[pos + stp - 1], k, i)) pos += stp;
+    if (pair_lt(sk[pos], si[pos], k, i)) pos++;  // (pos <= kChunk - 1 here)
+    rank += pos;
   }
-  perm[rank] = i;
-  skeys[rank] = k;  // the keys in sorted order: the slot layout reads (h, w) from them
+  if (valid) {
+    perm[rank] = i;
+    skeys[rank] = k;  // the keys in sorted order: the slot layout reads (h, w) from them
+  }
 }
-
 
 // N <= 2^17: rank of key i = #{j : (key_j, j) < (key_i, i)}, counted over a 2-D
 // grid of (i block, j tile) with one atomicAdd per thread and tile, then a
@@ -400,7 +413,6 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
                                           int32_t* tix, Status* st, int32_t* rdy,
                                           const uint64_t* skey = nullptr, int skey_shift = 12) {
   __shared__ int32_t sh[2][kW + 1];
-  __shared__ int32_t idl[kT];
   __shared__ unsigned long long asum[2][kW];
   __shared__ int32_t ext_max[2][kW];
   // Area bound on the candidate scales: the packed charts are disjoint and
@@ -466,61 +478,105 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
       st->atot_hi = (unsigned long long)(uint64_t)(tot >> 64);
     }
   }
-  int32_t carry_c = 0, carry_r = 0, carry_t = 0, prev_id = -1;
-  for (int t0 = 0; t0 < pp.n; t0 += kT) {
-    const int s = t0 + threadIdx.x;
-    int32_t cw = 0, rh = 0;
-    if (s < pp.n) {
-      int32_t w, h;
-      if (skey) {  // the sorted key holds (h, w): no dependent global loads
-        const uint64_t k = skey[s] >> skey_shift;  // order_key(h, w) [<< 12 | index]
-        h = (int32_t)(0x3ffffffu - (uint32_t)((k >> 26) & 0x3ffffffu));
-        w = (int32_t)(0x3ffffffu - (uint32_t)(k & 0x3ffffffu));
-      } else {
-        const int c = perm[s];
-        w = ww[c];
-        h = hh[c];
-      }
-      const int64_t wd = ceildiv(w, TABI_UNITS) + 2 * pp.g;
-      const int64_t hd = ceildiv(h, TABI_UNITS) + 2 * pp.g;
-      cw = (int32_t)(wd < pp.Wp ? wd : pp.Wp);
-      rh = (int32_t)(hd < pp.Hp ? hd : pp.Hp);
-      hsorted[s] = h;
+  // Chunks of kE * kT sorted positions: the slot sizes are loaded coalesced
+  // into shared memory, then thread t runs over its kE consecutive positions
+  // with running sums -- two block-wide scans per chunk (slot prefixes, then
+  // tile starts) instead of two per kT positions.
+  constexpr int kE = 4;
+  constexpr int kCh = kE * kT;
+  __shared__ uint16_t scw[kCh], srh[kCh];  // slot sizes <= W', H'
+  static_assert(TABI_MAX_ATLAS_SIDE + 2 * 64 <= 65535, "slot sizes fit 16 bits (gutter <= 64)");
+  __shared__ int32_t last_id;
+  auto hw_at = [&](int s, int32_t& h, int32_t& w) {
+    if (skey) {  // the sorted key holds (h, w): no dependent global loads
+      const uint64_t k = skey[s] >> skey_shift;  // order_key(h, w) [<< 12 | index]
+      h = (int32_t)(0x3ffffffu - (uint32_t)((k >> 26) & 0x3ffffffu));
+      w = (int32_t)(0x3ffffffu - (uint32_t)(k & 0x3ffffffu));
+    } else {
+      const int c = perm[s];
+      w = ww[c];
+      h = hh[c];
     }
-    int32_t ec, er, tc, tr;
-    block_scan2(cw, rh, ec, er, tc, tr, sh);
-    // Fused-kernel raster tiles: consecutive sorted charts with tile key
-    // floor(slot prefix / kFusedTileCells) + floor(s / kFusedTileCharts) --
-    // non-decreasing in s, so equal keys are runs of <= kFusedTileCharts
-    // charts holding about kFusedTileCells footprint cells (the tallest
-    // charts come first and get small tiles, so their tiles are not the long
-    // pole every packer waits on).
-    // the first kFusedHeadCells cells (the tallest charts, which every packer
-    // needs first) are cut into quarter-size tiles so the first rows start early
-    const int64_t cum = (int64_t)carry_c + ec + carry_r + er;
+  };
+  // Fused-kernel raster tiles: consecutive sorted charts with tile key
+  // floor(slot prefix / kFusedTileCells) + floor(s / kFusedTileCharts) --
+  // non-decreasing in s, so equal keys are runs of <= kFusedTileCharts
+  // charts holding about kFusedTileCells footprint cells (the tallest
+  // charts come first and get small tiles, so their tiles are not the long
+  // pole every packer waits on).
+  // the first kFusedHeadCells cells (the tallest charts, which every packer
+  // needs first) are cut into quarter-size tiles so the first rows start early
+  auto tile_id = [&](int64_t cum, int s) -> int32_t {
     const int64_t q4 = kFusedTileCells / 4;
     const int64_t cell_key = cum < kFusedHeadCells
                                  ? cum / q4
                                  : kFusedHeadCells / q4 + (cum - kFusedHeadCells) / kFusedTileCells;
-    const int32_t id = s < pp.n ? (int32_t)(cell_key + s / kFusedTileCharts) : INT32_MAX;
-    idl[threadIdx.x] = id;
-    __syncthreads();
-    const int32_t idp = threadIdx.x == 0 ? prev_id : idl[threadIdx.x - 1];
-    const int32_t first = (s < pp.n && id != idp) ? 1 : 0;
-    int32_t ef, e2, tf, t2;
-    block_scan2(first, 0, ef, e2, tf, t2, sh);
-    if (s < pp.n) {
-      colofs[s] = carry_c + ec;
-      rowofs[s] = carry_r + er;
-      const int32_t t = carry_t + ef + first - 1;
-      tix[s] = t;
-      if (first) tstart[t] = s;
+    return (int32_t)(cell_key + s / kFusedTileCharts);
+  };
+  int32_t carry_c = 0, carry_r = 0, carry_t = 0, prev_id = -1;  // prev_id: the tile of the
+                                                                 // previous chunk's last position
+  for (int base = 0; base < pp.n; base += kCh) {
+    const int cn = min(kCh, pp.n - base);
+#pragma unroll
+    for (int u = 0; u < kE; u++) {
+      const int x = u * kT + threadIdx.x;
+      if (x < cn) {
+        int32_t h, w;
+        hw_at(base + x, h, w);
+        const int64_t wd = ceildiv(w, TABI_UNITS) + 2 * pp.g;
+        const int64_t hd = ceildiv(h, TABI_UNITS) + 2 * pp.g;
+        scw[x] = (uint16_t)(wd < pp.Wp ? wd : pp.Wp);
+        srh[x] = (uint16_t)(hd < pp.Hp ? hd : pp.Hp);
+        hsorted[base + x] = h;
+      }
     }
-    prev_id = idl[kT - 1];
+    __syncthreads();
+    const int q0 = min(cn, (int)threadIdx.x * kE), q1 = min(cn, q0 + kE);
+    int32_t sc = 0, sr = 0;
+    for (int q = q0; q < q1; q++) {
+      sc += scw[q];
+      sr += srh[q];
+    }
+    int32_t ec, er, tc, tr;
+    block_scan2(sc, sr, ec, er, tc, tr, sh);
+    ec += carry_c;
+    er += carry_r;
+    int32_t pid = q0 == 0 ? prev_id
+                  : q0 < q1 ? tile_id((int64_t)ec + er - scw[q0 - 1] - srh[q0 - 1], base + q0 - 1)
+                            : 0;
+    int32_t nf = 0;
+    {
+      int64_t cum = (int64_t)ec + er;
+      int32_t p = pid;
+      for (int q = q0; q < q1; q++) {
+        const int32_t id = tile_id(cum, base + q);
+        nf += id != p;
+        p = id;
+        cum += scw[q] + srh[q];
+      }
+    }
+    int32_t ef, e2, tf, t2;
+    block_scan2(nf, 0, ef, e2, tf, t2, sh);
+    {
+      int32_t c = ec, r = er, tt = carry_t + ef - 1;
+      for (int q = q0; q < q1; q++) {
+        const int s = base + q;
+        const int32_t id = tile_id((int64_t)c + r, s);
+        if (id != pid) tstart[++tt] = s;
+        colofs[s] = c;
+        rowofs[s] = r;
+        tix[s] = tt;
+        c += scw[q];
+        r += srh[q];
+        pid = id;
+      }
+      if (q0 < q1 && q1 == cn) last_id = pid;
+    }
     carry_c += tc;
     carry_r += tr;
     carry_t += tf;
     __syncthreads();
+    prev_id = last_id;
   }
   if (threadIdx.x == 0) {
     st->cols_total = carry_c;
@@ -673,7 +729,7 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
     // chunked bitonic + merge ranks (ck in keys, ci in perm2)
     const int nch = (n + kChunk - 1) / kChunk;
     chunk_sort_kernel<<<nch, kT, 0, s>>>(P.h, P.w, n, keys, perm2, st);
-    chunk_rank_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, perm2, n, perm, keys2, st);
+    chunk_rank_kernel<<<(n + kT - 1) / kT, kT, 0, s>>>(keys, perm2, n, perm, keys2, st);
     if (sorted_keys) *sorted_keys = keys2;
     return 2;
   }
