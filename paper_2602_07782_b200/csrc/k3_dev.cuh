@@ -228,42 +228,58 @@ __device__ __forceinline__ void raw_run(const ChartK3& H, const int32_t* tab, in
 }
 
 // raw_cell as an iterator over consecutive cells i0, i0 + 1, ... of one axis
-// (same values as raw_run).  Of the four OBB line progressions only the two
-// that can decide a cell are advanced: the low (high) bound uses line 1 (3)
-// up to its crossing index iA and line 0 (2) past it, so each bound carries
-// one progression and restarts it once where the run passes its crossing.
+// (same values as raw_run).  Each OBB bound is piecewise over the cells: the
+// low (high) bound follows line 1 (3) below its crossing band, the crossing
+// value star in the band [iB, iA], line 0 (2) past iA, and the last cell's
+// own value if the last cell is not past iA.  The iterator keeps only the
+// current piece of each bound -- a progression (a constant piece is one with
+// zero step) and the cell index where the next piece starts -- and reads the
+// next piece's constants from the chart's ObbC in shared memory there, so the
+// per-cell loop carries few registers.
 struct RawIter {
   const int32_t* t;
-  const LinDiv* lin;
+  const ObbC* O;
   int64_t nx, rl, rh;                // slice-index progressions: remainders mod nx
   int64_t dr;                        // SCk - dq * nx (SCk = SC k: 2^28 k in tail mode)
-  int32_t dq, ql, qh, k, cnt, ext, i;
-  bool obb, pL, pH;                  // past the low / high crossing
-  // OBB bound state, clamped to +-2^30 where only compared with cell indices /
-  // texel values (both far smaller)
-  int32_t iA0, iA1, iB0, iB1, st0, st1, la0, la1, lb0, lb1;
-  int32_t vL, vH, sqL, sqH;          // the active line progressions (values in texels)
-  int64_t rL, rH, srL, srH, DL, DH;
+  int32_t dq, ql, qh, k, cnt, ext, i, ax;
+  bool obb;
+  // bound b (0 low, 1 high): value (the high bound's negated), clamped to
+  // +-2^30 where only compared with cell indices / texel values (both far
+  // smaller); its step, remainder, divisor; the cell where its piece ends
+  int32_t v[2], sq[2], sw[2];
+  int64_t r[2], sr[2], D[2];
   __device__ __forceinline__ static int32_t clamp30(int64_t v) {
     return (int32_t)(v < -(1ll << 30) ? -(1ll << 30) : v > (1ll << 30) ? (1ll << 30) : v);
   }
-  __device__ __forceinline__ void load_low(int32_t at) {
-    const LinDiv& L = lin[pL ? 0 : 1];
-    int64_t v;
-    lindiv_start(L, at, v, rL);
-    vL = clamp30(v);
-    sqL = (int32_t)L.qB; srL = L.rB; DL = L.D;
+  // bound b's piece containing cell `at`
+  __device__ __forceinline__ void seg(int b, int32_t at) {
+    const int q = 2 * ax + b;
+    const int32_t iA = clamp30(O->iA[q]), iB = clamp30(O->iB[q]), last = cnt - 1;
+    const bool line = at > iA || (at != last && at < iB);
+    if (line) {  // floor((A + i B) / D) from cell `at` on
+      const LinDiv& L = O->lin[4 * ax + 2 * b + (at > iA ? 0 : 1)];
+      int64_t vv;
+      lindiv_start(L, at, vv, r[b]);
+      v[b] = clamp30(vv);
+      sq[b] = (int32_t)L.qB;
+      sr[b] = L.rB;
+      D[b] = L.D;
+      sw[b] = at > iA ? INT32_MAX : min(min(iB, iA + 1), last);
+    } else {  // the crossing value, or the last cell's
+      const int32_t c = at == last ? clamp30(O->lastB[q] != 0 ? O->star[q] : O->last[q])
+                                   : clamp30(O->star[q]);
+      v[b] = b ? -c : c;
+      sq[b] = 0;
+      r[b] = 0;
+      sr[b] = 0;
+      D[b] = 1;
+      sw[b] = at == last ? INT32_MAX : min(iA + 1, last);
+    }
   }
-  __device__ __forceinline__ void load_high(int32_t at) {
-    const LinDiv& L = lin[pH ? 2 : 3];
-    int64_t v;
-    lindiv_start(L, at, v, rH);
-    vH = clamp30(v);
-    sqH = (int32_t)L.qB; srH = L.rB; DH = L.D;
-  }
-  __device__ __forceinline__ void init(const ChartK3& H, const int32_t* tab, int k_, int ax,
+  __device__ __forceinline__ void init(const ChartK3& H, const int32_t* tab, int k_, int ax_,
                                        int32_t i0, int64_t SC) {
     k = k_;
+    ax = ax_;
     nx = ax ? H.nh : H.nw;
     const double rnx = ax ? H.rnh : H.rnw;
     const int64_t SCk = SC * k;
@@ -284,18 +300,9 @@ struct RawIter {
     i = i0;
     obb = H.j8 != 0;
     if (obb) {
-      const ObbC& O = H.O;
-      const int q0 = 2 * ax, q1 = 2 * ax + 1;
-      lin = O.lin + 4 * ax;
-      iA0 = clamp30(O.iA[q0]); iA1 = clamp30(O.iA[q1]);
-      iB0 = clamp30(O.iB[q0]); iB1 = clamp30(O.iB[q1]);
-      st0 = clamp30(O.star[q0]); st1 = clamp30(O.star[q1]);
-      la0 = clamp30(O.last[q0]); la1 = clamp30(O.last[q1]);
-      lb0 = O.lastB[q0]; lb1 = O.lastB[q1];
-      pL = i0 > iA0;
-      pH = i0 > iA1;
-      load_low(i0);
-      load_high(i0);
+      O = &H.O;
+      seg(0, i0);
+      seg(1, i0);
     }
   }
   // value of cell i (packed lo | hi << 16), then move to i + 1
@@ -308,23 +315,15 @@ struct RawIter {
     }
     int32_t L = max(0, lo), Hh = min(hi, ext);
     if (obb) {
-      const bool last = i == cnt - 1;
-      int32_t w;
-      if (pL) w = vL;
-      else if (last ? lb0 != 0 : i >= iB0) w = st0;
-      else w = last ? la0 : vL;
-      L = max(L, w);
-      if (pH) w = -vH;
-      else if (last ? lb1 != 0 : i >= iB1) w = st1;
-      else w = last ? la1 : -vH;
-      Hh = min(Hh, w);
-      // advance to i + 1 (restart a bound's progression where i + 1 passes its crossing)
-      vL += sqL; rL += srL;
-      if (rL >= DL) { rL -= DL; vL++; }
-      vH += sqH; rH += srH;
-      if (rH >= DH) { rH -= DH; vH++; }
-      if (!pL && i + 1 > iA0) { pL = true; load_low(i + 1); }
-      if (!pH && i + 1 > iA1) { pH = true; load_high(i + 1); }
+      L = max(L, v[0]);
+      Hh = min(Hh, -v[1]);
+#pragma unroll
+      for (int b = 0; b < 2; b++) {
+        v[b] += sq[b];
+        r[b] += sr[b];
+        if (r[b] >= D[b]) { r[b] -= D[b]; v[b]++; }
+        if (i + 1 == sw[b]) seg(b, i + 1);
+      }
     }
     ql += dq; rl += dr;
     if (rl >= nx) { rl -= nx; ql++; }
