@@ -286,14 +286,15 @@ struct RawIter {
     const int64_t q = fdiv_r64(SCk, nx, rnx);
     dq = (int32_t)q;
     dr = SCk - q * nx;
-    int64_t a = (int64_t)i0 * SCk;
-    int64_t f = fdiv_r64(a, nx, rnx);
+    const int64_t a = (int64_t)i0 * SCk;
+    const int64_t f = fdiv_r64(a, nx, rnx);
     ql = (int32_t)f;
     rl = a - f * nx;
-    a += SCk - 1;
-    f = fdiv_r64(a, nx, rnx);
-    qh = (int32_t)f;
-    rh = a - f * nx;
+    // a + SCk - 1 = (ql + dq) nx + (rl + dr - 1), with rl + dr - 1 in [-1, 2 nx - 2]
+    rh = rl + dr - 1;
+    qh = ql + dq;
+    if (rh < 0) { rh += nx; qh--; }
+    else if (rh >= nx) { rh -= nx; qh++; }
     t = tab + ax * 2 * k;
     cnt = ax ? H.hs : H.ws;
     ext = ax ? H.ws : H.hs;
@@ -309,9 +310,11 @@ struct RawIter {
   __device__ __forceinline__ uint32_t next() {
     const int32_t jl = ql < 0 ? 0 : ql, jh = qh > k - 1 ? k - 1 : qh;
     int32_t lo = INT32_MAX, hi = INT32_MIN;
+    const int2* t2 = reinterpret_cast<const int2*>(t);  // (lo, hi) of slice j: one 8-byte load
     for (int32_t j = jl; j <= jh; j++) {
-      lo = min(lo, t[2 * j]);
-      hi = max(hi, t[2 * j + 1]);
+      const int2 e = t2[j];
+      lo = min(lo, e.x);
+      hi = max(hi, e.y);
     }
     int32_t L = max(0, lo), Hh = min(hi, ext);
     if (obb) {
