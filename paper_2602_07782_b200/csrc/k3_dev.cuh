@@ -486,14 +486,34 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
     // (with rstash: cpre = the prefix of the dilated row counts, and each
     // chart's row outputs also go to rstash + cpre[ci] -- the caller's pair
     // offsets then read shared memory; only if they all fit rstash_cap)
+    // Runs: each chart axis (Wd column outputs, then Hd row outputs) is cut
+    // into runs of at most R outputs and every thread takes one run, so a
+    // run never crosses into another chart: each thread starts one iterator
+    // and the warps' loops have (nearly) equal lengths.  R is the smallest
+    // length (from ceil(outputs / TT) up) whose runs fit the TT threads --
+    // some R <= max(Wd, Hd) does (2 runs per chart, 2 TC <= TT).
+    // opre = the prefix of the charts' run counts.
     if (tid < 32) {
       const int lane = tid;
-      int e = 0, otot = 0, rtot = 0;
-      if (lane == 0) { opre[0] = 0; cpre[0] = 0; }
-      for (; e < nt; e += 32) {
+      int32_t nout = 0;
+      for (int idx = lane; idx < nt; idx += 32)
+        if (CH[idx].small) nout += CH[idx].ws + CH[idx].hs + 4 * g;
+      nout = warp_sum(nout);
+      int32_t R = max(kRunMin, (nout + TT - 1) / TT);
+      while (true) {
+        int32_t runs = 0;
+        for (int idx = lane; idx < nt; idx += 32)
+          if (CH[idx].small)
+            runs += (CH[idx].ws + 2 * g + R - 1) / R + (CH[idx].hs + 2 * g + R - 1) / R;
+        if (warp_sum(runs) <= TT) break;
+        R += max(1, R >> 3);
+      }
+      int otot = 0, rtot = 0;
+      if (lane == 0) { opre[0] = 0; cpre[0] = 0; *chunk_end = R; }
+      for (int e = 0; e < nt; e += 32) {
         const int idx = e + lane;
         const bool sm = idx < nt && CH[idx].small;
-        int io = sm ? CH[idx].ws + CH[idx].hs + 4 * g : 0;
+        int io = sm ? (CH[idx].ws + 2 * g + R - 1) / R + (CH[idx].hs + 2 * g + R - 1) / R : 0;
         int ir = sm ? CH[idx].hs + 2 * g : 0;
         // (the pass covers fitting charts only; big[] stays 0 on this path)
 #pragma unroll
@@ -510,33 +530,23 @@ __device__ void tile_raster(const Proxies& P, const int32_t* __restrict__ perm, 
     sync();
     setup_done(1);
     if (rstash && cpre[nt] > rstash_cap) rstash = nullptr;  // (uniform)
-    const int32_t nout = opre[nt];
-    // run length per thread (odd: the runs' stores hit distinct banks); each
-    // run pays one iterator start, so short runs spend most of their
-    // instructions there
-    const int32_t R = max(((nout + TT - 1) / TT) | 1, kRunMin);
-    int32_t e = tid * R;
-    const int32_t e1 = min(nout, e + R);
-    if (e < e1) {
+    const int32_t R = *chunk_end;
+    if (tid < opre[nt]) {
       int lo = 0, hi = nt - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (opre[mid] <= e) lo = mid;
+        if (opre[mid] <= tid) lo = mid;
         else hi = mid - 1;
       }
-      while (e < e1) {
-        const ChartK3& H = CH[lo];
-        const int32_t y = e - opre[lo];
-        const int32_t Wd = H.ws + 2 * g;
-        const int ax = y >= Wd;
-        const int32_t o = ax ? y - Wd : y;
-        const int32_t len = min(e1 - e, (ax ? H.hs + 2 * g : Wd) - o);
-        dil_run<kDilMax>(H, tabs + lo * 4 * k, k, ax, o, len, SC, g,
-                         (ax ? rowb + H.row_o : colb + H.col_o) + o,
-                         ax && rstash ? rstash + cpre[lo] + o : nullptr);
-        e += len;
-        while (lo < nt - 1 && opre[lo + 1] <= e) lo++;
-      }
+      const ChartK3& H = CH[lo];
+      const int32_t Wd = H.ws + 2 * g, Hd = H.hs + 2 * g;
+      const int32_t u = tid - opre[lo], ncol = (Wd + R - 1) / R;
+      const int ax = u >= ncol;
+      const int32_t o = (ax ? u - ncol : u) * R;
+      const int32_t len = min(R, (ax ? Hd : Wd) - o);
+      dil_run<kDilMax>(H, tabs + lo * 4 * k, k, ax, o, len, SC, g,
+                       (ax ? rowb + H.row_o : colb + H.col_o) + o,
+                       ax && rstash ? rstash + cpre[lo] + o : nullptr);
     }
     sync();
     return;
