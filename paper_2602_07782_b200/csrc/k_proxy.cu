@@ -83,7 +83,30 @@ __device__ void accumulate_slices(const Group<G>& g, const int32_t* A, const int
                                   int64_t ext, int k, int32_t* lo, int32_t* hi) {
   const uint32_t e = (uint32_t)ext;
   const double re = rcp_approx((double)ext);
-  for (int v = g.gl; v < nv; v += G) {
+  // one crossing y = ya + (L*ext - k*xa) * dy / den of line L with an edge
+  // (xa, ya) -> (xa + dx, ya + dy), dx > 0: floored into the top bound and
+  // ceiled into the bottom bound of strips L - 1 and L
+  auto crossing = [&](int32_t L, int64_t xa, int64_t ya, int64_t dx, int64_t dy) {
+    const int64_t den = (int64_t)k * dx;
+    const double rd = rcp_approx((double)den);
+    // |num| <= den * 2^25 < 2^57
+    const int64_t num = ((int64_t)L * e - (int64_t)k * xa) * dy;
+    int64_t q = (int64_t)floor((double)num * rd);
+    int64_t r = num - q * den;
+    while (r < 0) { q--; r += den; }
+    while (r >= den) { q++; r -= den; }
+    const int32_t yf = (int32_t)(ya + q), yc = yf + (r != 0 ? 1 : 0);
+    atomicMin(&lo[L - 1], yf);
+    atomicMax(&hi[L - 1], yc);
+    atomicMin(&lo[L], yf);
+    atomicMax(&hi[L], yc);
+  };
+  // vertex v: the closed strips holding it; edge (v, v+1): the range [L0, L0 +
+  // cnt) of strip boundary lines L*ext strictly inside it (k*xa < L*ext <
+  // k*xb, L in [1, k-1]) and its endpoints ordered by the sliced coordinate
+  auto vertex_edge = [&](int v, int32_t& xa, int32_t& ya, int32_t& dx, int32_t& dy, int32_t& L0,
+                         int32_t& cnt) {
+    cnt = 0;
     const int u = v + 1 == nv ? 0 : v + 1;
     const int32_t av = A[v], bv = B[v], au = A[u], bu = B[u];
     uint32_t rv, ru;
@@ -92,31 +115,55 @@ __device__ void accumulate_slices(const Group<G>& g, const int32_t* A, const int
     // closed strips holding vertex v: q (unless q = k) and q - 1 when on a line
     if (qv <= k - 1) { atomicMin(&lo[qv], bv); atomicMax(&hi[qv], bv); }
     if (rv == 0 && qv >= 1) { atomicMin(&lo[qv - 1], bv); atomicMax(&hi[qv - 1], bv); }
-    if (av == au) continue;
+    if (av == au) return;
     const bool fw = av < au;
-    const int64_t xa = fw ? av : au, xb = fw ? au : av, ya = fw ? bv : bu, yb = fw ? bu : bv;
     const int32_t qa = fw ? qv : qu, qb = fw ? qu : qv;
     const uint32_t rb = fw ? ru : rv;
-    // lines L*ext with k*xa < L*ext < k*xb, L in [1, k-1]
-    const int32_t L0 = max(qa + 1, 1);
+    L0 = max(qa + 1, 1);
     const int32_t L1 = min(rb == 0 ? qb - 1 : qb, k - 1);
-    if (L0 > L1) continue;
-    const int64_t dy = yb - ya, den = (int64_t)k * (xb - xa);
-    const double rd = rcp_approx((double)den);
-    const int64_t kxa = (int64_t)k * xa;
-    for (int32_t L = L0; L <= L1; L++) {
-      // crossing y = ya + (L*ext - k*xa) * dy / den, |num| <= den * 2^25 < 2^57
-      const int64_t num = ((int64_t)L * e - kxa) * dy;
-      int64_t q = (int64_t)floor((double)num * rd);
-      int64_t r = num - q * den;
-      while (r < 0) { q--; r += den; }
-      while (r >= den) { q++; r -= den; }
-      const int32_t yf = (int32_t)(ya + q), yc = yf + (r != 0 ? 1 : 0);
-      atomicMin(&lo[L - 1], yf);
-      atomicMax(&hi[L - 1], yc);
-      atomicMin(&lo[L], yf);
-      atomicMax(&hi[L], yc);
+    if (L0 > L1) return;
+    cnt = L1 - L0 + 1;
+    xa = fw ? av : au;
+    ya = fw ? bv : bu;
+    dx = (fw ? au : av) - xa;
+    dy = (fw ? bu : bv) - ya;
+  };
+  if (nv <= G) {
+    // one vertex / edge per lane, then the crossings of all edges spread over
+    // the lanes (an edge may cross up to k - 1 lines while its neighbours
+    // cross none): lane x takes flattened crossings x, x + G, ..., its edge
+    // found by a binary search over the lanes' inclusive crossing counts and
+    // the edge's values read from the owning lane by shuffles.  The bounds are
+    // min / max atomics, so the assignment does not change the result.
+    int32_t xa = 0, ya = 0, dx = 0, dy = 0, L0 = 0, cnt = 0;
+    if (g.gl < nv) vertex_edge(g.gl, xa, ya, dx, dy, L0, cnt);
+    int32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int32_t t = __shfl_up_sync(g.mask, inc, o, G);
+      if (g.gl >= o) inc += t;
     }
+    const int32_t total = __shfl_sync(g.mask, inc, G - 1, G);
+    for (int32_t x0 = 0; x0 < total; x0 += G) {  // (uniform over the group)
+      const int32_t x = x0 + g.gl;
+      int pos = 0;  // lanes whose inclusive count is <= x = the owning edge
+#pragma unroll
+      for (int s = G / 2; s >= 1; s >>= 1) {
+        const int32_t iv = __shfl_sync(g.mask, inc, pos + s - 1, G);
+        if (iv <= x) pos += s;
+      }
+      const int32_t ex = __shfl_sync(g.mask, inc - cnt, pos, G);
+      const int32_t oL0 = __shfl_sync(g.mask, L0, pos, G);
+      const int32_t oxa = __shfl_sync(g.mask, xa, pos, G), oya = __shfl_sync(g.mask, ya, pos, G);
+      const int32_t odx = __shfl_sync(g.mask, dx, pos, G), ody = __shfl_sync(g.mask, dy, pos, G);
+      if (x < total) crossing(oL0 + (x - ex), oxa, oya, odx, ody);
+    }
+    return;
+  }
+  for (int v = g.gl; v < nv; v += G) {
+    int32_t xa, ya, dx, dy, L0, cnt;
+    vertex_edge(v, xa, ya, dx, dy, L0, cnt);
+    for (int32_t L = L0; L < L0 + cnt; L++) crossing(L, xa, ya, dx, dy);
   }
 }
 
@@ -207,12 +254,20 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   // with abase[a] <= c (uniform per group), which owns the status block, the
   // resolution and the chart index reported on EINVAL
   int32_t cl = c;
+  const int gl0 = g.gl;
   if (am.abase) {
+    // G-ary search by the group (one probe per lane, a ballot per round: 2-3
+    // dependent loads instead of log2(na)); invariant abase[lo] <= c, the
+    // answer in [lo, hi]; the probes are monotone, so the ballot's popcount
+    // locates the last true one
     int lo = 0, hi = am.na - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (am.abase[mid] <= c) lo = mid;
-      else hi = mid - 1;
+    while (lo < hi) {  // (uniform over the group)
+      const int step = (hi - lo + G) / G;
+      const int idx = lo + gl0 * step;
+      const bool p = idx <= hi && am.abase[idx] <= c;
+      const int j = __popc(__ballot_sync(g.mask, p)) - 1;
+      lo += j * step;
+      hi = min(hi, lo + step - 1);
     }
     st += lo;
     cl = c - am.abase[lo];

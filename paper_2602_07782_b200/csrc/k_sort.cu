@@ -437,35 +437,41 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
       ext_max[1][wid] = hm;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      i128 tot = 0;
-      int32_t wmx = 0, hmx = 0;
-      for (int w = 0; w < kW; w++) {
-        tot += (i128)(((unsigned __int128)asum[1][w] << 64) | asum[0][w]);
-        wmx = max(wmx, ext_max[0][w]);
-        hmx = max(hmx, ext_max[1][w]);
-      }
-      st->wmax = wmx;
-      st->hmax = hmx;
+    if (wid == 0) {  // warp 0: the totals, then the scale bounds by ballots
+      i128 tot = (i128)(((unsigned __int128)asum[1][lane] << 64) | asum[0][lane]);
+      tot = warp_sum128(tot);
+      const int32_t wmx = warp_max(ext_max[0][lane]), hmx = warp_max(ext_max[1][lane]);
       const i128 rhs = (i128)2 * 65536 * pp.W * pp.H * (i128)pp.M * pp.M;
       // R2: sequential mode only -- every chart keeps m/M, so a successful
       // (overlap-free, in-bounds) packing needs (m/M)^2 A <= W H.  In hybrid
       // mode the prefix tail's intermediate downscale (D24) can make a
       // candidate above that bound succeed, so the search starts at M.
+      // m_hi = the largest m <= M passing it (the test is monotone in m: lane
+      // l of round r tests m = M - 32 r - l; the lowest passing lane wins)
       int m_hi = 0;
-      for (int m = pp.M; m >= 1; m--)
-        if (pp.t_opt > 0 || (i128)m * m * tot <= rhs) { m_hi = m; break; }
-      st->pad[2] = m_hi;
+      for (int base = 0; base < pp.M && m_hi == 0; base += 32) {  // (uniform)
+        const int m = pp.M - base - lane;
+        const unsigned ok = __ballot_sync(0xffffffffu, m >= 1 && (pp.t_opt > 0 || (i128)m * m * tot <= rhs));
+        if (ok) m_hi = pp.M - base - (__ffs(ok) - 1);
+      }
       // Wave 0's width: the candidates from m_hi down to the scale at which
       // the charts would fill 55 % of the atlas (TSS sets pack at ~60 %) -- below that a success is
       // unlikely, and a narrower first wave leaves the top candidate's chain
       // with less contention.  Later waves take B each and the wave loop's
       // stopping rule (select_kernel; hybrid mode: the V bound of D25) is
       // unchanged, so the result is the exhaustive search's either way.
+      // m_lo = 1 + the largest m' < m_hi below the fill level (monotone in
+      // m'), else 1
       int b0 = pp.B;
       if (pp.B > 2 && m_hi >= 1) {
-        int m_lo = m_hi;
-        while (m_lo > 1 && (i128)100 * (m_lo - 1) * (m_lo - 1) * tot >= (i128)TABI_B0_FILL * rhs) m_lo--;
+        int m_lo = 0;
+        for (int base = 1; base < m_hi && m_lo == 0; base += 32) {  // (uniform)
+          const int mp = m_hi - base - lane;
+          const unsigned lowr = __ballot_sync(
+              0xffffffffu, mp >= 1 && (i128)100 * mp * mp * tot < (i128)TABI_B0_FILL * rhs);
+          if (lowr) m_lo = m_hi - base - (__ffs(lowr) - 1) + 1;
+        }
+        if (m_lo == 0) m_lo = 1;
         b0 = min(pp.B, max(2, m_hi - m_lo + 1));
         // hybrid mode: the prefix tail's downscale absorbs the overflow that
         // fails a sequential candidate, so the top candidates usually succeed
@@ -473,9 +479,14 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
         // loop's V bound decides whether lower ones still need a wave
         if (pp.t_opt > 0) b0 = min(b0, TABI_B0_HYBRID);
       }
+      if (lane == 0) {
+      st->wmax = wmx;
+      st->hmax = hmx;
+      st->pad[2] = m_hi;
       st->b0 = b0;
       st->atot_lo = (unsigned long long)(uint64_t)tot;
       st->atot_hi = (unsigned long long)(uint64_t)(tot >> 64);
+      }
     }
   }
   // Chunks of kE * kT sorted positions: the slot sizes are loaded coalesced
