@@ -222,7 +222,10 @@ struct LazyRaster {
   int64_t atot;          // 2 x the atlas's total polygon area (fits int64 for n <= 2048)
   unsigned long long* cycles;  // [2]: SM cycles in the lazy raster, in its pair offsets
 };
-constexpr int kLzTC = 64;  // charts per lazy raster tile (the whole CTA, 8 threads per chart)
+#ifndef TABI_LZ_TC
+#define TABI_LZ_TC 64
+#endif
+constexpr int kLzTC = TABI_LZ_TC;  // charts per lazy raster tile (the whole CTA, 8 threads per chart)
 
 __device__ __forceinline__ int32_t atom_add_acq_rel(int32_t* p, int32_t v) {
   int32_t old;
@@ -1838,7 +1841,7 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
       lzr.cbad = cbad;
       lzr.area = A.area + gcta * nm;
       lzr.sc = k3::Scale{m, SCm, 0};
-      lzr.ahead = 96;
+      lzr.ahead = A.ahead;
       lzr.early_fail = A.early_fail;
       lzr.atot = (int64_t)st->atot_lo;
       lzr.cycles = A.cycles;

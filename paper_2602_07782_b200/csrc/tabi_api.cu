@@ -1385,6 +1385,13 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
       ma.lazy = !(le && le[0] == '0') && many_lazy_ok(pp.k, pp.g, pp.Wp);
       ma.early_fail = ma.lazy && !(fe && fe[0] == '0') && !(pp.flags & TABI_F_ADJACENT_LOCKS_ONLY);
       lazy_used = ma.lazy != 0;
+      // positions rasterized beyond the fold's need: 0 (the lazy raster
+      // still takes whole 64-chart tiles); measured on C5: 0 / 32 / 64 / 96 /
+      // 160 -> 9.35 / 9.42 / 9.74 / 9.75 / 10.42 ms (a failing candidate
+      // rasterizes fewer charts it never reaches).  TABI_LZ_AHEAD: test knob
+      const char* ae = getenv("TABI_LZ_AHEAD");
+      ma.ahead = ae ? atoi(ae) : 0;
+      if (ma.ahead < 0) ma.ahead = 0;
     }
     ma.nmax = w.nmax;
     ma.pair_cap = w.pair_cap;

@@ -537,6 +537,7 @@ struct ManyArgs {
   int32_t carry;                  // a CTA whose rank failed continues with the next rank
                                   // (else the next rank goes to the queue's tail)
   int32_t early_fail;             // lazy mode: the row-end area test (R8)
+  int32_t ahead;                  // lazy mode: positions rasterized beyond the fold's need
   int32_t nmax;
   int64_t pair_cap;
 };
