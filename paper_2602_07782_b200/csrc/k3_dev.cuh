@@ -21,10 +21,19 @@ struct ObbC {
   LinDiv lin[8];
   int64_t last[4];   // value at the clipped high edge of the last cell
   int64_t star[4];   // value at the crossing
-  int64_t iA[4];     // crossing at or beyond cell i's low edge  <=>  i <= iA
-  int64_t iB[4];     // crossing at or before cell i's high edge <=>  i >= iB (non-last)
+  // iA / iB are only compared with cell indices (< 2^30), so they are kept
+  // clamped to +-2^30 (the same comparisons), in 32 bits
+  int32_t iA[4];     // crossing at or beyond cell i's low edge  <=>  i <= iA
+  int32_t iB[4];     // crossing at or before cell i's high edge <=>  i >= iB (non-last)
   int32_t lastB[4];  // same test for the last cell (edge = chart extent)
+  int32_t starc[4], lastc[4];  // star / last clamped to +-2^30 (RawIter's bounds)
 };
+
+// v clamped to +-2^30: where a value is only compared with cell indices or
+// texel values (both far smaller), the clamp changes no comparison
+__device__ __forceinline__ int32_t clamp30(int64_t v) {
+  return (int32_t)(v < -(1ll << 30) ? -(1ll << 30) : v > (1ll << 30) ? (1ll << 30) : v);
+}
 
 struct ChartK3 {
   int32_t s, c, ws, hs, j8, small;  // small: handled by the tile kernel
@@ -100,8 +109,8 @@ __device__ inline void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i
       rden = rN2SC;
     }
     const int64_t v = sg * fdiv_r128(sg > 0 ? nm : -nm, den, rden, false);
-    if (r < 4) O.last[q] = v;
-    else O.star[q] = v;
+    if (r < 4) { O.last[q] = v; O.lastc[q] = clamp30(v); }
+    else { O.star[q] = v; O.starc[q] = clamp30(v); }
   }
   {  // crossing x* / x** / y* / y**: i <= iA  (jobs 0-3), i >= iB (jobs 4-7)
     const int64_t m1 = q < 2 ? C : S;
@@ -110,10 +119,10 @@ __device__ inline void obb_job(ObbC& O, int r, int64_t C, int64_t S, i128 UMN, i
     const i128 X2 = q == 0 ? VMN : q == 1 ? VXN : q == 2 ? VXN : VMN;
     const i128 cross = (i128)m1 * X1 + (i128)m2 * X2;
     if (r < 4) {
-      O.iA[q] = fdiv_r128(cross, N2SC, rN2SC, true);
+      O.iA[q] = clamp30(fdiv_r128(cross, N2SC, rN2SC, true));
       O.lastB[q] = cross <= mul_wide(q < 2 ? nw : nh, N2);
     } else {
-      O.iB[q] = -fdiv_r128(-cross, N2SC, rN2SC, true) - 1;
+      O.iB[q] = clamp30(-fdiv_r128(-cross, N2SC, rN2SC, true) - 1);
     }
   }
 }
@@ -248,13 +257,10 @@ struct RawIter {
   // smaller); its step, remainder, divisor; the cell where its piece ends
   int32_t v[2], sq[2], sw[2];
   int64_t r[2], sr[2], D[2];
-  __device__ __forceinline__ static int32_t clamp30(int64_t v) {
-    return (int32_t)(v < -(1ll << 30) ? -(1ll << 30) : v > (1ll << 30) ? (1ll << 30) : v);
-  }
   // bound b's piece containing cell `at`
   __device__ __forceinline__ void seg(int b, int32_t at) {
     const int q = 2 * ax + b;
-    const int32_t iA = clamp30(O->iA[q]), iB = clamp30(O->iB[q]), last = cnt - 1;
+    const int32_t iA = O->iA[q], iB = O->iB[q], last = cnt - 1;
     const bool line = at > iA || (at != last && at < iB);
     if (line) {  // floor((A + i B) / D) from cell `at` on
       const LinDiv& L = O->lin[4 * ax + 2 * b + (at > iA ? 0 : 1)];
@@ -266,8 +272,7 @@ struct RawIter {
       D[b] = L.D;
       sw[b] = at > iA ? INT32_MAX : min(min(iB, iA + 1), last);
     } else {  // the crossing value, or the last cell's
-      const int32_t c = at == last ? clamp30(O->lastB[q] != 0 ? O->star[q] : O->last[q])
-                                   : clamp30(O->star[q]);
+      const int32_t c = at == last && O->lastB[q] == 0 ? O->lastc[q] : O->starc[q];
       v[b] = b ? -c : c;
       sq[b] = 0;
       r[b] = 0;
