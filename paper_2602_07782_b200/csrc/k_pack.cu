@@ -1757,6 +1757,65 @@ __device__ __forceinline__ void st_release_i(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Idle speculation (batch, carry mode): an undecided atlas of the LPT order
+// with fewer than A.spec ranks in flight gets its next rank issued here (warp
+// 0 scans 32 order positions per step; a hint skips the leading decided
+// ones).  The rank counts as issued BEFORE it is taken, as a continuation is,
+// so a completion can never decide the atlas while it is being taken; a taken
+// index past the last candidate is completed at once (and decides the atlas
+// if it was the last outstanding rank).  Returns the item for every lane, or
+// -1.
+__device__ __noinline__ int spec_pick(const ManyArgs& A, int lane) {
+  const int h0 = *(volatile int32_t*)(A.qctl + 3);
+  for (int p0 = h0; p0 < A.E; p0 += 32) {
+    const int p = p0 + lane;
+    bool dec = true, cand = false;
+    int a = 0;
+    if (p < A.E) {
+      a = A.order[p];
+      const AtlasRes& R = A.res[a];
+      const Status* st = A.sts + a;
+      dec = *(volatile int32_t*)&R.done != 0;
+      const int32_t nr = *(volatile int32_t*)&R.next_r;
+      cand = !dec && *(volatile int32_t*)&st->win_j == INT32_MAX &&
+             *(volatile int32_t*)&st->bad_chart == INT32_MAX &&
+             *(volatile int32_t*)&st->capacity == 0 &&
+             *(volatile int32_t*)&R.issued - *(volatile int32_t*)&R.completed < A.spec &&
+             st->pad[2] - nr >= 1 && nr < 256;
+    }
+    const unsigned dm = __ballot_sync(0xffffffffu, dec);
+    if (lane == 0 && p0 == h0 && (dm & 1u)) {
+      const int lead = dm == 0xffffffffu ? 32 : __ffs(~dm) - 1;
+      atomicMax(A.qctl + 3, p0 + lead);
+    }
+    unsigned cm = __ballot_sync(0xffffffffu, cand);
+    while (cm) {
+      const int src = __ffs(cm) - 1;
+      int v = -1;
+      if (lane == src) {
+        AtlasRes& R = A.res[a];
+        Status* st = A.sts + a;
+        atomicAdd(&R.issued, 1);
+        const int nr = atomicAdd(&R.next_r, 1);
+        if (st->pad[2] - nr >= 1 && nr < 256) {
+          v = a | (nr << 20);
+        } else {
+          const int done_now = atomicAdd(&R.completed, 1) + 1;
+          if (done_now == *(volatile int32_t*)&R.issued &&
+              *(volatile int32_t*)&st->win_j == INT32_MAX && atomicCAS(&R.done, 0, 1) == 0) {
+            __threadfence();
+            atomicSub(A.qctl + 2, 1);
+          }
+        }
+      }
+      v = __shfl_sync(0xffffffffu, v, src);
+      if (v >= 0) return v;
+      cm &= cm - 1;
+    }
+  }
+  return -1;
+}
+
 __global__ void __launch_bounds__(kNT, 1)
 many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -1782,17 +1841,34 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
   // per-CTA timeline (globaltimer ns): start, end of its last item
   if (tid == 0) A.cycles[3 + 2 * gcta] = A.cycles[3 + 2 * gcta + 1] = gtime();
   while (true) {
-    if (tid == 0) {
-      int v = carry;
+    if (wid == 0) {
+      int v = __shfl_sync(0xffffffffu, carry, 0);  // (carry lives in thread 0)
       if (v < 0) {
-        const int i = atomicAdd(&A.qctl[0], 1);
+        int i = lane == 0 ? atomicAdd(&A.qctl[0], 1) : 0;
+        i = __shfl_sync(0xffffffffu, i, 0);
         if (i < A.qcap) {
-          while ((v = ld_acquire_i(A.q + i)) < 0) {
-            if (ld_acquire_i(A.qctl + 2) == 0) break;  // every atlas decided
+          while (true) {
+            int got = -1, stop = 0;
+            if (lane == 0) {
+              got = ld_acquire_i(A.q + i);
+              if (got < 0) stop = ld_acquire_i(A.qctl + 2) == 0;  // every atlas decided
+            }
+            got = __shfl_sync(0xffffffffu, got, 0);
+            stop = __shfl_sync(0xffffffffu, stop, 0);
+            if (got >= 0) { v = got; break; }
+            if (stop) break;
+            // idle: in carry mode no rank is ever requeued, so an index at or
+            // past the tail is never filled -- start the next rank of an
+            // undecided atlas instead (speculation that costs an idle SM only)
+            if (A.spec > 1 && i >= *(volatile int32_t*)(A.qctl + 1)) {
+              v = spec_pick(A, lane);
+              if (v >= 0) break;
+            }
             __nanosleep(256);
           }
         }
       }
+      if (lane == 0) {
       item_s = v;
       // a rank of an atlas already decided, or above a lower rank that won, is
       // skipped -- decided HERE, once, for the whole CTA (other CTAs change
@@ -1806,6 +1882,7 @@ many_kernel(PackParams pp0, ManyArgs A, int32_t prof_cap) {
         skip_s = bad_a ? 2
                  : (*(volatile int32_t*)&sa->win_j < r || *(volatile int32_t*)&A.res[a].done != 0) ? 1
                                                                                                   : 0;
+      }
       }
     }
     __syncthreads();

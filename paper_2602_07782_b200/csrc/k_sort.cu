@@ -673,6 +673,7 @@ __global__ void many_reset_kernel(Status* sts, AtlasRes* res, int32_t A, const i
     qctl[0] = 0;      // head
     qctl[1] = E * K;  // tail
     qctl[2] = E;      // atlases not yet decided
+    qctl[3] = 0;      // idle speculation: order positions below are decided
   }
 }
 

@@ -1364,6 +1364,19 @@ extern "C" tabi_status tabi_pack_many(tabi_ctx* ctx, int32_t A, const float* xy,
       // 12.9 ms)
       ma.carry = (inflight > 1 || E < 2 * w.G || (cenv && cenv[0] == '1')) ? 1 : 0;
       if (cenv && cenv[0] == '0') ma.carry = inflight > 1 ? 1 : 0;
+      // Idle speculation: once the queue is drained, an idle CTA starts the
+      // next rank of an undecided atlas (up to 2 in flight per atlas) instead
+      // of waiting -- the batch's tail is the top-down chains of its last
+      // atlases.  Needs carry mode (no rank is requeued, so a queue index past
+      // the tail is never filled).  Measured on C5 (kernel ms, same box):
+      // 9.93 without, 9.83 carry alone, 9.16 / 9.13 / 9.17 with 2 / 3 / 4
+      // ranks (load-balance tail 1.40 -> 0.53 / 0.30 / 0.18 ms, 4,017 ->
+      // 4,131 / 4,208 / 4,278 items).  TABI_MANY_SPEC: test knob (0 = off).
+      const char* senv = getenv("TABI_MANY_SPEC");
+      ma.spec = senv ? atoi(senv) : 2;
+      if (ma.spec > 1) ma.carry = 1;
+      ma.order = d_order;
+      ma.E = E;
     }
     ma.dcol = w.dcol;
     ma.drow = w.drow;

@@ -536,6 +536,10 @@ struct ManyArgs {
   int32_t inflight;               // ranks of one atlas in flight at once (K >= 1)
   int32_t carry;                  // a CTA whose rank failed continues with the next rank
                                   // (else the next rank goes to the queue's tail)
+  int32_t spec;                   // > 1: idle CTAs start ranks of undecided atlases, up to
+                                  // this many in flight per atlas (carry mode only)
+  const int32_t* order;           // [E] the batched atlases, LPT order
+  int32_t E;
   int32_t early_fail;             // lazy mode: the row-end area test (R8)
   int32_t ahead;                  // lazy mode: positions rasterized beyond the fold's need
   int32_t nmax;

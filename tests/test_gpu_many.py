@@ -212,6 +212,7 @@ def test_pack_many_lazy_and_early_fail_are_exact(ctx, monkeypatch, mode):
     # one rank per atlas in flight: the evaluated-candidate count is then
     # schedule-independent (speculative ranks are compared below)
     monkeypatch.setenv("TABI_MANY_INFLIGHT", "1")
+    monkeypatch.setenv("TABI_MANY_SPEC", "0")  # (no idle speculation either)
     ref = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res)
     for k, v in mode.items():
         monkeypatch.setenv(k, v)
@@ -270,7 +271,9 @@ def test_pack_many_ranks_in_flight_are_exact(ctx, monkeypatch, k):
         [chartgen.small_case(s, n=90, side=2048, family="tss", rho=3.0) for s in range(3)]
     xy, cst, abase, res = concat_chart_sets(sets)
     monkeypatch.setenv("TABI_MANY_INFLIGHT", "1")
+    monkeypatch.setenv("TABI_MANY_SPEC", "0")
     ref = ctx.pack_many(xy, cst, abase, spec_of(sets[0]), res_xy=res, raise_on_error=False)
+    monkeypatch.delenv("TABI_MANY_SPEC")
     monkeypatch.setenv("TABI_MANY_INFLIGHT", k)
     for carry in ("0", "1"):
         monkeypatch.setenv("TABI_MANY_CARRY", carry)
@@ -279,3 +282,36 @@ def test_pack_many_ranks_in_flight_are_exact(ctx, monkeypatch, k):
             assert list(ref[3]) == list(alt[3])
             assert [i.scale_index for i in ref[2]] == [i.scale_index for i in alt[2]]
             assert ref[1].tobytes() == alt[1].tobytes()
+
+
+@pytest.mark.parametrize("spec", ["2", "3", "8"])
+def test_pack_many_idle_speculation_is_exact(ctx, monkeypatch, spec):
+    """Idle speculation (batch kernel): a CTA with no queued item
+    starts the next rank of an undecided atlas, up to `spec` ranks in flight.
+    One rank per atlas queued and far fewer atlases than CTAs, so almost every
+    CTA speculates from the start -- on C5 atlases, NO_FIT atlases (every rank
+    fails: the last outstanding rank, possibly a speculative index past the
+    last candidate, decides them) and trivial ones; the bytes of the plain
+    top-down search, run after run."""
+    from paper_2602_07782_b200 import concat_chart_sets, spec_of
+    from paper_2602_07782_b200 import NO_FIT
+    # a 20,000 x 5 texel sliver exceeds the 2048^2 atlas at every scale m / 8:
+    # all 8 ranks fail
+    sliver = chartgen.from_polygons([[(0, 0), (20000, 0), (20000, 5), (0, 5)],
+                                     [(0, 0), (30, 0), (30, 30), (0, 30)]], 2048, 2048)
+    sets = [chartgen.config5(i) for i in range(300, 316)] + [sliver, sliver] + \
+        [chartgen.small_case(s, n=90, side=2048, family="tss", rho=3.0) for s in range(3)] + \
+        [chartgen.small_case(s, n=40, side=2048, family="tss", rho=0.2) for s in range(2)]
+    xy, cst, abase, res = concat_chart_sets(sets)
+    sp = spec_of(sets[0], scale_count=8)
+    monkeypatch.setenv("TABI_MANY_INFLIGHT", "1")
+    monkeypatch.setenv("TABI_MANY_SPEC", "0")
+    ref = ctx.pack_many(xy, cst, abase, sp, res_xy=res, raise_on_error=False)
+    assert list(ref[3][16:18]) == [NO_FIT, NO_FIT] and all(s == 0 for s in ref[3][:16])
+    monkeypatch.setenv("TABI_MANY_SPEC", spec)
+    for _ in range(4):
+        alt = ctx.pack_many(xy, cst, abase, sp, res_xy=res, raise_on_error=False)
+        assert list(ref[3]) == list(alt[3])
+        assert [i.scale_index for i in ref[2]] == [i.scale_index for i in alt[2]]
+        assert ref[1].tobytes() == alt[1].tobytes()
+        assert alt[4].candidates_evaluated >= ref[4].candidates_evaluated
