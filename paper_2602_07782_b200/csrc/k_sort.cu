@@ -403,6 +403,73 @@ __global__ void rank_scatter_kernel(const int32_t* __restrict__ rank, int32_t n,
   if (i < n) perm[rank[i]] = i;
 }
 
+__device__ __forceinline__ void st_release_flag(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_flag(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Fused-kernel raster tiles: consecutive sorted charts with tile key
+// floor(slot prefix / kFusedTileCells) + floor(s / kFusedTileCharts) --
+// non-decreasing in s, so equal keys are runs of <= kFusedTileCharts charts
+// holding about kFusedTileCells footprint cells (the tallest charts come first
+// and get small tiles, so their tiles are not the long pole every packer waits
+// on); the first kFusedHeadCells cells (the tallest charts, which every packer
+// needs first) are cut into quarter-size tiles so the first rows start early.
+__device__ __forceinline__ int32_t fused_tile_id(int64_t cum, int s) {
+  const int64_t q4 = kFusedTileCells / 4;
+  const int64_t cell_key = cum < kFusedHeadCells
+                               ? cum / q4
+                               : kFusedHeadCells / q4 + (cum - kFusedHeadCells) / kFusedTileCells;
+  return (int32_t)(cell_key + s / kFusedTileCharts);
+}
+
+// Scale bounds from the total polygon area (warp 0, every lane gets them).
+// R2: sequential mode only -- every chart keeps m/M, so a successful
+// (overlap-free, in-bounds) packing needs (m/M)^2 A <= W H; in units (2*area,
+// 1/256 texel): m^2 * A2 <= 2 * 65536 * W * H * M^2.  In hybrid mode the prefix
+// tail's intermediate downscale (D24) can make a candidate above that bound
+// succeed, so the search starts at M.  m_hi = the largest m <= M passing it
+// (monotone in m: lane l of round r tests m = M - 32 r - l; the lowest passing
+// lane wins).  Wave 0's width b0: the candidates from m_hi down to the scale
+// at which the charts would fill TABI_B0_FILL % of the atlas (TSS sets pack at
+// ~60 %) -- below that a success is unlikely, and a narrower first wave leaves
+// the top candidate's chain with less contention.  Later waves take B each
+// and the wave loop's stopping rule (select_kernel; hybrid mode: the V bound
+// of D25) is unchanged, so the result is the exhaustive search's either way.
+// m_lo = 1 + the largest m' < m_hi below the fill level (monotone), else 1.
+__device__ __forceinline__ void scale_bounds(const PackParams& pp, i128 tot, int lane, int& m_hi,
+                                             int& b0) {
+  const i128 rhs = (i128)2 * 65536 * pp.W * pp.H * (i128)pp.M * pp.M;
+  m_hi = 0;
+  for (int base = 0; base < pp.M && m_hi == 0; base += 32) {  // (uniform)
+    const int m = pp.M - base - lane;
+    const unsigned ok =
+        __ballot_sync(0xffffffffu, m >= 1 && (pp.t_opt > 0 || (i128)m * m * tot <= rhs));
+    if (ok) m_hi = pp.M - base - (__ffs(ok) - 1);
+  }
+  b0 = pp.B;
+  if (pp.B > 2 && m_hi >= 1) {
+    int m_lo = 0;
+    for (int base = 1; base < m_hi && m_lo == 0; base += 32) {  // (uniform)
+      const int mp = m_hi - base - lane;
+      const unsigned lowr = __ballot_sync(
+          0xffffffffu, mp >= 1 && (i128)100 * mp * mp * tot < (i128)TABI_B0_FILL * rhs);
+      if (lowr) m_lo = m_hi - base - (__ffs(lowr) - 1) + 1;
+    }
+    if (m_lo == 0) m_lo = 1;
+    b0 = min(pp.B, max(2, m_hi - m_lo + 1));
+    // hybrid mode: the prefix tail's downscale absorbs the overflow that
+    // fails a sequential candidate, so the top candidates usually succeed
+    // and then win (D25) -- a first wave of TABI_B0_HYBRID; the device
+    // loop's V bound decides whether lower ones still need a wave
+    if (pp.t_opt > 0) b0 = min(b0, TABI_B0_HYBRID);
+  }
+}
+
 // Footprint slots: column slot of sorted position s = min(ceil(w/256) + 2g, W'),
 // row slot = min(ceil(h/256) + 2g, H') -- the footprint at the largest scale
 // (m = M, scale 1) bounds every candidate's (w_s is monotone in m).
@@ -441,44 +508,8 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
       i128 tot = (i128)(((unsigned __int128)asum[1][lane] << 64) | asum[0][lane]);
       tot = warp_sum128(tot);
       const int32_t wmx = warp_max(ext_max[0][lane]), hmx = warp_max(ext_max[1][lane]);
-      const i128 rhs = (i128)2 * 65536 * pp.W * pp.H * (i128)pp.M * pp.M;
-      // R2: sequential mode only -- every chart keeps m/M, so a successful
-      // (overlap-free, in-bounds) packing needs (m/M)^2 A <= W H.  In hybrid
-      // mode the prefix tail's intermediate downscale (D24) can make a
-      // candidate above that bound succeed, so the search starts at M.
-      // m_hi = the largest m <= M passing it (the test is monotone in m: lane
-      // l of round r tests m = M - 32 r - l; the lowest passing lane wins)
-      int m_hi = 0;
-      for (int base = 0; base < pp.M && m_hi == 0; base += 32) {  // (uniform)
-        const int m = pp.M - base - lane;
-        const unsigned ok = __ballot_sync(0xffffffffu, m >= 1 && (pp.t_opt > 0 || (i128)m * m * tot <= rhs));
-        if (ok) m_hi = pp.M - base - (__ffs(ok) - 1);
-      }
-      // Wave 0's width: the candidates from m_hi down to the scale at which
-      // the charts would fill 55 % of the atlas (TSS sets pack at ~60 %) -- below that a success is
-      // unlikely, and a narrower first wave leaves the top candidate's chain
-      // with less contention.  Later waves take B each and the wave loop's
-      // stopping rule (select_kernel; hybrid mode: the V bound of D25) is
-      // unchanged, so the result is the exhaustive search's either way.
-      // m_lo = 1 + the largest m' < m_hi below the fill level (monotone in
-      // m'), else 1
-      int b0 = pp.B;
-      if (pp.B > 2 && m_hi >= 1) {
-        int m_lo = 0;
-        for (int base = 1; base < m_hi && m_lo == 0; base += 32) {  // (uniform)
-          const int mp = m_hi - base - lane;
-          const unsigned lowr = __ballot_sync(
-              0xffffffffu, mp >= 1 && (i128)100 * mp * mp * tot < (i128)TABI_B0_FILL * rhs);
-          if (lowr) m_lo = m_hi - base - (__ffs(lowr) - 1) + 1;
-        }
-        if (m_lo == 0) m_lo = 1;
-        b0 = min(pp.B, max(2, m_hi - m_lo + 1));
-        // hybrid mode: the prefix tail's downscale absorbs the overflow that
-        // fails a sequential candidate, so the top candidates usually succeed
-        // and then win (D25) -- a first wave of TABI_B0_HYBRID; the device
-        // loop's V bound decides whether lower ones still need a wave
-        if (pp.t_opt > 0) b0 = min(b0, TABI_B0_HYBRID);
-      }
+      int m_hi, b0;
+      scale_bounds(pp, tot, lane, m_hi, b0);
       if (lane == 0) {
       st->wmax = wmx;
       st->hmax = hmx;
@@ -517,13 +548,7 @@ __device__ __forceinline__ void prep_body(const int32_t* __restrict__ hh,
   // pole every packer waits on).
   // the first kFusedHeadCells cells (the tallest charts, which every packer
   // needs first) are cut into quarter-size tiles so the first rows start early
-  auto tile_id = [&](int64_t cum, int s) -> int32_t {
-    const int64_t q4 = kFusedTileCells / 4;
-    const int64_t cell_key = cum < kFusedHeadCells
-                                 ? cum / q4
-                                 : kFusedHeadCells / q4 + (cum - kFusedHeadCells) / kFusedTileCells;
-    return (int32_t)(cell_key + s / kFusedTileCharts);
-  };
+  auto tile_id = [&](int64_t cum, int s) -> int32_t { return fused_tile_id(cum, s); };
   int32_t carry_c = 0, carry_r = 0, carry_t = 0, prev_id = -1;  // prev_id: the tile of the
                                                                  // previous chunk's last position
   for (int base = 0; base < pp.n; base += kCh) {
@@ -614,6 +639,212 @@ prep_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww, cons
             int32_t* tstart, int32_t* tix, Status* st, int32_t* rdy, const uint64_t* skeys) {
   if (st->bad_chart != INT32_MAX) return;
   prep_body(hh, ww, area2, perm, pp, colofs, rowofs, hsorted, tstart, tix, st, rdy, skeys, 0);
+}
+
+// 4096 < N <= 2^17: the same layout by one CTA per 4096 sorted positions with
+// decoupled look-back (the carries of a block are the published aggregates
+// of all lower blocks, read in parallel by warp 0 -- no serial chain): pass 1
+// slot-size sums (and the blocks' area / extent partials), pass 2 tile-start
+// counts.  Every block of the grid is resident (<= 32 blocks), and a block
+// waits only for lower ones.  Flags carry an epoch (PrepSync::epoch + 1,
+// read by every block at its start; the last block -- which has seen every
+// block's pass-1 flag, so every block has read the epoch -- advances it), so
+// nothing is reset between packs.  The last block finishes the totals: the
+// scale bounds, the tile end, the capacity test and the fused wave-0 flags.
+__global__ void __launch_bounds__(kT, 1)
+prep_multi_kernel(const int32_t* __restrict__ hh, const int32_t* __restrict__ ww,
+                  const int64_t* area2, const int32_t* perm, PackParams pp, int32_t* colofs,
+                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
+                  int32_t* rdy, const uint64_t* skey, PrepSync* ps) {
+  if (st->bad_chart != INT32_MAX) return;
+  constexpr int kE = 4;
+  constexpr int kCh = kE * kT;
+  __shared__ int32_t sh[2][kW + 1];
+  __shared__ unsigned long long asum[2][kW];
+  __shared__ int32_t ext_max[2][kW];
+  __shared__ uint16_t scw[kCh], srh[kCh];
+  __shared__ int32_t s_ep, s_cc, s_cr, s_ct;
+  const int b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool last = b == nb - 1;
+  if (tid == 0) s_ep = *(volatile int32_t*)&ps->epoch + 1;
+  const int base = b * kCh, cn = min(kCh, pp.n - base);
+  auto hw_at = [&](int s, int32_t& h, int32_t& w) {
+    if (skey) {  // the sorted key holds (h, w): no dependent global loads
+      const uint64_t k = skey[s];
+      h = (int32_t)(0x3ffffffu - (uint32_t)((k >> 26) & 0x3ffffffu));
+      w = (int32_t)(0x3ffffffu - (uint32_t)(k & 0x3ffffffu));
+    } else {
+      const int c = perm[s];
+      w = ww[c];
+      h = hh[c];
+    }
+  };
+  // this block's share of the area / extent reductions (by chart index)
+  {
+    i128 a = 0;
+    int32_t wm = 0, hm = 0;
+    for (int i = base + tid; i < base + cn; i += kT) {
+      a += area2[i];
+      wm = max(wm, ww[i]);
+      hm = max(hm, hh[i]);
+    }
+    a = warp_sum128(a);
+    wm = warp_max(wm);
+    hm = warp_max(hm);
+    if (lane == 0) {
+      asum[0][wid] = (unsigned long long)(uint64_t)a;
+      asum[1][wid] = (unsigned long long)(uint64_t)(a >> 64);
+      ext_max[0][wid] = wm;
+      ext_max[1][wid] = hm;
+    }
+  }
+  // slot sizes of the block's sorted positions (as prep_body)
+#pragma unroll
+  for (int u = 0; u < kE; u++) {
+    const int x = u * kT + tid;
+    if (x < cn) {
+      int32_t h, w;
+      hw_at(base + x, h, w);
+      const int64_t wd = ceildiv(w, TABI_UNITS) + 2 * pp.g;
+      const int64_t hd = ceildiv(h, TABI_UNITS) + 2 * pp.g;
+      scw[x] = (uint16_t)(wd < pp.Wp ? wd : pp.Wp);
+      srh[x] = (uint16_t)(hd < pp.Hp ? hd : pp.Hp);
+      hsorted[base + x] = h;
+    }
+  }
+  __syncthreads();
+  const int q0 = min(cn, tid * kE), q1 = min(cn, q0 + kE);
+  int32_t sc = 0, sr = 0;
+  for (int q = q0; q < q1; q++) {
+    sc += scw[q];
+    sr += srh[q];
+  }
+  int32_t ec, er, tc, tr;
+  block_scan2(sc, sr, ec, er, tc, tr, sh);
+  const int32_t ep = s_ep;
+  // pass 1: publish the block's aggregate, then the lower blocks' carries
+  if (wid == 0) {
+    i128 a = (i128)(((unsigned __int128)asum[1][lane] << 64) | asum[0][lane]);
+    a = warp_sum128(a);
+    const int32_t wm = warp_max(ext_max[0][lane]), hm = warp_max(ext_max[1][lane]);
+    if (lane == 0) {
+      ps->c[b] = tc;
+      ps->r[b] = tr;
+      ps->alo[b] = (unsigned long long)(uint64_t)a;
+      ps->ahi[b] = (unsigned long long)(uint64_t)(a >> 64);
+      ps->wm[b] = wm;
+      ps->hm[b] = hm;
+      __threadfence();
+      st_release_flag(&ps->f1[b], ep);
+    }
+    int32_t cc = 0, cr = 0;
+    i128 at = 0;
+    int32_t wmx = 0, hmx = 0;
+    if (lane < b) {
+      while (ld_acquire_flag(&ps->f1[lane]) != ep) __nanosleep(32);
+      cc = ps->c[lane];
+      cr = ps->r[lane];
+      at = (i128)(((unsigned __int128)ps->ahi[lane] << 64) | ps->alo[lane]);
+      wmx = ps->wm[lane];
+      hmx = ps->hm[lane];
+    }
+    cc = warp_sum(cc);
+    cr = warp_sum(cr);
+    if (lane == 0) { s_cc = cc; s_cr = cr; }
+    if (last) {  // every block's partials: the area bound, extents, wave-0 width
+      at = warp_sum128(at) + a;
+      wmx = max(warp_max(wmx), wm);
+      hmx = max(warp_max(hmx), hm);
+      int m_hi, b0;
+      scale_bounds(pp, at, lane, m_hi, b0);
+      if (lane == 0) {
+        st->wmax = wmx;
+        st->hmax = hmx;
+        st->pad[2] = m_hi;
+        st->b0 = b0;
+        st->atot_lo = (unsigned long long)(uint64_t)at;
+        st->atot_hi = (unsigned long long)(uint64_t)(at >> 64);
+        ps->epoch = ep;  // (every block has read the epoch: all pass-1 flags seen)
+      }
+    }
+  }
+  __syncthreads();
+  ec += s_cc;
+  er += s_cr;
+  // the tile of the position before this block's first one
+  int32_t prev_id = -1;
+  if (base > 0) {
+    int32_t h, w;
+    hw_at(base - 1, h, w);
+    const int64_t wd = min(ceildiv(w, TABI_UNITS) + 2 * pp.g, (int64_t)pp.Wp);
+    const int64_t hd = min(ceildiv(h, TABI_UNITS) + 2 * pp.g, (int64_t)pp.Hp);
+    prev_id = fused_tile_id((int64_t)s_cc + s_cr - wd - hd, base - 1);
+  }
+  int32_t pid = q0 == 0 ? prev_id
+                : q0 < q1 ? fused_tile_id((int64_t)ec + er - scw[q0 - 1] - srh[q0 - 1], base + q0 - 1)
+                          : 0;
+  int32_t nf = 0;
+  {
+    int64_t cum = (int64_t)ec + er;
+    int32_t p = pid;
+    for (int q = q0; q < q1; q++) {
+      const int32_t id = fused_tile_id(cum, base + q);
+      nf += id != p;
+      p = id;
+      cum += scw[q] + srh[q];
+    }
+  }
+  int32_t ef, e2, tf, t2;
+  block_scan2(nf, 0, ef, e2, tf, t2, sh);
+  // pass 2: tile-start counts
+  if (wid == 0) {
+    if (lane == 0) {
+      ps->t[b] = tf;
+      __threadfence();
+      st_release_flag(&ps->f2[b], ep);
+    }
+    int32_t ct = 0;
+    if (lane < b) {
+      while (ld_acquire_flag(&ps->f2[lane]) != ep) __nanosleep(32);
+      ct = ps->t[lane];
+    }
+    ct = warp_sum(ct);
+    if (lane == 0) s_ct = ct;
+  }
+  __syncthreads();
+  const int32_t carry_t = s_ct;
+  {
+    int32_t c = ec, r = er, tt = carry_t + ef - 1;
+    for (int q = q0; q < q1; q++) {
+      const int s = base + q;
+      const int32_t id = fused_tile_id((int64_t)c + r, s);
+      if (id != pid) tstart[++tt] = s;
+      colofs[s] = c;
+      rowofs[s] = r;
+      tix[s] = tt;
+      c += scw[q];
+      r += srh[q];
+      pid = id;
+    }
+  }
+  if (!last) return;
+  const int32_t cols = s_cc + tc, rows = s_cr + tr, ntiles = carry_t + tf;
+  if (tid == 0) {
+    st->cols_total = cols;
+    st->rows_total = rows;
+    st->ntiles = ntiles;
+    tstart[ntiles] = pp.n;
+    // +4: the TMA bulk copy of a row window rounds its end up to 16 bytes
+    if ((int64_t)cols + 4 > pp.col_cap || (int64_t)rows + 4 > pp.row_cap) st->capacity |= 1;
+  }
+  if (rdy) {  // fused wave 0 (as prep_body)
+    const int64_t bt = (int64_t)pp.B * ntiles, bn = (int64_t)pp.B * pp.n;
+    for (int64_t q = tid; q < bt; q += kT) {
+      rdy[q] = 0;
+      rdy[bn + q] = 0;
+    }
+    for (int q = tid; q < 2 * pp.B; q += kT) rdy[2 * bn + q] = 0;
+  }
 }
 
 // N <= 2048: order and slot layout in one launch (the block that sorted reads
@@ -784,7 +1015,14 @@ void launch_many_reset(Status* sts, AtlasRes* res, int32_t A, const int32_t* ord
 
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                 int32_t* rdy, cudaStream_t s, const uint64_t* sorted_keys) {
+                 int32_t* rdy, cudaStream_t s, const uint64_t* sorted_keys, PrepSync* ps) {
+  const int nb = (pp.n + 4 * kT - 1) / (4 * kT);
+  const char* env = getenv("TABI_PREP_MULTI");  // test knob: 0 = one CTA
+  if (ps && nb > 1 && nb <= kPrepMaxBlocks && !(env && env[0] == '0')) {
+    prep_multi_kernel<<<nb, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted,
+                                        tstart, tix, st, rdy, sorted_keys, ps);
+    return;
+  }
   prep_kernel<<<1, kT, 0, s>>>(P.h, P.w, P.area2, perm, pp, colofs, rowofs, hsorted, tstart, tix,
                                st, rdy, sorted_keys);
 }

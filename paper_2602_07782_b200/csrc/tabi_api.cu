@@ -154,6 +154,7 @@ struct tabi_ctx {
   int32_t* rowofs = nullptr;
   int32_t* hsorted = nullptr;
   const uint64_t* sorted_keys = nullptr;  // keys in sorted order (chunked sort), else nullptr
+  PrepSync* prep_sync = nullptr;          // multi-CTA slot layout's look-back state (zeroed once)
   tabi_placement* d_out = nullptr;
   Status* d_status = nullptr;
   Status* h_status = nullptr;  // pinned
@@ -233,7 +234,7 @@ static void dfree_all(tabi_ctx* ctx) {
   void* ps[] = {ctx->d_xy, ctx->d_start, ctx->d_qx, ctx->d_qy, ctx->P.w, ctx->P.h, ctx->P.area2,
                 ctx->P.xmin, ctx->P.ymin, ctx->P.pose, ctx->P.prerot, ctx->P.sl, ctx->P.obb_j, ctx->P.obb,
                 ctx->keys, ctx->keys2, ctx->perm, ctx->perm2, ctx->colofs, ctx->rowofs,
-                ctx->hsorted, ctx->d_out, ctx->d_status, ctx->wd, ctx->hd, ctx->off,
+                ctx->hsorted, ctx->d_out, ctx->d_status, ctx->prep_sync, ctx->wd, ctx->hd, ctx->off,
                 ctx->lockbits, ctx->cand_bad, ctx->big_list, ctx->rdy, ctx->tstart, ctx->tix, ctx->X, ctx->Y, ctx->mir,
                 ctx->dcol, ctx->t_state, ctx->t_r0, ctx->t_p, ctx->t_iter,
                 ctx->t_fsave,
@@ -299,7 +300,8 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
             dalloc(&ctx->colofs, N) == cudaSuccess && dalloc(&ctx->rowofs, N) == cudaSuccess &&
             dalloc(&ctx->hsorted, N) == cudaSuccess && dalloc(&ctx->d_out, N) == cudaSuccess &&
             dalloc(&ctx->tstart, N + 1) == cudaSuccess && dalloc(&ctx->tix, N) == cudaSuccess &&
-            dalloc(&ctx->d_status, 1) == cudaSuccess;
+            dalloc(&ctx->d_status, 1) == cudaSuccess && dalloc(&ctx->prep_sync, 1) == cudaSuccess &&
+            cudaMemset(ctx->prep_sync, 0, sizeof(PrepSync)) == cudaSuccess;
   if (!ok) return fail();
   if (cudaMallocHost((void**)&ctx->h_status, sizeof(Status)) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->h_xy, sizeof(float) * (2 * V + N + 1)) != cudaSuccess ||
@@ -690,7 +692,8 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     }
     if (!prep_done) {
       launch_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted, ctx->tstart,
-                  ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s, ctx->sorted_keys);
+                  ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s, ctx->sorted_keys,
+                  ctx->prep_sync);
       nl++;
     }
     return TABI_OK;

@@ -469,9 +469,20 @@ int launch_sort(const Proxies& P, int32_t n, uint64_t* keys, uint64_t* keys2, in
 bool launch_sort_prep(const Proxies& P, int32_t* perm, const PackParams& pp, int32_t* colofs,
                       int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
                       int32_t* rdy, cudaStream_t s);  // rdy: zeroed for the fused wave, or nullptr
+// Multi-CTA slot layout (prep_multi_kernel): decoupled look-back state,
+// never reset (flags carry an epoch).  <= kPrepMaxBlocks blocks of 4096
+// sorted positions (N <= 2^17).
+constexpr int kPrepMaxBlocks = 32;
+struct PrepSync {
+  int32_t epoch;
+  int32_t f1[kPrepMaxBlocks], f2[kPrepMaxBlocks];
+  int32_t c[kPrepMaxBlocks], r[kPrepMaxBlocks], t[kPrepMaxBlocks];
+  int32_t wm[kPrepMaxBlocks], hm[kPrepMaxBlocks];
+  unsigned long long alo[kPrepMaxBlocks], ahi[kPrepMaxBlocks];
+};
 void launch_prep(const Proxies& P, const int32_t* perm, const PackParams& pp, int32_t* colofs,
                  int32_t* rowofs, int32_t* hsorted, int32_t* tstart, int32_t* tix, Status* st,
-                 int32_t* rdy, cudaStream_t s, const uint64_t* sorted_keys = nullptr);
+                 int32_t* rdy, cudaStream_t s, const uint64_t* sorted_keys = nullptr, PrepSync* ps = nullptr);
 void launch_profiles(const Proxies& P, const int32_t* perm, const PackParams& pp,
                      const int32_t* colofs, const int32_t* rowofs, int16_t* dcol, int16_t* drow,
                      int32_t* wd, int32_t* hd, int32_t* cand_bad, int32_t* big_list, Status* st,

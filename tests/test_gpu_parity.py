@@ -437,3 +437,31 @@ def test_obb_angle_ties_parity(orc, ctx):
         polys += [[(x * s, y * s) for x, y in p] for p in D6_TIES]
     cs = chartgen.from_polygons(polys, 1024, 1024)
     _compare_pack(orc, ctx, cs, check_profiles=4)
+
+
+@pytest.mark.parametrize("sort_path", ["default", "rank"])
+def test_multi_cta_slot_layout(ctx, monkeypatch, sort_path):
+    """The slot layout for 4096 < N <= 2^17 runs as one CTA per 4096 sorted
+    positions with decoupled look-back (prep_multi_kernel): the same packs
+    and winning candidate record as the one-CTA prep_kernel
+    (TABI_PREP_MULTI=0), at ragged sizes (one position past a block, several
+    blocks, C4's 20,000), from the chunked sort's keys and from the rank sort
+    (no sorted keys: perm loads), twice in a row (the look-back epochs)."""
+    from paper_2602_07782_b200 import spec_of
+    if sort_path != "default":
+        monkeypatch.setenv("TABI_SORT", sort_path)
+    for cs in (chartgen.generate("lightmap", 4097, 4096, 4096, 3, rho=0.8),
+               chartgen.generate("tss", 9000, 8192, 8192, 4, rho=1.2),
+               chartgen.config4(0, t_opt_bp=0)):
+        sp = spec_of(cs)
+        monkeypatch.setenv("TABI_PREP_MULTI", "0")
+        st0, pl0, info0 = ctx.pack(cs.xy, cs.start, sp)
+        c0 = ctx.candidates(cs.scale_count)
+        monkeypatch.delenv("TABI_PREP_MULTI")
+        for _ in range(2):
+            st1, pl1, info1 = ctx.pack(cs.xy, cs.start, sp)
+            c1 = ctx.candidates(cs.scale_count)
+            assert st0 == st1 and info0.scale_index == info1.scale_index, cs.name
+            assert pl0.tobytes() == pl1.tobytes(), cs.name
+            w = info0.scale_index - 1  # (the winner's record: aborted lower
+            assert c0[w].tobytes() == c1[w].tobytes(), cs.name  # candidates are schedule-dependent)
