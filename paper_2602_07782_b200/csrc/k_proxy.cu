@@ -242,7 +242,7 @@ template <int G>
 __global__ void __launch_bounds__(kBlock)
 proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
              float ry, int k, uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P,
-             Status* st, AtlasMap am) {
+             Status* st, AtlasMap am, bool skip_wh) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, gib = threadIdx.x / G;
   Group<G> g;
@@ -448,9 +448,11 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   const int bj = obb_angle(g, X, Y, nv, S, (flags & TABI_F_NO_OBB) ? 1 : 8, fx, fy, (int32_t)w,
                            (int32_t)h);
   if (gl == 0) {
-    P.w[c] = (int32_t)w;
-    P.h[c] = (int32_t)h;
-    P.area2[c] = s2;
+    if (!skip_wh) {  // (else written by sizes_kernel, which the order is waiting on)
+      P.w[c] = (int32_t)w;
+      P.h[c] = (int32_t)h;
+      P.area2[c] = s2;
+    }
     P.xmin[c] = xmn;
     P.ymin[c] = ymn;
     P.pose[c] = (uint8_t)((rot ? 1 : 0) | (fx ? 2 : 0) | (fy ? 4 : 0));
@@ -463,10 +465,80 @@ proxy_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, in
   }
 }
 
+// The order's inputs alone (A1-A3's AABB, 90-degree normalization and area,
+// no prerotation): the snapped extents w, h (swapped when w > h, D3) and the
+// doubled area |shoelace| of the snapped polygon -- translation- and
+// rotation-invariant, so the normalized polygon's exactly -- with the same
+// capacity / bad-chart decisions as proxy_kernel.  One 8-lane group per chart;
+// nothing is written but w, h, area2 and the status words.  Lets the sort
+// start while proxy_kernel computes the slices and OBBs on a second stream.
+__global__ void __launch_bounds__(kBlock)
+sizes_kernel(const float* __restrict__ xy, const int32_t* __restrict__ start, int32_t n, float rx,
+             float ry, int64_t max_v, Proxies P, Status* st) {
+  constexpr int G = 8;
+  const int lane = threadIdx.x & 31, gl = lane % G;
+  const unsigned mask = ((1u << G) - 1u) << (lane / G * G);
+  const int c = blockIdx.x * (kBlock / G) + threadIdx.x / G;
+  if (c >= n) return;  // (the whole group)
+  const int32_t a0 = start[c];
+  const int nv = start[c + 1] - a0;
+  if (a0 < 0 || (int64_t)a0 + (nv > 0 ? nv : 0) > max_v) {
+    if (gl == 0) atomicOr(&st->capacity, 4);
+    return;
+  }
+  if (nv < 3) {
+    if (gl == 0) atomicMin(&st->bad_chart, c);
+    return;
+  }
+  auto snap = [&](int v, int32_t& ix, int32_t& iy) -> bool {
+    const double fx = (double)xy[2 * ((int64_t)a0 + v)] * (double)rx * 256.0;
+    const double fy = (double)xy[2 * ((int64_t)a0 + v) + 1] * (double)ry * 256.0;
+    if (!isfinite(fx) || !isfinite(fy) || fabs(fx) > (double)TABI_QMAX || fabs(fy) > (double)TABI_QMAX)
+      return false;
+    ix = (int32_t)__double2ll_rn(fx);
+    iy = (int32_t)__double2ll_rn(fy);
+    return true;
+  };
+  bool ok = true;
+  int32_t xmn = INT32_MAX, xmx = INT32_MIN, ymn = INT32_MAX, ymx = INT32_MIN;
+  int64_t s2 = 0;
+  for (int v = gl; v < nv; v += G) {
+    int32_t x, y, xu, yu;
+    const bool okv = snap(v, x, y), oku = snap(v + 1 == nv ? 0 : v + 1, xu, yu);
+    if (!okv || !oku) { ok = false; continue; }
+    xmn = min(xmn, x); xmx = max(xmx, x);
+    ymn = min(ymn, y); ymx = max(ymx, y);
+    s2 += (int64_t)x * yu - (int64_t)xu * y;  // (exact modulo 2^64; |2A| < 2^51)
+  }
+  if (__ballot_sync(mask, !ok) != 0u) {
+    if (gl == 0) atomicMin(&st->bad_chart, c);
+    return;
+  }
+  xmn = __reduce_min_sync(mask, xmn); xmx = __reduce_max_sync(mask, xmx);
+  ymn = __reduce_min_sync(mask, ymn); ymx = __reduce_max_sync(mask, ymx);
+  const uint64_t u = (uint64_t)s2;
+  const uint64_t c0 = __reduce_add_sync(mask, (uint32_t)(u & 0xffffu));
+  const uint64_t c1 = __reduce_add_sync(mask, (uint32_t)((u >> 16) & 0xffffu));
+  const uint64_t c2 = __reduce_add_sync(mask, (uint32_t)((u >> 32) & 0xffffu));
+  const uint64_t c3 = __reduce_add_sync(mask, (uint32_t)(u >> 48));
+  int64_t a2 = (int64_t)(c0 + (c1 << 16) + (c2 << 32) + (c3 << 48));
+  if (a2 < 0) a2 = -a2;
+  if (gl != 0) return;
+  if (a2 == 0) {
+    atomicMin(&st->bad_chart, c);
+    return;
+  }
+  int64_t w = (int64_t)xmx - xmn, h = (int64_t)ymx - ymn;
+  if (w > h) { const int64_t t = w; w = h; h = t; }
+  P.w[c] = (int32_t)w;
+  P.h[c] = (int32_t)h;
+  P.area2[c] = a2;
+}
+
 template <int G>
 void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
               uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-              AtlasMap am, cudaStream_t s) {
+              AtlasMap am, cudaStream_t s, bool skip_wh) {
   constexpr int per_block = kBlock / G;
   const int blocks = (n - am.c0 + per_block - 1) / per_block;
   if (blocks < 1) return;
@@ -474,14 +546,22 @@ void launch_g(const float* xy, const int32_t* start, int32_t n, float rx, float 
   static std::atomic<unsigned long long> attr{0};  // k = 64 with 8-lane groups: 32 charts x 4.4 KB per block
   ensure_dyn_smem((const void*)proxy_kernel<G>, (int)(slice_bytes(TABI_KMAX) * per_block), attr);
   proxy_kernel<G><<<blocks, kBlock, smem, s>>>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P,
-                                                st, am);
+                                                st, am, skip_wh);
 }
 
 }  // namespace
 
+void launch_sizes(const float* xy, const int32_t* start, int32_t n, float rx, float ry,
+                  int64_t max_v, Proxies P, Status* st, cudaStream_t s) {
+  constexpr int per_block = kBlock / 8;
+  const int blocks = (n + per_block - 1) / per_block;
+  if (blocks < 1) return;
+  sizes_kernel<<<blocks, kBlock, 0, s>>>(xy, start, n, rx, ry, max_v, P, st);
+}
+
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
-                    cudaStream_t s, AtlasMap am, int64_t nverts) {
+                    cudaStream_t s, AtlasMap am, int64_t nverts, bool skip_wh) {
   const char* genv = getenv("TABI_PROXY_LANES");  // test knob: force 8 / 16 / 32
   const int forced = genv ? atoi(genv) : 0;
   // Lanes per chart.  Below 4096 charts a pack is latency-bound per chart: 32.
@@ -492,9 +572,9 @@ void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, 
   const int64_t avg = nverts > 0 ? (nverts + n - 1) / n : 0;
   const int G = forced == 8 || forced == 16 || forced == 32 ? forced
                 : n < 4096 ? 32 : avg >= 8 ? 32 : avg >= 6 ? 16 : n < 8192 ? 16 : 8;
-  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
-  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
-  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s);
+  if (G == 32) launch_g<32>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s, skip_wh);
+  else if (G == 16) launch_g<16>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s, skip_wh);
+  else launch_g<8>(xy, start, n, rx, ry, k, flags, qx, qy, max_v, P, st, am, s, skip_wh);
 }
 
 }  // namespace tabi

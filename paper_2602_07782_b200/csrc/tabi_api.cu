@@ -205,6 +205,8 @@ struct tabi_ctx {
   ManyWs many;             // tabi_pack_many
   cudaStream_t cap_stream = nullptr;  // captures the graph's wave-loop body
   cudaStream_t cap_stream2 = nullptr; // captures the hybrid tail's rounds-loop body
+  cudaStream_t fork_stream = nullptr; // proxy_kernel beside the sizes -> sort -> slot layout chain
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int g_body = 0;                     // kernels per wave of the graph's loop body
   bool loop_off = false;              // the graph's device wave loop failed once
   bool pend = false;                  // an asynchronous pack is in flight
@@ -282,6 +284,10 @@ extern "C" tabi_status tabi_ctx_create(tabi_ctx** out, int cuda_device, int32_t 
   };
   if (cudaSetDevice(cuda_device) != cudaSuccess) return fail();
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail();
+  if (cudaStreamCreateWithFlags(&ctx->fork_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return fail();
   if (cudaEventCreate(&ctx->span[0]) != cudaSuccess || cudaEventCreate(&ctx->span[1]) != cudaSuccess)
     return fail();
   const size_t N = (size_t)max_charts, V = (size_t)max_vertices;
@@ -325,6 +331,9 @@ extern "C" void tabi_ctx_destroy(tabi_ctx* ctx) {
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
+  if (ctx->fork_stream) cudaStreamDestroy(ctx->fork_stream);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -673,12 +682,33 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
     // (prep_kernel zeroes the fused kernel's flags for the T tiles it lays out)
     launch_reset(ctx->d_status, 2, ctx->cands, ctx->t_state, ctx->cand_bad, M, ctx->rdy, 0, s);
     nl++;
+    // Fork: the order and the slot layout need only w, h and the area
+    // (sizes_kernel), so they run while proxy_kernel computes the slices and
+    // OBBs on a second stream (joined before the candidate waves); not with
+    // the prerotation (its w, h follow the OBB angle) or under TABI_TIMING
+    // (stage times stay sequential).  Above 4096 charts only: measured C4
+    // (20,000 charts) 1.141 -> 1.129 ms, while C3 (1,572) and C2 (214) gained
+    // nothing (the graph's fork / join costs what the shorter chain saves).
+    // TABI_PROXY_FORK=0 / 1: test knob (off / on at any size).
+    const char* fenv2 = getenv("TABI_PROXY_FORK");
+    const bool fork = full && !(pp.flags & TABI_F_PREROTATE) && !tm.on &&
+                      (fenv2 ? fenv2[0] == '1' : n > 4096);
     if (full) {
       ctx->sorted_keys = nullptr;  // (set by launch_sort when its ranks write them)
-      launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
-                     ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s,
-                     AtlasMap{nullptr, 1, nullptr}, V_in);
-      nl++;
+      if (fork) {
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        CK(cudaStreamWaitEvent(ctx->fork_stream, ctx->ev_fork, 0));
+        launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags, ctx->d_qx, ctx->d_qy,
+                       ctx->max_v, ctx->P, ctx->d_status, ctx->fork_stream,
+                       AtlasMap{nullptr, 1, nullptr}, V_in, true);
+        launch_sizes(d_xy, d_start, n, res_x, res_y, ctx->max_v, ctx->P, ctx->d_status, s);
+        nl += 2;
+      } else {
+        launch_proxies(d_xy, d_start, n, res_x, res_y, pp.k, pp.flags,
+                       ctx->d_qx, ctx->d_qy, ctx->max_v, ctx->P, ctx->d_status, s,
+                       AtlasMap{nullptr, 1, nullptr}, V_in);
+        nl++;
+      }
       tm.mark(s);
       if (launch_sort_prep(ctx->P, ctx->perm, pp, ctx->colofs, ctx->rowofs, ctx->hsorted,
                            ctx->tstart, ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s)) {
@@ -695,6 +725,10 @@ static tabi_status pack_impl(tabi_ctx* ctx, const float* xy, const int32_t* char
                   ctx->tix, ctx->d_status, fused ? ctx->rdy : nullptr, s, ctx->sorted_keys,
                   ctx->prep_sync);
       nl++;
+    }
+    if (fork) {  // join: the waves need the slices and OBBs
+      CK(cudaEventRecord(ctx->ev_join, ctx->fork_stream));
+      CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     }
     return TABI_OK;
   };

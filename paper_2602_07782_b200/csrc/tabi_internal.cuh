@@ -456,7 +456,12 @@ struct AtlasMap {
 void launch_proxies(const float* xy, const int32_t* start, int32_t n, float rx, float ry, int k,
                     uint32_t flags, int32_t* qx, int32_t* qy, int64_t max_v, Proxies P, Status* st,
                     cudaStream_t s, AtlasMap am = AtlasMap{nullptr, 1, nullptr},
-                    int64_t nverts = 0);  // total vertices if known (picks the lane group)
+                    int64_t nverts = 0, bool skip_wh = false);
+// w, h, area2 and the status words alone (single pack, no prerotation): the
+// order's inputs, so the sort can overlap proxy_kernel (skip_wh) on a second
+// stream
+void launch_sizes(const float* xy, const int32_t* start, int32_t n, float rx, float ry,
+                  int64_t max_v, Proxies P, Status* st, cudaStream_t s);  // total vertices if known (picks the lane group)
 // Status / per-wave state reset (k_sort.cu), one launch; see reset_kernel.
 void launch_reset(Status* st, int mode, Cand* cands, int32_t* t_state, int32_t* cand_bad, int M,
                   int32_t* rdy, int64_t nrdy, cudaStream_t s);

@@ -465,3 +465,24 @@ def test_multi_cta_slot_layout(ctx, monkeypatch, sort_path):
             assert pl0.tobytes() == pl1.tobytes(), cs.name
             w = info0.scale_index - 1  # (the winner's record: aborted lower
             assert c0[w].tobytes() == c1[w].tobytes(), cs.name  # candidates are schedule-dependent)
+
+
+def test_proxy_fork_is_exact(orc, ctx, monkeypatch):
+    """The prologue fork (sizes_kernel -> order -> slot layout on the pack's
+    stream while proxy_kernel runs on a second one; default above 4,096
+    charts): forced on for small packs it matches the oracle, and a bad chart
+    (zero area: collinear outlines) is reported with the same index as without
+    the fork."""
+    from paper_2602_07782_b200 import spec_of
+    monkeypatch.setenv("TABI_PROXY_FORK", "1")
+    _compare_pack(orc, ctx, chartgen.config2(1), check_profiles=0)
+    _compare_pack(orc, ctx, chartgen.config3(1, rho=2.0), check_profiles=0)
+    sq = [(0, 0), (10, 0), (10, 10), (0, 10)]
+    for bad in ([(0, 0), (5, 0), (9, 0)], [(0, 0), (5, 5), (10, 10), (3, 3)]):
+        cs = chartgen.from_polygons([sq, sq, bad, sq, bad], 512, 512)
+        res = []
+        for f in ("1", "0"):
+            monkeypatch.setenv("TABI_PROXY_FORK", f)
+            st, _, info = ctx.pack(cs.xy, cs.start, spec_of(cs), raise_on_error=False)
+            res.append((st, info.bad_chart))
+        assert res[0] == res[1] and res[0][1] == 2, res
